@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark of the all-mode CP gradient on B200 (BASELINE.json metric).
+
+A "step" is one all-mode CP gradient (cp_gradient_all) of the workload tensor.
+Default workload (N=1): BASELINE.json configs[1], the 60^4 fp64 tensor with
+R=20 factors, synthetic N(0,1) inputs from the counter-based generator.
+For N>1 (torchrun, one rank per GPU) every rank holds one 60^4 slab of a
+60x60x60x(60N) tensor sharded along its last mode (weak scaling): the local
+gradient runs with the global pivot, then one NCCL all_reduce of the partial
+G(1..3) and one all_gather of the G(4) rows (paper_1204_1586_b200/sharded.py).
+
+Timing: W untimed warm-up steps; then exactly K steps bracketed by a barrier +
+cuda synchronize on both sides.  Every step is preceded by an L2 flush (a
+256 MiB device memset, outside the events) because the 104 MB tensor fits in
+the 126 MB L2; each step is timed with CUDA events on the launching stream and
+the max over ranks of the summed step time is reported.
+
+  value      whole-job tensor bytes per second (GB/s) through the device API
+  e2e        same metric through the host C-ABI (cpdgpu_cp_gradient_all): H2D
+             copy of Y from pinned host memory + factors in, gradients out
+  roofline   dominant kernel = K1 seed contraction (fp64 DMMA); its CUDA-event
+             time against the FP64 tensor peak measured on B200 (compute bound
+             at R=20) with the HBM fraction beside it
+  cpu_baseline  the CPU oracle (a port of the reference) on this host's cores
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port, all host threads) on the same workload and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (dims, R, dtype, description)
+    "c1": ([200, 200, 200], 10, "f64", "3-D 200^3 fp64 R=10"),
+    "c2": ([60, 60, 60, 60], 20, "f64", "4-D 60^4 fp64 R=20"),
+    "c3": ([14] * 7, 10, "f64", "7-D 14^7 fp64 R=10"),
+}
+FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 microbenchmark on B200, profiles/r01_fp64_peak_microbench.txt
+L2_FLUSH_BYTES = 256 << 20
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU is busy."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            mx = m
+            sm.append(s)
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def device_normal(ctx, seed, rows, R):
+    """Factor matrix drawn by the product's device generator (N(0,1), counter-based)."""
+    import paper_1204_1586_b200 as cpd
+    t = cpd.DenseTensor.generate([rows, R], cpd.DIST_NORMAL, seed=seed, ctx=ctx)
+    v = t.values().reshape(rows, R, order="F")
+    t.free()
+    return np.asfortranarray(v)
+
+
+# ---------------------------------------------------------------------------- reference arm
+
+def run_reference(args, cfg):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    dims, R, dtype, desc = cfg
+    n = int(np.prod(dims))
+    cores = host_cores()
+    y = O.fill_normal(1, n, nthreads=cores)
+    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
+    for _ in range(args.warmup):
+        O.cp_gradient_all(y, dims, f, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.cp_gradient_all(y, dims, f, nthreads=cores)
+    dt = time.perf_counter() - t0
+    ms = dt / args.steps * 1e3
+    gbs = n * 8 / (ms * 1e-3) / 1e9
+    line = {
+        "impl": "reference", "metric": f"all-mode CP gradient throughput ({desc})", "value": gbs,
+        "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic N(0,1), counter-based generator",
+        "config": {"workload": args.config, "dims": dims, "R": R},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"full {args.config} gradient x {args.steps} steps (oracle/cpd_oracle.c, OpenMP)"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- our arm
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1204_1586_b200 as cpd
+    from paper_1204_1586_b200 import build as B
+    from paper_1204_1586_b200 import sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and args.gpus != 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if rank == 0:
+        B.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+    B.build()  # no-op after rank 0 built it; loads the in-tree .so
+    dims, R, dtype, desc = cfg
+    N = len(dims)
+    ctx = cpd.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    # global tensor: dims[:-1] x (dims[-1] * world); this rank's slab is dims
+    gdims = list(dims[:-1]) + [dims[-1] * world]
+    plan = sharded.make_plan(gdims, R, rank, world) if world > 1 else None
+    slab = int(np.prod(dims))
+    a0 = plan.bounds[0] if plan else 0
+    y = cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=1, ctx=ctx,
+                                 offset=a0 * int(np.prod(dims[:-1])))
+    gfac = [device_normal(ctx, 100 + k, d, R) for k, d in enumerate(gdims)]
+    if plan:
+        packed = sharded.pack_local_factors(plan, gfac, np)
+        pivot = plan.pivot
+    else:
+        packed = np.concatenate([f.reshape(-1, order="F") for f in gfac])
+        pivot = 0
+    fdev = torch.from_numpy(packed).to(dev)
+    gdev = torch.zeros_like(fdev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step():
+        cpd.cp_gradient_all_device(y, R, fdev.data_ptr(), gdev.data_ptr(), pivot)
+        if plan:
+            sharded.exchange(plan, gdev, dist)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            step()
+            stops[i].record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        # clocks need a busy window long enough to sample: keep the same step
+        # running for ~1 s after the timed region when the region was short
+        t_end = time.time() + 1.0
+        while time.time() < t_end and len(clk.lines) < 10:
+            for _ in range(50):
+                step()
+            torch.cuda.synchronize(dev)
+    gpu_launches = ctx.launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, stops)]
+    tot_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms = tot_ms / args.steps
+    total_bytes = slab * 8 * world
+    value = total_bytes / (ms * 1e-3) / 1e9
+
+    # dominant kernel: K1 seed contraction, timed live with CUDA events
+    ctx.set_timing(True)
+    seed_ms = []
+    for _ in range(max(10, min(args.steps, 50))):
+        flush.zero_()
+        cpd.cp_gradient_all_device(y, R, fdev.data_ptr(), gdev.data_ptr(), pivot)
+        seed_ms.append(ctx.last_seed_ms())
+    ctx.set_timing(False)
+    seed_avg = float(np.mean(seed_ms))
+    flops = 4.0 * R * slab
+    bytes_alg = 8.0 * slab + 2 * 8.0 * R * sum(dims)
+    peaks = measured_peaks()
+    tflops = flops / (seed_avg * 1e-3) / 1e12
+    hbm_gbs = bytes_alg / (seed_avg * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_seed_{args.config}.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": "seed_f64_kernel (K1, fp64 DMMA)", "kernel_ms": seed_avg,
+                "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
+                "peak_source": "FP64 DMMA peak measured on B200 (profiles/r01_fp64_peak_microbench.txt)",
+                "hbm": {"achieved": hbm_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                        "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0)}}
+
+    # e2e through the host C-ABI: H2D of Y from pinned memory + factors, D2H of gradients
+    e2e = None
+    if not args.no_e2e and world == 1:
+        host_y = torch.empty(slab, dtype=torch.float64).pin_memory()
+        host_y.copy_(torch.from_numpy(y.values()))
+        facs = [f.copy(order="F") for f in gfac]
+        e_steps = max(3, min(args.steps, 20))
+        for _ in range(2):
+            y.update(host_y.data_ptr())
+            cpd.cp_gradient_all(y, facs)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            y.update(host_y.data_ptr())
+            cpd.cp_gradient_all(y, facs)
+        dt = (time.perf_counter() - t0) / e_steps
+        e2e = {"value": slab * 8 / dt / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": slab * 8 + 8 * R * sum(dims),
+               "d2h_bytes_per_step": 8 * R * sum(dims), "ms_per_step": dt * 1e3,
+               "timing": "wall clock around synchronous host-API calls"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, cfg)
+
+    if rank == 0:
+        line = {
+            "metric": f"all-mode CP gradient throughput ({desc})", "value": value, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic N(0,1), counter-based generator",
+            "config": {"workload": args.config, "dims": dims, "R": R,
+                       "global_dims": gdims, "parallelism": f"slab{world}" if world > 1 else "single",
+                       "l2": "flushed before every step (256 MiB memset outside the events)"},
+            "gpu_launches": gpu_launches, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(args, cfg):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    dims, R, dtype, desc = cfg
+    n = int(np.prod(dims))
+    cores = host_cores()
+    y = O.fill_normal(1, n, nthreads=cores)
+    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
+    O.cp_gradient_all(y, dims, f, nthreads=cores)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.cp_gradient_all(y, dims, f, nthreads=cores)
+        reps += 1
+        if time.perf_counter() - t0 > args.cpu_seconds:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": n * 8 / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{reps} full {args.config} gradients (~{args.cpu_seconds:.0f} s), oracle/cpd_oracle.c OpenMP",
+            "ms_per_step": dt * 1e3}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(CONFIGS), default="c2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,146 @@
+/* cpdgpu.h — C-ABI of the B200-native all-mode CP gradient / fast CP_ALS.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/core).  Each entry point names the reference
+ * interface it replaces (file:line, relative to /root/reference/proj/core).
+ * Plain pointers and sizes only: no C++ types, no torch types, no exceptions.
+ *
+ * Conventions (identical to the reference):
+ *   - tensors are dense, column-major (first index fastest; dense_tensor.hpp:12-14);
+ *   - factor n is an I_n x R column-major fp64 matrix (kron.hpp:13-14);
+ *   - modes are 1-based; results come back in the caller's mode order
+ *     (mttkrp.cpp:134-136);
+ *   - every call returns a cpdgpu_status; the message of the last failure is
+ *     cpdgpu_last_error(ctx).  Statuses map 1:1 onto the reference exception
+ *     types (errors.hpp:8-35); see INTEGRATION.md.
+ *   - one host thread per context; calls are synchronous with respect to the
+ *     host unless they take device pointers (the *_device variants), which are
+ *     ordered on the context's stream (cpdgpu_set_stream).
+ */
+#ifndef CPDGPU_H
+#define CPDGPU_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CPDGPU_OK = 0,
+  CPDGPU_SHAPE_ERROR = 1,    /* cpd::ShapeError    (errors.hpp:9-11)  */
+  CPDGPU_INDEX_ERROR = 2,    /* cpd::IndexError    (errors.hpp:14-16) */
+  CPDGPU_ARGUMENT_ERROR = 3, /* cpd::ArgumentError (errors.hpp:19-21) */
+  CPDGPU_NUMERIC_ERROR = 4,  /* cpd::NumericError  (errors.hpp:29-31) */
+  CPDGPU_DOMAIN_ERROR = 5,   /* cpd::DomainError   (errors.hpp:24-26) */
+  CPDGPU_CUDA_ERROR = 6,     /* device / driver failure                */
+  CPDGPU_NO_MEMORY = 7       /* device allocation failed               */
+} cpdgpu_status;
+
+typedef enum { CPDGPU_F64 = 0, CPDGPU_F32 = 1 } cpdgpu_dtype;
+typedef enum { CPDGPU_DIST_NORMAL = 0, CPDGPU_DIST_UNIFORM_PM1 = 1 } cpdgpu_dist;
+
+typedef struct cpdgpu_ctx cpdgpu_ctx;
+typedef struct cpdgpu_tensor cpdgpu_tensor;
+
+/* Per-mode callback for the generic ModeHook (mttkrp.hpp:49-51): called right
+ * after G^(mode) is ready (rows x R, column-major, host memory) and after the
+ * mode's multiplication count has been reported through `mults`.  It may
+ * overwrite the caller's factor for `mode` (the buffer passed in `factors`),
+ * which the sweep re-reads before moving on (mttkrp.cpp:137-144).  A non-zero
+ * return aborts the sweep with that status. */
+typedef int (*cpdgpu_mode_hook)(void* user, int mode, const double* gradient, int64_t rows,
+                                int64_t rank, uint64_t mults);
+
+/* ---- context ------------------------------------------------------------ */
+int cpdgpu_create(cpdgpu_ctx** ctx, int device);
+int cpdgpu_destroy(cpdgpu_ctx* ctx);
+const char* cpdgpu_last_error(const cpdgpu_ctx* ctx);
+/* cudaStream_t as void*; NULL = the context's own stream. */
+int cpdgpu_set_stream(cpdgpu_ctx* ctx, void* stream);
+int cpdgpu_synchronize(cpdgpu_ctx* ctx);
+/* 1 = capture the per-gradient launch sequence into a CUDA graph (default 1). */
+int cpdgpu_set_graphs(cpdgpu_ctx* ctx, int enabled);
+/* Kernels launched by this context so far (evidence counter for bench.py). */
+uint64_t cpdgpu_launch_count(const cpdgpu_ctx* ctx);
+/* 1 = bracket every seed-contraction launch (K1) with CUDA events on the
+ * context stream; cpdgpu_last_seed_ms then returns the summed K1 device time
+ * of the most recent gradient / sweep call (synchronises on the last event). */
+int cpdgpu_set_timing(cpdgpu_ctx* ctx, int enabled);
+int cpdgpu_last_seed_ms(cpdgpu_ctx* ctx, double* ms);
+
+/* ---- tensors (DenseTensor, dense_tensor.hpp:15-47) -------------------------
+ * A tensor is immutable once created, as the reference's is; the context may
+ * cache a mode-sorted copy (sort_modes, mttkrp.cpp:67-90) for its lifetime. */
+int cpdgpu_tensor_upload(cpdgpu_ctx* ctx, const void* host, cpdgpu_dtype dtype, int N,
+                         const int64_t* dims, cpdgpu_tensor** out);
+/* Zero-copy view of caller-owned device memory (not freed by the library). */
+int cpdgpu_tensor_wrap_device(cpdgpu_ctx* ctx, void* device_ptr, cpdgpu_dtype dtype, int N,
+                              const int64_t* dims, cpdgpu_tensor** out);
+/* Device-side generation: entry at global linear index (offset + q) is drawn
+ * from the counter-based generator of DESIGN.md "Synthetic inputs". */
+int cpdgpu_tensor_generate(cpdgpu_ctx* ctx, cpdgpu_dtype dtype, int N, const int64_t* dims,
+                           cpdgpu_dist dist, uint64_t seed, int64_t offset, cpdgpu_tensor** out);
+/* Y <- alpha * Y + beta * full(model)  (full: kruskal.cpp:23-31). */
+int cpdgpu_tensor_axpby_kruskal(cpdgpu_ctx* ctx, cpdgpu_tensor* t, double alpha, double beta,
+                                const double* const* factors, int64_t R);
+/* Refresh an existing tensor's values from host memory (same dims/dtype);
+ * the H2D copy of the end-to-end path.  Pinned host memory copies at full
+ * PCIe/C2C rate; drops the cached norm and sorted copy. */
+int cpdgpu_tensor_update(cpdgpu_ctx* ctx, cpdgpu_tensor* t, const void* host);
+int cpdgpu_tensor_download(cpdgpu_ctx* ctx, const cpdgpu_tensor* t, void* host);
+/* |Y|_F^2 in fp64 (DenseTensor::norm, dense_tensor.cpp:32-34, squared). */
+int cpdgpu_tensor_norm2(cpdgpu_ctx* ctx, cpdgpu_tensor* t, double* out);
+int cpdgpu_tensor_device_ptr(const cpdgpu_tensor* t, void** device_ptr);
+int cpdgpu_tensor_free(cpdgpu_tensor* t);
+
+/* ---- ordering helpers (mttkrp.hpp:24,35,73) ----------------------------- */
+int cpdgpu_select_pivot(int N, const int64_t* dims, int* pivot);            /* mttkrp.cpp:56-65  */
+int cpdgpu_sort_modes(int N, const int64_t* dims, int* perm, int* inverse); /* mttkrp.cpp:67-90  */
+int cpdgpu_fast_update_order(int N, const int64_t* dims, int* order);       /* mttkrp.cpp:92-111 */
+/* mttkrp.cpp:292-320 (dims must be ascending); 0 on bad input. */
+uint64_t cpdgpu_fast_count_realized(int N, const int64_t* dims, int64_t R, int n);
+
+/* ---- all-mode CP gradient (cp_gradient_all, mttkrp.hpp:59-69, mttkrp.cpp:113-253)
+ * factors[k] / gradients[k]: host I_{k+1} x R column-major fp64 buffers in the
+ * caller's mode order.  mults_per_mode (N entries, optional) receives the
+ * reference's per-mode multiplication charges (fast_count_realized);
+ * peak_workspace (optional) the FastStats::peak_workspace_doubles figure. */
+int cpdgpu_cp_gradient_all(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R,
+                           const double* const* factors, double* const* gradients,
+                           uint64_t* mults_per_mode, int64_t* peak_workspace);
+/* Hook form (mttkrp.hpp:59-63): factors[] are mutable; hook runs per mode in
+ * fast_update_order and the sweep reads back any factor it replaced. */
+int cpdgpu_cp_gradient_all_hook(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R,
+                                double* const* factors, double* const* gradients,
+                                cpdgpu_mode_hook hook, void* user, int64_t* peak_workspace);
+/* Device form: factors_dev / gradients_dev are device buffers holding the N
+ * factor (gradient) matrices packed back to back in the caller's mode order
+ * (sum_n I_n x R doubles).  pivot = 0 selects p*; a positive pivot forces the
+ * split point (slab shards of a larger tensor use the global p*).  Ordered on
+ * the context stream; no host synchronisation. */
+int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R,
+                                  const double* factors_dev, double* gradients_dev, int pivot);
+
+/* ---- fast CP_ALS (als.hpp:48-93) ----------------------------------------- */
+/* pinv_psd (als.cpp:34-47) of a host R x R symmetric matrix, on the device. */
+int cpdgpu_pinv_psd(cpdgpu_ctx* ctx, int64_t R, const double* s, double rtol, double* out);
+/* als_update_mode (als.cpp:49-56): out = m * pinv_psd(gram_hadamard_skip(factors, n)). */
+int cpdgpu_als_update_mode(cpdgpu_ctx* ctx, int N, const int64_t* dims, int64_t R,
+                           const double* m, const double* const* factors, int n, double rtol,
+                           double* out);
+/* als_sweep_fast (als.cpp:69-78): factors updated in place; the whole sweep
+ * (gradients, Gram/Hadamard, pseudo-inverse, update) runs on the device.
+ * cost_out (optional) receives cost(y, model) after the sweep (kruskal.cpp:58-77). */
+int cpdgpu_als_sweep(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors,
+                     double pinv_rtol, double* cost_out, uint64_t* mults);
+/* run(y, init, Algorithm::als_fast, opts) (als.cpp:147-210).  Traces hold
+ * max_iters entries; sec_trace times each sweep on the device (CUDA events). */
+int cpdgpu_als_run(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors,
+                   int max_iters, double tol, double pinv_rtol, double* cost_trace,
+                   double* rel_trace, double* sec_trace, uint64_t* mults_trace, int* iters_run);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPDGPU_H */

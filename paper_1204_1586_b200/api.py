@@ -1,0 +1,453 @@
+"""Host-side mirror of the reference's hot-path API (proj/core/include/cpd/
+{mttkrp,als,kruskal,cost_counter}.hpp) over the C-ABI.
+
+Same names, argument meaning, column-major layout and error behaviour as the
+reference; arrays are numpy.  Every numeric call runs on the B200 through
+libcpdgpu.so — nothing here computes the gradient on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib, errors
+
+F64, F32 = 0, 1
+DIST_NORMAL, DIST_UNIFORM_PM1 = 0, 1
+
+
+# ---- instrumentation (cost_counter.hpp:11-27, mttkrp.hpp:44-47) -------------
+
+class CostCounter:
+    """Running tally of scalar multiplications (cost_counter.hpp:11-27)."""
+
+    def __init__(self) -> None:
+        self._total = 0
+
+    def charge(self, mults: int) -> None:
+        self._total += int(mults)
+
+    def charge_gemm(self, m: int, k: int, p: int) -> None:
+        self._total += int(m) * int(k) * int(p)
+
+    def charge_kron(self, p: int, q: int) -> None:
+        self._total += int(p) * int(q)
+
+    def total(self) -> int:
+        return self._total
+
+    def reset(self) -> None:
+        self._total = 0
+
+
+@dataclass
+class FastStats:
+    """mttkrp.hpp:44-47: high-water mark of workspace doubles (outputs excluded)."""
+    peak_workspace_doubles: int = 0
+
+
+# ---- context and tensors (dense_tensor.hpp:15-47) ----------------------------
+
+class Context:
+    """One B200 device plus a CUDA stream (cpdgpu_ctx)."""
+
+    def __init__(self, device: int = 0) -> None:
+        self._L = _lib.load()
+        h = C.c_void_p()
+        _lib.check(self._L.cpdgpu_create(C.byref(h), int(device)))
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self._L.cpdgpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self) -> None:  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int) -> None:
+        """Order all work on an external cudaStream_t (e.g. torch's current stream)."""
+        _lib.check(self._L.cpdgpu_set_stream(self.h, C.c_void_p(stream_ptr)), self.h)
+
+    def synchronize(self) -> None:
+        _lib.check(self._L.cpdgpu_synchronize(self.h), self.h)
+
+    def launch_count(self) -> int:
+        return int(self._L.cpdgpu_launch_count(self.h))
+
+    def set_timing(self, enabled: bool) -> None:
+        _lib.check(self._L.cpdgpu_set_timing(self.h, int(bool(enabled))), self.h)
+
+    def last_seed_ms(self) -> float:
+        v = C.c_double()
+        _lib.check(self._L.cpdgpu_last_seed_ms(self.h, C.byref(v)), self.h)
+        return float(v.value)
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def _dims_arg(dims: Sequence[int]):
+    arr = (C.c_int64 * len(dims))(*[int(d) for d in dims])
+    return arr
+
+
+class DenseTensor:
+    """Immutable dense column-major tensor resident on the device.
+
+    Mirrors cpd::DenseTensor (dense_tensor.hpp:15-47): entry (i_1..i_N) lives at
+    the vectorization-order position; values never change after creation.
+    """
+
+    def __init__(self, ctx: Context, handle: C.c_void_p, dims: Sequence[int], dtype: int) -> None:
+        self.ctx, self.h, self.dims, self.dtype = ctx, handle, tuple(int(d) for d in dims), dtype
+
+    # constructors -----------------------------------------------------------
+    @classmethod
+    def from_values(cls, values, dims: Sequence[int], ctx: Optional[Context] = None,
+                    dtype: int = F64) -> "DenseTensor":
+        """values: flat vector in vectorization order (first index fastest), or an
+        N-d numpy array (interpreted by its logical indices, any memory order)."""
+        ctx = ctx or default_context()
+        np_dtype = np.float64 if dtype == F64 else np.float32
+        a = np.asarray(values)
+        if a.ndim > 1:
+            if tuple(a.shape) != tuple(dims):
+                raise errors.ShapeError(f"tensor: array shape {a.shape} != dims {tuple(dims)}")
+            flat = np.asarray(a, dtype=np_dtype).reshape(-1, order="F")
+        else:
+            flat = np.ascontiguousarray(a, dtype=np_dtype)
+        n = int(np.prod([int(d) for d in dims])) if len(dims) else 0
+        if flat.size != n:
+            raise errors.ShapeError(f"tensor: {flat.size} values for a shape holding {n} entries")
+        h = C.c_void_p()
+        d = _dims_arg(dims)
+        _lib.check(ctx._L.cpdgpu_tensor_upload(ctx.h, flat.ctypes.data_as(C.c_void_p), dtype,
+                                               len(dims), d, C.byref(h)), ctx.h)
+        return cls(ctx, h, dims, dtype)
+
+    @classmethod
+    def generate(cls, dims: Sequence[int], dist: int = DIST_NORMAL, seed: int = 0,
+                 ctx: Optional[Context] = None, dtype: int = F64, offset: int = 0) -> "DenseTensor":
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _lib.check(ctx._L.cpdgpu_tensor_generate(ctx.h, dtype, len(dims), _dims_arg(dims), dist,
+                                                 C.c_uint64(seed), int(offset), C.byref(h)), ctx.h)
+        return cls(ctx, h, dims, dtype)
+
+    @classmethod
+    def wrap_device(cls, ptr: int, dims: Sequence[int], ctx: Optional[Context] = None,
+                    dtype: int = F64) -> "DenseTensor":
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _lib.check(ctx._L.cpdgpu_tensor_wrap_device(ctx.h, C.c_void_p(ptr), dtype, len(dims),
+                                                    _dims_arg(dims), C.byref(h)), ctx.h)
+        return cls(ctx, h, dims, dtype)
+
+    # queries ------------------------------------------------------------------
+    def order(self) -> int:
+        return len(self.dims)
+
+    def size(self) -> int:
+        return int(np.prod(self.dims))
+
+    def values(self) -> np.ndarray:
+        out = np.empty(self.size(), dtype=np.float64 if self.dtype == F64 else np.float32)
+        _lib.check(self.ctx._L.cpdgpu_tensor_download(self.ctx.h, self.h,
+                                                      out.ctypes.data_as(C.c_void_p)), self.ctx.h)
+        return out
+
+    def update(self, host_ptr: int) -> None:
+        """H2D refresh of the values from host memory at host_ptr (same dims/dtype)."""
+        _lib.check(self.ctx._L.cpdgpu_tensor_update(self.ctx.h, self.h, C.c_void_p(host_ptr)), self.ctx.h)
+
+    def norm2(self) -> float:
+        v = C.c_double()
+        _lib.check(self.ctx._L.cpdgpu_tensor_norm2(self.ctx.h, self.h, C.byref(v)), self.ctx.h)
+        return float(v.value)
+
+    def norm(self) -> float:
+        return float(np.sqrt(self.norm2()))
+
+    def device_ptr(self) -> int:
+        p = C.c_void_p()
+        _lib.check(self.ctx._L.cpdgpu_tensor_device_ptr(self.h, C.byref(p)))
+        return int(p.value or 0)
+
+    def axpby_kruskal(self, alpha: float, beta: float, factors: Sequence[np.ndarray]) -> None:
+        """Y <- alpha Y + beta full(model) on the device (setup helper)."""
+        bufs = _factor_bufs(factors, self.dims)
+        _lib.check(self.ctx._L.cpdgpu_tensor_axpby_kruskal(self.ctx.h, self.h, alpha, beta,
+                                                           _ptr_array(bufs), bufs[0].shape[1]),
+                   self.ctx.h)
+
+    def free(self) -> None:
+        if self.h:
+            self.ctx._L.cpdgpu_tensor_free(self.h)
+            self.h = None
+
+    def __del__(self) -> None:  # pragma: no cover
+        try:
+            if self.h and self.ctx.h:
+                self.free()
+        except Exception:
+            pass
+
+
+# ---- helpers ---------------------------------------------------------------------
+
+def _factor_bufs(factors: Sequence[np.ndarray], dims: Sequence[int]) -> list:
+    """Column-major float64 copies; validates factor_shape (kron.cpp:25-45)."""
+    if len(factors) == 0:
+        raise errors.ArgumentError("factors: empty list")
+    bufs = [np.asfortranarray(np.asarray(f, dtype=np.float64)) for f in factors]
+    for k, b in enumerate(bufs):
+        if b.ndim == 1:
+            bufs[k] = b = np.asfortranarray(b.reshape(-1, 1))
+        if b.ndim != 2:
+            raise errors.ShapeError(f"factors: mode {k + 1} is not a matrix")
+    R = bufs[0].shape[1]
+    for k, b in enumerate(bufs):
+        if b.shape[1] != R:
+            raise errors.ShapeError(f"factors: mode {k + 1} has rank {b.shape[1]}, expected {R}")
+        if b.shape[0] < 1:
+            raise errors.ShapeError(f"factors: mode {k + 1} has no rows")
+    if len(bufs) != len(dims) or any(b.shape[0] != d for b, d in zip(bufs, dims)):
+        raise errors.ShapeError("cp_gradient_all: factor row counts do not match the tensor")
+    return bufs
+
+
+def _ptr_array(bufs: Sequence[np.ndarray]):
+    arr = (_lib.c_dbl_p * len(bufs))()
+    for i, b in enumerate(bufs):
+        arr[i] = b.ctypes.data_as(_lib.c_dbl_p)
+    return arr
+
+
+# ---- ordering helpers (mttkrp.hpp:24,35,73) ------------------------------------
+
+def select_pivot(dims: Sequence[int]) -> int:
+    L = _lib.load()
+    p = C.c_int()
+    _lib.check(L.cpdgpu_select_pivot(len(dims), _dims_arg(dims), C.byref(p)))
+    return p.value
+
+
+def sort_modes(dims: Sequence[int]) -> tuple[list[int], list[int]]:
+    """(perm, inverse), 1-based, as SortResult::perm / ::inverse (mttkrp.hpp:28-33)."""
+    L = _lib.load()
+    n = len(dims)
+    perm, inv = (C.c_int * max(n, 1))(), (C.c_int * max(n, 1))()
+    _lib.check(L.cpdgpu_sort_modes(n, _dims_arg(dims), perm, inv))
+    return list(perm)[:n], list(inv)[:n]
+
+
+def fast_update_order(dims: Sequence[int]) -> list[int]:
+    L = _lib.load()
+    n = len(dims)
+    out = (C.c_int * max(n, 1))()
+    _lib.check(L.cpdgpu_fast_update_order(n, _dims_arg(dims), out))
+    return list(out)[:n]
+
+
+def fast_count_realized(dims: Sequence[int], R: int, n: int) -> int:
+    L = _lib.load()
+    if list(dims) != sorted(dims):
+        raise errors.ArgumentError("fast_count_realized: dims must be ascending")
+    if R < 1:
+        raise errors.ArgumentError("fast_count_realized: rank must be positive")
+    if n < 1 or n > len(dims):
+        raise errors.IndexError(f"fast_count_realized: mode {n} outside 1..{len(dims)}")
+    return int(L.cpdgpu_fast_count_realized(len(dims), _dims_arg(dims), R, n))
+
+
+# ---- the all-mode gradient (mttkrp.hpp:59-69) ----------------------------------
+
+ModeHook = Callable[[int, np.ndarray], None]
+
+
+def cp_gradient_all(y: DenseTensor, factors: list, counter: Optional[CostCounter] = None,
+                    hook: Optional[ModeHook] = None,
+                    stats: Optional[FastStats] = None) -> list[np.ndarray]:
+    """All-mode CP gradients G^(n) = Y_(n) (KR_{k != n} A^(k)) (mttkrp.cpp:113-253).
+
+    With a hook, ``hook(n, G)`` runs right after mode n's gradient is ready (in
+    fast_update_order) and may replace ``factors[n-1]``; the sweep re-reads it
+    (mttkrp.cpp:134-145).  The counter is charged per mode before the hook.
+    """
+    if y.order() < 2:
+        raise errors.ArgumentError("cp_gradient_all: need an order-2 or higher tensor")
+    bufs = _factor_bufs(factors, y.dims)
+    R = bufs[0].shape[1]
+    grads = [np.empty((d, R), dtype=np.float64, order="F") for d in y.dims]
+    fptr, gptr = _ptr_array(bufs), _ptr_array(grads)
+    peak = C.c_int64()
+    ctx = y.ctx
+    if hook is None:
+        mults = (C.c_uint64 * len(y.dims))()
+        _lib.check(ctx._L.cpdgpu_cp_gradient_all(ctx.h, y.h, R, fptr, gptr, mults, C.byref(peak)), ctx.h)
+        if counter is not None:
+            counter.charge(sum(int(m) for m in mults))
+    else:
+        err: list = []
+
+        def _cb(user, mode, g, rows, rank, m):  # runs on the caller's thread
+            try:
+                if counter is not None:
+                    counter.charge(int(m))
+                hook(mode, grads[mode - 1].copy(order="F"))
+                F = np.asarray(factors[mode - 1], dtype=np.float64)
+                if F.ndim == 1:
+                    F = F.reshape(-1, 1)
+                if F.shape != (y.dims[mode - 1], R):
+                    raise errors.ShapeError(
+                        f"cp_gradient_all: hook left factor of mode {mode} with the wrong size")
+                bufs[mode - 1][...] = F
+                return 0
+            except BaseException as e:  # noqa: BLE001 - re-raised below
+                err.append(e)
+                return 3
+
+        cb = _lib.HOOK(_cb)
+        st = ctx._L.cpdgpu_cp_gradient_all_hook(ctx.h, y.h, R, fptr, gptr, cb, None, C.byref(peak))
+        if err:
+            raise err[0]
+        _lib.check(st, ctx.h)
+    if stats is not None:
+        stats.peak_workspace_doubles = int(peak.value)
+    return grads
+
+
+def cp_gradient_all_device(y: DenseTensor, R: int, factors_dev_ptr: int, grads_dev_ptr: int,
+                           pivot: int = 0) -> None:
+    """Device-buffer form (packed factors/gradients in caller mode order), ordered on
+    the context stream; used by the sharded multi-GPU driver."""
+    ctx = y.ctx
+    _lib.check(ctx._L.cpdgpu_cp_gradient_all_device(ctx.h, y.h, int(R), C.c_void_p(factors_dev_ptr),
+                                                    C.c_void_p(grads_dev_ptr), int(pivot)), ctx.h)
+
+
+# ---- ALS (als.hpp:48-93) ---------------------------------------------------------
+
+def pinv_psd(s: np.ndarray, rtol: float = 1e-12, ctx: Optional[Context] = None) -> np.ndarray:
+    """Moore-Penrose inverse of a symmetric PSD matrix (als.cpp:34-47), on the device."""
+    ctx = ctx or default_context()
+    a = np.asfortranarray(np.asarray(s, dtype=np.float64))
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise errors.ShapeError("pinv_psd: matrix must be square")
+    out = np.empty_like(a, order="F")
+    _lib.check(ctx._L.cpdgpu_pinv_psd(ctx.h, a.shape[0], a.ctypes.data_as(_lib.c_dbl_p), rtol,
+                                      out.ctypes.data_as(_lib.c_dbl_p)), ctx.h)
+    return out
+
+
+def als_update_mode(m: np.ndarray, factors: list, n: int, pinv_rtol: float = 1e-12,
+                    ctx: Optional[Context] = None) -> np.ndarray:
+    """A^(n) <- M pinv(hadamard of the skip-mode Grams) (als.cpp:49-56)."""
+    ctx = ctx or default_context()
+    if n < 1 or n > len(factors):
+        raise errors.IndexError(f"als_update_mode: mode {n} outside 1..{len(factors)}")
+    dims = [np.asarray(f).shape[0] for f in factors]
+    bufs = _factor_bufs(factors, dims)
+    R = bufs[0].shape[1]
+    mm = np.asfortranarray(np.asarray(m, dtype=np.float64))
+    if mm.shape != (dims[n - 1], R):
+        raise errors.ShapeError("als_update_mode: mttkrp matrix has the wrong size")
+    out = np.empty_like(mm, order="F")
+    _lib.check(ctx._L.cpdgpu_als_update_mode(ctx.h, len(dims), _dims_arg(dims), R,
+                                             mm.ctypes.data_as(_lib.c_dbl_p), _ptr_array(bufs), n,
+                                             pinv_rtol, out.ctypes.data_as(_lib.c_dbl_p)), ctx.h)
+    return out
+
+
+def als_sweep_fast(y: DenseTensor, factors: list, pinv_rtol: float = 1e-12,
+                   counter: Optional[CostCounter] = None, stats: Optional[FastStats] = None) -> None:
+    """One ALS sweep threaded through the all-mode recursion (als.cpp:69-78);
+    factors are replaced in place (list elements)."""
+    if y.order() < 2:
+        raise errors.ArgumentError("cp_gradient_all: need an order-2 or higher tensor")
+    bufs = _factor_bufs(factors, y.dims)
+    R = bufs[0].shape[1]
+    mults = C.c_uint64()
+    ctx = y.ctx
+    _lib.check(ctx._L.cpdgpu_als_sweep(ctx.h, y.h, R, _ptr_array(bufs), pinv_rtol, None,
+                                       C.byref(mults)), ctx.h)
+    for k, b in enumerate(bufs):
+        factors[k] = b
+    if counter is not None:
+        counter.charge(int(mults.value))
+
+
+@dataclass
+class SolveOptions:
+    """als.hpp:21-29 (the fields the fast ALS driver reads)."""
+    max_iters: int = 20
+    tol: float = 0.0
+    pinv_rtol: float = 1e-12
+    mu_eps: float = 1e-12
+    gd_eta: float = 1e-3
+    seed: int = 0
+
+
+@dataclass
+class RunTrace:
+    """als.hpp:31-39; `seconds` are device-timed sweeps (CUDA events)."""
+    cost: list = field(default_factory=list)
+    rel_error: list = field(default_factory=list)
+    seconds: list = field(default_factory=list)
+    mults: list = field(default_factory=list)
+    iters_run: int = 0
+
+
+@dataclass
+class SolveResult:
+    factors: list
+    trace: RunTrace
+
+
+def run(y: DenseTensor, init: list, opts: Optional[SolveOptions] = None,
+        counter: Optional[CostCounter] = None) -> SolveResult:
+    """run(y, init, Algorithm::als_fast, opts) (als.cpp:147-210) on the device."""
+    opts = opts or SolveOptions()
+    if opts.max_iters < 1:
+        raise errors.ArgumentError("run: max_iters must be at least 1")
+    if opts.tol < 0.0 or opts.pinv_rtol < 0.0 or opts.mu_eps < 0.0:
+        raise errors.ArgumentError("run: tolerances must be nonnegative")
+    try:
+        bufs = _factor_bufs(init, y.dims)
+    except errors.ShapeError:
+        raise errors.ShapeError("run: init factors do not match the tensor") from None
+    bufs = [b.copy(order="F") for b in bufs]
+    R = bufs[0].shape[1]
+    n = opts.max_iters
+    cost = np.zeros(n)
+    rel = np.zeros(n)
+    sec = np.zeros(n)
+    mults = (C.c_uint64 * n)()
+    iters = C.c_int()
+    ctx = y.ctx
+    _lib.check(ctx._L.cpdgpu_als_run(ctx.h, y.h, R, _ptr_array(bufs), n, opts.tol, opts.pinv_rtol,
+                                     cost.ctypes.data_as(_lib.c_dbl_p), rel.ctypes.data_as(_lib.c_dbl_p),
+                                     sec.ctypes.data_as(_lib.c_dbl_p), mults, C.byref(iters)), ctx.h)
+    k = iters.value
+    base = counter.total() if counter is not None else 0
+    tr = RunTrace(cost=list(cost[:k]), rel_error=list(rel[:k]), seconds=list(sec[:k]),
+                  mults=[base + int(m) for m in list(mults)[:k]] if counter is not None else [0] * k,
+                  iters_run=k)
+    if counter is not None and k:
+        counter.charge(int(mults[k - 1]))
+    return SolveResult(factors=bufs, trace=tr)

@@ -1,0 +1,52 @@
+// common.cuh — shared device-side types for the B200 all-mode CP gradient.
+//
+// The index vocabulary follows the reference (SURVEY.md shorthand): Y is the
+// dense column-major tensor in the ascending-sorted mode frame, p the pivot,
+// J_n / K_n the prefix / suffix products, the right seed J_p x R and the left
+// seed K_p x R (mttkrp.cpp:149-210).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cpdgpu {
+
+constexpr int kMaxModes = 16;  // modes per Khatri-Rao range
+
+// A contiguous range of modes lo..hi of the sorted frame whose factor columns
+// form a Khatri-Rao row on the fly: row index q has mixed-radix digits
+// d_k (first mode fastest) and  KR[q, r] = prod_k A_k[d_k + I_k r]
+// (kron_range_column, kron.cpp:54-68: later modes outermost).
+struct KRSpec {
+  int n;                           // number of modes in the range (0 => KR == 1)
+  int64_t dims[kMaxModes];         // I_k
+  const double* A[kMaxModes];      // device factor k, column-major I_k x R
+};
+
+__device__ __forceinline__ double kr_entry(const KRSpec& s, int64_t q, int r) {
+  double prod = 1.0;
+#pragma unroll 1
+  for (int k = 0; k < s.n; ++k) {
+    const int64_t I = s.dims[k];
+    const int64_t d = q % I;
+    q /= I;
+    prod *= __ldg(s.A[k] + d + I * r);
+  }
+  return prod;
+}
+
+// 32-bit fast path when every intermediate fits (the common case).
+__device__ __forceinline__ double kr_entry32(const KRSpec& s, uint32_t q, int r) {
+  double prod = 1.0;
+#pragma unroll 1
+  for (int k = 0; k < s.n; ++k) {
+    const uint32_t I = static_cast<uint32_t>(s.dims[k]);
+    const uint32_t d = q % I;
+    q /= I;
+    prod *= __ldg(s.A[k] + d + static_cast<int64_t>(I) * r);
+  }
+  return prod;
+}
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace cpdgpu

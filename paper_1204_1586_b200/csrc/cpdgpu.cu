@@ -1,0 +1,1099 @@
+// cpdgpu.cu — host orchestration and the C-ABI (include/cpdgpu.h).
+//
+// Drives Algorithm 2 of the reference (cp_gradient_all, mttkrp.cpp:113-253)
+// and the fast ALS sweep / driver (als.cpp:69-78, 147-210) on one B200:
+//   sort_modes (hoisted, cached per tensor) -> K1 seed contraction(s) ->
+//   deterministic partial reduction -> rank-batched recursion tail -> ALS
+//   update (on device) / gradients out.
+// Everything below the C-ABI is sm_100a device code; there is no CPU fallback.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/cpdgpu.h"
+#include "kernels.h"
+
+namespace {
+
+using cpdgpu::KRSpec;
+using cpdgpu::kMaxModes;
+
+struct Failure : std::exception {
+  int code;
+  std::string msg;
+  Failure(int c, std::string m) : code(c), msg(std::move(m)) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Failure(code, buf);
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) fail(CPDGPU_NO_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+  if (e != cudaSuccess) fail(CPDGPU_CUDA_ERROR, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    CK(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  double* d() const { return static_cast<double*>(p); }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    CK(cudaHostAlloc(&p, b, cudaHostAllocDefault));
+    bytes = b;
+  }
+  double* d() const { return static_cast<double*>(p); }
+};
+
+// ---- shape arithmetic (shape.cpp:8-36) ---------------------------------------
+
+std::vector<int64_t> prefix(const std::vector<int64_t>& dims) {
+  std::vector<int64_t> J(dims.size() + 1, 1);
+  for (size_t k = 0; k < dims.size(); ++k) {
+    if (dims[k] < 1)
+      fail(CPDGPU_SHAPE_ERROR, "shape: mode %zu has nonpositive extent %lld", k + 1,
+           static_cast<long long>(dims[k]));
+    int64_t next;
+    if (__builtin_mul_overflow(J[k], dims[k], &next))
+      fail(CPDGPU_SHAPE_ERROR, "shape: entry count overflows at mode %zu", k + 1);
+    J[k + 1] = next;
+  }
+  return J;
+}
+
+// select_pivot (mttkrp.cpp:56-65): max{n : J_n <= K_n}, ties to the larger n.
+int select_pivot(const std::vector<int64_t>& dims) {
+  const int N = static_cast<int>(dims.size());
+  if (N < 2) fail(CPDGPU_ARGUMENT_ERROR, "select_pivot: need an order-2 or higher shape");
+  const auto J = prefix(dims);
+  int pivot = 0;
+  for (int n = 1; n <= N; ++n)
+    if (J[n] <= J[N] / J[n]) pivot = n;
+  if (pivot == 0)
+    fail(CPDGPU_SHAPE_ERROR, "select_pivot: no mode satisfies J_n <= K_n; sort modes first");
+  return pivot;
+}
+
+// stable ascending sort (mttkrp.cpp:67-90); perm[j] = original mode at sorted j (1-based)
+std::vector<int> sort_perm(const std::vector<int64_t>& dims) {
+  std::vector<int> perm(dims.size());
+  for (size_t j = 0; j < dims.size(); ++j) perm[j] = static_cast<int>(j) + 1;
+  std::stable_sort(perm.begin(), perm.end(),
+                   [&](int a, int b) { return dims[a - 1] < dims[b - 1]; });
+  return perm;
+}
+
+bool ascending(const std::vector<int64_t>& dims) {
+  for (size_t k = 1; k < dims.size(); ++k)
+    if (dims[k] < dims[k - 1]) return false;
+  return true;
+}
+
+// fast_count_realized (mttkrp.cpp:292-320), ascending dims.
+uint64_t count_realized(const std::vector<int64_t>& dims, int64_t R, int n) {
+  const int N = static_cast<int>(dims.size());
+  const auto J = prefix(dims);
+  const int p = select_pivot(dims);
+  auto sumj = [&](int lo, int hi, int64_t div) {
+    uint64_t t = 0;
+    for (int k = std::max(lo, 0); k <= hi; ++k) t += static_cast<uint64_t>(J[k] / div);
+    return t;
+  };
+  auto K = [&](int m) { return static_cast<uint64_t>(J[N] / J[m]); };
+  const uint64_t uR = static_cast<uint64_t>(R);
+  if (n == p)
+    return uR * (static_cast<uint64_t>(J[N]) + sumj(n + 2, N, J[n]) + sumj(2, n - 1, 1) +
+                 static_cast<uint64_t>(J[n]));
+  if (n == p + 1)
+    return uR * (static_cast<uint64_t>(J[N]) + sumj(2, n - 1, 1) + sumj(n + 2, N, J[n]) + K(n - 1));
+  if (n < p) return uR * (static_cast<uint64_t>(J[n + 1]) + sumj(2, n - 1, 1) + static_cast<uint64_t>(J[n]));
+  return uR * (K(n - 2) + sumj(n + 2, N, J[n]) + K(n - 1));
+}
+
+// FastStats::peak_workspace_doubles as the reference tracks it (mttkrp.cpp:127-131,
+// 147-243): seeds, Khatri-Rao staging and recursion scratch, outputs excluded.
+int64_t reference_peak_workspace(const std::vector<int64_t>& sd, int p, int64_t R) {
+  const int N = static_cast<int>(sd.size());
+  const auto J = prefix(sd);
+  const int64_t Jp = J[p], Kp = J[N] / J[p];
+  int64_t live = 0, peak = 0;
+  auto track = [&](int64_t d) {
+    live += d;
+    peak = std::max(peak, live);
+  };
+  track(Kp * R);
+  track(Jp * R);
+  track(-Kp * R);
+  int64_t scr = std::max<int64_t>(J[p - 1], 1);
+  track(scr);
+  for (int j = p; j >= 1; --j) {
+    track(J[j - 1]);
+    track(-J[j - 1]);
+  }
+  track(-scr);
+  track(-Jp * R);
+  if (p + 1 <= N) {
+    track(Jp * R);
+    track(Kp * R);
+    track(-Jp * R);
+    scr = std::max<int64_t>(J[N] / J[p + 1], 1);
+    track(scr);
+    for (int j = p + 1; j <= N; ++j) {
+      const int64_t t = J[N] / J[j];
+      track(t);
+      track(-t);
+    }
+    track(-scr);
+    track(-Kp * R);
+  }
+  return peak;
+}
+
+}  // namespace
+
+// ---- objects -----------------------------------------------------------------
+
+struct Plan;
+
+struct cpdgpu_tensor {
+  cpdgpu_ctx* ctx = nullptr;
+  cpdgpu_dtype dtype = CPDGPU_F64;
+  std::vector<int64_t> dims;  // caller's mode order
+  int64_t numel = 0;
+  void* data = nullptr;
+  bool owned = false;
+  std::vector<int> perm;      // sorted position -> original mode (1-based)
+  bool identity = true;
+  void* sorted = nullptr;     // mode-sorted copy (== data when identity)
+  bool sorted_ready = false;
+  double norm2 = -1.0;
+  uint64_t id = 0;
+  size_t elem() const { return dtype == CPDGPU_F64 ? 8 : 4; }
+  ~cpdgpu_tensor() {
+    if (sorted && sorted != data) cudaFree(sorted);
+    if (owned && data) cudaFree(data);
+  }
+};
+
+struct Plan {
+  // sorted frame
+  int N = 0, p = 0;
+  int64_t R = 0;
+  std::vector<int64_t> sd, J;
+  int64_t Jp = 0, Kp = 0;
+  std::vector<int> perm;  // sorted j (0-based) -> original mode (1-based)
+  std::vector<int64_t> off_sorted, off_orig;
+  int64_t total_factor = 0;
+  // K1 chunks over the rank (<= 32 columns per pass)
+  struct Chunk {
+    int r0, Rc, NT;
+    cpdgpu::SeedParams sp;
+  };
+  std::vector<Chunk> chunks;
+  bool lpart_direct = false;  // one row block: the left partial is the seed itself
+  bool raw_frame = false;     // forced pivot: the caller's frame is used unsorted
+  DevBuf Fs, Forig, Gorig, Rpart, Lpart, Rs, Ls, Rtmp, Ltmp, cbpart, grams, costs, status, norm;
+  HostBuf hF, hG;
+  size_t cbpart_bytes = 0;
+
+  KRSpec spec(int lo, int hi, int r0) const {  // 1-based sorted modes lo..hi
+    KRSpec s{};
+    s.n = lo > hi ? 0 : hi - lo + 1;
+    for (int k = 0; k < s.n; ++k) {
+      const int j = lo - 1 + k;
+      s.dims[k] = sd[j];
+      s.A[k] = Fs.d() + off_sorted[j] + sd[j] * r0;
+    }
+    return s;
+  }
+  double* factor(int j) const { return Fs.d() + off_sorted[j - 1]; }  // sorted 1-based
+  int64_t K(int m) const { return J[N] / J[m]; }
+};
+
+struct cpdgpu_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own = nullptr, stream = nullptr;
+  std::string err;
+  bool graphs = true;
+  uint64_t launches = 0;
+  uint64_t next_id = 1;
+  std::map<std::tuple<uint64_t, int64_t, int>, std::unique_ptr<Plan>> plans;
+  DevBuf scratch;
+  bool timing = false;
+  std::vector<cudaEvent_t> seed_events;  // pairs around K1 launches
+  size_t seed_used = 0;                  // events used by the current call
+  ~cpdgpu_ctx() {
+    for (auto e : seed_events) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+int set_error(cpdgpu_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(cpdgpu_ctx* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) ctx->err.clear();
+    return CPDGPU_OK;
+  } catch (const Failure& e) {
+    return set_error(ctx, e.code, e.msg);
+  } catch (const std::exception& e) {
+    return set_error(ctx, CPDGPU_CUDA_ERROR, e.what());
+  }
+}
+
+void use_device(cpdgpu_ctx* ctx) { CK(cudaSetDevice(ctx->device)); }
+
+void ensure_sorted(cpdgpu_ctx* ctx, cpdgpu_tensor* t) {
+  if (t->sorted_ready) return;
+  if (t->identity) {
+    t->sorted = t->data;
+  } else {  // hoisted sort_modes copy (als.cpp:159-165)
+    CK(cudaMalloc(&t->sorted, static_cast<size_t>(t->numel) * t->elem()));
+    ctx->launches += cpdgpu::launch_permute(t->data, t->sorted, static_cast<int>(t->elem()),
+                                            static_cast<int>(t->dims.size()), t->dims.data(),
+                                            t->perm.data(), ctx->stream);
+    CK(cudaGetLastError());
+  }
+  t->sorted_ready = true;
+}
+
+int pick_nt(int64_t Rc) { return static_cast<int>((Rc + 7) / 8); }
+
+Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
+  auto key = std::make_tuple(t->id, R, pivot);
+  auto it = ctx->plans.find(key);
+  if (it != ctx->plans.end()) return it->second.get();
+  if (t->dtype != CPDGPU_F64)
+    fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: fp32 tensors use the tensor-core path (not built in this library)");
+  auto holder = std::make_unique<Plan>();
+  Plan& pl = *holder;
+  pl.N = static_cast<int>(t->dims.size());
+  pl.R = R;
+  pl.raw_frame = pivot > 0;
+  if (pl.raw_frame) {  // slab shards: the caller's (global, sorted) frame as is
+    pl.perm.resize(pl.N);
+    for (int j = 0; j < pl.N; ++j) pl.perm[j] = j + 1;
+  } else {
+    pl.perm = t->perm;
+  }
+  pl.sd.resize(pl.N);
+  for (int j = 0; j < pl.N; ++j) pl.sd[j] = t->dims[pl.perm[j] - 1];
+  pl.J = prefix(pl.sd);
+  pl.p = pivot > 0 ? pivot : select_pivot(pl.sd);
+  if (pl.p < 1 || pl.p > pl.N) fail(CPDGPU_ARGUMENT_ERROR, "pivot %d outside 1..%d", pl.p, pl.N);
+  pl.Jp = pl.J[pl.p];
+  pl.Kp = pl.J[pl.N] / pl.Jp;
+  pl.off_sorted.resize(pl.N);
+  pl.off_orig.resize(pl.N);
+  int64_t off = 0;
+  for (int m = 0; m < pl.N; ++m) {
+    pl.off_orig[m] = off;
+    off += t->dims[m] * R;
+  }
+  pl.total_factor = off;
+  off = 0;
+  for (int j = 0; j < pl.N; ++j) {
+    pl.off_sorted[j] = off;
+    off += pl.sd[j] * R;
+  }
+  const size_t fbytes = static_cast<size_t>(pl.total_factor) * sizeof(double);
+  pl.Fs.ensure(fbytes);
+  pl.Forig.ensure(fbytes);
+  pl.Gorig.ensure(fbytes);
+  pl.hF.ensure(fbytes);
+  pl.hG.ensure(fbytes);
+
+  // K1 geometry
+  const int64_t Jp = pl.Jp, Kp = pl.Kp;
+  const int64_t nRB = cpdgpu::ceil_div(Jp, 208);
+  int TI = static_cast<int>(cpdgpu::ceil_div(cpdgpu::ceil_div(Jp, nRB), 8) * 8);
+  const int LDY = TI + ((TI % 16 == 0) ? 4 : 12);
+  const int64_t nCT = cpdgpu::ceil_div(Kp, 32);
+  const int64_t T = nRB * nCT;
+  const int P = static_cast<int>(std::min<int64_t>(ctx->num_sms, T));
+  const int64_t per = cpdgpu::ceil_div(T, P);
+  const int slots = static_cast<int>(cpdgpu::ceil_div(per, nCT) + 1);
+  pl.lpart_direct = (nRB == 1);
+  size_t rpart = 0, lpart = 0;
+  for (int64_t r0 = 0; r0 < R; r0 += 32) {
+    Plan::Chunk c;
+    c.r0 = static_cast<int>(r0);
+    c.Rc = static_cast<int>(std::min<int64_t>(32, R - r0));
+    c.NT = pick_nt(c.Rc);
+    auto& sp = c.sp;
+    sp = cpdgpu::SeedParams{};
+    sp.J = Jp;
+    sp.K = Kp;
+    sp.R = c.Rc;
+    sp.TI = TI;
+    sp.LDY = LDY;
+    sp.LDK = (c.NT % 2 == 1) ? c.NT * 8 : c.NT * 8 + 8;
+    sp.nRB = nRB;
+    sp.nCT = nCT;
+    sp.T = T;
+    sp.P = P;
+    sp.slots = slots;
+    sp.use32 = (Jp < (1LL << 31) && Kp < (1LL << 31)) ? 1 : 0;
+    rpart = std::max(rpart, static_cast<size_t>(P) * slots * c.NT * 8 * TI);
+    lpart = std::max(lpart, static_cast<size_t>(nRB) * c.Rc * Kp);
+    pl.chunks.push_back(c);
+  }
+  pl.Rpart.ensure(rpart * sizeof(double));
+  if (!pl.lpart_direct) pl.Lpart.ensure(lpart * sizeof(double));
+  pl.Rs.ensure(static_cast<size_t>(Jp * R) * sizeof(double));
+  pl.Ls.ensure(static_cast<size_t>(Kp * R) * sizeof(double));
+  pl.Rtmp.ensure(static_cast<size_t>(Jp * R) * sizeof(double));
+  pl.Ltmp.ensure(static_cast<size_t>(Kp * R) * sizeof(double));
+  size_t cb = 0;
+  for (int j = pl.p + 1; j <= pl.N; ++j)
+    cb = std::max(cb, cpdgpu::contract_b_scratch(pl.sd[j - 1], pl.K(j), static_cast<int>(R),
+                                                 ctx->num_sms));
+  for (int j = pl.p - 1; j >= 1; --j)
+    cb = std::max(cb, cpdgpu::contract_b_scratch(pl.J[j], pl.sd[j], static_cast<int>(R),
+                                                 ctx->num_sms));
+  pl.cbpart.ensure(std::max<size_t>(cb, 1) * sizeof(double));
+  pl.grams.ensure(static_cast<size_t>(pl.N) * R * R * sizeof(double));
+  pl.status.ensure(sizeof(int) * 4);
+  pl.norm.ensure(sizeof(double) * 4);
+  Plan* raw = holder.get();
+  ctx->plans.emplace(key, std::move(holder));
+  return raw;
+}
+
+void bind_seed_inputs(Plan& pl, cpdgpu_tensor* t) {
+  for (auto& c : pl.chunks) {
+    c.sp.Y = static_cast<const double*>(pl.raw_frame ? t->data : t->sorted);
+    c.sp.left = pl.spec(1, pl.p, c.r0);
+    c.sp.right = pl.spec(pl.p + 1, pl.N, c.r0);
+    c.sp.Rpart = pl.Rpart.d();
+    c.sp.Lpart = pl.lpart_direct ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d();
+  }
+}
+
+// K1 + reduction.  mode 1: right seed, 2: left seed, 3: both (one HBM pass).
+cudaEvent_t seed_event(cpdgpu_ctx* ctx) {
+  if (ctx->seed_used == ctx->seed_events.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->seed_events.push_back(e);
+  }
+  return ctx->seed_events[ctx->seed_used++];
+}
+
+void run_seeds(cpdgpu_ctx* ctx, Plan& pl, int mode) {
+  cudaStream_t s = ctx->stream;
+  for (auto& c : pl.chunks) {
+    if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+    ctx->launches += cpdgpu::launch_seed_f64(c.sp, c.NT, mode, s);
+    if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+    if (mode & 1)
+      ctx->launches += cpdgpu::launch_reduce_right(c.sp, c.NT * 8, pl.Rs.d() + c.r0 * pl.Jp, pl.Jp, s);
+    if ((mode & 2) && !pl.lpart_direct)
+      ctx->launches += cpdgpu::launch_reduce_left(pl.Lpart.d(), c.sp.nRB, c.Rc, pl.Kp,
+                                                  pl.Ls.d() + c.r0 * pl.Kp, pl.Kp, s);
+  }
+  CK(cudaGetLastError());
+}
+
+using ModeCallback = std::function<void(int j, double* G)>;  // sorted 1-based mode
+
+// Right phase j = p..1 (mttkrp.cpp:165-193).  G(j) lands at gbase + off_orig.
+void right_phase(cpdgpu_ctx* ctx, Plan& pl, double* gbase, const ModeCallback& after) {
+  cudaStream_t s = ctx->stream;
+  const int R = static_cast<int>(pl.R);
+  double* cur = pl.Rs.d();
+  double* nxt = pl.Rtmp.d();
+  for (int j = pl.p; j >= 1; --j) {
+    if (j < pl.p) {  // Eq 3.20
+      ctx->launches += cpdgpu::launch_contract_b(cur, pl.Jp, pl.J[j], pl.sd[j], R, pl.spec(j + 1, j + 1, 0),
+                                                 nxt, pl.Jp, pl.cbpart.d(), ctx->num_sms, s);
+      std::swap(cur, nxt);
+    }
+    double* G = gbase + pl.off_orig[pl.perm[j - 1] - 1];
+    ctx->launches += cpdgpu::launch_contract_a(cur, pl.Jp, pl.J[j - 1], pl.sd[j - 1], R,
+                                               pl.spec(1, j - 1, 0), G, pl.sd[j - 1], s);  // Eq 3.12
+    CK(cudaGetLastError());
+    if (after) after(j, G);
+  }
+}
+
+// Left phase j = p+1..N (mttkrp.cpp:212-241).
+void left_phase(cpdgpu_ctx* ctx, Plan& pl, double* gbase, const ModeCallback& after) {
+  cudaStream_t s = ctx->stream;
+  const int R = static_cast<int>(pl.R);
+  double* cur = pl.Ls.d();
+  double* nxt = pl.Ltmp.d();
+  for (int j = pl.p + 1; j <= pl.N; ++j) {
+    if (j > pl.p + 1) {  // Eq 3.22
+      ctx->launches += cpdgpu::launch_contract_a(cur, pl.Kp, pl.sd[j - 2], pl.K(j - 1), R,
+                                                 pl.spec(j - 1, j - 1, 0), nxt, pl.Kp, s);
+      std::swap(cur, nxt);
+    }
+    double* G = gbase + pl.off_orig[pl.perm[j - 1] - 1];
+    ctx->launches += cpdgpu::launch_contract_b(cur, pl.Kp, pl.sd[j - 1], pl.K(j), R,
+                                               pl.spec(j + 1, pl.N, 0), G, pl.sd[j - 1],
+                                               pl.cbpart.d(), ctx->num_sms, s);  // Eq 3.16
+    CK(cudaGetLastError());
+    if (after) after(j, G);
+  }
+}
+
+void gather_factors(cpdgpu_ctx* ctx, Plan& pl, const double* src_orig) {
+  int64_t so[kMaxModes], dof[kMaxModes], len[kMaxModes];
+  for (int j = 0; j < pl.N; ++j) {
+    so[j] = pl.off_orig[pl.perm[j] - 1];
+    dof[j] = pl.off_sorted[j];
+    len[j] = pl.sd[j] * pl.R;
+  }
+  ctx->launches += cpdgpu::launch_gather_blocks(src_orig, pl.Fs.d(), pl.N, so, dof, len, ctx->stream);
+}
+
+void scatter_factors(cpdgpu_ctx* ctx, Plan& pl, double* dst_orig) {
+  int64_t so[kMaxModes], dof[kMaxModes], len[kMaxModes];
+  // inverse gather: orig block m <- sorted block inverse(m)
+  for (int j = 0; j < pl.N; ++j) {
+    const int m = pl.perm[j] - 1;
+    so[m] = pl.off_sorted[j];
+    dof[m] = pl.off_orig[m];
+    len[m] = pl.sd[j] * pl.R;
+  }
+  ctx->launches += cpdgpu::launch_gather_blocks(pl.Fs.d(), dst_orig, pl.N, so, dof, len, ctx->stream);
+}
+
+void upload_host_factors(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const double* const* factors) {
+  for (int m = 0; m < pl.N; ++m)
+    std::memcpy(pl.hF.d() + pl.off_orig[m], factors[m],
+                static_cast<size_t>(t->dims[m] * pl.R) * sizeof(double));
+  CK(cudaMemcpyAsync(pl.Forig.d(), pl.hF.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  gather_factors(ctx, pl, pl.Forig.d());
+}
+
+void validate_common(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const char* who) {
+  if (!ctx || !y) fail(CPDGPU_ARGUMENT_ERROR, "%s: null context or tensor", who);
+  if (y->dims.size() < 2) fail(CPDGPU_ARGUMENT_ERROR, "%s: need an order-2 or higher tensor", who);
+  if (R < 1) fail(CPDGPU_ARGUMENT_ERROR, "%s: rank must be positive", who);
+  use_device(ctx);
+  ctx->seed_used = 0;
+}
+
+void compute_norm2(cpdgpu_ctx* ctx, cpdgpu_tensor* t) {
+  if (t->norm2 >= 0.0) return;
+  ctx->scratch.ensure(2048 * sizeof(double));
+  DevBuf out;
+  out.ensure(sizeof(double));
+  ctx->launches += cpdgpu::launch_norm2(t->data, static_cast<int>(t->elem()), t->numel,
+                                        ctx->scratch.d(), out.d(), ctx->stream);
+  double v = 0.0;
+  CK(cudaMemcpyAsync(&v, out.d(), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  t->norm2 = v;
+}
+
+cpdgpu_tensor* new_tensor(cpdgpu_ctx* ctx, cpdgpu_dtype dtype, int N, const int64_t* dims) {
+  if (N < 1 || N > kMaxModes) fail(CPDGPU_ARGUMENT_ERROR, "tensor: order %d outside 1..%d", N, kMaxModes);
+  if (dtype != CPDGPU_F64 && dtype != CPDGPU_F32) fail(CPDGPU_ARGUMENT_ERROR, "tensor: unknown dtype");
+  auto t = std::make_unique<cpdgpu_tensor>();
+  t->ctx = ctx;
+  t->dtype = dtype;
+  t->dims.assign(dims, dims + N);
+  t->numel = prefix(t->dims).back();
+  t->perm = sort_perm(t->dims);
+  t->identity = true;
+  for (int j = 0; j < N; ++j) t->identity &= (t->perm[j] == j + 1);
+  t->id = ctx->next_id++;
+  return t.release();
+}
+
+// Drop cached plans of a tensor (its id is never reused).
+void forget_tensor(cpdgpu_ctx* ctx, uint64_t id) {
+  for (auto it = ctx->plans.begin(); it != ctx->plans.end();) {
+    if (std::get<0>(it->first) == id) it = ctx->plans.erase(it);
+    else ++it;
+  }
+}
+
+void init_grams(cpdgpu_ctx* ctx, Plan& pl) {
+  const int R = static_cast<int>(pl.R);
+  for (int j = 1; j <= pl.N; ++j)
+    ctx->launches += cpdgpu::launch_gram(pl.factor(j), pl.sd[j - 1], R,
+                                         pl.grams.d() + static_cast<int64_t>(j - 1) * R * R, ctx->stream);
+}
+
+// One fast ALS sweep on the device (als.cpp:69-78): right seed pass, modes
+// p..1, left seed pass with the updated factors, modes p+1..N; then the fit.
+void als_sweep_device(cpdgpu_ctx* ctx, Plan& pl, double rtol, double* cost_slot) {
+  const int R = static_cast<int>(pl.R);
+  auto update = [&](int j, double* G) {
+    ctx->launches += cpdgpu::launch_als_update(G, pl.sd[j - 1], R, pl.grams.d(), pl.N, j - 1, rtol,
+                                               pl.factor(j),
+                                               pl.grams.d() + static_cast<int64_t>(j - 1) * R * R,
+                                               static_cast<int*>(pl.status.p), ctx->stream);
+  };
+  run_seeds(ctx, pl, 1);
+  right_phase(ctx, pl, pl.Gorig.d(), update);
+  if (pl.p + 1 <= pl.N) {
+    run_seeds(ctx, pl, 2);
+    left_phase(ctx, pl, pl.Gorig.d(), update);
+  }
+  if (cost_slot) {
+    const int L = pl.p + 1 <= pl.N ? pl.N : 1;  // last visited mode (fast_update_order)
+    ctx->launches += cpdgpu::launch_als_cost(pl.factor(L), pl.Gorig.d() + pl.off_orig[pl.perm[L - 1] - 1],
+                                             pl.sd[L - 1], R, pl.grams.d(), pl.N, pl.norm.d(), cost_slot,
+                                             ctx->stream);
+  }
+  CK(cudaGetLastError());
+}
+
+void download_factors(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, double* const* factors) {
+  scatter_factors(ctx, pl, pl.Forig.d());
+  CK(cudaMemcpyAsync(pl.hF.d(), pl.Forig.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int m = 0; m < pl.N; ++m)
+    std::memcpy(factors[m], pl.hF.d() + pl.off_orig[m],
+                static_cast<size_t>(t->dims[m] * pl.R) * sizeof(double));
+}
+
+void check_status(cpdgpu_ctx* ctx, Plan& pl) {
+  int st = 0;
+  CK(cudaMemcpyAsync(&st, pl.status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (st == 4) fail(CPDGPU_NUMERIC_ERROR, "als_update_mode: non-finite gradient input");
+}
+
+void prepare_als(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* y) {
+  compute_norm2(ctx, y);
+  CK(cudaMemcpyAsync(pl.norm.d(), &y->norm2, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(pl.status.p, 0, sizeof(int), ctx->stream));
+  init_grams(ctx, pl);
+}
+
+}  // namespace
+
+// ---- C-ABI ---------------------------------------------------------------------
+
+extern "C" {
+
+int cpdgpu_create(cpdgpu_ctx** out, int device) {
+  if (!out) return CPDGPU_ARGUMENT_ERROR;
+  *out = nullptr;
+  auto ctx = std::make_unique<cpdgpu_ctx>();
+  const int st = guarded(nullptr, [&] {
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) fail(CPDGPU_ARGUMENT_ERROR, "device %d outside 0..%d", device, n - 1);
+    ctx->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0, minor = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10 || minor != 0)
+      fail(CPDGPU_CUDA_ERROR, "device %d is sm_%d%d; this library is built for sm_100a (B200) only",
+           device, major, minor);
+    CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+    ctx->stream = ctx->own;
+  });
+  if (st != CPDGPU_OK) return st;
+  *out = ctx.release();
+  return CPDGPU_OK;
+}
+
+int cpdgpu_destroy(cpdgpu_ctx* ctx) {
+  if (!ctx) return CPDGPU_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->plans.clear();
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+  return CPDGPU_OK;
+}
+
+const char* cpdgpu_last_error(const cpdgpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int cpdgpu_set_stream(cpdgpu_ctx* ctx, void* stream) {
+  if (!ctx) return CPDGPU_ARGUMENT_ERROR;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return CPDGPU_OK;
+}
+
+int cpdgpu_synchronize(cpdgpu_ctx* ctx) {
+  return guarded(ctx, [&] {
+    use_device(ctx);
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int cpdgpu_set_graphs(cpdgpu_ctx* ctx, int enabled) {
+  if (!ctx) return CPDGPU_ARGUMENT_ERROR;
+  ctx->graphs = enabled != 0;
+  return CPDGPU_OK;
+}
+
+uint64_t cpdgpu_launch_count(const cpdgpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cpdgpu_set_timing(cpdgpu_ctx* ctx, int enabled) {
+  if (!ctx) return CPDGPU_ARGUMENT_ERROR;
+  ctx->timing = enabled != 0;
+  return CPDGPU_OK;
+}
+
+int cpdgpu_last_seed_ms(cpdgpu_ctx* ctx, double* ms) {
+  return guarded(ctx, [&] {
+    if (!ms) fail(CPDGPU_ARGUMENT_ERROR, "last_seed_ms: null argument");
+    use_device(ctx);
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < ctx->seed_used; i += 2) {
+      CK(cudaEventSynchronize(ctx->seed_events[i + 1]));
+      float f = 0.f;
+      CK(cudaEventElapsedTime(&f, ctx->seed_events[i], ctx->seed_events[i + 1]));
+      tot += f;
+    }
+    *ms = tot;
+  });
+}
+
+int cpdgpu_tensor_update(cpdgpu_ctx* ctx, cpdgpu_tensor* t, const void* host) {
+  return guarded(ctx, [&] {
+    if (!ctx || !t || !host) fail(CPDGPU_ARGUMENT_ERROR, "tensor_update: null argument");
+    use_device(ctx);
+    CK(cudaMemcpyAsync(t->data, host, static_cast<size_t>(t->numel) * t->elem(), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    t->norm2 = -1.0;
+    if (!t->identity && t->sorted_ready) {  // refresh the sorted copy lazily
+      cudaFree(t->sorted);
+      t->sorted = nullptr;
+      t->sorted_ready = false;
+    }
+  });
+}
+
+int cpdgpu_tensor_upload(cpdgpu_ctx* ctx, const void* host, cpdgpu_dtype dtype, int N,
+                         const int64_t* dims, cpdgpu_tensor** out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !out || !dims) fail(CPDGPU_ARGUMENT_ERROR, "tensor_upload: null argument");
+    use_device(ctx);
+    std::unique_ptr<cpdgpu_tensor> t(new_tensor(ctx, dtype, N, dims));
+    const size_t bytes = static_cast<size_t>(t->numel) * t->elem();
+    CK(cudaMalloc(&t->data, bytes));
+    t->owned = true;
+    if (host) CK(cudaMemcpyAsync(t->data, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    else CK(cudaMemsetAsync(t->data, 0, bytes, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = t.release();
+  });
+}
+
+int cpdgpu_tensor_wrap_device(cpdgpu_ctx* ctx, void* device_ptr, cpdgpu_dtype dtype, int N,
+                              const int64_t* dims, cpdgpu_tensor** out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !out || !dims || !device_ptr) fail(CPDGPU_ARGUMENT_ERROR, "tensor_wrap_device: null argument");
+    use_device(ctx);
+    std::unique_ptr<cpdgpu_tensor> t(new_tensor(ctx, dtype, N, dims));
+    t->data = device_ptr;
+    t->owned = false;
+    *out = t.release();
+  });
+}
+
+int cpdgpu_tensor_generate(cpdgpu_ctx* ctx, cpdgpu_dtype dtype, int N, const int64_t* dims,
+                           cpdgpu_dist dist, uint64_t seed, int64_t offset, cpdgpu_tensor** out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !out || !dims) fail(CPDGPU_ARGUMENT_ERROR, "tensor_generate: null argument");
+    if (dist != CPDGPU_DIST_NORMAL && dist != CPDGPU_DIST_UNIFORM_PM1)
+      fail(CPDGPU_ARGUMENT_ERROR, "tensor_generate: unknown distribution");
+    use_device(ctx);
+    std::unique_ptr<cpdgpu_tensor> t(new_tensor(ctx, dtype, N, dims));
+    CK(cudaMalloc(&t->data, static_cast<size_t>(t->numel) * t->elem()));
+    t->owned = true;
+    ctx->launches += cpdgpu::launch_generate(t->data, static_cast<int>(t->elem()), t->numel,
+                                             static_cast<int>(dist), seed, offset, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = t.release();
+  });
+}
+
+int cpdgpu_tensor_axpby_kruskal(cpdgpu_ctx* ctx, cpdgpu_tensor* t, double alpha, double beta,
+                                const double* const* factors, int64_t R) {
+  return guarded(ctx, [&] {
+    if (!ctx || !t || !factors) fail(CPDGPU_ARGUMENT_ERROR, "tensor_axpby_kruskal: null argument");
+    if (R < 1) fail(CPDGPU_ARGUMENT_ERROR, "tensor_axpby_kruskal: rank must be positive");
+    use_device(ctx);
+    const int N = static_cast<int>(t->dims.size());
+    int64_t total = 0;
+    for (int m = 0; m < N; ++m) total += t->dims[m] * R;
+    DevBuf F;
+    F.ensure(static_cast<size_t>(total) * sizeof(double));
+    KRSpec all{};
+    all.n = N;
+    int64_t off = 0;
+    for (int m = 0; m < N; ++m) {
+      CK(cudaMemcpyAsync(F.d() + off, factors[m], static_cast<size_t>(t->dims[m] * R) * sizeof(double),
+                         cudaMemcpyHostToDevice, ctx->stream));
+      all.dims[m] = t->dims[m];
+      all.A[m] = F.d() + off;
+      off += t->dims[m] * R;
+    }
+    ctx->launches += cpdgpu::launch_axpby_kruskal(t->data, static_cast<int>(t->elem()), N, t->dims.data(),
+                                                  all, static_cast<int>(R), alpha, beta, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    t->norm2 = -1.0;
+    t->sorted_ready = t->identity ? t->sorted_ready : false;
+    if (!t->identity && t->sorted) {
+      cudaFree(t->sorted);
+      t->sorted = nullptr;
+    }
+  });
+}
+
+int cpdgpu_tensor_download(cpdgpu_ctx* ctx, const cpdgpu_tensor* t, void* host) {
+  return guarded(ctx, [&] {
+    if (!ctx || !t || !host) fail(CPDGPU_ARGUMENT_ERROR, "tensor_download: null argument");
+    use_device(ctx);
+    CK(cudaMemcpyAsync(host, t->data, static_cast<size_t>(t->numel) * t->elem(), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int cpdgpu_tensor_norm2(cpdgpu_ctx* ctx, cpdgpu_tensor* t, double* out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !t || !out) fail(CPDGPU_ARGUMENT_ERROR, "tensor_norm2: null argument");
+    use_device(ctx);
+    compute_norm2(ctx, t);
+    *out = t->norm2;
+  });
+}
+
+int cpdgpu_tensor_device_ptr(const cpdgpu_tensor* t, void** device_ptr) {
+  if (!t || !device_ptr) return CPDGPU_ARGUMENT_ERROR;
+  *device_ptr = t->data;
+  return CPDGPU_OK;
+}
+
+int cpdgpu_tensor_free(cpdgpu_tensor* t) {
+  if (!t) return CPDGPU_OK;
+  if (t->ctx) {
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    forget_tensor(t->ctx, t->id);
+  }
+  delete t;
+  return CPDGPU_OK;
+}
+
+int cpdgpu_select_pivot(int N, const int64_t* dims, int* pivot) {
+  return guarded(nullptr, [&] {
+    if (!dims || !pivot || N < 0) fail(CPDGPU_ARGUMENT_ERROR, "select_pivot: null argument");
+    *pivot = select_pivot(std::vector<int64_t>(dims, dims + N));
+  });
+}
+
+int cpdgpu_sort_modes(int N, const int64_t* dims, int* perm, int* inverse) {
+  return guarded(nullptr, [&] {
+    if (!dims || !perm || N < 1) fail(CPDGPU_ARGUMENT_ERROR, "sort_modes: bad argument");
+    const auto p = sort_perm(std::vector<int64_t>(dims, dims + N));
+    for (int j = 0; j < N; ++j) {
+      perm[j] = p[j];
+      if (inverse) inverse[p[j] - 1] = j + 1;
+    }
+  });
+}
+
+int cpdgpu_fast_update_order(int N, const int64_t* dims, int* order) {
+  return guarded(nullptr, [&] {
+    if (!dims || !order) fail(CPDGPU_ARGUMENT_ERROR, "fast_update_order: null argument");
+    if (N < 2) fail(CPDGPU_ARGUMENT_ERROR, "fast_update_order: need an order-2 or higher shape");
+    const std::vector<int64_t> d(dims, dims + N);
+    const auto perm = sort_perm(d);
+    std::vector<int64_t> sd(N);
+    for (int j = 0; j < N; ++j) sd[j] = d[perm[j] - 1];
+    const int p = select_pivot(sd);
+    int at = 0;
+    for (int j = p; j >= 1; --j) order[at++] = perm[j - 1];
+    for (int j = p + 1; j <= N; ++j) order[at++] = perm[j - 1];
+  });
+}
+
+uint64_t cpdgpu_fast_count_realized(int N, const int64_t* dims, int64_t R, int n) {
+  try {
+    if (!dims || N < 2 || R < 1 || n < 1 || n > N) return 0;
+    const std::vector<int64_t> d(dims, dims + N);
+    if (!ascending(d)) return 0;
+    return count_realized(d, R, n);
+  } catch (...) {
+    return 0;
+  }
+}
+
+int cpdgpu_cp_gradient_all(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const double* const* factors,
+                           double* const* gradients, uint64_t* mults_per_mode, int64_t* peak_workspace) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "cp_gradient_all");
+    if (!factors || !gradients) fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: null factor or gradient list");
+    ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, 0);
+    bind_seed_inputs(pl, y);
+    upload_host_factors(ctx, pl, y, factors);
+    run_seeds(ctx, pl, 3);
+    right_phase(ctx, pl, pl.Gorig.d(), nullptr);
+    left_phase(ctx, pl, pl.Gorig.d(), nullptr);
+    CK(cudaMemcpyAsync(pl.hG.d(), pl.Gorig.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int m = 0; m < pl.N; ++m)
+      std::memcpy(gradients[m], pl.hG.d() + pl.off_orig[m],
+                  static_cast<size_t>(y->dims[m] * R) * sizeof(double));
+    if (mults_per_mode)
+      for (int j = 1; j <= pl.N; ++j) mults_per_mode[pl.perm[j - 1] - 1] = count_realized(pl.sd, R, j);
+    if (peak_workspace) *peak_workspace = reference_peak_workspace(pl.sd, pl.p, R);
+  });
+}
+
+int cpdgpu_cp_gradient_all_hook(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors,
+                                double* const* gradients, cpdgpu_mode_hook hook, void* user,
+                                int64_t* peak_workspace) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "cp_gradient_all");
+    if (!factors || !gradients) fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: null factor or gradient list");
+    ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, 0);
+    bind_seed_inputs(pl, y);
+    upload_host_factors(ctx, pl, y, factors);
+    // emit (mttkrp.cpp:134-145): gradient out, counter charge, hook, re-read factor
+    auto emit = [&](int j, double* G) {
+      const int orig = pl.perm[j - 1];
+      const int64_t rows = pl.sd[j - 1];
+      const size_t bytes = static_cast<size_t>(rows * R) * sizeof(double);
+      CK(cudaMemcpyAsync(gradients[orig - 1], G, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (hook) {
+        const int st = hook(user, orig, gradients[orig - 1], rows, R, count_realized(pl.sd, R, j));
+        if (st != 0) fail(st, "cp_gradient_all: hook for mode %d failed", orig);
+        CK(cudaMemcpyAsync(pl.factor(j), factors[orig - 1], bytes, cudaMemcpyHostToDevice, ctx->stream));
+      }
+    };
+    // The left seed must see factors the hook replaced on the right side
+    // (mttkrp.cpp:143, 203): two seed passes, as in the ALS sweep.
+    run_seeds(ctx, pl, 1);
+    right_phase(ctx, pl, pl.Gorig.d(), emit);
+    if (pl.p + 1 <= pl.N) {
+      run_seeds(ctx, pl, 2);
+      left_phase(ctx, pl, pl.Gorig.d(), emit);
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (peak_workspace) *peak_workspace = reference_peak_workspace(pl.sd, pl.p, R);
+  });
+}
+
+int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const double* factors_dev,
+                                  double* gradients_dev, int pivot) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "cp_gradient_all");
+    if (!factors_dev || !gradients_dev) fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: null device buffer");
+    if (pivot < 0 || pivot > static_cast<int>(y->dims.size()))
+      fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: pivot %d outside 0..%zu", pivot, y->dims.size());
+    if (pivot == 0) ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, pivot);
+    bind_seed_inputs(pl, y);
+    gather_factors(ctx, pl, factors_dev);
+    run_seeds(ctx, pl, pl.p + 1 <= pl.N ? 3 : 1);
+    right_phase(ctx, pl, gradients_dev, nullptr);
+    left_phase(ctx, pl, gradients_dev, nullptr);
+    CK(cudaGetLastError());
+  });
+}
+
+int cpdgpu_pinv_psd(cpdgpu_ctx* ctx, int64_t R, const double* s, double rtol, double* out) {
+  return guarded(ctx, [&] {
+    if (!ctx || (R > 0 && (!s || !out))) fail(CPDGPU_ARGUMENT_ERROR, "pinv_psd: null argument");
+    if (rtol < 0.0) fail(CPDGPU_ARGUMENT_ERROR, "pinv_psd: rtol must be nonnegative");
+    if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "pinv_psd: rank %lld above the device limit 64", (long long)R);
+    if (R == 0) return;
+    use_device(ctx);
+    DevBuf d;
+    d.ensure(2 * static_cast<size_t>(R * R) * sizeof(double));
+    CK(cudaMemcpyAsync(d.d(), s, static_cast<size_t>(R * R) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->launches += cpdgpu::launch_pinv_psd(d.d(), static_cast<int>(R), rtol, d.d() + R * R, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, d.d() + R * R, static_cast<size_t>(R * R) * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int cpdgpu_als_update_mode(cpdgpu_ctx* ctx, int N, const int64_t* dims, int64_t R, const double* m,
+                           const double* const* factors, int n, double rtol, double* out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !dims || !m || !factors || !out) fail(CPDGPU_ARGUMENT_ERROR, "als_update_mode: null argument");
+    if (n < 1 || n > N) fail(CPDGPU_INDEX_ERROR, "als_update_mode: mode %d outside 1..%d", n, N);
+    if (R < 1 || R > 64) fail(CPDGPU_ARGUMENT_ERROR, "als_update_mode: rank %lld outside 1..64", (long long)R);
+    if (rtol < 0.0) fail(CPDGPU_ARGUMENT_ERROR, "pinv_psd: rtol must be nonnegative");
+    use_device(ctx);
+    int64_t total = 0;
+    for (int k = 0; k < N; ++k) total += dims[k] * R;
+    DevBuf F, G, grams, st;
+    F.ensure(static_cast<size_t>(total) * sizeof(double));
+    G.ensure(static_cast<size_t>(dims[n - 1] * R) * sizeof(double) * 2);
+    grams.ensure(static_cast<size_t>(N + 1) * R * R * sizeof(double));
+    st.ensure(sizeof(int));
+    CK(cudaMemsetAsync(st.p, 0, sizeof(int), ctx->stream));
+    int64_t off = 0;
+    for (int k = 0; k < N; ++k) {
+      CK(cudaMemcpyAsync(F.d() + off, factors[k], static_cast<size_t>(dims[k] * R) * sizeof(double),
+                         cudaMemcpyHostToDevice, ctx->stream));
+      ctx->launches += cpdgpu::launch_gram(F.d() + off, dims[k], static_cast<int>(R), grams.d() + k * R * R,
+                                           ctx->stream);
+      off += dims[k] * R;
+    }
+    const size_t gb = static_cast<size_t>(dims[n - 1] * R) * sizeof(double);
+    CK(cudaMemcpyAsync(G.d(), m, gb, cudaMemcpyHostToDevice, ctx->stream));
+    double* A = G.d() + dims[n - 1] * R;
+    ctx->launches += cpdgpu::launch_als_update(G.d(), dims[n - 1], static_cast<int>(R), grams.d(), N, n - 1, rtol,
+                                               A, grams.d() + N * R * R, static_cast<int*>(st.p), ctx->stream);
+    CK(cudaGetLastError());
+    int status = 0;
+    CK(cudaMemcpyAsync(&status, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(out, A, gb, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (status == 4) fail(CPDGPU_NUMERIC_ERROR, "als_update_mode: non-finite gradient input");
+  });
+}
+
+int cpdgpu_als_sweep(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, double pinv_rtol,
+                     double* cost_out, uint64_t* mults) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "als_sweep_fast");
+    if (!factors) fail(CPDGPU_ARGUMENT_ERROR, "als_sweep_fast: null factor list");
+    if (pinv_rtol < 0.0) fail(CPDGPU_ARGUMENT_ERROR, "pinv_psd: rtol must be nonnegative");
+    if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "als_sweep_fast: rank above the device ALS limit 64");
+    ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, 0);
+    bind_seed_inputs(pl, y);
+    upload_host_factors(ctx, pl, y, factors);
+    prepare_als(ctx, pl, y);
+    pl.costs.ensure(sizeof(double));
+    als_sweep_device(ctx, pl, pinv_rtol, pl.costs.d());
+    check_status(ctx, pl);
+    download_factors(ctx, pl, y, factors);
+    if (cost_out) CK(cudaMemcpy(cost_out, pl.costs.d(), sizeof(double), cudaMemcpyDeviceToHost));
+    if (mults) {
+      uint64_t tot = 0;
+      for (int j = 1; j <= pl.N; ++j) tot += count_realized(pl.sd, R, j);
+      *mults = tot;
+    }
+  });
+}
+
+int cpdgpu_als_run(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, int max_iters,
+                   double tol, double pinv_rtol, double* cost_trace, double* rel_trace, double* sec_trace,
+                   uint64_t* mults_trace, int* iters_run) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "run");
+    if (max_iters < 1) fail(CPDGPU_ARGUMENT_ERROR, "run: max_iters must be at least 1");
+    if (tol < 0.0 || pinv_rtol < 0.0) fail(CPDGPU_ARGUMENT_ERROR, "run: tolerances must be nonnegative");
+    if (!factors || !cost_trace || !rel_trace || !iters_run) fail(CPDGPU_ARGUMENT_ERROR, "run: null argument");
+    if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "run: rank above the device ALS limit 64");
+    ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, 0);
+    bind_seed_inputs(pl, y);
+    upload_host_factors(ctx, pl, y, factors);
+    prepare_als(ctx, pl, y);
+    pl.costs.ensure(static_cast<size_t>(max_iters) * sizeof(double));
+    uint64_t per_sweep = 0;
+    for (int j = 1; j <= pl.N; ++j) per_sweep += count_realized(pl.sd, R, j);
+    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(max_iters));
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    const double ynorm = std::sqrt(y->norm2);
+    double prev = std::nan("");
+    int done = 0;
+    for (int it = 1; it <= max_iters; ++it) {
+      CK(cudaEventRecord(ev[2 * (it - 1)], ctx->stream));
+      als_sweep_device(ctx, pl, pinv_rtol, nullptr);
+      CK(cudaEventRecord(ev[2 * (it - 1) + 1], ctx->stream));
+      const int L = pl.p + 1 <= pl.N ? pl.N : 1;
+      ctx->launches += cpdgpu::launch_als_cost(pl.factor(L), pl.Gorig.d() + pl.off_orig[pl.perm[L - 1] - 1],
+                                               pl.sd[L - 1], static_cast<int>(R), pl.grams.d(), pl.N, pl.norm.d(),
+                                               pl.costs.d() + (it - 1), ctx->stream);
+      ++done;
+      if (tol > 0.0) {  // early stop needs the fit on the host every sweep
+        double d = 0.0;
+        CK(cudaMemcpyAsync(&d, pl.costs.d() + (it - 1), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (it > 1 && std::abs(d - prev) / std::max(prev, 1e-15) < tol) break;
+        prev = d;
+      }
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    check_status(ctx, pl);
+    CK(cudaMemcpy(cost_trace, pl.costs.d(), static_cast<size_t>(done) * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < done; ++i) {
+      rel_trace[i] = ynorm > 0.0 ? std::sqrt(cost_trace[i]) / ynorm : std::sqrt(cost_trace[i]);
+      if (sec_trace) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+        sec_trace[i] = ms * 1e-3;
+      }
+      if (mults_trace) mults_trace[i] = per_sweep * static_cast<uint64_t>(i + 1);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    *iters_run = done;
+    download_factors(ctx, pl, y, factors);
+  });
+}
+
+}  // extern "C"
