@@ -194,7 +194,8 @@ def run_ours(args, cfg):
     dims, R, dtype, desc = cfg
     N = len(dims)
     ctx = cpd.Context(local)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # a real stream handle (the legacy default is 0)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
     # global tensor: dims[:-1] x (dims[-1] * world); this rank's slab is dims

@@ -233,10 +233,20 @@ __global__ void als_cost_kernel(const double* __restrict__ A, const double* __re
   }
 }
 
+// Opt-in dynamic shared memory, once per (kernel, size): never inside a graph capture.
 void set_smem(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024)
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(bytes));
+  static const void* done_fn[8] = {nullptr};
+  static size_t done_bytes[8] = {0};
+  if (bytes <= 48 * 1024) return;
+  for (int i = 0; i < 8; ++i)
+    if (done_fn[i] == fn && done_bytes[i] >= bytes) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  for (int i = 0; i < 8; ++i)
+    if (done_fn[i] == fn || done_fn[i] == nullptr) {
+      done_fn[i] = fn;
+      done_bytes[i] = bytes;
+      return;
+    }
 }
 
 }  // namespace

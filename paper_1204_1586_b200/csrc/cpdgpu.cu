@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -231,14 +232,38 @@ struct Plan {
   // K1 chunks over the rank (<= 32 columns per pass)
   struct Chunk {
     int r0, Rc, NT;
+    int64_t rpart_off = 0, lpart_off = 0;
     cpdgpu::SeedParams sp;
+    std::unique_ptr<DevBuf> KRr, KRl;  // pre-built Khatri-Rao rows [K][LDK], [J][LDK]
+    CUtensorMap kmap{};
+    bool kmap_ok = false;
   };
   std::vector<Chunk> chunks;
   bool lpart_direct = false;  // one row block: the left partial is the seed itself
   bool raw_frame = false;     // forced pivot: the caller's frame is used unsorted
-  DevBuf Fs, Forig, Gorig, Rpart, Lpart, Rs, Ls, Rtmp, Ltmp, cbpart, grams, costs, status, norm;
+  bool tma_ok = false;        // Y tiles by 2-D TMA (even leading extent)
+  CUtensorMap tmap{};         // bound to the tensor's device address
+  const void* tmap_base = nullptr;
+  DevBuf Fs, Forig, Gorig, Rpart, Lpart, Rs, Ls, Rtmp, Ltmp, grams, costs, status, norm;
+  DevBuf slot_tab;            // CSR of right-partial slots per row block: [nRB + 1] + [slots]
+  int slot_tab_ptr_len = 0;
+  int slot_tab_max = 0;         // most slots any row block has
   HostBuf hF, hG;
-  size_t cbpart_bytes = 0;
+  DevBuf gtab;                              // device table of the N output pointers
+  cudaGraph_t grad_graph = nullptr;         // hook-free gradient
+  cudaGraphExec_t grad_exec = nullptr;
+  cudaGraphNode_t prologue_node = nullptr;  // patched per call (inputs / outputs)
+  uint64_t grad_graph_launches = 0;
+  bool grad_warm = false;
+  cudaGraphExec_t als_exec = nullptr;       // one fast ALS sweep
+  uint64_t als_graph_launches = 0;
+  bool als_warm = false;
+  double als_rtol = -1.0;
+  ~Plan() {
+    if (grad_exec) cudaGraphExecDestroy(grad_exec);
+    if (grad_graph) cudaGraphDestroy(grad_graph);
+    if (als_exec) cudaGraphExecDestroy(als_exec);
+  }
 
   KRSpec spec(int lo, int hi, int r0) const {  // 1-based sorted modes lo..hi
     KRSpec s{};
@@ -356,9 +381,26 @@ Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
 
   // K1 geometry
   const int64_t Jp = pl.Jp, Kp = pl.Kp;
-  const int64_t nRB = cpdgpu::ceil_div(Jp, 208);
-  int TI = static_cast<int>(cpdgpu::ceil_div(cpdgpu::ceil_div(Jp, nRB), 8) * 8);
-  const int LDY = TI + ((TI % 16 == 0) ? 4 : 12);
+  // Row block TI: multiple of 8 (DMMA fragments) and == 8 (mod 16) so the dense
+  // TMA tile (LDY == TI) keeps the right-product fragment loads conflict-free.
+  int ti_max = 208;
+  for (int64_t r0 = 0; r0 < R; r0 += 32)
+    ti_max = std::min(ti_max, cpdgpu::seed_f64_max_ti(pick_nt(std::min<int64_t>(32, R - r0))));
+  if (ti_max % 16 != 8) ti_max -= 8;
+  auto ti_for = [](int64_t rows) {
+    int64_t ti = (rows + 7) / 8 * 8;
+    if (ti % 16 == 0) ti += 8;
+    return static_cast<int>(ti);
+  };
+  int64_t nRB = cpdgpu::ceil_div(Jp, ti_max);
+  int TI = ti_for(cpdgpu::ceil_div(Jp, nRB));
+  while (TI > ti_max) {
+    ++nRB;
+    TI = ti_for(cpdgpu::ceil_div(Jp, nRB));
+  }
+  pl.tma_ok = (Jp % 2 == 0);
+  // TMA box rows TI + 4 (== 12 mod 16): conflict-free fragment loads for both products
+  const int LDY = pl.tma_ok ? TI + 4 : TI + 12;
   const int64_t nCT = cpdgpu::ceil_div(Kp, 32);
   const int64_t T = nRB * nCT;
   const int P = static_cast<int>(std::min<int64_t>(ctx->num_sms, T));
@@ -385,25 +427,53 @@ Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
     sp.P = P;
     sp.slots = slots;
     sp.use32 = (Jp < (1LL << 31) && Kp < (1LL << 31)) ? 1 : 0;
-    rpart = std::max(rpart, static_cast<size_t>(P) * slots * c.NT * 8 * TI);
-    lpart = std::max(lpart, static_cast<size_t>(nRB) * c.Rc * Kp);
-    pl.chunks.push_back(c);
+    const int lk = (c.NT % 2 == 1) ? c.NT * 8 : c.NT * 8 + 8;
+    const size_t ldy = pl.tma_ok ? TI + 4 : TI + 12;
+    sp.stages = std::max(cpdgpu::seed_f64_smem_bytes(c.NT, TI, ldy, lk, 3, 3, 0),
+                         cpdgpu::seed_f64_smem_bytes(c.NT, TI, ldy, lk, 2, 3, 0)) <= cpdgpu::kSeedSmemLimit
+                    ? 3 : 2;
+    if (const char* e = std::getenv("CPDGPU_SEED_STAGES")) sp.stages = std::atoi(e);
+    c.KRr = std::make_unique<DevBuf>();
+    c.KRl = std::make_unique<DevBuf>();
+    c.KRr->ensure(static_cast<size_t>(Kp) * lk * sizeof(double));
+    c.KRl->ensure(static_cast<size_t>(Jp) * lk * sizeof(double));
+    sp.KRr_g = c.KRr->d();
+    sp.KRl_g = c.KRl->d();
+    c.kmap_ok = pl.tma_ok && cpdgpu::make_tensor_map_2d(&c.kmap, c.KRr->p, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                                                       static_cast<uint64_t>(lk), static_cast<uint64_t>(Kp),
+                                                       static_cast<uint64_t>(lk) * 8, static_cast<uint32_t>(lk), 32);
+    c.rpart_off = static_cast<int64_t>(rpart);  // per-chunk partials: all chunks run before the reduction
+    c.lpart_off = static_cast<int64_t>(lpart);
+    rpart += static_cast<size_t>(P) * slots * c.NT * 8 * TI;
+    lpart += static_cast<size_t>(nRB) * c.Rc * Kp;
+    pl.chunks.push_back(std::move(c));
   }
   pl.Rpart.ensure(rpart * sizeof(double));
+  {  // slot table: CTA c owns tiles [c T / P, (c + 1) T / P) and one slot per row block it touches
+    std::vector<std::vector<int>> per(static_cast<size_t>(nRB));
+    for (int64_t c = 0; c < P; ++c) {
+      const int64_t a = c * T / P, b = (c + 1) * T / P;
+      if (a >= b) continue;
+      for (int64_t rb = a / nCT; rb <= (b - 1) / nCT; ++rb)
+        per[static_cast<size_t>(rb)].push_back(static_cast<int>(c * slots + (rb - a / nCT)));
+    }
+    std::vector<int> tab(static_cast<size_t>(nRB) + 1, 0);
+    for (int64_t rb = 0; rb < nRB; ++rb) {
+      tab[rb + 1] = tab[rb] + static_cast<int>(per[rb].size());
+      pl.slot_tab_max = std::max(pl.slot_tab_max, static_cast<int>(per[rb].size()));
+    }
+    for (auto& v : per) tab.insert(tab.end(), v.begin(), v.end());
+    pl.slot_tab.ensure(tab.size() * sizeof(int));
+    CK(cudaMemcpy(pl.slot_tab.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+    pl.slot_tab_ptr_len = static_cast<int>(nRB) + 1;
+  }
   if (!pl.lpart_direct) pl.Lpart.ensure(lpart * sizeof(double));
   pl.Rs.ensure(static_cast<size_t>(Jp * R) * sizeof(double));
   pl.Ls.ensure(static_cast<size_t>(Kp * R) * sizeof(double));
   pl.Rtmp.ensure(static_cast<size_t>(Jp * R) * sizeof(double));
   pl.Ltmp.ensure(static_cast<size_t>(Kp * R) * sizeof(double));
-  size_t cb = 0;
-  for (int j = pl.p + 1; j <= pl.N; ++j)
-    cb = std::max(cb, cpdgpu::contract_b_scratch(pl.sd[j - 1], pl.K(j), static_cast<int>(R),
-                                                 ctx->num_sms));
-  for (int j = pl.p - 1; j >= 1; --j)
-    cb = std::max(cb, cpdgpu::contract_b_scratch(pl.J[j], pl.sd[j], static_cast<int>(R),
-                                                 ctx->num_sms));
-  pl.cbpart.ensure(std::max<size_t>(cb, 1) * sizeof(double));
   pl.grams.ensure(static_cast<size_t>(pl.N) * R * R * sizeof(double));
+  pl.gtab.ensure(kMaxModes * sizeof(double*));
   pl.status.ensure(sizeof(int) * 4);
   pl.norm.ensure(sizeof(double) * 4);
   Plan* raw = holder.get();
@@ -412,16 +482,28 @@ Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
 }
 
 void bind_seed_inputs(Plan& pl, cpdgpu_tensor* t) {
+  const void* ybase = pl.raw_frame ? t->data : t->sorted;
+  bool tma = pl.tma_ok;
+  if (tma && pl.tmap_base != ybase) {
+    tma = cpdgpu::make_tensor_map_2d(&pl.tmap, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                                     static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
+                                     static_cast<uint64_t>(pl.Jp) * 8,
+                                     static_cast<uint32_t>(pl.chunks[0].sp.TI + 4), 32);
+    pl.tmap_base = tma ? ybase : nullptr;
+  }
+  tma = tma && pl.tmap_base == ybase;
   for (auto& c : pl.chunks) {
-    c.sp.Y = static_cast<const double*>(pl.raw_frame ? t->data : t->sorted);
+    c.sp.use_tma = (tma && c.kmap_ok) ? 1 : 0;
+    c.sp.LDY = c.sp.use_tma ? c.sp.TI + 4 : c.sp.TI + 12;
+    c.sp.Y = static_cast<const double*>(ybase);
     c.sp.left = pl.spec(1, pl.p, c.r0);
     c.sp.right = pl.spec(pl.p + 1, pl.N, c.r0);
-    c.sp.Rpart = pl.Rpart.d();
-    c.sp.Lpart = pl.lpart_direct ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d();
+    c.sp.Rpart = pl.Rpart.d() + c.rpart_off;
+    c.sp.Lpart = pl.lpart_direct ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d() + c.lpart_off;
   }
 }
 
-// K1 + reduction.  mode 1: right seed, 2: left seed, 3: both (one HBM pass).
+// ---- K1 launches ---------------------------------------------------------------
 cudaEvent_t seed_event(cpdgpu_ctx* ctx) {
   if (ctx->seed_used == ctx->seed_events.size()) {
     cudaEvent_t e;
@@ -431,64 +513,362 @@ cudaEvent_t seed_event(cpdgpu_ctx* ctx) {
   return ctx->seed_events[ctx->seed_used++];
 }
 
+// K1 seed contraction(s).  mode 1: right seed, 2: left seed, 3: both (one HBM pass).
+// The Khatri-Rao rows must already be in the chunks' KRr / KRl buffers.
 void run_seeds(cpdgpu_ctx* ctx, Plan& pl, int mode) {
   cudaStream_t s = ctx->stream;
+  static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
   for (auto& c : pl.chunks) {
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
-    ctx->launches += cpdgpu::launch_seed_f64(c.sp, c.NT, mode, s);
+    DevBuf tb;
+    if (trace) {
+      tb.ensure(static_cast<size_t>(c.sp.P) * 9 * 4 * 8);
+      CK(cudaMemsetAsync(tb.p, 0, tb.bytes, s));
+      c.sp.trace = static_cast<unsigned long long*>(tb.p);
+    }
+    ctx->launches += cpdgpu::launch_seed_f64(c.sp, &pl.tmap, &c.kmap, c.NT, mode, s);
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
-    if (mode & 1)
-      ctx->launches += cpdgpu::launch_reduce_right(c.sp, c.NT * 8, pl.Rs.d() + c.r0 * pl.Jp, pl.Jp, s);
-    if ((mode & 2) && !pl.lpart_direct)
-      ctx->launches += cpdgpu::launch_reduce_left(pl.Lpart.d(), c.sp.nRB, c.Rc, pl.Kp,
-                                                  pl.Ls.d() + c.r0 * pl.Kp, pl.Kp, s);
+    if (trace) {
+      std::vector<unsigned long long> h(static_cast<size_t>(c.sp.P) * 36);
+      CK(cudaMemcpyAsync(h.data(), tb.p, tb.bytes, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      c.sp.trace = nullptr;
+      double w[9] = {0}, tot[9] = {0}, mx = 0;
+      for (int cta = 0; cta < c.sp.P; ++cta)
+        for (int wp = 0; wp < 9; ++wp) {
+          const unsigned long long* e = &h[(static_cast<size_t>(cta) * 9 + wp) * 4];
+          w[wp] += e[0];
+          tot[wp] += e[2];
+          mx = std::max(mx, static_cast<double>(e[2]));
+        }
+      std::fprintf(stderr, "[seed trace mode %d] per-warp avg cycles (wait/total): ", mode);
+      for (int wp = 0; wp < 9; ++wp) std::fprintf(stderr, "w%d %.0f/%.0f  ", wp, w[wp] / c.sp.P, tot[wp] / c.sp.P);
+      std::fprintf(stderr, "max warp total %.0f\n", mx);
+    }
   }
   CK(cudaGetLastError());
 }
 
-using ModeCallback = std::function<void(int j, double* G)>;  // sorted 1-based mode
+// ---- prologue and recursion-tail steps -----------------------------------------
 
-// Right phase j = p..1 (mttkrp.cpp:165-193).  G(j) lands at gbase + off_orig.
-void right_phase(cpdgpu_ctx* ctx, Plan& pl, double* gbase, const ModeCallback& after) {
-  cudaStream_t s = ctx->stream;
-  const int R = static_cast<int>(pl.R);
-  double* cur = pl.Rs.d();
-  double* nxt = pl.Rtmp.d();
+// Khatri-Rao spec over sorted modes lo..hi whose factors live at base (packed
+// in the caller's mode order when orig, in the sorted order otherwise).
+KRSpec spec_over(const Plan& pl, const double* base, bool orig, int lo, int hi, int r0) {
+  KRSpec s{};
+  s.n = lo > hi ? 0 : hi - lo + 1;
+  for (int k = 0; k < s.n; ++k) {
+    const int j = lo - 1 + k;
+    const int64_t off = orig ? pl.off_orig[pl.perm[j] - 1] : pl.off_sorted[j];
+    s.dims[k] = pl.sd[j];
+    s.A[k] = base + off + pl.sd[j] * r0;
+  }
+  return s;
+}
+
+// Khatri-Rao rows for the chunks' K1 launches: kr_mask 1 = KR(p+1..N) rows
+// (right product), 2 = KR(1..p) rows (left product).
+void add_kr_jobs(const Plan& pl, cpdgpu::Prologue& pr, const double* base, bool orig, int kr_mask) {
+  for (const auto& c : pl.chunks) {
+    if (kr_mask & 1) {
+      cpdgpu::KRJob& k = pr.kr[pr.nkr++];
+      k.spec = spec_over(pl, base, orig, pl.p + 1, pl.N, c.r0);
+      k.L = pl.Kp;
+      k.R = c.Rc;
+      k.NT = c.NT;
+      k.LDK = c.sp.LDK;
+      k.out = c.KRr->d();
+    }
+    if (kr_mask & 2) {
+      cpdgpu::KRJob& k = pr.kr[pr.nkr++];
+      k.spec = spec_over(pl, base, orig, 1, pl.p, c.r0);
+      k.L = pl.Jp;
+      k.R = c.Rc;
+      k.NT = c.NT;
+      k.LDK = c.sp.LDK;
+      k.out = c.KRl->d();
+    }
+  }
+}
+
+// Gradient prologue: sorted factors <- fin (caller order), output table <- gout
+// (caller order, gout_base + off_orig), Khatri-Rao rows read straight from fin.
+cpdgpu::Prologue grad_prologue(const Plan& pl, const double* fin, double* gout_base, int kr_mask) {
+  cpdgpu::Prologue pr{};
+  pr.N = pl.N;
+  pr.fin = fin;
+  pr.Fs = pl.Fs.d();
+  for (int j = 0; j < pl.N; ++j) {
+    pr.src_off[j] = pl.off_orig[pl.perm[j] - 1];
+    pr.dst_off[j] = pl.off_sorted[j];
+    pr.len[j] = pl.sd[j] * pl.R;
+  }
+  for (int m = 0; m < pl.N; ++m) pr.gout[m] = gout_base ? gout_base + pl.off_orig[m] : nullptr;
+  add_kr_jobs(pl, pr, fin, true, kr_mask);
+  return pr;
+}
+
+// Khatri-Rao rows only, from the sorted device factors (ALS / hook sweeps).
+void launch_kr_from_fs(cpdgpu_ctx* ctx, Plan& pl, int kr_mask) {
+  cpdgpu::Prologue pr{};
+  pr.N = 0;
+  pr.Fs = nullptr;
+  add_kr_jobs(pl, pr, pl.Fs.d(), false, kr_mask);
+  ctx->launches += cpdgpu::launch_prologue(pr, static_cast<double**>(pl.gtab.p), ctx->num_sms, ctx->stream);
+}
+
+void set_gtab(cpdgpu_ctx* ctx, Plan& pl, double* gout_base) {
+  cpdgpu::Prologue pr{};
+  pr.N = pl.N;
+  pr.Fs = nullptr;
+  for (int m = 0; m < pl.N; ++m) pr.gout[m] = gout_base + pl.off_orig[m];
+  ctx->launches += cpdgpu::launch_prologue(pr, static_cast<double**>(pl.gtab.p), ctx->num_sms, ctx->stream);
+}
+
+cpdgpu::TailOp op_base(int type, int R) {
+  cpdgpu::TailOp o{};
+  o.type = type;
+  o.R = R;
+  o.out_slot = -1;
+  return o;
+}
+
+// Seed-partial reductions for the given seed mode.
+void add_reduce_ops(const Plan& pl, cpdgpu::TailStep& st, int mode) {
+  for (const auto& c : pl.chunks) {
+    if (mode & 1) {
+      cpdgpu::TailOp o = op_base(cpdgpu::kOpReduceRight, c.Rc);
+      o.Z = pl.Rpart.d() + c.rpart_off;
+      o.B = pl.slot_tab_max >= 16 ? 1 : 0;  // many slots per row: lanes over slots
+      o.M = pl.Jp;
+      o.RP = c.NT * 8;
+      o.TI = c.sp.TI;
+      o.rb_ptr = static_cast<const int*>(pl.slot_tab.p);
+      o.slot_list = static_cast<const int*>(pl.slot_tab.p) + pl.slot_tab_ptr_len;
+      o.out = pl.Rs.d() + static_cast<int64_t>(c.r0) * pl.Jp;
+      o.ldo = pl.Jp;
+      st.op[st.n++] = o;
+    }
+    if ((mode & 2) && !pl.lpart_direct) {
+      cpdgpu::TailOp o = op_base(cpdgpu::kOpReduceLeft, c.Rc);
+      o.Z = pl.Lpart.d() + c.lpart_off;
+      o.M = pl.Kp;
+      o.B = c.sp.nRB;
+      o.out = pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp;
+      o.ldo = pl.Kp;
+      st.op[st.n++] = o;
+    }
+  }
+}
+
+// Right phase at sorted mode j (mttkrp.cpp:165-193), reading R^(j) at cur:
+//   extraction  G(j)[b, r] = sum_a R^(j)[a + J_{j-1} b, r] KR(1..j-1)[a, r]   (Eq 3.12)
+//   recursion   R^(j-1)[a, r] = sum_b R^(j)[a + J_{j-1} b, r] A_j[b, r]      (Eq 3.20)
+void add_right_extract(const Plan& pl, cpdgpu::TailStep& st, int j, const double* cur) {
+  cpdgpu::TailOp o = op_base(cpdgpu::kOpContractA, static_cast<int>(pl.R));
+  o.Z = cur;
+  o.ldz = pl.Jp;
+  o.M = pl.J[j - 1];
+  o.B = pl.sd[j - 1];
+  o.kr = spec_over(pl, pl.Fs.d(), false, 1, j - 1, 0);
+  o.out_slot = pl.perm[j - 1] - 1;
+  o.ldo = pl.sd[j - 1];
+  st.op[st.n++] = o;
+}
+void add_right_recurse(const Plan& pl, cpdgpu::TailStep& st, int j, const double* cur, double* nxt) {
+  cpdgpu::TailOp o = op_base(cpdgpu::kOpContractB, static_cast<int>(pl.R));
+  o.Z = cur;
+  o.ldz = pl.Jp;
+  o.M = pl.J[j - 1];
+  o.B = pl.sd[j - 1];
+  o.kr = spec_over(pl, pl.Fs.d(), false, j, j, 0);
+  o.out = nxt;
+  o.ldo = pl.Jp;
+  st.op[st.n++] = o;
+}
+// Left phase at sorted mode j (mttkrp.cpp:212-241), reading L^(j) at cur:
+//   extraction  G(j)[b, r] = sum_c L^(j)[b + I_j c, r] KR(j+1..N)[c, r]      (Eq 3.16)
+//   recursion   L^(j+1)[c, r] = sum_b L^(j)[b + I_j c, r] A_j[b, r]          (Eq 3.22)
+void add_left_extract(const Plan& pl, cpdgpu::TailStep& st, int j, const double* cur) {
+  cpdgpu::TailOp o = op_base(cpdgpu::kOpContractB, static_cast<int>(pl.R));
+  o.Z = cur;
+  o.ldz = pl.Kp;
+  o.M = pl.sd[j - 1];
+  o.B = pl.K(j);
+  o.kr = spec_over(pl, pl.Fs.d(), false, j + 1, pl.N, 0);
+  o.out_slot = pl.perm[j - 1] - 1;
+  o.ldo = pl.sd[j - 1];
+  st.op[st.n++] = o;
+}
+void add_left_recurse(const Plan& pl, cpdgpu::TailStep& st, int j, const double* cur, double* nxt) {
+  cpdgpu::TailOp o = op_base(cpdgpu::kOpContractA, static_cast<int>(pl.R));
+  o.Z = cur;
+  o.ldz = pl.Kp;
+  o.M = pl.sd[j - 1];
+  o.B = pl.K(j);
+  o.kr = spec_over(pl, pl.Fs.d(), false, j, j, 0);
+  o.out = nxt;
+  o.ldo = pl.Kp;
+  st.op[st.n++] = o;
+}
+
+void launch_step(cpdgpu_ctx* ctx, Plan& pl, const cpdgpu::TailStep& st) {
+  ctx->launches += cpdgpu::launch_tail_step(st, static_cast<double* const*>(pl.gtab.p), ctx->num_sms, ctx->stream);
+}
+
+// Whole hook-free gradient after the prologue: fused seeds, reductions, then
+// the right and left phases advancing together, one launch per level.
+void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
+  const bool left = pl.p + 1 <= pl.N;
+  run_seeds(ctx, pl, left ? 3 : 1);
+  cpdgpu::TailStep st{};
+  add_reduce_ops(pl, st, left ? 3 : 1);
+  launch_step(ctx, pl, st);
+  double* rc = pl.Rs.d();
+  double* rn = pl.Rtmp.d();
+  double* lc = pl.Ls.d();
+  double* ln = pl.Ltmp.d();
+  const int levels = std::max(pl.p, pl.N - pl.p);
+  for (int lv = 0; lv < levels; ++lv) {
+    cpdgpu::TailStep s{};
+    const int jr = pl.p - lv;      // right phase mode at this level
+    const int jl = pl.p + 1 + lv;  // left phase mode at this level
+    if (jr >= 1) {
+      add_right_extract(pl, s, jr, rc);
+      if (jr >= 2) add_right_recurse(pl, s, jr, rc, rn);
+    }
+    if (jl <= pl.N) {
+      add_left_extract(pl, s, jl, lc);
+      if (jl < pl.N) add_left_recurse(pl, s, jl, lc, ln);
+    }
+    launch_step(ctx, pl, s);
+    if (jr >= 2) std::swap(rc, rn);
+    if (jl < pl.N) std::swap(lc, ln);
+  }
+  CK(cudaGetLastError());
+}
+
+// Gauss-Seidel sweep body shared by ALS and the generic hook: separate right /
+// left seed passes; after(j) runs once G(j) is out and may replace A_j before
+// the recursion consumes it (mttkrp.cpp:137-144, 174, 203, 222).
+using ModeCallback = std::function<void(int j)>;
+
+void sweep_body(cpdgpu_ctx* ctx, Plan& pl, const ModeCallback& after) {
+  launch_kr_from_fs(ctx, pl, 1);
+  run_seeds(ctx, pl, 1);
+  {
+    cpdgpu::TailStep st{};
+    add_reduce_ops(pl, st, 1);
+    launch_step(ctx, pl, st);
+  }
+  double* rc = pl.Rs.d();
+  double* rn = pl.Rtmp.d();
   for (int j = pl.p; j >= 1; --j) {
-    if (j < pl.p) {  // Eq 3.20
-      ctx->launches += cpdgpu::launch_contract_b(cur, pl.Jp, pl.J[j], pl.sd[j], R, pl.spec(j + 1, j + 1, 0),
-                                                 nxt, pl.Jp, pl.cbpart.d(), ctx->num_sms, s);
-      std::swap(cur, nxt);
+    cpdgpu::TailStep st{};
+    add_right_extract(pl, st, j, rc);
+    launch_step(ctx, pl, st);
+    after(j);
+    if (j >= 2) {
+      cpdgpu::TailStep sr{};
+      add_right_recurse(pl, sr, j, rc, rn);
+      launch_step(ctx, pl, sr);
+      std::swap(rc, rn);
     }
-    double* G = gbase + pl.off_orig[pl.perm[j - 1] - 1];
-    ctx->launches += cpdgpu::launch_contract_a(cur, pl.Jp, pl.J[j - 1], pl.sd[j - 1], R,
-                                               pl.spec(1, j - 1, 0), G, pl.sd[j - 1], s);  // Eq 3.12
-    CK(cudaGetLastError());
-    if (after) after(j, G);
   }
+  if (pl.p + 1 <= pl.N) {
+    launch_kr_from_fs(ctx, pl, 2);
+    run_seeds(ctx, pl, 2);
+    if (!pl.lpart_direct) {
+      cpdgpu::TailStep st{};
+      add_reduce_ops(pl, st, 2);
+      launch_step(ctx, pl, st);
+    }
+    double* lc = pl.Ls.d();
+    double* ln = pl.Ltmp.d();
+    for (int j = pl.p + 1; j <= pl.N; ++j) {
+      cpdgpu::TailStep st{};
+      add_left_extract(pl, st, j, lc);
+      launch_step(ctx, pl, st);
+      after(j);
+      if (j < pl.N) {
+        cpdgpu::TailStep sl{};
+        add_left_recurse(pl, sl, j, lc, ln);
+        launch_step(ctx, pl, sl);
+        std::swap(lc, ln);
+      }
+    }
+  }
+  CK(cudaGetLastError());
 }
 
-// Left phase j = p+1..N (mttkrp.cpp:212-241).
-void left_phase(cpdgpu_ctx* ctx, Plan& pl, double* gbase, const ModeCallback& after) {
-  cudaStream_t s = ctx->stream;
-  const int R = static_cast<int>(pl.R);
-  double* cur = pl.Ls.d();
-  double* nxt = pl.Ltmp.d();
-  for (int j = pl.p + 1; j <= pl.N; ++j) {
-    if (j > pl.p + 1) {  // Eq 3.22
-      ctx->launches += cpdgpu::launch_contract_a(cur, pl.Kp, pl.sd[j - 2], pl.K(j - 1), R,
-                                                 pl.spec(j - 1, j - 1, 0), nxt, pl.Kp, s);
-      std::swap(cur, nxt);
-    }
-    double* G = gbase + pl.off_orig[pl.perm[j - 1] - 1];
-    ctx->launches += cpdgpu::launch_contract_b(cur, pl.Kp, pl.sd[j - 1], pl.K(j), R,
-                                               pl.spec(j + 1, pl.N, 0), G, pl.sd[j - 1],
-                                               pl.cbpart.d(), ctx->num_sms, s);  // Eq 3.16
-    CK(cudaGetLastError());
-    if (after) after(j, G);
+// Graph of the hook-free gradient (prologue + body), captured once per plan;
+// each call patches the prologue node (input factors, output pointers).
+void run_gradient(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_base) {
+  const bool left = pl.p + 1 <= pl.N;
+  const cpdgpu::Prologue pr = grad_prologue(pl, fin, gout_base, left ? 3 : 1);
+  const bool use_graph = ctx->graphs && !ctx->timing && std::getenv("CPDGPU_SEED_TRACE") == nullptr;
+  if (!use_graph) {
+    ctx->launches += cpdgpu::launch_prologue(pr, static_cast<double**>(pl.gtab.p), ctx->num_sms, ctx->stream);
+    gradient_body(ctx, pl);
+    return;
   }
+  if (!pl.grad_exec) {
+    if (!pl.grad_warm) {  // first call eager: configures kernel attributes outside capture
+      ctx->launches += cpdgpu::launch_prologue(pr, static_cast<double**>(pl.gtab.p), ctx->num_sms, ctx->stream);
+      gradient_body(ctx, pl);
+      pl.grad_warm = true;
+      return;
+    }
+    const uint64_t before = ctx->launches;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    cpdgpu::launch_prologue(pr, static_cast<double**>(pl.gtab.p), ctx->num_sms, ctx->stream);
+    gradient_body(ctx, pl);
+    CK(cudaStreamEndCapture(ctx->stream, &g));
+    pl.grad_graph_launches = ctx->launches - before + 1;
+    ctx->launches = before;
+    size_t n = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(g, nodes.data(), &n));
+    pl.prologue_node = nullptr;
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      CK(cudaGraphNodeGetType(nd, &ty));
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp{};
+      CK(cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == cpdgpu::prologue_kernel_fn()) pl.prologue_node = nd;
+    }
+    if (!pl.prologue_node) fail(CPDGPU_CUDA_ERROR, "graph capture: prologue node not found");
+    CK(cudaGraphInstantiate(&pl.grad_exec, g, 0));
+    pl.grad_graph = g;
+  }
+  // patch the prologue's arguments, then replay
+  cudaKernelNodeParams kp{};
+  dim3 grid, block;
+  cpdgpu::prologue_geometry(pr, ctx->num_sms, &grid, &block);
+  void* gt = pl.gtab.p;
+  void* args[] = {const_cast<cpdgpu::Prologue*>(&pr), &gt};
+  kp.func = const_cast<void*>(cpdgpu::prologue_kernel_fn());
+  kp.gridDim = grid;
+  kp.blockDim = block;
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  CK(cudaGraphExecKernelNodeSetParams(pl.grad_exec, pl.prologue_node, &kp));
+  CK(cudaGraphLaunch(pl.grad_exec, ctx->stream));
+  ctx->launches += pl.grad_graph_launches;
 }
 
+void upload_host_factors(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const double* const* factors) {
+  for (int m = 0; m < pl.N; ++m)
+    std::memcpy(pl.hF.d() + pl.off_orig[m], factors[m],
+                static_cast<size_t>(t->dims[m] * pl.R) * sizeof(double));
+  CK(cudaMemcpyAsync(pl.Forig.d(), pl.hF.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
+                     cudaMemcpyHostToDevice, ctx->stream));
+}
+
+// Sorted device factors <- caller-order device buffer (ALS / hook entry).
 void gather_factors(cpdgpu_ctx* ctx, Plan& pl, const double* src_orig) {
   int64_t so[kMaxModes], dof[kMaxModes], len[kMaxModes];
   for (int j = 0; j < pl.N; ++j) {
@@ -501,23 +881,13 @@ void gather_factors(cpdgpu_ctx* ctx, Plan& pl, const double* src_orig) {
 
 void scatter_factors(cpdgpu_ctx* ctx, Plan& pl, double* dst_orig) {
   int64_t so[kMaxModes], dof[kMaxModes], len[kMaxModes];
-  // inverse gather: orig block m <- sorted block inverse(m)
-  for (int j = 0; j < pl.N; ++j) {
+  for (int j = 0; j < pl.N; ++j) {  // caller block m <- sorted block j with perm[j] = m + 1
     const int m = pl.perm[j] - 1;
     so[m] = pl.off_sorted[j];
     dof[m] = pl.off_orig[m];
     len[m] = pl.sd[j] * pl.R;
   }
   ctx->launches += cpdgpu::launch_gather_blocks(pl.Fs.d(), dst_orig, pl.N, so, dof, len, ctx->stream);
-}
-
-void upload_host_factors(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const double* const* factors) {
-  for (int m = 0; m < pl.N; ++m)
-    std::memcpy(pl.hF.d() + pl.off_orig[m], factors[m],
-                static_cast<size_t>(t->dims[m] * pl.R) * sizeof(double));
-  CK(cudaMemcpyAsync(pl.Forig.d(), pl.hF.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
-                     cudaMemcpyHostToDevice, ctx->stream));
-  gather_factors(ctx, pl, pl.Forig.d());
 }
 
 void validate_common(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const char* who) {
@@ -572,28 +942,55 @@ void init_grams(cpdgpu_ctx* ctx, Plan& pl) {
 }
 
 // One fast ALS sweep on the device (als.cpp:69-78): right seed pass, modes
-// p..1, left seed pass with the updated factors, modes p+1..N; then the fit.
-void als_sweep_device(cpdgpu_ctx* ctx, Plan& pl, double rtol, double* cost_slot) {
+// p..1, left seed pass with the updated factors, modes p+1..N.  G(n) lands in
+// Gorig (through the output table set by prepare_als).
+void als_sweep_device(cpdgpu_ctx* ctx, Plan& pl, double rtol) {
   const int R = static_cast<int>(pl.R);
-  auto update = [&](int j, double* G) {
+  sweep_body(ctx, pl, [&](int j) {
+    double* G = pl.Gorig.d() + pl.off_orig[pl.perm[j - 1] - 1];
     ctx->launches += cpdgpu::launch_als_update(G, pl.sd[j - 1], R, pl.grams.d(), pl.N, j - 1, rtol,
-                                               pl.factor(j),
-                                               pl.grams.d() + static_cast<int64_t>(j - 1) * R * R,
+                                               pl.factor(j), pl.grams.d() + static_cast<int64_t>(j - 1) * R * R,
                                                static_cast<int*>(pl.status.p), ctx->stream);
-  };
-  run_seeds(ctx, pl, 1);
-  right_phase(ctx, pl, pl.Gorig.d(), update);
-  if (pl.p + 1 <= pl.N) {
-    run_seeds(ctx, pl, 2);
-    left_phase(ctx, pl, pl.Gorig.d(), update);
+  });
+}
+
+// cost after a sweep: last visited mode L (fast_update_order) gives <Y, Yhat>
+void als_cost(cpdgpu_ctx* ctx, Plan& pl, double* cost_slot) {
+  const int L = pl.p + 1 <= pl.N ? pl.N : 1;
+  ctx->launches += cpdgpu::launch_als_cost(pl.factor(L), pl.Gorig.d() + pl.off_orig[pl.perm[L - 1] - 1],
+                                           pl.sd[L - 1], static_cast<int>(pl.R), pl.grams.d(), pl.N, pl.norm.d(),
+                                           cost_slot, ctx->stream);
+}
+
+// Sweep through a CUDA graph captured once per plan (fixed device buffers).
+void als_sweep_graph(cpdgpu_ctx* ctx, Plan& pl, double rtol) {
+  if (!ctx->graphs || ctx->timing) {
+    als_sweep_device(ctx, pl, rtol);
+    return;
   }
-  if (cost_slot) {
-    const int L = pl.p + 1 <= pl.N ? pl.N : 1;  // last visited mode (fast_update_order)
-    ctx->launches += cpdgpu::launch_als_cost(pl.factor(L), pl.Gorig.d() + pl.off_orig[pl.perm[L - 1] - 1],
-                                             pl.sd[L - 1], R, pl.grams.d(), pl.N, pl.norm.d(), cost_slot,
-                                             ctx->stream);
+  if (pl.als_exec && pl.als_rtol != rtol) {
+    cudaGraphExecDestroy(pl.als_exec);
+    pl.als_exec = nullptr;
   }
-  CK(cudaGetLastError());
+  if (!pl.als_exec) {
+    if (!pl.als_warm) {
+      als_sweep_device(ctx, pl, rtol);
+      pl.als_warm = true;
+      return;
+    }
+    const uint64_t before = ctx->launches;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    als_sweep_device(ctx, pl, rtol);
+    CK(cudaStreamEndCapture(ctx->stream, &g));
+    pl.als_graph_launches = ctx->launches - before;
+    ctx->launches = before;
+    CK(cudaGraphInstantiate(&pl.als_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+    pl.als_rtol = rtol;
+  }
+  CK(cudaGraphLaunch(pl.als_exec, ctx->stream));
+  ctx->launches += pl.als_graph_launches;
 }
 
 void download_factors(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, double* const* factors) {
@@ -617,6 +1014,8 @@ void prepare_als(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* y) {
   compute_norm2(ctx, y);
   CK(cudaMemcpyAsync(pl.norm.d(), &y->norm2, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(pl.status.p, 0, sizeof(int), ctx->stream));
+  gather_factors(ctx, pl, pl.Forig.d());
+  set_gtab(ctx, pl, pl.Gorig.d());
   init_grams(ctx, pl);
 }
 
@@ -889,9 +1288,7 @@ int cpdgpu_cp_gradient_all(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const d
     Plan& pl = *get_plan(ctx, y, R, 0);
     bind_seed_inputs(pl, y);
     upload_host_factors(ctx, pl, y, factors);
-    run_seeds(ctx, pl, 3);
-    right_phase(ctx, pl, pl.Gorig.d(), nullptr);
-    left_phase(ctx, pl, pl.Gorig.d(), nullptr);
+    run_gradient(ctx, pl, pl.Forig.d(), pl.Gorig.d());
     CK(cudaMemcpyAsync(pl.hG.d(), pl.Gorig.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -914,12 +1311,15 @@ int cpdgpu_cp_gradient_all_hook(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, do
     Plan& pl = *get_plan(ctx, y, R, 0);
     bind_seed_inputs(pl, y);
     upload_host_factors(ctx, pl, y, factors);
+    gather_factors(ctx, pl, pl.Forig.d());
+    set_gtab(ctx, pl, pl.Gorig.d());
     // emit (mttkrp.cpp:134-145): gradient out, counter charge, hook, re-read factor
-    auto emit = [&](int j, double* G) {
+    auto emit = [&](int j) {
       const int orig = pl.perm[j - 1];
       const int64_t rows = pl.sd[j - 1];
       const size_t bytes = static_cast<size_t>(rows * R) * sizeof(double);
-      CK(cudaMemcpyAsync(gradients[orig - 1], G, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(gradients[orig - 1], pl.Gorig.d() + pl.off_orig[orig - 1], bytes, cudaMemcpyDeviceToHost,
+                         ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
       if (hook) {
         const int st = hook(user, orig, gradients[orig - 1], rows, R, count_realized(pl.sd, R, j));
@@ -929,12 +1329,7 @@ int cpdgpu_cp_gradient_all_hook(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, do
     };
     // The left seed must see factors the hook replaced on the right side
     // (mttkrp.cpp:143, 203): two seed passes, as in the ALS sweep.
-    run_seeds(ctx, pl, 1);
-    right_phase(ctx, pl, pl.Gorig.d(), emit);
-    if (pl.p + 1 <= pl.N) {
-      run_seeds(ctx, pl, 2);
-      left_phase(ctx, pl, pl.Gorig.d(), emit);
-    }
+    sweep_body(ctx, pl, emit);
     CK(cudaStreamSynchronize(ctx->stream));
     if (peak_workspace) *peak_workspace = reference_peak_workspace(pl.sd, pl.p, R);
   });
@@ -950,10 +1345,7 @@ int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, 
     if (pivot == 0) ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, pivot);
     bind_seed_inputs(pl, y);
-    gather_factors(ctx, pl, factors_dev);
-    run_seeds(ctx, pl, pl.p + 1 <= pl.N ? 3 : 1);
-    right_phase(ctx, pl, gradients_dev, nullptr);
-    left_phase(ctx, pl, gradients_dev, nullptr);
+    run_gradient(ctx, pl, factors_dev, gradients_dev);
     CK(cudaGetLastError());
   });
 }
@@ -1027,7 +1419,8 @@ int cpdgpu_als_sweep(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const
     upload_host_factors(ctx, pl, y, factors);
     prepare_als(ctx, pl, y);
     pl.costs.ensure(sizeof(double));
-    als_sweep_device(ctx, pl, pinv_rtol, pl.costs.d());
+    als_sweep_graph(ctx, pl, pinv_rtol);
+    als_cost(ctx, pl, pl.costs.d());
     check_status(ctx, pl);
     download_factors(ctx, pl, y, factors);
     if (cost_out) CK(cudaMemcpy(cost_out, pl.costs.d(), sizeof(double), cudaMemcpyDeviceToHost));
@@ -1063,12 +1456,9 @@ int cpdgpu_als_run(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* 
     int done = 0;
     for (int it = 1; it <= max_iters; ++it) {
       CK(cudaEventRecord(ev[2 * (it - 1)], ctx->stream));
-      als_sweep_device(ctx, pl, pinv_rtol, nullptr);
+      als_sweep_graph(ctx, pl, pinv_rtol);
       CK(cudaEventRecord(ev[2 * (it - 1) + 1], ctx->stream));
-      const int L = pl.p + 1 <= pl.N ? pl.N : 1;
-      ctx->launches += cpdgpu::launch_als_cost(pl.factor(L), pl.Gorig.d() + pl.off_orig[pl.perm[L - 1] - 1],
-                                               pl.sd[L - 1], static_cast<int>(R), pl.grams.d(), pl.N, pl.norm.d(),
-                                               pl.costs.d() + (it - 1), ctx->stream);
+      als_cost(ctx, pl, pl.costs.d() + (it - 1));
       ++done;
       if (tol > 0.0) {  // early stop needs the fit on the host every sweep
         double d = 0.0;

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -20,35 +21,89 @@ struct SeedParams {
   int P;            // CTAs (persistent)
   int slots;        // right-partial slots per CTA
   int use32;        // all KR row indices fit in 32 bits
+  int use_tma;      // Y tiles arrive by 2-D TMA (dense LDY == TI); else plain copies
+  int stages;       // pipeline depth (2 or 3)
+  int debug;        // experiment knobs (CPDGPU_SEED_DEBUG): bit 0 skips KR generation
   KRSpec left;      // modes 1..p   (rows of the view)
   KRSpec right;     // modes p+1..N (columns of the view)
+  const double* KRl_g;  // Khatri-Rao rows of the view's rows    [J][LDK] (kr_materialize)
+  const double* KRr_g;  // Khatri-Rao rows of the view's columns [K][LDK]
+  unsigned long long* trace;  // optional per-warp cycle counters [P][9][4] (CPDGPU_SEED_TRACE)
   double* Rpart;    // [P * slots][R8][TI]
   double* Lpart;    // [nRB][R][K]
 };
-int seed_f64_stages(int NT);
-size_t seed_f64_smem_bytes(int NT, int TI, int LDY, int LDK, int mode);
-int launch_seed_f64(const SeedParams& p, int NT, int mode, cudaStream_t s);
+int seed_f64_stages(int NT);  // default depth before the factor-staging choice
+// largest row block the fused kernel can hold in registers for this NT
+int seed_f64_max_ti(int NT);
+size_t seed_f64_smem_bytes(int NT, int TI, int LDY, int LDK, int mode, int stages, int64_t fac_doubles);
+constexpr size_t kSeedSmemLimit = 232448 - 1024;  // per-block opt-in limit, minus slack
+// tmap: 2-D tensor map of Y (dim0 = rows J, dim1 = columns K, box TI x 32), or
+// nullptr when p.use_tma == 0.
+// kmap: 2-D tensor map of KRr_g (dim0 = LDK, dim1 = K, box LDK x 32).
+int launch_seed_f64(const SeedParams& p, const CUtensorMap* tmap, const CUtensorMap* kmap, int NT, int mode,
+                    cudaStream_t s);
 
-// ---- reductions of the seed partials (tail.cu) ------------------------------
-// Rs[r * ldo + i] = sum over the (CTA, row block) slots covering row i.
-int launch_reduce_right(const SeedParams& p, int RP, double* Rs, int64_t ldo, cudaStream_t s);
-// Ls[r * ldo + j] = sum_rb Lpart[rb][r][j]
-int launch_reduce_left(const double* Lpart, int64_t nRB, int R, int64_t K, double* Ls,
-                        int64_t ldo, cudaStream_t s);
+// Host helper: 2-D tiled tensor map (driver entry point, no -lcuda link).
+bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, int elem_bytes,
+                        uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1);
 
-// ---- K2: rank-batched TTV contractions of the recursion tail (tail.cu) -------
-// out[r*ldo + b] = sum_{a<M} Z[r*ldz + a + M*b] * KR_v[a, r]      (Eq 3.12 / 3.22)
-int launch_contract_a(const double* Z, int64_t ldz, int64_t M, int64_t B, int R,
-                       const KRSpec& v, double* out, int64_t ldo, cudaStream_t s);
-// out[r*ldo + a] = sum_{b<B} Z[r*ldz + a + M*b] * KR_w[b, r]      (Eq 3.20 / 3.16)
-// part: scratch of at least contract_b_scratch(M, B, R) doubles.
-size_t contract_b_scratch(int64_t M, int64_t B, int R, int num_sms);
-int launch_contract_b(const double* Z, int64_t ldz, int64_t M, int64_t B, int R,
-                       const KRSpec& w, double* out, int64_t ldo, double* part, int num_sms,
-                       cudaStream_t s);
+// ---- prologue + recursion tail (tail.cu) ------------------------------------
+enum TailOpType { kOpNone = 0, kOpContractA = 1, kOpContractB = 2, kOpReduceRight = 3, kOpReduceLeft = 4 };
+
+// One rank-batched contraction / reduction (all R columns):
+//  ContractA: out[r*ldo + b] = sum_{a<M} Z[r*ldz + a + M*b] * KR(kr)[a, r]   (Eq 3.12 / 3.22)
+//  ContractB: out[r*ldo + a] = sum_{b<B} Z[r*ldz + a + M*b] * KR(kr)[b, r]   (Eq 3.20 / 3.16)
+//  ReduceRight: out[r*ldo + i] = sum over the right-partial slots of row block i / TI
+//               (Z = Rpart [slots][RP][TI], M = J rows, CSR rb_ptr / slot_list)
+//  ReduceLeft:  out[r*ldo + j] = sum_{rb < B} Z[(rb*R + r)*M + j]  (M = K columns)
+// out_slot >= 0 writes through the device pointer table instead of `out`.
+struct TailOp {
+  int type;
+  int R;
+  const double* Z;
+  int64_t ldz, M, B;
+  KRSpec kr;
+  double* out;
+  int64_t ldo;
+  int out_slot;
+  int64_t out_off;
+  int RP, TI;
+  const int* rb_ptr;
+  const int* slot_list;
+};
+constexpr int kMaxTailOps = 8;
+struct TailStep {
+  int n;
+  TailOp op[kMaxTailOps];
+};
+int64_t tail_step_units(const TailStep& st);
+int launch_tail_step(const TailStep& st, double* const* gtab, int num_sms, cudaStream_t s);
+
+// Khatri-Rao rows for K1: out[q*LDK + r] = KR(spec)[q, r] for q < L (zero past R).
+struct KRJob {
+  KRSpec spec;
+  int64_t L;
+  int R, NT, LDK;
+  double* out;
+};
+constexpr int kMaxKRJobs = 8;
+// Prologue of a gradient: Fs block j <- fin block (src_off[j]) (skipped when Fs
+// is null), gtab[m] <- gout[m], then every KR job.
+struct Prologue {
+  int N;
+  const double* fin;
+  double* Fs;
+  int64_t src_off[kMaxModes], dst_off[kMaxModes], len[kMaxModes];
+  double* gout[kMaxModes];
+  int nkr;
+  KRJob kr[kMaxKRJobs];
+};
+int launch_prologue(const Prologue& pr, double** gtab, int num_sms, cudaStream_t s);
+const void* prologue_kernel_fn();
+void prologue_geometry(const Prologue& pr, int num_sms, dim3* grid, dim3* block);
 
 // ---- utilities (util.cu) -----------------------------------------------------
-// packed factor gather: dst block j <- src block perm[j]-1 (sorted frame)
+// packed factor gather: dst block j <- src block (src_off[j]); plain block copies
 int launch_gather_blocks(const double* src, double* dst, int N, const int64_t* src_off,
                           const int64_t* dst_off, const int64_t* len, cudaStream_t s);
 // out (sorted frame) <- permute(in, perm) (tensor_ops.cpp:39-71), dtype size 4 or 8

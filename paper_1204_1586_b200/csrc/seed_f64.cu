@@ -8,23 +8,30 @@
 // seed must see factors the right phase already updated (mttkrp.cpp:143,203),
 // so the two products run as separate passes (MODE 1, MODE 2).
 //
-// Design (DESIGN.md §Kernels/K1):
-//  * Y tiles of TI rows x 32 columns stream HBM -> shared memory with
-//    cp.async (16-byte LDGSTS, zero-filled at the edges), STAGES deep.
-//  * Khatri-Rao rows are never materialised in HBM: the KR(p+1..N) rows of a
-//    tile (32 x RP) and the KR(1..p) rows of a row block (TI x RP) are
-//    generated in shared memory from factor rows (kron_range_column,
-//    kron.cpp:54-68, later modes outermost).
-//  * Right product (M = rows, N = rank, K = columns) and left product computed
-//    as  L^T = KR^T * Y  (M = rank, N = columns, K = rows) with
-//    mma.sync.m8n8k4.f64 (DMMA): measured 37.1 TF/s on B200 vs 36.7 TF/s for
-//    DFMA at full occupancy, with ~1/16 of the issue slots.
-//  * Each persistent CTA owns a contiguous range of the row-block-major tile
-//    space.  Right partials persist in registers across a row block and are
-//    written once per (CTA, row block) slot; left partials are written per tile
-//    per row block.  A deterministic reduction (tail.cu) sums them in a fixed
-//    order, so results are bitwise reproducible run to run.
+// Design (DESIGN.md §K1):
+//  * Warp-specialised persistent CTA: warp 8 is the producer, warps 0-7 consume.
+//    Per tile (TI rows x 32 columns of Y) the producer issues two 2-D TMA loads
+//    onto one mbarrier: the Y tile and the tile's 32 Khatri-Rao rows
+//    KR(p+1..N) (kron_range_column, kron.cpp:54-68, later modes outermost).
+//    STAGES-deep ring; out-of-range rows/columns arrive zero-filled.
+//  * The Khatri-Rao rows are built by a pre-pass kernel (kr_materialize) into a
+//    small L2-resident buffer (K_p x R and J_p x R, <= 1% of Y) instead of inside
+//    this kernel: on B200 fp64 multiplies issue to the same FP64 datapath as
+//    DMMA, and generating them here made the producer warp the bottleneck
+//    (measured 87% busy on config 3, profiles/r01_seed_trace.txt).
+//  * Consumers run mma.sync.m8n8k4.f64 (DMMA): measured 37.1 TF/s on B200 vs
+//    36.7 TF/s for DFMA, with a sixteenth of the issue slots.  Right product
+//    Rs = Y * KR_r (M = rows, N = rank, K = columns); left product as
+//    Ls^T = KR_l^T * Y (M = rank, N = columns, K = rows).
+//  * MODE 3 splits the consumers by product (warps 0-3 right, 4-7 left) so no
+//    cross-warp reduction is needed; right partials persist in registers over a
+//    row block and go out once per (CTA, row block) slot, left partials once per
+//    tile and row block.  tail.cu reduces both in a fixed order, so results are
+//    bitwise reproducible.
 #include <cstdint>
+#include <cstring>
+
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -38,29 +45,309 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
-constexpr int kTJ = 32;       // columns per tile
-constexpr int kThreads = 256;  // 8 warps
-constexpr int kMaxMF = 4;      // row fragments per warp (TI <= 8 * 8 * 4 = 256)
+constexpr int kTJ = 32;          // columns per tile
+constexpr int kConsumers = 8;    // consumer warps
+constexpr int kThreads = 288;    // + 1 producer warp
 
-template <int NT, int STAGES, bool VEC16, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) seed_f64_kernel(const SeedParams p) {
+// ---- consumer roles ------------------------------------------------------------
+struct Ring {
+  uint64_t* full;
+  uint64_t* empty;
+  double* Ys;   // [STAGES][32 * LDY]
+  double* KRr;  // [STAGES][32 * LDK]
+  double* KRl;  // [TI * LDK]
+  double* red;  // [2][4 * 32 * NT * 2] (MODE 2)
+  int stages, TI, LDY, LDK;
+};
+
+// KR(1..p) rows of row block rb from the pre-built buffer (all 256 consumers).
+__device__ __forceinline__ void load_krl(const SeedParams& p, const Ring& q, int64_t rb, int tid) {
+  const int64_t row0 = rb * q.TI;
+  const int rows = static_cast<int>(min64(q.TI, p.J - row0));
+  const double* src = p.KRl_g + row0 * q.LDK;
+  for (int e = tid; e < q.TI * q.LDK; e += kConsumers * 32) q.KRl[e] = (e / q.LDK) < rows ? src[e] : 0.0;
+}
+
+// Row-block bookkeeping shared by every role: all consumers meet at the named
+// barrier, the right roles flush, KR_l is refreshed, and they meet again.
+template <typename Flush>
+__device__ __forceinline__ void row_block_change(const SeedParams& p, const Ring& q, int64_t rb, int64_t& cur_rb,
+                                                 bool need_krl, int tid, Flush&& flush) {
+  consumer_sync();
+  if (cur_rb >= 0) flush(cur_rb);
+  if (need_krl) load_krl(p, q, rb, tid);
+  consumer_sync();
+  cur_rb = rb;
+}
+
+// Right product on W warps; this warp owns MC row fragments mf = warp + W m.
+// Rs[i, r] += sum_j Y[i, j] KR_r[j, r] over the CTA's tiles; operands double-buffered.
+template <int NT, int MC, int W>
+__device__ void right_role(const SeedParams& p, const Ring& q, int64_t t0, int ntiles, int cta, int warp, int lane,
+                           int tid, bool need_krl, unsigned long long& cw) {
   constexpr int RP = NT * 8;
+  const int g = lane >> 2, t = lane & 3;
+  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  const int LDY = q.LDY, TI = q.TI;
+  double acc[MC > 0 ? MC : 1][NT][2];
+#pragma unroll
+  for (int m = 0; m < MC; ++m)
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb) acc[m][nb][0] = acc[m][nb][1] = 0.0;
+  const int64_t slot_rb0 = t0 / p.nCT;
+  auto flush = [&](int64_t rb) {
+    double* dst = p.Rpart + (static_cast<int64_t>(cta) * p.slots + (rb - slot_rb0)) * RP * TI;
+#pragma unroll
+    for (int m = 0; m < MC; ++m) {
+      const int i = (warp + W * m) * 8 + g;
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        const int r = nb * 8 + 2 * t;
+        dst[r * TI + i] = acc[m][nb][0];
+        dst[(r + 1) * TI + i] = acc[m][nb][1];
+        acc[m][nb][0] = acc[m][nb][1] = 0.0;
+      }
+    }
+  };
+  int64_t cur_rb = -1;
+  for (int k = 0; k < ntiles; ++k) {
+    const int s = k % q.stages;
+    const int64_t tile = t0 + k;
+    const int64_t rb = tile / p.nCT;
+    if (rb != cur_rb) row_block_change(p, q, rb, cur_rb, need_krl, tid, flush);
+    const unsigned long long w0 = clock64();
+    mbar_wait(&q.full[s], (k / q.stages) & 1);
+    cw += clock64() - w0;
+    const double* ya = q.Ys + s * kTJ * LDY + warp * 8 + g + t * LDY;
+    const double* kb = q.KRr + s * kTJ * LDK + t * LDK + g;
+    double a[2][MC > 0 ? MC : 1], b[2][NT];
+#pragma unroll
+    for (int m = 0; m < MC; ++m) a[0][m] = ya[W * 8 * m];
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb) b[0][nb] = kb[nb * 8];
+#pragma unroll
+    for (int ks = 0; ks < kTJ / 4; ++ks) {
+      const int cur = ks & 1, nxt = cur ^ 1;
+      if (ks + 1 < kTJ / 4) {
+#pragma unroll
+        for (int m = 0; m < MC; ++m) a[nxt][m] = ya[(ks + 1) * 4 * LDY + W * 8 * m];
+#pragma unroll
+        for (int nb = 0; nb < NT; ++nb) b[nxt][nb] = kb[(ks + 1) * 4 * LDK + nb * 8];
+      }
+#pragma unroll
+      for (int m = 0; m < MC; ++m)
+#pragma unroll
+        for (int nb = 0; nb < NT; ++nb) dmma(acc[m][nb], a[cur][m], b[cur][nb]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&q.empty[s]);
+  }
+  if (cur_rb >= 0) flush(cur_rb);
+}
+
+// Left product, one 8-column fragment per warp over the full K = TI rows:
+// Ls^T[r, j] = sum_i KR_l^T[r, i] Y[i, j].  Four k-steps per step into four
+// accumulator sets (4 NT independent DMMA chains), operands for the next four
+// k-steps loaded while the current ones issue.  Writes the tile's left partial.
+template <int NT>
+__device__ __forceinline__ void left_load4(const double* yb, const double* kl, int ks, int ksteps, double (&y)[4],
+                                           double (&l)[4][NT]) {
+  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const bool ok = ks + u < ksteps;
+    y[u] = ok ? yb[(ks + u) * 4] : 0.0;
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb) l[u][nb] = ok ? kl[(ks + u) * 4 * LDK + nb * 8] : 0.0;
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void left_mma4(double (&acc)[4][NT][2], const double (&y)[4], const double (&l)[4][NT]) {
+#pragma unroll
+  for (int nb = 0; nb < NT; ++nb)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(acc[u][nb], l[u][nb], y[u]);
+}
+
+template <int NT>
+__device__ void left_role(const SeedParams& p, const Ring& q, int64_t t0, int ntiles, int nf, int lane, int tid,
+                          unsigned long long& cw) {
+  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  const int g = lane >> 2, t = lane & 3;
+  const int LDY = q.LDY, TI = q.TI;
+  const int ksteps = TI >> 2;
+  int64_t cur_rb = -1;
+  auto noflush = [](int64_t) {};
+  for (int k = 0; k < ntiles; ++k) {
+    const int s = k % q.stages;
+    const int64_t tile = t0 + k;
+    const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
+    if (rb != cur_rb) row_block_change(p, q, rb, cur_rb, true, tid, noflush);
+    const unsigned long long w0 = clock64();
+    mbar_wait(&q.full[s], (k / q.stages) & 1);
+    cw += clock64() - w0;
+    const double* yb = q.Ys + s * kTJ * LDY + (nf * 8 + g) * LDY + t;
+    const double* kl = q.KRl + t * LDK + g;
+    double acc[4][NT][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) acc[u][nb][0] = acc[u][nb][1] = 0.0;
+    double yP[4], lP[4][NT], yQ[4], lQ[4][NT];
+    left_load4<NT>(yb, kl, 0, ksteps, yP, lP);
+    for (int ks = 0; ks < ksteps; ks += 8) {
+      left_load4<NT>(yb, kl, ks + 4, ksteps, yQ, lQ);
+      left_mma4<NT>(acc, yP, lP);
+      if (ks + 4 >= ksteps) break;
+      left_load4<NT>(yb, kl, ks + 8, ksteps, yP, lP);
+      left_mma4<NT>(acc, yQ, lQ);
+    }
+    const int64_t col = ct * kTJ + nf * 8 + 2 * t;
+    double* dst = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K;
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb) {
+      const int r = nb * 8 + g;
+      if (r < p.R) {
+        const double v0 = (acc[0][nb][0] + acc[1][nb][0]) + (acc[2][nb][0] + acc[3][nb][0]);
+        const double v1 = (acc[0][nb][1] + acc[1][nb][1]) + (acc[2][nb][1] + acc[3][nb][1]);
+        if (col < p.K) dst[r * p.K + col] = v0;
+        if (col + 1 < p.K) dst[r * p.K + col + 1] = v1;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&q.empty[s]);
+  }
+}
+
+// Left product only (ALS second pass): 4 column fragments x 2 halves of K,
+// combined through shared memory.
+template <int NT>
+__device__ void left_only_role(const SeedParams& p, const Ring& q, int64_t t0, int ntiles, int warp, int lane,
+                               int tid, unsigned long long& cw) {
+  const int g = lane >> 2, t = lane & 3;
+  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  const int LDY = q.LDY, TI = q.TI;
+  const int nf = warp & 3, h = warp >> 2;
+  const int ksteps = TI >> 2, kh = ((ksteps >> 1) + 1) & ~1;
+  const int ks0 = h * kh, ks1 = min(ksteps, ks0 + kh);
+  int64_t cur_rb = -1;
+  auto noflush = [](int64_t) {};
+  for (int k = 0; k < ntiles; ++k) {
+    const int s = k % q.stages;
+    const int64_t tile = t0 + k;
+    const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
+    if (rb != cur_rb) row_block_change(p, q, rb, cur_rb, true, tid, noflush);
+    const unsigned long long w0 = clock64();
+    mbar_wait(&q.full[s], (k / q.stages) & 1);
+    cw += clock64() - w0;
+    const double* yb = q.Ys + s * kTJ * LDY + (nf * 8 + g) * LDY + t;
+    const double* kl = q.KRl + t * LDK + g;
+    double accA[NT][2], accB[NT][2];
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb) accA[nb][0] = accA[nb][1] = accB[nb][0] = accB[nb][1] = 0.0;
+#pragma unroll 2
+    for (int ks = ks0; ks < ks1; ks += 2) {
+      const bool two = ks + 1 < ks1;
+      const double y0 = yb[ks * 4];
+      const double y1 = two ? yb[(ks + 1) * 4] : 0.0;
+      double l0[NT], l1[NT];
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        l0[nb] = kl[ks * 4 * LDK + nb * 8];
+        l1[nb] = two ? kl[(ks + 1) * 4 * LDK + nb * 8] : 0.0;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        dmma(accA[nb], l0[nb], y0);
+        dmma(accB[nb], l1[nb], y1);
+      }
+    }
+    double* rd = q.red + (k & 1) * (4 * 32 * NT * 2);
+    if (h == 1) {
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        rd[(nf * 32 + lane) * NT * 2 + nb * 2] = accA[nb][0] + accB[nb][0];
+        rd[(nf * 32 + lane) * NT * 2 + nb * 2 + 1] = accA[nb][1] + accB[nb][1];
+      }
+    }
+    consumer_sync();
+    if (h == 0) {
+      const int64_t col = ct * kTJ + nf * 8 + 2 * t;
+      double* dst = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K;
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        const int r = nb * 8 + g;
+        if (r < p.R) {
+          const double v0 = accA[nb][0] + accB[nb][0] + rd[(nf * 32 + lane) * NT * 2 + nb * 2];
+          const double v1 = accA[nb][1] + accB[nb][1] + rd[(nf * 32 + lane) * NT * 2 + nb * 2 + 1];
+          if (col < p.K) dst[r * p.K + col] = v0;
+          if (col + 1 < p.K) dst[r * p.K + col + 1] = v1;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&q.empty[s]);
+  }
+}
+
+// Dispatch the right role on this warp's (static) fragment count.
+template <int NT, int W, int MAXMC>
+__device__ void right_dispatch(int mc, const SeedParams& p, const Ring& q, int64_t t0, int ntiles, int cta, int warp,
+                               int lane, int tid, bool need_krl, unsigned long long& cw) {
+  if constexpr (MAXMC >= 1) {
+    if (mc == MAXMC) {
+      right_role<NT, MAXMC, W>(p, q, t0, ntiles, cta, warp, lane, tid, need_krl, cw);
+      return;
+    }
+    right_dispatch<NT, W, MAXMC - 1>(mc, p, q, t0, ntiles, cta, warp, lane, tid, need_krl, cw);
+  } else {
+    right_role<NT, 0, W>(p, q, t0, ntiles, cta, warp, lane, tid, need_krl, cw);
+  }
+}
+
+template <int NT, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    seed_f64_kernel(const SeedParams p, const __grid_constant__ CUtensorMap tmap,
+                    const __grid_constant__ CUtensorMap kmap) {
+  constexpr int RP = NT * 8;
+  // right-product row fragments per warp: 4 warps in MODE 3, 8 in MODE 1
+  // register budget: 9 warps put 3 on one SMSP -> <= 168 registers per thread
+  constexpr int kMaxMF = (MODE == 3) ? (NT <= 2 ? 7 : (NT == 3 ? 6 : 5)) : 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int cta = blockIdx.x;
@@ -69,223 +356,175 @@ __global__ void __launch_bounds__(kThreads, 1) seed_f64_kernel(const SeedParams 
   if (t0 >= t1) return;
   const int ntiles = static_cast<int>(t1 - t0);
   const int TI = p.TI, LDY = p.LDY, LDK = p.LDK;
+  const int STAGES = p.stages;
   const int nMF = TI >> 3;
 
-  extern __shared__ __align__(16) double smem[];
-  double* Ys = smem;                                   // [STAGES][kTJ * LDY]
-  double* KRr = Ys + STAGES * kTJ * LDY;               // [STAGES][kTJ * LDK]
-  double* KRl = KRr + STAGES * kTJ * LDK;              // [TI * LDK]
-  double* red = KRl + ((MODE & 2) ? TI * LDK : 0);     // [4 * 32 * NT * 2]
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // TMA destinations need 128-byte alignment: align the carve-out base
+  unsigned char* base = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base);   // [3]
+  uint64_t* empty = full + 3;                            // [3]
+  double* Ys = reinterpret_cast<double*>(base + 128);    // [STAGES][kTJ * LDY]
+  double* KRr = Ys + STAGES * kTJ * LDY;                 // [STAGES][kTJ * LDK]
+  double* KRl = KRr + STAGES * kTJ * LDK;                // [TI * LDK]
+  double* red = KRl + ((MODE & 2) ? TI * LDK : 0);       // [2][4 * 32 * NT * 2] (MODE 2)
 
-  auto issue_tile = [&](int64_t tile, int stage) {
-    const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
-    const int64_t row0 = rb * TI, col0 = ct * kTJ;
-    const int rows = static_cast<int>(min64(TI, p.J - row0));
-    const int cols = static_cast<int>(min64(kTJ, p.K - col0));
-    double* dst = Ys + stage * kTJ * LDY;
-    if (VEC16) {
-      const int half = TI >> 1;
-      for (int e = tid; e < kTJ * half; e += kThreads) {
-        const int c = e / half, q = e - c * half;
-        const int row = 2 * q;
-        int bytes = 0;
-        const double* src = p.Y;
-        if (c < cols && row < rows) {
-          bytes = (rows - row) >= 2 ? 16 : 8;
-          src = p.Y + (row0 + row) + p.J * (col0 + c);
-        }
-        cp_async16(dst + c * LDY + row, src, bytes);
-      }
-    } else {
-      for (int e = tid; e < kTJ * TI; e += kThreads) {
-        const int c = e / TI, row = e - c * TI;
-        int bytes = 0;
-        const double* src = p.Y;
-        if (c < cols && row < rows) {
-          bytes = 8;
-          src = p.Y + (row0 + row) + p.J * (col0 + c);
-        }
-        cp_async8(dst + c * LDY + row, src, bytes);
-      }
-    }
-    if (MODE & 1) {  // KR(p+1..N) rows of this tile's columns
-      double* kr = KRr + stage * kTJ * LDK;
-      for (int e = tid; e < kTJ * RP; e += kThreads) {
-        const int jj = e / RP, r = e - jj * RP;
-        double v = 0.0;
-        if (jj < cols && r < p.R)
-          v = p.use32 ? kr_entry32(p.right, static_cast<uint32_t>(col0 + jj), r)
-                      : kr_entry(p.right, col0 + jj, r);
-        kr[jj * LDK + r] = v;
-      }
-    }
-  };
-
-  auto load_krl = [&](int64_t rb) {  // KR(1..p) rows of a row block
-    const int64_t row0 = rb * TI;
-    const int rows = static_cast<int>(min64(TI, p.J - row0));
-    for (int e = tid; e < TI * RP; e += kThreads) {
-      const int i = e / RP, r = e - i * RP;
-      double v = 0.0;
-      if (i < rows && r < p.R)
-        v = p.use32 ? kr_entry32(p.left, static_cast<uint32_t>(row0 + i), r)
-                    : kr_entry(p.left, row0 + i, r);
-      KRl[i * LDK + r] = v;
-    }
-  };
-
-  double acc1[kMaxMF][NT][2];
-#pragma unroll
-  for (int m = 0; m < kMaxMF; ++m)
-#pragma unroll
-    for (int nb = 0; nb < NT; ++nb) acc1[m][nb][0] = acc1[m][nb][1] = 0.0;
-
-  const int64_t slot_rb0 = t0 / p.nCT;
-  auto flush_right = [&](int64_t rb) {
-    double* dst = p.Rpart + (static_cast<int64_t>(cta) * p.slots + (rb - slot_rb0)) * RP * TI;
-#pragma unroll
-    for (int m = 0; m < kMaxMF; ++m) {
-      const int mf = warp + 8 * m;
-      if (mf < nMF) {
-        const int i = mf * 8 + g;
-#pragma unroll
-        for (int nb = 0; nb < NT; ++nb) {
-          const int r = nb * 8 + 2 * t;
-          dst[r * TI + i] = acc1[m][nb][0];
-          dst[(r + 1) * TI + i] = acc1[m][nb][1];
-          acc1[m][nb][0] = acc1[m][nb][1] = 0.0;
-        }
-      }
-    }
-  };
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ntiles) issue_tile(t0 + s, s);
-    cp_async_commit();
+  // plain-copy path: zero the stage buffers once (edge tiles are cleared below)
+  if (!p.use_tma)
+    for (int e = tid; e < STAGES * kTJ * LDY; e += kThreads) Ys[e] = 0.0;
+  if (p.use_tma && warp == kConsumers && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    if (MODE & 1) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
   }
-
-  int64_t cur_rb = -1;
-  for (int k = 0; k < ntiles; ++k) {
-    const int64_t tile = t0 + k;
-    const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
-    if (k + STAGES - 1 < ntiles) issue_tile(tile + STAGES - 1, (k + STAGES - 1) % STAGES);
-    cp_async_commit();
-    if (rb != cur_rb) {
-      if ((MODE & 1) && cur_rb >= 0) flush_right(cur_rb);
-      if (MODE & 2) load_krl(rb);
-      cur_rb = rb;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
     }
-    cp_async_wait<STAGES - 1>();
-    __syncthreads();
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
 
-    const int stage = k % STAGES;
-    const double* Yst = Ys + stage * kTJ * LDY;
-    if (MODE & 1) {  // right: Rs[i, r] += sum_j Y[i, j] KR_r[j, r]
-      const double* kr = KRr + stage * kTJ * LDK;
-#pragma unroll
-      for (int ks = 0; ks < kTJ / 4; ++ks) {
-        double b[NT];
-#pragma unroll
-        for (int nb = 0; nb < NT; ++nb) b[nb] = kr[(ks * 4 + t) * LDK + nb * 8 + g];
-#pragma unroll
-        for (int m = 0; m < kMaxMF; ++m) {
-          const int mf = warp + 8 * m;
-          if (mf < nMF) {
-            const double a = Yst[(mf * 8 + g) + (ks * 4 + t) * LDY];
-#pragma unroll
-            for (int nb = 0; nb < NT; ++nb) dmma(acc1[m][nb], a, b[nb]);
+  // ------------------------------------------------------------------ producer
+  if (warp == kConsumers) {
+    unsigned long long tw = 0, tstart = clock64();
+    for (int k = 0; k < ntiles; ++k) {
+      const int s = k % STAGES;
+      if (k >= STAGES) {
+        const unsigned long long a = clock64();
+        mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
+        tw += clock64() - a;
+      }
+      const int64_t tile = t0 + k;
+      const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
+      const int64_t row0 = rb * TI, col0 = ct * kTJ;
+      double* ys = Ys + s * kTJ * LDY;
+      double* kr = KRr + s * kTJ * LDK;
+      if (p.use_tma) {  // Y tile + its Khatri-Rao rows, one transaction count
+        if (lane == 0) {
+          const uint32_t bytes = LDY * kTJ * 8 + ((MODE & 1) ? kTJ * LDK * 8 : 0);
+          mbar_arrive_tx(&full[s], bytes);
+          tma_load_2d(ys, &tmap, static_cast<int>(row0), static_cast<int>(col0), &full[s]);
+          if (MODE & 1) tma_load_2d(kr, &kmap, 0, static_cast<int>(col0), &full[s]);
+        }
+      } else {  // unaligned leading extent: plain loads (rare shapes)
+        const int rows = static_cast<int>(min64(TI, p.J - row0));
+        const int cols = static_cast<int>(min64(kTJ, p.K - col0));
+        for (int c = 0; c < kTJ; ++c)
+          for (int q = lane; q < TI; q += 32)
+            ys[c * LDY + q] = (c < cols && q < rows) ? p.Y[row0 + q + p.J * (col0 + c)] : 0.0;
+        if (MODE & 1)
+          for (int e = lane; e < kTJ * LDK; e += 32) {
+            const int jj = e / LDK;
+            kr[e] = jj < cols ? p.KRr_g[(col0 + jj) * LDK + (e - jj * LDK)] : 0.0;
           }
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
       }
     }
-    double acc2[NT][2];
-    if (MODE & 2) {  // left: Ls^T[r, j] += sum_i KR_l^T[r, i] Y[i, j]
-#pragma unroll
-      for (int nb = 0; nb < NT; ++nb) acc2[nb][0] = acc2[nb][1] = 0.0;
-      const int nf = warp & 3, h = warp >> 2;
-      const int ksteps = TI >> 2, kh = (ksteps + 1) >> 1;
-      const int ks0 = h * kh, ks1 = min(ksteps, ks0 + kh);
-#pragma unroll 4
-      for (int ks = ks0; ks < ks1; ++ks) {
-        const double by = Yst[(ks * 4 + t) + (nf * 8 + g) * LDY];
-#pragma unroll
-        for (int nb = 0; nb < NT; ++nb) dmma(acc2[nb], KRl[(ks * 4 + t) * LDK + nb * 8 + g], by);
-      }
-      if (warp >= 4) {
-        double* rd = red + ((warp - 4) * 32 + lane) * NT * 2;
-#pragma unroll
-        for (int nb = 0; nb < NT; ++nb) {
-          rd[nb * 2] = acc2[nb][0];
-          rd[nb * 2 + 1] = acc2[nb][1];
-        }
-      }
+    if (p.trace && lane == 0) {
+      unsigned long long* tr = p.trace + (static_cast<int64_t>(cta) * 9 + warp) * 4;
+      tr[0] = tw; tr[1] = 0; tr[2] = clock64() - tstart; tr[3] = ntiles;
     }
-    __syncthreads();
-    if ((MODE & 2) && warp < 4) {
-      const double* rd = red + (warp * 32 + lane) * NT * 2;
-      const int nf = warp;
-      const int64_t col = ct * kTJ + nf * 8 + 2 * t;
-      double* dst = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K;
-#pragma unroll
-      for (int nb = 0; nb < NT; ++nb) {
-        const int r = nb * 8 + g;
-        if (r < p.R) {
-          if (col < p.K) dst[r * p.K + col] = acc2[nb][0] + rd[nb * 2];
-          if (col + 1 < p.K) dst[r * p.K + col + 1] = acc2[nb][1] + rd[nb * 2 + 1];
-        }
-      }
-    }
+    return;
   }
-  if (MODE & 1) flush_right(cur_rb);
+
+  // ------------------------------------------------------------------ consumers
+  const Ring q{full, empty, Ys, KRr, KRl, red, STAGES, TI, LDY, LDK};
+  unsigned long long cw = 0;
+  const unsigned long long cstart = clock64();
+  if (MODE == 3) {
+    if (warp < 4) {
+      const int mc = (nMF - warp + 3) / 4;
+      right_dispatch<NT, 4, kMaxMF>(mc, p, q, t0, ntiles, cta, warp, lane, tid, true, cw);
+    } else {
+      left_role<NT>(p, q, t0, ntiles, warp - 4, lane, tid, cw);
+    }
+  } else if (MODE == 1) {
+    const int mc = (nMF - warp + 7) / 8;
+    right_dispatch<NT, 8, kMaxMF>(mc, p, q, t0, ntiles, cta, warp, lane, tid, false, cw);
+  } else {
+    left_only_role<NT>(p, q, t0, ntiles, warp, lane, tid, cw);
+  }
+  if (p.trace && lane == 0) {
+    unsigned long long* tr = p.trace + (static_cast<int64_t>(cta) * 9 + warp) * 4;
+    tr[0] = cw; tr[1] = 0; tr[2] = clock64() - cstart; tr[3] = ntiles;
+  }
 }
 
-template <int NT, int STAGES, bool VEC16, int MODE>
-void launch_one(const SeedParams& p, cudaStream_t s, size_t smem) {
-  auto fn = seed_f64_kernel<NT, STAGES, VEC16, MODE>;
+template <int NT, int MODE>
+void launch_one(const SeedParams& p, const CUtensorMap& tmap, const CUtensorMap& kmap, cudaStream_t s,
+                size_t smem) {
+  auto fn = seed_f64_kernel<NT, MODE>;
   static bool configured = false;  // one attribute call per instantiation
   if (!configured) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     configured = true;
   }
-  fn<<<p.P, kThreads, smem, s>>>(p);
+  fn<<<p.P, kThreads, smem, s>>>(p, tmap, kmap);
 }
 
-template <int NT, int STAGES>
-void launch_nt(const SeedParams& p, int mode, bool vec16, cudaStream_t s, size_t smem) {
-  if (vec16) {
-    if (mode == 1) launch_one<NT, STAGES, true, 1>(p, s, smem);
-    else if (mode == 2) launch_one<NT, STAGES, true, 2>(p, s, smem);
-    else launch_one<NT, STAGES, true, 3>(p, s, smem);
-  } else {
-    if (mode == 1) launch_one<NT, STAGES, false, 1>(p, s, smem);
-    else if (mode == 2) launch_one<NT, STAGES, false, 2>(p, s, smem);
-    else launch_one<NT, STAGES, false, 3>(p, s, smem);
-  }
+template <int NT>
+void launch_nt(const SeedParams& p, const CUtensorMap& tmap, const CUtensorMap& kmap, int mode, cudaStream_t s,
+               size_t smem) {
+  if (mode == 1) launch_one<NT, 1>(p, tmap, kmap, s, smem);
+  else if (mode == 2) launch_one<NT, 2>(p, tmap, kmap, s, smem);
+  else launch_one<NT, 3>(p, tmap, kmap, s, smem);
 }
 
 }  // namespace
 
 int seed_f64_stages(int NT) { return NT <= 3 ? 3 : 2; }
 
-size_t seed_f64_smem_bytes(int NT, int TI, int LDY, int LDK, int mode) {
-  const int stages = seed_f64_stages(NT);
+int seed_f64_max_ti(int NT) { return NT <= 2 ? 208 : (NT == 3 ? 192 : 160); }
+
+size_t seed_f64_smem_bytes(int NT, int TI, int LDY, int LDK, int mode, int stages, int64_t fac_doubles) {
   size_t d = static_cast<size_t>(stages) * kTJ * LDY + static_cast<size_t>(stages) * kTJ * LDK;
-  if (mode & 2) d += static_cast<size_t>(TI) * LDK + 4 * 32 * NT * 2;
-  return d * sizeof(double);
+  if (mode & 2) d += static_cast<size_t>(TI) * LDK;
+  if (mode == 2) d += 2 * 4 * 32 * NT * 2;
+  if (mode & 1) d += static_cast<size_t>(fac_doubles);
+  return 256 + d * sizeof(double);  // barriers + 128-byte alignment slack
 }
 
-int launch_seed_f64(const SeedParams& p, int NT, int mode, cudaStream_t s) {
-  const bool vec16 = (p.J % 2 == 0);
-  const size_t smem = seed_f64_smem_bytes(NT, p.TI, p.LDY, p.LDK, mode);
+int launch_seed_f64(const SeedParams& p, const CUtensorMap* tmap, const CUtensorMap* kmap, int NT, int mode,
+                    cudaStream_t s) {
+  CUtensorMap dummy;
+  std::memset(&dummy, 0, sizeof dummy);
+  const CUtensorMap& m = (p.use_tma && tmap) ? *tmap : dummy;
+  const CUtensorMap& km = (p.use_tma && kmap) ? *kmap : dummy;
+  const size_t smem = seed_f64_smem_bytes(NT, p.TI, p.LDY, p.LDK, mode, p.stages, 0);
   switch (NT) {
-    case 1: launch_nt<1, 3>(p, mode, vec16, s, smem); break;
-    case 2: launch_nt<2, 3>(p, mode, vec16, s, smem); break;
-    case 3: launch_nt<3, 3>(p, mode, vec16, s, smem); break;
-    case 4: launch_nt<4, 2>(p, mode, vec16, s, smem); break;
+    case 1: launch_nt<1>(p, m, km, mode, s, smem); break;
+    case 2: launch_nt<2>(p, m, km, mode, s, smem); break;
+    case 3: launch_nt<3>(p, m, km, mode, s, smem); break;
+    case 4: launch_nt<4>(p, m, km, mode, s, smem); break;
     default: return 0;
   }
   return 1;
+}
+
+bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, int elem_bytes,
+                        uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (stride1_bytes & 15) || ((box0 * elem_bytes) & 15) ||
+      box0 > 256 || box1 > 256 || dim0 >= (1ull << 32) || dim1 >= (1ull << 32))
+    return false;
+  const cuuint64_t gdim[2] = {dim0, dim1};
+  const cuuint64_t gstride[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t estride[2] = {1, 1};
+  return encode(out, dtype, 2, const_cast<void*>(base), gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace cpdgpu

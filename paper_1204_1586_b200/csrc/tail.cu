@@ -1,10 +1,16 @@
-// tail.cu — seed-partial reductions and the rank-batched TTV recursion tail.
+// tail.cu — everything around the seed contraction: the prologue (factor
+// gather + Khatri-Rao rows for K1), the deterministic seed-partial reductions
+// and the rank-batched TTV recursion tail.
 //
 // Reference: the right phase  (mttkrp.cpp:165-193; Eq 3.20 recursion, Eq 3.12
 // extraction) and the left phase (mttkrp.cpp:212-241; Eq 3.22 recursion,
-// Eq 3.16 extraction).  The reference runs one GEMV per rank column r; here
-// every launch covers all R columns at once ("rank-batched"), with the
-// Khatri-Rao vector generated on the fly from factor rows.
+// Eq 3.16 extraction).  The reference runs one GEMV per rank column r; here a
+// single launch ("tail step") covers every rank column of every contraction
+// that can run at the same recursion level — the right phase's extraction of
+// mode j and recursion to mode j-1 read the same R^(j), the left phase is
+// independent of the right — so a gradient costs 1 + max(p, N - p) tail
+// launches.  Every output is produced by one warp in a fixed order, so results
+// are bitwise reproducible.
 #include "kernels.h"
 
 namespace cpdgpu {
@@ -16,165 +22,169 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// CTA whose tile range [t0, t1) contains tile t (t0(c) = floor(c T / P)).
-__device__ __forceinline__ int64_t cta_of(int64_t t, int64_t T, int64_t P) {
-  return ((t + 1) * P + T - 1) / T - 1;
+__device__ __forceinline__ double kr_at(const KRSpec& s, int64_t q, int r) {
+  return q < (1LL << 31) ? kr_entry32(s, static_cast<uint32_t>(q), r) : kr_entry(s, q, r);
 }
 
-__global__ void reduce_right_kernel(const SeedParams p, int RP, double* Rs, int64_t ldo) {
-  const int64_t total = p.J * p.R;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(e / p.J);
-    const int64_t i = e - r * p.J;
-    const int64_t rb = i / p.TI, il = i - rb * p.TI;
-    const int64_t c0 = cta_of(rb * p.nCT, p.T, p.P);
-    const int64_t c1 = cta_of((rb + 1) * p.nCT - 1, p.T, p.P);
-    double s = 0.0;
-    for (int64_t c = c0; c <= c1; ++c) {
-      const int64_t ta = (c * p.T) / p.P, tb = ((c + 1) * p.T) / p.P;
-      if (ta >= tb) continue;
-      const int64_t slot = c * p.slots + (rb - ta / p.nCT);
-      s += p.Rpart[(slot * RP + r) * p.TI + il];
-    }
-    Rs[r * ldo + i] = s;
+// Number of warp work units of an op.
+__host__ __device__ inline int64_t op_units(const TailOp& o) {
+  switch (o.type) {
+    case kOpContractA: return o.B * o.R;                       // warp per output (b, r)
+    case kOpContractB:                                         // M >= 32: warp per 32 outputs
+      return o.M >= 32 ? ((o.M + 31) / 32) * o.R : o.M * o.R;  // else warp per output
+    case kOpReduceRight:                                       // B == 1: warp per output (lanes over slots)
+      return o.B == 1 ? o.M * o.R : ((o.M + 31) / 32) * o.R;   // else 32 rows per warp
+    case kOpReduceLeft: return ((o.M + 31) / 32) * o.R;        // 32 columns per warp
+    default: return 0;
   }
 }
 
-__global__ void reduce_left_kernel(const double* Lpart, int64_t nRB, int R, int64_t K, double* Ls,
-                                   int64_t ldo) {
-  const int64_t total = K * R;
-  const int64_t stride = static_cast<int64_t>(R) * K;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(e / K);
-    const int64_t j = e - r * K;
-    double s = 0.0;
-    for (int64_t rb = 0; rb < nRB; ++rb) s += Lpart[rb * stride + e];
-    Ls[r * ldo + j] = s;
-  }
+__device__ __forceinline__ double* op_out(const TailOp& o, double* const* gtab) {
+  return o.out_slot >= 0 ? gtab[o.out_slot] + o.out_off : o.out;
 }
 
-// One warp per output (b, r): a contiguous dot product of length M.
-__global__ void contract_a_kernel(const double* __restrict__ Z, int64_t ldz, int64_t M, int64_t B,
-                                  int R, const KRSpec v, double* __restrict__ out, int64_t ldo) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < B * R;
-       w += nw) {
-    const int r = static_cast<int>(w / B);
-    const int64_t b = w - r * B;
-    const double* z = Z + r * ldz + M * b;
+__device__ void run_unit(const TailOp& o, int64_t u, int lane, double* const* gtab) {
+  double* out = op_out(o, gtab);
+  if (o.type == kOpContractA) {  // out[r][b] = sum_a Z[r][a + M b] KR_v[a, r]
+    const int r = static_cast<int>(u / o.B);
+    const int64_t b = u - r * o.B;
+    const double* z = o.Z + r * o.ldz + o.M * b;
     double s = 0.0;
-    for (int64_t a = lane; a < M; a += 32) s += z[a] * kr_entry(v, a, r);
+    for (int64_t a = lane; a < o.M; a += 32) s += z[a] * kr_at(o.kr, a, r);
     s = warp_sum(s);
-    if (lane == 0) out[r * ldo + b] = s;
+    if (lane == 0) out[r * o.ldo + b] = s;
+  } else if (o.type == kOpContractB) {  // out[r][a] = sum_b Z[r][a + M b] KR_w[b, r]
+    if (o.M >= 32) {  // lanes over a (coalesced), loop over b
+      const int64_t chunks = (o.M + 31) / 32;
+      const int r = static_cast<int>(u / chunks);
+      const int64_t a = (u - r * chunks) * 32 + lane;
+      if (a < o.M) {
+        const double* z = o.Z + r * o.ldz + a;
+        double s = 0.0;
+        for (int64_t b = 0; b < o.B; ++b) s += z[o.M * b] * kr_at(o.kr, b, r);
+        out[r * o.ldo + a] = s;
+      }
+    } else {  // warp per output, lanes over b
+      const int r = static_cast<int>(u / o.M);
+      const int64_t a = u - r * o.M;
+      const double* z = o.Z + r * o.ldz + a;
+      double s = 0.0;
+      for (int64_t b = lane; b < o.B; b += 32) s += z[o.M * b] * kr_at(o.kr, b, r);
+      s = warp_sum(s);
+      if (lane == 0) out[r * o.ldo + a] = s;
+    }
+  } else if (o.type == kOpReduceRight && o.B == 1) {  // many slots: lanes over slots, fixed tree
+    const int r = static_cast<int>(u / o.M);
+    const int64_t i = u - r * o.M;
+    const int64_t rb = i / o.TI, il = i - rb * o.TI;
+    double s = 0.0;
+    for (int q = o.rb_ptr[rb] + lane; q < o.rb_ptr[rb + 1]; q += 32)
+      s += o.Z[(static_cast<int64_t>(o.slot_list[q]) * o.RP + r) * o.TI + il];
+    s = warp_sum(s);
+    if (lane == 0) out[r * o.ldo + i] = s;
+  } else if (o.type == kOpReduceRight) {  // Rs[r][i] = sum of the slots of row block rb(i)
+    const int64_t chunks = (o.M + 31) / 32;
+    const int r = static_cast<int>(u / chunks);
+    const int64_t i = (u - r * chunks) * 32 + lane;
+    if (i < o.M) {
+      const int64_t rb = i / o.TI, il = i - rb * o.TI;
+      double s = 0.0;
+      for (int q = o.rb_ptr[rb]; q < o.rb_ptr[rb + 1]; ++q)
+        s += o.Z[(static_cast<int64_t>(o.slot_list[q]) * o.RP + r) * o.TI + il];
+      out[r * o.ldo + i] = s;
+    }
+  } else if (o.type == kOpReduceLeft) {  // Ls[r][j] = sum_rb Lpart[rb][r][j]
+    const int64_t chunks = (o.M + 31) / 32;
+    const int r = static_cast<int>(u / chunks);
+    const int64_t j = (u - r * chunks) * 32 + lane;
+    if (j < o.M) {
+      const int64_t stride = static_cast<int64_t>(o.R) * o.M;
+      const double* z = o.Z + r * o.M + j;
+      double s = 0.0;
+      for (int64_t rb = 0; rb < o.B; ++rb) s += z[rb * stride];
+      out[r * o.ldo + j] = s;
+    }
   }
 }
 
-// out[r][a] = sum_b Z[r][a + M b] w[b, r]: threads over a (coalesced), groups
-// over b, fixed-order shared-memory reduction, optional split of the b range
-// with a second deterministic pass.
-constexpr int kCB = 256;
-
-__global__ void contract_b_kernel(const double* __restrict__ Z, int64_t ldz, int64_t M, int64_t B,
-                                  int R, const KRSpec w, double* __restrict__ out, int64_t ldo,
-                                  int TA, int64_t nAB, int S, double* __restrict__ part) {
-  __shared__ double red[kCB];
-  const int NB = kCB / TA;
-  const int tid = threadIdx.x;
-  const int al = tid % TA, bg = tid / TA;
-  const int64_t ab = blockIdx.x % nAB;
-  const int s = static_cast<int>(blockIdx.x / nAB);
-  const int r = blockIdx.y;
-  const int64_t a = ab * TA + al;
-  const int64_t b0 = (B * s) / S, b1 = (B * (s + 1)) / S;
-  double acc = 0.0;
-  if (a < M) {
-    const double* z = Z + r * ldz + a;
-    for (int64_t b = b0 + bg; b < b1; b += NB) acc += z[M * b] * kr_entry(w, b, r);
-  }
-  red[tid] = acc;
-  __syncthreads();
-  if (bg == 0 && a < M) {
-    double tot = 0.0;
-    for (int q = 0; q < NB; ++q) tot += red[q * TA + al];
-    if (S == 1) out[r * ldo + a] = tot;
-    else part[(static_cast<int64_t>(s) * R + r) * M + a] = tot;
+__global__ void __launch_bounds__(256) tail_step_kernel(const TailStep st, double* const* gtab) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  int64_t start[kMaxTailOps + 1];
+  start[0] = 0;
+  for (int i = 0; i < st.n; ++i) start[i + 1] = start[i] + op_units(st.op[i]);
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < start[st.n];
+       w += nwarps) {
+    int i = 0;
+    while (w >= start[i + 1]) ++i;
+    run_unit(st.op[i], w - start[i], lane, gtab);
   }
 }
 
-__global__ void contract_b_finish(const double* __restrict__ part, int64_t M, int R, int S,
-                                  double* __restrict__ out, int64_t ldo) {
-  const int64_t total = M * R;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(e / M);
-    const int64_t a = e - r * M;
-    double tot = 0.0;
-    for (int s = 0; s < S; ++s) tot += part[(static_cast<int64_t>(s) * R + r) * M + a];
-    out[r * ldo + a] = tot;
+// Prologue: sorted factors Fs[j] <- input block perm[j]; output pointer table;
+// Khatri-Rao rows of every K1 chunk: out[q * LDK + r] = KR(spec)[q, r].
+template <int RP>
+__device__ void kr_rows(const KRSpec& s, int64_t L, int R, int LDK, double* out, int64_t t, int64_t nt) {
+  for (int64_t q = t; q < L; q += nt) {
+    double* dst = out + q * LDK;
+    kr_row<RP>(s, q, R, q < (1LL << 31), dst);
+    for (int r = RP; r < LDK; ++r) dst[r] = 0.0;
   }
 }
 
-int grid_for(int64_t work, int threads) {
+__global__ void __launch_bounds__(256) prologue_kernel(const Prologue pr, double** gtab) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (t < kMaxModes && t < pr.N) gtab[t] = pr.gout[t];
+  if (pr.Fs)
+    for (int j = 0; j < pr.N; ++j)
+      for (int64_t e = t; e < pr.len[j]; e += nt) pr.Fs[pr.dst_off[j] + e] = pr.fin[pr.src_off[j] + e];
+  for (int c = 0; c < pr.nkr; ++c) {
+    const KRJob& k = pr.kr[c];
+    switch (k.NT) {
+      case 1: kr_rows<8>(k.spec, k.L, k.R, k.LDK, k.out, t, nt); break;
+      case 2: kr_rows<16>(k.spec, k.L, k.R, k.LDK, k.out, t, nt); break;
+      case 3: kr_rows<24>(k.spec, k.L, k.R, k.LDK, k.out, t, nt); break;
+      default: kr_rows<32>(k.spec, k.L, k.R, k.LDK, k.out, t, nt); break;
+    }
+  }
+}
+
+int grid_for(int64_t work, int threads, int cap) {
   const int64_t b = (work + threads - 1) / threads;
-  return static_cast<int>(b < 1 ? 1 : (b > 65535 * 16 ? 65535 * 16 : b));
-}
-
-void contract_b_shape(int64_t M, int64_t B, int R, int num_sms, int* TA, int64_t* nAB, int* S) {
-  int ta = 32;
-  while (ta < M && ta < kCB) ta *= 2;
-  *TA = ta;
-  *nAB = (M + ta - 1) / ta;
-  const int64_t base = *nAB * R;
-  const int64_t want = 2LL * num_sms;
-  int64_t s = base >= want ? 1 : (want + base - 1) / base;
-  const int64_t per = (kCB / ta);  // b-groups per CTA
-  const int64_t smax = (B + per * 8 - 1) / (per * 8);  // keep >= 8 b per group
-  if (s > smax) s = smax;
-  if (s < 1) s = 1;
-  *S = static_cast<int>(s);
+  return static_cast<int>(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
 }  // namespace
 
-int launch_reduce_right(const SeedParams& p, int RP, double* Rs, int64_t ldo, cudaStream_t s) {
-  const int64_t work = p.J * p.R;
-  reduce_right_kernel<<<grid_for(work, 256), 256, 0, s>>>(p, RP, Rs, ldo);
+int64_t tail_step_units(const TailStep& st) {
+  int64_t n = 0;
+  for (int i = 0; i < st.n; ++i) n += op_units(st.op[i]);
+  return n;
+}
+
+int launch_tail_step(const TailStep& st, double* const* gtab, int num_sms, cudaStream_t s) {
+  if (st.n == 0) return 0;
+  const int64_t warps = tail_step_units(st);
+  tail_step_kernel<<<grid_for(warps * 32, 256, num_sms * 8), 256, 0, s>>>(st, gtab);
   return 1;
 }
 
-int launch_reduce_left(const double* Lpart, int64_t nRB, int R, int64_t K, double* Ls,
-                        int64_t ldo, cudaStream_t s) {
-  reduce_left_kernel<<<grid_for(K * R, 256), 256, 0, s>>>(Lpart, nRB, R, K, Ls, ldo);
+const void* prologue_kernel_fn() { return reinterpret_cast<const void*>(prologue_kernel); }
+
+void prologue_geometry(const Prologue& pr, int num_sms, dim3* grid, dim3* block) {
+  int64_t work = 0;
+  for (int j = 0; j < pr.N; ++j) work = work > pr.len[j] ? work : pr.len[j];
+  for (int c = 0; c < pr.nkr; ++c) work = work > pr.kr[c].L ? work : pr.kr[c].L;
+  *grid = dim3(static_cast<unsigned>(grid_for(work, 256, num_sms * 4)));
+  *block = dim3(256);
+}
+
+int launch_prologue(const Prologue& pr, double** gtab, int num_sms, cudaStream_t s) {
+  dim3 grid, block;
+  prologue_geometry(pr, num_sms, &grid, &block);
+  prologue_kernel<<<grid, block, 0, s>>>(pr, gtab);
   return 1;
-}
-
-int launch_contract_a(const double* Z, int64_t ldz, int64_t M, int64_t B, int R,
-                       const KRSpec& v, double* out, int64_t ldo, cudaStream_t s) {
-  const int64_t warps = B * R;
-  contract_a_kernel<<<grid_for(warps * 32, 256), 256, 0, s>>>(Z, ldz, M, B, R, v, out, ldo);
-  return 1;
-}
-
-size_t contract_b_scratch(int64_t M, int64_t B, int R, int num_sms) {
-  int TA, S;
-  int64_t nAB;
-  contract_b_shape(M, B, R, num_sms, &TA, &nAB, &S);
-  return S > 1 ? static_cast<size_t>(S) * R * M : 0;
-}
-
-int launch_contract_b(const double* Z, int64_t ldz, int64_t M, int64_t B, int R,
-                       const KRSpec& w, double* out, int64_t ldo, double* part, int num_sms,
-                       cudaStream_t s) {
-  int TA, S;
-  int64_t nAB;
-  contract_b_shape(M, B, R, num_sms, &TA, &nAB, &S);
-  dim3 grid(static_cast<unsigned>(nAB * S), static_cast<unsigned>(R));
-  contract_b_kernel<<<grid, kCB, 0, s>>>(Z, ldz, M, B, R, w, out, ldo, TA, nAB, S, part);
-  if (S > 1) contract_b_finish<<<grid_for(M * R, 256), 256, 0, s>>>(part, M, R, S, out, ldo);
-  return S > 1 ? 2 : 1;
 }
 
 }  // namespace cpdgpu
