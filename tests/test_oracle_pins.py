@@ -1,0 +1,382 @@
+"""Pins the CPU oracle (oracle/cpd_oracle.c) to the reference's own known
+answers and test fixtures before anything is checked against it.
+
+Every case restates a reference test (proj/tests/*.cpp, proj/tests/
+acceptance_main.cpp) on the same Uniform01-seeded inputs (rng.hpp:16-26,
+reproduced bit-for-bit).  The reference itself cannot be built in this image
+(Eigen is absent), so these known answers and the entrywise definition
+(test_util.hpp:44-60) are the pins.
+"""
+import numpy as np
+import pytest
+
+
+def max_rel_diff(a, b):
+    scale = max(np.abs(a).max(initial=0.0), np.abs(b).max(initial=0.0), 1e-30)
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max(initial=0.0) / scale)
+
+
+# ---- generators -----------------------------------------------------------------
+
+def test_uniform01_matches_std_mt19937_64(oracle):
+    # first draws of std::mt19937_64(mix_seed(20240901)) >> 11 * 2^-53, computed
+    # with libstdc++ (g++ 13) in this container
+    got = oracle.uniform01(20240901, 5)
+    want = [0.40673788021788759, 0.019265679107233646, 0.75923538947682068,
+            0.087608002855280698, 0.43253904052064951]
+    assert list(got) == want
+    assert oracle.uniform01(7, 401)[-1] == 0.75280540072332258  # draw 401: past one twist
+
+
+def test_random_factors_layout(oracle):
+    # test_util.hpp:30-41: one stream, column-major, factors in mode order
+    f = oracle.random_factors([2, 3], 2, 5)
+    v = oracle.uniform01(5, 10)
+    assert np.array_equal(f[0].reshape(-1, order="F"), v[:4])
+    assert np.array_equal(f[1].reshape(-1, order="F"), v[4:])
+
+
+def test_counter_generator_is_exact(oracle):
+    u = oracle.fill_upm1_f32(9, 1000)
+    assert u.dtype == np.float32
+    assert u.min() >= -1.0 and u.max() < 1.0
+    ints = u.astype(np.float64) * 2.0 ** 23
+    assert np.array_equal(ints, np.round(ints))  # multiples of 2^-23
+    x = oracle.fill_normal(3, 200000)
+    assert abs(x.mean()) < 0.01 and abs(x.std() - 1.0) < 0.01
+    assert np.array_equal(oracle.fill_normal(3, 100, offset=50), x[50:150])
+
+
+# ---- known answers (test_mttkrp.cpp) ----------------------------------------------
+
+def test_ladder_tensor_kat(oracle):
+    # test_mttkrp.cpp:13-35
+    g, _, _ = oracle.cp_gradient_all(np.arange(1, 9, dtype=float), [2, 2, 2], [np.ones((2, 2))] * 3)
+    want = [[16, 20], [14, 22], [10, 26]]
+    for n in range(3):
+        for r in range(2):
+            assert list(g[n][:, r]) == want[n]
+        assert list(oracle.brute_mttkrp(np.arange(1, 9, dtype=float), [2, 2, 2], [np.ones((2, 2))] * 3,
+                                        n + 1)[:, 0]) == want[n]
+
+
+def test_unit_basis_fiber(oracle):
+    # test_mttkrp.cpp:37-51
+    y = np.arange(1, 9, dtype=float)
+    e1 = [np.array([[1.0], [0.0]])] * 3
+    assert list(oracle.brute_mttkrp(y, [2, 2, 2], e1, 1)[:, 0]) == [1.0, 2.0]
+    assert list(oracle.brute_mttkrp(y, [2, 2, 2], e1, 3)[:, 0]) == [1.0, 5.0]
+    g, _, _ = oracle.cp_gradient_all(y, [2, 2, 2], e1)
+    assert list(g[0][:, 0]) == [1.0, 2.0] and list(g[2][:, 0]) == [1.0, 5.0]
+
+
+def test_select_pivot_kats(oracle):
+    # test_mttkrp.cpp:62-69
+    assert oracle.select_pivot([10, 10, 10]) == 1
+    assert oracle.select_pivot([10, 10, 10, 10]) == 2
+    assert oracle.select_pivot([2, 3, 4, 5]) == 2
+    assert oracle.select_pivot([3, 5]) == 1
+    assert oracle.select_pivot([2, 2, 3, 3, 4]) == 3
+    assert oracle.select_pivot([7]) < 0  # ArgumentError
+
+
+def test_sort_modes_kats(oracle):
+    # test_mttkrp.cpp:71-100
+    perm, inv = oracle.sort_perm([5, 3, 4])
+    assert perm == [2, 3, 1] and inv == [3, 1, 2]
+    assert oracle.sort_perm([2, 3, 3])[0] == [1, 2, 3]
+    assert oracle.sort_perm([4, 4, 4])[0] == [1, 2, 3]  # stable
+    y = oracle.random_tensor([5, 3, 4], 21)
+    yp = oracle.permute(y, [5, 3, 4], perm)
+    Y = y.reshape(5, 3, 4, order="F")
+    YP = yp.reshape(3, 4, 5, order="F")
+    for i1 in range(5):
+        for i2 in range(3):
+            for i3 in range(4):
+                assert YP[i2, i3, i1] == Y[i1, i2, i3]
+
+
+def test_fast_update_order_kats(oracle):
+    # test_mttkrp.cpp:151-157
+    assert oracle.fast_update_order([2, 3, 4, 5]) == [2, 1, 3, 4]
+    assert oracle.fast_update_order([10, 10, 10]) == [1, 2, 3]
+    assert oracle.fast_update_order([5, 3, 4]) == [2, 3, 1]
+
+
+SHAPES = [[2, 3, 4], [4, 3, 2], [3, 1, 4], [2, 2], [2, 3, 2, 4], [1, 5, 2], [6, 6]]
+
+
+@pytest.mark.parametrize("dims", SHAPES, ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("R", [1, 3])
+def test_fast_equals_brute(oracle, dims, R):
+    # test_mttkrp.cpp:102-119
+    y = oracle.random_tensor(dims, 100 + R)
+    f = oracle.random_factors(dims, R, 200 + R)
+    g, _, _ = oracle.cp_gradient_all(y, dims, f)
+    for n in range(1, len(dims) + 1):
+        assert max_rel_diff(g[n - 1], oracle.brute_mttkrp(y, dims, f, n)) < 1e-12
+
+
+def test_permutation_equivariance(oracle):
+    # test_mttkrp.cpp:121-136
+    dims = [3, 4, 2, 3]
+    y = oracle.random_tensor(dims, 301)
+    f = oracle.random_factors(dims, 2, 302)
+    base, _, _ = oracle.cp_gradient_all(y, dims, f)
+    perm = [3, 1, 4, 2]
+    moved, _, _ = oracle.cp_gradient_all(oracle.permute(y, dims, perm), [dims[p - 1] for p in perm],
+                                         [f[p - 1] for p in perm])
+    for k in range(4):
+        assert max_rel_diff(moved[k], base[perm[k] - 1]) < 1e-12
+
+
+def test_columns_independent(oracle):
+    # test_mttkrp.cpp:138-149
+    dims = [3, 2, 4]
+    y = oracle.random_tensor(dims, 401)
+    f = oracle.random_factors(dims, 3, 402)
+    joint, _, _ = oracle.cp_gradient_all(y, dims, f)
+    for r in range(3):
+        one, _, _ = oracle.cp_gradient_all(y, dims, [a[:, r:r + 1] for a in f])
+        for n in range(3):
+            assert max_rel_diff(joint[n][:, r], one[n][:, 0]) < 1e-12
+
+
+def test_hook_gauss_seidel(oracle):
+    # test_mttkrp.cpp:159-186
+    dims = [3, 4, 2, 3]
+    y = oracle.random_tensor(dims, 501)
+    f0 = oracle.random_factors(dims, 2, 502)
+    ref = [a.copy() for a in f0]
+    ref_grad = [None] * 4
+    for n in oracle.fast_update_order(dims):
+        ref_grad[n - 1] = oracle.brute_mttkrp(y, dims, ref, n)
+        ref[n - 1] = oracle.random_factors(dims, 2, 600 + n)[n - 1]
+    f = [a.copy() for a in f0]
+    got = [None] * 4
+
+    def hook(n, g, facs):
+        got[n - 1] = g
+        facs[n - 1] = oracle.random_factors(dims, 2, 600 + n)[n - 1]
+
+    oracle.cp_gradient_all(y, dims, f, hook=hook)
+    for n in range(4):
+        assert max_rel_diff(got[n], ref_grad[n]) < 1e-12
+        assert np.abs(f[n] - ref[n]).max() == 0.0
+
+
+def test_workspace_bound(oracle):
+    # test_mttkrp.cpp:188-198
+    dims = [4, 5, 6, 7]
+    _, _, peak = oracle.cp_gradient_all(oracle.random_tensor(dims, 601), dims, oracle.random_factors(dims, 3, 602))
+    p = oracle.select_pivot(dims)
+    J = int(np.prod(dims[:p]))
+    big = max(J, int(np.prod(dims)) // J)
+    assert 0 < peak <= 2 * 3 * big + big
+
+
+# ---- counts (test_counts.cpp) --------------------------------------------------------
+
+def test_count_kats(oracle):
+    # test_counts.cpp:35-53
+    assert oracle.predicted_mult_count([10, 10, 10], 1, 2, "direct") == 1100
+    assert oracle.predicted_mult_count([10, 10, 10], 1, 3, "direct") == 1100
+    assert oracle.predicted_mult_count([10, 10, 10], 1, 1, "direct") == 1110
+    assert oracle.predicted_mult_count([10, 10, 10], 5, 2, "direct") == 5500
+    assert oracle.predicted_mult_count([10, 10, 10, 10], 2, 1, "fast") == 200
+    assert oracle.predicted_mult_count([10, 10, 10], 1, 1, "fast") == 1110
+    assert oracle.predicted_mult_count([10, 10, 10], 1, 2, "fast") == 1100
+    assert oracle.predicted_mult_count([10, 10, 10], 1, 3, "fast") == 110
+
+
+@pytest.mark.parametrize("dims", [[2, 3, 4, 5], [3, 3, 3], [2, 3, 4], [4, 5], [2, 2, 2, 2, 2], [10, 10, 10]],
+                         ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("R", [1, 3])
+def test_instrumented_charges(oracle, dims, R):
+    # test_counts.cpp:81-93: counter snapshots inside the hook
+    y = oracle.random_tensor(dims, 1000 + R)
+    f = oracle.random_factors(dims, R, 1001 + R)
+    snaps = {"snaps": []}
+    _, total, _ = oracle.cp_gradient_all(y, dims, f, hook=lambda n, g, fa: None, counter=snaps)
+    prev, charges = 0, {}
+    for n, t in snaps["snaps"]:
+        charges[n] = t - prev
+        prev = t
+    for n in range(1, len(dims) + 1):
+        assert charges[n] == oracle.fast_count_realized(dims, R, n)
+    assert total == sum(oracle.fast_count_realized(dims, R, n) for n in range(1, len(dims) + 1))
+
+
+@pytest.mark.parametrize("dims", [[2, 3, 4, 5], [3, 3, 3], [2, 3, 4], [4, 5], [2, 2, 2, 2, 2],
+                                  [10, 10, 10], [10, 10, 10, 10], [2, 3, 3, 3], [2, 2, 9]],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_realized_vs_closed_forms(oracle, dims):
+    # test_counts.cpp:95-136
+    N = len(dims)
+    p = oracle.select_pivot(dims)
+    J = np.cumprod([1] + dims)
+    for R in (1, 2, 7):
+        for n in range(1, N + 1):
+            real = oracle.fast_count_realized(dims, R, n)
+            table = oracle.predicted_mult_count(dims, R, n, "fast")
+            derived = oracle.predicted_mult_count(dims, R, n, "fast_derived")
+            if n == p or 2 <= n < p:
+                assert real == table
+            elif n == 1:
+                assert real == table + R * int(J[1])
+            elif n == p + 1:
+                Kp, Jn = int(J[-1] // J[p]), int(J[n])
+                assert real == (table if Kp <= Jn else table + R * (Kp - Jn))
+            else:
+                assert real == derived
+            assert (table == derived) if n <= p + 1 else (derived <= table)
+
+
+def test_acceptance_criterion_1(oracle):
+    # acceptance_main.cpp:91-123: 100 random instances, per-entry relative <= 1e-12
+    rng = oracle.uniform01(20240901, 4000)
+    at = 0
+
+    def nxt():
+        nonlocal at
+        at += 1
+        return rng[at - 1]
+
+    worst = 0.0
+    for inst in range(100):
+        N = 3 + int(nxt() * 4.0)
+        while True:
+            dims = [1 + int(nxt() * 6.0) for _ in range(N)]
+            if int(np.prod(dims)) <= 20000:
+                break
+        R = 1 + int(nxt() * 4.0)
+        y = oracle.random_tensor(dims, 9000 + inst)
+        f = oracle.random_factors(dims, R, 9500 + inst)
+        g, _, _ = oracle.cp_gradient_all(y, dims, f)
+        for n in range(1, N + 1):
+            want = oracle.brute_mttkrp(y, dims, f, n)
+            worst = max(worst, float((np.abs(g[n - 1] - want) / np.maximum(np.abs(want), 1e-300)).max()))
+    assert worst <= 1e-12
+
+
+# ---- ALS (test_als.cpp, test_kruskal.cpp) -----------------------------------------------
+
+def test_pinv_psd(oracle):
+    # test_als.cpp:21-43
+    eye = np.eye(4)
+    assert max_rel_diff(oracle.pinv_psd(eye), eye) < 1e-14
+    d = np.zeros((2, 2))
+    d[0, 0] = 2.0
+    dp = oracle.pinv_psd(d)
+    assert abs(dp[0, 0] - 0.5) <= 0.5e-14 and dp[1, 1] == 0.0
+    assert np.abs(oracle.pinv_psd(np.zeros((3, 3)))).max() == 0.0
+    x = np.random.default_rng(0).uniform(-1, 1, (3, 5))
+    s = x.T @ x
+    sp = oracle.pinv_psd(s)
+    assert max_rel_diff(s @ sp @ s, s) < 1e-10
+    assert max_rel_diff(sp @ s @ sp, sp) < 1e-10
+    assert max_rel_diff(sp, sp.T) < 1e-12
+    assert max_rel_diff(sp, np.linalg.pinv(s, rcond=1e-12, hermitian=True)) < 1e-9
+    with pytest.raises(ValueError):
+        oracle.pinv_psd(eye, -1.0)
+
+
+def test_update_stationary_zero_nan(oracle):
+    # test_als.cpp:45-61
+    dims = [3, 4, 2]
+    f = oracle.random_factors(dims, 2, 11)
+    y = oracle.full(dims, f)
+    for n in range(1, 4):
+        m = oracle.brute_mttkrp(y, dims, f, n)
+        assert max_rel_diff(oracle.als_update_mode(m, f, n), f[n - 1]) < 1e-10
+    m0 = oracle.brute_mttkrp(np.zeros(24), dims, f, 1)
+    assert np.abs(oracle.als_update_mode(m0, f, 1)).max() == 0.0
+    with pytest.raises(ValueError):
+        oracle.als_update_mode(np.full((3, 2), np.nan), f, 1)
+
+
+def test_rank1_two_sweeps_and_monotone(oracle):
+    # test_als.cpp:63-70 (fast sweeps here), 89-104
+    truth = oracle.random_factors([4, 3, 5], 1, 21)
+    y = oracle.full([4, 3, 5], truth)
+    f = oracle.random_factors([4, 3, 5], 1, 22)
+    oracle.als_sweep_fast(y, [4, 3, 5], f)
+    oracle.als_sweep_fast(y, [4, 3, 5], f)
+    assert np.sqrt(oracle.cost(y, [4, 3, 5], f)) / np.linalg.norm(y) < 1e-10
+    yr = oracle.random_tensor([4, 5, 3], 41)
+    f = oracle.random_factors([4, 5, 3], 3, 42)
+    prev = oracle.cost(yr, [4, 5, 3], f)
+    for _ in range(20):
+        oracle.als_sweep_fast(yr, [4, 5, 3], f)
+        d = oracle.cost(yr, [4, 5, 3], f)
+        assert d <= prev * (1 + 1e-10) + 1e-12
+        prev = d
+
+
+def test_exact_fit_fixed_point(oracle):
+    # test_als.cpp:106-112
+    f = oracle.random_factors([3, 3, 4], 2, 51)
+    g = [a.copy() for a in f]
+    oracle.als_sweep_fast(oracle.full([3, 3, 4], f), [3, 3, 4], g)
+    for n in range(3):
+        assert max_rel_diff(f[n], g[n]) < 1e-9
+
+
+def test_cost_kats(oracle):
+    # test_kruskal.cpp:53-77
+    t8 = np.arange(1, 9, dtype=float)
+    assert abs(oracle.cost(t8, [2, 2, 2], [np.zeros((2, 2))] * 3) - 204.0) <= 204 * 1e-14
+    f = oracle.random_factors([3, 4, 2], 2, 41)
+    assert oracle.cost(oracle.full([3, 4, 2], f), [3, 4, 2], f) < 1e-16
+    yr = oracle.random_tensor([3, 4, 2], 43)
+    a = oracle.cost(yr, [3, 4, 2], f, materialize_limit=0)  # Gram identity path
+    b = oracle.cost(yr, [3, 4, 2], f)
+    assert abs(a - b) <= 1e-12 * b
+
+
+def test_run_trace_and_recovery(oracle):
+    # test_als.cpp:198-222, 240-249, 264-279
+    y = oracle.random_tensor([4, 3, 5], 91)
+    _, tr = oracle.run_als_fast(y, [4, 3, 5], oracle.random_factors([4, 3, 5], 2, 92), max_iters=4)
+    assert tr["iters_run"] == 4
+    yn = np.linalg.norm(y)
+    for i in range(4):
+        assert abs(tr["rel_error"][i] - np.sqrt(tr["cost"][i]) / yn) <= 1e-12 * tr["rel_error"][i]
+    assert all(tr["mults"][i] >= tr["mults"][i - 1] for i in range(1, 4))
+    truth = oracle.random_factors([4, 4, 4], 1, 111)
+    _, tr = oracle.run_als_fast(oracle.full([4, 4, 4], truth), [4, 4, 4],
+                                oracle.random_factors([4, 4, 4], 1, 112), max_iters=50, tol=1e-6)
+    assert 2 <= tr["iters_run"] < 50
+    truth = oracle.random_factors([6, 6, 6], 2, 131)
+    y6 = oracle.full([6, 6, 6], truth)
+    ok = any(oracle.run_als_fast(y6, [6, 6, 6], oracle.random_factors([6, 6, 6], 2, s), max_iters=150)[1]
+             ["rel_error"][-1] < 1e-4 for s in (201, 202, 203))
+    assert ok
+
+
+def test_unsorted_run_matches_sorted(oracle):
+    # test_als.cpp:224-238 (run on an unsorted shape == run in the sorted frame)
+    dims = [5, 3, 4]
+    y = oracle.random_tensor(dims, 101)
+    init = oracle.random_factors(dims, 2, 102)
+    fa, ta = oracle.run_als_fast(y, dims, init, max_iters=6)
+    perm, _ = oracle.sort_perm(dims)
+    ys = oracle.permute(y, dims, perm)
+    fb, tb = oracle.run_als_fast(ys, [dims[p - 1] for p in perm], [init[p - 1] for p in perm], max_iters=6)
+    for j, p in enumerate(perm):
+        assert max_rel_diff(fa[p - 1], fb[j]) < 1e-12
+    assert np.allclose(ta["cost"], tb["cost"], rtol=1e-12)
+
+
+def test_golden_fixtures_reproduce(oracle):
+    """The committed fixtures (tests/golden/make_golden.py) still match the oracle."""
+    from pathlib import Path
+    files = sorted((Path(__file__).resolve().parent / "golden").glob("grad_*.npz"))
+    assert len(files) >= 8
+    for fn in files:
+        z = np.load(fn)
+        dims = [int(d) for d in z["dims"]]
+        f = [z[f"A{k}"] for k in range(len(dims))]
+        g, _, _ = oracle.cp_gradient_all(z["y"], dims, f)
+        for k in range(len(dims)):
+            assert max_rel_diff(g[k], z[f"G{k}"]) < 1e-13, fn.name
