@@ -23,6 +23,7 @@ struct SeedParams {
   int use32;        // all KR row indices fit in 32 bits
   int use_tma;      // Y tiles arrive by 2-D TMA (dense LDY == TI); else plain copies
   int stages;       // pipeline depth (2 or 3)
+  int prefetch;     // Y tiles prefetched into L2 beyond the ring (CPDGPU_SEED_PREFETCH)
   int debug;        // experiment knobs (CPDGPU_SEED_DEBUG): bit 0 skips KR generation
   KRSpec left;      // modes 1..p   (rows of the view)
   KRSpec right;     // modes p+1..N (columns of the view)

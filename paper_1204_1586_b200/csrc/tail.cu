@@ -23,15 +23,32 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __device__ __forceinline__ double kr_at(const KRSpec& s, int64_t q, int r) {
+  if (s.n == 0) return 1.0;
+  if (s.n == 1) return __ldg(s.A[0] + q + s.dims[0] * r);  // one factor: no digits
   return q < (1LL << 31) ? kr_entry32(s, static_cast<uint32_t>(q), r) : kr_entry(s, q, r);
+}
+
+// sum_{x = lane, lane + 32, ... < n} z[x * stride] * KR(s)[x, r], four
+// independent partial sums in flight (latency of the L2-resident operands).
+__device__ __forceinline__ double strided_dot(const double* z, int64_t stride, int64_t n, const KRSpec& s, int r,
+                                              int lane) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t x = lane;
+  for (; x + 96 < n; x += 128) {
+    s0 += z[x * stride] * kr_at(s, x, r);
+    s1 += z[(x + 32) * stride] * kr_at(s, x + 32, r);
+    s2 += z[(x + 64) * stride] * kr_at(s, x + 64, r);
+    s3 += z[(x + 96) * stride] * kr_at(s, x + 96, r);
+  }
+  for (; x < n; x += 32) s0 += z[x * stride] * kr_at(s, x, r);
+  return (s0 + s1) + (s2 + s3);
 }
 
 // Number of warp work units of an op.
 __host__ __device__ inline int64_t op_units(const TailOp& o) {
   switch (o.type) {
     case kOpContractA: return o.B * o.R;                       // warp per output (b, r)
-    case kOpContractB:                                         // M >= 32: warp per 32 outputs
-      return o.M >= 32 ? ((o.M + 31) / 32) * o.R : o.M * o.R;  // else warp per output
+    case kOpContractB: return o.M * o.R;                       // warp per output (a, r)
     case kOpReduceRight:                                       // B == 1: warp per output (lanes over slots)
       return o.B == 1 ? o.M * o.R : ((o.M + 31) / 32) * o.R;   // else 32 rows per warp
     case kOpReduceLeft: return ((o.M + 31) / 32) * o.R;        // 32 columns per warp
@@ -48,31 +65,13 @@ __device__ void run_unit(const TailOp& o, int64_t u, int lane, double* const* gt
   if (o.type == kOpContractA) {  // out[r][b] = sum_a Z[r][a + M b] KR_v[a, r]
     const int r = static_cast<int>(u / o.B);
     const int64_t b = u - r * o.B;
-    const double* z = o.Z + r * o.ldz + o.M * b;
-    double s = 0.0;
-    for (int64_t a = lane; a < o.M; a += 32) s += z[a] * kr_at(o.kr, a, r);
-    s = warp_sum(s);
+    const double s = warp_sum(strided_dot(o.Z + r * o.ldz + o.M * b, 1, o.M, o.kr, r, lane));
     if (lane == 0) out[r * o.ldo + b] = s;
   } else if (o.type == kOpContractB) {  // out[r][a] = sum_b Z[r][a + M b] KR_w[b, r]
-    if (o.M >= 32) {  // lanes over a (coalesced), loop over b
-      const int64_t chunks = (o.M + 31) / 32;
-      const int r = static_cast<int>(u / chunks);
-      const int64_t a = (u - r * chunks) * 32 + lane;
-      if (a < o.M) {
-        const double* z = o.Z + r * o.ldz + a;
-        double s = 0.0;
-        for (int64_t b = 0; b < o.B; ++b) s += z[o.M * b] * kr_at(o.kr, b, r);
-        out[r * o.ldo + a] = s;
-      }
-    } else {  // warp per output, lanes over b
-      const int r = static_cast<int>(u / o.M);
-      const int64_t a = u - r * o.M;
-      const double* z = o.Z + r * o.ldz + a;
-      double s = 0.0;
-      for (int64_t b = lane; b < o.B; b += 32) s += z[o.M * b] * kr_at(o.kr, b, r);
-      s = warp_sum(s);
-      if (lane == 0) out[r * o.ldo + a] = s;
-    }
+    const int r = static_cast<int>(u / o.M);
+    const int64_t a = u - r * o.M;
+    const double s = warp_sum(strided_dot(o.Z + r * o.ldz + a, o.M, o.B, o.kr, r, lane));
+    if (lane == 0) out[r * o.ldo + a] = s;
   } else if (o.type == kOpReduceRight && o.B == 1) {  // many slots: lanes over slots, fixed tree
     const int r = static_cast<int>(u / o.M);
     const int64_t i = u - r * o.M;
@@ -122,13 +121,31 @@ __global__ void __launch_bounds__(256) tail_step_kernel(const TailStep st, doubl
 }
 
 // Prologue: sorted factors Fs[j] <- input block perm[j]; output pointer table;
-// Khatri-Rao rows of every K1 chunk: out[q * LDK + r] = KR(spec)[q, r].
-template <int RP>
-__device__ void kr_rows(const KRSpec& s, int64_t L, int R, int LDK, double* out, int64_t t, int64_t nt) {
-  for (int64_t q = t; q < L; q += nt) {
-    double* dst = out + q * LDK;
-    kr_row<RP>(s, q, R, q < (1LL << 31), dst);
-    for (int r = RP; r < LDK; ++r) dst[r] = 0.0;
+// Khatri-Rao rows of every K1 chunk: out[q * LDK + r] = KR(spec)[q, r], one
+// thread per (row, 8 rank columns).
+__device__ void kr_rows(const KRJob& k, int64_t t, int64_t nt) {
+  const int chunks = k.LDK / 8;
+  for (int64_t e = t; e < k.L * chunks; e += nt) {
+    const int64_t q = e / chunks;
+    const int r0 = static_cast<int>(e - q * chunks) * 8;
+    double acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r] = r0 + r < k.R ? 1.0 : 0.0;
+    if (r0 < k.R) {
+      int64_t rem = q;
+      for (int m = 0; m < k.spec.n; ++m) {
+        const int64_t I = k.spec.dims[m];
+        const int64_t d = rem % I;
+        rem /= I;
+        const double* a = k.spec.A[m] + d + I * r0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r0 + r < k.R) acc[r] *= __ldg(a + I * r);
+      }
+    }
+    double* dst = k.out + q * k.LDK + r0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) dst[r] = acc[r];
   }
 }
 
@@ -139,15 +156,7 @@ __global__ void __launch_bounds__(256) prologue_kernel(const Prologue pr, double
   if (pr.Fs)
     for (int j = 0; j < pr.N; ++j)
       for (int64_t e = t; e < pr.len[j]; e += nt) pr.Fs[pr.dst_off[j] + e] = pr.fin[pr.src_off[j] + e];
-  for (int c = 0; c < pr.nkr; ++c) {
-    const KRJob& k = pr.kr[c];
-    switch (k.NT) {
-      case 1: kr_rows<8>(k.spec, k.L, k.R, k.LDK, k.out, t, nt); break;
-      case 2: kr_rows<16>(k.spec, k.L, k.R, k.LDK, k.out, t, nt); break;
-      case 3: kr_rows<24>(k.spec, k.L, k.R, k.LDK, k.out, t, nt); break;
-      default: kr_rows<32>(k.spec, k.L, k.R, k.LDK, k.out, t, nt); break;
-    }
-  }
+  for (int c = 0; c < pr.nkr; ++c) kr_rows(pr.kr[c], t, nt);
 }
 
 int grid_for(int64_t work, int threads, int cap) {
@@ -175,7 +184,7 @@ const void* prologue_kernel_fn() { return reinterpret_cast<const void*>(prologue
 void prologue_geometry(const Prologue& pr, int num_sms, dim3* grid, dim3* block) {
   int64_t work = 0;
   for (int j = 0; j < pr.N; ++j) work = work > pr.len[j] ? work : pr.len[j];
-  for (int c = 0; c < pr.nkr; ++c) work = work > pr.kr[c].L ? work : pr.kr[c].L;
+  for (int c = 0; c < pr.nkr; ++c) work = work > pr.kr[c].L * (pr.kr[c].LDK / 8) ? work : pr.kr[c].L * (pr.kr[c].LDK / 8);
   *grid = dim3(static_cast<unsigned>(grid_for(work, 256, num_sms * 4)));
   *block = dim3(256);
 }

@@ -52,6 +52,20 @@ __global__ void smem_gemm(double* out, int iters) {
   if (s == 1.2345) out[0] = s;
 }
 
+// every DMMA with fresh A and B registers (no operand reuse between neighbours)
+template <int CH>
+__global__ void noreuse(double* out, int iters) {
+  double c[CH][2], a[CH], b[CH];
+  for (int i = 0; i < CH; ++i) { c[i][0] = c[i][1] = 0; a[i] = 1e-3 * (i + threadIdx.x); b[i] = 1.0 + 1e-6 * i; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) dmma(c[i], a[i], b[i]);
+  }
+  double s = 0;
+  for (int i = 0; i < CH; ++i) s += c[i][0] + c[i][1];
+  if (s == 1.2345) out[0] = s;
+}
+
 template <typename F>
 float timeit(F f) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -81,5 +95,11 @@ int main() {
     report("smem_gemm<" #M "," #N ">", w, (double)M * N * 8 * (iters / 8), ms);                       \
   }
   SG(6, 3) SG(7, 2) SG(4, 3) SG(2, 3) SG(1, 3)
+#define NR(N)                                                                                         \
+  for (int w : {4, 8, 16}) {                                                                          \
+    float ms = timeit([&] { noreuse<N><<<sms, 32 * w>>>(out, iters); });                             \
+    report("noreuse<" #N ">", w, (double)N * iters, ms);                                             \
+  }
+  NR(4) NR(8) NR(12)
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
 }
