@@ -47,7 +47,11 @@ CONFIGS = {
     "c1": ([200, 200, 200], 10, "f64", "3-D 200^3 fp64 R=10"),
     "c2": ([60, 60, 60, 60], 20, "f64", "4-D 60^4 fp64 R=20"),
     "c3": ([14] * 7, 10, "f64", "7-D 14^7 fp64 R=10"),
+    # CP_ALS end to end: a step is one fast ALS sweep (BASELINE.json configs[3])
+    "c4": ([60] * 5, 16, "f64", "5-D 60^5 fp64 rank-16 model + 20 dB noise, R=16"),
 }
+ALS_CONFIGS = {"c4"}
+C4_ITERS = 50
 FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 microbenchmark on B200, profiles/r01_fp64_peak_microbench.txt
 L2_FLUSH_BYTES = 256 << 20
 
@@ -239,6 +243,7 @@ def run_ours(args, cfg):
             step()
             stops[i].record(stream)
         torch.cuda.synchronize(dev)
+        gpu_launches = ctx.launch_count() - launches0  # kernels of the K timed steps
         if world > 1:
             dist.barrier()
         # clocks need a busy window long enough to sample: keep the same step
@@ -248,7 +253,6 @@ def run_ours(args, cfg):
             for _ in range(50):
                 step()
             torch.cuda.synchronize(dev)
-    gpu_launches = ctx.launch_count() - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, stops)]
     tot_ms = float(np.sum(step_ms))
     if world > 1:
@@ -353,6 +357,203 @@ def cpu_baseline(args, cfg):
             "ms_per_step": dt * 1e3}
 
 
+# ---------------------------------------------------------------------------- CP_ALS (c4)
+
+def c4_truth(I, R, N, seed, fill):
+    """Factors of the rank-R N(0,1) ground-truth model and of the init (separate seed)."""
+    truth = [fill(seed * 100 + k, I * R).reshape(I, R, order="F") for k in range(N)]
+    init = [fill(seed * 1000 + 7 + k, I * R).reshape(I, R, order="F") for k in range(N)]
+    return truth, init
+
+
+def c4_device_tensor(ctx, dims, truth, seed=4):
+    """Y = sigma E + full(model), sigma = |full| / (10 |E|) (SNR 20 dB), built on the device."""
+    import paper_1204_1586_b200 as cpd
+    y = cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=seed, ctx=ctx)
+    e2 = y.norm2()
+    t = cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=seed, ctx=ctx)
+    t.axpby_kruskal(0.0, 1.0, truth)
+    full2 = t.norm2()
+    t.free()
+    y.axpby_kruskal(float(np.sqrt(full2) / (10.0 * np.sqrt(e2))), 1.0, truth)
+    return y
+
+
+def als_metric(desc):
+    return f"CP_ALS iterations per second ({desc})"
+
+
+def run_reference_als(args, cfg):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    dims, R, dtype, desc = cfg
+    cores = host_cores()
+    n = int(np.prod(dims))
+    truth, init = c4_truth(dims[0], R, len(dims), 4, O.fill_normal)
+    e = O.fill_normal(4, n, nthreads=cores)
+    full = O.full(dims, truth)
+    sigma = float(np.sqrt(np.dot(full, full)) / (10.0 * np.sqrt(np.dot(e, e))))
+    y = sigma * e + full
+    del e, full
+    f = [a.copy(order="F") for a in init]
+    for _ in range(min(args.warmup, 1)):
+        O.als_sweep_fast(y, dims, f, nthreads=cores)
+    done, t0 = 0, time.perf_counter()
+    while done < args.steps and (done < 2 or time.perf_counter() - t0 < args.cpu_seconds * 6):
+        O.als_sweep_fast(y, dims, f, nthreads=cores)
+        done += 1
+    dt = (time.perf_counter() - t0) / done
+    line = {
+        "impl": "reference", "metric": als_metric(desc), "value": 1.0 / dt, "unit": "iters/s", "n_gpus": 1,
+        "steps": done, "warmup": min(args.warmup, 1), "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic rank-16 N(0,1) model + N(0,1) noise at 20 dB, counter-based generator",
+        "config": {"workload": args.config, "dims": dims, "R": R},
+        "cpu_baseline": {"value": 1.0 / dt, "unit": "iters/s", "cores": cores, "kind": "port",
+                         "sample": f"{done} fast ALS sweeps of the full {args.config} tensor "
+                                   "(oracle/cpd_oracle.c, OpenMP), time-bounded"},
+        "e2e": {"value": 1.0 / dt, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours_als(args, cfg):
+    """c4: K fast ALS sweeps on the device (cpdgpu_als_run), per-sweep CUDA events
+    on the launching stream.  Y (6.2 GB) is far larger than L2.  N>1 runs
+    independent replicas (the Gauss-Seidel sweep is not sharded)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1204_1586_b200 as cpd
+    from paper_1204_1586_b200 import build as B
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if rank == 0:
+        B.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+    B.build()
+    dims, R, dtype, desc = cfg
+    N = len(dims)
+    slab = int(np.prod(dims))
+    ctx = cpd.Context(local)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    truth, init = c4_truth(dims[0], R, N, 4, lambda s, n: device_normal(ctx, s, n, 1).reshape(-1))
+    y = c4_device_tensor(ctx, dims, truth)
+
+    cpd.run(y, init, cpd.SolveOptions(max_iters=max(args.warmup, 3)))  # warm-up (graph capture)
+    torch.cuda.synchronize(dev)
+    launches0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        res = cpd.run(y, init, cpd.SolveOptions(max_iters=args.steps))
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        gpu_launches = ctx.launch_count() - launches0
+        if world > 1:
+            dist.barrier()
+        t_end = time.time() + 2.0  # keep the same sweep busy until the sampler has seen it
+        while time.time() < t_end and len(clk.lines) < 10:
+            cpd.run(y, init, cpd.SolveOptions(max_iters=20))
+    sweep_s = float(np.sum(res.trace.seconds))
+    if world > 1:
+        t = torch.tensor([sweep_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sweep_s = float(t.item())
+    ms = sweep_s / args.steps * 1e3
+    value = world * args.steps / sweep_s
+
+    # dominant kernel: the two seed contractions of a sweep (K1 right + K1 left)
+    ctx.set_timing(True)
+    seed_ms = []
+    fdev = torch.from_numpy(np.concatenate([f.reshape(-1, order="F") for f in init])).to(dev)
+    gdev = torch.zeros_like(fdev)
+    for _ in range(10):
+        cpd.cp_gradient_all_device(y, R, fdev.data_ptr(), gdev.data_ptr(), 0)
+        seed_ms.append(ctx.last_seed_ms())
+    ctx.set_timing(False)
+    seed_avg = float(np.mean(seed_ms))
+    flops = 4.0 * R * slab
+    peaks = measured_peaks()
+    tflops = flops / (seed_avg * 1e-3) / 1e12
+    hbm_gbs = (8.0 * slab) / (seed_avg * 1e-3) / 1e9
+    roofline = {"bound": "tensor", "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": tflops / FP64_PEAK_TFLOPS, "traffic": None,
+                "kernel": "seed_f64_kernel (K1, fp64 DMMA; one Y pass of a gradient)", "kernel_ms": seed_avg,
+                "algorithmic_flops": flops,
+                "peak_source": "FP64 DMMA peak measured on B200 (profiles/r01_fp64_peak_microbench.txt)",
+                "hbm": {"achieved": hbm_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                        "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0)}}
+
+    # e2e: a full run() through the host API with Y uploaded from pinned host memory
+    e2e = None
+    if not args.no_e2e and world == 1:
+        host_y = torch.empty(slab, dtype=torch.float64).pin_memory()
+        host_y.copy_(torch.from_numpy(y.values()))
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        y.update(host_y.data_ptr())
+        r2 = cpd.run(y, init, cpd.SolveOptions(max_iters=C4_ITERS))
+        dt = time.perf_counter() - t0
+        e2e = {"value": C4_ITERS / dt, "unit": "iters/s",
+               "h2d_bytes_per_step": (slab * 8 + 8 * R * sum(dims)) / C4_ITERS,
+               "d2h_bytes_per_step": (8 * R * sum(dims) + 8 * 3 * C4_ITERS) / C4_ITERS,
+               "ms_per_step": dt * 1e3 / C4_ITERS,
+               "timing": f"wall clock around one host-API run(): H2D of Y + {C4_ITERS} sweeps + fit trace + "
+                         "factors back, divided by the sweep count",
+               "final_rel_error": r2.trace.rel_error[-1]}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle as O
+        cores = host_cores()
+        yh = y.values()
+        f = [a.copy(order="F") for a in init]
+        done, t0 = 0, time.perf_counter()
+        while done < 1 or time.perf_counter() - t0 < args.cpu_seconds:
+            O.als_sweep_fast(yh, dims, f, nthreads=cores)
+            done += 1
+        dt = (time.perf_counter() - t0) / done
+        del yh
+        cpu = {"value": 1.0 / dt, "unit": "iters/s", "cores": cores, "kind": "port",
+               "sample": f"{done} fast ALS sweeps of the same {args.config} tensor (~{args.cpu_seconds:.0f} s), "
+                         "oracle/cpd_oracle.c OpenMP", "ms_per_step": dt * 1e3}
+    if rank == 0:
+        line = {
+            "metric": als_metric(desc), "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic rank-16 N(0,1) model + N(0,1) noise at 20 dB, counter-based generator",
+            "config": {"workload": args.config, "dims": dims, "R": R,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (6.2 GB tensor)",
+                       "run_ms_incl_fit": ev0.elapsed_time(ev1),
+                       "final_rel_error": res.trace.rel_error[-1]},
+            "gpu_launches": gpu_launches, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -365,6 +566,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.config in ALS_CONFIGS:
+        return run_reference_als(args, cfg) if args.impl == "reference" else run_ours_als(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)
