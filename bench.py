@@ -49,7 +49,10 @@ CONFIGS = {
     "c3": ([14] * 7, 10, "f64", "7-D 14^7 fp64 R=10"),
     # CP_ALS end to end: a step is one fast ALS sweep (BASELINE.json configs[3])
     "c4": ([60] * 5, 16, "f64", "5-D 60^5 fp64 rank-16 model + 20 dB noise, R=16"),
+    # fp32 on the tensor cores; the 300^4 tensor is split over the GPUs (strong scaling)
+    "c5": ([300] * 4, 64, "f32", "4-D 300^4 fp32 R=64"),
 }
+STRONG_CONFIGS = {"c5"}
 ALS_CONFIGS = {"c4"}
 C4_ITERS = 50
 FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 microbenchmark on B200, profiles/r01_fp64_peak_microbench.txt
@@ -146,26 +149,37 @@ def run_reference(args, cfg):
     if rank != 0:
         return 0
     dims, R, dtype, desc = cfg
-    n = int(np.prod(dims))
+    sd = sample_dims(dims, dtype)
+    n = int(np.prod(sd))
     cores = host_cores()
-    y = O.fill_normal(1, n, nthreads=cores)
-    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
-    for _ in range(args.warmup):
-        O.cp_gradient_all(y, dims, f, nthreads=cores)
+    esize = 4 if dtype == "f32" else 8
+    if dtype == "f32":  # fp64 oracle on the upcast fp32 values (the reference is fp64-only)
+        y = O.fill_upm1_f32(1, n, nthreads=cores).astype(np.float64)
+    else:
+        y = O.fill_normal(1, n, nthreads=cores)
+    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(sd)]
+    steps = args.steps
+    for _ in range(min(args.warmup, 3)):
+        O.cp_gradient_all(y, sd, f, nthreads=cores)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        O.cp_gradient_all(y, dims, f, nthreads=cores)
+    done = 0
+    while done < steps and (done < 3 or time.perf_counter() - t0 < args.cpu_seconds * 6):
+        O.cp_gradient_all(y, sd, f, nthreads=cores)
+        done += 1
     dt = time.perf_counter() - t0
-    ms = dt / args.steps * 1e3
-    gbs = n * 8 / (ms * 1e-3) / 1e9
+    ms = dt / done * 1e3
+    gbs = n * esize / (ms * 1e-3) / 1e9
+    what = "full" if sd == list(dims) else f"{'x'.join(map(str, sd))}-slab sample of the"
     line = {
         "impl": "reference", "metric": f"all-mode CP gradient throughput ({desc})", "value": gbs,
-        "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic N(0,1), counter-based generator",
-        "config": {"workload": args.config, "dims": dims, "R": R},
+        "unit": "GB/s", "n_gpus": 1, "steps": done, "warmup": min(args.warmup, 3), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if args.config in STRONG_CONFIGS else "weak",
+        "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic, counter-based generator (same values as the GPU arm)",
+        "config": {"workload": args.config, "dims": dims, "R": R, "sample_dims": sd},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"full {args.config} gradient x {args.steps} steps (oracle/cpd_oracle.c, OpenMP)"},
+                         "sample": f"{what} {args.config} gradient x {done} steps (oracle/cpd_oracle.c, OpenMP, "
+                                   "time-bounded)"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -202,13 +216,18 @@ def run_ours(args, cfg):
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
-    # global tensor: dims[:-1] x (dims[-1] * world); this rank's slab is dims
-    gdims = list(dims[:-1]) + [dims[-1] * world]
+    f32 = dtype == "f32"
+    esize = 4 if f32 else 8
+    strong = args.config in STRONG_CONFIGS
+    # weak: global dims[:-1] x (dims[-1] * world), every rank one dims-sized slab;
+    # strong: the global tensor is dims, each rank a contiguous last-mode slab
+    gdims = list(dims) if strong else list(dims[:-1]) + [dims[-1] * world]
     plan = sharded.make_plan(gdims, R, rank, world) if world > 1 else None
-    slab = int(np.prod(dims))
-    a0 = plan.bounds[0] if plan else 0
-    y = cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=1, ctx=ctx,
-                                 offset=a0 * int(np.prod(dims[:-1])))
+    a0, a1 = plan.bounds if plan else (0, gdims[-1])
+    ldims = list(gdims[:-1]) + [a1 - a0]
+    slab = int(np.prod(ldims))
+    y = cpd.DenseTensor.generate(ldims, cpd.DIST_UNIFORM_PM1 if f32 else cpd.DIST_NORMAL, seed=1, ctx=ctx,
+                                 offset=a0 * int(np.prod(gdims[:-1])), dtype=cpd.F32 if f32 else cpd.F64)
     gfac = [device_normal(ctx, 100 + k, d, R) for k, d in enumerate(gdims)]
     if plan:
         packed = sharded.pack_local_factors(plan, gfac, np)
@@ -218,7 +237,8 @@ def run_ours(args, cfg):
         pivot = 0
     fdev = torch.from_numpy(packed).to(dev)
     gdev = torch.zeros_like(fdev)
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    flush_needed = slab * esize < 4 * L2_FLUSH_BYTES  # inputs larger than L2 need no flush
+    flush = torch.empty(L2_FLUSH_BYTES if flush_needed else 16, dtype=torch.uint8, device=dev)
 
     def step():
         cpd.cp_gradient_all_device(y, R, fdev.data_ptr(), gdev.data_ptr(), pivot)
@@ -260,7 +280,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     ms = tot_ms / args.steps
-    total_bytes = slab * 8 * world
+    total_bytes = int(np.prod(gdims)) * esize
     value = total_bytes / (ms * 1e-3) / 1e9
 
     # dominant kernel: K1 seed contraction, timed live with CUDA events
@@ -273,7 +293,7 @@ def run_ours(args, cfg):
     ctx.set_timing(False)
     seed_avg = float(np.mean(seed_ms))
     flops = 4.0 * R * slab
-    bytes_alg = 8.0 * slab + 2 * 8.0 * R * sum(dims)
+    bytes_alg = esize * slab + 2 * 8.0 * R * sum(ldims)
     peaks = measured_peaks()
     tflops = flops / (seed_avg * 1e-3) / 1e12
     hbm_gbs = bytes_alg / (seed_avg * 1e-3) / 1e9
@@ -284,21 +304,31 @@ def run_ours(args, cfg):
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": "seed_f64_kernel (K1, fp64 DMMA)", "kernel_ms": seed_avg,
-                "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
-                "peak_source": "FP64 DMMA peak measured on B200 (profiles/r01_fp64_peak_microbench.txt)",
-                "hbm": {"achieved": hbm_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                        "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0)}}
+    if f32:  # two tcgen05 passes over Y (right and left seeds): HBM-bound
+        hbm_peak = peaks.get("hbm_gbs", 6539.9)
+        roofline = {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hbm_gbs / hbm_peak, "traffic": traffic,
+                    "kernel": "seed_f32_kernel<0>+<1> (K1, tcgen05 kind::f16 split-fp16, two passes)",
+                    "kernel_ms": seed_avg, "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                    "tensor": {"executed_flops": 3 * flops, "achieved_tflops": 3 * tflops,
+                               "note": "3 fp16 MMAs per product (hi*hi + lo*hi + hi*lo)"}}
+    else:
+        roofline = {"bound": "tensor", "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
+                    "kernel": "seed_f64_kernel (K1, fp64 DMMA)", "kernel_ms": seed_avg,
+                    "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
+                    "peak_source": "FP64 DMMA peak measured on B200 (profiles/r01_fp64_peak_microbench.txt)",
+                    "hbm": {"achieved": hbm_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                            "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0)}}
 
     # e2e through the host C-ABI: H2D of Y from pinned memory + factors, D2H of gradients
     e2e = None
-    if not args.no_e2e and world == 1:
-        host_y = torch.empty(slab, dtype=torch.float64).pin_memory()
+    if not args.no_e2e and world == 1 and host_memory_ok(3 * slab * esize):
+        host_y = torch.empty(slab, dtype=torch.float32 if f32 else torch.float64).pin_memory()
         host_y.copy_(torch.from_numpy(y.values()))
         facs = [f.copy(order="F") for f in gfac]
-        e_steps = max(3, min(args.steps, 20))
+        e_steps = max(3, min(args.steps, 20 if slab * esize < (1 << 30) else 3))
         for _ in range(2):
             y.update(host_y.data_ptr())
             cpd.cp_gradient_all(y, facs)
@@ -308,24 +338,27 @@ def run_ours(args, cfg):
             y.update(host_y.data_ptr())
             cpd.cp_gradient_all(y, facs)
         dt = (time.perf_counter() - t0) / e_steps
-        e2e = {"value": slab * 8 / dt / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": slab * 8 + 8 * R * sum(dims),
+        e2e = {"value": slab * esize / dt / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": slab * esize + 8 * R * sum(dims),
                "d2h_bytes_per_step": 8 * R * sum(dims), "ms_per_step": dt * 1e3,
                "timing": "wall clock around synchronous host-API calls"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, cfg)
+        cpu = cpu_baseline(args, cfg, y if f32 else None)
 
     if rank == 0:
         line = {
             "metric": f"all-mode CP gradient throughput ({desc})", "value": value, "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic N(0,1), counter-based generator",
-            "config": {"workload": args.config, "dims": dims, "R": R,
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": dtype,
+            "data": ("synthetic U(-1,1) fp32 tensor, N(0,1) factors" if f32 else "synthetic N(0,1)")
+                    + ", counter-based generator",
+            "config": {"workload": args.config, "dims": dims, "R": R, "local_dims": ldims,
                        "global_dims": gdims, "parallelism": f"slab{world}" if world > 1 else "single",
-                       "l2": "flushed before every step (256 MiB memset outside the events)"},
+                       "l2": ("flushed before every step (256 MiB memset outside the events)" if flush_needed
+                              else "inputs larger than L2 (no flush)")},
             "gpu_launches": gpu_launches, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
@@ -336,14 +369,35 @@ def run_ours(args, cfg):
     return 0
 
 
-def cpu_baseline(args, cfg):
+def host_memory_ok(nbytes):
+    try:
+        import psutil
+        return psutil.virtual_memory().available > nbytes
+    except Exception:
+        return False
+
+
+def sample_dims(dims, dtype):
+    """Bounded CPU sample: the first k last-mode slices of the workload tensor
+    (fp32 configs are sampled; the fp64 configs run in full)."""
+    if dtype != "f32":
+        return list(dims)
+    return list(dims[:-1]) + [4]
+
+
+def cpu_baseline(args, cfg, ydev=None):
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as O
     dims, R, dtype, desc = cfg
-    n = int(np.prod(dims))
+    sd = sample_dims(dims, dtype)
+    n = int(np.prod(sd))
     cores = host_cores()
-    y = O.fill_normal(1, n, nthreads=cores)
-    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
+    if dtype == "f32":  # fp64 oracle on the upcast fp32 values
+        y = O.fill_upm1_f32(1, n, nthreads=cores).astype(np.float64)
+    else:
+        y = O.fill_normal(1, n, nthreads=cores)
+    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(sd)]
+    dims = sd
     O.cp_gradient_all(y, dims, f, nthreads=cores)
     reps, t0 = 0, time.perf_counter()
     while True:
@@ -352,8 +406,11 @@ def cpu_baseline(args, cfg):
         if time.perf_counter() - t0 > args.cpu_seconds:
             break
     dt = (time.perf_counter() - t0) / reps
-    return {"value": n * 8 / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
-            "sample": f"{reps} full {args.config} gradients (~{args.cpu_seconds:.0f} s), oracle/cpd_oracle.c OpenMP",
+    esize = 4 if dtype == "f32" else 8
+    what = "full" if sd == list(cfg[0]) else f"{'x'.join(map(str, sd))}-slab sample of the"
+    return {"value": n * esize / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{reps} {what} {args.config} gradients (~{args.cpu_seconds:.0f} s), "
+                      "oracle/cpd_oracle.c OpenMP (fp64 arithmetic)",
             "ms_per_step": dt * 1e3}
 
 
@@ -501,8 +558,8 @@ def run_ours_als(args, cfg):
 
     # e2e: a full run() through the host API with Y uploaded from pinned host memory
     e2e = None
-    if not args.no_e2e and world == 1:
-        host_y = torch.empty(slab, dtype=torch.float64).pin_memory()
+    if not args.no_e2e and world == 1 and host_memory_ok(3 * slab * esize):
+        host_y = torch.empty(slab, dtype=torch.float32 if f32 else torch.float64).pin_memory()
         host_y.copy_(torch.from_numpy(y.values()))
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()

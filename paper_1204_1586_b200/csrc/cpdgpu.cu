@@ -213,6 +213,9 @@ struct cpdgpu_tensor {
   bool sorted_ready = false;
   double norm2 = -1.0;
   uint64_t id = 0;
+  uint64_t version = 0;              // bumped whenever the values change
+  DevBuf yscale;                     // fp32: [float scale | double inv | uint amax] (seed_f32.cu)
+  uint64_t scale_version = ~0ull;
   size_t elem() const { return dtype == CPDGPU_F64 ? 8 : 4; }
   ~cpdgpu_tensor() {
     if (sorted && sorted != data) cudaFree(sorted);
@@ -237,6 +240,7 @@ struct Plan {
     std::unique_ptr<DevBuf> KRr, KRl;  // pre-built Khatri-Rao rows [K][LDK], [J][LDK]
     CUtensorMap kmap{};
     bool kmap_ok = false;
+    std::unique_ptr<DevBuf> KRr16, KRl16, scales;  // fp32 path: split tiles, [scale 128 | inv 128]
   };
   std::vector<Chunk> chunks;
   bool lpart_direct = false;  // one row block: the left partial is the seed itself
@@ -249,6 +253,20 @@ struct Plan {
   int slot_tab_ptr_len = 0;
   int slot_tab_max = 0;         // most slots any row block has
   HostBuf hF, hG;
+  // fp32 tensors: tcgen05 seed passes (seed_f32.cu), one per side
+  bool f32 = false;
+  const cpdgpu_tensor* tensor = nullptr;  // the tensor this plan belongs to
+  struct F32Pass {
+    int64_t nB = 0, nK = 0, U = 0;
+    int P = 0, slots = 0, tab_len = 0, tab_max = 0;
+    DevBuf tab;  // CSR of partial slots per output block
+  };
+  F32Pass fr, fl;
+  int64_t J8 = 0;               // J_p rounded up to 8 (3-D TMA view)
+  DevBuf ypad;                  // padded copy when J_p % 8 != 0
+  CUtensorMap ymap_r{}, ymap_l{};
+  const void* ymap_base = nullptr;
+  uint64_t ypad_version = ~0ull;
   DevBuf gtab;                              // device table of the N output pointers
   cudaGraph_t grad_graph = nullptr;         // hook-free gradient
   cudaGraphExec_t grad_exec = nullptr;
@@ -335,50 +353,31 @@ void ensure_sorted(cpdgpu_ctx* ctx, cpdgpu_tensor* t) {
 
 int pick_nt(int64_t Rc) { return static_cast<int>((Rc + 7) / 8); }
 
-Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
-  auto key = std::make_tuple(t->id, R, pivot);
-  auto it = ctx->plans.find(key);
-  if (it != ctx->plans.end()) return it->second.get();
-  if (t->dtype != CPDGPU_F64)
-    fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: fp32 tensors use the tensor-core path (not built in this library)");
-  auto holder = std::make_unique<Plan>();
-  Plan& pl = *holder;
-  pl.N = static_cast<int>(t->dims.size());
-  pl.R = R;
-  pl.raw_frame = pivot > 0;
-  if (pl.raw_frame) {  // slab shards: the caller's (global, sorted) frame as is
-    pl.perm.resize(pl.N);
-    for (int j = 0; j < pl.N; ++j) pl.perm[j] = j + 1;
-  } else {
-    pl.perm = t->perm;
+// CSR of partial slots per output block for a persistent launch: CTA c owns
+// units [c T / P, (c + 1) T / P) of unit = block * nCT + tile, one slot per block.
+void build_slot_tab(DevBuf& buf, int64_t nB, int64_t nCT, int64_t T, int P, int slots, int* ptr_len, int* tab_max) {
+  std::vector<std::vector<int>> per(static_cast<size_t>(nB));
+  for (int64_t c = 0; c < P; ++c) {
+    const int64_t a = c * T / P, b = (c + 1) * T / P;
+    if (a >= b) continue;
+    for (int64_t rb = a / nCT; rb <= (b - 1) / nCT; ++rb)
+      per[static_cast<size_t>(rb)].push_back(static_cast<int>(c * slots + (rb - a / nCT)));
   }
-  pl.sd.resize(pl.N);
-  for (int j = 0; j < pl.N; ++j) pl.sd[j] = t->dims[pl.perm[j] - 1];
-  pl.J = prefix(pl.sd);
-  pl.p = pivot > 0 ? pivot : select_pivot(pl.sd);
-  if (pl.p < 1 || pl.p > pl.N) fail(CPDGPU_ARGUMENT_ERROR, "pivot %d outside 1..%d", pl.p, pl.N);
-  pl.Jp = pl.J[pl.p];
-  pl.Kp = pl.J[pl.N] / pl.Jp;
-  pl.off_sorted.resize(pl.N);
-  pl.off_orig.resize(pl.N);
-  int64_t off = 0;
-  for (int m = 0; m < pl.N; ++m) {
-    pl.off_orig[m] = off;
-    off += t->dims[m] * R;
+  std::vector<int> tab(static_cast<size_t>(nB) + 1, 0);
+  int mx = 0;
+  for (int64_t rb = 0; rb < nB; ++rb) {
+    tab[rb + 1] = tab[rb] + static_cast<int>(per[rb].size());
+    mx = std::max(mx, static_cast<int>(per[rb].size()));
   }
-  pl.total_factor = off;
-  off = 0;
-  for (int j = 0; j < pl.N; ++j) {
-    pl.off_sorted[j] = off;
-    off += pl.sd[j] * R;
-  }
-  const size_t fbytes = static_cast<size_t>(pl.total_factor) * sizeof(double);
-  pl.Fs.ensure(fbytes);
-  pl.Forig.ensure(fbytes);
-  pl.Gorig.ensure(fbytes);
-  pl.hF.ensure(fbytes);
-  pl.hG.ensure(fbytes);
+  for (auto& v : per) tab.insert(tab.end(), v.begin(), v.end());
+  buf.ensure(tab.size() * sizeof(int));
+  CK(cudaMemcpy(buf.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+  *ptr_len = static_cast<int>(nB) + 1;
+  *tab_max = mx;
+}
 
+void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
+  const int64_t R = pl.R;
   // K1 geometry
   const int64_t Jp = pl.Jp, Kp = pl.Kp;
   // Row block TI: multiple of 8 (DMMA fragments) and == 8 (mod 16) so the dense
@@ -452,25 +451,103 @@ Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
     pl.chunks.push_back(std::move(c));
   }
   pl.Rpart.ensure(rpart * sizeof(double));
-  {  // slot table: CTA c owns tiles [c T / P, (c + 1) T / P) and one slot per row block it touches
-    std::vector<std::vector<int>> per(static_cast<size_t>(nRB));
-    for (int64_t c = 0; c < P; ++c) {
-      const int64_t a = c * T / P, b = (c + 1) * T / P;
-      if (a >= b) continue;
-      for (int64_t rb = a / nCT; rb <= (b - 1) / nCT; ++rb)
-        per[static_cast<size_t>(rb)].push_back(static_cast<int>(c * slots + (rb - a / nCT)));
-    }
-    std::vector<int> tab(static_cast<size_t>(nRB) + 1, 0);
-    for (int64_t rb = 0; rb < nRB; ++rb) {
-      tab[rb + 1] = tab[rb] + static_cast<int>(per[rb].size());
-      pl.slot_tab_max = std::max(pl.slot_tab_max, static_cast<int>(per[rb].size()));
-    }
-    for (auto& v : per) tab.insert(tab.end(), v.begin(), v.end());
-    pl.slot_tab.ensure(tab.size() * sizeof(int));
-    CK(cudaMemcpy(pl.slot_tab.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
-    pl.slot_tab_ptr_len = static_cast<int>(nRB) + 1;
-  }
+  build_slot_tab(pl.slot_tab, nRB, nCT, T, P, slots, &pl.slot_tab_ptr_len, &pl.slot_tab_max);
   if (!pl.lpart_direct) pl.Lpart.ensure(lpart * sizeof(double));
+}
+
+// fp32 tensors: one tcgen05 pass per seed, 64 rank columns per chunk.
+void build_f32_geometry(cpdgpu_ctx* ctx, Plan& pl) {
+  pl.f32 = true;
+  pl.lpart_direct = false;
+  const int64_t Jp = pl.Jp, Kp = pl.Kp;
+  const int RPc = cpdgpu::seed_f32_rank_cols();
+  pl.J8 = (Jp + 7) / 8 * 8;
+  auto pass = [&](Plan::F32Pass& f, int64_t rows, int64_t kdim) {
+    f.nB = cpdgpu::ceil_div(rows, 128);
+    f.nK = cpdgpu::ceil_div(kdim, 64);
+    f.U = f.nB * f.nK;
+    f.P = static_cast<int>(std::min<int64_t>(ctx->num_sms, f.U));
+    f.slots = static_cast<int>(cpdgpu::ceil_div(cpdgpu::ceil_div(f.U, f.P), f.nK) + 1);
+    build_slot_tab(f.tab, f.nB, f.nK, f.U, f.P, f.slots, &f.tab_len, &f.tab_max);
+  };
+  pass(pl.fr, Jp, Kp);
+  pass(pl.fl, Kp, Jp);
+  size_t rpart = 0, lpart = 0;
+  for (int64_t r0 = 0; r0 < pl.R; r0 += RPc) {
+    Plan::Chunk c;
+    c.r0 = static_cast<int>(r0);
+    c.Rc = static_cast<int>(std::min<int64_t>(RPc, pl.R - r0));
+    c.NT = RPc / 8;
+    c.sp = cpdgpu::SeedParams{};
+    c.sp.LDK = RPc;
+    c.KRr = std::make_unique<DevBuf>();
+    c.KRl = std::make_unique<DevBuf>();
+    c.KRr16 = std::make_unique<DevBuf>();
+    c.KRl16 = std::make_unique<DevBuf>();
+    c.scales = std::make_unique<DevBuf>();
+    c.KRr->ensure(static_cast<size_t>(Kp) * RPc * sizeof(double));
+    c.KRl->ensure(static_cast<size_t>(Jp) * RPc * sizeof(double));
+    c.KRr16->ensure(static_cast<size_t>(pl.fr.nK * cpdgpu::seed_f32_tile_bytes()));
+    c.KRl16->ensure(static_cast<size_t>(pl.fl.nK * cpdgpu::seed_f32_tile_bytes()));
+    c.scales->ensure(4 * RPc * sizeof(double));
+    c.rpart_off = static_cast<int64_t>(rpart);
+    c.lpart_off = static_cast<int64_t>(lpart);
+    rpart += static_cast<size_t>(pl.fr.P) * pl.fr.slots * RPc * 128;
+    lpart += static_cast<size_t>(pl.fl.P) * pl.fl.slots * RPc * 128;
+    pl.chunks.push_back(std::move(c));
+  }
+  pl.Rpart.ensure(rpart * sizeof(double));
+  pl.Lpart.ensure(lpart * sizeof(double));
+}
+
+Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
+  auto key = std::make_tuple(t->id, R, pivot);
+  auto it = ctx->plans.find(key);
+  if (it != ctx->plans.end()) return it->second.get();
+  auto holder = std::make_unique<Plan>();
+  Plan& pl = *holder;
+  pl.N = static_cast<int>(t->dims.size());
+  pl.R = R;
+  pl.tensor = t;
+  pl.raw_frame = pivot > 0;
+  if (pl.raw_frame) {  // slab shards: the caller's (global, sorted) frame as is
+    pl.perm.resize(pl.N);
+    for (int j = 0; j < pl.N; ++j) pl.perm[j] = j + 1;
+  } else {
+    pl.perm = t->perm;
+  }
+  pl.sd.resize(pl.N);
+  for (int j = 0; j < pl.N; ++j) pl.sd[j] = t->dims[pl.perm[j] - 1];
+  pl.J = prefix(pl.sd);
+  pl.p = pivot > 0 ? pivot : select_pivot(pl.sd);
+  if (pl.p < 1 || pl.p > pl.N) fail(CPDGPU_ARGUMENT_ERROR, "pivot %d outside 1..%d", pl.p, pl.N);
+  pl.Jp = pl.J[pl.p];
+  pl.Kp = pl.J[pl.N] / pl.Jp;
+  pl.off_sorted.resize(pl.N);
+  pl.off_orig.resize(pl.N);
+  int64_t off = 0;
+  for (int m = 0; m < pl.N; ++m) {
+    pl.off_orig[m] = off;
+    off += t->dims[m] * R;
+  }
+  pl.total_factor = off;
+  off = 0;
+  for (int j = 0; j < pl.N; ++j) {
+    pl.off_sorted[j] = off;
+    off += pl.sd[j] * R;
+  }
+  const size_t fbytes = static_cast<size_t>(pl.total_factor) * sizeof(double);
+  pl.Fs.ensure(fbytes);
+  pl.Forig.ensure(fbytes);
+  pl.Gorig.ensure(fbytes);
+  pl.hF.ensure(fbytes);
+  pl.hG.ensure(fbytes);
+
+  if (t->dtype == CPDGPU_F32)
+    build_f32_geometry(ctx, pl);
+  else
+    build_f64_geometry(ctx, pl);
+  const int64_t Jp = pl.Jp, Kp = pl.Kp;
   pl.Rs.ensure(static_cast<size_t>(Jp * R) * sizeof(double));
   pl.Ls.ensure(static_cast<size_t>(Kp * R) * sizeof(double));
   pl.Rtmp.ensure(static_cast<size_t>(Jp * R) * sizeof(double));
@@ -484,7 +561,43 @@ Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
   return raw;
 }
 
-void bind_seed_inputs(Plan& pl, cpdgpu_tensor* t) {
+// fp32: power-of-two Y scale (cached per tensor version), rows padded to a
+// multiple of 8 when needed, and the two 3-D TMA views.  Runs eagerly.
+void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
+  const float* src = static_cast<const float*>(pl.raw_frame ? t->data : t->sorted);
+  if (t->scale_version != t->version) {
+    t->yscale.ensure(32);
+    char* b = static_cast<char*>(t->yscale.p);
+    ctx->launches += cpdgpu::launch_y_scale(static_cast<const float*>(t->data), t->numel,
+                                            reinterpret_cast<unsigned int*>(b + 16), reinterpret_cast<float*>(b),
+                                            reinterpret_cast<double*>(b + 8), ctx->num_sms, ctx->stream);
+    CK(cudaGetLastError());
+    t->scale_version = t->version;
+  }
+  const void* base = src;
+  if (pl.J8 != pl.Jp) {
+    if (pl.ypad_version != t->version || !pl.ypad.p) {
+      pl.ypad.ensure(static_cast<size_t>(pl.J8 * pl.Kp) * sizeof(float));
+      ctx->launches += cpdgpu::launch_pad_rows_f32(src, static_cast<float*>(pl.ypad.p), pl.Jp, pl.J8, pl.Kp,
+                                                   ctx->num_sms, ctx->stream);
+      CK(cudaGetLastError());
+      pl.ypad_version = t->version;
+    }
+    base = pl.ypad.p;
+  }
+  if (pl.ymap_base != base) {
+    if (!cpdgpu::make_tensor_map_y32(&pl.ymap_r, base, pl.J8, pl.Kp, 0) ||
+        !cpdgpu::make_tensor_map_y32(&pl.ymap_l, base, pl.J8, pl.Kp, 1))
+      fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: fp32 tensor view not addressable by TMA");
+    pl.ymap_base = base;
+  }
+}
+
+void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
+  if (pl.f32) {
+    bind_f32_inputs(ctx, pl, t);
+    return;
+  }
   const void* ybase = pl.raw_frame ? t->data : t->sorted;
   bool tma = pl.tma_ok;
   if (tma && pl.tmap_base != ybase) {
@@ -518,7 +631,47 @@ cudaEvent_t seed_event(cpdgpu_ctx* ctx) {
 
 // K1 seed contraction(s).  mode 1: right seed, 2: left seed, 3: both (one HBM pass).
 // The Khatri-Rao rows must already be in the chunks' KRr / KRl buffers.
+// fp32 seeds: Khatri-Rao column scales and split tiles from the sorted factors
+// (Fs), then one tcgen05 pass per requested side.
+void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) {
+  cudaStream_t s = ctx->stream;
+  const int RPc = cpdgpu::seed_f32_rank_cols();
+  const char* yb = static_cast<const char*>(t->yscale.p);
+  for (auto& c : pl.chunks) {
+    double* sc = c.scales->d();
+    ctx->launches += cpdgpu::launch_kr_scale(pl.spec(pl.p + 1, pl.N, c.r0), pl.spec(1, pl.p, c.r0), c.Rc, sc,
+                                             sc + 2 * RPc, s);
+    if (mode & 1)
+      ctx->launches += cpdgpu::launch_kr_split(c.KRr->d(), pl.Kp, RPc, sc, c.KRr16->p, s);
+    if (mode & 2)
+      ctx->launches += cpdgpu::launch_kr_split(c.KRl->d(), pl.Jp, RPc, sc + RPc, c.KRl16->p, s);
+    for (int side = 0; side < 2; ++side) {
+      if (!(mode & (1 << side))) continue;
+      const Plan::F32Pass& f = side ? pl.fl : pl.fr;
+      cpdgpu::Seed32Params q{};
+      q.kr_tiles = static_cast<const unsigned char*>(side ? c.KRl16->p : c.KRr16->p);
+      q.scale_y = reinterpret_cast<const float*>(yb);
+      q.inv_scale_y = reinterpret_cast<const double*>(yb + 8);
+      q.inv_scale_kr = sc + 2 * RPc + side * RPc;
+      q.part = (side ? pl.Lpart.d() + c.lpart_off : pl.Rpart.d() + c.rpart_off);
+      q.nK = f.nK;
+      q.units = f.U;
+      q.P = f.P;
+      q.slots = f.slots;
+      q.chunk = 4;
+      if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+      ctx->launches += cpdgpu::launch_seed_f32(q, side ? &pl.ymap_l : &pl.ymap_r, side, s);
+      if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+    }
+  }
+  CK(cudaGetLastError());
+}
+
 void run_seeds(cpdgpu_ctx* ctx, Plan& pl, int mode) {
+  if (pl.f32) {
+    run_seeds_f32(ctx, pl, mode, pl.tensor);
+    return;
+  }
   cudaStream_t s = ctx->stream;
   static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
   for (auto& c : pl.chunks) {
@@ -637,6 +790,25 @@ cpdgpu::TailOp op_base(int type, int R) {
 
 // Seed-partial reductions for the given seed mode.
 void add_reduce_ops(const Plan& pl, cpdgpu::TailStep& st, int mode) {
+  if (pl.f32) {  // both sides: per-CTA fp64 partial blocks [slot][64][128]
+    for (const auto& c : pl.chunks)
+      for (int side = 0; side < 2; ++side) {
+        if (!(mode & (1 << side))) continue;
+        const Plan::F32Pass& f = side ? pl.fl : pl.fr;
+        cpdgpu::TailOp o = op_base(cpdgpu::kOpReduceRight, c.Rc);
+        o.Z = side ? pl.Lpart.d() + c.lpart_off : pl.Rpart.d() + c.rpart_off;
+        o.B = f.tab_max >= 16 ? 1 : 0;
+        o.M = side ? pl.Kp : pl.Jp;
+        o.RP = cpdgpu::seed_f32_rank_cols();
+        o.TI = 128;
+        o.rb_ptr = static_cast<const int*>(f.tab.p);
+        o.slot_list = static_cast<const int*>(f.tab.p) + f.tab_len;
+        o.out = (side ? pl.Ls.d() : pl.Rs.d()) + static_cast<int64_t>(c.r0) * o.M;
+        o.ldo = o.M;
+        st.op[st.n++] = o;
+      }
+    return;
+  }
   for (const auto& c : pl.chunks) {
     if (mode & 1) {
       cpdgpu::TailOp o = op_base(cpdgpu::kOpReduceRight, c.Rc);
@@ -1114,6 +1286,7 @@ int cpdgpu_tensor_update(cpdgpu_ctx* ctx, cpdgpu_tensor* t, const void* host) {
     CK(cudaMemcpyAsync(t->data, host, static_cast<size_t>(t->numel) * t->elem(), cudaMemcpyHostToDevice,
                        ctx->stream));
     t->norm2 = -1.0;
+    ++t->version;
     if (!t->identity && t->sorted_ready) {  // refresh the sorted copy lazily
       cudaFree(t->sorted);
       t->sorted = nullptr;
@@ -1194,6 +1367,7 @@ int cpdgpu_tensor_axpby_kruskal(cpdgpu_ctx* ctx, cpdgpu_tensor* t, double alpha,
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     t->norm2 = -1.0;
+    ++t->version;
     t->sorted_ready = t->identity ? t->sorted_ready : false;
     if (!t->identity && t->sorted) {
       cudaFree(t->sorted);
@@ -1289,7 +1463,7 @@ int cpdgpu_cp_gradient_all(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const d
     if (!factors || !gradients) fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: null factor or gradient list");
     ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, 0);
-    bind_seed_inputs(pl, y);
+    bind_seed_inputs(ctx, pl, y);
     upload_host_factors(ctx, pl, y, factors);
     run_gradient(ctx, pl, pl.Forig.d(), pl.Gorig.d());
     CK(cudaMemcpyAsync(pl.hG.d(), pl.Gorig.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
@@ -1312,7 +1486,7 @@ int cpdgpu_cp_gradient_all_hook(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, do
     if (!factors || !gradients) fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: null factor or gradient list");
     ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, 0);
-    bind_seed_inputs(pl, y);
+    bind_seed_inputs(ctx, pl, y);
     upload_host_factors(ctx, pl, y, factors);
     gather_factors(ctx, pl, pl.Forig.d());
     set_gtab(ctx, pl, pl.Gorig.d());
@@ -1347,7 +1521,7 @@ int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, 
       fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: pivot %d outside 0..%zu", pivot, y->dims.size());
     if (pivot == 0) ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, pivot);
-    bind_seed_inputs(pl, y);
+    bind_seed_inputs(ctx, pl, y);
     run_gradient(ctx, pl, factors_dev, gradients_dev);
     CK(cudaGetLastError());
   });
@@ -1418,7 +1592,7 @@ int cpdgpu_als_sweep(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const
     if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "als_sweep_fast: rank above the device ALS limit 64");
     ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, 0);
-    bind_seed_inputs(pl, y);
+    bind_seed_inputs(ctx, pl, y);
     upload_host_factors(ctx, pl, y, factors);
     prepare_als(ctx, pl, y);
     pl.costs.ensure(sizeof(double));
@@ -1446,7 +1620,7 @@ int cpdgpu_als_run(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* 
     if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "run: rank above the device ALS limit 64");
     ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, 0);
-    bind_seed_inputs(pl, y);
+    bind_seed_inputs(ctx, pl, y);
     upload_host_factors(ctx, pl, y, factors);
     prepare_als(ctx, pl, y);
     pl.costs.ensure(static_cast<size_t>(max_iters) * sizeof(double));

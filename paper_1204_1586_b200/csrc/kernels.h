@@ -48,6 +48,36 @@ int launch_seed_f64(const SeedParams& p, const CUtensorMap* tmap, const CUtensor
 bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, int elem_bytes,
                         uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1);
 
+// ---- K1 for fp32 tensors: tcgen05 split-fp16 seed contraction (seed_f32.cu) ---
+// One pass computes ONE seed (right: blocks over the view's rows i, k-tiles over
+// columns j; left: blocks over columns j, k-tiles over rows i) for up to 64 rank
+// columns.  CTA c owns units [c U / P, (c + 1) U / P) of unit = block * nK + tile
+// and writes one fp64 partial [64][128] per block it touches (slot c * slots + s).
+struct Seed32Params {
+  const unsigned char* kr_tiles;  // [nK][16 KB] scaled fp16 hi / lo Khatri-Rao tiles
+  const float* scale_y;           // [1] power-of-two Y scale
+  const double* inv_scale_y;      // [1]
+  const double* inv_scale_kr;     // [64] Khatri-Rao column unscales of this side
+  double* part;                   // [P * slots][64][128]
+  int64_t nK, units;
+  int P, slots, chunk;
+};
+size_t seed_f32_smem_bytes();
+int seed_f32_rank_cols();         // 64
+int64_t seed_f32_tile_bytes();    // bytes of one Khatri-Rao tile (64 rows)
+int launch_seed_f32(const Seed32Params& p, const CUtensorMap* ymap, int left, cudaStream_t s);
+// column scales of the right (scale[0..63]) and left (scale[64..127]) Khatri-Rao rows
+int launch_kr_scale(const KRSpec& right, const KRSpec& left, int R, double* scale, double* inv, cudaStream_t s);
+// fp64 rows [L][ld] (ld <= 64) -> tiles (see Seed32Params::kr_tiles)
+int launch_kr_split(const double* rows, int64_t L, int ld, const double* scale, void* tiles, cudaStream_t s);
+int launch_y_scale(const float* y, int64_t n, unsigned int* amax_scratch, float* scale, double* inv, int num_sms,
+                   cudaStream_t s);
+int launch_pad_rows_f32(const float* src, float* dst, int64_t J, int64_t J8, int64_t K, int num_sms,
+                        cudaStream_t s);
+// 2-D map of a J8 x K column-major fp32 matrix; box for the right (128 i x 64 j)
+// or left (64 i x 128 j) pass.  J8 % 8 == 0.
+bool make_tensor_map_y32(CUtensorMap* out, const void* base, int64_t J8, int64_t K, int left);
+
 // ---- prologue + recursion tail (tail.cu) ------------------------------------
 enum TailOpType { kOpNone = 0, kOpContractA = 1, kOpContractB = 2, kOpReduceRight = 3, kOpReduceLeft = 4 };
 

@@ -1,0 +1,533 @@
+// seed_f32.cu — the split-point seed contractions for fp32 tensors on the
+// 5th-generation tensor cores (tcgen05.mma kind::f16, accumulators in TMEM).
+//
+//   right pass  Rs[i, r] = sum_j Y[i + J j] KR(p+1..N)[j, r]   (mttkrp.cpp:149-163)
+//   left pass   Ls[j, r] = sum_i Y[i + J j] KR(1..p)[i, r]     (mttkrp.cpp:195-210)
+//
+// fp32 accuracy from fp16 tensor cores: every operand x is split into
+// x_hi = fp16(x) and x_lo = fp16(x - x_hi) (22 significant bits together), and
+// a product is the three MMAs hi*hi + lo*hi + hi*lo accumulated in fp32 in TMEM
+// (the dropped lo*lo term is ~2^-22 relative).  Y and every Khatri-Rao column
+// are scaled by powers of two into [-1, 1] first (exact), and the fp32 TMEM
+// accumulator is drained into fp64 registers every `chunk` k-tiles, so the
+// long K = 90000 sums of config 5 keep ~1e-7 relative accuracy.
+//
+// One CTA per SM (persistent), 320 threads:
+//   warp 8      producer: 2-D TMA of the fp32 Y tile (512 B / 256 B rows) + one
+//               bulk copy of the pre-split Khatri-Rao tile per stage
+//   warps 0-7   split each Y tile into fp16 hi and lo operand tiles laid out as
+//               128B-swizzled core-matrix atoms (MN-major for the right product,
+//               A = Y: M = i; K-major for the left product, A = Y^T: M = j), then
+//               drain the TMEM accumulators into fp64 registers (warp w: TMEM
+//               lanes 32 (w % 4).., rank columns 32 (w / 4)..) and write the
+//               per-CTA partial rows
+//   warp 9      allocates TMEM and issues the MMAs (one elected lane)
+//
+// Y tiles arrive as plain column-major boxes (right: 128 i x 64 j, left: 64 i x
+// 128 j), so every TMA row is a 512 / 256 B run; the split writes the fp16
+// operands in the layouts the MMA reads with 128-byte swizzling, which keeps both
+// the fp32 row reads and the fp16 atom writes free of bank conflicts.
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.h"
+
+namespace cpdgpu {
+namespace {
+
+constexpr int kBK = 64;             // K extent of one stage (j for right, i for left)
+constexpr int kBM = 128;            // output rows per block (MMA M)
+constexpr int kRP = 64;             // rank columns per pass (MMA N)
+constexpr int kYTile = kBK * kBM * 4;           // fp32 tile bytes (32 KB)
+constexpr int kKTile = 2 * kBK * kRP * 2;       // fp16 hi + lo Khatri-Rao tile (16 KB)
+constexpr int kStages = 3;          // raw ring (Y fp32 + Khatri-Rao tile)
+constexpr int kConv = 2;            // split operand ring (fp16 hi + lo)
+constexpr int kConvTile = kBK * kBM * 2 * 2;    // 32 KB
+constexpr int kSplitWarps = 8;
+constexpr int kThreads = (kSplitWarps + 2) * 32;
+constexpr int kTmemCols = 2 * kRP;  // double-buffered accumulator
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// tcgen05 shared-memory matrix descriptor: start, leading- and stride-dimension
+// byte offsets, descriptor version 1 (sm_100), layout type (0: interleaved core
+// matrices of 8 rows x 16 B, 2: 128-byte swizzle atoms of 8 rows x 128 B).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = 0) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (static_cast<uint64_t>(layout) << 61);
+}
+constexpr uint32_t kSwizzle128 = 2;  // layout type SWIZZLE_128B
+// Instruction descriptor, kind::f16: fp16 A and B, fp32 D, M = 128, N = kRP.
+__host__ __device__ constexpr uint32_t umma_idesc(bool a_mn_major) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((a_mn_major ? 1u : 0u) << 15) | (0u << 16) |
+         (static_cast<uint32_t>(kRP >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(r[c]);
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// x -> (fp16 hi, fp16 lo) of 2 values, packed
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  hi = pack_half2(a, b);
+  const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+  lo = pack_half2(a - back.x, b - back.y);
+}
+
+// Right pass: raw tile [64 j][128 i] fp32 (512 B rows) -> MN-major SW128 atoms
+// (8 j-rows x 64 i): atom (k-group j / 8, MN half i / 64) at ((j / 8) * 2 + i / 64) KB,
+// row j % 8 at 128 B, 16-B chunk (i % 64) / 8 XOR (j % 8).  Warp w: rows w, w + 8, ...
+template <bool SCALE>
+__device__ __forceinline__ void split_right(const unsigned char* raw, unsigned char* hi, unsigned char* lo, float sy,
+                                            int warp, int lane) {
+  const int ma = lane >> 4, c = (lane & 15) >> 1, half = lane & 1;
+#pragma unroll 4
+  for (int j = warp; j < kBK; j += kSplitWarps) {
+    float4 v = *reinterpret_cast<const float4*>(raw + j * 512 + lane * 16);
+    if (SCALE) {
+      v.x *= sy; v.y *= sy; v.z *= sy; v.w *= sy;
+    }
+    uint2 h, l;
+    split2(v.x, v.y, h.x, l.x);
+    split2(v.z, v.w, h.y, l.y);
+    const int r = j & 7;
+    const int off = ((j >> 3) * 2 + ma) * 1024 + r * 128 + ((c ^ r) << 4) + half * 8;
+    *reinterpret_cast<uint2*>(hi + off) = h;
+    *reinterpret_cast<uint2*>(lo + off) = l;
+  }
+}
+// Left pass: raw tile [128 j][64 i] fp32 (256 B rows) -> K-major SW128 atoms
+// (8 j-rows x 64 i): atom j / 8 at (j / 8) KB, row j % 8, chunk i / 8 XOR (j % 8).
+template <bool SCALE>
+__device__ __forceinline__ void split_left(const unsigned char* raw, unsigned char* hi, unsigned char* lo, float sy,
+                                           int warp, int lane) {
+  const int c = lane >> 2, q = lane & 3;
+#pragma unroll 4
+  for (int j = warp; j < kBM; j += kSplitWarps) {
+    float2 v = *reinterpret_cast<const float2*>(raw + j * 256 + lane * 8);
+    if (SCALE) {
+      v.x *= sy; v.y *= sy;
+    }
+    uint32_t h, l;
+    split2(v.x, v.y, h, l);
+    const int r = j & 7;
+    const int off = (j >> 3) * 1024 + r * 128 + ((c ^ r) << 4) + q * 4;
+    *reinterpret_cast<uint32_t*>(hi + off) = h;
+    *reinterpret_cast<uint32_t*>(lo + off) = l;
+  }
+}
+
+// Walk of one CTA's units [a, a + n) (unit = block * nK + k-tile): segment
+// (one output block) and chunk (fp32 accumulation window) boundaries.
+struct Walk {
+  int64_t a, nK;
+  int chunk;
+  __device__ bool seg_start(int64_t k) const { return k == 0 || (a + k) % nK == 0; }
+};
+
+template <int LEFT>
+__global__ void __launch_bounds__(kThreads, 1)
+    seed_f32_kernel(const Seed32Params p, const __grid_constant__ CUtensorMap ymap) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cta = blockIdx.x;
+  const int64_t a = static_cast<int64_t>(cta) * p.units / p.P;
+  const int64_t b = static_cast<int64_t>(cta + 1) * p.units / p.P;
+  const int n = static_cast<int>(b - a);
+  const Walk w{a, p.nK, p.chunk};
+  constexpr int kProducer = kSplitWarps, kMma = kSplitWarps + 1;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* conv = base;                            // [kConv][hi 16 KB | lo 16 KB], 1 KB atoms
+  unsigned char* ytiles = conv + kConv * kConvTile;      // [kStages][32 KB] fp32
+  unsigned char* ktiles = ytiles + kStages * kYTile;     // [kStages][16 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ktiles + kStages * kKTile);
+  uint64_t* full = bars;                   // raw stage landed          (1 + tx)
+  uint64_t* empty = full + kStages;        // raw stage consumed        (MMA commit)
+  uint64_t* cfull = empty + kStages;       // split operands ready      (8 warps)
+  uint64_t* cempty = cfull + kConv;        // split operands consumed   (MMA commit)
+  uint64_t* accfull = cempty + kConv;      // [2] chunk accumulated     (commit)
+  uint64_t* accempty = accfull + 2;        // [2] chunk drained         (8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+  double* unscale = reinterpret_cast<double*>(tmem_slot + 2);  // [kRP]
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int c = 0; c < kConv; ++c) {
+      mbar_init(&cfull[c], kSplitWarps);
+      mbar_init(&cempty[c], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&accfull[q], 1);
+      mbar_init(&accempty[q], kSplitWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (tid < kRP) unscale[tid] = p.inv_scale_y[0] * p.inv_scale_kr[tid];
+  if (warp == kMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (warp == kProducer && lane == 0)
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&ymap)));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProducer) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (int k = 0; k < n; ++k) {
+        const int s = k % kStages;
+        if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
+        const int64_t u = a + k, blk = u / p.nK, t = u - blk * p.nK;
+        mbar_arrive_tx(&full[s], kYTile + kKTile);
+        if (LEFT)  // rows i in [64 t, +64), columns j in [128 blk, +128)
+          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(t * kBK), static_cast<int>(blk * kBM), &full[s]);
+        else       // rows i in [128 blk, +128), columns j in [64 t, +64)
+          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(blk * kBM), static_cast<int>(t * kBK), &full[s]);
+        bulk_load(ktiles + s * kKTile, p.kr_tiles + t * kKTile, kKTile, &full[s]);
+      }
+    }
+  } else if (warp == kMma) {
+    // ------------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc(!LEFT);
+    // A: right = MN-major SW128 (LBO: next 64 i = 1 KB, SBO: next 8 j = 2 KB, +4 KB per 16 j);
+    //    left  = K-major SW128  (SBO: next 8 j = 1 KB, +32 B per 16 i inside the atom)
+    constexpr uint32_t a_lbo = LEFT ? 16 : 1024, a_sbo = LEFT ? 1024 : 2048, a_kstep = LEFT ? 32 : 4096;
+    // B (Khatri-Rao, K-major interleaved): SBO next 8 r = 128 B, LBO next 8 K = kRP * 16 B
+    constexpr uint32_t b_lbo = kRP * 16, b_sbo = 128, b_kstep = 2 * kRP * 16, b_lo = kBK * kRP * 2;
+    int q = -1, pos = 0;
+    for (int k = 0; k < n; ++k) {
+      const int s = k % kStages, c = k % kConv;
+      if (w.seg_start(k) || pos == w.chunk) {  // new accumulation chunk
+        ++q;
+        pos = 0;
+        if (q >= 2) {
+          mbar_wait(&accempty[q & 1], ((q >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+      }
+      mbar_wait(&cfull[c], (k / kConv) & 1);  // implies the raw stage landed
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t d = tmem + static_cast<uint32_t>((q & 1) * kRP);
+        const uint32_t ha = smem_u32(conv + c * kConvTile), la = ha + kConvTile / 2;
+        const uint32_t kb = smem_u32(ktiles + s * kKTile);
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks) {
+          const uint64_t ahi = umma_desc(ha + ks * a_kstep, a_lbo, a_sbo, kSwizzle128);
+          const uint64_t alo = umma_desc(la + ks * a_kstep, a_lbo, a_sbo, kSwizzle128);
+          const uint64_t bhi = umma_desc(kb + ks * b_kstep, b_lbo, b_sbo);
+          const uint64_t blo = umma_desc(kb + b_lo + ks * b_kstep, b_lbo, b_sbo);
+          umma_f16(d, ahi, bhi, idesc, (pos > 0 || ks > 0) ? 1u : 0u);
+          umma_f16(d, alo, bhi, idesc, 1u);
+          umma_f16(d, ahi, blo, idesc, 1u);
+        }
+        umma_commit(&empty[s]);
+        umma_commit(&cempty[c]);
+      }
+      __syncwarp();
+      ++pos;
+      const bool chunk_end = (k == n - 1) || w.seg_start(k + 1) || pos == w.chunk;
+      if (chunk_end && lane == 0) umma_commit(&accfull[q & 1]);
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------------ split + drain
+    double acc[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+    const float sy = p.scale_y[0];
+    const bool scale = sy != 1.0f;
+    const int sp = warp & 3, colh = warp >> 2;  // TMEM lane quarter, rank-column half
+    const uint32_t lane_base = static_cast<uint32_t>(sp * 32) << 16;
+    int q = -1, pos = 0, seg = -1;
+    int pend_q = -1, pend_k = -1, pend_seg = -1;
+    bool pend_last = false;
+    for (int k = 0; k <= n; ++k) {
+      if (k < n) {
+        const int s = k % kStages, c = k % kConv;
+        if (w.seg_start(k)) ++seg;
+        if (w.seg_start(k) || pos == w.chunk) {
+          ++q;
+          pos = 0;
+        }
+        mbar_wait(&full[s], (k / kStages) & 1);
+        if (k >= kConv) mbar_wait(&cempty[c], ((k / kConv) - 1) & 1);
+        unsigned char* hi = conv + c * kConvTile;
+        const unsigned char* raw = ytiles + s * kYTile;
+        if (LEFT) {
+          if (scale) split_left<true>(raw, hi, hi + kConvTile / 2, sy, warp, lane);
+          else split_left<false>(raw, hi, hi + kConvTile / 2, sy, warp, lane);
+        } else {
+          if (scale) split_right<true>(raw, hi, hi + kConvTile / 2, sy, warp, lane);
+          else split_right<false>(raw, hi, hi + kConvTile / 2, sy, warp, lane);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cfull[c]);
+      }
+      // drain the previous chunk one stage late, so the MMAs of this stage overlap it
+      if (pend_q >= 0 && pend_k < k) {
+        mbar_wait(&accfull[pend_q & 1], (pend_q >> 1) & 1);
+        tc_fence_after();
+        float v[32];
+        tmem_ld32(tmem + lane_base + static_cast<uint32_t>((pend_q & 1) * kRP + colh * 32), v);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] += static_cast<double>(v[c]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&accempty[pend_q & 1]);
+        if (pend_last) {  // block segment finished: unscaled fp64 partial rows
+          double* out = p.part + (static_cast<int64_t>(cta) * p.slots + pend_seg) * kRP * kBM +
+                        static_cast<int64_t>(colh * 32) * kBM + sp * 32 + lane;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            out[c * kBM] = acc[c] * unscale[colh * 32 + c];
+            acc[c] = 0.0;
+          }
+        }
+        pend_q = -1;
+      }
+      if (k < n) {
+        ++pos;
+        const bool seg_end = (k == n - 1) || w.seg_start(k + 1);
+        if (seg_end || pos == w.chunk) {
+          pend_q = q;
+          pend_k = k;
+          pend_last = seg_end;
+          pend_seg = seg;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMma) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// ---- Khatri-Rao operand preparation ----------------------------------------------
+
+// Power-of-two column scales: max_x |KR[x, r]| = prod_m max_i |A_m[i, r]| (the
+// Khatri-Rao product runs over every index combination), scaled into [0.5, 1).
+__global__ void kr_scale_kernel(const KRSpec right, const KRSpec left, int R, double* scale, double* inv) {
+  const int r = threadIdx.x;
+  if (r >= kRP) return;
+  for (int side = 0; side < 2; ++side) {
+    const KRSpec& s = side == 0 ? right : left;
+    double bound = r < R ? 1.0 : 0.0;
+    for (int m = 0; m < s.n && r < R; ++m) {
+      double mx = 0.0;
+      for (int64_t i = 0; i < s.dims[m]; ++i) mx = fmax(mx, fabs(s.A[m][i + s.dims[m] * r]));
+      bound *= mx;
+    }
+    int e = 0;
+    if (bound > 0.0 && isfinite(bound)) frexp(bound, &e);
+    scale[side * kRP + r] = ldexp(1.0, -e);
+    inv[side * kRP + r] = ldexp(1.0, e);
+  }
+}
+
+// fp64 Khatri-Rao rows [L][ld] -> scaled fp16 hi / lo tiles laid out as the
+// K-major B operand: tile t = rows [64 t, 64 t + 64): [piece][j8][r8][8 r][8 j].
+__global__ void kr_split_kernel(const double* __restrict__ rows, int64_t L, int ld, const double* __restrict__ scale,
+                                __half* __restrict__ tiles, int64_t ntiles) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // (t, j8, r8, rr)
+  if (e >= ntiles * 8 * (kRP / 8) * 8) return;
+  const int rr = static_cast<int>(e & 7);
+  const int r8 = static_cast<int>((e >> 3) % (kRP / 8));
+  const int64_t rest = (e >> 3) / (kRP / 8);
+  const int j8 = static_cast<int>(rest & 7);
+  const int64_t t = rest >> 3;
+  const int r = r8 * 8 + rr;
+  const double sc = scale[r];
+  __half hi[8], lo[8];
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int64_t j = t * kBK + j8 * 8 + jj;
+    const double x = (j < L && r < ld) ? rows[j * ld + r] * sc : 0.0;
+    hi[jj] = __double2half(x);
+    lo[jj] = __double2half(x - static_cast<double>(__half2float(hi[jj])));
+  }
+  __half* dst = tiles + t * (kKTile / 2) + (static_cast<int64_t>(j8) * (kRP / 8) + r8) * 64 + rr * 8;
+  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hi);
+  *reinterpret_cast<uint4*>(dst + kBK * kRP) = *reinterpret_cast<const uint4*>(lo);
+}
+
+// Y scale: power of two taking max |Y| into [0.5, 1).
+__global__ void absmax_f32_kernel(const float* __restrict__ y, int64_t n, unsigned int* out) {
+  float m = 0.0f;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = fmaxf(m, fabsf(y[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+__global__ void y_scale_kernel(const unsigned int* amax, float* scale, double* inv) {
+  const float m = __uint_as_float(*amax);
+  int e = 0;
+  if (m > 0.0f && isfinite(m)) frexpf(m, &e);
+  scale[0] = ldexpf(1.0f, -e);
+  inv[0] = ldexp(1.0, e);
+}
+
+// Rows [J, J8) of a padded copy stay zero; columns are copied as is.
+__global__ void pad_rows_f32_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t J, int64_t J8,
+                                    int64_t K) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < J8 * K;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / J8, i = e - j * J8;
+    dst[e] = i < J ? src[i + J * j] : 0.0f;
+  }
+}
+
+}  // namespace
+
+size_t seed_f32_smem_bytes() {
+  return 1024 + kConv * kConvTile + kStages * (kYTile + kKTile) + 256 + kRP * sizeof(double);
+}
+int seed_f32_rank_cols() { return kRP; }
+int64_t seed_f32_tile_bytes() { return kKTile; }
+
+int launch_seed_f32(const Seed32Params& p, const CUtensorMap* ymap, int left, cudaStream_t s) {
+  const size_t smem = seed_f32_smem_bytes();
+  if (left) {
+    static bool cfg = false;
+    if (!cfg) {
+      cudaFuncSetAttribute(seed_f32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cfg = true;
+    }
+    seed_f32_kernel<1><<<p.P, kThreads, smem, s>>>(p, *ymap);
+  } else {
+    static bool cfg = false;
+    if (!cfg) {
+      cudaFuncSetAttribute(seed_f32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cfg = true;
+    }
+    seed_f32_kernel<0><<<p.P, kThreads, smem, s>>>(p, *ymap);
+  }
+  return 1;
+}
+
+int launch_kr_scale(const KRSpec& right, const KRSpec& left, int R, double* scale, double* inv, cudaStream_t s) {
+  kr_scale_kernel<<<1, kRP, 0, s>>>(right, left, R, scale, inv);
+  return 1;
+}
+
+int launch_kr_split(const double* rows, int64_t L, int ld, const double* scale, void* tiles, cudaStream_t s) {
+  const int64_t ntiles = (L + kBK - 1) / kBK;
+  const int64_t work = ntiles * 8 * (kRP / 8) * 8;
+  kr_split_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, s>>>(rows, L, ld, scale,
+                                                                             static_cast<__half*>(tiles), ntiles);
+  return 1;
+}
+
+int launch_y_scale(const float* y, int64_t n, unsigned int* amax_scratch, float* scale, double* inv,
+                   int num_sms, cudaStream_t s) {
+  cudaMemsetAsync(amax_scratch, 0, sizeof(unsigned int), s);
+  absmax_f32_kernel<<<num_sms * 8, 256, 0, s>>>(y, n, amax_scratch);
+  y_scale_kernel<<<1, 1, 0, s>>>(amax_scratch, scale, inv);
+  return 2;
+}
+
+int launch_pad_rows_f32(const float* src, float* dst, int64_t J, int64_t J8, int64_t K, int num_sms,
+                        cudaStream_t s) {
+  pad_rows_f32_kernel<<<num_sms * 8, 256, 0, s>>>(src, dst, J, J8, K);
+  return 1;
+}
+
+bool make_tensor_map_y32(CUtensorMap* out, const void* base, int64_t J8, int64_t K, int left) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (J8 & 7) || K >= (1ll << 32) || J8 >= (1ll << 32)) return false;
+  // J8 x K column-major fp32; right tiles 128 i x 64 j, left tiles 64 i x 128 j
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(J8), static_cast<cuuint64_t>(K)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(J8) * 4};
+  const cuuint32_t box[2] = {left ? 64u : 128u, left ? 128u : 64u};
+  const cuuint32_t estride[2] = {1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estride,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace cpdgpu

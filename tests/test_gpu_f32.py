@@ -1,0 +1,101 @@
+"""fp32 tensors on the tensor-core path (seed_f32.cu: tcgen05 kind::f16 with
+hi/lo operand splitting, fp64 drains).  Parity bar from the north star: relative
+Frobenius error <= 1e-5 per mode against the fp64 oracle run on the same fp32
+values (upcast), BASELINE config 5 construction (U(-1,1) fp32 tensor, N(0,1)
+factors) at sizes the oracle finishes in seconds, plus the edge shapes the
+fp32 path handles specially (rows padded to a multiple of 8, R > 64 chunks,
+unsorted modes, partial tiles)."""
+import numpy as np
+import pytest
+
+import paper_1204_1586_b200 as cpd
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5  # fp32 bar (BASELINE.json north star)
+
+
+def rel_errs(got, want):
+    return [float(np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-300)) for g, w in zip(got, want)]
+
+
+def _case(ctx, oracle, dims, R, seed=11):
+    y = cpd.DenseTensor.generate(dims, cpd.DIST_UNIFORM_PM1, seed=seed, ctx=ctx, dtype=cpd.F32)
+    yv = y.values().astype(np.float64)
+    f = [oracle.fill_normal(seed * 10 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
+    return y, yv, f
+
+
+@pytest.mark.parametrize("dims,R", [
+    ([16, 16, 16, 16], 5),
+    ([40, 40, 40, 40], 64),      # config-5 shape family, full 64-column pass
+    ([24, 30, 40], 33),
+    ([7, 9, 11, 13], 8),         # J_p = 63: rows padded to 64
+    ([300, 300, 20], 16),        # long K, several fp32 accumulation chunks
+    ([130, 257], 3),             # N = 2, partial row block and k-tile
+    ([12, 10, 14, 9, 8], 70),    # R > 64: two rank chunks, unsorted modes
+])
+def test_f32_gradient_matches_oracle(gpu_ctx, oracle, dims, R):
+    y, yv, f = _case(gpu_ctx, oracle, dims, R)
+    got = cpd.cp_gradient_all(y, f)
+    want, _, _ = oracle.cp_gradient_all(yv, dims, f)
+    errs = rel_errs(got, want)
+    assert max(errs) <= TOL, errs
+
+
+def test_f32_scaling_extremes(gpu_ctx, oracle):
+    """Y and factor magnitudes far outside fp16 range: power-of-two scaling keeps accuracy."""
+    dims, R = [20, 24, 28], 6
+    vals = (np.random.default_rng(3).uniform(-1, 1, int(np.prod(dims))) * 3e7).astype(np.float32)
+    y = cpd.DenseTensor.from_values(vals, dims, ctx=gpu_ctx, dtype=cpd.F32)
+    f = [np.random.default_rng(10 + k).normal(size=(d, R)) * s for k, (d, s) in
+         enumerate(zip(dims, [1e-6, 1e5, 3.0]))]
+    got = cpd.cp_gradient_all(y, f)
+    want, _, _ = oracle.cp_gradient_all(vals.astype(np.float64), dims, f)
+    assert max(rel_errs(got, want)) <= TOL
+
+
+def test_f32_update_refreshes_scale(gpu_ctx, oracle):
+    dims, R = [16, 24, 32], 4
+    y, yv, f = _case(gpu_ctx, oracle, dims, R)
+    cpd.cp_gradient_all(y, f)
+    big = (yv * 1000.0).astype(np.float32)
+    y.update(big.ctypes.data)
+    got = cpd.cp_gradient_all(y, f)
+    want, _, _ = oracle.cp_gradient_all(big.astype(np.float64), dims, f)
+    assert max(rel_errs(got, want)) <= TOL
+
+
+def test_f32_deterministic(gpu_ctx, oracle):
+    y, _, f = _case(gpu_ctx, oracle, [32, 32, 32, 32], 64)
+    a = cpd.cp_gradient_all(y, f)
+    b = cpd.cp_gradient_all(y, f)
+    for x, z in zip(a, b):
+        assert np.array_equal(x, z)
+
+
+def test_f32_hook_gauss_seidel(gpu_ctx, oracle):
+    dims, R = [12, 16, 10, 14], 7
+    y, yv, f0 = _case(gpu_ctx, oracle, dims, R)
+    f = [a.copy(order="F") for a in f0]
+    ref = [a.copy(order="F") for a in f0]
+    got = [None] * 4
+
+    def hook(n, g):
+        got[n - 1] = g
+        f[n - 1] = oracle.fill_normal(900 + n, dims[n - 1] * R).reshape(dims[n - 1], R, order="F")
+
+    cpd.cp_gradient_all(y, f, hook=hook)
+    for n in oracle.fast_update_order(dims):
+        want = oracle.brute_mttkrp(yv, dims, ref, n)
+        assert rel_errs([got[n - 1]], [want])[0] <= TOL
+        ref[n - 1] = oracle.fill_normal(900 + n, dims[n - 1] * R).reshape(dims[n - 1], R, order="F")
+
+
+def test_f32_als_fit_trace(gpu_ctx, oracle):
+    dims, R = [20, 22, 24, 18], 5
+    y, yv, f = _case(gpu_ctx, oracle, dims, R)
+    res = cpd.run(y, f, cpd.SolveOptions(max_iters=8))
+    _, ot = oracle.run_als_fast(yv, dims, f, max_iters=8)
+    for i in range(8):
+        assert abs(res.trace.rel_error[i] - ot["rel_error"][i]) <= 1e-5 * ot["rel_error"][i]
