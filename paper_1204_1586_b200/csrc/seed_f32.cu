@@ -40,7 +40,8 @@ constexpr int kBM = 128;            // output rows per block (MMA M)
 constexpr int kRP = 64;             // rank columns per pass (MMA N)
 constexpr int kYTile = kBK * kBM * 4;           // fp32 tile bytes (32 KB)
 constexpr int kKTile = 2 * kBK * kRP * 2;       // fp16 hi + lo Khatri-Rao tile (16 KB)
-constexpr int kStages = 3;          // raw ring (Y fp32 + Khatri-Rao tile)
+constexpr int kStages = 4;          // raw Y ring (fp32), released as soon as it is split
+constexpr int kKStages = 2;         // Khatri-Rao tile ring, released by the MMAs
 constexpr int kConv = 2;            // split operand ring (fp16 hi + lo)
 constexpr int kConvTile = kBK * kBM * 2 * 2;    // 32 KB
 constexpr int kSplitWarps = 8;
@@ -70,18 +71,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// L2 policies: Y streams through once (evict first); the Khatri-Rao tiles are
+// re-read by every CTA (evict last), so they stay resident while Y streams.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
 // tcgen05 shared-memory matrix descriptor: start, leading- and stride-dimension
@@ -161,31 +176,38 @@ __device__ __forceinline__ void split_right(const unsigned char* raw, unsigned c
 }
 // Left pass: raw tile [128 j][64 i] fp32 (256 B rows) -> K-major SW128 atoms
 // (8 j-rows x 64 i): atom j / 8 at (j / 8) KB, row j % 8, chunk i / 8 XOR (j % 8).
+// Half-warps take rows j and j + 1 (4 values per lane).
 template <bool SCALE>
 __device__ __forceinline__ void split_left(const unsigned char* raw, unsigned char* hi, unsigned char* lo, float sy,
                                            int warp, int lane) {
-  const int c = lane >> 2, q = lane & 3;
+  const int hw = lane >> 4, l16 = lane & 15, c = l16 >> 1, half = l16 & 1;
 #pragma unroll 4
-  for (int j = warp; j < kBM; j += kSplitWarps) {
-    float2 v = *reinterpret_cast<const float2*>(raw + j * 256 + lane * 8);
+  for (int j0 = 2 * warp; j0 < kBM; j0 += 2 * kSplitWarps) {
+    const int j = j0 + hw;
+    float4 v = *reinterpret_cast<const float4*>(raw + j * 256 + l16 * 16);
     if (SCALE) {
-      v.x *= sy; v.y *= sy;
+      v.x *= sy; v.y *= sy; v.z *= sy; v.w *= sy;
     }
-    uint32_t h, l;
-    split2(v.x, v.y, h, l);
+    uint2 h, l;
+    split2(v.x, v.y, h.x, l.x);
+    split2(v.z, v.w, h.y, l.y);
     const int r = j & 7;
-    const int off = (j >> 3) * 1024 + r * 128 + ((c ^ r) << 4) + q * 4;
-    *reinterpret_cast<uint32_t*>(hi + off) = h;
-    *reinterpret_cast<uint32_t*>(lo + off) = l;
+    const int off = (j >> 3) * 1024 + r * 128 + ((c ^ r) << 4) + half * 8;
+    *reinterpret_cast<uint2*>(hi + off) = h;
+    *reinterpret_cast<uint2*>(lo + off) = l;
   }
 }
 
 // Walk of one CTA's units [a, a + n) (unit = block * nK + k-tile): segment
 // (one output block) and chunk (fp32 accumulation window) boundaries.
 struct Walk {
-  int64_t a, nK;
+  int64_t nK;
   int chunk;
-  __device__ bool seg_start(int64_t k) const { return k == 0 || (a + k) % nK == 0; }
+  int64_t t;  // k-tile index of the current unit
+  __device__ Walk(int64_t a, int64_t nk, int ch) : nK(nk), chunk(ch), t(a % nk) {}
+  __device__ bool seg_start(int k) const { return k == 0 || t == 0; }
+  __device__ bool next_starts() const { return t + 1 == nK; }
+  __device__ void advance() { t = (t + 1 == nK) ? 0 : t + 1; }
 };
 
 template <int LEFT>
@@ -196,18 +218,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t a = static_cast<int64_t>(cta) * p.units / p.P;
   const int64_t b = static_cast<int64_t>(cta + 1) * p.units / p.P;
   const int n = static_cast<int>(b - a);
-  const Walk w{a, p.nK, p.chunk};
+  Walk w(a, p.nK, p.chunk);
   constexpr int kProducer = kSplitWarps, kMma = kSplitWarps + 1;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* conv = base;                            // [kConv][hi 16 KB | lo 16 KB], 1 KB atoms
   unsigned char* ytiles = conv + kConv * kConvTile;      // [kStages][32 KB] fp32
-  unsigned char* ktiles = ytiles + kStages * kYTile;     // [kStages][16 KB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ktiles + kStages * kKTile);
-  uint64_t* full = bars;                   // raw stage landed          (1 + tx)
-  uint64_t* empty = full + kStages;        // raw stage consumed        (MMA commit)
-  uint64_t* cfull = empty + kStages;       // split operands ready      (8 warps)
+  unsigned char* ktiles = ytiles + kStages * kYTile;     // [kKStages][16 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ktiles + kKStages * kKTile);
+  uint64_t* full = bars;                   // raw Y landed              (1 + tx)
+  uint64_t* empty = full + kStages;        // raw Y split               (8 warps)
+  uint64_t* kfull = empty + kStages;       // Khatri-Rao tile landed    (1 + tx)
+  uint64_t* kempty = kfull + kKStages;     // Khatri-Rao tile consumed  (MMA commit)
+  uint64_t* cfull = kempty + kKStages;     // split operands ready      (8 warps)
   uint64_t* cempty = cfull + kConv;        // split operands consumed   (MMA commit)
   uint64_t* accfull = cempty + kConv;      // [2] chunk accumulated     (commit)
   uint64_t* accempty = accfull + 2;        // [2] chunk drained         (8 warps)
@@ -217,7 +241,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kSplitWarps);
+    }
+    for (int s = 0; s < kKStages; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
     }
     for (int c = 0; c < kConv; ++c) {
       mbar_init(&cfull[c], kSplitWarps);
@@ -245,16 +273,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kProducer) {
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
+      // Y runs up to kStages tiles ahead, the Khatri-Rao tiles kKStages ahead
+      const uint64_t pol_y = policy_evict_first(), pol_k = policy_evict_last();
+      int kk = 0;
       for (int k = 0; k < n; ++k) {
         const int s = k % kStages;
         if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
         const int64_t u = a + k, blk = u / p.nK, t = u - blk * p.nK;
-        mbar_arrive_tx(&full[s], kYTile + kKTile);
+        mbar_arrive_tx(&full[s], kYTile);
         if (LEFT)  // rows i in [64 t, +64), columns j in [128 blk, +128)
-          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(t * kBK), static_cast<int>(blk * kBM), &full[s]);
+          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(t * kBK), static_cast<int>(blk * kBM), &full[s], pol_y);
         else       // rows i in [128 blk, +128), columns j in [64 t, +64)
-          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(blk * kBM), static_cast<int>(t * kBK), &full[s]);
-        bulk_load(ktiles + s * kKTile, p.kr_tiles + t * kKTile, kKTile, &full[s]);
+          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(blk * kBM), static_cast<int>(t * kBK), &full[s], pol_y);
+        for (; kk < n && kk <= k - (kStages - kKStages); ++kk) {
+          const int sk = kk % kKStages;
+          if (kk >= kKStages) mbar_wait(&kempty[sk], ((kk / kKStages) - 1) & 1);
+          const int64_t uk = a + kk, tk = uk - (uk / p.nK) * p.nK;
+          mbar_arrive_tx(&kfull[sk], kKTile);
+          bulk_load(ktiles + sk * kKTile, p.kr_tiles + tk * kKTile, kKTile, &kfull[sk], pol_k);
+        }
+      }
+      for (; kk < n; ++kk) {
+        const int sk = kk % kKStages;
+        if (kk >= kKStages) mbar_wait(&kempty[sk], ((kk / kKStages) - 1) & 1);
+        const int64_t uk = a + kk, tk = uk - (uk / p.nK) * p.nK;
+        mbar_arrive_tx(&kfull[sk], kKTile);
+        bulk_load(ktiles + sk * kKTile, p.kr_tiles + tk * kKTile, kKTile, &kfull[sk], pol_k);
       }
     }
   } else if (warp == kMma) {
@@ -267,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t b_lbo = kRP * 16, b_sbo = 128, b_kstep = 2 * kRP * 16, b_lo = kBK * kRP * 2;
     int q = -1, pos = 0;
     for (int k = 0; k < n; ++k) {
-      const int s = k % kStages, c = k % kConv;
+      const int sk = k % kKStages, c = k % kConv;
       if (w.seg_start(k) || pos == w.chunk) {  // new accumulation chunk
         ++q;
         pos = 0;
@@ -276,12 +320,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
       }
-      mbar_wait(&cfull[c], (k / kConv) & 1);  // implies the raw stage landed
+      mbar_wait(&cfull[c], (k / kConv) & 1);
+      mbar_wait(&kfull[sk], (k / kKStages) & 1);
       tc_fence_after();
       if (lane == 0) {
         const uint32_t d = tmem + static_cast<uint32_t>((q & 1) * kRP);
         const uint32_t ha = smem_u32(conv + c * kConvTile), la = ha + kConvTile / 2;
-        const uint32_t kb = smem_u32(ktiles + s * kKTile);
+        const uint32_t kb = smem_u32(ktiles + sk * kKTile);
 #pragma unroll
         for (int ks = 0; ks < kBK / 16; ++ks) {
           const uint64_t ahi = umma_desc(ha + ks * a_kstep, a_lbo, a_sbo, kSwizzle128);
@@ -292,12 +337,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_f16(d, alo, bhi, idesc, 1u);
           umma_f16(d, ahi, blo, idesc, 1u);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&kempty[sk]);
         umma_commit(&cempty[c]);
       }
       __syncwarp();
       ++pos;
-      const bool chunk_end = (k == n - 1) || w.seg_start(k + 1) || pos == w.chunk;
+      const bool chunk_end = (k == n - 1) || w.next_starts() || pos == w.chunk;
+      w.advance();
       if (chunk_end && lane == 0) umma_commit(&accfull[q & 1]);
       __syncwarp();
     }
@@ -334,7 +380,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&cfull[c]);
+        if (lane == 0) {
+          mbar_arrive(&empty[s]);
+          mbar_arrive(&cfull[c]);
+        }
       }
       // drain the previous chunk one stage late, so the MMAs of this stage overlap it
       if (pend_q >= 0 && pend_k < k) {
@@ -360,7 +409,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (k < n) {
         ++pos;
-        const bool seg_end = (k == n - 1) || w.seg_start(k + 1);
+        const bool seg_end = (k == n - 1) || w.next_starts();
+        w.advance();
         if (seg_end || pos == w.chunk) {
           pend_q = q;
           pend_k = k;
@@ -457,7 +507,7 @@ __global__ void pad_rows_f32_kernel(const float* __restrict__ src, float* __rest
 }  // namespace
 
 size_t seed_f32_smem_bytes() {
-  return 1024 + kConv * kConvTile + kStages * (kYTile + kKTile) + 256 + kRP * sizeof(double);
+  return 1024 + kConv * kConvTile + kStages * kYTile + kKStages * kKTile + 256 + kRP * sizeof(double);
 }
 int seed_f32_rank_cols() { return kRP; }
 int64_t seed_f32_tile_bytes() { return kKTile; }
