@@ -13,20 +13,20 @@
 // long K = 90000 sums of config 5 keep ~1e-7 relative accuracy.
 //
 // One CTA per SM (persistent), 320 threads:
-//   warp 8      producer: 2-D TMA of the fp32 Y tile (512 B / 256 B rows) + one
-//               bulk copy of the pre-split Khatri-Rao tile per stage
-//   warps 0-7   split each Y tile into fp16 hi and lo operand tiles laid out as
-//               128B-swizzled core-matrix atoms (MN-major for the right product,
-//               A = Y: M = i; K-major for the left product, A = Y^T: M = j), then
-//               drain the TMEM accumulators into fp64 registers (warp w: TMEM
-//               lanes 32 (w % 4).., rank columns 32 (w / 4)..) and write the
-//               per-CTA partial rows
-//   warp 9      allocates TMEM and issues the MMAs (one elected lane)
+//   warp 8      producer: 2-D TMA of the fp32 Y tile + one bulk copy of the
+//               pre-split Khatri-Rao tile per stage
+//   warps 0-7   split each Y tile into fp16 hi and lo A operands written straight
+//               into tensor memory (tcgen05.st; thread = A row = TMEM lane), then
+//               drain the TMEM accumulators into fp64 registers and write the
+//               per-CTA partial rows.  Warp w serves TMEM lanes 32 (w % 4).. and
+//               K half / rank-column half w / 4.
+//   warp 9      allocates TMEM and issues the MMAs (one elected lane):
+//               D[tmem] += A[tmem] * B[smem], kind::f16, M = 128, N = 64, K = 16
 //
-// Y tiles arrive as plain column-major boxes (right: 128 i x 64 j, left: 64 i x
-// 128 j), so every TMA row is a 512 / 256 B run; the split writes the fp16
-// operands in the layouts the MMA reads with 128-byte swizzling, which keeps both
-// the fp32 row reads and the fp16 atom writes free of bank conflicts.
+// Shared memory then carries only the fp32 tile (TMA in, split out) and the
+// Khatri-Rao B operand; the right tile (128 i x 64 j) is read down its columns
+// (one row i per thread, conflict-free), the left tile (64 i x 128 j, fetched as
+// two 128B-swizzled 32 i halves) along its rows.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
@@ -40,13 +40,14 @@ constexpr int kBM = 128;            // output rows per block (MMA M)
 constexpr int kRP = 64;             // rank columns per pass (MMA N)
 constexpr int kYTile = kBK * kBM * 4;           // fp32 tile bytes (32 KB)
 constexpr int kKTile = 2 * kBK * kRP * 2;       // fp16 hi + lo Khatri-Rao tile (16 KB)
-constexpr int kStages = 4;          // raw Y ring (fp32), released as soon as it is split
-constexpr int kKStages = 2;         // Khatri-Rao tile ring, released by the MMAs
-constexpr int kConv = 2;            // split operand ring (fp16 hi + lo)
-constexpr int kConvTile = kBK * kBM * 2 * 2;    // 32 KB
+constexpr int kStages = 5;          // raw Y ring (fp32), released as soon as it is split
+constexpr int kKStages = 3;         // Khatri-Rao tile ring, released by the MMAs
+constexpr int kConv = 2;            // A operand ring in TMEM (fp16 hi + lo, 64 columns each)
 constexpr int kSplitWarps = 8;
 constexpr int kThreads = (kSplitWarps + 2) * 32;
-constexpr int kTmemCols = 2 * kRP;  // double-buffered accumulator
+constexpr int kTmemA = 0;                  // A buffers: columns [0, 128)
+constexpr int kTmemAcc = kConv * kBK;      // accumulators: columns [128, 256)
+constexpr int kTmemCols = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -106,17 +107,25 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint3
   return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (static_cast<uint64_t>(layout) << 61);
 }
-constexpr uint32_t kSwizzle128 = 2;  // layout type SWIZZLE_128B
 // Instruction descriptor, kind::f16: fp16 A and B, fp32 D, M = 128, N = kRP.
 __host__ __device__ constexpr uint32_t umma_idesc(bool a_mn_major) {
   return (1u << 4) | (0u << 7) | (0u << 10) | ((a_mn_major ? 1u : 0u) << 15) | (0u << 16) |
          (static_cast<uint32_t>(kRP >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
 }
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -152,50 +161,45 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
   lo = pack_half2(a - back.x, b - back.y);
 }
 
-// Right pass: raw tile [64 j][128 i] fp32 (512 B rows) -> MN-major SW128 atoms
-// (8 j-rows x 64 i): atom (k-group j / 8, MN half i / 64) at ((j / 8) * 2 + i / 64) KB,
-// row j % 8 at 128 B, 16-B chunk (i % 64) / 8 XOR (j % 8).  Warp w: rows w, w + 8, ...
+// Right pass: raw tile [64 j][128 i] fp32 (512 B rows).  Thread = row i
+// (= TMEM lane 32 (w % 4) + lane), K half h = w / 4: j in [32 h, 32 h + 32).
 template <bool SCALE>
-__device__ __forceinline__ void split_right(const unsigned char* raw, unsigned char* hi, unsigned char* lo, float sy,
-                                            int warp, int lane) {
-  const int ma = lane >> 4, c = (lane & 15) >> 1, half = lane & 1;
-#pragma unroll 4
-  for (int j = warp; j < kBK; j += kSplitWarps) {
-    float4 v = *reinterpret_cast<const float4*>(raw + j * 512 + lane * 16);
+__device__ __forceinline__ void split_right(const unsigned char* raw, uint32_t tA, float sy, int warp, int lane) {
+  const int i = (warp & 3) * 32 + lane, h = warp >> 2;
+  const float* col = reinterpret_cast<const float*>(raw) + i + (32 * h) * kBM;
+  uint32_t hw[16], lw[16];
+#pragma unroll
+  for (int jj = 0; jj < 16; ++jj) {
+    float x0 = col[(2 * jj) * kBM], x1 = col[(2 * jj + 1) * kBM];
     if (SCALE) {
-      v.x *= sy; v.y *= sy; v.z *= sy; v.w *= sy;
+      x0 *= sy;
+      x1 *= sy;
     }
-    uint2 h, l;
-    split2(v.x, v.y, h.x, l.x);
-    split2(v.z, v.w, h.y, l.y);
-    const int r = j & 7;
-    const int off = ((j >> 3) * 2 + ma) * 1024 + r * 128 + ((c ^ r) << 4) + half * 8;
-    *reinterpret_cast<uint2*>(hi + off) = h;
-    *reinterpret_cast<uint2*>(lo + off) = l;
+    split2(x0, x1, hw[jj], lw[jj]);
   }
+  const uint32_t lanes = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  tmem_st16(tA + lanes + 16 * h, hw);
+  tmem_st16(tA + lanes + 32 + 16 * h, lw);
 }
-// Left pass: raw tile [128 j][64 i] fp32 (256 B rows) -> K-major SW128 atoms
-// (8 j-rows x 64 i): atom j / 8 at (j / 8) KB, row j % 8, chunk i / 8 XOR (j % 8).
-// Half-warps take rows j and j + 1 (4 values per lane).
+// Left pass: raw tile = two 128B-swizzled halves [128 j][32 i] fp32 (128 B rows,
+// 16-B chunk c of row j at c ^ (j % 8)).  Thread = row j, K half h = w / 4.
 template <bool SCALE>
-__device__ __forceinline__ void split_left(const unsigned char* raw, unsigned char* hi, unsigned char* lo, float sy,
-                                           int warp, int lane) {
-  const int hw = lane >> 4, l16 = lane & 15, c = l16 >> 1, half = l16 & 1;
-#pragma unroll 4
-  for (int j0 = 2 * warp; j0 < kBM; j0 += 2 * kSplitWarps) {
-    const int j = j0 + hw;
-    float4 v = *reinterpret_cast<const float4*>(raw + j * 256 + l16 * 16);
+__device__ __forceinline__ void split_left(const unsigned char* raw, uint32_t tA, float sy, int warp, int lane) {
+  const int j = (warp & 3) * 32 + lane, h = warp >> 2;
+  const unsigned char* row = raw + h * (kYTile / 2) + j * 128;
+  uint32_t hw[16], lw[16];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (j & 7)) << 4));
     if (SCALE) {
       v.x *= sy; v.y *= sy; v.z *= sy; v.w *= sy;
     }
-    uint2 h, l;
-    split2(v.x, v.y, h.x, l.x);
-    split2(v.z, v.w, h.y, l.y);
-    const int r = j & 7;
-    const int off = (j >> 3) * 1024 + r * 128 + ((c ^ r) << 4) + half * 8;
-    *reinterpret_cast<uint2*>(hi + off) = h;
-    *reinterpret_cast<uint2*>(lo + off) = l;
+    split2(v.x, v.y, hw[2 * c], lw[2 * c]);
+    split2(v.z, v.w, hw[2 * c + 1], lw[2 * c + 1]);
   }
+  const uint32_t lanes = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  tmem_st16(tA + lanes + 16 * h, hw);
+  tmem_st16(tA + lanes + 32 + 16 * h, lw);
 }
 
 // Walk of one CTA's units [a, a + n) (unit = block * nK + k-tile): segment
@@ -223,16 +227,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  unsigned char* conv = base;                            // [kConv][hi 16 KB | lo 16 KB], 1 KB atoms
-  unsigned char* ytiles = conv + kConv * kConvTile;      // [kStages][32 KB] fp32
+  unsigned char* ytiles = base;                          // [kStages][32 KB] fp32
   unsigned char* ktiles = ytiles + kStages * kYTile;     // [kKStages][16 KB]
   uint64_t* bars = reinterpret_cast<uint64_t*>(ktiles + kKStages * kKTile);
   uint64_t* full = bars;                   // raw Y landed              (1 + tx)
   uint64_t* empty = full + kStages;        // raw Y split               (8 warps)
   uint64_t* kfull = empty + kStages;       // Khatri-Rao tile landed    (1 + tx)
   uint64_t* kempty = kfull + kKStages;     // Khatri-Rao tile consumed  (MMA commit)
-  uint64_t* cfull = kempty + kKStages;     // split operands ready      (8 warps)
-  uint64_t* cempty = cfull + kConv;        // split operands consumed   (MMA commit)
+  uint64_t* cfull = kempty + kKStages;     // A operands in TMEM        (8 warps)
+  uint64_t* cempty = cfull + kConv;        // A operands consumed       (MMA commit)
   uint64_t* accfull = cempty + kConv;      // [2] chunk accumulated     (commit)
   uint64_t* accempty = accfull + 2;        // [2] chunk drained         (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
@@ -281,10 +284,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
         const int64_t u = a + k, blk = u / p.nK, t = u - blk * p.nK;
         mbar_arrive_tx(&full[s], kYTile);
-        if (LEFT)  // rows i in [64 t, +64), columns j in [128 blk, +128)
-          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(t * kBK), static_cast<int>(blk * kBM), &full[s], pol_y);
-        else       // rows i in [128 blk, +128), columns j in [64 t, +64)
-          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(blk * kBM), static_cast<int>(t * kBK), &full[s], pol_y);
+        if (LEFT) {  // rows i in [64 t, +64) as two 32-row halves, columns j in [128 blk, +128)
+          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(t * kBK), static_cast<int>(blk * kBM), &full[s],
+                      pol_y);
+          tma_load_2d(ytiles + s * kYTile + kYTile / 2, &ymap, static_cast<int>(t * kBK + 32),
+                      static_cast<int>(blk * kBM), &full[s], pol_y);
+        } else {     // rows i in [128 blk, +128), columns j in [64 t, +64)
+          tma_load_2d(ytiles + s * kYTile, &ymap, static_cast<int>(blk * kBM), static_cast<int>(t * kBK), &full[s],
+                      pol_y);
+        }
         for (; kk < n && kk <= k - (kStages - kKStages); ++kk) {
           const int sk = kk % kKStages;
           if (kk >= kKStages) mbar_wait(&kempty[sk], ((kk / kKStages) - 1) & 1);
@@ -303,10 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMma) {
     // ------------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc(!LEFT);
-    // A: right = MN-major SW128 (LBO: next 64 i = 1 KB, SBO: next 8 j = 2 KB, +4 KB per 16 j);
-    //    left  = K-major SW128  (SBO: next 8 j = 1 KB, +32 B per 16 i inside the atom)
-    constexpr uint32_t a_lbo = LEFT ? 16 : 1024, a_sbo = LEFT ? 1024 : 2048, a_kstep = LEFT ? 32 : 4096;
+    constexpr uint32_t idesc = umma_idesc(false);  // A from TMEM (K-major rows)
     // B (Khatri-Rao, K-major interleaved): SBO next 8 r = 128 B, LBO next 8 K = kRP * 16 B
     constexpr uint32_t b_lbo = kRP * 16, b_sbo = 128, b_kstep = 2 * kRP * 16, b_lo = kBK * kRP * 2;
     int q = -1, pos = 0;
@@ -324,18 +329,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&kfull[sk], (k / kKStages) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t d = tmem + static_cast<uint32_t>((q & 1) * kRP);
-        const uint32_t ha = smem_u32(conv + c * kConvTile), la = ha + kConvTile / 2;
+        const uint32_t d = tmem + static_cast<uint32_t>(kTmemAcc + (q & 1) * kRP);
+        const uint32_t ahi = tmem + static_cast<uint32_t>(kTmemA + c * kBK), alo = ahi + kBK / 2;
         const uint32_t kb = smem_u32(ktiles + sk * kKTile);
 #pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks) {
-          const uint64_t ahi = umma_desc(ha + ks * a_kstep, a_lbo, a_sbo, kSwizzle128);
-          const uint64_t alo = umma_desc(la + ks * a_kstep, a_lbo, a_sbo, kSwizzle128);
+        for (int ks = 0; ks < kBK / 16; ++ks) {  // K = 16 per MMA = 8 packed TMEM columns
           const uint64_t bhi = umma_desc(kb + ks * b_kstep, b_lbo, b_sbo);
           const uint64_t blo = umma_desc(kb + b_lo + ks * b_kstep, b_lbo, b_sbo);
-          umma_f16(d, ahi, bhi, idesc, (pos > 0 || ks > 0) ? 1u : 0u);
-          umma_f16(d, alo, bhi, idesc, 1u);
-          umma_f16(d, ahi, blo, idesc, 1u);
+          umma_f16_ts(d, ahi + 8 * ks, bhi, idesc, (pos > 0 || ks > 0) ? 1u : 0u);
+          umma_f16_ts(d, alo + 8 * ks, bhi, idesc, 1u);
+          umma_f16_ts(d, ahi + 8 * ks, blo, idesc, 1u);
         }
         umma_commit(&kempty[sk]);
         umma_commit(&cempty[c]);
@@ -368,17 +371,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           pos = 0;
         }
         mbar_wait(&full[s], (k / kStages) & 1);
-        if (k >= kConv) mbar_wait(&cempty[c], ((k / kConv) - 1) & 1);
-        unsigned char* hi = conv + c * kConvTile;
+        if (k >= kConv) {
+          mbar_wait(&cempty[c], ((k / kConv) - 1) & 1);
+          tc_fence_after();
+        }
+        const uint32_t tA = tmem + static_cast<uint32_t>(kTmemA + c * kBK);
         const unsigned char* raw = ytiles + s * kYTile;
         if (LEFT) {
-          if (scale) split_left<true>(raw, hi, hi + kConvTile / 2, sy, warp, lane);
-          else split_left<false>(raw, hi, hi + kConvTile / 2, sy, warp, lane);
+          if (scale) split_left<true>(raw, tA, sy, warp, lane);
+          else split_left<false>(raw, tA, sy, warp, lane);
         } else {
-          if (scale) split_right<true>(raw, hi, hi + kConvTile / 2, sy, warp, lane);
-          else split_right<false>(raw, hi, hi + kConvTile / 2, sy, warp, lane);
+          if (scale) split_right<true>(raw, tA, sy, warp, lane);
+          else split_right<false>(raw, tA, sy, warp, lane);
         }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&empty[s]);
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&accfull[pend_q & 1], (pend_q >> 1) & 1);
         tc_fence_after();
         float v[32];
-        tmem_ld32(tmem + lane_base + static_cast<uint32_t>((pend_q & 1) * kRP + colh * 32), v);
+        tmem_ld32(tmem + lane_base + static_cast<uint32_t>(kTmemAcc + (pend_q & 1) * kRP + colh * 32), v);
 #pragma unroll
         for (int c = 0; c < 32; ++c) acc[c] += static_cast<double>(v[c]);
         tc_fence_before();
@@ -507,7 +514,7 @@ __global__ void pad_rows_f32_kernel(const float* __restrict__ src, float* __rest
 }  // namespace
 
 size_t seed_f32_smem_bytes() {
-  return 1024 + kConv * kConvTile + kStages * kYTile + kKStages * kKTile + 256 + kRP * sizeof(double);
+  return 1024 + kStages * kYTile + kKStages * kKTile + 256 + kRP * sizeof(double);
 }
 int seed_f32_rank_cols() { return kRP; }
 int64_t seed_f32_tile_bytes() { return kKTile; }
@@ -573,11 +580,11 @@ bool make_tensor_map_y32(CUtensorMap* out, const void* base, int64_t J8, int64_t
   // J8 x K column-major fp32; right tiles 128 i x 64 j, left tiles 64 i x 128 j
   const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(J8), static_cast<cuuint64_t>(K)};
   const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(J8) * 4};
-  const cuuint32_t box[2] = {left ? 64u : 128u, left ? 128u : 64u};
+  const cuuint32_t box[2] = {left ? 32u : 128u, left ? 128u : 64u};
   const cuuint32_t estride[2] = {1, 1};
   return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estride,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                CU_TENSOR_MAP_INTERLEAVE_NONE, left ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace cpdgpu
