@@ -584,7 +584,10 @@ bool make_tensor_map_y32(CUtensorMap* out, const void* base, int64_t J8, int64_t
   const cuuint32_t estride[2] = {1, 1};
   return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estride,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, left ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                // no 256 B promotion: column starts are only 64 B aligned in general (J * 4 bytes apart),
+                // and a promoted line straddling the neighbouring row block is evicted before that block
+                // (another CTA) reads it
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace cpdgpu
