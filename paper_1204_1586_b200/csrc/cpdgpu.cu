@@ -886,6 +886,22 @@ void add_left_recurse(const Plan& pl, cpdgpu::TailStep& st, int j, const double*
   st.op[st.n++] = o;
 }
 
+// Point the seed-partial reduction of one side straight at its gradient slot
+// (rows x R column-major): used when that seed already is R^(1) or L^(N).
+void redirect_to_gradient(const Plan& pl, cpdgpu::TailStep& st, bool right) {
+  const double* base = right ? pl.Rs.d() : pl.Ls.d();
+  const int64_t rows = right ? pl.Jp : pl.Kp;
+  const int m = right ? pl.perm[0] - 1 : pl.perm[pl.N - 1] - 1;
+  for (int i = 0; i < st.n; ++i) {
+    cpdgpu::TailOp& o = st.op[i];
+    if (!o.out || o.out < base || o.out >= base + rows * pl.R) continue;
+    o.out_off = o.out - base;  // r0 * rows for the chunk
+    o.out = nullptr;
+    o.out_slot = m;
+    o.ldo = rows;
+  }
+}
+
 void launch_step(cpdgpu_ctx* ctx, Plan& pl, const cpdgpu::TailStep& st) {
   ctx->launches += cpdgpu::launch_tail_step(st, static_cast<double* const*>(pl.gtab.p), ctx->num_sms, ctx->stream);
 }
@@ -897,6 +913,12 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
   run_seeds(ctx, pl, left ? 3 : 1);
   cpdgpu::TailStep st{};
   add_reduce_ops(pl, st, left ? 3 : 1);
+  // The extractions G(1) = R^(1) and G(N) = L^(N) are copies (empty Khatri-Rao
+  // products): the step producing R^(1) / L^(N) writes the gradient directly.
+  const bool g1_direct = pl.p == 1;  // the right seed is R^(1)
+  if (g1_direct) redirect_to_gradient(pl, st, /*right=*/true);
+  const bool gN_direct = left && pl.p + 1 == pl.N && !pl.lpart_direct;  // the left seed is L^(N)
+  if (gN_direct) redirect_to_gradient(pl, st, /*right=*/false);
   launch_step(ctx, pl, st);
   double* rc = pl.Rs.d();
   double* rn = pl.Rtmp.d();
@@ -907,15 +929,35 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
     cpdgpu::TailStep s{};
     const int jr = pl.p - lv;      // right phase mode at this level
     const int jl = pl.p + 1 + lv;  // left phase mode at this level
-    if (jr >= 1) {
+    if (jr >= 2) {
       add_right_extract(pl, s, jr, rc);
-      if (jr >= 2) add_right_recurse(pl, s, jr, rc, rn);
+      add_right_recurse(pl, s, jr, rc, rn);
+      if (jr == 2) {  // R^(1) is G(1)
+        cpdgpu::TailOp& o = s.op[s.n - 1];
+        o.out = nullptr;
+        o.out_slot = pl.perm[0] - 1;
+        o.ldo = pl.sd[0];
+      }
+    } else if (jr == 1 && !g1_direct && pl.p >= 2) {
+      // already written by the previous level's recursion
+    } else if (jr == 1 && !g1_direct) {
+      add_right_extract(pl, s, jr, rc);
     }
     if (jl <= pl.N) {
-      add_left_extract(pl, s, jl, lc);
-      if (jl < pl.N) add_left_recurse(pl, s, jl, lc, ln);
+      if (jl < pl.N) {
+        add_left_extract(pl, s, jl, lc);
+        add_left_recurse(pl, s, jl, lc, ln);
+        if (jl + 1 == pl.N) {  // L^(N) is G(N)
+          cpdgpu::TailOp& o = s.op[s.n - 1];
+          o.out = nullptr;
+          o.out_slot = pl.perm[pl.N - 1] - 1;
+          o.ldo = pl.sd[pl.N - 1];
+        }
+      } else if (!gN_direct && jl == pl.p + 1) {
+        add_left_extract(pl, s, jl, lc);  // the left seed itself is L^(N) (lpart_direct)
+      }
     }
-    launch_step(ctx, pl, s);
+    if (s.n > 0) launch_step(ctx, pl, s);
     if (jr >= 2) std::swap(rc, rn);
     if (jl < pl.N) std::swap(lc, ln);
   }
