@@ -12,6 +12,30 @@ namespace cpdgpu {
 
 constexpr int kMaxModes = 16;  // modes per Khatri-Rao range
 
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialization attribute may start while its predecessor runs; it must
+// pdl_wait() before touching anything the predecessor writes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// Host: launch with (pdl = true) or without the programmatic attribute.
+template <typename... Exp, typename... Act>
+inline cudaError_t launch_k(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Act&&>(args)...);
+}
+bool pdl_enabled();  // CPDGPU_PDL=0 disables (default on)
+
 // A contiguous range of modes lo..hi of the sorted frame whose factor columns
 // form a Khatri-Rao row on the fly: row index q has mixed-radix digits
 // d_k (first mode fastest) and  KR[q, r] = prod_k A_k[d_k + I_k r]

@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (warp != kProducer) pdl_wait();  // scales and partial buffers: preceding kernels
   if (tid < kRP) unscale[tid] = p.inv_scale_y[0] * p.inv_scale_kr[tid];
   if (warp == kMma) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
@@ -276,10 +277,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kProducer) {
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
-      // Y runs up to kStages tiles ahead, the Khatri-Rao tiles kKStages ahead
+      // Y runs up to kStages tiles ahead, the Khatri-Rao tiles kKStages ahead.
+      // Y does not depend on the preceding kernel (PDL): the first stages are
+      // requested before the wait.
       const uint64_t pol_y = policy_evict_first(), pol_k = policy_evict_last();
       int kk = 0;
+      const int early = n < kStages ? n : kStages;
+      for (int k = 0; k < early; ++k) {
+        const int64_t u = a + k, blk = u / p.nK, t = u - blk * p.nK;
+        mbar_arrive_tx(&full[k], kYTile);
+        if (LEFT) {
+          tma_load_2d(ytiles + k * kYTile, &ymap, static_cast<int>(t * kBK), static_cast<int>(blk * kBM), &full[k],
+                      pol_y);
+          tma_load_2d(ytiles + k * kYTile + kYTile / 2, &ymap, static_cast<int>(t * kBK + 32),
+                      static_cast<int>(blk * kBM), &full[k], pol_y);
+        } else {
+          tma_load_2d(ytiles + k * kYTile, &ymap, static_cast<int>(blk * kBM), static_cast<int>(t * kBK), &full[k],
+                      pol_y);
+        }
+      }
+      pdl_wait();
       for (int k = 0; k < n; ++k) {
+        if (k < early) {  // Y already requested
+          for (; kk < n && kk <= k - (kStages - kKStages); ++kk) {
+            const int sk = kk % kKStages;
+            if (kk >= kKStages) mbar_wait(&kempty[sk], ((kk / kKStages) - 1) & 1);
+            const int64_t uk = a + kk, tk = uk - (uk / p.nK) * p.nK;
+            mbar_arrive_tx(&kfull[sk], kKTile);
+            bulk_load(ktiles + sk * kKTile, p.kr_tiles + tk * kKTile, kKTile, &kfull[sk], pol_k);
+          }
+          continue;
+        }
         const int s = k % kStages;
         if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
         const int64_t u = a + k, blk = u / p.nK, t = u - blk * p.nK;
@@ -527,14 +555,14 @@ int launch_seed_f32(const Seed32Params& p, const CUtensorMap* ymap, int left, cu
       cudaFuncSetAttribute(seed_f32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       cfg = true;
     }
-    seed_f32_kernel<1><<<p.P, kThreads, smem, s>>>(p, *ymap);
+    launch_k(seed_f32_kernel<1>, dim3(p.P), dim3(kThreads), smem, s, pdl_enabled(), p, *ymap);
   } else {
     static bool cfg = false;
     if (!cfg) {
       cudaFuncSetAttribute(seed_f32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       cfg = true;
     }
-    seed_f32_kernel<0><<<p.P, kThreads, smem, s>>>(p, *ymap);
+    launch_k(seed_f32_kernel<0>, dim3(p.P), dim3(kThreads), smem, s, pdl_enabled(), p, *ymap);
   }
   return 1;
 }

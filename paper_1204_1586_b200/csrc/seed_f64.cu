@@ -389,7 +389,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ------------------------------------------------------------------ producer
   if (warp == kConsumers) {
     unsigned long long tw = 0, tstart = clock64();
-    for (int k = 0; k < ntiles; ++k) {
+    // Y does not depend on the preceding kernel (PDL): the first stages' Y tiles
+    // are requested before the wait, their Khatri-Rao rows after it.
+    const int early = p.use_tma ? min(STAGES, ntiles) : 0;
+    if (lane == 0)
+      for (int k = 0; k < early; ++k) {
+        const int64_t tile = t0 + k;
+        const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
+        mbar_arrive_tx(&full[k], LDY * kTJ * 8 + ((MODE & 1) ? kTJ * LDK * 8 : 0));
+        tma_load_2d(Ys + k * kTJ * LDY, &tmap, static_cast<int>(rb * TI), static_cast<int>(ct * kTJ), &full[k]);
+      }
+    pdl_wait();
+    if (lane == 0 && (MODE & 1))
+      for (int k = 0; k < early; ++k) {
+        const int64_t ct = (t0 + k) % p.nCT;
+        tma_load_2d(KRr + k * kTJ * LDK, &kmap, 0, static_cast<int>(ct * kTJ), &full[k]);
+      }
+    for (int k = early; k < ntiles; ++k) {
       const int s = k % STAGES;
       if (k >= STAGES) {
         const unsigned long long a = clock64();
@@ -431,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ------------------------------------------------------------------ consumers
+  pdl_wait();  // Khatri-Rao rows and the partial buffers belong to the preceding kernels
   const Ring q{full, empty, Ys, KRr, KRl, red, STAGES, TI, LDY, LDK};
   unsigned long long cw = 0;
   const unsigned long long cstart = clock64();
@@ -462,7 +479,7 @@ void launch_one(const SeedParams& p, const CUtensorMap& tmap, const CUtensorMap&
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     configured = true;
   }
-  fn<<<p.P, kThreads, smem, s>>>(p, tmap, kmap);
+  launch_k(fn, dim3(p.P), dim3(kThreads), smem, s, pdl_enabled(), p, tmap, kmap);
 }
 
 template <int NT>

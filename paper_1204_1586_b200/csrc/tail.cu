@@ -11,6 +11,8 @@
 // independent of the right — so a gradient costs 1 + max(p, N - p) tail
 // launches.  Every output is produced by one warp in a fixed order, so results
 // are bitwise reproducible.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace cpdgpu {
@@ -107,6 +109,8 @@ __device__ void run_unit(const TailOp& o, int64_t u, int lane, double* const* gt
 }
 
 __global__ void __launch_bounds__(256) tail_step_kernel(const TailStep st, double* const* gtab) {
+  pdl_wait();     // inputs come from the previous step / seed
+  pdl_trigger();  // the next step may launch and wait
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   int64_t start[kMaxTailOps + 1];
@@ -150,6 +154,7 @@ __device__ void kr_rows(const KRJob& k, int64_t t, int64_t nt) {
 }
 
 __global__ void __launch_bounds__(256) prologue_kernel(const Prologue pr, double** gtab) {
+  pdl_trigger();  // the seed contraction may start streaming Y now
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
   if (t < kMaxModes && t < pr.N) gtab[t] = pr.gout[t];
@@ -172,10 +177,18 @@ int64_t tail_step_units(const TailStep& st) {
   return n;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CPDGPU_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int launch_tail_step(const TailStep& st, double* const* gtab, int num_sms, cudaStream_t s) {
   if (st.n == 0) return 0;
   const int64_t warps = tail_step_units(st);
-  tail_step_kernel<<<grid_for(warps * 32, 256, num_sms * 8), 256, 0, s>>>(st, gtab);
+  launch_k(tail_step_kernel, dim3(grid_for(warps * 32, 256, num_sms * 8)), dim3(256), 0, s, pdl_enabled(), st, gtab);
   return 1;
 }
 
