@@ -95,11 +95,16 @@ struct Ring {
 };
 
 // KR(1..p) rows of row block rb from the pre-built buffer (all 256 consumers).
-__device__ __forceinline__ void load_krl(const SeedParams& p, const Ring& q, int64_t rb, int tid) {
+__device__ __forceinline__ void load_krl(const SeedParams& p, const Ring& q, int64_t rb, int tid,
+                                         int nthreads = kConsumers * 32) {
   const int64_t row0 = rb * q.TI;
   const int rows = static_cast<int>(min64(q.TI, p.J - row0));
-  const double* src = p.KRl_g + row0 * q.LDK;
-  for (int e = tid; e < q.TI * q.LDK; e += kConsumers * 32) q.KRl[e] = (e / q.LDK) < rows ? src[e] : 0.0;
+  // 16-byte pieces (LDK is even), eight independent loads in flight per thread
+  const double2* src = reinterpret_cast<const double2*>(p.KRl_g + row0 * q.LDK);
+  double2* dst = reinterpret_cast<double2*>(q.KRl);
+  const int n2 = (q.TI * q.LDK) >> 1, valid = (rows * q.LDK) >> 1;
+#pragma unroll 8
+  for (int e = tid; e < n2; e += nthreads) dst[e] = e < valid ? __ldg(src + e) : make_double2(0.0, 0.0);
 }
 
 // Row-block bookkeeping shared by every role: all consumers meet at the named
@@ -148,7 +153,10 @@ __device__ void right_role(const SeedParams& p, const Ring& q, int64_t t0, int n
     const int s = k % q.stages;
     const int64_t tile = t0 + k;
     const int64_t rb = tile / p.nCT;
-    if (rb != cur_rb) row_block_change(p, q, rb, cur_rb, need_krl, tid, flush);
+    if (rb != cur_rb) {  // the right product never reads KR_l: flush and go on
+      if (cur_rb >= 0) flush(cur_rb);
+      cur_rb = rb;
+    }
     const unsigned long long w0 = clock64();
     mbar_wait(&q.full[s], (k / q.stages) & 1);
     cw += clock64() - w0;
@@ -212,12 +220,16 @@ __device__ void left_role(const SeedParams& p, const Ring& q, int64_t t0, int nt
   const int LDY = q.LDY, TI = q.TI;
   const int ksteps = TI >> 2;
   int64_t cur_rb = -1;
-  auto noflush = [](int64_t) {};
   for (int k = 0; k < ntiles; ++k) {
     const int s = k % q.stages;
     const int64_t tile = t0 + k;
     const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
-    if (rb != cur_rb) row_block_change(p, q, rb, cur_rb, true, tid, noflush);
+    if (rb != cur_rb) {  // only the four left warps read KR_l
+      asm volatile("bar.sync 2, 128;\n" ::: "memory");
+      load_krl(p, q, rb, tid - 128, 128);
+      asm volatile("bar.sync 2, 128;\n" ::: "memory");
+      cur_rb = rb;
+    }
     const unsigned long long w0 = clock64();
     mbar_wait(&q.full[s], (k / q.stages) & 1);
     cw += clock64() - w0;
@@ -271,7 +283,7 @@ __device__ void left_only_role(const SeedParams& p, const Ring& q, int64_t t0, i
     const int s = k % q.stages;
     const int64_t tile = t0 + k;
     const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
-    if (rb != cur_rb) row_block_change(p, q, rb, cur_rb, true, tid, noflush);
+    if (rb != cur_rb) row_block_change(p, q, rb, cur_rb, true, tid, [](int64_t) {});
     const unsigned long long w0 = clock64();
     mbar_wait(&q.full[s], (k / q.stages) & 1);
     cw += clock64() - w0;
