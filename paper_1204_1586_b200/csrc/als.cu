@@ -9,6 +9,9 @@
 //    shared memory (round-robin pairing, R/2 disjoint rotations per step)
 //    instead of Eigen's tridiagonal QR; the pseudo-inverse keeps the
 //    reference's cutoff rule (lambda <= rtol*max|lambda| or lambda <= 0 -> 0);
+//  * inside the ALS update a Cholesky inverse replaces the eigensolve when the
+//    matrix is certified positive definite with no eigenvalue near the cutoff
+//    (then pinv_psd(W) = W^{-1}); anything else takes the Jacobi route;
 //  * <Y, Yhat> comes from sum(A_L .* G_L) of the last updated mode L (exact:
 //    G_L was computed from the final factors of every other mode), so the fit
 //    needs no extra pass over Y.
@@ -32,16 +35,26 @@ __global__ void gram_kernel(const double* __restrict__ A, int64_t I, int R,
 }
 
 // Parallel cyclic Jacobi on the Rp x Rp (Rp even) matrix in M; V receives the
-// eigenvectors (columns).  A pair is rotated only while
-// |a_pq| > eps * sqrt(|a_pp a_qq|) (the high-relative-accuracy criterion);
-// the sweep loop stops after a sweep with no rotation.  M2 / V2 are ping-pong
-// buffers; the eigenvalues are left on the diagonal of M.
+// eigenvectors (columns).  A pair is rotated while |a_pq| is above both the
+// relative-accuracy level eps sqrt(|a_pp a_qq|) and the rounding floor of the
+// matrix, eps max_k |a_kk| (backward-stable accuracy, as a QR-based solver);
+// below the floor a rotation only shuffles rounding noise and the sweep loop
+// would never see a rotation-free sweep.  The loop stops after such a sweep.
+// M2 / V2 are ping-pong buffers; the eigenvalues are left on the diagonal of M.
 __device__ void jacobi_eig(double* M, double* M2, double* V, double* V2, double* cs, int* partner,
                            int Rp) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int RR = Rp * Rp;
   for (int e = tid; e < RR; e += nt) V[e] = (e % Rp == e / Rp) ? 1.0 : 0.0;
   __shared__ int s_rot;
+  __shared__ double s_floor;
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int x = 0; x < Rp; ++x) mx = fmax(mx, fabs(M[x + Rp * x]));
+    s_floor = 2.2e-16 * mx;  // trace-scale rounding floor (diagonal max of a PSD matrix)
+  }
+  __syncthreads();
+  const double floor_abs = s_floor;
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) s_rot = 0;
     __syncthreads();
@@ -55,7 +68,7 @@ __device__ void jacobi_eig(double* M, double* M2, double* V, double* V2, double*
         const double apq = M[p + Rp * q];
         const double app = M[p + Rp * p], aqq = M[q + Rp * q];
         double c = 1.0, s = 0.0;
-        if (apq != 0.0 && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
+        if (apq != 0.0 && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq)) && fabs(apq) > floor_abs) {
           const double theta = (aqq - app) / (2.0 * apq);
           const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
           c = 1.0 / sqrt(t * t + 1.0);
@@ -118,6 +131,71 @@ __device__ void pinv_from_eig(const double* M, const double* V, double* inv, int
   __syncthreads();
 }
 
+// Fast path of pinv_psd for a certified well-conditioned PD matrix: Cholesky
+// W = L L^T, X = W^{-1} by two triangular solves per column.  Accepted only when
+// the factorization succeeded and lambda_min >= 1 / ||X||_inf exceeds
+// 10 rtol ||W||_inf >= 10 rtol lambda_max: then no eigenvalue reaches the
+// pinv_psd cutoff and the pseudo-inverse IS the inverse.  Otherwise the caller
+// runs the Jacobi eigensolver.  L and X use the M2 / V2 scratch (ld Rp).
+__device__ bool chol_inverse(const double* W, double* L, double* X, int R, int Rp, double rtol, double* P) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ int s_fail;
+  __shared__ double s_wn, s_xn;
+  if (tid == 0) {
+    s_fail = 0;
+    s_wn = 0.0;
+    s_xn = 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < R; ++k) {
+    if (tid == 0) {
+      double d = W[k + Rp * k];
+      for (int j = 0; j < k; ++j) d -= L[k + Rp * j] * L[k + Rp * j];
+      if (!(d > 0.0)) s_fail = 1;
+      L[k + Rp * k] = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    for (int i = k + 1 + tid; i < R; i += nt) {
+      double v = W[i + Rp * k];
+      for (int j = 0; j < k; ++j) v -= L[i + Rp * j] * L[k + Rp * j];
+      L[i + Rp * k] = v / L[k + Rp * k];
+    }
+    __syncthreads();
+  }
+  if (s_fail) return false;
+  for (int c = tid; c < R; c += nt) {  // column c of W^{-1}: L y = e_c, L^T x = y
+    for (int i = 0; i < R; ++i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int j = 0; j < i; ++j) v -= L[i + Rp * j] * X[j + Rp * c];
+      X[i + Rp * c] = v / L[i + Rp * i];
+    }
+    for (int i = R - 1; i >= 0; --i) {
+      double v = X[i + Rp * c];
+      for (int j = i + 1; j < R; ++j) v -= L[j + Rp * i] * X[j + Rp * c];
+      X[i + Rp * c] = v / L[i + Rp * i];
+    }
+  }
+  __syncthreads();
+  for (int a = tid; a < R; a += nt) {  // infinity norms (row sums)
+    double w = 0.0, x = 0.0;
+    for (int c = 0; c < R; ++c) {
+      w += fabs(W[a + Rp * c]);
+      x += fabs(X[a + Rp * c]);
+    }
+    atomicMax(reinterpret_cast<unsigned long long*>(&s_wn), __double_as_longlong(w));
+    atomicMax(reinterpret_cast<unsigned long long*>(&s_xn), __double_as_longlong(x));
+  }
+  __syncthreads();
+  const bool ok = s_xn > 0.0 && (1.0 / s_xn) > 10.0 * rtol * s_wn;
+  if (ok)
+    for (int e = tid; e < R * R; e += nt) {
+      const int a = e % R, c = e / R;
+      P[a + R * c] = 0.5 * (X[a + Rp * c] + X[c + Rp * a]);
+    }
+  __syncthreads();
+  return ok;
+}
+
 struct EigSmem {
   double *M, *M2, *V, *V2, *cs, *inv, *P;
   int* partner;
@@ -170,8 +248,10 @@ __global__ void __launch_bounds__(kAlsThreads, 1)
     s.M[e] = w;
   }
   __syncthreads();
-  jacobi_eig(s.M, s.M2, s.V, s.V2, s.cs, s.partner, Rp);
-  pinv_from_eig(s.M, s.V, s.inv, R, Rp, rtol, s.P);
+  if (!chol_inverse(s.M, s.M2, s.V2, R, Rp, rtol, s.P)) {
+    jacobi_eig(s.M, s.M2, s.V, s.V2, s.cs, s.partner, Rp);
+    pinv_from_eig(s.M, s.V, s.inv, R, Rp, rtol, s.P);
+  }
   // A_n = G * P  (als.cpp:55)
   for (int64_t e = tid; e < I * R; e += nt) {
     const int64_t i = e % I;
