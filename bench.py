@@ -313,14 +313,18 @@ def run_ours(args, cfg):
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                     "tensor": {"executed_flops": 3 * flops, "achieved_tflops": 3 * tflops,
                                "note": "3 fp16 MMAs per product (hi*hi + lo*hi + hi*lo)"}}
-    else:
-        roofline = {"bound": "tensor", "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
-                    "kernel": "seed_f64_kernel (K1, fp64 DMMA)", "kernel_ms": seed_avg,
-                    "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
-                    "peak_source": "FP64 DMMA peak measured on B200 (profiles/r01_fp64_peak_microbench.txt)",
-                    "hbm": {"achieved": hbm_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                            "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0)}}
+    else:  # the binding roof is the slower ideal: bytes / HBM peak vs flops / FP64 DMMA peak
+        hbm_peak = peaks.get("hbm_gbs", 6539.9)
+        fp64 = {"achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": tflops / FP64_PEAK_TFLOPS,
+                "peak_source": "FP64 DMMA peak measured on B200 (profiles/r01_fp64_peak_microbench.txt)"}
+        hbm = {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
+               "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+        hbm_bound = bytes_alg / (hbm_peak * 1e9) > flops / (FP64_PEAK_TFLOPS * 1e12)
+        main, other = (hbm, fp64) if hbm_bound else (fp64, hbm)
+        roofline = {"bound": "hbm" if hbm_bound else "tensor", **{k: main[k] for k in ("achieved", "peak", "unit", "frac")},
+                    "traffic": traffic, "kernel": "seed_f64_kernel (K1, fp64 DMMA, both seeds in one pass)",
+                    "kernel_ms": seed_avg, "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
+                    "peak_source": main["peak_source"], ("tensor" if hbm_bound else "hbm"): other}
 
     # e2e through the host C-ABI: H2D of Y from pinned memory + factors, D2H of gradients
     e2e = None
@@ -501,6 +505,7 @@ def run_ours_als(args, cfg):
     dims, R, dtype, desc = cfg
     N = len(dims)
     slab = int(np.prod(dims))
+    esize = 8
     ctx = cpd.Context(local)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
@@ -559,7 +564,7 @@ def run_ours_als(args, cfg):
     # e2e: a full run() through the host API with Y uploaded from pinned host memory
     e2e = None
     if not args.no_e2e and world == 1 and host_memory_ok(3 * slab * esize):
-        host_y = torch.empty(slab, dtype=torch.float32 if f32 else torch.float64).pin_memory()
+        host_y = torch.empty(slab, dtype=torch.float64).pin_memory()
         host_y.copy_(torch.from_numpy(y.values()))
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
