@@ -126,30 +126,24 @@ __global__ void __launch_bounds__(256) tail_step_kernel(const TailStep st, doubl
 
 // Prologue: sorted factors Fs[j] <- input block perm[j]; output pointer table;
 // Khatri-Rao rows of every K1 chunk: out[q * LDK + r] = KR(spec)[q, r], one
-// thread per (row, 8 rank columns).
+// thread per entry (one dependent load per mode: latency, not bandwidth, is the
+// cost of this small kernel).
 __device__ void kr_rows(const KRJob& k, int64_t t, int64_t nt) {
-  const int chunks = k.LDK / 8;
-  for (int64_t e = t; e < k.L * chunks; e += nt) {
-    const int64_t q = e / chunks;
-    const int r0 = static_cast<int>(e - q * chunks) * 8;
-    double acc[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) acc[r] = r0 + r < k.R ? 1.0 : 0.0;
-    if (r0 < k.R) {
+  const int64_t total = k.L * k.LDK;
+  for (int64_t e = t; e < total; e += nt) {
+    const int64_t q = e / k.LDK;
+    const int r = static_cast<int>(e - q * k.LDK);
+    double v = r < k.R ? 1.0 : 0.0;
+    if (r < k.R) {
       int64_t rem = q;
       for (int m = 0; m < k.spec.n; ++m) {
         const int64_t I = k.spec.dims[m];
         const int64_t d = rem % I;
         rem /= I;
-        const double* a = k.spec.A[m] + d + I * r0;
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (r0 + r < k.R) acc[r] *= __ldg(a + I * r);
+        v *= __ldg(k.spec.A[m] + d + I * r);
       }
     }
-    double* dst = k.out + q * k.LDK + r0;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) dst[r] = acc[r];
+    k.out[e] = v;
   }
 }
 
@@ -197,8 +191,8 @@ const void* prologue_kernel_fn() { return reinterpret_cast<const void*>(prologue
 void prologue_geometry(const Prologue& pr, int num_sms, dim3* grid, dim3* block) {
   int64_t work = 0;
   for (int j = 0; j < pr.N; ++j) work = work > pr.len[j] ? work : pr.len[j];
-  for (int c = 0; c < pr.nkr; ++c) work = work > pr.kr[c].L * (pr.kr[c].LDK / 8) ? work : pr.kr[c].L * (pr.kr[c].LDK / 8);
-  *grid = dim3(static_cast<unsigned>(grid_for(work, 256, num_sms * 4)));
+  for (int c = 0; c < pr.nkr; ++c) work = work > pr.kr[c].L * pr.kr[c].LDK ? work : pr.kr[c].L * pr.kr[c].LDK;
+  *grid = dim3(static_cast<unsigned>(grid_for(work, 256, num_sms * 8)));
   *block = dim3(256);
 }
 
