@@ -241,9 +241,18 @@ struct Plan {
     CUtensorMap kmap{};
     bool kmap_ok = false;
     std::unique_ptr<DevBuf> KRr16, KRl16, scales;  // fp32 path: split tiles, [scale 128 | inv 128]
+    CUtensorMap kmapL{};                           // KR_l rows for the column-block left pass
+    int64_t lc_off = 0;
   };
   std::vector<Chunk> chunks;
   bool lpart_direct = false;  // one row block: the left partial is the seed itself
+  // left seed alone (ALS / hook second pass): column-block kernel
+  bool use_lc = false;
+  int64_t lc_TJ = 256, lc_nCB = 0, lc_nRT = 0, lc_U = 0;
+  int lc_P = 0, lc_slots = 0, lc_tab_len = 0, lc_tab_max = 0;
+  DevBuf lc_tab, LCpart;
+  CUtensorMap ymapL{};
+  const void* ymapL_base = nullptr;
   bool raw_frame = false;     // forced pivot: the caller's frame is used unsorted
   bool tma_ok = false;        // Y tiles by 2-D TMA (even leading extent)
   CUtensorMap tmap{};         // bound to the tensor's device address
@@ -452,6 +461,28 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
   }
   pl.Rpart.ensure(rpart * sizeof(double));
   build_slot_tab(pl.slot_tab, nRB, nCT, T, P, slots, &pl.slot_tab_ptr_len, &pl.slot_tab_max);
+  // column-block left pass (needs the TMA views of Y and of the KR_l rows)
+  if (pl.tma_ok && std::getenv("CPDGPU_NO_LC") == nullptr) {
+    pl.lc_nCB = cpdgpu::ceil_div(Kp, pl.lc_TJ);
+    pl.lc_nRT = cpdgpu::ceil_div(Jp, 32);
+    pl.lc_U = pl.lc_nCB * pl.lc_nRT;
+    pl.lc_P = static_cast<int>(std::min<int64_t>(ctx->num_sms, pl.lc_U));
+    pl.lc_slots = static_cast<int>(cpdgpu::ceil_div(cpdgpu::ceil_div(pl.lc_U, pl.lc_P), pl.lc_nRT) + 1);
+    build_slot_tab(pl.lc_tab, pl.lc_nCB, pl.lc_nRT, pl.lc_U, pl.lc_P, pl.lc_slots, &pl.lc_tab_len, &pl.lc_tab_max);
+    size_t lc = 0;
+    bool ok = true;
+    for (auto& c : pl.chunks) {
+      c.lc_off = static_cast<int64_t>(lc);
+      lc += static_cast<size_t>(pl.lc_P) * pl.lc_slots * c.NT * 8 * pl.lc_TJ;
+      ok = ok && cpdgpu::make_tensor_map_2d(&c.kmapL, c.KRl->p, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                                            static_cast<uint64_t>(c.sp.LDK), static_cast<uint64_t>(Jp),
+                                            static_cast<uint64_t>(c.sp.LDK) * 8, static_cast<uint32_t>(c.sp.LDK), 32);
+    }
+    if (ok) {
+      pl.LCpart.ensure(lc * sizeof(double));
+      pl.use_lc = true;
+    }
+  }
   if (!pl.lpart_direct) pl.Lpart.ensure(lpart * sizeof(double));
 }
 
@@ -599,6 +630,14 @@ void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
     return;
   }
   const void* ybase = pl.raw_frame ? t->data : t->sorted;
+  if (pl.use_lc && pl.ymapL_base != ybase) {
+    if (!cpdgpu::make_tensor_map_2d(&pl.ymapL, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                                    static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
+                                    static_cast<uint64_t>(pl.Jp) * 8, 16, static_cast<uint32_t>(pl.lc_TJ), true))
+      pl.use_lc = false;
+    else
+      pl.ymapL_base = ybase;
+  }
   bool tma = pl.tma_ok;
   if (tma && pl.tmap_base != ybase) {
     tma = cpdgpu::make_tensor_map_2d(&pl.tmap, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
@@ -682,7 +721,20 @@ void run_seeds(cpdgpu_ctx* ctx, Plan& pl, int mode) {
       CK(cudaMemsetAsync(tb.p, 0, tb.bytes, s));
       c.sp.trace = static_cast<unsigned long long*>(tb.p);
     }
-    ctx->launches += cpdgpu::launch_seed_f64(c.sp, &pl.tmap, &c.kmap, c.NT, mode, s);
+    if (mode == 2 && pl.use_lc) {
+      cpdgpu::SeedParams q = c.sp;
+      q.TI = static_cast<int>(pl.lc_TJ);
+      q.nRB = pl.lc_nCB;
+      q.nCT = pl.lc_nRT;
+      q.T = pl.lc_U;
+      q.P = pl.lc_P;
+      q.slots = pl.lc_slots;
+      q.stages = 3;
+      q.Rpart = pl.LCpart.d() + c.lc_off;
+      ctx->launches += cpdgpu::launch_seed_left_cols(q, &pl.ymapL, &c.kmapL, c.NT, s);
+    } else {
+      ctx->launches += cpdgpu::launch_seed_f64(c.sp, &pl.tmap, &c.kmap, c.NT, mode, s);
+    }
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
     if (trace) {
       std::vector<unsigned long long> h(static_cast<size_t>(c.sp.P) * 36);
@@ -823,7 +875,19 @@ void add_reduce_ops(const Plan& pl, cpdgpu::TailStep& st, int mode) {
       o.ldo = pl.Jp;
       st.op[st.n++] = o;
     }
-    if ((mode & 2) && !pl.lpart_direct) {
+    if (mode == 2 && pl.use_lc) {  // column-block partial slots [slot][RP][TJ]
+      cpdgpu::TailOp o = op_base(cpdgpu::kOpReduceRight, c.Rc);
+      o.Z = pl.LCpart.d() + c.lc_off;
+      o.B = pl.lc_tab_max >= 16 ? 1 : 0;
+      o.M = pl.Kp;
+      o.RP = c.NT * 8;
+      o.TI = static_cast<int>(pl.lc_TJ);
+      o.rb_ptr = static_cast<const int*>(pl.lc_tab.p);
+      o.slot_list = static_cast<const int*>(pl.lc_tab.p) + pl.lc_tab_len;
+      o.out = pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp;
+      o.ldo = pl.Kp;
+      st.op[st.n++] = o;
+    } else if ((mode & 2) && !pl.lpart_direct) {
       cpdgpu::TailOp o = op_base(cpdgpu::kOpReduceLeft, c.Rc);
       o.Z = pl.Lpart.d() + c.lpart_off;
       o.M = pl.Kp;
@@ -994,7 +1058,7 @@ void sweep_body(cpdgpu_ctx* ctx, Plan& pl, const ModeCallback& after) {
   if (pl.p + 1 <= pl.N) {
     launch_kr_from_fs(ctx, pl, 2);
     run_seeds(ctx, pl, 2);
-    if (!pl.lpart_direct) {
+    if (!pl.lpart_direct || pl.use_lc) {
       cpdgpu::TailStep st{};
       add_reduce_ops(pl, st, 2);
       launch_step(ctx, pl, st);

@@ -46,7 +46,15 @@ int launch_seed_f64(const SeedParams& p, const CUtensorMap* tmap, const CUtensor
 
 // Host helper: 2-D tiled tensor map (driver entry point, no -lcuda link).
 bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, int elem_bytes,
-                        uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1);
+                        uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1,
+                        bool swizzle128 = false);
+// Left seed alone with column-block accumulation (ALS / hook second pass): TI =
+// columns per block (256), nRB = column blocks, nCT = 32-row stages per block,
+// Rpart = partial slots [P * slots][8 NT][TI].  ymap: Y (dim0 J, dim1 K), box
+// 16 x TI, 128-byte swizzle; kmap: KR_l rows (dim0 LDK, dim1 J), box LDK x 32.
+int launch_seed_left_cols(const SeedParams& p, const CUtensorMap* ymap, const CUtensorMap* kmap, int NT,
+                          cudaStream_t s);
+size_t seed_left_cols_smem_bytes(int NT, int TJ, int stages);
 
 // ---- K1 for fp32 tensors: tcgen05 split-fp16 seed contraction (seed_f32.cu) ---
 // One pass computes ONE seed (right: blocks over the view's rows i, k-tiles over

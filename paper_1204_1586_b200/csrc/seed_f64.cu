@@ -482,6 +482,147 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- left seed with column-block accumulation (ALS / hook second pass) -----------
+// Ls[j, r] = sum_i Y[i, j] KR_l[i, r] with the MMA's M = j: a block of TJ columns
+// is walked down the rows in 32-row stages and its accumulators persist across
+// the rows, flushed once per block into the CTA's partial slot (MODE 2 wrote a
+// partial per tile and reduced four K slices per tile through shared memory).
+// Y stages arrive as two 16-row halves with 128-byte swizzle ([TJ][16] doubles,
+// 16-byte chunk c of column j at c ^ (j % 8)): conflict-free Y^T fragments.
+// The Khatri-Rao rows of each stage (32 x LDK) come by TMA like KR_r in MODE 1.
+// SeedParams reuse: TI = TJ, nRB = column blocks, nCT = 32-row stages per block,
+// T = units, Rpart = partial slots [P * slots][8 NT][TJ].
+template <int NT, int MC>
+__global__ void __launch_bounds__(kThreads, 1)
+    seed_left_cols_kernel(const SeedParams p, const __grid_constant__ CUtensorMap ymap,
+                          const __grid_constant__ CUtensorMap kmap) {
+  constexpr int RP = NT * 8;
+  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int cta = blockIdx.x;
+  const int64_t t0 = (static_cast<int64_t>(cta) * p.T) / p.P;
+  const int64_t t1 = (static_cast<int64_t>(cta + 1) * p.T) / p.P;
+  if (t0 >= t1) return;
+  const int ntiles = static_cast<int>(t1 - t0);
+  const int TJ = p.TI, STAGES = p.stages;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  double* Ys = reinterpret_cast<double*>(base);                  // [STAGES][2][TJ][16]
+  double* KRs = Ys + STAGES * kTJ * TJ;                           // [STAGES][32][LDK]
+  uint64_t* full = reinterpret_cast<uint64_t*>(KRs + STAGES * kTJ * LDK);
+  uint64_t* empty = full + 4;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == kConsumers && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+
+  if (warp == kConsumers) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint32_t bytes = kTJ * TJ * 8 + kTJ * LDK * 8;
+      auto load_y = [&](int k, int s) {
+        const int64_t u = t0 + k, cb = u / p.nCT, rt = u - cb * p.nCT;
+        double* ys = Ys + s * kTJ * TJ;
+        tma_load_2d(ys, &ymap, static_cast<int>(rt * kTJ), static_cast<int>(cb * TJ), &full[s]);
+        tma_load_2d(ys + 16 * TJ, &ymap, static_cast<int>(rt * kTJ + 16), static_cast<int>(cb * TJ), &full[s]);
+      };
+      auto load_k = [&](int k, int s) {
+        const int64_t u = t0 + k, rt = u % p.nCT;
+        tma_load_2d(KRs + s * kTJ * LDK, &kmap, 0, static_cast<int>(rt * kTJ), &full[s]);
+      };
+      const int early = min(STAGES, ntiles);
+      for (int k = 0; k < early; ++k) {  // Y does not depend on the preceding kernel (PDL)
+        mbar_arrive_tx(&full[k], bytes);
+        load_y(k, k);
+      }
+      pdl_wait();
+      for (int k = 0; k < early; ++k) load_k(k, k);
+      for (int k = early; k < ntiles; ++k) {
+        const int s = k % STAGES;
+        mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
+        mbar_arrive_tx(&full[s], bytes);
+        load_y(k, s);
+        load_k(k, s);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
+  pdl_wait();
+  double acc[MC > 0 ? MC : 1][NT][2];
+#pragma unroll
+  for (int m = 0; m < MC; ++m)
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb) acc[m][nb][0] = acc[m][nb][1] = 0.0;
+  const int64_t slot_cb0 = t0 / p.nCT;
+  auto flush = [&](int64_t cb) {
+    double* dst = p.Rpart + (static_cast<int64_t>(cta) * p.slots + (cb - slot_cb0)) * RP * TJ;
+#pragma unroll
+    for (int m = 0; m < MC; ++m) {
+      const int j = (warp + kConsumers * m) * 8 + g;
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        const int r = nb * 8 + 2 * t;
+        dst[r * TJ + j] = acc[m][nb][0];
+        dst[(r + 1) * TJ + j] = acc[m][nb][1];
+        acc[m][nb][0] = acc[m][nb][1] = 0.0;
+      }
+    }
+  };
+  // byte offset of Y^T fragment element (k-step ks, row-fragment m) inside a stage
+  auto yoff = [&](int ks, int m) {
+    const int j = (warp + kConsumers * m) * 8 + g;
+    const int ip = (4 * ks + t) & 15;
+    return (ks >> 2) * (16 * TJ * 8) + j * 128 + (((ip >> 1) ^ (j & 7)) << 4) + (ip & 1) * 8;
+  };
+  int64_t cur_cb = -1;
+  for (int k = 0; k < ntiles; ++k) {
+    const int s = k % STAGES;
+    const int64_t cb = (t0 + k) / p.nCT;
+    if (cb != cur_cb) {
+      if (cur_cb >= 0) flush(cur_cb);
+      cur_cb = cb;
+    }
+    mbar_wait(&full[s], (k / STAGES) & 1);
+    const unsigned char* ys = reinterpret_cast<const unsigned char*>(Ys + s * kTJ * TJ);
+    const double* kb = KRs + s * kTJ * LDK + t * LDK + g;
+    double a[2][MC > 0 ? MC : 1], b[2][NT];
+#pragma unroll
+    for (int m = 0; m < MC; ++m) a[0][m] = *reinterpret_cast<const double*>(ys + yoff(0, m));
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb) b[0][nb] = kb[nb * 8];
+#pragma unroll
+    for (int ks = 0; ks < kTJ / 4; ++ks) {
+      const int cur = ks & 1, nxt = cur ^ 1;
+      if (ks + 1 < kTJ / 4) {
+#pragma unroll
+        for (int m = 0; m < MC; ++m) a[nxt][m] = *reinterpret_cast<const double*>(ys + yoff(ks + 1, m));
+#pragma unroll
+        for (int nb = 0; nb < NT; ++nb) b[nxt][nb] = kb[(ks + 1) * 4 * LDK + nb * 8];
+      }
+#pragma unroll
+      for (int m = 0; m < MC; ++m)
+#pragma unroll
+        for (int nb = 0; nb < NT; ++nb) dmma(acc[m][nb], a[cur][m], b[cur][nb]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (cur_cb >= 0) flush(cur_cb);
+}
+
 template <int NT, int MODE>
 void launch_one(const SeedParams& p, const CUtensorMap& tmap, const CUtensorMap& kmap, cudaStream_t s,
                 size_t smem) {
@@ -516,6 +657,36 @@ size_t seed_f64_smem_bytes(int NT, int TI, int LDY, int LDK, int mode, int stage
   return 256 + d * sizeof(double);  // barriers + 128-byte alignment slack
 }
 
+size_t seed_left_cols_smem_bytes(int NT, int TJ, int stages) {
+  const int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  return 1024 + static_cast<size_t>(stages) * kTJ * (TJ + LDK) * sizeof(double) + 64;
+}
+
+template <int NT>
+void launch_lc(const SeedParams& p, const CUtensorMap& ym, const CUtensorMap& km, cudaStream_t s, size_t smem) {
+  constexpr int MC = 4;  // TJ = 8 warps x 4 fragments x 8 = 256 columns
+  auto fn = seed_left_cols_kernel<NT, MC>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    configured = true;
+  }
+  launch_k(fn, dim3(p.P), dim3(kThreads), smem, s, pdl_enabled(), p, ym, km);
+}
+
+int launch_seed_left_cols(const SeedParams& p, const CUtensorMap* ymap, const CUtensorMap* kmap, int NT,
+                          cudaStream_t s) {
+  const size_t smem = seed_left_cols_smem_bytes(NT, p.TI, p.stages);
+  switch (NT) {
+    case 1: launch_lc<1>(p, *ymap, *kmap, s, smem); break;
+    case 2: launch_lc<2>(p, *ymap, *kmap, s, smem); break;
+    case 3: launch_lc<3>(p, *ymap, *kmap, s, smem); break;
+    case 4: launch_lc<4>(p, *ymap, *kmap, s, smem); break;
+    default: return 0;
+  }
+  return 1;
+}
+
 int launch_seed_f64(const SeedParams& p, const CUtensorMap* tmap, const CUtensorMap* kmap, int NT, int mode,
                     cudaStream_t s) {
   CUtensorMap dummy;
@@ -534,7 +705,8 @@ int launch_seed_f64(const SeedParams& p, const CUtensorMap* tmap, const CUtensor
 }
 
 bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, int elem_bytes,
-                        uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
+                        uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1,
+                        bool swizzle128) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -552,7 +724,7 @@ bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType 
   const cuuint32_t box[2] = {box0, box1};
   const cuuint32_t estride[2] = {1, 1};
   return encode(out, dtype, 2, const_cast<void*>(base), gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
