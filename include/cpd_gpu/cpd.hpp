@@ -419,6 +419,22 @@ inline std::vector<Matrix> cp_gradient_all(const DenseTensor& y, const FactorLis
   return cp_gradient_all(y, copy, counter, ModeHook{}, stats);
 }
 
+// ---- direct MTTKRP (mttkrp.hpp:19-20): one pass over Y per mode ----------------------------
+inline Matrix mttkrp_direct(const DenseTensor& y, const FactorList& factors, int n, CostCounter* counter = nullptr) {
+  const int N = y.order();
+  if (n < 1 || n > N) throw IndexError("mttkrp_direct: mode " + std::to_string(n) + " outside 1.." + std::to_string(N));
+  detail::check_factors_match(y, factors, "mttkrp_direct");
+  const index_t R = factor_rank(factors);
+  auto& ctx = gpu::context();
+  std::vector<const double*> fp(factors.size());
+  for (size_t k = 0; k < factors.size(); ++k) fp[k] = factors[k].data();
+  Matrix out(y.shape().dim(n), R);
+  uint64_t mults = 0;
+  ctx.check(cpdgpu_mttkrp_direct(ctx.h, y.device(), R, fp.data(), n, out.data(), &mults));
+  if (counter) counter->charge(mults);
+  return out;
+}
+
 // ---- ALS (als.hpp:21-93, kruskal.hpp:14-29) -----------------------------------------------
 class KruskalModel {
  public:
@@ -501,6 +517,20 @@ inline void als_sweep_fast(const DenseTensor& y, FactorList& factors, double pin
   ctx.check(cpdgpu_als_sweep(ctx.h, y.device(), R, fp.data(), pinv_rtol, nullptr, &mults));
   if (counter) counter->charge(mults);
   (void)stats;
+}
+
+// als_sweep_direct (als.hpp:58-60): direct MTTKRP + update per mode of `order`.
+inline void als_sweep_direct(const DenseTensor& y, FactorList& factors, const std::vector<int>& order,
+                             double pinv_rtol = 1e-12, CostCounter* counter = nullptr) {
+  detail::check_factors_match(y, factors, "als_sweep_direct");
+  const index_t R = factor_rank(factors);
+  auto& ctx = gpu::context();
+  std::vector<double*> fp(factors.size());
+  for (size_t k = 0; k < factors.size(); ++k) fp[k] = factors[k].data();
+  uint64_t mults = 0;
+  ctx.check(cpdgpu_als_sweep_direct(ctx.h, y.device(), R, fp.data(), order.data(), static_cast<int>(order.size()),
+                                    pinv_rtol, &mults));
+  if (counter) counter->charge(mults);
 }
 
 // run(y, init, Algorithm::als_fast, opts) (als.cpp:147-210).  The device path

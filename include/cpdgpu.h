@@ -122,6 +122,19 @@ int cpdgpu_cp_gradient_all_hook(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R,
 int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R,
                                   const double* factors_dev, double* gradients_dev, int pivot);
 
+/* ---- direct MTTKRP (Algorithm 1 cost model; mttkrp.hpp:19-20, mttkrp.cpp:29-54)
+ * One pass over Y for one mode: out = Y_(n) (KR_{k != n} A(k)), I_n x R column-major,
+ * caller's mode order; mults (optional) receives the reference's charge. */
+int cpdgpu_mttkrp_direct(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const double* const* factors, int n,
+                         double* out, uint64_t* mults);
+/* Device form: packed factors in, block n of the packed gradient buffer written. */
+int cpdgpu_mttkrp_direct_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const double* factors_dev, int n,
+                                double* gradients_dev);
+/* als_sweep_direct (als.hpp:58-60, als.cpp:58-67): modes in `order` (1-based), each
+ * update sees the previous ones; factors updated in place. */
+int cpdgpu_als_sweep_direct(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, const int* order,
+                            int norder, double pinv_rtol, uint64_t* mults);
+
 /* ---- fast CP_ALS (als.hpp:48-93) ----------------------------------------- */
 /* pinv_psd (als.cpp:34-47) of a host R x R symmetric matrix, on the device. */
 int cpdgpu_pinv_psd(cpdgpu_ctx* ctx, int64_t R, const double* s, double rtol, double* out);

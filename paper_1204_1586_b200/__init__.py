@@ -8,7 +8,8 @@ from .errors import (ArgumentError, CpdError, DeviceError, DomainError, IndexErr
 from .api import (DIST_NORMAL, DIST_UNIFORM_PM1, F32, F64, Context, CostCounter, DenseTensor,
                   FastStats, RunTrace, SolveOptions, SolveResult, als_sweep_fast, als_update_mode,
                   cp_gradient_all, cp_gradient_all_device, default_context, fast_count_realized,
-                  fast_update_order, pinv_psd, run, select_pivot, sort_modes)
+                  fast_update_order, pinv_psd, run, select_pivot, sort_modes, mttkrp_direct,
+                  mttkrp_direct_device, als_sweep_direct)
 
 __all__ = [
     "ArgumentError", "CpdError", "DeviceError", "DomainError", "IndexError", "NumericError",
@@ -16,4 +17,5 @@ __all__ = [
     "DenseTensor", "FastStats", "RunTrace", "SolveOptions", "SolveResult", "als_sweep_fast",
     "als_update_mode", "cp_gradient_all", "cp_gradient_all_device", "default_context",
     "fast_count_realized", "fast_update_order", "pinv_psd", "run", "select_pivot", "sort_modes",
+    "mttkrp_direct", "mttkrp_direct_device", "als_sweep_direct",
 ]

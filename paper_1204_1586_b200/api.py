@@ -341,6 +341,49 @@ def cp_gradient_all_device(y: DenseTensor, R: int, factors_dev_ptr: int, grads_d
                                                     C.c_void_p(grads_dev_ptr), int(pivot)), ctx.h)
 
 
+# ---- direct MTTKRP (mttkrp.hpp:19-20): Algorithm 1's one-pass-per-mode cost ---------
+
+def mttkrp_direct(y: DenseTensor, factors: list, n: int, counter: Optional[CostCounter] = None) -> np.ndarray:
+    """M^(n) = Y_(n) (KR_{k != n} A^(k)) for one mode (mttkrp.cpp:29-54), on the device:
+    one pass over Y per call (the baseline the all-mode recursion is measured against)."""
+    bufs = _factor_bufs(factors, y.dims)
+    R = bufs[0].shape[1]
+    if not 1 <= n <= len(y.dims):
+        raise errors.IndexError(f"mttkrp_direct: mode {n} outside 1..{len(y.dims)}")
+    out = np.empty((y.dims[n - 1], R), dtype=np.float64, order="F")
+    mults = C.c_uint64()
+    ctx = y.ctx
+    _lib.check(ctx._L.cpdgpu_mttkrp_direct(ctx.h, y.h, R, _ptr_array(bufs), int(n),
+                                           out.ctypes.data_as(_lib.c_dbl_p), C.byref(mults)), ctx.h)
+    if counter is not None:
+        counter.charge(int(mults.value))
+    return out
+
+
+def mttkrp_direct_device(y: DenseTensor, R: int, factors_dev_ptr: int, grads_dev_ptr: int, n: int) -> None:
+    """Device-buffer form (packed factors in, block n of the packed gradients written)."""
+    ctx = y.ctx
+    _lib.check(ctx._L.cpdgpu_mttkrp_direct_device(ctx.h, y.h, int(R), C.c_void_p(factors_dev_ptr), int(n),
+                                                  C.c_void_p(grads_dev_ptr)), ctx.h)
+
+
+def als_sweep_direct(y: DenseTensor, factors: list, order: Sequence[int], pinv_rtol: float = 1e-12,
+                     counter: Optional[CostCounter] = None) -> None:
+    """One ALS sweep over `order` with direct MTTKRPs (als.cpp:58-67); factors updated in place."""
+    bufs = _factor_bufs(factors, y.dims)
+    R = bufs[0].shape[1]
+    bufs = [np.asfortranarray(b).copy(order="F") for b in bufs]
+    arr = (C.c_int * len(order))(*[int(n) for n in order])
+    mults = C.c_uint64()
+    ctx = y.ctx
+    _lib.check(ctx._L.cpdgpu_als_sweep_direct(ctx.h, y.h, R, _ptr_array(bufs), arr, len(order), pinv_rtol,
+                                              C.byref(mults)), ctx.h)
+    for k, b in enumerate(bufs):
+        factors[k] = b
+    if counter is not None:
+        counter.charge(int(mults.value))
+
+
 # ---- ALS (als.hpp:48-93) ---------------------------------------------------------
 
 def pinv_psd(s: np.ndarray, rtol: float = 1e-12, ctx: Optional[Context] = None) -> np.ndarray:

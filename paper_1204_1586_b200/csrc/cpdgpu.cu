@@ -1141,6 +1141,52 @@ void run_gradient(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_bas
   ctx->launches += pl.grad_graph_launches;
 }
 
+// Direct mode-n MTTKRP (Algorithm 1's cost: one pass over Y per mode) with the
+// seed machinery at a forced split: for n < N the right seed at split n,
+// R^(n) = Y_(1:n) KR(n+1..N), then G(n) = extraction with KR(1..n-1) (the identity
+// copy for n = 1); for n = N the left seed at split N-1 is G(N) itself.  The plan
+// comes from get_plan(.., pivot = min(n, N-1)) in the caller's mode frame.
+void direct_body(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_base, int n) {
+  const bool right = n < pl.N;
+  ctx->launches += cpdgpu::launch_prologue(grad_prologue(pl, fin, gout_base, right ? 1 : 2),
+                                           static_cast<double**>(pl.gtab.p), ctx->num_sms, ctx->stream);
+  run_seeds(ctx, pl, right ? 1 : 2);
+  cpdgpu::TailStep st{};
+  add_reduce_ops(pl, st, right ? 1 : 2);
+  if (right && n == 1) redirect_to_gradient(pl, st, true);
+  if (!right && st.n > 0) redirect_to_gradient(pl, st, false);
+  if (st.n > 0) launch_step(ctx, pl, st);
+  if (right && n >= 2) {
+    cpdgpu::TailStep s2{};
+    add_right_extract(pl, s2, n, pl.Rs.d());
+    launch_step(ctx, pl, s2);
+  } else if (!right && st.n == 0) {  // the left seed was written to Ls directly (one row block)
+    cpdgpu::TailStep s2{};
+    add_left_extract(pl, s2, n, pl.Ls.d());
+    launch_step(ctx, pl, s2);
+  }
+  CK(cudaGetLastError());
+}
+
+// mttkrp_direct's multiplication charge (mttkrp.cpp:29-54, kron.cpp:85-93):
+// R (J_N + sum_{k=2}^{n-1} J_k + sum_{k=n+1}^{N} J_k / I_n), caller's mode order.
+uint64_t direct_count(const std::vector<int64_t>& dims, int64_t R, int n) {
+  const int N = static_cast<int>(dims.size());
+  std::vector<uint64_t> J(static_cast<size_t>(N) + 1, 1);
+  for (int k = 1; k <= N; ++k) J[k] = J[k - 1] * static_cast<uint64_t>(dims[k - 1]);
+  uint64_t s = J[N];
+  for (int k = 2; k <= n - 1; ++k) s += J[k];
+  for (int k = n + 1; k <= N; ++k) s += J[k] / static_cast<uint64_t>(dims[n - 1]);
+  return static_cast<uint64_t>(R) * s;
+}
+
+Plan& direct_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, int n) {
+  const int N = static_cast<int>(y->dims.size());
+  Plan& pl = *get_plan(ctx, y, R, n < N ? n : N - 1);
+  bind_seed_inputs(ctx, pl, y);
+  return pl;
+}
+
 void upload_host_factors(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const double* const* factors) {
   for (int m = 0; m < pl.N; ++m)
     std::memcpy(pl.hF.d() + pl.off_orig[m], factors[m],
@@ -1630,6 +1676,60 @@ int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, 
     bind_seed_inputs(ctx, pl, y);
     run_gradient(ctx, pl, factors_dev, gradients_dev);
     CK(cudaGetLastError());
+  });
+}
+
+int cpdgpu_mttkrp_direct(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const double* const* factors, int n,
+                         double* out, uint64_t* mults) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "mttkrp_direct");
+    const int N = static_cast<int>(y->dims.size());
+    if (n < 1 || n > N) fail(CPDGPU_INDEX_ERROR, "mttkrp_direct: mode %d outside 1..%d", n, N);
+    if (!factors || !out) fail(CPDGPU_ARGUMENT_ERROR, "mttkrp_direct: null factor list or output");
+    Plan& pl = direct_plan(ctx, y, R, n);
+    upload_host_factors(ctx, pl, y, factors);
+    direct_body(ctx, pl, pl.Forig.d(), pl.Gorig.d(), n);
+    CK(cudaMemcpyAsync(out, pl.Gorig.d() + pl.off_orig[n - 1], static_cast<size_t>(y->dims[n - 1] * R) * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (mults) *mults = direct_count(y->dims, R, n);
+  });
+}
+
+int cpdgpu_mttkrp_direct_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const double* factors_dev, int n,
+                                double* gradients_dev) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "mttkrp_direct");
+    const int N = static_cast<int>(y->dims.size());
+    if (n < 1 || n > N) fail(CPDGPU_INDEX_ERROR, "mttkrp_direct: mode %d outside 1..%d", n, N);
+    if (!factors_dev || !gradients_dev) fail(CPDGPU_ARGUMENT_ERROR, "mttkrp_direct: null device buffer");
+    Plan& pl = direct_plan(ctx, y, R, n);
+    direct_body(ctx, pl, factors_dev, gradients_dev, n);
+  });
+}
+
+int cpdgpu_als_sweep_direct(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, const int* order,
+                            int norder, double pinv_rtol, uint64_t* mults) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "als_sweep_direct");
+    const int N = static_cast<int>(y->dims.size());
+    if (!factors || (norder > 0 && !order)) fail(CPDGPU_ARGUMENT_ERROR, "als_sweep_direct: null argument");
+    if (pinv_rtol < 0.0) fail(CPDGPU_ARGUMENT_ERROR, "pinv_psd: rtol must be nonnegative");
+    if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "als_sweep_direct: rank above the device ALS limit 64");
+    uint64_t total = 0;
+    std::vector<double> m;
+    for (int i = 0; i < norder; ++i) {  // als.cpp:58-67: each update sees the previous ones
+      const int n = order[i];
+      if (n < 1 || n > N) fail(CPDGPU_INDEX_ERROR, "als_sweep_direct: mode %d outside 1..%d", n, N);
+      m.resize(static_cast<size_t>(y->dims[n - 1] * R));
+      uint64_t c = 0;
+      int st = cpdgpu_mttkrp_direct(ctx, y, R, factors, n, m.data(), &c);
+      if (st != CPDGPU_OK) fail(st, "%s", ctx->err.c_str());
+      total += c;
+      st = cpdgpu_als_update_mode(ctx, N, y->dims.data(), R, m.data(), factors, n, pinv_rtol, factors[n - 1]);
+      if (st != CPDGPU_OK) fail(st, "%s", ctx->err.c_str());
+    }
+    if (mults) *mults = total;
   });
 }
 

@@ -238,6 +238,18 @@ void test_counts_and_workspace() {  // test_counts.cpp:16-31, test_mttkrp.cpp:18
   CHECK(throws<cpd::IndexError>([&] { cpd::fast_count_realized(y.shape(), 3, 0); }));
 }
 
+void test_direct() {  // mttkrp_direct (test_mttkrp.cpp-style: equals brute force for every mode)
+  const std::vector<cpd::index_t> d = {5, 4, 6, 3};
+  auto y = random_tensor(d, 77);
+  auto f = random_factors(d, 4, 78);
+  for (int n = 1; n <= 4; ++n) CHECK_LT(max_rel_diff(cpd::mttkrp_direct(y, f, n), brute(y, f, n)), 1e-12);
+  CHECK(throws<cpd::IndexError>([&] { cpd::mttkrp_direct(y, f, 5); }));
+  cpd::FactorList a = f, b = f;
+  cpd::als_sweep_direct(y, a, {1, 2, 3, 4});
+  for (int n = 1; n <= 4; ++n) b[static_cast<size_t>(n - 1)] = cpd::als_update_mode(brute(y, b, n), b, n);
+  for (int k = 0; k < 4; ++k) CHECK_LT(max_rel_diff(a[static_cast<size_t>(k)], b[static_cast<size_t>(k)]), 1e-10);
+}
+
 void test_errors() {  // errors.hpp mapping
   auto y = random_tensor({3, 4, 5}, 7);
   auto f = random_factors({3, 4, 6}, 2, 8);
@@ -310,6 +322,7 @@ int main() {
     test_hook_gauss_seidel();
     test_counts_and_workspace();
     test_errors();
+    test_direct();
     test_pinv_and_als();
   } catch (const std::exception& e) {
     std::fprintf(stderr, "uncaught: %s\n", e.what());
