@@ -326,6 +326,25 @@ def run_ours(args, cfg):
                     "kernel_ms": seed_avg, "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
                     "peak_source": main["peak_source"], ("tensor" if hbm_bound else "hbm"): other}
 
+    # the paper's comparison (Algorithm 1 vs 2): N direct mode-n MTTKRPs, one pass over Y each
+    alg1 = None
+    if world == 1 and not args.no_alg1:
+        reps = 3
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+        for i in range(reps + 1):
+            if i:
+                flush.zero_()
+                ev[2 * (i - 1)].record(stream)
+            for n in range(1, N + 1):
+                cpd.mttkrp_direct_device(y, R, fdev.data_ptr(), gdev.data_ptr(), n)
+            if i:
+                ev[2 * (i - 1) + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        a_ms = float(np.mean([ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(reps)]))
+        alg1 = {"ms_per_step": a_ms, "rho": a_ms / ms,
+                "what": f"all-mode gradient as {N} direct mode-n MTTKRPs (mttkrp_direct, one pass over Y each) "
+                        "on the same device, same inputs; rho = Algorithm 1 time / Algorithm 2 time"}
+
     # e2e through the host C-ABI: H2D of Y from pinned memory + factors, D2H of gradients
     e2e = None
     if not args.no_e2e and world == 1 and host_memory_ok(3 * slab * esize):
@@ -364,7 +383,7 @@ def run_ours(args, cfg):
                        "l2": ("flushed before every step (256 MiB memset outside the events)" if flush_needed
                               else "inputs larger than L2 (no flush)")},
             "gpu_launches": gpu_launches, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "algorithm1_direct": alg1, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -625,6 +644,7 @@ def main():
     ap.add_argument("--config", choices=list(CONFIGS), default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-alg1", action="store_true", help="skip the Algorithm 1 (direct MTTKRP) comparison")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

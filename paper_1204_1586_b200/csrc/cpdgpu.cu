@@ -1141,29 +1141,47 @@ void run_gradient(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_bas
   ctx->launches += pl.grad_graph_launches;
 }
 
-// Direct mode-n MTTKRP (Algorithm 1's cost: one pass over Y per mode) with the
-// seed machinery at a forced split: for n < N the right seed at split n,
-// R^(n) = Y_(1:n) KR(n+1..N), then G(n) = extraction with KR(1..n-1) (the identity
-// copy for n = 1); for n = N the left seed at split N-1 is G(N) itself.  The plan
-// comes from get_plan(.., pivot = min(n, N-1)) in the caller's mode frame.
+// Direct mode-n MTTKRP (Algorithm 1's cost model: one pass over Y per mode)
+// with the gradient's own machinery in the sorted frame: sorted mode j <= p* takes
+// the right seed at p* and the right recursions down to j (extraction at j);
+// j > p* takes the left seed (column-block pass) and the left recursions up to j.
+// One seed pass plus small recursions per call, for any aspect ratio.
 void direct_body(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_base, int n) {
-  const bool right = n < pl.N;
+  int j = 1;
+  while (pl.perm[j - 1] != n) ++j;  // sorted position of caller mode n
+  const bool right = j <= pl.p;
   ctx->launches += cpdgpu::launch_prologue(grad_prologue(pl, fin, gout_base, right ? 1 : 2),
                                            static_cast<double**>(pl.gtab.p), ctx->num_sms, ctx->stream);
   run_seeds(ctx, pl, right ? 1 : 2);
-  cpdgpu::TailStep st{};
-  add_reduce_ops(pl, st, right ? 1 : 2);
-  if (right && n == 1) redirect_to_gradient(pl, st, true);
-  if (!right && st.n > 0) redirect_to_gradient(pl, st, false);
-  if (st.n > 0) launch_step(ctx, pl, st);
-  if (right && n >= 2) {
-    cpdgpu::TailStep s2{};
-    add_right_extract(pl, s2, n, pl.Rs.d());
-    launch_step(ctx, pl, s2);
-  } else if (!right && st.n == 0) {  // the left seed was written to Ls directly (one row block)
-    cpdgpu::TailStep s2{};
-    add_left_extract(pl, s2, n, pl.Ls.d());
-    launch_step(ctx, pl, s2);
+  {
+    cpdgpu::TailStep st{};
+    add_reduce_ops(pl, st, right ? 1 : 2);
+    if (st.n > 0) launch_step(ctx, pl, st);
+  }
+  if (right) {
+    double* rc = pl.Rs.d();
+    double* rn = pl.Rtmp.d();
+    for (int k = pl.p; k > j; --k) {
+      cpdgpu::TailStep s{};
+      add_right_recurse(pl, s, k, rc, rn);
+      launch_step(ctx, pl, s);
+      std::swap(rc, rn);
+    }
+    cpdgpu::TailStep s{};
+    add_right_extract(pl, s, j, rc);
+    launch_step(ctx, pl, s);
+  } else {
+    double* lc = pl.Ls.d();
+    double* ln = pl.Ltmp.d();
+    for (int k = pl.p + 1; k < j; ++k) {
+      cpdgpu::TailStep s{};
+      add_left_recurse(pl, s, k, lc, ln);
+      launch_step(ctx, pl, s);
+      std::swap(lc, ln);
+    }
+    cpdgpu::TailStep s{};
+    add_left_extract(pl, s, j, lc);
+    launch_step(ctx, pl, s);
   }
   CK(cudaGetLastError());
 }
@@ -1180,9 +1198,9 @@ uint64_t direct_count(const std::vector<int64_t>& dims, int64_t R, int n) {
   return static_cast<uint64_t>(R) * s;
 }
 
-Plan& direct_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, int n) {
-  const int N = static_cast<int>(y->dims.size());
-  Plan& pl = *get_plan(ctx, y, R, n < N ? n : N - 1);
+Plan& direct_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R) {
+  ensure_sorted(ctx, y);
+  Plan& pl = *get_plan(ctx, y, R, 0);
   bind_seed_inputs(ctx, pl, y);
   return pl;
 }
@@ -1686,7 +1704,7 @@ int cpdgpu_mttkrp_direct(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const dou
     const int N = static_cast<int>(y->dims.size());
     if (n < 1 || n > N) fail(CPDGPU_INDEX_ERROR, "mttkrp_direct: mode %d outside 1..%d", n, N);
     if (!factors || !out) fail(CPDGPU_ARGUMENT_ERROR, "mttkrp_direct: null factor list or output");
-    Plan& pl = direct_plan(ctx, y, R, n);
+    Plan& pl = direct_plan(ctx, y, R);
     upload_host_factors(ctx, pl, y, factors);
     direct_body(ctx, pl, pl.Forig.d(), pl.Gorig.d(), n);
     CK(cudaMemcpyAsync(out, pl.Gorig.d() + pl.off_orig[n - 1], static_cast<size_t>(y->dims[n - 1] * R) * sizeof(double),
@@ -1703,7 +1721,7 @@ int cpdgpu_mttkrp_direct_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, co
     const int N = static_cast<int>(y->dims.size());
     if (n < 1 || n > N) fail(CPDGPU_INDEX_ERROR, "mttkrp_direct: mode %d outside 1..%d", n, N);
     if (!factors_dev || !gradients_dev) fail(CPDGPU_ARGUMENT_ERROR, "mttkrp_direct: null device buffer");
-    Plan& pl = direct_plan(ctx, y, R, n);
+    Plan& pl = direct_plan(ctx, y, R);
     direct_body(ctx, pl, factors_dev, gradients_dev, n);
   });
 }
