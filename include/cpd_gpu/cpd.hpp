@@ -533,12 +533,31 @@ inline void als_sweep_direct(const DenseTensor& y, FactorList& factors, const st
   if (counter) counter->charge(mults);
 }
 
-// run(y, init, Algorithm::als_fast, opts) (als.cpp:147-210).  The device path
-// implements the fast ALS engine; the other algorithms are not on it.
+// mu_sweep (als.hpp:68-71): multiplicative updates; negative entries -> DomainError.
+inline void mu_sweep(const DenseTensor& y, FactorList& factors, double eps = 1e-12, CostCounter* counter = nullptr) {
+  detail::check_factors_match(y, factors, "mu_sweep");
+  auto& ctx = gpu::context();
+  std::vector<double*> fp(factors.size());
+  for (size_t k = 0; k < factors.size(); ++k) fp[k] = factors[k].data();
+  uint64_t mults = 0;
+  ctx.check(cpdgpu_mu_sweep(ctx.h, y.device(), factor_rank(factors), fp.data(), eps, &mults));
+  if (counter) counter->charge(mults);
+}
+
+// gd_step (als.hpp:73-76): simultaneous gradient step.
+inline void gd_step(const DenseTensor& y, FactorList& factors, double eta, CostCounter* counter = nullptr) {
+  detail::check_factors_match(y, factors, "gd_step");
+  auto& ctx = gpu::context();
+  std::vector<double*> fp(factors.size());
+  for (size_t k = 0; k < factors.size(); ++k) fp[k] = factors[k].data();
+  uint64_t mults = 0;
+  ctx.check(cpdgpu_gd_step(ctx.h, y.device(), factor_rank(factors), fp.data(), eta, &mults));
+  if (counter) counter->charge(mults);
+}
+
+// run(y, init, algo, opts) (als.cpp:147-210) for every Algorithm on the device.
 inline SolveResult run(const DenseTensor& y, const KruskalModel& init, Algorithm algo, const SolveOptions& opts = {},
                        CostCounter* counter = nullptr) {
-  if (algo != Algorithm::als_fast)
-    throw ArgumentError("run: only Algorithm::als_fast runs on the device path");
   if (opts.max_iters < 1) throw ArgumentError("run: max_iters must be at least 1");
   if (opts.tol < 0.0 || opts.pinv_rtol < 0.0 || opts.mu_eps < 0.0)
     throw ArgumentError("run: tolerances must be nonnegative");
@@ -555,8 +574,10 @@ inline SolveResult run(const DenseTensor& y, const KruskalModel& init, Algorithm
   tr.seconds.resize(n);
   tr.mults.resize(n);
   int iters = 0;
-  ctx.check(cpdgpu_als_run(ctx.h, y.device(), R, fp.data(), opts.max_iters, opts.tol, opts.pinv_rtol,
-                           tr.cost.data(), tr.rel_error.data(), tr.seconds.data(), tr.mults.data(), &iters));
+  const int code = algo == Algorithm::als_direct ? 0 : algo == Algorithm::als_fast ? 1 : algo == Algorithm::mu ? 2 : 3;
+  ctx.check(cpdgpu_run_algo(ctx.h, y.device(), R, fp.data(), code, opts.order == UpdateOrder::pivot ? 1 : 0,
+                            opts.max_iters, opts.tol, opts.pinv_rtol, opts.mu_eps, opts.gd_eta, tr.cost.data(),
+                            tr.rel_error.data(), tr.seconds.data(), tr.mults.data(), &iters));
   tr.iters_run = iters;
   tr.cost.resize(static_cast<size_t>(iters));
   tr.rel_error.resize(static_cast<size_t>(iters));

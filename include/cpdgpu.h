@@ -147,6 +147,19 @@ int cpdgpu_als_update_mode(cpdgpu_ctx* ctx, int N, const int64_t* dims, int64_t 
  * cost_out (optional) receives cost(y, model) after the sweep (kruskal.cpp:58-77). */
 int cpdgpu_als_sweep(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors,
                      double pinv_rtol, double* cost_out, uint64_t* mults);
+/* mu_sweep (als.cpp:80-91): A <- A .* G ./ (A W + eps) per mode through the
+ * Gauss-Seidel sweep; negative tensor / factor entries -> DomainError. */
+int cpdgpu_mu_sweep(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, double eps,
+                    uint64_t* mults);
+/* gd_step (als.cpp:93-101): a <- a + 2 eta (M - A W) for all modes at the pre-step factors. */
+int cpdgpu_gd_step(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, double eta,
+                   uint64_t* mults);
+/* run(y, init, algo, opts) (als.cpp:147-210) for every Algorithm: 0 als_direct
+ * (order_pivot != 0: fast_update_order, else 1..N), 1 als_fast, 2 mu, 3 gd. */
+int cpdgpu_run_algo(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, int algo,
+                    int order_pivot, int max_iters, double tol, double pinv_rtol, double mu_eps, double gd_eta,
+                    double* cost_trace, double* rel_trace, double* sec_trace, uint64_t* mults_trace,
+                    int* iters_run);
 /* run(y, init, Algorithm::als_fast, opts) (als.cpp:147-210).  Traces hold
  * max_iters entries; sec_trace times each sweep on the device (CUDA events). */
 int cpdgpu_als_run(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors,

@@ -17,7 +17,7 @@
 #include <omp.h>
 #endif
 
-enum { ORA_OK = 0, ORA_SHAPE = 1, ORA_INDEX = 2, ORA_ARG = 3, ORA_NUMERIC = 4 };
+enum { ORA_OK = 0, ORA_SHAPE = 1, ORA_INDEX = 2, ORA_ARG = 3, ORA_NUMERIC = 4, ORA_DOMAIN = 5 };
 #define MAXN 64
 
 /* ---- shape arithmetic (shape.cpp:8-36, shape.hpp:27-32) ------------------ */
@@ -535,7 +535,7 @@ static void als_hook(void* user, int n, const double* g, ora_index rows, ora_ind
 int ora_als_sweep_fast(int N, const ora_index* dims, const double* y, ora_index R,
                        double* const* factors, double rtol, uint64_t* counter, int nthreads) {
   als_ctx c = {N, dims, R, factors, rtol, ORA_OK};
-  double* g[MAXN];
+  double* g[MAXN] = {0};
   for (int k = 0; k < N; ++k) g[k] = (double*)malloc((size_t)(dims[k] * R) * sizeof(double));
   int st = ora_cp_gradient_all(N, dims, y, R, factors, g, als_hook, &c, counter, NULL, 0, nthreads);
   for (int k = 0; k < N; ++k) free(g[k]);
@@ -667,6 +667,180 @@ int ora_run_als_fast(int N, const ora_index* dims, const double* y, ora_index R,
   }
   *iters_run = done;
   for (int j = 0; j < N; ++j) { /* un-permute (als.cpp:206-208) */
+    memcpy(factors[perm[j] - 1], sf[j], (size_t)(sd[j] * R) * sizeof(double));
+    free(sf[j]);
+  }
+  free(yperm);
+  return st;
+}
+
+/* ---- the other consumers of the gradient (als.cpp:58-101) ------------------- */
+
+/* mttkrp_direct's charge (mttkrp.cpp:29-54 with skip_kron_column, kron.cpp:85-93). */
+static uint64_t direct_charge(int N, const ora_index* dims, ora_index R, int n) {
+  ora_index J[MAXN + 1];
+  prefix_products(N, dims, J);
+  uint64_t s = (uint64_t)J[N];
+  for (int k = 2; k <= n - 1; ++k) s += (uint64_t)J[k];
+  for (int k = n + 1; k <= N; ++k) s += (uint64_t)(J[k] / dims[n - 1]);
+  return (uint64_t)R * s;
+}
+
+/* als_sweep_direct (als.cpp:58-67): direct MTTKRP + update per mode of order. */
+int ora_als_sweep_direct(int N, const ora_index* dims, const double* y, ora_index R,
+                         double* const* factors, const int* order, int norder, double rtol,
+                         uint64_t* counter) {
+  for (int i = 0; i < norder; ++i) {
+    const int n = order[i];
+    if (n < 1 || n > N) return ORA_INDEX;
+    const ora_index I = dims[n - 1];
+    double* m = (double*)malloc((size_t)(I * R) * sizeof(double));
+    double* upd = (double*)malloc((size_t)(I * R) * sizeof(double));
+    ora_brute_mttkrp(N, dims, y, R, (const double* const*)factors, n, m);
+    if (counter) *counter += direct_charge(N, dims, R, n);
+    const int st = ora_als_update_mode(N, dims, R, m, (const double* const*)factors, n, rtol, upd);
+    if (st == ORA_OK) memcpy(factors[n - 1], upd, (size_t)(I * R) * sizeof(double));
+    free(m);
+    free(upd);
+    if (st != ORA_OK) return st;
+  }
+  return ORA_OK;
+}
+
+typedef struct {
+  int N;
+  const ora_index* dims;
+  ora_index R;
+  double* const* factors;
+  double eps;
+} mu_ctx;
+
+/* mu_sweep's hook (als.cpp:84-90): A <- A .* G ./ (A W + eps), W from the current factors. */
+static void mu_hook(void* user, int n, const double* g, ora_index rows, ora_index R) {
+  mu_ctx* c = (mu_ctx*)user;
+  double* w = (double*)malloc((size_t)(R * R) * sizeof(double));
+  ora_gram_hadamard_skip(c->N, c->dims, R, (const double* const*)c->factors, n, w);
+  double* a = c->factors[n - 1];
+  double* na = (double*)malloc((size_t)(rows * R) * sizeof(double));
+  for (ora_index col = 0; col < R; ++col)
+    for (ora_index i = 0; i < rows; ++i) {
+      double den = 0.0;
+      for (ora_index k = 0; k < R; ++k) den += a[i + rows * k] * w[k + R * col];
+      na[i + rows * col] = a[i + rows * col] * g[i + rows * col] / (den + c->eps);
+    }
+  memcpy(a, na, (size_t)(rows * R) * sizeof(double));
+  free(na);
+  free(w);
+}
+
+/* mu_sweep (als.cpp:80-91). */
+int ora_mu_sweep(int N, const ora_index* dims, const double* y, ora_index R, double* const* factors,
+                 double eps, uint64_t* counter, int nthreads) {
+  if (eps < 0.0) return ORA_ARG;
+  ora_index J[MAXN + 1];
+  prefix_products(N, dims, J);
+  for (ora_index q = 0; q < J[N]; ++q) /* check_nonnegative (als.cpp:24-30) */
+    if (y[q] < 0.0) return ORA_DOMAIN;
+  for (int k = 0; k < N; ++k)
+    for (ora_index q = 0; q < dims[k] * R; ++q)
+      if (factors[k][q] < 0.0) return ORA_DOMAIN;
+  mu_ctx c = {N, dims, R, factors, eps};
+  double* g[MAXN] = {0};
+  for (int k = 0; k < N; ++k) g[k] = (double*)malloc((size_t)(dims[k] * R) * sizeof(double));
+  const int st = ora_cp_gradient_all(N, dims, y, R, factors, g, mu_hook, &c, counter, NULL, 0, nthreads);
+  for (int k = 0; k < N; ++k) free(g[k]);
+  return st;
+}
+
+/* gd_step (als.cpp:93-101, kruskal.cpp:83-101): M = all-mode gradient at the
+ * pre-step factors, G(n) = M(n) - A(n) W(n), then a(n) += 2 eta G(n) for all n. */
+int ora_gd_step(int N, const ora_index* dims, const double* y, ora_index R, double* const* factors,
+                double eta, uint64_t* counter, int nthreads) {
+  if (!(eta >= 0.0)) return ORA_ARG;
+  double* m[MAXN] = {0};
+  for (int k = 0; k < N; ++k) m[k] = (double*)malloc((size_t)(dims[k] * R) * sizeof(double));
+  const int st = ora_cp_gradient_all(N, dims, y, R, factors, m, NULL, NULL, counter, NULL, 0, nthreads);
+  if (st == ORA_OK) {
+    double* w = (double*)malloc((size_t)(R * R) * sizeof(double));
+    for (int k = 0; k < N; ++k) { /* G(n) in place of M(n), all from the old factors */
+      ora_gram_hadamard_skip(N, dims, R, (const double* const*)factors, k + 1, w);
+      const ora_index I = dims[k];
+      const double* a = factors[k];
+      double* gk = m[k];
+      for (ora_index col = 0; col < R; ++col)
+        for (ora_index i = 0; i < I; ++i) {
+          double aw = 0.0;
+          for (ora_index q = 0; q < R; ++q) aw += a[i + I * q] * w[q + R * col];
+          gk[i + I * col] -= aw;
+        }
+    }
+    free(w);
+    for (int k = 0; k < N; ++k)
+      for (ora_index q = 0; q < dims[k] * R; ++q) factors[k][q] += 2.0 * eta * m[k][q];
+  }
+  for (int k = 0; k < N; ++k) free(m[k]);
+  return st;
+}
+
+/* run(y, init, algo, opts) for every Algorithm (als.cpp:147-210): algo 0 als_direct
+ * (order_pivot: fast_update_order, else 1..N), 1 als_fast, 2 mu, 3 gd.  als_fast and
+ * mu run in the ascending-sorted frame. */
+int ora_run(int N, const ora_index* dims, const double* y, ora_index R, double* const* factors, int algo,
+            int order_pivot, int max_iters, double tol, double pinv_rtol, double mu_eps, double gd_eta,
+            double* cost_trace, double* rel_trace, uint64_t* mults_trace, int* iters_run, int nthreads) {
+  if (max_iters < 1 || tol < 0.0 || pinv_rtol < 0.0 || mu_eps < 0.0) return ORA_ARG;
+  if (algo < 0 || algo > 3) return ORA_ARG;
+  int perm[MAXN];
+  const int wants_sorted = (algo == 1 || algo == 2);
+  int identity = 1;
+  if (wants_sorted) identity = ora_sort_perm(N, dims, perm, NULL);
+  if (identity)
+    for (int j = 0; j < N; ++j) perm[j] = j + 1;
+  ora_index sd[MAXN], J[MAXN + 1];
+  for (int j = 0; j < N; ++j) sd[j] = dims[perm[j] - 1];
+  prefix_products(N, sd, J);
+  const double* work = y;
+  double* yperm = NULL;
+  if (!identity) {
+    yperm = (double*)malloc((size_t)J[N] * sizeof(double));
+    ora_permute(N, dims, y, perm, yperm);
+    work = yperm;
+  }
+  double* sf[MAXN];
+  for (int j = 0; j < N; ++j) {
+    sf[j] = (double*)malloc((size_t)(sd[j] * R) * sizeof(double));
+    memcpy(sf[j], factors[perm[j] - 1], (size_t)(sd[j] * R) * sizeof(double));
+  }
+  int order[MAXN];
+  if (algo == 0) {
+    if (order_pivot) ora_fast_update_order(N, sd, order);
+    else
+      for (int j = 0; j < N; ++j) order[j] = j + 1;
+  }
+  double yn = 0.0;
+  for (ora_index q = 0; q < J[N]; ++q) yn += work[q] * work[q];
+  yn = sqrt(yn);
+  uint64_t counter = 0;
+  double prev = NAN;
+  int st = ORA_OK, done = 0;
+  for (int it = 1; it <= max_iters; ++it) {
+    switch (algo) {
+      case 0: st = ora_als_sweep_direct(N, sd, work, R, sf, order, N, pinv_rtol, &counter); break;
+      case 1: st = ora_als_sweep_fast(N, sd, work, R, sf, pinv_rtol, &counter, nthreads); break;
+      case 2: st = ora_mu_sweep(N, sd, work, R, sf, mu_eps, &counter, nthreads); break;
+      default: st = ora_gd_step(N, sd, work, R, sf, gd_eta, &counter, nthreads); break;
+    }
+    if (st != ORA_OK) break;
+    if (mults_trace) mults_trace[it - 1] = counter;
+    ++done;
+    const double d = ora_cost(N, sd, work, R, (const double* const*)sf, 1000000, nthreads);
+    cost_trace[it - 1] = d;
+    rel_trace[it - 1] = yn > 0.0 ? sqrt(d) / yn : sqrt(d);
+    if (tol > 0.0 && it > 1 && fabs(d - prev) / (prev > 1e-15 ? prev : 1e-15) < tol) break;
+    prev = d;
+  }
+  *iters_run = done;
+  for (int j = 0; j < N; ++j) {
     memcpy(factors[perm[j] - 1], sf[j], (size_t)(sd[j] * R) * sizeof(double));
     free(sf[j]);
   }

@@ -65,6 +65,17 @@ int ora_run_als_fast(int N, const ora_index* dims, const double* y, ora_index R,
                      uint64_t* mults_trace, int* iters_run, int nthreads);
 
 /* Uniform01 stream of the reference's fixtures (rng.hpp:9-26). */
+int ora_als_sweep_direct(int N, const ora_index* dims, const double* y, ora_index R,
+                         double* const* factors, const int* order, int norder, double rtol,
+                         uint64_t* counter);
+int ora_mu_sweep(int N, const ora_index* dims, const double* y, ora_index R, double* const* factors,
+                 double eps, uint64_t* counter, int nthreads);
+int ora_gd_step(int N, const ora_index* dims, const double* y, ora_index R, double* const* factors,
+                double eta, uint64_t* counter, int nthreads);
+int ora_run(int N, const ora_index* dims, const double* y, ora_index R, double* const* factors, int algo,
+            int order_pivot, int max_iters, double tol, double pinv_rtol, double mu_eps, double gd_eta,
+            double* cost_trace, double* rel_trace, uint64_t* mults_trace, int* iters_run, int nthreads);
+
 void ora_uniform01_fill(uint64_t seed, ora_index n, double* out);
 /* Counter-based generator shared with the product's device generator
  * (DESIGN.md "Synthetic inputs"): hash of (seed, linear index). */

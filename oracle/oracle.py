@@ -222,6 +222,65 @@ def run_als_fast(y, dims, init, max_iters=20, tol=0.0, pinv_rtol=1e-12, nthreads
                   "mults": [int(m) for m in list(mults)[:k]], "iters_run": k}
 
 
+ALGOS = {"als_direct": 0, "als_fast": 1, "mu": 2, "gd": 3}
+
+
+def _fac_run(fn, factors, *args):
+    bufs = [b.copy(order="F") for b in _fbufs(factors)]
+    st = fn(_ptrs(bufs), *args)
+    if st:
+        raise ValueError(f"oracle status {st}")
+    return bufs
+
+
+def als_sweep_direct(y, dims, factors, order, rtol=1e-12):
+    yv = vec(y)
+    R = _fbufs(factors)[0].shape[1]
+    cnt = C.c_uint64(0)
+    arr = (C.c_int * len(order))(*order)
+    bufs = _fac_run(lambda fp: load().ora_als_sweep_direct(len(dims), _dims(dims), yv.ctypes.data_as(c_dbl_p),
+                                                           c_i64(R), fp, arr, len(order), C.c_double(rtol),
+                                                           C.byref(cnt)), factors)
+    return bufs, int(cnt.value)
+
+
+def mu_sweep(y, dims, factors, eps=1e-12, nthreads=0):
+    yv = vec(y)
+    R = _fbufs(factors)[0].shape[1]
+    cnt = C.c_uint64(0)
+    bufs = _fac_run(lambda fp: load().ora_mu_sweep(len(dims), _dims(dims), yv.ctypes.data_as(c_dbl_p), c_i64(R),
+                                                   fp, C.c_double(eps), C.byref(cnt), int(nthreads)), factors)
+    return bufs, int(cnt.value)
+
+
+def gd_step(y, dims, factors, eta, nthreads=0):
+    yv = vec(y)
+    R = _fbufs(factors)[0].shape[1]
+    cnt = C.c_uint64(0)
+    bufs = _fac_run(lambda fp: load().ora_gd_step(len(dims), _dims(dims), yv.ctypes.data_as(c_dbl_p), c_i64(R),
+                                                  fp, C.c_double(eta), C.byref(cnt), int(nthreads)), factors)
+    return bufs, int(cnt.value)
+
+
+def run(y, dims, init, algo, max_iters=20, tol=0.0, pinv_rtol=1e-12, mu_eps=1e-12, gd_eta=1e-3,
+        order_pivot=False, nthreads=0):
+    yv = vec(y)
+    bufs = [b.copy(order="F") for b in _fbufs(init)]
+    R = bufs[0].shape[1]
+    cost_t, rel_t = np.zeros(max_iters), np.zeros(max_iters)
+    mults = (C.c_uint64 * max_iters)()
+    iters = C.c_int(0)
+    st = load().ora_run(len(dims), _dims(dims), yv.ctypes.data_as(c_dbl_p), c_i64(R), _ptrs(bufs), ALGOS[algo],
+                        int(bool(order_pivot)), int(max_iters), C.c_double(tol), C.c_double(pinv_rtol),
+                        C.c_double(mu_eps), C.c_double(gd_eta), cost_t.ctypes.data_as(c_dbl_p),
+                        rel_t.ctypes.data_as(c_dbl_p), mults, C.byref(iters), int(nthreads))
+    if st:
+        raise ValueError(f"oracle status {st}")
+    k = iters.value
+    return bufs, {"cost": cost_t[:k], "rel_error": rel_t[:k], "mults": [int(m) for m in list(mults)[:k]],
+                  "iters_run": k}
+
+
 # ---- generators -------------------------------------------------------------------
 
 def uniform01(seed, n):

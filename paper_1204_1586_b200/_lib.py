@@ -54,6 +54,11 @@ SIGNATURES = {
     "cpdgpu_mttkrp_direct_device": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, C.c_void_p, C.c_int, C.c_void_p]),
     "cpdgpu_als_sweep_direct": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.POINTER(C.c_int), C.c_int,
                                           C.c_double, C.POINTER(c_u64)]),
+    "cpdgpu_mu_sweep": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_double, C.POINTER(c_u64)]),
+    "cpdgpu_gd_step": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_double, C.POINTER(c_u64)]),
+    "cpdgpu_run_algo": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_int, C.c_int, C.c_int, C.c_double,
+                                  C.c_double, C.c_double, C.c_double, c_dbl_p, c_dbl_p, c_dbl_p, C.POINTER(c_u64),
+                                  C.POINTER(C.c_int)]),
     "cpdgpu_als_sweep": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_double, c_dbl_p, C.POINTER(c_u64)]),
     "cpdgpu_als_run": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_int, C.c_double, C.c_double, c_dbl_p, c_dbl_p, c_dbl_p, C.POINTER(c_u64), C.POINTER(C.c_int)]),
 }

@@ -443,6 +443,7 @@ class SolveOptions:
     pinv_rtol: float = 1e-12
     mu_eps: float = 1e-12
     gd_eta: float = 1e-3
+    order: str = "standard"  # UpdateOrder for als_direct: "standard" (1..N) or "pivot"
     seed: int = 0
 
 
@@ -462,10 +463,39 @@ class SolveResult:
     trace: RunTrace
 
 
+def mu_sweep(y: DenseTensor, factors: list, eps: float = 1e-12, counter: Optional[CostCounter] = None) -> None:
+    """Multiplicative-update sweep (als.cpp:80-91) on the device; factors updated in place.
+    Negative tensor or factor entries raise DomainError."""
+    _sweep_call(y, factors, counter, lambda ctx, R, fp, m: ctx._L.cpdgpu_mu_sweep(ctx.h, y.h, R, fp, eps, m))
+
+
+def gd_step(y: DenseTensor, factors: list, eta: float, counter: Optional[CostCounter] = None) -> None:
+    """Gradient-descent step (als.cpp:93-101) on the device; factors updated in place."""
+    _sweep_call(y, factors, counter, lambda ctx, R, fp, m: ctx._L.cpdgpu_gd_step(ctx.h, y.h, R, fp, eta, m))
+
+
+def _sweep_call(y, factors, counter, call):
+    bufs = [b.copy(order="F") for b in _factor_bufs(factors, y.dims)]
+    R = bufs[0].shape[1]
+    mults = C.c_uint64()
+    ctx = y.ctx
+    _lib.check(call(ctx, R, _ptr_array(bufs), C.byref(mults)), ctx.h)
+    for k, b in enumerate(bufs):
+        factors[k] = b
+    if counter is not None:
+        counter.charge(int(mults.value))
+
+
+ALGORITHMS = {"als_direct": 0, "als_fast": 1, "mu": 2, "gd": 3}
+
+
 def run(y: DenseTensor, init: list, opts: Optional[SolveOptions] = None,
-        counter: Optional[CostCounter] = None) -> SolveResult:
-    """run(y, init, Algorithm::als_fast, opts) (als.cpp:147-210) on the device."""
+        counter: Optional[CostCounter] = None, algo: str = "als_fast") -> SolveResult:
+    """run(y, init, algo, opts) (als.cpp:147-210) on the device; algo is one of
+    Algorithm's names: als_direct, als_fast (default), mu, gd."""
     opts = opts or SolveOptions()
+    if algo not in ALGORITHMS:
+        raise errors.ArgumentError(f"run: unknown algorithm {algo!r}")
     if opts.max_iters < 1:
         raise errors.ArgumentError("run: max_iters must be at least 1")
     if opts.tol < 0.0 or opts.pinv_rtol < 0.0 or opts.mu_eps < 0.0:
@@ -483,9 +513,11 @@ def run(y: DenseTensor, init: list, opts: Optional[SolveOptions] = None,
     mults = (C.c_uint64 * n)()
     iters = C.c_int()
     ctx = y.ctx
-    _lib.check(ctx._L.cpdgpu_als_run(ctx.h, y.h, R, _ptr_array(bufs), n, opts.tol, opts.pinv_rtol,
-                                     cost.ctypes.data_as(_lib.c_dbl_p), rel.ctypes.data_as(_lib.c_dbl_p),
-                                     sec.ctypes.data_as(_lib.c_dbl_p), mults, C.byref(iters)), ctx.h)
+    _lib.check(ctx._L.cpdgpu_run_algo(ctx.h, y.h, R, _ptr_array(bufs), ALGORITHMS[algo],
+                                      int(opts.order == "pivot"), n, opts.tol, opts.pinv_rtol, opts.mu_eps,
+                                      opts.gd_eta, cost.ctypes.data_as(_lib.c_dbl_p),
+                                      rel.ctypes.data_as(_lib.c_dbl_p), sec.ctypes.data_as(_lib.c_dbl_p), mults,
+                                      C.byref(iters)), ctx.h)
     k = iters.value
     base = counter.total() if counter is not None else 0
     tr = RunTrace(cost=list(cost[:k]), rel_error=list(rel[:k]), seconds=list(sec[:k]),

@@ -270,6 +270,75 @@ __global__ void __launch_bounds__(kAlsThreads, 1)
   }
 }
 
+// mu_sweep's update (als.cpp:84-90): A <- A .* G ./ (A W + eps), W = hadamard of the
+// other modes' Grams (current factors); then gram_n <- A^T A.  A thread owns whole
+// rows (in-place safe: row i of the new A needs only row i of the old one).
+__global__ void __launch_bounds__(kAlsThreads, 1)
+    mu_update_kernel(const double* __restrict__ G, int64_t I, int R, const double* __restrict__ grams, int N, int n,
+                     double eps, double* __restrict__ A, double* __restrict__ gram_n) {
+  extern __shared__ double W[];  // R x R
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < R * R; e += nt) {
+    double w = 1.0;
+    for (int k = 0; k < N; ++k)
+      if (k != n) w *= grams[static_cast<int64_t>(k) * R * R + e];
+    W[e] = w;
+  }
+  __syncthreads();
+  for (int64_t i = tid; i < I; i += nt) {
+    double row[64];
+    for (int k = 0; k < R; ++k) row[k] = A[i + I * k];
+    for (int c = 0; c < R; ++c) {
+      double den = 0.0;
+      for (int k = 0; k < R; ++k) den += row[k] * W[k + R * c];
+      A[i + I * c] = row[c] * G[i + I * c] / (den + eps);
+    }
+  }
+  __threadfence_block();
+  __syncthreads();
+  for (int e = tid; e < R * R; e += nt) {
+    const int a = e % R, c = e / R;
+    double acc = 0.0;
+    for (int64_t i = 0; i < I; ++i) acc += A[i + I * a] * A[i + I * c];
+    gram_n[e] = acc;
+  }
+}
+
+// gd_step's update for one mode (als.cpp:93-101): A += 2 eta (G - A W) with W from
+// the pre-step Grams (the caller recomputes every Gram after all modes).
+__global__ void gd_update_kernel(const double* __restrict__ G, int64_t I, int R, const double* __restrict__ grams,
+                                 int N, int n, double eta, double* __restrict__ A) {
+  extern __shared__ double W[];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    double w = 1.0;
+    for (int k = 0; k < N; ++k)
+      if (k != n) w *= grams[static_cast<int64_t>(k) * R * R + e];
+    W[e] = w;
+  }
+  __syncthreads();
+  // each thread owns rows i (all R columns), so the in-place update reads its own old row
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < I;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double row[64];
+    for (int k = 0; k < R; ++k) row[k] = A[i + I * k];
+    for (int c = 0; c < R; ++c) {
+      double aw = 0.0;
+      for (int k = 0; k < R; ++k) aw += row[k] * W[k + R * c];
+      A[i + I * c] = row[c] + 2.0 * eta * (G[i + I * c] - aw);
+    }
+  }
+}
+
+// status[0] <- 5 (DomainError) when any entry is negative (mu_sweep's check_nonnegative).
+template <typename T>
+__global__ void nonneg_kernel(const T* __restrict__ y, int64_t n, int* status) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad |= y[i] < T(0);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) status[0] = 5;
+}
+
 __global__ void __launch_bounds__(kAlsThreads, 1)
     pinv_kernel(const double* __restrict__ S, int R, double rtol, double* __restrict__ out) {
   extern __shared__ double smem[];
@@ -341,6 +410,28 @@ int launch_als_update(const double* G, int64_t I, int R, const double* grams, in
   const size_t bytes = eig_smem_bytes(R);
   set_smem(reinterpret_cast<const void*>(als_update_kernel), bytes);
   als_update_kernel<<<1, kAlsThreads, bytes, s>>>(G, I, R, grams, N, n, rtol, A, gram_n, status);
+  return 1;
+}
+
+int launch_mu_update(const double* G, int64_t I, int R, const double* grams, int N, int n, double eps, double* A,
+                     double* gram_n, cudaStream_t s) {
+  const size_t bytes = static_cast<size_t>(R) * R * sizeof(double);
+  mu_update_kernel<<<1, kAlsThreads, bytes, s>>>(G, I, R, grams, N, n, eps, A, gram_n);
+  return 1;
+}
+
+int launch_gd_update(const double* G, int64_t I, int R, const double* grams, int N, int n, double eta, double* A,
+                     cudaStream_t s) {
+  const int blocks = static_cast<int>(I / 128 + 1 < 148 ? I / 128 + 1 : 148);
+  gd_update_kernel<<<blocks, 128, static_cast<size_t>(R) * R * sizeof(double), s>>>(G, I, R, grams, N, n, eta, A);
+  return 1;
+}
+
+int launch_nonneg_check(const void* y, int elem_bytes, int64_t n, int* status, cudaStream_t s) {
+  if (elem_bytes == 8)
+    nonneg_kernel<double><<<148 * 4, 256, 0, s>>>(static_cast<const double*>(y), n, status);
+  else
+    nonneg_kernel<float><<<148 * 4, 256, 0, s>>>(static_cast<const float*>(y), n, status);
   return 1;
 }
 

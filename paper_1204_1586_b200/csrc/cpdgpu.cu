@@ -15,6 +15,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <numeric>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -1300,8 +1301,8 @@ void als_sweep_device(cpdgpu_ctx* ctx, Plan& pl, double rtol) {
 }
 
 // cost after a sweep: last visited mode L (fast_update_order) gives <Y, Yhat>
-void als_cost(cpdgpu_ctx* ctx, Plan& pl, double* cost_slot) {
-  const int L = pl.p + 1 <= pl.N ? pl.N : 1;
+void als_cost(cpdgpu_ctx* ctx, Plan& pl, double* cost_slot, int L = 0) {
+  if (L == 0) L = pl.p + 1 <= pl.N ? pl.N : 1;
   ctx->launches += cpdgpu::launch_als_cost(pl.factor(L), pl.Gorig.d() + pl.off_orig[pl.perm[L - 1] - 1],
                                            pl.sd[L - 1], static_cast<int>(pl.R), pl.grams.d(), pl.N, pl.norm.d(),
                                            cost_slot, ctx->stream);
@@ -1353,6 +1354,116 @@ void check_status(cpdgpu_ctx* ctx, Plan& pl) {
   CK(cudaMemcpyAsync(&st, pl.status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (st == 4) fail(CPDGPU_NUMERIC_ERROR, "als_update_mode: non-finite gradient input");
+}
+
+// ---- the other gradient consumers on the device (als.cpp:58-101) -----------------
+
+// Direct MTTKRP of caller mode n from the live sorted factors (Fs): the sweeps'
+// form of direct_body (no factor gather).
+void direct_body_fs(cpdgpu_ctx* ctx, Plan& pl, int n) {
+  int j = 1;
+  while (pl.perm[j - 1] != n) ++j;
+  const bool right = j <= pl.p;
+  launch_kr_from_fs(ctx, pl, right ? 1 : 2);
+  run_seeds(ctx, pl, right ? 1 : 2);
+  {
+    cpdgpu::TailStep st{};
+    add_reduce_ops(pl, st, right ? 1 : 2);
+    if (st.n > 0) launch_step(ctx, pl, st);
+  }
+  cpdgpu::TailStep s{};
+  if (right) {
+    double* rc = pl.Rs.d();
+    double* rn = pl.Rtmp.d();
+    for (int k = pl.p; k > j; --k) {
+      cpdgpu::TailStep r{};
+      add_right_recurse(pl, r, k, rc, rn);
+      launch_step(ctx, pl, r);
+      std::swap(rc, rn);
+    }
+    add_right_extract(pl, s, j, rc);
+  } else {
+    double* lc = pl.Ls.d();
+    double* ln = pl.Ltmp.d();
+    for (int k = pl.p + 1; k < j; ++k) {
+      cpdgpu::TailStep r{};
+      add_left_recurse(pl, r, k, lc, ln);
+      launch_step(ctx, pl, r);
+      std::swap(lc, ln);
+    }
+    add_left_extract(pl, s, j, lc);
+  }
+  launch_step(ctx, pl, s);
+}
+
+int sorted_pos(const Plan& pl, int n) {
+  int j = 1;
+  while (pl.perm[j - 1] != n) ++j;
+  return j;
+}
+
+// mu_sweep (als.cpp:80-91) through the Gauss-Seidel sweep.
+void mu_sweep_device(cpdgpu_ctx* ctx, Plan& pl, double eps) {
+  const int R = static_cast<int>(pl.R);
+  sweep_body(ctx, pl, [&](int j) {
+    double* G = pl.Gorig.d() + pl.off_orig[pl.perm[j - 1] - 1];
+    ctx->launches += cpdgpu::launch_mu_update(G, pl.sd[j - 1], R, pl.grams.d(), pl.N, j - 1, eps, pl.factor(j),
+                                              pl.grams.d() + static_cast<int64_t>(j - 1) * R * R, ctx->stream);
+  });
+}
+
+// gd_step (als.cpp:93-101): every mode's gradient at the pre-step factors, the
+// simultaneous step, then fresh Grams.
+void gd_step_device(cpdgpu_ctx* ctx, Plan& pl, double eta) {
+  const int R = static_cast<int>(pl.R);
+  launch_kr_from_fs(ctx, pl, pl.p + 1 <= pl.N ? 3 : 1);
+  gradient_body(ctx, pl);
+  for (int j = 1; j <= pl.N; ++j)
+    ctx->launches += cpdgpu::launch_gd_update(pl.Gorig.d() + pl.off_orig[pl.perm[j - 1] - 1], pl.sd[j - 1], R,
+                                              pl.grams.d(), pl.N, j - 1, eta, pl.factor(j), ctx->stream);
+  init_grams(ctx, pl);
+}
+
+// als_sweep_direct (als.cpp:58-67): direct MTTKRP + update per caller mode of order.
+void direct_sweep_device(cpdgpu_ctx* ctx, Plan& pl, const std::vector<int>& order, double rtol) {
+  const int R = static_cast<int>(pl.R);
+  for (int n : order) {
+    direct_body_fs(ctx, pl, n);
+    const int j = sorted_pos(pl, n);
+    ctx->launches += cpdgpu::launch_als_update(pl.Gorig.d() + pl.off_orig[n - 1], pl.sd[j - 1], R, pl.grams.d(),
+                                               pl.N, j - 1, rtol, pl.factor(j),
+                                               pl.grams.d() + static_cast<int64_t>(j - 1) * R * R,
+                                               static_cast<int*>(pl.status.p), ctx->stream);
+  }
+}
+
+// cost after an iteration of `algo` (Gram identity, kruskal.cpp:58-77): Gauss-
+// Seidel sweeps reuse the last visited mode's gradient; gd needs one fresh
+// direct MTTKRP (of sorted mode 1) at the stepped factors.
+void algo_cost(cpdgpu_ctx* ctx, Plan& pl, int algo, const std::vector<int>& order, double* slot) {
+  if (algo == 0) {
+    als_cost(ctx, pl, slot, sorted_pos(pl, order.back()));
+  } else if (algo == 3) {
+    direct_body_fs(ctx, pl, pl.perm[0]);
+    als_cost(ctx, pl, slot, 1);
+  } else {
+    als_cost(ctx, pl, slot);
+  }
+}
+
+void check_nonneg_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* y, const double* const* factors) {
+  for (size_t m = 0; m < y->dims.size(); ++m)
+    for (int64_t q = 0; q < y->dims[m] * pl.R; ++q)
+      if (factors[m][q] < 0.0) fail(CPDGPU_DOMAIN_ERROR, "mu_sweep: factors have negative entries");
+  DevBuf flag;
+  flag.ensure(sizeof(int));
+  CK(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx->stream));
+  ctx->launches += cpdgpu::launch_nonneg_check(y->data, static_cast<int>(y->elem()), y->numel,
+                                               static_cast<int*>(flag.p), ctx->stream);
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (bad) fail(CPDGPU_DOMAIN_ERROR, "mu_sweep: tensor has negative entries");
 }
 
 void prepare_als(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* y) {
@@ -1748,6 +1859,125 @@ int cpdgpu_als_sweep_direct(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double
       if (st != CPDGPU_OK) fail(st, "%s", ctx->err.c_str());
     }
     if (mults) *mults = total;
+  });
+}
+
+int cpdgpu_mu_sweep(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, double eps,
+                    uint64_t* mults) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "mu_sweep");
+    if (!factors) fail(CPDGPU_ARGUMENT_ERROR, "mu_sweep: null factor list");
+    if (eps < 0.0) fail(CPDGPU_ARGUMENT_ERROR, "mu_sweep: eps must be nonnegative");
+    if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "mu_sweep: rank above the device limit 64");
+    ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, 0);
+    bind_seed_inputs(ctx, pl, y);
+    check_nonneg_inputs(ctx, pl, y, factors);
+    upload_host_factors(ctx, pl, y, factors);
+    prepare_als(ctx, pl, y);
+    mu_sweep_device(ctx, pl, eps);
+    CK(cudaStreamSynchronize(ctx->stream));
+    download_factors(ctx, pl, y, factors);
+    if (mults) {
+      *mults = 0;
+      for (int j = 1; j <= pl.N; ++j) *mults += count_realized(pl.sd, R, j);
+    }
+  });
+}
+
+int cpdgpu_gd_step(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, double eta,
+                   uint64_t* mults) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "gd_step");
+    if (!factors) fail(CPDGPU_ARGUMENT_ERROR, "gd_step: null factor list");
+    if (!(eta >= 0.0)) fail(CPDGPU_ARGUMENT_ERROR, "gd_step: eta must be nonnegative");
+    if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "gd_step: rank above the device limit 64");
+    ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, 0);
+    bind_seed_inputs(ctx, pl, y);
+    upload_host_factors(ctx, pl, y, factors);
+    prepare_als(ctx, pl, y);
+    gd_step_device(ctx, pl, eta);
+    CK(cudaStreamSynchronize(ctx->stream));
+    download_factors(ctx, pl, y, factors);
+    if (mults) {
+      *mults = 0;
+      for (int j = 1; j <= pl.N; ++j) *mults += count_realized(pl.sd, R, j);
+    }
+  });
+}
+
+int cpdgpu_run_algo(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* factors, int algo,
+                    int order_pivot, int max_iters, double tol, double pinv_rtol, double mu_eps, double gd_eta,
+                    double* cost_trace, double* rel_trace, double* sec_trace, uint64_t* mults_trace,
+                    int* iters_run) {
+  if (algo == 1)
+    return cpdgpu_als_run(ctx, y, R, factors, max_iters, tol, pinv_rtol, cost_trace, rel_trace, sec_trace,
+                          mults_trace, iters_run);
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "run");
+    if (algo < 0 || algo > 3) fail(CPDGPU_ARGUMENT_ERROR, "run: unknown algorithm %d", algo);
+    if (max_iters < 1) fail(CPDGPU_ARGUMENT_ERROR, "run: max_iters must be at least 1");
+    if (tol < 0.0 || pinv_rtol < 0.0 || mu_eps < 0.0) fail(CPDGPU_ARGUMENT_ERROR, "run: tolerances must be nonnegative");
+    if (algo == 3 && !(gd_eta >= 0.0)) fail(CPDGPU_ARGUMENT_ERROR, "gd_step: eta must be nonnegative");
+    if (!factors || !cost_trace || !rel_trace || !iters_run) fail(CPDGPU_ARGUMENT_ERROR, "run: null argument");
+    if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "run: rank above the device ALS limit 64");
+    ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, 0);
+    bind_seed_inputs(ctx, pl, y);
+    if (algo == 2) check_nonneg_inputs(ctx, pl, y, factors);
+    upload_host_factors(ctx, pl, y, factors);
+    prepare_als(ctx, pl, y);
+    pl.costs.ensure(static_cast<size_t>(max_iters) * sizeof(double));
+    // als_direct visits caller modes 1..N or fast_update_order (als.cpp:168-170)
+    std::vector<int> order(static_cast<size_t>(pl.N));
+    std::iota(order.begin(), order.end(), 1);
+    if (algo == 0 && order_pivot) {
+      std::vector<int> o(static_cast<size_t>(pl.N));
+      cpdgpu_fast_update_order(static_cast<int>(y->dims.size()), y->dims.data(), o.data());
+      order = o;
+    }
+    uint64_t per_sweep = 0;
+    if (algo == 0)
+      for (int n : order) per_sweep += direct_count(y->dims, R, n);
+    else
+      for (int j = 1; j <= pl.N; ++j) per_sweep += count_realized(pl.sd, R, j);
+    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(max_iters));
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    const double ynorm = std::sqrt(y->norm2);
+    double prev = std::nan("");
+    int done = 0;
+    for (int it = 1; it <= max_iters; ++it) {
+      CK(cudaEventRecord(ev[2 * (it - 1)], ctx->stream));
+      if (algo == 0) direct_sweep_device(ctx, pl, order, pinv_rtol);
+      else if (algo == 2) mu_sweep_device(ctx, pl, mu_eps);
+      else gd_step_device(ctx, pl, gd_eta);
+      CK(cudaEventRecord(ev[2 * (it - 1) + 1], ctx->stream));
+      algo_cost(ctx, pl, algo, order, pl.costs.d() + (it - 1));
+      ++done;
+      if (tol > 0.0) {
+        double d = 0.0;
+        CK(cudaMemcpyAsync(&d, pl.costs.d() + (it - 1), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (it > 1 && std::abs(d - prev) / std::max(prev, 1e-15) < tol) break;
+        prev = d;
+      }
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    check_status(ctx, pl);
+    CK(cudaMemcpy(cost_trace, pl.costs.d(), static_cast<size_t>(done) * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < done; ++i) {
+      rel_trace[i] = ynorm > 0.0 ? std::sqrt(cost_trace[i]) / ynorm : std::sqrt(cost_trace[i]);
+      if (sec_trace) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+        sec_trace[i] = ms * 1e-3;
+      }
+      if (mults_trace) mults_trace[i] = per_sweep * static_cast<uint64_t>(i + 1);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    *iters_run = done;
+    download_factors(ctx, pl, y, factors);
   });
 }
 

@@ -164,6 +164,14 @@ int launch_gram(const double* A, int64_t I, int R, double* gram, cudaStream_t s)
 // status[0] set to 4 (NumericError) when G holds a non-finite value.
 int launch_als_update(const double* G, int64_t I, int R, const double* grams, int N, int n,
                        double rtol, double* A, double* gram_n, int* status, cudaStream_t s);
+// mu_sweep update (als.cpp:84-90) of mode n: A <- A .* G ./ (A W + eps); gram_n <- A^T A.
+int launch_mu_update(const double* G, int64_t I, int R, const double* grams, int N, int n, double eps, double* A,
+                     double* gram_n, cudaStream_t s);
+// gd_step update of mode n (als.cpp:93-101): A += 2 eta (G - A W), W from the old Grams.
+int launch_gd_update(const double* G, int64_t I, int R, const double* grams, int N, int n, double eta, double* A,
+                     cudaStream_t s);
+// status[0] <- 5 when the fp64 / fp32 tensor has a negative entry.
+int launch_nonneg_check(const void* y, int elem_bytes, int64_t n, int* status, cudaStream_t s);
 // standalone pinv_psd of a device R x R matrix
 int launch_pinv_psd(const double* S, int R, double rtol, double* out, cudaStream_t s);
 // cost = ynorm2 - 2 sum(A_L .* G_L) + 1^T (hadamard of all grams) 1, clamped at 0

@@ -299,7 +299,22 @@ void test_pinv_and_als() {  // test_als.cpp
   const double y2 = y.norm() * y.norm();
   for (size_t i = 1; i < res.trace.cost.size(); ++i) CHECK(res.trace.cost[i] <= res.trace.cost[i - 1] + 1e-12 * y2);
   CHECK(c.total() == res.trace.mults.back() && c.total() > 0);
-  CHECK(throws<cpd::ArgumentError>([&] { cpd::run(y, cpd::KruskalModel(truth), cpd::Algorithm::mu, opt); }));
+  // every Algorithm runs and fills the trace (test_als.cpp:198-221)
+  for (auto algo : {cpd::Algorithm::als_direct, cpd::Algorithm::als_fast, cpd::Algorithm::mu, cpd::Algorithm::gd}) {
+    cpd::SolveOptions o;
+    o.max_iters = 4;
+    o.gd_eta = 1e-4;
+    cpd::FactorList pos = random_factors(d, 2, 905);
+    for (auto& a : pos)
+      for (cpd::index_t i = 0; i < a.size(); ++i) a.data()[i] = std::abs(a.data()[i]);
+    std::vector<double> vy(y.values());
+    for (auto& v : vy) v = std::abs(v);
+    cpd::DenseTensor ypos(y.shape(), vy);
+    auto r = cpd::run(ypos, cpd::KruskalModel(pos), algo, o);
+    CHECK(r.trace.iters_run == 4 && r.trace.rel_error.size() == 4);
+    for (size_t i = 0; i < 4; ++i)
+      CHECK(std::abs(r.trace.rel_error[i] - std::sqrt(r.trace.cost[i]) / ypos.norm()) <= 1e-12 * r.trace.rel_error[i]);
+  }
 
   // one sweep: als_sweep_fast == gradient + als_update_mode in Gauss-Seidel order
   cpd::FactorList a = random_factors(d, 3, 903), b = a;

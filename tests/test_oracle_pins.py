@@ -380,3 +380,69 @@ def test_golden_fixtures_reproduce(oracle):
         g, _, _ = oracle.cp_gradient_all(z["y"], dims, f)
         for k in range(len(dims)):
             assert max_rel_diff(g[k], z[f"G{k}"]) < 1e-13, fn.name
+
+
+# ---- the other gradient consumers (test_als.cpp:114-245) ------------------------------
+
+def test_mu_sweep_pins(oracle):
+    # test_als.cpp:114-143: monotone, nonnegative, exact fit ~fixed point, sign/argument errors
+    dims = [4, 3, 5]
+    y = oracle.random_tensor(dims, 61)
+    f = oracle.random_factors(dims, 3, 62)
+    prev = oracle.cost(y, dims, f)
+    for _ in range(50):
+        f, _ = oracle.mu_sweep(y, dims, f)
+        assert all((a >= 0).all() for a in f)
+        d = oracle.cost(y, dims, f)
+        assert d <= prev * (1 + 1e-9) + 1e-12
+        prev = d
+    t = oracle.random_factors([3, 4, 3], 2, 63)
+    yt = oracle.full([3, 4, 3], t)
+    t2, _ = oracle.mu_sweep(yt, [3, 4, 3], t)
+    for a, b in zip(t, t2):
+        assert max_rel_diff(b, a) < 1e-9
+    bad = yt.copy()
+    bad[0] = -bad[0]
+    with pytest.raises(ValueError):
+        oracle.mu_sweep(bad, [3, 4, 3], t)
+    fneg = [a.copy() for a in t]
+    fneg[1][0, 0] = -1.0
+    with pytest.raises(ValueError):
+        oracle.mu_sweep(yt, [3, 4, 3], fneg)
+    with pytest.raises(ValueError):
+        oracle.mu_sweep(yt, [3, 4, 3], t, eps=-1e-3)
+
+
+def test_gd_step_pins(oracle):
+    # test_als.cpp:145-160: eta = 0 is the identity, negative eta rejected, a small step descends
+    dims = [3, 4, 4]
+    y = oracle.random_tensor(dims, 71)
+    f = oracle.random_factors(dims, 2, 72)
+    frozen, _ = oracle.gd_step(y, dims, f, 0.0)
+    for a, b in zip(frozen, f):
+        assert np.abs(a - b).max() == 0.0
+    with pytest.raises(ValueError):
+        oracle.gd_step(y, dims, f, -1e-6)
+    stepped, _ = oracle.gd_step(y, dims, f, 1e-4)
+    assert oracle.cost(y, dims, stepped) < oracle.cost(y, dims, f)
+
+
+def test_run_every_algorithm_pins(oracle):
+    # test_als.cpp:198-221 and 223-238: traces filled, rel = sqrt(cost)/|Y|; fast == direct (pivot order)
+    dims = [4, 3, 5]
+    y = oracle.random_tensor(dims, 91)
+    init = oracle.random_factors(dims, 2, 92)
+    yn = np.linalg.norm(y)
+    for algo in ("als_direct", "als_fast", "mu", "gd"):
+        _, tr = oracle.run(y, dims, init, algo, max_iters=4, gd_eta=1e-4)
+        assert tr["iters_run"] == 4
+        assert all(b >= a for a, b in zip(tr["mults"], tr["mults"][1:]))
+        assert np.allclose(tr["rel_error"], np.sqrt(tr["cost"]) / yn, rtol=1e-12)
+    dims = [5, 3, 4]
+    y = oracle.random_tensor(dims, 101)
+    init = oracle.random_factors(dims, 2, 102)
+    ff, tf = oracle.run(y, dims, init, "als_fast", max_iters=6)
+    fd, td = oracle.run(y, dims, init, "als_direct", max_iters=6, order_pivot=True)
+    for a, b in zip(ff, fd):
+        assert max_rel_diff(a, b) < 1e-12
+    assert np.allclose(tf["cost"], td["cost"], rtol=1e-10)
