@@ -7,7 +7,7 @@ R=20 factors, synthetic N(0,1) inputs from the counter-based generator.
 For N>1 (torchrun, one rank per GPU) every rank holds one 60^4 slab of a
 60x60x60x(60N) tensor sharded along its last mode (weak scaling): the local
 gradient runs with the global pivot, then one NCCL all_reduce of the partial
-G(1..3) and one all_gather of the G(4) rows (paper_1204_1586_b200/sharded.py).
+G(1..3) carrying the G(4) rows at each slab's offset (paper_1204_1586_b200/sharded.py).
 
 Timing: W untimed warm-up steps; then exactly K steps bracketed by a barrier +
 cuda synchronize on both sides.  Every step is preceded by an L2 flush (a

@@ -6,8 +6,8 @@ slab, the right seed and every G(1..N-1) are linear sums over slabs, while the
 rows of G(N) are owned by the slab that holds them:
 
     local step   : cpdgpu_cp_gradient_all_device(slab, pivot = p*)   (no collective)
-    exchange     : all_reduce(SUM) of the packed partial G(1..N-1)  (one NCCL call)
-                   all_gather of the (padded) local G(N) row blocks  (one NCCL call)
+    exchange     : one all_reduce(SUM) of [partial G(1..N-1) | G(N) rows at the
+                   slab's offset, zeros elsewhere]                    (one NCCL call)
 
 The collective is torch.distributed (NCCL over NVLink on the B200 box, gloo in the
 CPU tests); the per-slab compute is injected so the host logic can be tested with
@@ -93,23 +93,21 @@ def pack_local_factors(plan: SlabPlan, factors: Sequence, xp):
 
 
 def exchange(plan: SlabPlan, local_out, dist, group=None):
-    """all_reduce(SUM) of the partial G(1..N-1) and all_gather of G(N) rows.
-    local_out: 1-D torch tensor (packed local gradients, caller mode order).
-    Returns (packed partial-summed G(1..N-1), G(N) as an I_N x R column-major
+    """One all_reduce(SUM) carrying both results: the partial G(1..N-1) and the
+    G(N) rows, each rank's rows placed at its slab offset of a zero I_N x R block
+    (a single latency-bound collective instead of an all_reduce plus an
+    all_gather).  local_out: 1-D torch tensor (packed local gradients, caller mode
+    order).  Returns (packed summed G(1..N-1), G(N) as an I_N x R column-major
     tensor viewed (R, I_N))."""
     import torch
     P = plan.partial_len
-    partial = local_out[:P].contiguous()
-    dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
     a, b = plan.bounds
-    rows = b - a
-    gN = local_out[P:].view(plan.R, rows)  # column-major rows x R == (R, rows) row-major
-    pad = torch.zeros((plan.R, plan.max_rows), dtype=local_out.dtype, device=local_out.device)
-    pad[:, :rows] = gN
-    gathered = [torch.empty_like(pad) for _ in range(plan.world)]
-    dist.all_gather(gathered, pad, group=group)
-    cols = [g[:, : (hi - lo)] for g, (lo, hi) in zip(gathered, slab_bounds(plan.dims[-1], plan.world))]
-    return partial, torch.cat(cols, dim=1)
+    IN = int(plan.dims[-1])
+    buf = torch.zeros(P + plan.R * IN, dtype=local_out.dtype, device=local_out.device)
+    buf[:P] = local_out[:P]
+    buf[P:].view(plan.R, IN)[:, a:b] = local_out[P:].view(plan.R, b - a)
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return buf[:P], buf[P:].view(plan.R, IN)
 
 
 def unpack(plan: SlabPlan, partial, gN_rt) -> list[np.ndarray]:
