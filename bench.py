@@ -203,10 +203,18 @@ def run_ours(args, cfg):
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     if rank == 0:
         B.build()
+    # BENCH_FUNCTIONAL_1GPU=1: functional check of the N>1 code path on a one-GPU box
+    # (every rank on device 0, gloo collectives through the host) — never a timing
+    functional = os.environ.get("BENCH_FUNCTIONAL_1GPU") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         dist.barrier()
     B.build()  # no-op after rank 0 built it; loads the in-tree .so
     dims, R, dtype, desc = cfg
@@ -515,10 +523,18 @@ def run_ours_als(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if rank == 0:
         B.build()
+    # BENCH_FUNCTIONAL_1GPU=1: functional check of the N>1 code path on a one-GPU box
+    # (every rank on device 0, gloo collectives through the host) — never a timing
+    functional = os.environ.get("BENCH_FUNCTIONAL_1GPU") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         dist.barrier()
     B.build()
     dims, R, dtype, desc = cfg
