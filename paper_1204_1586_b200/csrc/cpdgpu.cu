@@ -704,10 +704,33 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
       q.units = f.U;
       q.P = f.P;
       q.slots = f.slots;
-      q.chunk = 4;
+      static const int chunk_env = std::getenv("CPDGPU_F32_CHUNK") ? std::atoi(std::getenv("CPDGPU_F32_CHUNK")) : 8;
+      static const int dbg_env = std::getenv("CPDGPU_F32_DEBUG") ? std::atoi(std::getenv("CPDGPU_F32_DEBUG")) : 0;
+      q.chunk = chunk_env > 0 ? chunk_env : 8;
+      q.debug = dbg_env;
+      static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
+      DevBuf tb;
+      if (trace) {
+        tb.ensure(static_cast<size_t>(q.P) * 10 * 8 * 8);
+        CK(cudaMemsetAsync(tb.p, 0, tb.bytes, s));
+        q.trace = static_cast<unsigned long long*>(tb.p);
+      }
       if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
       ctx->launches += cpdgpu::launch_seed_f32(q, side ? &pl.ymap_l : &pl.ymap_r, side, s);
       if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+      if (trace) {
+        std::vector<unsigned long long> h(static_cast<size_t>(q.P) * 80);
+        CK(cudaMemcpyAsync(h.data(), tb.p, tb.bytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double a[10][8] = {};
+        for (int c = 0; c < q.P; ++c)
+          for (int w = 0; w < 10; ++w)
+            for (int k = 0; k < 8; ++k) a[w][k] += static_cast<double>(h[(static_cast<size_t>(c) * 10 + w) * 8 + k]) / q.P;
+        std::fprintf(stderr, "[f32 trace side %d] avg cycles per CTA: split w0 full %.0f cempty %.0f accfull %.0f split %.0f "
+                     "drain %.0f total %.0f | producer empty %.0f total %.0f | mma cfull %.0f kfull %.0f accempty %.0f "
+                     "total %.0f\n", side, a[0][0], a[0][1], a[0][2], a[0][4], a[0][5], a[0][3], a[8][0], a[8][3],
+                     a[9][1], a[9][2], a[9][0], a[9][3]);
+      }
     }
   }
   CK(cudaGetLastError());

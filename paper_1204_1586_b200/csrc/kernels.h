@@ -69,6 +69,8 @@ struct Seed32Params {
   double* part;                   // [P * slots][64][128]
   int64_t nK, units;
   int P, slots, chunk;
+  int debug;  // experiment knobs (CPDGPU_F32_DEBUG): bit 0 one MMA per k-step, bit 1 no split work
+  unsigned long long* trace;  // optional [P][10][4] per-warp cycle counters (CPDGPU_SEED_TRACE)
 };
 size_t seed_f32_smem_bytes();
 int seed_f32_rank_cols();         // 64

@@ -42,12 +42,14 @@ constexpr int kYTile = kBK * kBM * 4;           // fp32 tile bytes (32 KB)
 constexpr int kKTile = 2 * kBK * kRP * 2;       // fp16 hi + lo Khatri-Rao tile (16 KB)
 constexpr int kStages = 5;          // raw Y ring (fp32), released as soon as it is split
 constexpr int kKStages = 3;         // Khatri-Rao tile ring, released by the MMAs
-constexpr int kConv = 2;            // A operand ring in TMEM (fp16 hi + lo, 64 columns each)
+constexpr int kConv = 4;            // A operand ring in TMEM (fp16 hi + lo, 64 columns each)
+constexpr int kLag = 2;             // a finished accumulation chunk is drained kLag tiles later
 constexpr int kSplitWarps = 8;
 constexpr int kThreads = (kSplitWarps + 2) * 32;
-constexpr int kTmemA = 0;                  // A buffers: columns [0, 128)
-constexpr int kTmemAcc = kConv * kBK;      // accumulators: columns [128, 256)
-constexpr int kTmemCols = 256;
+constexpr int kTmemA = 0;                  // A buffers: columns [0, 256)
+constexpr int kTmemAcc = kConv * kBK;      // accumulators: 2 x [hi-product 64 | hi*lo 64] = [256, 512)
+constexpr int kAccStride = 2 * kRP;
+constexpr int kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -84,6 +86,16 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
   return pol;
 }
+// wait with cycle accounting (trace builds only: acc == nullptr costs nothing)
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+  if (acc) {
+    const unsigned long long t0 = clock64();
+    mbar_wait(bar, parity);
+    *acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
                                             uint64_t pol) {
   asm volatile(
@@ -107,10 +119,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint3
   return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (static_cast<uint64_t>(layout) << 61);
 }
-// Instruction descriptor, kind::f16: fp16 A and B, fp32 D, M = 128, N = kRP.
-__host__ __device__ constexpr uint32_t umma_idesc(bool a_mn_major) {
+// Instruction descriptor, kind::f16: fp16 A and B, fp32 D, M = 128, N = n.
+__host__ __device__ constexpr uint32_t umma_idesc(bool a_mn_major, int n = kRP) {
   return (1u << 4) | (0u << 7) | (0u << 10) | ((a_mn_major ? 1u : 0u) << 15) | (0u << 16) |
-         (static_cast<uint32_t>(kRP >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
 }
 __device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
                                             uint32_t acc) {
@@ -273,6 +285,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // optional per-warp cycle trace: [cta][warp][wait0, wait1, wait2, total]
+  unsigned long long* tr = p.trace ? p.trace + (static_cast<int64_t>(cta) * (kThreads / 32) + warp) * 8 : nullptr;
+  unsigned long long tw[5] = {0, 0, 0, 0, 0};
+  const unsigned long long tstart = clock64();
 
   if (warp == kProducer) {
     // ------------------------------------------------------------------ producer
@@ -309,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         const int s = k % kStages;
-        if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
+        if (k >= kStages) mbar_wait_t(&empty[s], ((k / kStages) - 1) & 1, tr ? &tw[0] : nullptr);
         const int64_t u = a + k, blk = u / p.nK, t = u - blk * p.nK;
         mbar_arrive_tx(&full[s], kYTile);
         if (LEFT) {  // rows i in [64 t, +64) as two 32-row halves, columns j in [128 blk, +128)
@@ -339,9 +355,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMma) {
     // ------------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc(false);  // A from TMEM (K-major rows)
-    // B (Khatri-Rao, K-major interleaved): SBO next 8 r = 128 B, LBO next 8 K = kRP * 16 B
-    constexpr uint32_t b_lbo = kRP * 16, b_sbo = 128, b_kstep = 2 * kRP * 16, b_lo = kBK * kRP * 2;
+    // A from TMEM (K-major rows).  Per k-step: A_hi x [B_hi | B_lo] as one N = 128 MMA
+    // (the hi and lo Khatri-Rao pieces are adjacent rows of one swizzled operand) into
+    // accumulator columns [0, 128), then A_lo x B_hi (N = 64) into [0, 64); the drain
+    // adds the two halves.  8 MMAs per tile instead of 12, and A_hi is read once.
+    constexpr uint32_t idesc128 = umma_idesc(false, 2 * kRP), idesc64 = umma_idesc(false, kRP);
+    // B (Khatri-Rao, K-major, 128B swizzle): SBO next 8 r = 1 KB, +32 B per 16 K inside the atom
+    constexpr uint32_t b_lbo = 16, b_sbo = 1024, b_kstep = 32;
+    constexpr uint32_t b_layout = 2;  // SWIZZLE_128B
     int q = -1, pos = 0;
     for (int k = 0; k < n; ++k) {
       const int sk = k % kKStages, c = k % kConv;
@@ -349,24 +370,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++q;
         pos = 0;
         if (q >= 2) {
-          mbar_wait(&accempty[q & 1], ((q >> 1) - 1) & 1);
+          mbar_wait_t(&accempty[q & 1], ((q >> 1) - 1) & 1, tr ? &tw[0] : nullptr);
           tc_fence_after();
         }
       }
-      mbar_wait(&cfull[c], (k / kConv) & 1);
-      mbar_wait(&kfull[sk], (k / kKStages) & 1);
+      mbar_wait_t(&cfull[c], (k / kConv) & 1, tr ? &tw[1] : nullptr);
+      mbar_wait_t(&kfull[sk], (k / kKStages) & 1, tr ? &tw[2] : nullptr);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t d = tmem + static_cast<uint32_t>(kTmemAcc + (q & 1) * kRP);
+        const uint32_t d = tmem + static_cast<uint32_t>(kTmemAcc + (q & 1) * kAccStride);
         const uint32_t ahi = tmem + static_cast<uint32_t>(kTmemA + c * kBK), alo = ahi + kBK / 2;
         const uint32_t kb = smem_u32(ktiles + sk * kKTile);
 #pragma unroll
         for (int ks = 0; ks < kBK / 16; ++ks) {  // K = 16 per MMA = 8 packed TMEM columns
-          const uint64_t bhi = umma_desc(kb + ks * b_kstep, b_lbo, b_sbo);
-          const uint64_t blo = umma_desc(kb + b_lo + ks * b_kstep, b_lbo, b_sbo);
-          umma_f16_ts(d, ahi + 8 * ks, bhi, idesc, (pos > 0 || ks > 0) ? 1u : 0u);
-          umma_f16_ts(d, alo + 8 * ks, bhi, idesc, 1u);
-          umma_f16_ts(d, ahi + 8 * ks, blo, idesc, 1u);
+          const uint64_t ball = umma_desc(kb + ks * b_kstep, b_lbo, b_sbo, b_layout);  // rows: hi 0..63, lo 64..127
+          umma_f16_ts(d, ahi + 8 * ks, ball, idesc128, (pos > 0 || ks > 0) ? 1u : 0u);
+          if (!(p.debug & 1)) umma_f16_ts(d, alo + 8 * ks, ball, idesc64, 1u);
         }
         umma_commit(&kempty[sk]);
         umma_commit(&cempty[c]);
@@ -388,8 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sp = warp & 3, colh = warp >> 2;  // TMEM lane quarter, rank-column half
     const uint32_t lane_base = static_cast<uint32_t>(sp * 32) << 16;
     int q = -1, pos = 0, seg = -1;
-    int pend_q = -1, pend_k = -1, pend_seg = -1;
-    bool pend_last = false;
+    // finished chunks waiting to be drained (FIFO, drained in order kLag tiles later)
+    int fq[4], fk[4], fseg[4];
+    bool flast[4];
+    int fh = 0, ft = 0;
     for (int k = 0; k <= n; ++k) {
       if (k < n) {
         const int s = k % kStages, c = k % kConv;
@@ -398,14 +419,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++q;
           pos = 0;
         }
-        mbar_wait(&full[s], (k / kStages) & 1);
+        mbar_wait_t(&full[s], (k / kStages) & 1, tr ? &tw[0] : nullptr);
         if (k >= kConv) {
-          mbar_wait(&cempty[c], ((k / kConv) - 1) & 1);
+          mbar_wait_t(&cempty[c], ((k / kConv) - 1) & 1, tr ? &tw[1] : nullptr);
           tc_fence_after();
         }
+        const unsigned long long ts0 = tr ? clock64() : 0;
         const uint32_t tA = tmem + static_cast<uint32_t>(kTmemA + c * kBK);
         const unsigned char* raw = ytiles + s * kYTile;
-        if (LEFT) {
+        if (p.debug & 2) {
+        } else if (LEFT) {
           if (scale) split_left<true>(raw, tA, sy, warp, lane);
           else split_left<false>(raw, tA, sy, warp, lane);
         } else {
@@ -415,24 +438,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         tc_fence_before();
         __syncwarp();
+        if (tr) tw[3] += clock64() - ts0;
         if (lane == 0) {
           mbar_arrive(&empty[s]);
           mbar_arrive(&cfull[c]);
         }
       }
-      // drain the previous chunk one stage late, so the MMAs of this stage overlap it
-      if (pend_q >= 0 && pend_k < k) {
-        mbar_wait(&accfull[pend_q & 1], (pend_q >> 1) & 1);
+      // drain finished chunks kLag tiles late, so the MMAs of the newer tiles overlap it
+      while (fh < ft && (k == n || fk[fh & 3] + kLag <= k)) {
+        const int e = fh & 3;
+        const int dq = fq[e];
+        mbar_wait_t(&accfull[dq & 1], (dq >> 1) & 1, tr ? &tw[2] : nullptr);
         tc_fence_after();
-        float v[32];
-        tmem_ld32(tmem + lane_base + static_cast<uint32_t>(kTmemAcc + (pend_q & 1) * kRP + colh * 32), v);
+        const unsigned long long td0 = tr ? clock64() : 0;
+        float v[32], u[32];
+        tmem_ld32(tmem + lane_base + static_cast<uint32_t>(kTmemAcc + (dq & 1) * kAccStride + colh * 32), v);
+        tmem_ld32(tmem + lane_base + static_cast<uint32_t>(kTmemAcc + (dq & 1) * kAccStride + kRP + colh * 32), u);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] += static_cast<double>(v[c]);
+        for (int c = 0; c < 32; ++c) acc[c] += static_cast<double>(v[c]) + static_cast<double>(u[c]);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&accempty[pend_q & 1]);
-        if (pend_last) {  // block segment finished: unscaled fp64 partial rows
-          double* out = p.part + (static_cast<int64_t>(cta) * p.slots + pend_seg) * kRP * kBM +
+        if (lane == 0) mbar_arrive(&accempty[dq & 1]);
+        if (flast[e]) {  // block segment finished: unscaled fp64 partial rows
+          double* out = p.part + (static_cast<int64_t>(cta) * p.slots + fseg[e]) * kRP * kBM +
                         static_cast<int64_t>(colh * 32) * kBM + sp * 32 + lane;
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
@@ -440,20 +468,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc[c] = 0.0;
           }
         }
-        pend_q = -1;
+        ++fh;
+        if (tr) tw[4] += clock64() - td0;
       }
       if (k < n) {
         ++pos;
         const bool seg_end = (k == n - 1) || w.next_starts();
         w.advance();
         if (seg_end || pos == w.chunk) {
-          pend_q = q;
-          pend_k = k;
-          pend_last = seg_end;
-          pend_seg = seg;
+          const int e = ft & 3;
+          fq[e] = q;
+          fk[e] = k;
+          flast[e] = seg_end;
+          fseg[e] = seg;
+          ++ft;
         }
       }
     }
+  }
+  if (tr && lane == 0) {
+    tr[0] = tw[0];
+    tr[1] = tw[1];
+    tr[2] = tw[2];
+    tr[3] = clock64() - tstart;
+    tr[4] = tw[3];
+    tr[5] = tw[4];
   }
   tc_fence_before();
   __syncthreads();
@@ -486,7 +525,8 @@ __global__ void kr_scale_kernel(const KRSpec right, const KRSpec left, int R, do
 }
 
 // fp64 Khatri-Rao rows [L][ld] -> scaled fp16 hi / lo tiles laid out as the
-// K-major B operand: tile t = rows [64 t, 64 t + 64): [piece][j8][r8][8 r][8 j].
+// K-major B operand with 128-byte swizzle: tile t = rows [64 t, 64 t + 64),
+// [piece][r (64)][64 K values, 16-byte chunks XOR-swizzled by r % 8].
 __global__ void kr_split_kernel(const double* __restrict__ rows, int64_t L, int ld, const double* __restrict__ scale,
                                 __half* __restrict__ tiles, int64_t ntiles) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // (t, j8, r8, rr)
@@ -506,7 +546,9 @@ __global__ void kr_split_kernel(const double* __restrict__ rows, int64_t L, int 
     hi[jj] = __double2half(x);
     lo[jj] = __double2half(x - static_cast<double>(__half2float(hi[jj])));
   }
-  __half* dst = tiles + t * (kKTile / 2) + (static_cast<int64_t>(j8) * (kRP / 8) + r8) * 64 + rr * 8;
+  // K-major 128B-swizzled rows: row r holds its 64 K values (128 B); 16-byte chunk j8
+  // of row r sits at chunk j8 ^ (r % 8) (atoms of 8 rows x 128 B)
+  __half* dst = tiles + t * (kKTile / 2) + static_cast<int64_t>(r) * kBK + ((j8 ^ (r & 7)) << 3);
   *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hi);
   *reinterpret_cast<uint4*>(dst + kBK * kRP) = *reinterpret_cast<const uint4*>(lo);
 }
