@@ -99,3 +99,20 @@ def test_f32_als_fit_trace(gpu_ctx, oracle):
     _, ot = oracle.run_als_fast(yv, dims, f, max_iters=8)
     for i in range(8):
         assert abs(res.trace.rel_error[i] - ot["rel_error"][i]) <= 1e-5 * ot["rel_error"][i]
+
+
+@pytest.mark.slow
+def test_f32_full_c5_matches_fp64_device_path(gpu_ctx, oracle):
+    """BASELINE config 5 at full size (300^4 fp32, R=64): the tensor-core gradient
+    against the fp64 DMMA gradient of the same values (U(-1,1) draws are exact in
+    both precisions; the fp64 path is oracle-pinned at c1-c3) at the fp32 bar."""
+    dims, R = [300] * 4, 64
+    f = [oracle.fill_normal(500 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
+    y32 = cpd.DenseTensor.generate(dims, cpd.DIST_UNIFORM_PM1, seed=7, ctx=gpu_ctx, dtype=cpd.F32)
+    g32 = cpd.cp_gradient_all(y32, f)
+    y32.free()
+    y64 = cpd.DenseTensor.generate(dims, cpd.DIST_UNIFORM_PM1, seed=7, ctx=gpu_ctx, dtype=cpd.F64)
+    g64 = cpd.cp_gradient_all(y64, f)
+    y64.free()
+    errs = rel_errs(g32, g64)
+    assert max(errs) <= TOL, errs
