@@ -390,22 +390,46 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
   const int64_t R = pl.R;
   // K1 geometry
   const int64_t Jp = pl.Jp, Kp = pl.Kp;
-  // Row block TI: multiple of 8 (DMMA fragments) and == 8 (mod 16) so the dense
-  // TMA tile (LDY == TI) keeps the right-product fragment loads conflict-free.
+  // Row block TI: a multiple of 8 (DMMA fragments); the TMA box is TI + 4 rows
+  // (LDY == 4 or 12 mod 16: conflict-free fragment loads for both products).
+  // When the columns start on 128-byte lines (J_p % 16 == 0) TI is a multiple of
+  // 16 as well, so row blocks never share a line with a neighbour that another
+  // CTA streams later (a shared line is fetched from HBM twice); among those the
+  // largest TI whose last row block wastes <= 2 % of J_p is taken.
   int ti_max = 208;
   for (int64_t r0 = 0; r0 < R; r0 += 32)
     ti_max = std::min(ti_max, cpdgpu::seed_f64_max_ti(pick_nt(std::min<int64_t>(32, R - r0))));
-  if (ti_max % 16 != 8) ti_max -= 8;
-  auto ti_for = [](int64_t rows) {
-    int64_t ti = (rows + 7) / 8 * 8;
-    if (ti % 16 == 0) ti += 8;
-    return static_cast<int>(ti);
-  };
-  int64_t nRB = cpdgpu::ceil_div(Jp, ti_max);
-  int TI = ti_for(cpdgpu::ceil_div(Jp, nRB));
-  while (TI > ti_max) {
-    ++nRB;
+  int64_t nRB = 0;
+  int TI = 0;
+  if (Jp % 16 == 0 && Jp >= 96) {
+    int best = 0;
+    double best_waste = 1e30;
+    for (int ti = ti_max / 16 * 16; ti >= 96; ti -= 16) {
+      const double waste = static_cast<double>(cpdgpu::ceil_div(Jp, ti) * ti - Jp) / static_cast<double>(Jp);
+      if (waste <= 0.02) {
+        best = ti;
+        break;
+      }
+      if (waste < best_waste) {
+        best_waste = waste;
+        best = ti;
+      }
+    }
+    TI = best;
+    nRB = cpdgpu::ceil_div(Jp, TI);
+  } else {
+    if (ti_max % 16 != 8) ti_max -= 8;
+    auto ti_for = [](int64_t rows) {
+      int64_t ti = (rows + 7) / 8 * 8;
+      if (ti % 16 == 0) ti += 8;
+      return static_cast<int>(ti);
+    };
+    nRB = cpdgpu::ceil_div(Jp, ti_max);
     TI = ti_for(cpdgpu::ceil_div(Jp, nRB));
+    while (TI > ti_max) {
+      ++nRB;
+      TI = ti_for(cpdgpu::ceil_div(Jp, nRB));
+    }
   }
   pl.tma_ok = (Jp % 2 == 0);
   // TMA box rows TI + 4 (== 12 mod 16): conflict-free fragment loads for both products
@@ -647,10 +671,12 @@ void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
   }
   bool tma = pl.tma_ok;
   if (tma && pl.tmap_base != ybase) {
+    // no 256 B L2 promotion for Y: row-block starts are not line aligned and the
+    // promoted neighbour lines belong to another CTA's (later) tiles
     tma = cpdgpu::make_tensor_map_2d(&pl.tmap, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
                                      static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
                                      static_cast<uint64_t>(pl.Jp) * 8,
-                                     static_cast<uint32_t>(pl.chunks[0].sp.TI + 4), 32);
+                                     static_cast<uint32_t>(pl.chunks[0].sp.TI + 4), 32, false, false);
     pl.tmap_base = tma ? ybase : nullptr;
   }
   tma = tma && pl.tmap_base == ybase;
