@@ -68,11 +68,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// 2-D TMA load with an L2 policy: Y streams through once (evict first), the
+// Khatri-Rao rows are re-read for every row block (evict last).
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            bool stream = false) {
+  uint64_t pol;
+  if (stream)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
@@ -409,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t tile = t0 + k;
         const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
         mbar_arrive_tx(&full[k], LDY * kTJ * 8 + ((MODE & 1) ? kTJ * LDK * 8 : 0));
-        tma_load_2d(Ys + k * kTJ * LDY, &tmap, static_cast<int>(rb * TI), static_cast<int>(ct * kTJ), &full[k]);
+        tma_load_2d(Ys + k * kTJ * LDY, &tmap, static_cast<int>(rb * TI), static_cast<int>(ct * kTJ), &full[k], true);
       }
     pdl_wait();
     if (lane == 0 && (MODE & 1))
@@ -433,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           const uint32_t bytes = LDY * kTJ * 8 + ((MODE & 1) ? kTJ * LDK * 8 : 0);
           mbar_arrive_tx(&full[s], bytes);
-          tma_load_2d(ys, &tmap, static_cast<int>(row0), static_cast<int>(col0), &full[s]);
+          tma_load_2d(ys, &tmap, static_cast<int>(row0), static_cast<int>(col0), &full[s], true);
           if (MODE & 1) tma_load_2d(kr, &kmap, 0, static_cast<int>(col0), &full[s]);
         }
       } else {  // unaligned leading extent: plain loads (rare shapes)
@@ -534,8 +542,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto load_y = [&](int k, int s) {
         const int64_t u = t0 + k, cb = u / p.nCT, rt = u - cb * p.nCT;
         double* ys = Ys + s * kTJ * TJ;
-        tma_load_2d(ys, &ymap, static_cast<int>(rt * kTJ), static_cast<int>(cb * TJ), &full[s]);
-        tma_load_2d(ys + 16 * TJ, &ymap, static_cast<int>(rt * kTJ + 16), static_cast<int>(cb * TJ), &full[s]);
+        tma_load_2d(ys, &ymap, static_cast<int>(rt * kTJ), static_cast<int>(cb * TJ), &full[s], true);
+        tma_load_2d(ys + 16 * TJ, &ymap, static_cast<int>(rt * kTJ + 16), static_cast<int>(cb * TJ), &full[s], true);
       };
       auto load_k = [&](int k, int s) {
         const int64_t u = t0 + k, rt = u % p.nCT;
