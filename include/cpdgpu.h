@@ -34,7 +34,8 @@ typedef enum {
   CPDGPU_NUMERIC_ERROR = 4,  /* cpd::NumericError  (errors.hpp:29-31) */
   CPDGPU_DOMAIN_ERROR = 5,   /* cpd::DomainError   (errors.hpp:24-26) */
   CPDGPU_CUDA_ERROR = 6,     /* device / driver failure                */
-  CPDGPU_NO_MEMORY = 7       /* device allocation failed               */
+  CPDGPU_NO_MEMORY = 7,      /* device allocation failed               */
+  CPDGPU_PARSE_ERROR = 8     /* cpd::ParseError    (errors.hpp:33-36) */
 } cpdgpu_status;
 
 typedef enum { CPDGPU_F64 = 0, CPDGPU_F32 = 1 } cpdgpu_dtype;
@@ -93,6 +94,16 @@ int cpdgpu_tensor_download(cpdgpu_ctx* ctx, const cpdgpu_tensor* t, void* host);
 int cpdgpu_tensor_norm2(cpdgpu_ctx* ctx, cpdgpu_tensor* t, double* out);
 int cpdgpu_tensor_device_ptr(const cpdgpu_tensor* t, void** device_ptr);
 int cpdgpu_tensor_free(cpdgpu_tensor* t);
+
+/* ---- TDNB tensor files (io.hpp:10-12, io.cpp:162-216) --------------------
+ * Binary form "TDNB" + u32 LE N + u32 LE dims + f64 LE values (vec order).
+ * load: streams the file through pinned double buffers straight to the device;
+ * slab_hi > slab_lo loads only last-mode slices [slab_lo, slab_hi) (a rank's
+ * shard), else the whole tensor.  Malformed files -> CPDGPU_PARSE_ERROR with the
+ * byte offset in the message.  save: f64 LE (fp32 tensors are widened exactly). */
+int cpdgpu_tensor_load_tdnb(cpdgpu_ctx* ctx, const char* path, int64_t slab_lo, int64_t slab_hi,
+                            cpdgpu_tensor** out);
+int cpdgpu_tensor_save_tdnb(cpdgpu_ctx* ctx, const cpdgpu_tensor* t, const char* path);
 
 /* ---- ordering helpers (mttkrp.hpp:24,35,73) ----------------------------- */
 int cpdgpu_select_pivot(int N, const int64_t* dims, int* pivot);            /* mttkrp.cpp:56-65  */

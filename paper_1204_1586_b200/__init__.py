@@ -4,7 +4,7 @@ The product is libcpdgpu.so (hand-written sm_100a CUDA behind a C-ABI,
 include/cpdgpu.h); this package is its host-side mirror of the reference API.
 """
 from .errors import (ArgumentError, CpdError, DeviceError, DomainError, IndexError,  # noqa: A004
-                     NumericError, ShapeError)
+                     NumericError, ParseError, ShapeError)
 from .api import (DIST_NORMAL, DIST_UNIFORM_PM1, F32, F64, Context, CostCounter, DenseTensor,
                   FastStats, RunTrace, SolveOptions, SolveResult, als_sweep_fast, als_update_mode,
                   cp_gradient_all, cp_gradient_all_device, default_context, fast_count_realized,
@@ -12,7 +12,7 @@ from .api import (DIST_NORMAL, DIST_UNIFORM_PM1, F32, F64, Context, CostCounter,
                   mttkrp_direct_device, als_sweep_direct, mu_sweep, gd_step)
 
 __all__ = [
-    "ArgumentError", "CpdError", "DeviceError", "DomainError", "IndexError", "NumericError",
+    "ArgumentError", "CpdError", "DeviceError", "DomainError", "IndexError", "NumericError", "ParseError",
     "ShapeError", "DIST_NORMAL", "DIST_UNIFORM_PM1", "F32", "F64", "Context", "CostCounter",
     "DenseTensor", "FastStats", "RunTrace", "SolveOptions", "SolveResult", "als_sweep_fast",
     "als_update_mode", "cp_gradient_all", "cp_gradient_all_device", "default_context",

@@ -50,6 +50,8 @@ SIGNATURES = {
     "cpdgpu_cp_gradient_all_device": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, C.c_void_p, C.c_void_p, C.c_int]),
     "cpdgpu_pinv_psd": (C.c_int, [C.c_void_p, c_i64, c_dbl_p, C.c_double, c_dbl_p]),
     "cpdgpu_als_update_mode": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(c_i64), c_i64, c_dbl_p, c_dbl_pp, C.c_int, C.c_double, c_dbl_p]),
+    "cpdgpu_tensor_load_tdnb": (C.c_int, [C.c_void_p, C.c_char_p, c_i64, c_i64, C.POINTER(C.c_void_p)]),
+    "cpdgpu_tensor_save_tdnb": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p]),
     "cpdgpu_mttkrp_direct": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_int, c_dbl_p, C.POINTER(c_u64)]),
     "cpdgpu_mttkrp_direct_device": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, C.c_void_p, C.c_int, C.c_void_p]),
     "cpdgpu_als_sweep_direct": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.POINTER(C.c_int), C.c_int,

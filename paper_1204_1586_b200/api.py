@@ -150,6 +150,26 @@ class DenseTensor:
         return cls(ctx, h, dims, dtype)
 
     @classmethod
+    def load_tdnb(cls, path: str, slab: Optional[tuple] = None, ctx: Optional[Context] = None) -> "DenseTensor":
+        """Binary tensor file (io.cpp:162-181) streamed through pinned buffers to the
+        device; slab=(lo, hi) loads only last-mode slices [lo, hi) (a rank's shard)."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        lo, hi = (int(slab[0]), int(slab[1])) if slab else (0, 0)
+        _lib.check(ctx._L.cpdgpu_tensor_load_tdnb(ctx.h, str(path).encode(), lo, hi, C.byref(h)), ctx.h)
+        with open(path, "rb") as f:
+            head = f.read(8)
+            n = int.from_bytes(head[4:8], "little")
+            dims = [int.from_bytes(f.read(4), "little") for _ in range(n)]
+        if slab:
+            dims[-1] = hi - lo
+        return cls(ctx, h, dims, F64)
+
+    def save_tdnb(self, path: str) -> None:
+        """Write the binary tensor file (io.cpp:192-203), f64 little-endian."""
+        _lib.check(self.ctx._L.cpdgpu_tensor_save_tdnb(self.ctx.h, self.h, str(path).encode()), self.ctx.h)
+
+    @classmethod
     def wrap_device(cls, ptr: int, dims: Sequence[int], ctx: Optional[Context] = None,
                     dtype: int = F64) -> "DenseTensor":
         ctx = ctx or default_context()

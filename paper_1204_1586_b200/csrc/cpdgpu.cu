@@ -1748,6 +1748,146 @@ int cpdgpu_tensor_free(cpdgpu_tensor* t) {
   return CPDGPU_OK;
 }
 
+// ---- TDNB files (io.cpp:162-216): binary tensor ingest straight to the device ------
+
+namespace {
+struct FileCloser {
+  FILE* f;
+  ~FileCloser() {
+    if (f) std::fclose(f);
+  }
+};
+struct PinnedBuf {
+  void* p = nullptr;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+}  // namespace
+
+int cpdgpu_tensor_load_tdnb(cpdgpu_ctx* ctx, const char* path, int64_t slab_lo, int64_t slab_hi,
+                            cpdgpu_tensor** out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !path || !out) fail(CPDGPU_ARGUMENT_ERROR, "load_tdnb: null argument");
+    *out = nullptr;
+    use_device(ctx);
+    FileCloser fc{std::fopen(path, "rb")};
+    if (!fc.f) fail(CPDGPU_PARSE_ERROR, "%s: cannot open", path);
+    std::fseek(fc.f, 0, SEEK_END);
+    const int64_t size = static_cast<int64_t>(std::ftell(fc.f));
+    std::fseek(fc.f, 0, SEEK_SET);
+    char magic[4] = {0, 0, 0, 0};
+    if (size < 4 || std::fread(magic, 1, 4, fc.f) != 4 || std::memcmp(magic, "TDNB", 4) != 0)
+      fail(CPDGPU_PARSE_ERROR, "%s: bad magic at byte 0", path);
+    auto u32 = [&](int64_t at, const char* what) {
+      unsigned char b[4];
+      if (at + 4 > size || std::fread(b, 1, 4, fc.f) != 4) fail(CPDGPU_PARSE_ERROR, "%s: truncated %s at byte %lld", path, what, (long long)at);
+      return static_cast<uint32_t>(b[0]) | (static_cast<uint32_t>(b[1]) << 8) | (static_cast<uint32_t>(b[2]) << 16) |
+             (static_cast<uint32_t>(b[3]) << 24);
+    };
+    const uint32_t n = u32(4, "order");
+    if (n < 1 || n > 64) fail(CPDGPU_PARSE_ERROR, "%s: implausible order at byte 4", path);
+    if (n > static_cast<uint32_t>(kMaxModes)) fail(CPDGPU_ARGUMENT_ERROR, "%s: order %u above %d", path, n, kMaxModes);
+    std::vector<int64_t> dims(n);
+    for (uint32_t k = 0; k < n; ++k) {
+      const int64_t at = 8 + 4 * static_cast<int64_t>(k);
+      const uint32_t d = u32(at, "dimension");
+      if (d < 1) fail(CPDGPU_PARSE_ERROR, "%s: nonpositive dimension at byte %lld", path, (long long)at);
+      dims[k] = d;
+    }
+    const int64_t head = 8 + 4 * static_cast<int64_t>(n);
+    const int64_t numel = prefix(dims).back();
+    const int64_t want = head + 8 * numel;
+    if (size < want) {  // the first value that is not complete
+      const int64_t at = head + 8 * ((size - head) / 8);
+      fail(CPDGPU_PARSE_ERROR, "%s: truncated value at byte %lld", path, (long long)at);
+    }
+    if (size > want) fail(CPDGPU_PARSE_ERROR, "%s: trailing data at byte %lld", path, (long long)want);
+    // slab of the last mode
+    const int64_t last = dims[n - 1];
+    int64_t lo = 0, hi = last;
+    if (slab_hi > slab_lo) {
+      if (slab_lo < 0 || slab_hi > last)
+        fail(CPDGPU_INDEX_ERROR, "%s: slab [%lld, %lld) outside the last mode 0..%lld", path, (long long)slab_lo,
+             (long long)slab_hi, (long long)last);
+      lo = slab_lo;
+      hi = slab_hi;
+    }
+    const int64_t plane = numel / last;
+    std::vector<int64_t> ld = dims;
+    ld[n - 1] = hi - lo;
+    std::unique_ptr<cpdgpu_tensor> t(new_tensor(ctx, CPDGPU_F64, static_cast<int>(n), ld.data()));
+    const size_t bytes = static_cast<size_t>(t->numel) * 8;
+    CK(cudaMalloc(&t->data, bytes));
+    t->owned = true;
+    // file -> pinned (double-buffered) -> device; the host reads chunk i + 1 while chunk i copies
+    const size_t chunk = std::min<size_t>(bytes, size_t(64) << 20);
+    PinnedBuf pb[2];
+    cudaEvent_t done[2];
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaHostAlloc(&pb[b].p, std::max<size_t>(chunk, 8), cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+    }
+    std::fseek(fc.f, static_cast<long>(head + 8 * lo * plane), SEEK_SET);
+    size_t at = 0;
+    int b = 0;
+    bool used[2] = {false, false};
+    while (at < bytes) {
+      const size_t len = std::min(chunk, bytes - at);
+      if (used[b]) CK(cudaEventSynchronize(done[b]));
+      if (std::fread(pb[b].p, 1, len, fc.f) != len)
+        fail(CPDGPU_PARSE_ERROR, "%s: read failed at byte %lld", path, (long long)(head + 8 * lo * plane + at));
+      CK(cudaMemcpyAsync(static_cast<char*>(t->data) + at, pb[b].p, len, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaEventRecord(done[b], ctx->stream));
+      used[b] = true;
+      at += len;
+      b ^= 1;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < 2; ++k) cudaEventDestroy(done[k]);
+    t->sorted = t->identity ? t->data : nullptr;
+    t->sorted_ready = t->identity;
+    *out = t.release();
+  });
+}
+
+int cpdgpu_tensor_save_tdnb(cpdgpu_ctx* ctx, const cpdgpu_tensor* t, const char* path) {
+  return guarded(ctx, [&] {
+    if (!ctx || !t || !path) fail(CPDGPU_ARGUMENT_ERROR, "save_tdnb: null argument");
+    use_device(ctx);
+    for (int64_t d : t->dims)
+      if (d > 0xFFFFFFFFll) fail(CPDGPU_ARGUMENT_ERROR, "%s: dimension too large for binary format", path);
+    FileCloser fc{std::fopen(path, "wb")};
+    if (!fc.f) fail(CPDGPU_ARGUMENT_ERROR, "%s: cannot open for writing", path);
+    std::vector<unsigned char> head;
+    head.insert(head.end(), {'T', 'D', 'N', 'B'});
+    auto put32 = [&](uint32_t v) {
+      for (int k = 0; k < 4; ++k) head.push_back(static_cast<unsigned char>(v >> (8 * k)));
+    };
+    put32(static_cast<uint32_t>(t->dims.size()));
+    for (int64_t d : t->dims) put32(static_cast<uint32_t>(d));
+    if (std::fwrite(head.data(), 1, head.size(), fc.f) != head.size()) fail(CPDGPU_ARGUMENT_ERROR, "%s: write failed", path);
+    const size_t chunk_el = size_t(8) << 20;  // elements per chunk
+    PinnedBuf pb, wide;
+    CK(cudaHostAlloc(&pb.p, chunk_el * t->elem(), cudaHostAllocDefault));
+    if (t->dtype == CPDGPU_F32) CK(cudaHostAlloc(&wide.p, chunk_el * 8, cudaHostAllocDefault));
+    for (int64_t at = 0; at < t->numel; at += static_cast<int64_t>(chunk_el)) {
+      const size_t n = static_cast<size_t>(std::min<int64_t>(static_cast<int64_t>(chunk_el), t->numel - at));
+      CK(cudaMemcpyAsync(pb.p, static_cast<const char*>(t->data) + at * t->elem(), n * t->elem(),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      const void* src = pb.p;
+      if (t->dtype == CPDGPU_F32) {  // exact widening to the file's f64
+        const float* f = static_cast<const float*>(pb.p);
+        double* w = static_cast<double*>(wide.p);
+        for (size_t k = 0; k < n; ++k) w[k] = static_cast<double>(f[k]);
+        src = wide.p;
+      }
+      if (std::fwrite(src, 8, n, fc.f) != n) fail(CPDGPU_ARGUMENT_ERROR, "%s: write failed", path);
+    }
+  });
+}
+
 int cpdgpu_select_pivot(int N, const int64_t* dims, int* pivot) {
   return guarded(nullptr, [&] {
     if (!dims || !pivot || N < 0) fail(CPDGPU_ARGUMENT_ERROR, "select_pivot: null argument");

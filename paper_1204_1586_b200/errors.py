@@ -27,12 +27,16 @@ class NumericError(CpdError, ArithmeticError):
     """Numerical failure, e.g. non-finite values (errors.hpp:29-31)."""
 
 
+class ParseError(CpdError, RuntimeError):
+    """Malformed tensor file; the message carries the byte offset (errors.hpp:33-36)."""
+
+
 class DeviceError(CpdError, RuntimeError):
     """CUDA/device failure or a missing device library (no reference counterpart)."""
 
 
 _BY_STATUS = {1: ShapeError, 2: IndexError, 3: ArgumentError, 4: NumericError, 5: DomainError,
-              6: DeviceError, 7: DeviceError}
+              6: DeviceError, 7: DeviceError, 8: ParseError}
 
 
 def from_status(status: int, msg: str) -> CpdError:

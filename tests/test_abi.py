@@ -104,5 +104,5 @@ def test_missing_library_is_an_error(monkeypatch, tmp_path):
 def test_status_mapping():
     from paper_1204_1586_b200 import errors
     for code, cls in [(1, cpd.ShapeError), (2, cpd.IndexError), (3, cpd.ArgumentError), (4, cpd.NumericError),
-                      (5, cpd.DomainError), (6, cpd.DeviceError)]:
+                      (5, cpd.DomainError), (6, cpd.DeviceError), (8, cpd.ParseError)]:
         assert isinstance(errors.from_status(code, "m"), cls)
