@@ -95,6 +95,13 @@ int cpdgpu_tensor_norm2(cpdgpu_ctx* ctx, cpdgpu_tensor* t, double* out);
 int cpdgpu_tensor_device_ptr(const cpdgpu_tensor* t, void** device_ptr);
 int cpdgpu_tensor_free(cpdgpu_tensor* t);
 
+/* ---- problem generation and cost (rng.hpp:9-26, kruskal.cpp:58-77) -------
+ * uniform01_fill: the reference's Uniform01 stream (mt19937_64, splitmix seed),
+ * host-side and bitwise identical; generate_problem / random_init draw from it.
+ * cost: |Y - full(model)|^2 on the device by the Gram identity. */
+int cpdgpu_uniform01_fill(uint64_t seed, int64_t n, double* out);
+int cpdgpu_cost(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const double* const* factors, double* out);
+
 /* ---- TDNB tensor files (io.hpp:10-12, io.cpp:162-216) --------------------
  * Binary form "TDNB" + u32 LE N + u32 LE dims + f64 LE values (vec order).
  * load: streams the file through pinned double buffers straight to the device;

@@ -9,7 +9,8 @@ from .api import (DIST_NORMAL, DIST_UNIFORM_PM1, F32, F64, Context, CostCounter,
                   FastStats, RunTrace, SolveOptions, SolveResult, als_sweep_fast, als_update_mode,
                   cp_gradient_all, cp_gradient_all_device, default_context, fast_count_realized,
                   fast_update_order, pinv_psd, run, select_pivot, sort_modes, mttkrp_direct,
-                  mttkrp_direct_device, als_sweep_direct, mu_sweep, gd_step)
+                  mttkrp_direct_device, als_sweep_direct, mu_sweep, gd_step, uniform01, random_init,
+                  generate_problem, cost, relative_error, cp_gradient_set)
 
 __all__ = [
     "ArgumentError", "CpdError", "DeviceError", "DomainError", "IndexError", "NumericError", "ParseError",
@@ -17,5 +18,6 @@ __all__ = [
     "DenseTensor", "FastStats", "RunTrace", "SolveOptions", "SolveResult", "als_sweep_fast",
     "als_update_mode", "cp_gradient_all", "cp_gradient_all_device", "default_context",
     "fast_count_realized", "fast_update_order", "pinv_psd", "run", "select_pivot", "sort_modes",
-    "mttkrp_direct", "mttkrp_direct_device", "als_sweep_direct", "mu_sweep", "gd_step",
+    "mttkrp_direct", "mttkrp_direct_device", "als_sweep_direct", "mu_sweep", "gd_step", "uniform01",
+    "random_init", "generate_problem", "cost", "relative_error", "cp_gradient_set",
 ]

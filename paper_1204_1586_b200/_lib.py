@@ -50,6 +50,8 @@ SIGNATURES = {
     "cpdgpu_cp_gradient_all_device": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, C.c_void_p, C.c_void_p, C.c_int]),
     "cpdgpu_pinv_psd": (C.c_int, [C.c_void_p, c_i64, c_dbl_p, C.c_double, c_dbl_p]),
     "cpdgpu_als_update_mode": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(c_i64), c_i64, c_dbl_p, c_dbl_pp, C.c_int, C.c_double, c_dbl_p]),
+    "cpdgpu_uniform01_fill": (C.c_int, [c_u64, c_i64, c_dbl_p]),
+    "cpdgpu_cost": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, c_dbl_p]),
     "cpdgpu_tensor_load_tdnb": (C.c_int, [C.c_void_p, C.c_char_p, c_i64, c_i64, C.POINTER(C.c_void_p)]),
     "cpdgpu_tensor_save_tdnb": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p]),
     "cpdgpu_mttkrp_direct": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_int, c_dbl_p, C.POINTER(c_u64)]),

@@ -506,6 +506,64 @@ def _sweep_call(y, factors, counter, call):
         counter.charge(int(mults.value))
 
 
+def uniform01(seed: int, n: int) -> np.ndarray:
+    """The reference's Uniform01 stream (rng.hpp:9-26): mt19937_64 with a splitmix seed."""
+    out = np.empty(int(n), dtype=np.float64)
+    _lib.check(_lib.load().cpdgpu_uniform01_fill(C.c_uint64(seed), int(n), out.ctypes.data_as(_lib.c_dbl_p)))
+    return out
+
+
+def random_init(dims: Sequence[int], rank: int, seed: int) -> list[np.ndarray]:
+    """random_init (als.cpp:122-135): uniform(0,1) factors, column-major per mode in order."""
+    if rank < 1:
+        raise errors.ArgumentError("random_init: rank must be positive")
+    v = uniform01(seed, sum(int(d) for d in dims) * int(rank))
+    out, at = [], 0
+    for d in dims:
+        out.append(v[at:at + int(d) * rank].reshape(int(d), rank, order="F").copy(order="F"))
+        at += int(d) * rank
+    return out
+
+
+def generate_problem(dims: Sequence[int], rank: int, seed: int, ctx: Optional[Context] = None):
+    """generate_problem (bench.cpp:129-137): tensor from `seed`, init factors from seed + 1."""
+    n = int(np.prod([int(d) for d in dims]))
+    return DenseTensor.from_values(uniform01(seed, n), dims, ctx=ctx), random_init(dims, rank, seed + 1)
+
+
+def cost(y: DenseTensor, factors: list) -> float:
+    """cost(y, model) (kruskal.cpp:58-77) on the device (Gram identity)."""
+    bufs = _factor_bufs(factors, y.dims)
+    out = C.c_double()
+    ctx = y.ctx
+    _lib.check(ctx._L.cpdgpu_cost(ctx.h, y.h, bufs[0].shape[1], _ptr_array(bufs), C.byref(out)), ctx.h)
+    return float(out.value)
+
+
+def relative_error(y: DenseTensor, factors: list) -> float:
+    """relative_error (kruskal.cpp:79-81)."""
+    return float(np.sqrt(cost(y, factors)) / np.sqrt(y.norm2()))
+
+
+def cp_gradient_set(y: DenseTensor, factors: list, mttkrp_results: list) -> tuple:
+    """cp_gradient_set (kruskal.cpp:83-101): G(n) = M(n) - A(n) W(n) and the stacked
+    derivative g = -2 [vec G(1); ...; vec G(N)] (host epilogue of device gradients)."""
+    bufs = _factor_bufs(factors, y.dims)
+    if len(mttkrp_results) != len(bufs):
+        raise errors.ArgumentError(f"cp_gradient_set: {len(mttkrp_results)} mttkrp matrices for order {len(bufs)}")
+    grams = [b.T @ b for b in bufs]
+    modes = []
+    for n, (M, A) in enumerate(zip(mttkrp_results, bufs)):
+        if M.shape != A.shape:
+            raise errors.ShapeError(f"cp_gradient_set: mttkrp matrix for mode {n + 1} has wrong size")
+        W = np.ones_like(grams[0])
+        for k, g in enumerate(grams):
+            if k != n:
+                W = W * g
+        modes.append(M - A @ W)
+    return modes, -2.0 * np.concatenate([G.reshape(-1, order="F") for G in modes])
+
+
 ALGORITHMS = {"als_direct": 0, "als_fast": 1, "mu": 2, "gd": 3}
 
 

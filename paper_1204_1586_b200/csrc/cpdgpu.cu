@@ -16,6 +16,7 @@
 #include <map>
 #include <memory>
 #include <numeric>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -1885,6 +1886,40 @@ int cpdgpu_tensor_save_tdnb(cpdgpu_ctx* ctx, const cpdgpu_tensor* t, const char*
       }
       if (std::fwrite(src, 8, n, fc.f) != n) fail(CPDGPU_ARGUMENT_ERROR, "%s: write failed", path);
     }
+  });
+}
+
+// Uniform01 (rng.hpp:9-26): std::mt19937_64 seeded with the splitmix of the seed,
+// 53-bit doubles in [0, 1); the reference's generate_problem / random_init draws.
+int cpdgpu_uniform01_fill(uint64_t seed, int64_t n, double* out) {
+  return guarded(nullptr, [&] {
+    if (n > 0 && !out) fail(CPDGPU_ARGUMENT_ERROR, "uniform01_fill: null output");
+    uint64_t x = seed + 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    std::mt19937_64 eng(x ^ (x >> 31));
+    for (int64_t i = 0; i < n; ++i) out[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+  });
+}
+
+// cost(y, model) (kruskal.cpp:58-77) on the device by the Gram identity:
+// |Y|^2 - 2 <Y, Yhat> + 1^T (hadamard of the Grams) 1, <Y, Yhat> = sum A_n .* M_n
+// with one direct MTTKRP (sorted mode 1, the cheapest side).
+int cpdgpu_cost(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const double* const* factors, double* out) {
+  return guarded(ctx, [&] {
+    validate_common(ctx, y, R, "cost");
+    if (!factors || !out) fail(CPDGPU_ARGUMENT_ERROR, "cost: null argument");
+    if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "cost: rank above the device limit 64");
+    ensure_sorted(ctx, y);
+    Plan& pl = *get_plan(ctx, y, R, 0);
+    bind_seed_inputs(ctx, pl, y);
+    upload_host_factors(ctx, pl, y, factors);
+    prepare_als(ctx, pl, y);
+    pl.costs.ensure(sizeof(double));
+    direct_body_fs(ctx, pl, pl.perm[0]);
+    als_cost(ctx, pl, pl.costs.d(), 1);
+    CK(cudaMemcpyAsync(out, pl.costs.d(), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
