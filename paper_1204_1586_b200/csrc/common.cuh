@@ -18,6 +18,32 @@ constexpr int kMaxModes = 16;  // modes per Khatri-Rao range
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// Launch timeline (diagnostics only; compiled in with -DCPDGPU_TIMELINE, enabled
+// at run time by CPDGPU_TIMELINE=1): per launch slot, the earliest CTA entry,
+// the earliest return from the dependency wait and the last warp exit, in
+// globaltimer nanoseconds.  Compiled out by default: even the null-pointer
+// checks measurably delayed the small latency-bound kernels (c1: +2 us/step).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+#ifndef CPDGPU_TIMELINE
+__device__ __forceinline__ void tl_begin(unsigned long long*, int) {}
+__device__ __forceinline__ void tl_mid(unsigned long long*, int) {}
+__device__ __forceinline__ void tl_end(unsigned long long*, int) {}
+#else
+__device__ __forceinline__ void tl_begin(unsigned long long* tl, int slot) {
+  if (tl && threadIdx.x == 0) atomicMin(tl + 3 * slot, gtimer());
+}
+__device__ __forceinline__ void tl_mid(unsigned long long* tl, int slot) {
+  if (tl && threadIdx.x == 0) atomicMin(tl + 3 * slot + 1, gtimer());
+}
+__device__ __forceinline__ void tl_end(unsigned long long* tl, int slot) {
+  if (tl && (threadIdx.x & 31) == 0) atomicMax(tl + 3 * slot + 2, gtimer());
+}
+#endif
+
 // Host: launch with (pdl = true) or without the programmatic attribute.
 template <typename... Exp, typename... Act>
 inline cudaError_t launch_k(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,

@@ -321,6 +321,16 @@ struct cpdgpu_ctx {
   bool timing = false;
   std::vector<cudaEvent_t> seed_events;  // pairs around K1 launches
   size_t seed_used = 0;                  // events used by the current call
+  // launch timeline (CPDGPU_TIMELINE=1, diagnostics): [slot][entry, wait return, exit]
+  bool tl_on = std::getenv("CPDGPU_TIMELINE") != nullptr;
+  DevBuf tl;
+  int tl_next = 0;
+  unsigned long long* tl_ptr() {
+    if (!tl_on) return nullptr;
+    tl.ensure(64 * 3 * sizeof(unsigned long long));
+    return static_cast<unsigned long long*>(tl.p);
+  }
+  int tl_slot() { return tl_next < 64 ? tl_next++ : 63; }
   ~cpdgpu_ctx() {
     for (auto e : seed_events) cudaEventDestroy(e);
   }
@@ -774,10 +784,12 @@ void run_seeds(cpdgpu_ctx* ctx, Plan& pl, int mode) {
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
     DevBuf tb;
     if (trace) {
-      tb.ensure(static_cast<size_t>(c.sp.P) * 9 * 4 * 8);
+      tb.ensure(static_cast<size_t>(c.sp.P) * 9 * 8 * 8);
       CK(cudaMemsetAsync(tb.p, 0, tb.bytes, s));
       c.sp.trace = static_cast<unsigned long long*>(tb.p);
     }
+    c.sp.tl = ctx->tl_ptr();
+    c.sp.tl_slot = c.sp.tl ? ctx->tl_slot() : 0;
     if (mode == 2 && pl.use_lc) {
       cpdgpu::SeedParams q = c.sp;
       q.TI = static_cast<int>(pl.lc_TJ);
@@ -794,21 +806,31 @@ void run_seeds(cpdgpu_ctx* ctx, Plan& pl, int mode) {
     }
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
     if (trace) {
-      std::vector<unsigned long long> h(static_cast<size_t>(c.sp.P) * 36);
+      std::vector<unsigned long long> h(static_cast<size_t>(c.sp.P) * 72);
       CK(cudaMemcpyAsync(h.data(), tb.p, tb.bytes, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       c.sp.trace = nullptr;
       double w[9] = {0}, tot[9] = {0}, mx = 0;
+      unsigned long long g0 = ~0ull;
+      for (int cta = 0; cta < c.sp.P; ++cta) g0 = std::min(g0, h[static_cast<size_t>(cta) * 72 + 1]);
+      double pdl[9] = {0}, end[9] = {0}, endmax = 0, entmax = 0;
       for (int cta = 0; cta < c.sp.P; ++cta)
         for (int wp = 0; wp < 9; ++wp) {
-          const unsigned long long* e = &h[(static_cast<size_t>(cta) * 9 + wp) * 4];
+          const unsigned long long* e = &h[(static_cast<size_t>(cta) * 9 + wp) * 8];
           w[wp] += e[0];
           tot[wp] += e[2];
           mx = std::max(mx, static_cast<double>(e[2]));
+          pdl[wp] += static_cast<double>(e[4] - g0);
+          end[wp] += static_cast<double>(e[6] - g0);
+          endmax = std::max(endmax, static_cast<double>(e[6] - g0));
+          entmax = std::max(entmax, static_cast<double>(e[1] - g0));
         }
       std::fprintf(stderr, "[seed trace mode %d] per-warp avg cycles (wait/total): ", mode);
       for (int wp = 0; wp < 9; ++wp) std::fprintf(stderr, "w%d %.0f/%.0f  ", wp, w[wp] / c.sp.P, tot[wp] / c.sp.P);
       std::fprintf(stderr, "max warp total %.0f\n", mx);
+      std::fprintf(stderr, "[seed trace mode %d] ns from first CTA entry: last entry %.0f, pdl return w0 %.0f w8 %.0f, "
+                   "end avg w0 %.0f w4 %.0f, last end %.0f\n", mode, entmax, pdl[0] / c.sp.P, pdl[8] / c.sp.P,
+                   end[0] / c.sp.P, end[4] / c.sp.P, endmax);
     }
   }
   CK(cudaGetLastError());
@@ -1023,8 +1045,39 @@ void redirect_to_gradient(const Plan& pl, cpdgpu::TailStep& st, bool right) {
   }
 }
 
-void launch_step(cpdgpu_ctx* ctx, Plan& pl, const cpdgpu::TailStep& st) {
+void launch_step(cpdgpu_ctx* ctx, Plan& pl, const cpdgpu::TailStep& st0) {
+  cpdgpu::TailStep st = st0;
+  st.tl = ctx->tl_ptr();
+  if (st.tl) st.tl_slot = ctx->tl_slot();
   ctx->launches += cpdgpu::launch_tail_step(st, static_cast<double* const*>(pl.gtab.p), ctx->num_sms, ctx->stream);
+}
+
+// CPDGPU_TIMELINE: reset the stamps before a call, print them after it.
+void timeline_reset(cpdgpu_ctx* ctx) {
+  if (!ctx->tl_on) return;
+  static std::vector<unsigned long long> init = [] {
+    std::vector<unsigned long long> v(64 * 3, ~0ull);
+    for (int i = 0; i < 64; ++i) v[3 * i + 2] = 0;
+    return v;
+  }();
+  CK(cudaMemcpyAsync(ctx->tl_ptr(), init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  ctx->tl_next = 1;  // slot 0: prologue
+}
+void timeline_print(cpdgpu_ctx* ctx, const char* what) {
+  if (!ctx->tl_on) return;
+  std::vector<unsigned long long> h(64 * 3);
+  CK(cudaMemcpyAsync(h.data(), ctx->tl_ptr(), h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double t0 = static_cast<double>(h[0]);
+  std::fprintf(stderr, "[timeline %s] us from prologue entry (entry/wait/exit):", what);
+  for (int i = 0; i < 64; ++i) {  // graph replays keep the slots of the capture
+    if (h[3 * i + 2] == 0) continue;
+    std::fprintf(stderr, "  #%d %.1f/%.1f/%.1f", i, (h[3 * i] - t0) * 1e-3, (h[3 * i + 1] - t0) * 1e-3,
+                 (h[3 * i + 2] - t0) * 1e-3);
+  }
+  std::fprintf(stderr, "\n");
 }
 
 // Whole hook-free gradient after the prologue: fused seeds, reductions, then
@@ -1142,7 +1195,18 @@ void sweep_body(cpdgpu_ctx* ctx, Plan& pl, const ModeCallback& after) {
 // each call patches the prologue node (input factors, output pointers).
 void run_gradient(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_base) {
   const bool left = pl.p + 1 <= pl.N;
-  const cpdgpu::Prologue pr = grad_prologue(pl, fin, gout_base, left ? 3 : 1);
+  cpdgpu::Prologue pr = grad_prologue(pl, fin, gout_base, left ? 3 : 1);
+  pr.tl = ctx->tl_ptr();
+  timeline_reset(ctx);
+  struct PrintAtExit {
+    cpdgpu_ctx* c;
+    ~PrintAtExit() {
+      try {
+        timeline_print(c, "gradient");
+      } catch (...) {
+      }
+    }
+  } print_at_exit{ctx};
   const bool use_graph = ctx->graphs && !ctx->timing && std::getenv("CPDGPU_SEED_TRACE") == nullptr;
   if (!use_graph) {
     ctx->launches += cpdgpu::launch_prologue(pr, static_cast<double**>(pl.gtab.p), ctx->num_sms, ctx->stream);

@@ -29,7 +29,9 @@ struct SeedParams {
   KRSpec right;     // modes p+1..N (columns of the view)
   const double* KRl_g;  // Khatri-Rao rows of the view's rows    [J][LDK] (kr_materialize)
   const double* KRr_g;  // Khatri-Rao rows of the view's columns [K][LDK]
-  unsigned long long* trace;  // optional per-warp cycle counters [P][9][4] (CPDGPU_SEED_TRACE)
+  unsigned long long* trace;  // optional per-warp counters [P][9][8] (CPDGPU_SEED_TRACE)
+  unsigned long long* tl;     // launch timeline (CPDGPU_TIMELINE) and this launch's slot
+  int tl_slot;
   double* Rpart;    // [P * slots][R8][TI]
   double* Lpart;    // [nRB][R][K]
 };
@@ -111,11 +113,14 @@ struct TailOp {
   int RP, TI;
   const int* rb_ptr;
   const int* slot_list;
+  int cta;  // set by launch_tail_step: long contractions run one output per CTA
 };
 constexpr int kMaxTailOps = 8;
 struct TailStep {
   int n;
   TailOp op[kMaxTailOps];
+  unsigned long long* tl = nullptr;  // launch timeline (CPDGPU_TIMELINE)
+  int tl_slot = 0;
 };
 int64_t tail_step_units(const TailStep& st);
 int launch_tail_step(const TailStep& st, double* const* gtab, int num_sms, cudaStream_t s);
@@ -138,6 +143,7 @@ struct Prologue {
   double* gout[kMaxModes];
   int nkr;
   KRJob kr[kMaxKRJobs];
+  unsigned long long* tl = nullptr;  // launch timeline (CPDGPU_TIMELINE), slot 0
 };
 int launch_prologue(const Prologue& pr, double** gtab, int num_sms, cudaStream_t s);
 const void* prologue_kernel_fn();

@@ -23,10 +23,11 @@
 //    36.7 TF/s for DFMA, with a sixteenth of the issue slots.  Right product
 //    Rs = Y * KR_r (M = rows, N = rank, K = columns); left product as
 //    Ls^T = KR_l^T * Y (M = rank, N = columns, K = rows).
-//  * MODE 3 splits the consumers by product (warps 0-3 right, 4-7 left) so no
-//    cross-warp reduction is needed; right partials persist in registers over a
-//    row block and go out once per (CTA, row block) slot, left partials once per
-//    tile and row block.  tail.cu reduces both in a fixed order, so results are
+//  * MODE 3 splits the consumers by product (warps 0-3 right, 4-7 left); right
+//    partials persist in registers over a row block and go out once per (CTA,
+//    row block) slot; the left warps split each tile's rows four ways with their
+//    KR_l slice held in registers and combine once per tile (left_reg_role),
+//    left partials go out once per tile and row block.  tail.cu reduces both in a fixed order, so results are
 //    bitwise reproducible.
 #include <cstdint>
 #include <cstring>
@@ -86,6 +87,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+
+// tile -> (row block, column tile) without the 64-bit division helper call
+__device__ __forceinline__ int64_t tile_rb(int64_t tile, int64_t nCT) {
+  if ((static_cast<uint64_t>(tile) >> 32) == 0 && (static_cast<uint64_t>(nCT) >> 32) == 0)
+    return static_cast<uint32_t>(tile) / static_cast<uint32_t>(nCT);
+  return tile / nCT;
+}
 
 constexpr int kTJ = 32;          // columns per tile
 constexpr int kConsumers = 8;    // consumer warps
@@ -98,7 +111,7 @@ struct Ring {
   double* Ys;   // [STAGES][32 * LDY]
   double* KRr;  // [STAGES][32 * LDK]
   double* KRl;  // [TI * LDK]
-  double* red;  // [2][4 * 32 * NT * 2] (MODE 2)
+  double* red;  // MODE 2: [2][4 * 32 * NT * 2]; MODE 3: [2][4][3][NT][2][32]
   int stages, TI, LDY, LDK;
 };
 
@@ -160,7 +173,7 @@ __device__ void right_role(const SeedParams& p, const Ring& q, int64_t t0, int n
   for (int k = 0; k < ntiles; ++k) {
     const int s = k % q.stages;
     const int64_t tile = t0 + k;
-    const int64_t rb = tile / p.nCT;
+    const int64_t rb = tile_rb(tile, p.nCT);
     if (rb != cur_rb) {  // the right product never reads KR_l: flush and go on
       if (cur_rb >= 0) flush(cur_rb);
       cur_rb = rb;
@@ -195,82 +208,90 @@ __device__ void right_role(const SeedParams& p, const Ring& q, int64_t t0, int n
   if (cur_rb >= 0) flush(cur_rb);
 }
 
-// Left product, one 8-column fragment per warp over the full K = TI rows:
-// Ls^T[r, j] = sum_i KR_l^T[r, i] Y[i, j].  Four k-steps per step into four
-// accumulator sets (4 NT independent DMMA chains), operands for the next four
-// k-steps loaded while the current ones issue.  Writes the tile's left partial.
+// Left product of the fused pass, alternating tiles between two warp pairs:
+// pair (k & 1) takes tile k, warp c of the pair the 8-column fragments 2c and
+// 2c + 1 over the full K = TI rows.  A k-step costs two Y fragment loads and NT
+// Khatri-Rao fragment loads for 2 NT DMMAs; two k-interleaved accumulator sets
+// give 4 NT independent chains.  No per-tile synchronisation: every tile is
+// released by the four right warps and the two warps of its pair (the empty
+// barriers count 6 arrivals in MODE 3).  All four left warps walk every tile
+// index so they meet at each row-block change to refresh KR_l.
 template <int NT>
-__device__ __forceinline__ void left_load4(const double* yb, const double* kl, int ks, int ksteps, double (&y)[4],
-                                           double (&l)[4][NT]) {
-  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const bool ok = ks + u < ksteps;
-    y[u] = ok ? yb[(ks + u) * 4] : 0.0;
-#pragma unroll
-    for (int nb = 0; nb < NT; ++nb) l[u][nb] = ok ? kl[(ks + u) * 4 * LDK + nb * 8] : 0.0;
-  }
-}
-
-template <int NT>
-__device__ __forceinline__ void left_mma4(double (&acc)[4][NT][2], const double (&y)[4], const double (&l)[4][NT]) {
-#pragma unroll
-  for (int nb = 0; nb < NT; ++nb)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) dmma(acc[u][nb], l[u][nb], y[u]);
-}
-
-template <int NT>
-__device__ void left_role(const SeedParams& p, const Ring& q, int64_t t0, int ntiles, int nf, int lane, int tid,
-                          unsigned long long& cw) {
+__device__ void left_pair_role(const SeedParams& p, const Ring& q, int64_t t0, int ntiles, int lw, int lane,
+                               unsigned long long& cw) {
   constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
   const int g = lane >> 2, t = lane & 3;
   const int LDY = q.LDY, TI = q.TI;
-  const int ksteps = TI >> 2;
+  const int ksteps = TI >> 2;  // even: TI is a multiple of 8
+  const int pair = lw >> 1, c = lw & 1;
   int64_t cur_rb = -1;
   for (int k = 0; k < ntiles; ++k) {
-    const int s = k % q.stages;
     const int64_t tile = t0 + k;
-    const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
-    if (rb != cur_rb) {  // only the four left warps read KR_l
+    const int64_t rb = tile_rb(tile, p.nCT), ct = tile - rb * p.nCT;
+    if (rb != cur_rb) {
       asm volatile("bar.sync 2, 128;\n" ::: "memory");
-      load_krl(p, q, rb, tid - 128, 128);
+      load_krl(p, q, rb, lw * 32 + lane, 128);
       asm volatile("bar.sync 2, 128;\n" ::: "memory");
       cur_rb = rb;
     }
+    if ((k & 1) != pair) continue;
+    const int s = k % q.stages;
     const unsigned long long w0 = clock64();
     mbar_wait(&q.full[s], (k / q.stages) & 1);
     cw += clock64() - w0;
-    const double* yb = q.Ys + s * kTJ * LDY + (nf * 8 + g) * LDY + t;
+    // B fragments: Y[ks 4 + t][(2c + f) 8 + g]; A fragments: KR_l[ks 4 + t][nb 8 + g]
+    const double* yb = q.Ys + s * kTJ * LDY + (c * 16 + g) * LDY + t;
     const double* kl = q.KRl + t * LDK + g;
-    double acc[4][NT][2];
+    double acc[2][2][NT][2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int nb = 0; nb < NT; ++nb) acc[u][nb][0] = acc[u][nb][1] = 0.0;
-    double yP[4], lP[4][NT], yQ[4], lQ[4][NT];
-    left_load4<NT>(yb, kl, 0, ksteps, yP, lP);
-    for (int ks = 0; ks < ksteps; ks += 8) {
-      left_load4<NT>(yb, kl, ks + 4, ksteps, yQ, lQ);
-      left_mma4<NT>(acc, yP, lP);
-      if (ks + 4 >= ksteps) break;
-      left_load4<NT>(yb, kl, ks + 8, ksteps, yP, lP);
-      left_mma4<NT>(acc, yQ, lQ);
-    }
-    const int64_t col = ct * kTJ + nf * 8 + 2 * t;
-    double* dst = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K;
+      for (int f = 0; f < 2; ++f)
 #pragma unroll
-    for (int nb = 0; nb < NT; ++nb) {
-      const int r = nb * 8 + g;
-      if (r < p.R) {
-        const double v0 = (acc[0][nb][0] + acc[1][nb][0]) + (acc[2][nb][0] + acc[3][nb][0]);
-        const double v1 = (acc[0][nb][1] + acc[1][nb][1]) + (acc[2][nb][1] + acc[3][nb][1]);
-        if (col < p.K) dst[r * p.K + col] = v0;
-        if (col + 1 < p.K) dst[r * p.K + col + 1] = v1;
+        for (int nb = 0; nb < NT; ++nb) acc[h][f][nb][0] = acc[h][f][nb][1] = 0.0;
+    double y[2][2][2], l[2][2][NT];  // [buffer][k-step of the pair][...]
+    auto load = [&](int buf, int ks) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int f = 0; f < 2; ++f) y[buf][h][f] = yb[f * 8 * LDY + (ks + h) * 4];
+#pragma unroll
+        for (int nb = 0; nb < NT; ++nb) l[buf][h][nb] = kl[(ks + h) * 4 * LDK + nb * 8];
       }
+    };
+    load(0, 0);
+    for (int ks = 0; ks < ksteps; ks += 4) {
+      if (ks + 2 < ksteps) load(1, ks + 2);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int nb = 0; nb < NT; ++nb)
+#pragma unroll
+          for (int f = 0; f < 2; ++f) dmma(acc[h][f][nb], l[0][h][nb], y[0][h][f]);
+      if (ks + 2 >= ksteps) break;
+      if (ks + 4 < ksteps) load(0, ks + 4);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int nb = 0; nb < NT; ++nb)
+#pragma unroll
+          for (int f = 0; f < 2; ++f) dmma(acc[h][f][nb], l[1][h][nb], y[1][h][f]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&q.empty[s]);
+    double* dst = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K;
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int64_t col = ct * kTJ + (c * 2 + f) * 8 + 2 * t;
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        const int r = nb * 8 + g;
+        if (r < p.R) {
+          if (col < p.K) dst[r * p.K + col] = acc[0][f][nb][0] + acc[1][f][nb][0];
+          if (col + 1 < p.K) dst[r * p.K + col + 1] = acc[0][f][nb][1] + acc[1][f][nb][1];
+        }
+      }
+    }
   }
 }
 
@@ -290,7 +311,7 @@ __device__ void left_only_role(const SeedParams& p, const Ring& q, int64_t t0, i
   for (int k = 0; k < ntiles; ++k) {
     const int s = k % q.stages;
     const int64_t tile = t0 + k;
-    const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
+    const int64_t rb = tile_rb(tile, p.nCT), ct = tile - rb * p.nCT;
     if (rb != cur_rb) row_block_change(p, q, rb, cur_rb, true, tid, [](int64_t) {});
     const unsigned long long w0 = clock64();
     mbar_wait(&q.full[s], (k / q.stages) & 1);
@@ -368,6 +389,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // right-product row fragments per warp: 4 warps in MODE 3, 8 in MODE 1
   // register budget: 9 warps put 3 on one SMSP -> <= 168 registers per thread
   constexpr int kMaxMF = (MODE == 3) ? (NT <= 2 ? 7 : (NT == 3 ? 6 : 5)) : 4;
+  const unsigned long long g_entry = p.trace ? gtime() : 0;
+  tl_begin(p.tl, p.tl_slot);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int cta = blockIdx.x;
@@ -387,7 +410,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* Ys = reinterpret_cast<double*>(base + 128);    // [STAGES][kTJ * LDY]
   double* KRr = Ys + STAGES * kTJ * LDY;                 // [STAGES][kTJ * LDK]
   double* KRl = KRr + STAGES * kTJ * LDK;                // [TI * LDK]
-  double* red = KRl + ((MODE & 2) ? TI * LDK : 0);       // [2][4 * 32 * NT * 2] (MODE 2)
+  // MODE 2: [2][4 * 32 * NT * 2] after KR_l; MODE 3 keeps KR_l in registers and
+  // uses the space for the left slices' reduction ([2][4][3][NT][2][32])
+  double* red = KRl + ((MODE & 2) ? TI * LDK : 0);
 
   // plain-copy path: zero the stage buffers once (edge tiles are cleared below)
   if (!p.use_tma)
@@ -399,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers);
+      mbar_init(&empty[s], MODE == 3 ? 6 : kConsumers);  // MODE 3: 4 right + the tile's left pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -415,14 +440,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0)
       for (int k = 0; k < early; ++k) {
         const int64_t tile = t0 + k;
-        const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
+        const int64_t rb = tile_rb(tile, p.nCT), ct = tile - rb * p.nCT;
         mbar_arrive_tx(&full[k], LDY * kTJ * 8 + ((MODE & 1) ? kTJ * LDK * 8 : 0));
         tma_load_2d(Ys + k * kTJ * LDY, &tmap, static_cast<int>(rb * TI), static_cast<int>(ct * kTJ), &full[k], true);
       }
     pdl_wait();
+    const unsigned long long g_pdl = p.trace ? gtime() : 0;
     if (lane == 0 && (MODE & 1))
       for (int k = 0; k < early; ++k) {
-        const int64_t ct = (t0 + k) % p.nCT;
+        const int64_t ct = (t0 + k) - tile_rb(t0 + k, p.nCT) * p.nCT;
         tma_load_2d(KRr + k * kTJ * LDK, &kmap, 0, static_cast<int>(ct * kTJ), &full[k]);
       }
     for (int k = early; k < ntiles; ++k) {
@@ -433,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tw += clock64() - a;
       }
       const int64_t tile = t0 + k;
-      const int64_t rb = tile / p.nCT, ct = tile - rb * p.nCT;
+      const int64_t rb = tile_rb(tile, p.nCT), ct = tile - rb * p.nCT;
       const int64_t row0 = rb * TI, col0 = ct * kTJ;
       double* ys = Ys + s * kTJ * LDY;
       double* kr = KRr + s * kTJ * LDK;
@@ -460,14 +486,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (p.trace && lane == 0) {
-      unsigned long long* tr = p.trace + (static_cast<int64_t>(cta) * 9 + warp) * 4;
-      tr[0] = tw; tr[1] = 0; tr[2] = clock64() - tstart; tr[3] = ntiles;
+      unsigned long long* tr = p.trace + (static_cast<int64_t>(cta) * 9 + warp) * 8;
+      tr[0] = tw; tr[1] = g_entry; tr[2] = clock64() - tstart; tr[3] = ntiles; tr[4] = g_pdl; tr[6] = gtime();
     }
+    tl_end(p.tl, p.tl_slot);
     return;
   }
 
   // ------------------------------------------------------------------ consumers
   pdl_wait();  // Khatri-Rao rows and the partial buffers belong to the preceding kernels
+  const unsigned long long g_pdl = p.trace ? gtime() : 0;
+  if (warp == 0) tl_mid(p.tl, p.tl_slot);
   const Ring q{full, empty, Ys, KRr, KRl, red, STAGES, TI, LDY, LDK};
   unsigned long long cw = 0;
   const unsigned long long cstart = clock64();
@@ -476,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int mc = (nMF - warp + 3) / 4;
       right_dispatch<NT, 4, kMaxMF>(mc, p, q, t0, ntiles, cta, warp, lane, tid, true, cw);
     } else {
-      left_role<NT>(p, q, t0, ntiles, warp - 4, lane, tid, cw);
+      left_pair_role<NT>(p, q, t0, ntiles, warp - 4, lane, cw);
     }
   } else if (MODE == 1) {
     const int mc = (nMF - warp + 7) / 8;
@@ -485,9 +514,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     left_only_role<NT>(p, q, t0, ntiles, warp, lane, tid, cw);
   }
   if (p.trace && lane == 0) {
-    unsigned long long* tr = p.trace + (static_cast<int64_t>(cta) * 9 + warp) * 4;
-    tr[0] = cw; tr[1] = 0; tr[2] = clock64() - cstart; tr[3] = ntiles;
+    unsigned long long* tr = p.trace + (static_cast<int64_t>(cta) * 9 + warp) * 8;
+    tr[0] = cw; tr[1] = g_entry; tr[2] = clock64() - cstart; tr[3] = ntiles; tr[4] = g_pdl; tr[6] = gtime();
   }
+  tl_end(p.tl, p.tl_slot);
 }
 
 // ---- left seed with column-block accumulation (ALS / hook second pass) -----------
@@ -540,13 +570,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t bytes = kTJ * TJ * 8 + kTJ * LDK * 8;
       auto load_y = [&](int k, int s) {
-        const int64_t u = t0 + k, cb = u / p.nCT, rt = u - cb * p.nCT;
+        const int64_t u = t0 + k, cb = tile_rb(u, p.nCT), rt = u - cb * p.nCT;
         double* ys = Ys + s * kTJ * TJ;
         tma_load_2d(ys, &ymap, static_cast<int>(rt * kTJ), static_cast<int>(cb * TJ), &full[s], true);
         tma_load_2d(ys + 16 * TJ, &ymap, static_cast<int>(rt * kTJ + 16), static_cast<int>(cb * TJ), &full[s], true);
       };
       auto load_k = [&](int k, int s) {
-        const int64_t u = t0 + k, rt = u % p.nCT;
+        const int64_t u = t0 + k, rt = u - tile_rb(u, p.nCT) * p.nCT;
         tma_load_2d(KRs + s * kTJ * LDK, &kmap, 0, static_cast<int>(rt * kTJ), &full[s]);
       };
       const int early = min(STAGES, ntiles);
@@ -598,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int64_t cur_cb = -1;
   for (int k = 0; k < ntiles; ++k) {
     const int s = k % STAGES;
-    const int64_t cb = (t0 + k) / p.nCT;
+    const int64_t cb = tile_rb(t0 + k, p.nCT);
     if (cb != cur_cb) {
       if (cur_cb >= 0) flush(cur_cb);
       cur_cb = cb;

@@ -11,6 +11,8 @@
 // independent of the right — so a gradient costs 1 + max(p, N - p) tail
 // launches.  Every output is produced by one warp in a fixed order, so results
 // are bitwise reproducible.
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -46,8 +48,24 @@ __device__ __forceinline__ double strided_dot(const double* z, int64_t stride, i
   return (s0 + s1) + (s2 + s3);
 }
 
+// Contractions at least this long run one output per CTA (256 threads and a
+// fixed-order block reduction) instead of one per warp: the top extraction of a
+// high-order tensor has few outputs, each a dot product over thousands of terms.
+constexpr int64_t kCtaContractLen = 1024;
+
+__host__ __device__ inline int64_t contract_len(const TailOp& o) {
+  return o.type == kOpContractA ? o.M : (o.type == kOpContractB ? o.B : 0);
+}
+
+// Number of CTA work units of an op (one per output of a long contraction).
+__host__ __device__ inline int64_t op_cta_units(const TailOp& o) {
+  if (!o.cta) return 0;
+  return o.type == kOpContractA ? o.B * o.R : o.M * o.R;
+}
+
 // Number of warp work units of an op.
 __host__ __device__ inline int64_t op_units(const TailOp& o) {
+  if (o.cta) return 0;
   switch (o.type) {
     case kOpContractA: return o.B * o.R;                       // warp per output (b, r)
     case kOpContractB: return o.M * o.R;                       // warp per output (a, r)
@@ -108,9 +126,71 @@ __device__ void run_unit(const TailOp& o, int64_t u, int lane, double* const* gt
   }
 }
 
+// One output of a long contraction on the whole CTA: 256 threads stride over the
+// contraction with four partial sums each, then warp sums and the eight warp
+// totals are added in warp order (bitwise reproducible).
+__device__ void run_cta_unit(const TailOp& o, int64_t u, double* red, double* const* gtab) {
+  double* out = op_out(o, gtab);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int r;
+  int64_t n, stride, oidx;
+  const double* z;
+  if (o.type == kOpContractA) {  // out[r][b] = sum_a Z[r][a + M b] KR_v[a, r]
+    r = static_cast<int>(u / o.B);
+    const int64_t b = u - r * o.B;
+    z = o.Z + r * o.ldz + o.M * b;
+    n = o.M;
+    stride = 1;
+    oidx = r * o.ldo + b;
+  } else {  // out[r][a] = sum_b Z[r][a + M b] KR_w[b, r]
+    r = static_cast<int>(u / o.M);
+    const int64_t a = u - r * o.M;
+    z = o.Z + r * o.ldz + a;
+    n = o.B;
+    stride = o.M;
+    oidx = r * o.ldo + a;
+  }
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t x = tid;
+  for (; x + 768 < n; x += 1024) {
+    s0 += z[x * stride] * kr_at(o.kr, x, r);
+    s1 += z[(x + 256) * stride] * kr_at(o.kr, x + 256, r);
+    s2 += z[(x + 512) * stride] * kr_at(o.kr, x + 512, r);
+    s3 += z[(x + 768) * stride] * kr_at(o.kr, x + 768, r);
+  }
+  for (; x < n; x += 256) s0 += z[x * stride] * kr_at(o.kr, x, r);
+  const double v = warp_sum((s0 + s1) + (s2 + s3));
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    out[oidx] = t;
+  }
+  __syncthreads();
+}
+
+// One recursion level.  CTA = false: every op is warp-granular (the common
+// case, kept lean); CTA = true: the step holds long contractions, whose outputs
+// run one per CTA before the warp units.
+template <bool CTA>
 __global__ void __launch_bounds__(256) tail_step_kernel(const TailStep st, double* const* gtab) {
+  tl_begin(st.tl, st.tl_slot);
   pdl_wait();     // inputs come from the previous step / seed
+  tl_mid(st.tl, st.tl_slot);
   pdl_trigger();  // the next step may launch and wait
+  if constexpr (CTA) {  // block-uniform loop over the CTA units
+    __shared__ double red[8];
+    int64_t cstart[kMaxTailOps + 1];
+    cstart[0] = 0;
+    for (int i = 0; i < st.n; ++i) cstart[i + 1] = cstart[i] + op_cta_units(st.op[i]);
+    for (int64_t cu = blockIdx.x; cu < cstart[st.n]; cu += gridDim.x) {
+      int i = 0;
+      while (cu >= cstart[i + 1]) ++i;
+      run_cta_unit(st.op[i], cu - cstart[i], red, gtab);
+    }
+  }
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   int64_t start[kMaxTailOps + 1];
@@ -122,6 +202,7 @@ __global__ void __launch_bounds__(256) tail_step_kernel(const TailStep st, doubl
     while (w >= start[i + 1]) ++i;
     run_unit(st.op[i], w - start[i], lane, gtab);
   }
+  tl_end(st.tl, st.tl_slot);
 }
 
 // Prologue: sorted factors Fs[j] <- input block perm[j]; output pointer table;
@@ -148,6 +229,8 @@ __device__ void kr_rows(const KRJob& k, int64_t t, int64_t nt) {
 }
 
 __global__ void __launch_bounds__(256) prologue_kernel(const Prologue pr, double** gtab) {
+  tl_begin(pr.tl, 0);
+  tl_mid(pr.tl, 0);
   pdl_trigger();  // the seed contraction may start streaming Y now
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -156,6 +239,7 @@ __global__ void __launch_bounds__(256) prologue_kernel(const Prologue pr, double
     for (int j = 0; j < pr.N; ++j)
       for (int64_t e = t; e < pr.len[j]; e += nt) pr.Fs[pr.dst_off[j] + e] = pr.fin[pr.src_off[j] + e];
   for (int c = 0; c < pr.nkr; ++c) kr_rows(pr.kr[c], t, nt);
+  tl_end(pr.tl, 0);
 }
 
 int grid_for(int64_t work, int threads, int cap) {
@@ -171,6 +255,12 @@ int64_t tail_step_units(const TailStep& st) {
   return n;
 }
 
+static int64_t tail_step_cta_units(const TailStep& st) {
+  int64_t n = 0;
+  for (int i = 0; i < st.n; ++i) n += op_cta_units(st.op[i]);
+  return n;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("CPDGPU_PDL");
@@ -179,10 +269,24 @@ bool pdl_enabled() {
   return on;
 }
 
-int launch_tail_step(const TailStep& st, double* const* gtab, int num_sms, cudaStream_t s) {
-  if (st.n == 0) return 0;
-  const int64_t warps = tail_step_units(st);
-  launch_k(tail_step_kernel, dim3(grid_for(warps * 32, 256, num_sms * 8)), dim3(256), 0, s, pdl_enabled(), st, gtab);
+int launch_tail_step(const TailStep& st0, double* const* gtab, int num_sms, cudaStream_t s) {
+  if (st0.n == 0) return 0;
+  TailStep st = st0;
+  for (int i = 0; i < st.n; ++i) st.op[i].cta = contract_len(st.op[i]) >= kCtaContractLen ? 1 : 0;
+  const int64_t warps = tail_step_units(st), ctas = tail_step_cta_units(st);
+  static const bool dbg = std::getenv("CPDGPU_TAIL_DEBUG") != nullptr;
+  if (dbg) {
+    std::fprintf(stderr, "[tail step] warps %lld ctas %lld:", static_cast<long long>(warps), static_cast<long long>(ctas));
+    for (int i = 0; i < st.n; ++i)
+      std::fprintf(stderr, " (type %d M %lld B %lld R %d cta %d)", st.op[i].type, static_cast<long long>(st.op[i].M),
+                   static_cast<long long>(st.op[i].B), st.op[i].R, st.op[i].cta);
+    std::fprintf(stderr, "\n");
+  }
+  const int grid = std::max(grid_for(warps * 32, 256, num_sms * 8), grid_for(ctas * 256, 256, num_sms * 8));
+  if (ctas > 0)
+    launch_k(tail_step_kernel<true>, dim3(grid), dim3(256), 0, s, pdl_enabled(), st, gtab);
+  else
+    launch_k(tail_step_kernel<false>, dim3(grid), dim3(256), 0, s, pdl_enabled(), st, gtab);
   return 1;
 }
 
