@@ -464,14 +464,14 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
     sp.R = c.Rc;
     sp.TI = TI;
     sp.LDY = LDY;
-    sp.LDK = (c.NT % 2 == 1) ? c.NT * 8 : c.NT * 8 + 8;
+    sp.LDK = cpdgpu::seed_ldk(c.NT);
     sp.nRB = nRB;
     sp.nCT = nCT;
     sp.T = T;
     sp.P = P;
     sp.slots = slots;
     sp.use32 = (Jp < (1LL << 31) && Kp < (1LL << 31)) ? 1 : 0;
-    const int lk = (c.NT % 2 == 1) ? c.NT * 8 : c.NT * 8 + 8;
+    const int lk = cpdgpu::seed_ldk(c.NT);
     const size_t ldy = pl.tma_ok ? TI + 4 : TI + 12;
     sp.stages = std::max(cpdgpu::seed_f64_smem_bytes(c.NT, TI, ldy, lk, 3, 3, 0),
                          cpdgpu::seed_f64_smem_bytes(c.NT, TI, ldy, lk, 2, 3, 0)) <= cpdgpu::kSeedSmemLimit

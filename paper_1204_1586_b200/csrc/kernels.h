@@ -35,6 +35,10 @@ struct SeedParams {
   double* Rpart;    // [P * slots][R8][TI]
   double* Lpart;    // [nRB][R][K]
 };
+// Row stride (doubles) of the Khatri-Rao row buffers and their shared-memory
+// tiles: == 4 mod 8, so the DMMA fragment loads (lane (g, t) reads row t,
+// column g) of a half-warp hit 16 distinct 8-byte banks.
+__host__ __device__ constexpr int seed_ldk(int NT) { return NT * 8 + 4; }
 int seed_f64_stages(int NT);  // default depth before the factor-staging choice
 // largest row block the fused kernel can hold in registers for this NT
 int seed_f64_max_ti(int NT);

@@ -147,7 +147,7 @@ __device__ void right_role(const SeedParams& p, const Ring& q, int64_t t0, int n
                            int tid, bool need_krl, unsigned long long& cw) {
   constexpr int RP = NT * 8;
   const int g = lane >> 2, t = lane & 3;
-  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  constexpr int LDK = seed_ldk(NT);
   const int LDY = q.LDY, TI = q.TI;
   double acc[MC > 0 ? MC : 1][NT][2];
 #pragma unroll
@@ -219,7 +219,7 @@ __device__ void right_role(const SeedParams& p, const Ring& q, int64_t t0, int n
 template <int NT>
 __device__ void left_pair_role(const SeedParams& p, const Ring& q, int64_t t0, int ntiles, int lw, int lane,
                                unsigned long long& cw) {
-  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  constexpr int LDK = seed_ldk(NT);
   const int g = lane >> 2, t = lane & 3;
   const int LDY = q.LDY, TI = q.TI;
   const int ksteps = TI >> 2;  // even: TI is a multiple of 8
@@ -301,7 +301,7 @@ template <int NT>
 __device__ void left_only_role(const SeedParams& p, const Ring& q, int64_t t0, int ntiles, int warp, int lane,
                                int tid, unsigned long long& cw) {
   const int g = lane >> 2, t = lane & 3;
-  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  constexpr int LDK = seed_ldk(NT);
   const int LDY = q.LDY, TI = q.TI;
   const int nf = warp & 3, h = warp >> 2;
   const int ksteps = TI >> 2, kh = ((ksteps >> 1) + 1) & ~1;
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     seed_left_cols_kernel(const SeedParams p, const __grid_constant__ CUtensorMap ymap,
                           const __grid_constant__ CUtensorMap kmap) {
   constexpr int RP = NT * 8;
-  constexpr int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  constexpr int LDK = seed_ldk(NT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int cta = blockIdx.x;
@@ -696,7 +696,7 @@ size_t seed_f64_smem_bytes(int NT, int TI, int LDY, int LDK, int mode, int stage
 }
 
 size_t seed_left_cols_smem_bytes(int NT, int TJ, int stages) {
-  const int LDK = (NT % 2 == 1) ? NT * 8 : NT * 8 + 8;
+  const int LDK = seed_ldk(NT);
   return 1024 + static_cast<size_t>(stages) * kTJ * (TJ + LDK) * sizeof(double) + 64;
 }
 
