@@ -828,6 +828,15 @@ void run_seeds(cpdgpu_ctx* ctx, Plan& pl, int mode) {
       std::fprintf(stderr, "[seed trace mode %d] per-warp avg cycles (wait/total): ", mode);
       for (int wp = 0; wp < 9; ++wp) std::fprintf(stderr, "w%d %.0f/%.0f  ", wp, w[wp] / c.sp.P, tot[wp] / c.sp.P);
       std::fprintf(stderr, "max warp total %.0f\n", mx);
+      if (std::getenv("CPDGPU_SEED_TRACE_CTAS")) {  // per-CTA end (max over warps), tiles, first tile
+        for (int cta = 0; cta < c.sp.P; ++cta) {
+          unsigned long long e = 0;
+          for (int wp = 0; wp < 9; ++wp) e = std::max(e, h[(static_cast<size_t>(cta) * 9 + wp) * 8 + 6]);
+          const long long t0 = static_cast<long long>(cta) * c.sp.T / c.sp.P;
+          std::fprintf(stderr, "cta %d end %.0f tiles %llu t0 %lld rb0 %lld ct0 %lld\n", cta, static_cast<double>(e - g0),
+                       h[(static_cast<size_t>(cta) * 9) * 8 + 3], t0, t0 / c.sp.nCT, t0 % c.sp.nCT);
+        }
+      }
       std::fprintf(stderr, "[seed trace mode %d] ns from first CTA entry: last entry %.0f, pdl return w0 %.0f w8 %.0f, "
                    "end avg w0 %.0f w4 %.0f, last end %.0f\n", mode, entmax, pdl[0] / c.sp.P, pdl[8] / c.sp.P,
                    end[0] / c.sp.P, end[4] / c.sp.P, endmax);
