@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1204_1586_b200 as cpd
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-dims, R = {"c1": ([200] * 3, 10), "c2": ([60] * 4, 20), "c3": ([14] * 7, 10)}[cfg]
+dims, R = {"c1": ([200] * 3, 10), "c2": ([60] * 4, 20), "c3": ([14] * 7, 10), "c5": ([300] * 4, 64)}[cfg]
 ctx = cpd.Context(0)
 y = cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=1, ctx=ctx)
 f = [np.random.default_rng(k).normal(size=(d, R)) for k, d in enumerate(dims)]
