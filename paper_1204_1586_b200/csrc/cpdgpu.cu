@@ -260,6 +260,7 @@ struct Plan {
   CUtensorMap tmap{};         // bound to the tensor's device address
   const void* tmap_base = nullptr;
   DevBuf Fs, Forig, Gorig, Rpart, Lpart, Rs, Ls, Rtmp, Ltmp, grams, costs, status, norm;
+  DevBuf l0_scratch, l0_tickets;  // fused first level: chunk partials, self-resetting tickets
   DevBuf slot_tab;            // CSR of right-partial slots per row block: [nRB + 1] + [slots]
   int slot_tab_ptr_len = 0;
   int slot_tab_max = 0;         // most slots any row block has
@@ -1091,6 +1092,106 @@ void timeline_print(cpdgpu_ctx* ctx, const char* what) {
 
 // Whole hook-free gradient after the prologue: fused seeds, reductions, then
 // the right and left phases advancing together, one launch per level.
+// Fused first level (L0Side, kernels.h) for the sides whose level-0 step holds an
+// extraction and a recursion over the seed: the right side when p >= 2, the left
+// when p + 1 < N.  fp64, one rank chunk, per-row slot sums (not lane-parallel).
+// Returns the number of sides set up; the caller drops their reductions and
+// level-0 ops.  Disabled by CPDGPU_NO_L0.
+int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& fuse_l) {
+  static const bool disabled = std::getenv("CPDGPU_NO_L0") != nullptr;
+  fuse_r = fuse_l = false;
+  if (disabled || pl.f32 || pl.chunks.size() != 1 || pl.slot_tab_max >= 16) return 0;
+  const Plan::Chunk& c = pl.chunks[0];
+  const int R = static_cast<int>(pl.R);
+  fuse_r = pl.p >= 2 && pl.J[pl.p - 1] <= cpdgpu::kL0MaxRows;
+  fuse_l = pl.p + 1 < pl.N && pl.sd[pl.p] <= cpdgpu::kL0MaxRows;
+  const int nsides = (fuse_r ? 1 : 0) + (fuse_l ? 1 : 0);
+  if (nsides == 0) return 0;
+  const int target = std::max(1, (2 * ctx->num_sms + R * nsides - 1) / (R * nsides));
+  auto chunks = [&](cpdgpu::L0Side& sd) {
+    int64_t nq = std::min<int64_t>(target, sd.B);
+    int64_t bq = cpdgpu::ceil_div(sd.B, nq);
+    if (bq * sd.M > cpdgpu::kL0MaxRows) bq = std::max<int64_t>(1, cpdgpu::kL0MaxRows / sd.M);
+    sd.bq = static_cast<int>(bq);
+    sd.nq = static_cast<int>(cpdgpu::ceil_div(sd.B, bq));
+  };
+  l0 = cpdgpu::L0Step{};
+  l0.R = R;
+  size_t scratch = 0;
+  if (fuse_r) {  // right: opA extraction G(p), opB recursion R^(p-1) (G(1) when p == 2)
+    cpdgpu::L0Side& sd = l0.side[l0.nsides++];
+    const int j = pl.p;
+    sd.zsrc = 1;
+    sd.Z = pl.Rpart.d() + c.rpart_off;
+    sd.RP = c.NT * 8;
+    sd.TI = c.sp.TI;
+    sd.rb_ptr = static_cast<const int*>(pl.slot_tab.p);
+    sd.slot_list = static_cast<const int*>(pl.slot_tab.p) + pl.slot_tab_ptr_len;
+    sd.M = pl.J[j - 1];
+    sd.B = pl.sd[j - 1];
+    sd.krA = spec_over(pl, pl.Fs.d(), false, 1, j - 1, 0);
+    sd.krB = spec_over(pl, pl.Fs.d(), false, j, j, 0);
+    sd.outA = nullptr;
+    sd.slotA = pl.perm[j - 1] - 1;
+    sd.ldoA = pl.sd[j - 1];
+    if (j == 2) {
+      sd.outB = nullptr;
+      sd.slotB = pl.perm[0] - 1;
+      sd.ldoB = pl.sd[0];
+    } else {
+      sd.outB = pl.Rtmp.d();
+      sd.ldoB = pl.Jp;
+    }
+    chunks(sd);
+    scratch += static_cast<size_t>(R) * sd.nq * sd.M;
+  }
+  if (fuse_l) {  // left: opA recursion L^(p+2) (G(N) when p + 2 == N), opB extraction G(p+1)
+    cpdgpu::L0Side& sd = l0.side[l0.nsides++];
+    const int j = pl.p + 1;
+    if (pl.lpart_direct) {
+      sd.zsrc = 0;
+      sd.Z = pl.Ls.d();
+      sd.ldz = pl.Kp;
+    } else {
+      sd.zsrc = 2;
+      sd.Z = pl.Lpart.d() + c.lpart_off;
+      sd.pcount = static_cast<int>(c.sp.nRB);
+      sd.pK = pl.Kp;
+      sd.ldz = static_cast<int64_t>(R) * pl.Kp;
+    }
+    sd.M = pl.sd[j - 1];
+    sd.B = pl.K(j);
+    sd.krA = spec_over(pl, pl.Fs.d(), false, j, j, 0);
+    sd.krB = spec_over(pl, pl.Fs.d(), false, j + 1, pl.N, 0);
+    if (j + 1 == pl.N) {
+      sd.outA = nullptr;
+      sd.slotA = pl.perm[pl.N - 1] - 1;
+      sd.ldoA = pl.sd[pl.N - 1];
+    } else {
+      sd.outA = pl.Ltmp.d();
+      sd.ldoA = pl.Kp;
+    }
+    sd.outB = nullptr;
+    sd.slotB = pl.perm[j - 1] - 1;
+    sd.ldoB = pl.sd[j - 1];
+    chunks(sd);
+    scratch += static_cast<size_t>(R) * sd.nq * sd.M;
+  }
+  if (pl.l0_scratch.bytes < scratch * sizeof(double)) pl.l0_scratch.ensure(scratch * sizeof(double));
+  if (pl.l0_tickets.bytes < 2 * static_cast<size_t>(R) * sizeof(unsigned)) {
+    pl.l0_tickets.ensure(2 * static_cast<size_t>(R) * sizeof(unsigned));
+    CK(cudaMemset(pl.l0_tickets.p, 0, pl.l0_tickets.bytes));
+  }
+  size_t off = 0;
+  for (int i = 0; i < l0.nsides; ++i) {
+    cpdgpu::L0Side& sd = l0.side[i];
+    sd.scratch = pl.l0_scratch.d() + off;
+    off += static_cast<size_t>(R) * sd.nq * sd.M;
+    sd.tickets = static_cast<unsigned*>(pl.l0_tickets.p) + i * R;
+  }
+  return l0.nsides;
+}
+
 void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
   const bool left = pl.p + 1 <= pl.N;
   run_seeds(ctx, pl, left ? 3 : 1);
@@ -1102,7 +1203,23 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
   if (g1_direct) redirect_to_gradient(pl, st, /*right=*/true);
   const bool gN_direct = left && pl.p + 1 == pl.N && !pl.lpart_direct;  // the left seed is L^(N)
   if (gN_direct) redirect_to_gradient(pl, st, /*right=*/false);
+  cpdgpu::L0Step l0{};
+  bool fuse_r = false, fuse_l = false;
+  const int nl0 = build_l0(ctx, pl, l0, fuse_r, fuse_l);
+  if (nl0 > 0) {  // the fused sides' reductions go; the rest of the step stays
+    cpdgpu::TailStep keep{};
+    for (int i = 0; i < st.n; ++i) {
+      const bool right = st.op[i].type == cpdgpu::kOpReduceRight;
+      if (!(right ? fuse_r : fuse_l)) keep.op[keep.n++] = st.op[i];
+    }
+    st = keep;
+  }
   launch_step(ctx, pl, st);
+  if (nl0 > 0) {
+    l0.tl = ctx->tl_ptr();
+    if (l0.tl) l0.tl_slot = ctx->tl_slot();
+    ctx->launches += cpdgpu::launch_l0_step(l0, static_cast<double* const*>(pl.gtab.p), ctx->stream);
+  }
   double* rc = pl.Rs.d();
   double* rn = pl.Rtmp.d();
   double* lc = pl.Ls.d();
@@ -1112,7 +1229,9 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
     cpdgpu::TailStep s{};
     const int jr = pl.p - lv;      // right phase mode at this level
     const int jl = pl.p + 1 + lv;  // left phase mode at this level
-    if (jr >= 2) {
+    if (jr >= 2 && lv == 0 && fuse_r) {
+      // done by the fused first level (R^(p-1) in Rtmp, or G(1))
+    } else if (jr >= 2) {
       add_right_extract(pl, s, jr, rc);
       add_right_recurse(pl, s, jr, rc, rn);
       if (jr == 2) {  // R^(1) is G(1)
@@ -1126,7 +1245,9 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
     } else if (jr == 1 && !g1_direct) {
       add_right_extract(pl, s, jr, rc);
     }
-    if (jl <= pl.N) {
+    if (jl <= pl.N && lv == 0 && fuse_l) {
+      // done by the fused first level (L^(p+2) in Ltmp, or G(N))
+    } else if (jl <= pl.N) {
       if (jl < pl.N) {
         add_left_extract(pl, s, jl, lc);
         add_left_recurse(pl, s, jl, lc, ln);

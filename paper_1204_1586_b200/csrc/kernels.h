@@ -126,6 +126,46 @@ struct TailStep {
   unsigned long long* tl = nullptr;  // launch timeline (CPDGPU_TIMELINE)
   int tl_slot = 0;
 };
+// First recursion level fused with the seed-partial reduction.  A side pairs
+// the two contractions of one seed Z (rows a + M b, a < M, b < B):
+//   opA: outA[r][b] = sum_a Z[a + M b, r] KR_A[a, r]   (complete per b)
+//   opB: outB[r][a] = sum_b Z[a + M b, r] KR_B[b, r]   (partial per b-chunk)
+// One CTA per (side, r, chunk of b): it sums its rows of Z from the partials
+// (zsrc as TailOp) into shared memory, writes opA's outputs and its opB partial;
+// the last CTA of (side, r) to finish (ticket counter) adds the chunk partials in
+// chunk order.  Right side: opA = extraction G(p), opB = recursion R^(p-1);
+// left side: opA = recursion L^(p+2), opB = extraction G(p+1).
+struct L0Side {
+  int zsrc;  // 0 direct (Z[r ldz + idx]), 1 right slots, 2 left row blocks (ldz = R pK)
+  const double* Z;
+  int64_t ldz;
+  int RP, TI;
+  const int* rb_ptr;
+  const int* slot_list;
+  int pcount;
+  int64_t pK;
+  int64_t M, B;
+  int nq, bq;  // b-chunks and b per chunk
+  KRSpec krA, krB;
+  double* outA;  // nullptr: gtab[slotA] + 0 (ld ldoA)
+  int slotA;
+  int64_t ldoA;
+  double* outB;
+  int slotB;
+  int64_t ldoB;
+  double* scratch;    // [R][nq][M]
+  unsigned* tickets;  // [R], zero between calls
+};
+struct L0Step {
+  int nsides, R;
+  L0Side side[2];
+  unsigned long long* tl = nullptr;
+  int tl_slot = 0;
+};
+constexpr int kL0Threads = 256;
+constexpr int64_t kL0MaxRows = 6144;  // Z rows per CTA staged in shared memory (48 KB)
+int launch_l0_step(const L0Step& st, double* const* gtab, cudaStream_t s);
+
 int64_t tail_step_units(const TailStep& st);
 int launch_tail_step(const TailStep& st, double* const* gtab, int num_sms, cudaStream_t s);
 

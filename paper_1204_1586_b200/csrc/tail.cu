@@ -242,6 +242,160 @@ __global__ void __launch_bounds__(256) prologue_kernel(const Prologue pr, double
   tl_end(pr.tl, 0);
 }
 
+// ---- first level fused with the seed reduction (see L0Side in kernels.h) ----------
+__global__ void __launch_bounds__(kL0Threads) l0_kernel(const L0Step st, double* const* gtab) {
+  tl_begin(st.tl, st.tl_slot);
+  pdl_wait();
+  tl_mid(st.tl, st.tl_slot);
+  pdl_trigger();
+  extern __shared__ double zs[];  // [bq][M]
+  __shared__ unsigned last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // block -> (side, r, chunk)
+  int bid = blockIdx.x, si = 0;
+  const int n0 = st.side[0].nq * st.R;
+  if (st.nsides > 1 && bid >= n0) {
+    si = 1;
+    bid -= n0;
+  }
+  const L0Side& sd = st.side[si];
+  const int r = bid / sd.nq, qc = bid - r * sd.nq;
+  const int64_t b0 = static_cast<int64_t>(qc) * sd.bq;
+  const int64_t b1 = min(sd.B, b0 + sd.bq);
+  const int64_t M = sd.M, rows = (b1 - b0) * M;
+  // 1. this chunk's rows of Z (contiguous: idx = a + M b) into shared memory;
+  //    two rows per thread and step, each summed from batches of eight
+  //    partial loads issued together (order of the reduction ops kept)
+  const int64_t base = b0 * M;
+  for (int64_t e0 = tid; e0 < rows; e0 += 2 * kL0Threads) {
+    const int64_t e1 = e0 + kL0Threads;
+    const bool has1 = e1 < rows;
+    if (sd.zsrc == 0) {
+      zs[e0] = sd.Z[r * sd.ldz + base + e0];
+      if (has1) zs[e1] = sd.Z[r * sd.ldz + base + e1];
+    } else if (sd.zsrc == 1) {
+      double sum[2] = {0.0, 0.0};
+      int q0[2], q1[2];
+      int64_t il[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int64_t idx = base + (k ? (has1 ? e1 : e0) : e0);
+        const uint32_t rb = static_cast<uint32_t>(idx) / static_cast<uint32_t>(sd.TI);
+        il[k] = idx - static_cast<int64_t>(rb) * sd.TI;
+        q0[k] = sd.rb_ptr[rb];
+        q1[k] = sd.rb_ptr[rb + 1];
+      }
+      for (int qq = 0;; qq += 8) {
+        bool more = false;
+        double v[2][8];
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int q = q0[k] + qq + u;
+            v[k][u] = q < q1[k] ? sd.Z[(static_cast<int64_t>(sd.slot_list[q]) * sd.RP + r) * sd.TI + il[k]] : 0.0;
+          }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (q0[k] + qq + u < q1[k]) sum[k] += v[k][u];
+          more = more || q0[k] + qq + 8 < q1[k];
+        }
+        if (!more) break;
+      }
+      zs[e0] = sum[0];
+      if (has1) zs[e1] = sum[1];
+    } else {
+      double sum[2] = {0.0, 0.0};
+      const double* z0 = sd.Z + r * sd.pK + base + e0;
+      const double* z1 = sd.Z + r * sd.pK + base + (has1 ? e1 : e0);
+      for (int rb0 = 0; rb0 < sd.pcount; rb0 += 8) {
+        double v0[8], v1[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool ok = rb0 + u < sd.pcount;
+          v0[u] = ok ? z0[static_cast<int64_t>(rb0 + u) * sd.ldz] : 0.0;
+          v1[u] = ok ? z1[static_cast<int64_t>(rb0 + u) * sd.ldz] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (rb0 + u < sd.pcount) {
+            sum[0] += v0[u];
+            sum[1] += v1[u];
+          }
+      }
+      zs[e0] = sum[0];
+      if (has1) zs[e1] = sum[1];
+    }
+  }
+  // Khatri-Rao values of this (r, chunk): KR_A[a, r] for every a, KR_B[b, r] for the chunk's b
+  double* kra = zs + rows;
+  double* krb = kra + M;
+  double* gp = krb + (b1 - b0);  // group partials of opB [groups][M]
+  for (int64_t x = tid; x < M; x += kL0Threads) kra[x] = kr_at(sd.krA, x, r);
+  for (int64_t x = tid; x < b1 - b0; x += kL0Threads) krb[x] = kr_at(sd.krB, b0 + x, r);
+  __syncthreads();
+  // 2. opA, complete for b in [b0, b1): warp per b
+  double* outA = sd.outA ? sd.outA : gtab[sd.slotA];
+  for (int64_t b = b0 + warp; b < b1; b += kL0Threads / 32) {
+    const double* z = zs + (b - b0) * M;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t a = lane;
+    for (; a + 32 < M; a += 64) {
+      s0 += z[a] * kra[a];
+      s1 += z[a + 32] * kra[a + 32];
+    }
+    for (; a < M; a += 32) s0 += z[a] * kra[a];
+    const double v = warp_sum(s0 + s1);
+    if (lane == 0) outA[r * sd.ldoA + b] = v;
+  }
+  // 3. opB partial over this chunk's b: thread per a, or G groups of threads
+  //    splitting the b's when M is small (group sums added in group order)
+  double* part = sd.scratch + (static_cast<int64_t>(r) * sd.nq + qc) * M;
+  const int64_t nb = b1 - b0;
+  const int64_t gmax = kL0Threads / M;
+  const int G = M >= kL0Threads ? 1 : static_cast<int>(gmax < nb ? gmax : nb);
+  if (G == 1) {
+    for (int64_t a = tid; a < M; a += kL0Threads) {
+      double s = 0.0;
+      for (int64_t b = 0; b < nb; ++b) s += zs[b * M + a] * krb[b];
+      part[a] = s;
+    }
+  } else {
+    const int g = tid / static_cast<int>(M);
+    const int64_t a = tid - static_cast<int64_t>(g) * M;
+    if (g < G) {
+      double s = 0.0;
+      for (int64_t b = g; b < nb; b += G) s += zs[b * M + a] * krb[b];
+      gp[g * M + a] = s;
+    }
+    __syncthreads();
+    if (tid < M) {
+      double s = 0.0;
+      for (int q = 0; q < G; ++q) s += gp[q * M + tid];
+      part[tid] = s;
+    }
+  }
+  // 4. the last chunk CTA of (side, r) adds the partials in chunk order
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(sd.tickets + r, 1u) == static_cast<unsigned>(sd.nq - 1);
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double* outB = sd.outB ? sd.outB : gtab[sd.slotB];
+    const double* p0 = sd.scratch + static_cast<int64_t>(r) * sd.nq * M;
+    for (int64_t a = tid; a < M; a += kL0Threads) {
+      double s = 0.0;
+      for (int q = 0; q < sd.nq; ++q) s += __ldcg(p0 + static_cast<int64_t>(q) * M + a);
+      outB[r * sd.ldoB + a] = s;
+    }
+    if (tid == 0) sd.tickets[r] = 0u;  // ready for the next replay
+  }
+  tl_end(st.tl, st.tl_slot);
+}
+
 int grid_for(int64_t work, int threads, int cap) {
   const int64_t b = (work + threads - 1) / threads;
   return static_cast<int>(b < 1 ? 1 : (b > cap ? cap : b));
@@ -298,6 +452,26 @@ void prologue_geometry(const Prologue& pr, int num_sms, dim3* grid, dim3* block)
   for (int c = 0; c < pr.nkr; ++c) work = work > pr.kr[c].L * pr.kr[c].LDK ? work : pr.kr[c].L * pr.kr[c].LDK;
   *grid = dim3(static_cast<unsigned>(grid_for(work, 256, num_sms * 8)));
   *block = dim3(256);
+}
+
+int launch_l0_step(const L0Step& st, double* const* gtab, cudaStream_t s) {
+  int blocks = 0;
+  int64_t rows = 0;
+  for (int i = 0; i < st.nsides; ++i) {
+    blocks += st.side[i].nq * st.R;
+    rows = std::max<int64_t>(rows, static_cast<int64_t>(st.side[i].bq) * st.side[i].M);
+  }
+  int64_t extra = 0;  // KR values and opB group partials
+  for (int i = 0; i < st.nsides; ++i) extra = std::max<int64_t>(extra, st.side[i].M + st.side[i].bq + kL0Threads);
+  const size_t smem = static_cast<size_t>(rows + extra) * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(l0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>((3 * kL0MaxRows + kL0Threads) * sizeof(double)));
+    configured = true;
+  }
+  launch_k(l0_kernel, dim3(blocks), dim3(kL0Threads), smem, s, pdl_enabled(), st, gtab);
+  return 1;
 }
 
 int launch_prologue(const Prologue& pr, double** gtab, int num_sms, cudaStream_t s) {
