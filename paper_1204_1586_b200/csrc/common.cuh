@@ -97,51 +97,6 @@ __device__ __forceinline__ double kr_entry32(const KRSpec& s, uint32_t q, int r)
   return prod;
 }
 
-// Whole Khatri-Rao row q (all RP rank columns, zero beyond R) into dst[0..RP):
-// eight rank columns at a time (independent products per mode for ILP, small
-// register footprint); the mixed-radix digits are recomputed per chunk.
-// fsm != nullptr: the factors were staged back to back (I_k x R each) in shared
-// memory at fsm, read with plain loads; otherwise s.A[k] via the read-only path.
-template <int RP>
-__device__ __forceinline__ void kr_row(const KRSpec& s, int64_t q, int R, bool use32, double* dst,
-                                       const double* fsm = nullptr) {
-#pragma unroll 1
-  for (int r0 = 0; r0 < RP; r0 += 8) {
-    double acc[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) acc[r] = r0 + r < R ? 1.0 : 0.0;
-    uint32_t q32 = static_cast<uint32_t>(q);
-    int64_t q64 = q;
-    const double* f = fsm;
-#pragma unroll 1
-    for (int k = 0; k < s.n; ++k) {
-      const int64_t I = s.dims[k];
-      int64_t d;
-      if (use32) {
-        const uint32_t I32 = static_cast<uint32_t>(I);
-        d = q32 % I32;
-        q32 /= I32;
-      } else {
-        d = q64 % I;
-        q64 /= I;
-      }
-      if (fsm) {
-        const double* a = f + d + I * r0;
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (r0 + r < R) acc[r] *= a[I * r];
-        f += I * R;
-      } else {
-        const double* a = s.A[k] + d + I * r0;
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (r0 + r < R) acc[r] *= __ldg(a + I * r);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) dst[r0 + r] = acc[r];
-  }
-}
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -478,9 +478,6 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
                          cpdgpu::seed_f64_smem_bytes(c.NT, TI, ldy, lk, 2, 3, 0)) <= cpdgpu::kSeedSmemLimit
                     ? 3 : 2;
     if (const char* e = std::getenv("CPDGPU_SEED_STAGES")) sp.stages = std::atoi(e);
-    if (const char* e = std::getenv("CPDGPU_SEED_DEBUG")) sp.debug = std::atoi(e);
-    sp.prefetch = 4;
-    if (const char* e = std::getenv("CPDGPU_SEED_PREFETCH")) sp.prefetch = std::atoi(e);
     c.KRr = std::make_unique<DevBuf>();
     c.KRl = std::make_unique<DevBuf>();
     c.KRr->ensure(static_cast<size_t>(Kp) * lk * sizeof(double));

@@ -23,8 +23,6 @@ struct SeedParams {
   int use32;        // all KR row indices fit in 32 bits
   int use_tma;      // Y tiles arrive by 2-D TMA (dense LDY == TI); else plain copies
   int stages;       // pipeline depth (2 or 3)
-  int prefetch;     // Y tiles prefetched into L2 beyond the ring (CPDGPU_SEED_PREFETCH)
-  int debug;        // experiment knobs (CPDGPU_SEED_DEBUG): bit 0 skips KR generation
   KRSpec left;      // modes 1..p   (rows of the view)
   KRSpec right;     // modes p+1..N (columns of the view)
   const double* KRl_g;  // Khatri-Rao rows of the view's rows    [J][LDK] (kr_materialize)
@@ -39,7 +37,6 @@ struct SeedParams {
 // tiles: == 4 mod 8, so the DMMA fragment loads (lane (g, t) reads row t,
 // column g) of a half-warp hit 16 distinct 8-byte banks.
 __host__ __device__ constexpr int seed_ldk(int NT) { return NT * 8 + 4; }
-int seed_f64_stages(int NT);  // default depth before the factor-staging choice
 // largest row block the fused kernel can hold in registers for this NT
 int seed_f64_max_ti(int NT);
 size_t seed_f64_smem_bytes(int NT, int TI, int LDY, int LDK, int mode, int stages, int64_t fac_doubles);

@@ -683,8 +683,6 @@ void launch_nt(const SeedParams& p, const CUtensorMap& tmap, const CUtensorMap& 
 
 }  // namespace
 
-int seed_f64_stages(int NT) { return NT <= 3 ? 3 : 2; }
-
 int seed_f64_max_ti(int NT) { return NT <= 2 ? 208 : (NT == 3 ? 192 : 160); }
 
 size_t seed_f64_smem_bytes(int NT, int TI, int LDY, int LDK, int mode, int stages, int64_t fac_doubles) {
