@@ -21,6 +21,7 @@ namespace cpdgpu {
 namespace {
 
 constexpr int kAlsThreads = 256;
+constexpr int64_t kAlsStage = 4096;  // I x R doubles of G (and of A) staged in shared memory
 
 __global__ void gram_kernel(const double* __restrict__ A, int64_t I, int R,
                             double* __restrict__ gram) {
@@ -131,13 +132,17 @@ __device__ void pinv_from_eig(const double* M, const double* V, double* inv, int
   __syncthreads();
 }
 
-// Fast path of pinv_psd for a certified well-conditioned PD matrix: Cholesky
-// W = L L^T, X = W^{-1} by two triangular solves per column.  Accepted only when
-// the factorization succeeded and lambda_min >= 1 / ||X||_inf exceeds
+// Fast path of pinv_psd for a certified well-conditioned PD matrix: X = W^{-1}
+// by Gauss-Jordan elimination without pivoting (stable for symmetric positive
+// definite W, the pivots are its Schur complements), all R x R entries updated
+// in parallel per pivot step (R steps; the former Cholesky + per-column
+// triangular solves ran R^2 dependent steps on R threads).  Accepted only when
+// every pivot was positive and lambda_min >= 1 / ||X||_inf exceeds
 // 10 rtol ||W||_inf >= 10 rtol lambda_max: then no eigenvalue reaches the
 // pinv_psd cutoff and the pseudo-inverse IS the inverse.  Otherwise the caller
-// runs the Jacobi eigensolver.  L and X use the M2 / V2 scratch (ld Rp).
-__device__ bool chol_inverse(const double* W, double* L, double* X, int R, int Rp, double rtol, double* P) {
+// runs the Jacobi eigensolver.  X and its ping-pong partner use the M2 / V2
+// scratch (ld Rp).
+__device__ bool chol_inverse(const double* W, double* X, double* X2, int R, int Rp, double rtol, double* P) {
   const int tid = threadIdx.x, nt = blockDim.x;
   __shared__ int s_fail;
   __shared__ double s_wn, s_xn;
@@ -146,41 +151,42 @@ __device__ bool chol_inverse(const double* W, double* L, double* X, int R, int R
     s_wn = 0.0;
     s_xn = 0.0;
   }
+  for (int e = tid; e < Rp * Rp; e += nt) X[e] = W[e];
   __syncthreads();
+  double* cur = X;
+  double* nxt = X2;
   for (int k = 0; k < R; ++k) {
-    if (tid == 0) {
-      double d = W[k + Rp * k];
-      for (int j = 0; j < k; ++j) d -= L[k + Rp * j] * L[k + Rp * j];
-      if (!(d > 0.0)) s_fail = 1;
-      L[k + Rp * k] = d > 0.0 ? sqrt(d) : 1.0;
+    const double piv = cur[k + Rp * k];
+    if (!(piv > 0.0)) {  // uniform: every thread reads the same pivot
+      if (tid == 0) s_fail = 1;
+      break;
+    }
+    const double ip = 1.0 / piv;
+    for (int e = tid; e < R * R; e += nt) {
+      const int i = e % R, j = e / R;
+      double v;
+      if (i == k && j == k)
+        v = ip;
+      else if (i == k)
+        v = cur[k + Rp * j] * ip;
+      else if (j == k)
+        v = -cur[i + Rp * k] * ip;
+      else
+        v = cur[i + Rp * j] - cur[i + Rp * k] * cur[k + Rp * j] * ip;
+      nxt[i + Rp * j] = v;
     }
     __syncthreads();
-    for (int i = k + 1 + tid; i < R; i += nt) {
-      double v = W[i + Rp * k];
-      for (int j = 0; j < k; ++j) v -= L[i + Rp * j] * L[k + Rp * j];
-      L[i + Rp * k] = v / L[k + Rp * k];
-    }
-    __syncthreads();
-  }
-  if (s_fail) return false;
-  for (int c = tid; c < R; c += nt) {  // column c of W^{-1}: L y = e_c, L^T x = y
-    for (int i = 0; i < R; ++i) {
-      double v = (i == c) ? 1.0 : 0.0;
-      for (int j = 0; j < i; ++j) v -= L[i + Rp * j] * X[j + Rp * c];
-      X[i + Rp * c] = v / L[i + Rp * i];
-    }
-    for (int i = R - 1; i >= 0; --i) {
-      double v = X[i + Rp * c];
-      for (int j = i + 1; j < R; ++j) v -= L[j + Rp * i] * X[j + Rp * c];
-      X[i + Rp * c] = v / L[i + Rp * i];
-    }
+    double* t = cur;
+    cur = nxt;
+    nxt = t;
   }
   __syncthreads();
+  if (s_fail) return false;
   for (int a = tid; a < R; a += nt) {  // infinity norms (row sums)
     double w = 0.0, x = 0.0;
     for (int c = 0; c < R; ++c) {
       w += fabs(W[a + Rp * c]);
-      x += fabs(X[a + Rp * c]);
+      x += fabs(cur[a + Rp * c]);
     }
     atomicMax(reinterpret_cast<unsigned long long*>(&s_wn), __double_as_longlong(w));
     atomicMax(reinterpret_cast<unsigned long long*>(&s_xn), __double_as_longlong(x));
@@ -190,12 +196,11 @@ __device__ bool chol_inverse(const double* W, double* L, double* X, int R, int R
   if (ok)
     for (int e = tid; e < R * R; e += nt) {
       const int a = e % R, c = e / R;
-      P[a + R * c] = 0.5 * (X[a + Rp * c] + X[c + Rp * a]);
+      P[a + R * c] = 0.5 * (cur[a + Rp * c] + cur[c + Rp * a]);
     }
   __syncthreads();
   return ok;
 }
-
 struct EigSmem {
   double *M, *M2, *V, *V2, *cs, *inv, *P;
   int* partner;
@@ -252,7 +257,32 @@ __global__ void __launch_bounds__(kAlsThreads, 1)
     jacobi_eig(s.M, s.M2, s.V, s.V2, s.cs, s.partner, Rp);
     pinv_from_eig(s.M, s.V, s.inv, R, Rp, rtol, s.P);
   }
-  // A_n = G * P  (als.cpp:55)
+  // A_n = G * P  (als.cpp:55); G staged in shared memory (after the eigen scratch)
+  // when it fits, so the products and the new Gram read shared memory
+  double* gs = s.partner ? reinterpret_cast<double*>(s.partner + Rp) : nullptr;
+  gs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(gs) + 15) & ~static_cast<uintptr_t>(15));
+  const bool staged = I * R <= kAlsStage;
+  if (staged) {
+    double* as = gs + I * R;
+    for (int64_t e = tid; e < I * R; e += nt) gs[e] = G[e];
+    __syncthreads();
+    for (int64_t e = tid; e < I * R; e += nt) {
+      const int64_t i = e % I;
+      const int c = static_cast<int>(e / I);
+      double acc = 0.0;
+      for (int k = 0; k < R; ++k) acc += gs[i + I * k] * s.P[k + R * c];
+      as[e] = acc;
+      A[e] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < R * R; e += nt) {
+      const int a = e % R, c = e / R;
+      double acc = 0.0;
+      for (int64_t i = 0; i < I; ++i) acc += as[i + I * a] * as[i + I * c];
+      gram_n[e] = acc;
+    }
+    return;
+  }
   for (int64_t e = tid; e < I * R; e += nt) {
     const int64_t i = e % I;
     const int c = static_cast<int>(e / I);
@@ -407,7 +437,7 @@ int launch_gram(const double* A, int64_t I, int R, double* gram, cudaStream_t s)
 
 int launch_als_update(const double* G, int64_t I, int R, const double* grams, int N, int n,
                        double rtol, double* A, double* gram_n, int* status, cudaStream_t s) {
-  const size_t bytes = eig_smem_bytes(R);
+  const size_t bytes = eig_smem_bytes(R) + 16 + (I * R <= kAlsStage ? 2 * static_cast<size_t>(I) * R * sizeof(double) : 0);
   set_smem(reinterpret_cast<const void*>(als_update_kernel), bytes);
   als_update_kernel<<<1, kAlsThreads, bytes, s>>>(G, I, R, grams, N, n, rtol, A, gram_n, status);
   return 1;
