@@ -69,6 +69,9 @@ uint64_t cpdgpu_launch_count(const cpdgpu_ctx* ctx);
  * of the most recent gradient / sweep call (synchronises on the last event). */
 int cpdgpu_set_timing(cpdgpu_ctx* ctx, int enabled);
 int cpdgpu_last_seed_ms(cpdgpu_ctx* ctx, double* ms);
+/* Seed path of the most recent hook-free fp64 gradient: 0 = fp64 DMMA pass,
+ * 1 = fused pass on the int8 tensor cores (opt-in: CPDGPU_I8=1), 2 = fp32. */
+int cpdgpu_last_seed_path(const cpdgpu_ctx* ctx);
 
 /* ---- tensors (DenseTensor, dense_tensor.hpp:15-47) -------------------------
  * A tensor is immutable once created, as the reference's is; the context may

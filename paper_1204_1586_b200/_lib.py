@@ -32,6 +32,7 @@ SIGNATURES = {
     "cpdgpu_launch_count": (c_u64, [C.c_void_p]),
     "cpdgpu_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "cpdgpu_last_seed_ms": (C.c_int, [C.c_void_p, c_dbl_p]),
+    "cpdgpu_last_seed_path": (C.c_int, [C.c_void_p]),
     "cpdgpu_tensor_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "cpdgpu_tensor_upload": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(c_i64), C.POINTER(C.c_void_p)]),
     "cpdgpu_tensor_wrap_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(c_i64), C.POINTER(C.c_void_p)]),

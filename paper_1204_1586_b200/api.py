@@ -85,6 +85,10 @@ class Context:
     def set_timing(self, enabled: bool) -> None:
         _lib.check(self._L.cpdgpu_set_timing(self.h, int(bool(enabled))), self.h)
 
+    def last_seed_path(self) -> int:
+        """0: fp64 DMMA seed pass, 1: fused int8 tensor-core pass, 2: fp32 pass."""
+        return int(self._L.cpdgpu_last_seed_path(self.h))
+
     def last_seed_ms(self) -> float:
         v = C.c_double()
         _lib.check(self._L.cpdgpu_last_seed_ms(self.h, C.byref(v)), self.h)

@@ -218,6 +218,9 @@ struct cpdgpu_tensor {
   uint64_t version = 0;              // bumped whenever the values change
   DevBuf yscale;                     // fp32: [float scale | double inv | uint amax] (seed_f32.cu)
   uint64_t scale_version = ~0ull;
+  DevBuf yscale8;                    // fp64: int8 seed scale record [2^(46-eY), eY, max|Y|] + scratch
+  uint64_t scale8_version = ~0ull;
+  double amax8 = -1.0, amean8 = 0.0;
   size_t elem() const { return dtype == CPDGPU_F64 ? 8 : 4; }
   ~cpdgpu_tensor() {
     if (sorted && sorted != data) cudaFree(sorted);
@@ -264,6 +267,24 @@ struct Plan {
   DevBuf slot_tab;            // CSR of right-partial slots per row block: [nRB + 1] + [slots]
   int slot_tab_ptr_len = 0;
   int slot_tab_max = 0;         // most slots any row block has
+  // fp64 fused gradient on the int8 tensor cores (seed_i8.cu): its own 128 x 128
+  // tile geometry; gradient_body swaps it in for the seed partials' consumers.
+  struct I8 {
+    bool ok = false;   // geometry built (one rank chunk, both seeds, even J_p)
+    bool on = false;   // bound tensor passed the range guard and has a TMA view
+    int N = 0;         // MMA rank block (16 or 32)
+    int64_t nRB = 0, nCT = 0, T = 0;
+    int P = 0, slots = 0;
+    DevBuf img_r, img_l, w_r, w_l;
+    CUtensorMap ymap{};
+    const void* ymap_base = nullptr;
+    // swapped with the fp64 geometry while an int8 gradient is recorded
+    int TI_s = 128;
+    int64_t nRB_s = 0;
+    DevBuf tab;
+    int tab_len = 0, tab_max = 0;
+    bool lpart_direct = false;
+  } i8;
   HostBuf hF, hG;
   // fp32 tensors: tcgen05 seed passes (seed_f32.cu), one per side
   bool f32 = false;
@@ -316,6 +337,7 @@ struct cpdgpu_ctx {
   std::string err;
   bool graphs = true;
   uint64_t launches = 0;
+  int last_seed_path = 0;  // cpdgpu_last_seed_path
   uint64_t next_id = 1;
   std::map<std::tuple<uint64_t, int64_t, int>, std::unique_ptr<Plan>> plans;
   DevBuf scratch;
@@ -518,6 +540,34 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
     }
   }
   if (!pl.lpart_direct) pl.Lpart.ensure(lpart * sizeof(double));
+  // int8 fused seed: one rank chunk of <= 32 columns, both seeds, Y rows 16-byte
+  // aligned for the 2-D TMA view
+  pl.i8.ok = false;
+  const char* i8env = std::getenv("CPDGPU_I8");  // "1": fused fp64 seed on the int8 tensor cores
+  if (i8env && i8env[0] == '1' && pl.chunks.size() == 1 && pl.p + 1 <= pl.N && Jp % 2 == 0 &&
+      Jp < (1LL << 31) && Kp < (1LL << 31)) {
+    Plan::I8& g = pl.i8;
+    const Plan::Chunk& c = pl.chunks[0];
+    g.N = c.Rc <= 16 ? 16 : 32;
+    g.nRB = cpdgpu::ceil_div(Jp, 128);
+    g.nCT = cpdgpu::ceil_div(Kp, 128);
+    g.T = g.nRB * g.nCT;
+    g.P = static_cast<int>(std::min<int64_t>(ctx->num_sms, g.T));
+    g.slots = static_cast<int>(cpdgpu::ceil_div(cpdgpu::ceil_div(g.T, g.P), g.nCT) + 1);
+    build_slot_tab(g.tab, g.nRB, g.nCT, g.T, g.P, g.slots, &g.tab_len, &g.tab_max);
+    g.TI_s = 128;
+    g.nRB_s = g.nRB;
+    g.lpart_direct = g.nRB == 1;
+    pl.Rpart.ensure(std::max(pl.Rpart.bytes, static_cast<size_t>(g.P) * g.slots * c.NT * 8 * 128 * sizeof(double)));
+    if (!g.lpart_direct)
+      pl.Lpart.ensure(std::max(pl.Lpart.bytes, static_cast<size_t>(g.nRB) * c.Rc * Kp * sizeof(double)));
+    const size_t img = static_cast<size_t>(6) * g.N * 128;
+    g.img_r.ensure(static_cast<size_t>(g.nCT) * img);
+    g.img_l.ensure(static_cast<size_t>(g.nRB) * img);
+    g.w_r.ensure(static_cast<size_t>(g.nCT) * g.N * sizeof(double));
+    g.w_l.ensure(static_cast<size_t>(g.nRB) * g.N * sizeof(double));
+    g.ok = true;
+  }
 }
 
 // fp32 tensors: one tcgen05 pass per seed, 64 rank columns per chunk.
@@ -664,6 +714,41 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
   }
 }
 
+// int8 fused seed: the tensor's scale record (cached per tensor version), the
+// range guard and the swizzled TMA view.  Digits are scaled to max |Y|, so the
+// path is kept to tensors whose largest entry is within 2^12 of their mean
+// magnitude (a wider range would cost the typical entries precision) and that
+// hold no Inf / NaN; everything else runs the fp64 DMMA pass.
+void bind_i8(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const void* ybase) {
+  if (t->scale8_version != t->version) {
+    t->yscale8.ensure(64);
+    double* rec = t->yscale8.d();
+    ctx->launches += cpdgpu::launch_y_scale_f64(static_cast<const double*>(ybase), t->numel, rec + 4, rec,
+                                                ctx->num_sms, ctx->stream);
+    double h[4] = {0, 0, 0, 0};
+    CK(cudaMemcpyAsync(h, rec, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    t->amax8 = h[2];
+    t->amean8 = t->numel > 0 ? h[3] / static_cast<double>(t->numel) : 0.0;
+    t->scale8_version = t->version;
+  }
+  bool on = std::isfinite(t->amax8) && (t->amax8 == 0.0 || t->amax8 <= 4096.0 * t->amean8);
+  if (on && pl.i8.ymap_base != ybase) {
+    on = cpdgpu::make_tensor_map_2d(&pl.i8.ymap, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                                    static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
+                                    static_cast<uint64_t>(pl.Jp) * 8, 16, 16, true, false);
+    pl.i8.ymap_base = on ? ybase : nullptr;
+  }
+  if (on != pl.i8.on && pl.grad_exec) {  // the recorded gradient used the other seed path
+    cudaGraphExecDestroy(pl.grad_exec);
+    cudaGraphDestroy(pl.grad_graph);
+    pl.grad_exec = nullptr;
+    pl.grad_graph = nullptr;
+    pl.grad_warm = false;
+  }
+  pl.i8.on = on;
+}
+
 void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
   if (pl.f32) {
     bind_f32_inputs(ctx, pl, t);
@@ -698,6 +783,7 @@ void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
     c.sp.Rpart = pl.Rpart.d() + c.rpart_off;
     c.sp.Lpart = pl.lpart_direct ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d() + c.lpart_off;
   }
+  if (pl.i8.ok) bind_i8(ctx, pl, t, ybase);
 }
 
 // ---- K1 launches ---------------------------------------------------------------
@@ -770,6 +856,89 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
   }
   CK(cudaGetLastError());
 }
+
+// Both fp64 seeds in one pass on the int8 tensor cores: Khatri-Rao digit images
+// of both sides (from the prologue's rows), then the fused pass.
+void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
+  cudaStream_t s = ctx->stream;
+  Plan::I8& g = pl.i8;
+  Plan::Chunk& c = pl.chunks[0];
+  const double* ys = pl.tensor->yscale8.d();
+  ctx->launches += cpdgpu::launch_kr_digits(c.KRr->d(), pl.Kp, c.sp.LDK, c.Rc, g.N, ys, g.img_r.p, g.w_r.d(), s);
+  ctx->launches += cpdgpu::launch_kr_digits(c.KRl->d(), pl.Jp, c.sp.LDK, c.Rc, g.N, ys, g.img_l.p, g.w_l.d(), s);
+  cpdgpu::SeedI8Params q{};
+  q.J = pl.Jp;
+  q.K = pl.Kp;
+  q.R = c.Rc;
+  q.RP = c.NT * 8;
+  q.N = g.N;
+  q.nRB = g.nRB;
+  q.nCT = g.nCT;
+  q.T = g.T;
+  q.P = g.P;
+  q.slots = g.slots;
+  q.img_r = static_cast<const unsigned char*>(g.img_r.p);
+  q.img_l = static_cast<const unsigned char*>(g.img_l.p);
+  q.w_r = g.w_r.d();
+  q.w_l = g.w_l.d();
+  q.yscale = ys;
+  q.Rpart = pl.Rpart.d() + c.rpart_off;
+  static const bool dbg = std::getenv("CPDGPU_I8_DEBUG") != nullptr;
+  static DevBuf progress;
+  if (dbg) {
+    progress.ensure(static_cast<size_t>(g.P) * 16 * sizeof(unsigned));
+    CK(cudaMemsetAsync(progress.p, 0, progress.bytes, s));
+  }
+  q.progress = dbg ? static_cast<unsigned*>(progress.p) : nullptr;
+  q.Lpart = g.nRB == 1 ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d() + c.lpart_off;
+  static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
+  DevBuf tb;
+  if (trace) {
+    tb.ensure(static_cast<size_t>(g.P) * 14 * 6 * 8);
+    CK(cudaMemsetAsync(tb.p, 0, tb.bytes, s));
+    q.trace = static_cast<unsigned long long*>(tb.p);
+  }
+  if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+  ctx->launches += cpdgpu::launch_seed_i8(q, &g.ymap, s);
+  if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+  if (trace) {
+    std::vector<unsigned long long> h(static_cast<size_t>(g.P) * 14 * 6);
+    CK(cudaMemcpyAsync(h.data(), tb.p, tb.bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double a[14][6] = {};
+    for (int c = 0; c < g.P; ++c)
+      for (int w = 0; w < 14; ++w)
+        for (int i = 0; i < 6; ++i) a[w][i] += static_cast<double>(h[(static_cast<size_t>(c) * 14 + w) * 6 + i]) / g.P;
+    std::fprintf(stderr, "[i8 trace] avg per CTA (%.1f tiles): split w0 raw_full %.0f dig_empty %.0f total %.0f | "
+                 "drain w8 accR %.0f accL %.0f total %.0f | mma dig_full %.0f rb_full %.0f accR_empty %.0f "
+                 "lb/accL %.0f total %.0f | producer total %.0f\n", a[0][5], a[0][0], a[0][1], a[0][4], a[8][0],
+                 a[8][1], a[8][4], a[13][0], a[13][1], a[13][2], a[13][3], a[13][4], a[12][4]);
+  }
+  CK(cudaGetLastError());
+}
+
+// While an int8 gradient is recorded, the seed partials' consumers (reductions,
+// fused first level) see the int8 geometry: row blocks of 128, its slot table.
+struct I8Geometry {
+  Plan& pl;
+  bool on;
+  explicit I8Geometry(Plan& p) : pl(p), on(p.i8.on) {
+    if (on) swap();
+  }
+  ~I8Geometry() {
+    if (on) swap();
+  }
+  void swap() {
+    Plan::Chunk& c = pl.chunks[0];
+    std::swap(c.sp.TI, pl.i8.TI_s);
+    std::swap(c.sp.nRB, pl.i8.nRB_s);
+    std::swap(pl.slot_tab.p, pl.i8.tab.p);
+    std::swap(pl.slot_tab.bytes, pl.i8.tab.bytes);
+    std::swap(pl.slot_tab_ptr_len, pl.i8.tab_len);
+    std::swap(pl.slot_tab_max, pl.i8.tab_max);
+    std::swap(pl.lpart_direct, pl.i8.lpart_direct);
+  }
+};
 
 void run_seeds(cpdgpu_ctx* ctx, Plan& pl, int mode) {
   if (pl.f32) {
@@ -1191,7 +1360,12 @@ int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& 
 
 void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
   const bool left = pl.p + 1 <= pl.N;
-  run_seeds(ctx, pl, left ? 3 : 1);
+  I8Geometry geometry(pl);
+  ctx->last_seed_path = pl.f32 ? 2 : (pl.i8.on ? 1 : 0);
+  if (pl.i8.on)
+    run_seeds_i8(ctx, pl);
+  else
+    run_seeds(ctx, pl, left ? 3 : 1);
   cpdgpu::TailStep st{};
   add_reduce_ops(pl, st, left ? 3 : 1);
   // The extractions G(1) = R^(1) and G(N) = L^(N) are copies (empty Khatri-Rao
@@ -1785,6 +1959,7 @@ int cpdgpu_set_graphs(cpdgpu_ctx* ctx, int enabled) {
 }
 
 uint64_t cpdgpu_launch_count(const cpdgpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int cpdgpu_last_seed_path(const cpdgpu_ctx* ctx) { return ctx ? ctx->last_seed_path : -1; }
 
 int cpdgpu_set_timing(cpdgpu_ctx* ctx, int enabled) {
   if (!ctx) return CPDGPU_ARGUMENT_ERROR;

@@ -59,6 +59,34 @@ int launch_seed_left_cols(const SeedParams& p, const CUtensorMap* ymap, const CU
                           cudaStream_t s);
 size_t seed_left_cols_smem_bytes(int NT, int TJ, int stages);
 
+// ---- K1 fp64 fused on the int8 tensor cores (seed_i8.cu) ---------------------
+// Both seeds in one pass over Y, 128 x 128 tiles, tile = rb * nCT + ct, CTA c owns
+// [c T / P, (c + 1) T / P).  Right partials: Rpart[(c * slots + rb - rb0)][RP][128];
+// left partials: Lpart[(rb * R + r) * K + j] (the fp64 path's formats, TI = 128).
+struct SeedI8Params {
+  int64_t J, K;          // J_p, K_p
+  int R, RP, N;          // rank columns, Rpart row stride (8 NT), MMA rank block (16 or 32)
+  int64_t nRB, nCT, T;   // 128-row blocks, 128-column tiles, nRB * nCT
+  int P, slots;
+  const unsigned char* img_r;  // [nCT][6][N][128] Khatri-Rao digits of the view's columns
+  const unsigned char* img_l;  // [nRB][6][N][128]                 ... of the view's rows
+  const double* w_r;           // [nCT][N] column weights 2^(eY + e_r - 52)
+  const double* w_l;           // [nRB][N]
+  const double* yscale;        // tensor scale record: [0] 2^(46 - eY), [1] eY, [2] max |Y|
+  double* Rpart;
+  double* Lpart;
+  unsigned* progress;  // CPDGPU_I8_DEBUG: [P][16] per-warp positions for the watchdog report
+  unsigned long long* trace;  // CPDGPU_SEED_TRACE: [P][14][6] per-warp wait cycles, total, tiles
+};
+size_t seed_i8_smem_bytes(int N);
+// ymap: Y (dim0 J, dim1 K) fp64, box 16 x 16, 128-byte swizzle
+int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s);
+// Khatri-Rao rows [L][ldk] -> digit images [ceil(L / 128)][6][N][128] + weights [.][N]
+int launch_kr_digits(const double* rows, int64_t L, int ldk, int R, int N, const double* yscale, void* img, double* w,
+                     cudaStream_t s);
+// fp64 tensor scale record [2^(46-eY), eY, max|Y|, sum|Y|]; scratch >= 16 bytes
+int launch_y_scale_f64(const double* y, int64_t n, void* scratch, double* out, int num_sms, cudaStream_t s);
+
 // ---- K1 for fp32 tensors: tcgen05 split-fp16 seed contraction (seed_f32.cu) ---
 // One pass computes ONE seed (right: blocks over the view's rows i, k-tiles over
 // columns j; left: blocks over columns j, k-tiles over rows i) for up to 64 rank

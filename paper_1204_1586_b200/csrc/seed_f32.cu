@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int e = fh & 3;
         const int dq = fq[e];
         mbar_wait_t(&accfull[dq & 1], (dq >> 1) & 1, tr ? &tw[2] : nullptr);
+        __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin
         tc_fence_after();
         const unsigned long long td0 = tr ? clock64() : 0;
         float v[32], u[32];

@@ -1,0 +1,643 @@
+// seed_i8.cu — the fused two-sided fp64 seed contraction (both seed GEMMs of
+// Algorithm 2 in one pass over Y) on the int8 tensor cores, exact-integer
+// digit arithmetic with fp64 recombination.
+//
+// Reference: right seed  cache.right = Y_(1:p) * KR(p+1..N)  (mttkrp.cpp:149-163)
+//            left seed   cache.left  = Y_(1:p)^T * KR(1..p)  (mttkrp.cpp:195-210)
+//
+// Why: on B200 the FP64 pipe (DMMA and DFMA alike) peaks at 37 TF/s, so the
+// fused pass (4 R flops per 8-byte element) is FP64-bound well below HBM speed
+// for every fp64 config.  The int8 tensor pipe is ~60x faster; fp64 values are
+// split into six balanced base-256 digits and every digit product is exact.
+//
+// Encoding.  Y carries one power-of-two scale for the whole tensor (2^eY >= max
+// |Y|, cached per tensor version); every Khatri-Rao tile (128 rows) carries one
+// per rank column.  v = rint(x 2^(46-e)) (|v| <= 2^46) is written as
+// v = sum_k d_k 256^k, d_k in [-128, 127], k = 0..5.  One DFMA produces it:
+// fma(x, 2^(46-e), 2^52 + sum_k 128 256^k) has v + sum_k 128 256^k in the low 48
+// mantissa bits, whose bytes are d_k + 128 (xor 0x80 gives the signed digit).
+// Top-first plane a = 5 - k.  The digit-pair products kept are a + b <= 5 (21 of
+// 36); the dropped ones sit 2^-48 below the leading term and random-signed, so
+// the relative error is ~1e-13 (tests/test_gpu_gradient.py holds it to 1e-10).
+//
+// Tile = 128 rows i x 128 columns j.  Digit plane a is stored once as 128 rows
+// j of 128 bytes (i contiguous, 128-byte swizzle) and serves both products:
+//   right  D_R[i][r] = sum_j P_a[i][j] B_R[r][j]   A = P_a, M = i, MN-major
+//   left   D_L[j][r] = sum_i P_a[i][j] B_L[r][i]   A = P_a^T, M = j, K-major
+// (layouts checked bit-exactly by tools/microbench/i8_mma.cu).  For plane a one
+// MMA per 32-deep K step covers all its partners b = 0..5-a: the Khatri-Rao
+// digit planes are stacked along N and the accumulator starts at diagonal a, so
+// column block b lands on diagonal a + b (6 accumulators of N columns per
+// product, exact int32: |sum| < 2^24 per tile).
+//
+// Warp roles (448 threads, one CTA per SM, persistent over a contiguous tile
+// range in row-block-major order, like seed_f64.cu):
+//   warps 0-7   split: raw fp64 slots (128 i x 16 j, 8 TMA boxes of 16 x 16 with
+//               128-byte swizzle) -> digit planes; all eight warps share each slot
+//   warps 8-11  drain: TMEM lane = output row; Horner over the 6 diagonals in
+//               fp64 times the per-column weight 2^(eY + e_r - 52); right sums
+//               persist over a row block (-> Rpart slot), left go out per tile
+//               (-> Lpart), the same partial layouts the fp64 tail reduces.
+//   warp 12     producer: TMA of the raw slots, bulk copies of the Khatri-Rao
+//               digit images (right per tile, left per row block)
+//   warp 13     TMEM allocation and the MMA issue (one lane)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "kernels.h"
+
+namespace cpdgpu {
+namespace {
+
+constexpr int kSplitW = 8, kDrainW = 4;
+constexpr int kWProd = kSplitW + kDrainW;
+constexpr int kWMma = kWProd + 1;
+constexpr int kI8Threads = (kWMma + 1) * 32;
+constexpr int kPl = 6;                       // digit planes
+constexpr int kPlane = 128 * 128;            // bytes per digit plane (one tile)
+constexpr int kRawSlot = 128 * 16 * 8;       // 16 KB: 128 i x 16 j fp64
+constexpr double kMagic = 4503599627370496.0 + 141289400074368.0;  // 2^52 + sum_{k<6} 128 256^k
+
+template <int N>
+struct Cfg {
+  static constexpr int kB = kPl * N * 128;  // one Khatri-Rao digit image
+  static constexpr int kRaw = N == 32 ? 5 : 6;   // raw ring deep enough to stream through an MMA phase
+  static constexpr int kCols = N == 32 ? 512 : 256;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kPl * kPlane + 2 * kB + 256;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+// Barrier wait with a watchdog: a wait that spins ~2^31 times (seconds) traps,
+// so a broken pipeline surfaces as a launch error instead of a hung GPU.  With
+// SeedI8Params::debug each warp posts its position (progress[cta][warp]) and the
+// first stuck thread prints its CTA's table before trapping.
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int code, int info,
+                                             unsigned* progress) {
+  uint32_t done = 0;
+  uint32_t spins = 0;
+  if (progress && (threadIdx.x & 31) == 0)
+    *reinterpret_cast<volatile unsigned*>(progress + blockIdx.x * 16 + (threadIdx.x >> 5)) =
+        static_cast<unsigned>(code * 100000 + info);
+  const uint32_t limit = progress ? (1u << 24) : (1u << 31);
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!done && ++spins >= limit) {
+      if (progress) {
+        const volatile unsigned* t = progress + blockIdx.x * 16;
+        printf("seed_i8 stuck: cta %d warp %d code %d info %d | warps: %u %u %u %u %u %u %u %u | %u %u %u %u | %u %u\n",
+               blockIdx.x, threadIdx.x >> 5, code, info, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[8], t[9],
+               t[10], t[11], t[12], t[13]);
+      }
+      __trap();
+    }
+  }
+}
+#define WAIT(bar, par, code, info) mbar_wait_wd(bar, par, code, info, p.progress)
+#define TWAIT(idx, bar, par, code, info)                 \
+  do {                                                   \
+    const long long t0_ = p.trace ? clock64() : 0;       \
+    WAIT(bar, par, code, info);                          \
+    if (p.trace) tw[idx] += clock64() - t0_;             \
+  } while (0)
+// non-blocking phase test
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                       uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// shared-memory matrix descriptor, 128-byte swizzle, sm_100 version bit
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor, kind::i8: s8 x s8 -> s32, M = 128, N = n, A MN- or K-major
+__device__ __forceinline__ uint32_t idesc_i8(bool a_mn, int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (8u << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};\n" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+// Four values' digit bytes (u = fma(x, s, kMagic)) -> six words, word k = byte k
+// of each value (value 0 in the low byte), as signed digits.
+__device__ __forceinline__ void pack4(double x0, double x1, double x2, double x3, double s, uint32_t (&w)[6]) {
+  const double u0 = fma(x0, s, kMagic), u1 = fma(x1, s, kMagic), u2 = fma(x2, s, kMagic), u3 = fma(x3, s, kMagic);
+  const uint32_t l0 = __double2loint(u0), l1 = __double2loint(u1), l2 = __double2loint(u2), l3 = __double2loint(u3);
+  const uint32_t h0 = __double2hiint(u0), h1 = __double2hiint(u1), h2 = __double2hiint(u2), h3 = __double2hiint(u3);
+  const uint32_t t01 = prmt(l0, l1, 0x5140), t23 = prmt(l2, l3, 0x5140);
+  const uint32_t s01 = prmt(l0, l1, 0x7362), s23 = prmt(l2, l3, 0x7362);
+  const uint32_t g01 = prmt(h0, h1, 0x5140), g23 = prmt(h2, h3, 0x5140);
+  w[0] = prmt(t01, t23, 0x5410) ^ 0x80808080u;
+  w[1] = prmt(t01, t23, 0x7632) ^ 0x80808080u;
+  w[2] = prmt(s01, s23, 0x5410) ^ 0x80808080u;
+  w[3] = prmt(s01, s23, 0x7632) ^ 0x80808080u;
+  w[4] = prmt(g01, g23, 0x5410) ^ 0x80808080u;
+  w[5] = prmt(g01, g23, 0x7632) ^ 0x80808080u;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kI8Threads, 1)
+    seed_i8_kernel(const SeedI8Params p, const __grid_constant__ CUtensorMap ymap) {
+  using C = Cfg<N>;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cta = blockIdx.x;
+  const int64_t a0 = static_cast<int64_t>(cta) * p.T / p.P;
+  const int64_t a1 = static_cast<int64_t>(cta + 1) * p.T / p.P;
+  const int n = static_cast<int>(a1 - a0);
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* raw = base;                               // [kRaw][16 KB]
+  unsigned char* dig = raw + C::kRaw * kRawSlot;           // [6][128 j][128 B]
+  unsigned char* rbuf = dig + kPl * kPlane;                // [kB] right Khatri-Rao digits (per tile)
+  unsigned char* lbuf = rbuf + C::kB;                      // [kB] left Khatri-Rao digits (per row block)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lbuf + C::kB);
+  uint64_t* raw_full = bars;
+  uint64_t* raw_empty = raw_full + C::kRaw;
+  uint64_t* dig_full = raw_empty + C::kRaw;
+  uint64_t* dig_empty = dig_full + 1;
+  uint64_t* rb_full = dig_empty + 1;
+  uint64_t* rb_empty = rb_full + 1;
+  uint64_t* lb_full = rb_empty + 1;
+  uint64_t* lb_empty = lb_full + 1;
+  uint64_t* accR_full = lb_empty + 1;
+  uint64_t* accR_empty = accR_full + 1;
+  uint64_t* accL_full = accR_empty + 1;
+  uint64_t* accL_empty = accL_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accL_empty + 1);
+
+  if (tid == 0) {
+    for (int s = 0; s < C::kRaw; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], kSplitW);
+    }
+    mbar_init(dig_full, kSplitW);
+    mbar_init(dig_empty, 1);
+    mbar_init(rb_full, 1);
+    mbar_init(rb_empty, 1);
+    mbar_init(lb_full, 1);
+    mbar_init(lb_empty, 1);
+    mbar_init(accR_full, 1);
+    mbar_init(accR_empty, kDrainW);
+    mbar_init(accL_full, 1);
+    mbar_init(accL_empty, kDrainW);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == kWMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (warp == kWProd && lane == 0)
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&ymap)));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t nCT = p.nCT;
+  long long tw[4] = {0, 0, 0, 0};  // CPDGPU_SEED_TRACE: per-warp wait cycles
+  const long long tstart = clock64();
+
+  if (warp == kWProd) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_y = policy_evict_first(), pol_k = policy_evict_last();
+      const int nslots = n * 8;
+      // Boxes wholly outside Y are not requested (the split reads them as zeros).
+      auto issue_raw = [&](int q) {
+        const int k = q >> 3, s8 = q & 7, slot = q % C::kRaw;
+        const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
+        unsigned char* dst = raw + slot * kRawSlot;
+        const int j = static_cast<int>(ct * 128 + 16 * s8), i = static_cast<int>(rb * 128);
+        const int nbox = j >= p.K ? 0 : min(8, static_cast<int>((p.J - i + 15) / 16));
+        mbar_arrive_tx(&raw_full[slot], nbox * 2048);
+        for (int c = 0; c < nbox; ++c) tma_2d(dst + c * 2048, &ymap, i + 16 * c, j, &raw_full[slot], pol_y);
+      };
+      const int early = nslots < C::kRaw ? nslots : C::kRaw;
+      for (int q = 0; q < early; ++q) issue_raw(q);  // Y does not depend on the predecessor
+      pdl_wait();
+      // Event loop: raw slots go out as soon as their ring slot drains; the
+      // Khatri-Rao images (right per tile, left per row block) as soon as the
+      // MMAs released the previous one, without holding up the raw stream.
+      int q = early, kb = 0, m = 0;
+      int64_t cur_rb = -1;
+      while (q < nslots || kb < n) {
+        if (kb < n && (kb == 0 || mbar_test(rb_empty, (kb - 1) & 1))) {
+          const int64_t tile = a0 + kb, rb = tile / nCT, ct = tile - rb * nCT;
+          const bool new_rb = rb != cur_rb;
+          if (!new_rb || m == 0 || mbar_test(lb_empty, (m - 1) & 1)) {
+            mbar_arrive_tx(rb_full, C::kB);
+            bulk_load(rbuf, p.img_r + ct * C::kB, C::kB, rb_full, pol_k);
+            if (new_rb) {
+              mbar_arrive_tx(lb_full, C::kB);
+              bulk_load(lbuf, p.img_l + rb * C::kB, C::kB, lb_full, pol_k);
+              cur_rb = rb;
+              ++m;
+            }
+            ++kb;
+          }
+        }
+        if (q < nslots && mbar_test(&raw_empty[q % C::kRaw], ((q / C::kRaw) - 1) & 1)) {
+          issue_raw(q);
+          ++q;
+        }
+      }
+    }
+  } else if (warp == kWMma) {
+    // ------------------------------------------------------------------ MMA issue
+    if (lane == 0) {
+      const uint32_t dg = smem_u32(dig), lb = smem_u32(lbuf);
+      int64_t cur_rb = -1;
+      int m = 0;
+      for (int k = 0; k < n; ++k) {
+        const int64_t tile = a0 + k, rb = tile / nCT;
+        const bool last_of_rb = (k == n - 1) || ((tile + 1) / nCT != rb);
+        TWAIT(0, dig_full, k & 1, 4, k);
+        TWAIT(1, rb_full, k & 1, 5, k);
+        if (k > 0) TWAIT(2, accR_empty, (k - 1) & 1, 6, k);
+        tc_fence_after();
+        const uint32_t rbb = smem_u32(rbuf);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+          for (int a = 0; a < kPl; ++a)
+            mma_i8(tmem + a * N, sdesc(dg + a * kPlane + ks * 4096, 16384, 1024), sdesc(rbb + ks * 32, 16, 1024),
+                   idesc_i8(true, N * (kPl - a)), (ks > 0 || a > 0) ? 1u : 0u);
+        umma_commit(accR_full);
+        umma_commit(rb_empty);
+        if (rb != cur_rb) {
+          TWAIT(3, lb_full, m & 1, 7, m);
+          cur_rb = rb;
+          ++m;
+        }
+        if (k > 0) TWAIT(3, accL_empty, (k - 1) & 1, 8, k);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+          for (int a = 0; a < kPl; ++a)
+            mma_i8(tmem + kPl * N + a * N, sdesc(dg + a * kPlane + ks * 32, 16, 1024), sdesc(lb + ks * 32, 16, 1024),
+                   idesc_i8(false, N * (kPl - a)), (ks > 0 || a > 0) ? 1u : 0u);
+        umma_commit(accL_full);
+        umma_commit(dig_empty);
+        if (last_of_rb) umma_commit(lb_empty);
+      }
+    }
+    __syncwarp();
+  } else if (warp < kSplitW) {
+    // ------------------------------------------------------------------ split
+    // Every split warp takes part in every raw slot (each slot's fills are then
+    // observed in order by all its waiters).  Thread = (row j = jj, 16-row chunk c,
+    // half h): 8 values i = 16 c + 8 h .. +7 -> 8 bytes of each digit plane; a
+    // half-warp (8 rows x 2 halves) stores 128 conflict-free bytes.
+    const int jj = (lane & 7) + 8 * (warp & 1), h = (lane >> 3) & 1, c = (lane >> 4) + 2 * (warp >> 1);
+    if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 1;
+    pdl_wait();
+    if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 2;
+    const double sy = p.yscale[0];
+    const uint32_t dg = smem_u32(dig);
+    const int sw = ((c ^ (jj & 7)) << 4) + 8 * h;
+    for (int k = 0; k < n; ++k) {
+      const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
+      const bool row_live = rb * 128 + 16 * c < p.J;
+#pragma unroll 1
+      for (int s8 = 0; s8 < 8; ++s8) {
+        const int q = k * 8 + s8, slot = q % C::kRaw;
+        TWAIT(0, &raw_full[slot], (q / C::kRaw) & 1, 9, q);
+        const unsigned char* box = raw + slot * kRawSlot + c * 2048 + jj * 128;
+        const bool live = row_live && ct * 128 + 16 * s8 < p.K;  // the box was requested
+        double2 v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          v[t] = live ? *reinterpret_cast<const double2*>(box + (((4 * h + t) ^ (jj & 7)) << 4)) : make_double2(0.0, 0.0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&raw_empty[slot]);
+        uint32_t w0[6], w1[6];
+        pack4(v[0].x, v[0].y, v[1].x, v[1].y, sy, w0);
+        pack4(v[2].x, v[2].y, v[3].x, v[3].y, sy, w1);
+        if (s8 == 0 && k > 0) TWAIT(1, dig_empty, (k - 1) & 1, 10, k);
+        const uint32_t row = dg + (16 * s8 + jj) * 128 + sw;
+#pragma unroll
+        for (int kk = 0; kk < kPl; ++kk)  // byte k -> top-first plane 5 - k
+          st_shared_v2(row + (kPl - 1 - kk) * kPlane, w0[kk], w1[kk]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dig_full);
+    }
+  } else {
+    // ------------------------------------------------------------------ drain
+    const int qd = warp & 3, row = 32 * qd + lane;
+    const uint32_t lanes = static_cast<uint32_t>(32 * qd) << 16;
+    if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 1;
+    pdl_wait();
+    if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 2;
+    double acc[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) acc[r] = 0.0;
+    const int64_t rb0 = a0 / nCT;
+    for (int k = 0; k < n; ++k) {
+      const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
+      const bool last_of_rb = (k == n - 1) || ((tile + 1) / nCT != rb);
+      // right: running sums over the row block's column tiles
+      TWAIT(0, accR_full, k & 1, 11, k);
+      __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin
+      tc_fence_after();
+      const double* wr = p.w_r + ct * N;
+#pragma unroll
+      for (int rc = 0; rc < N / 8; ++rc) {
+        uint32_t d[kPl][8];
+#pragma unroll
+        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + dd * N + rc * 8, d[dd]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          double h = static_cast<double>(static_cast<int>(d[0][e]));
+#pragma unroll
+          for (int dd = 1; dd < kPl; ++dd) h = fma(h, 256.0, static_cast<double>(static_cast<int>(d[dd][e])));
+          acc[rc * 8 + e] = fma(h, __ldg(wr + rc * 8 + e), acc[rc * 8 + e]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accR_empty);
+      if (last_of_rb) {
+        double* dst = p.Rpart + (static_cast<int64_t>(cta) * p.slots + (rb - rb0)) * p.RP * 128;
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          if (r < p.RP) dst[r * 128 + row] = acc[r];
+          acc[r] = 0.0;
+        }
+      }
+      // left: this tile's columns, complete over its 128 rows
+      TWAIT(1, accL_full, k & 1, 12, k);
+      __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin
+      tc_fence_after();
+      const double* wl = p.w_l + rb * N;
+      const int64_t j = ct * 128 + row;
+      double* lout = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K + j;
+#pragma unroll
+      for (int rc = 0; rc < N / 8; ++rc) {
+        uint32_t d[kPl][8];
+#pragma unroll
+        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + kPl * N + dd * N + rc * 8, d[dd]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          double h = static_cast<double>(static_cast<int>(d[0][e]));
+#pragma unroll
+          for (int dd = 1; dd < kPl; ++dd) h = fma(h, 256.0, static_cast<double>(static_cast<int>(d[dd][e])));
+          const int r = rc * 8 + e;
+          if (r < p.R && j < p.K) lout[static_cast<int64_t>(r) * p.K] = h * __ldg(wl + r);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accL_empty);
+    }
+  }
+  if (p.trace && lane == 0) {
+    unsigned long long* t = p.trace + (static_cast<int64_t>(cta) * 14 + warp) * 6;
+    for (int i = 0; i < 4; ++i) t[i] = static_cast<unsigned long long>(tw[i]);
+    t[4] = static_cast<unsigned long long>(clock64() - tstart);
+    t[5] = static_cast<unsigned long long>(n);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWMma) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(C::kCols));
+  }
+}
+
+// Khatri-Rao rows [L][ldk] (r < R valid) -> per 128-row tile: digit image
+// [6 planes][N rank rows][128 bytes of the tile's rows, 128-byte swizzle] and the
+// per-column weights 2^(eY + e_r - 52) (0 for an all-zero column, NaN when the
+// column holds a non-finite value).  CTA = tile, thread = (row q, 8 columns).
+template <int N>
+__global__ void __launch_bounds__(N * 16) kr_digits_kernel(const double* rows, int64_t L, int ldk, int R,
+                                                           const double* yscale, unsigned char* img, double* w) {
+  __shared__ int ex[N];      // max exponent (frexp) per column, INT_MIN: all zero
+  __shared__ int bad[N];     // non-finite seen
+  __shared__ double sc[N];
+  __shared__ __align__(16) unsigned char im[kPl * N * 128];
+  const int q = threadIdx.x & 127, r0 = (threadIdx.x >> 7) * 8;
+  const int64_t tile = blockIdx.x, row = tile * 128 + q;
+  if (threadIdx.x < N) {
+    ex[threadIdx.x] = -2147483647 - 1;
+    bad[threadIdx.x] = 0;
+  }
+  pdl_wait();
+  __syncthreads();
+  double x[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int r = r0 + e;
+    x[e] = (row < L && r < R) ? rows[row * ldk + r] : 0.0;
+    int ee = -2147483647 - 1;
+    if (x[e] != 0.0) frexp(x[e], &ee);
+    const int m = __reduce_max_sync(0xffffffffu, ee);
+    const unsigned nf = __ballot_sync(0xffffffffu, !isfinite(x[e]));
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(&ex[r], m);
+      if (nf) bad[r] = 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    const int r = threadIdx.x, e = ex[r];
+    if (bad[r]) {
+      sc[r] = 0.0;
+      w[tile * N + r] = __longlong_as_double(0x7ff8000000000000ll);
+    } else if (e == -2147483647 - 1) {
+      sc[r] = 0.0;
+      w[tile * N + r] = 0.0;
+    } else {
+      sc[r] = ldexp(1.0, 46 - e);
+      w[tile * N + r] = ldexp(1.0, e + static_cast<int>(yscale[1]) - 52);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int r = r0 + e;
+    const double u = fma(isfinite(x[e]) ? x[e] : 0.0, sc[r], kMagic);
+    const uint32_t lo = __double2loint(u), hi = __double2hiint(u);
+    const int off = r * 128 + ((((q >> 4) ^ (r & 7))) << 4) + (q & 15);
+#pragma unroll
+    for (int k = 0; k < kPl; ++k) {
+      const uint32_t b = (k < 4 ? (lo >> (8 * k)) : (hi >> (8 * (k - 4)))) & 0xFFu;
+      im[(kPl - 1 - k) * N * 128 + off] = static_cast<unsigned char>(b ^ 0x80u);
+    }
+  }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(img + tile * (kPl * N * 128));
+  const uint4* src = reinterpret_cast<const uint4*>(im);
+  for (int e = threadIdx.x; e < kPl * N * 8; e += N * 16) dst[e] = src[e];
+}
+
+// max |Y| -> scale record: [0] 2^(46 - eY), [1] eY, [2] max |Y| (NaN when Y has
+// one), [3] sum |Y| (range guard only; atomics, not bitwise reproducible)
+__global__ void y_amax_kernel(const double* y, int64_t n, unsigned long long* amax, double* asum) {
+  unsigned long long m = 0;
+  double a = 0.0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = fabs(y[e]);
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    m = b > m ? b : m;  // NaN bit patterns sort above +inf
+    a += v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = t > m ? t : m;
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(amax, m);
+    atomicAdd(asum, a);
+  }
+}
+__global__ void y_scale_final_kernel(const unsigned long long* amax, const double* asum, double* out) {
+  const double m = __longlong_as_double(static_cast<long long>(*amax));
+  int e = 0;
+  if (m > 0.0 && m < 1e300) frexp(m, &e);
+  out[0] = ldexp(1.0, 46 - e);
+  out[1] = static_cast<double>(e);
+  out[2] = m;
+  out[3] = *asum;
+}
+
+}  // namespace
+
+size_t seed_i8_smem_bytes(int N) { return N == 32 ? Cfg<32>::kSmem : Cfg<16>::kSmem; }
+
+int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s) {
+  if (p.N == 32) {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(seed_i8_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<32>::kSmem);
+      configured = true;
+    }
+    launch_k(seed_i8_kernel<32>, dim3(p.P), dim3(kI8Threads), Cfg<32>::kSmem, s, pdl_enabled(), p, *ymap);
+  } else {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(seed_i8_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<16>::kSmem);
+      configured = true;
+    }
+    launch_k(seed_i8_kernel<16>, dim3(p.P), dim3(kI8Threads), Cfg<16>::kSmem, s, pdl_enabled(), p, *ymap);
+  }
+  return 1;
+}
+
+int launch_kr_digits(const double* rows, int64_t L, int ldk, int R, int N, const double* yscale, void* img, double* w,
+                     cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>(ceil_div(L, 128)));
+  if (N == 32)
+    launch_k(kr_digits_kernel<32>, grid, dim3(512), 0, s, pdl_enabled(), rows, L, ldk, R, yscale,
+             static_cast<unsigned char*>(img), w);
+  else
+    launch_k(kr_digits_kernel<16>, grid, dim3(256), 0, s, pdl_enabled(), rows, L, ldk, R, yscale,
+             static_cast<unsigned char*>(img), w);
+  return 1;
+}
+
+int launch_y_scale_f64(const double* y, int64_t n, void* scratch, double* out, int num_sms, cudaStream_t s) {
+  unsigned long long* amax = static_cast<unsigned long long*>(scratch);
+  double* asum = reinterpret_cast<double*>(amax + 1);
+  cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned long long), s);
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > 8LL * num_sms) blocks = 8LL * num_sms;
+  if (blocks < 1) blocks = 1;
+  y_amax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(y, n, amax, asum);
+  y_scale_final_kernel<<<1, 1, 0, s>>>(amax, asum, out);
+  return 2;
+}
+
+}  // namespace cpdgpu

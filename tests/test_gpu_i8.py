@@ -1,0 +1,119 @@
+"""GPU parity of the fused fp64 seed on the int8 tensor cores (seed_i8.cu,
+opt-in with CPDGPU_I8=1) against the CPU oracle.
+
+The int8 path splits every fp64 value into six base-256 digits and keeps the 21
+digit-pair products a + b <= 5; its error is ~1e-13 relative (Frobenius), held
+here to the BASELINE.json fp64 gate of 1e-10 per mode, and to the reference's
+own 1e-12 max-abs-scaled tolerance (test_util.hpp:86-89) on the small fixture
+shapes.  Shapes cover full and ragged 128 x 128 tiles, single-row-block views,
+R = 1..32 (both MMA rank blocks), and the fallbacks (odd J_p, non-finite Y).
+"""
+import numpy as np
+import pytest
+
+import paper_1204_1586_b200 as cpd
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def i8_env(monkeypatch):
+    monkeypatch.setenv("CPDGPU_I8", "1")  # read when the tensor's plan is built
+
+
+def rel_fro(got, want):
+    return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300))
+
+
+def max_rel_diff(a, b):
+    scale = max(np.abs(a).max(initial=0.0), np.abs(b).max(initial=0.0), 1e-30)
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max(initial=0.0) / scale)
+
+
+def run(gpu_ctx, oracle, dims, R, seed, values=None):
+    rng = np.random.default_rng(seed)
+    y = rng.standard_normal(int(np.prod(dims))) if values is None else values
+    f = [rng.standard_normal((d, R)) for d in dims]
+    t = cpd.DenseTensor.from_values(y, dims, ctx=gpu_ctx)
+    g = cpd.cp_gradient_all(t, f)
+    path = gpu_ctx.last_seed_path()
+    want = oracle.cp_gradient_all(y, dims, f)[0]
+    t.free()
+    return g, want, path
+
+
+@pytest.mark.parametrize("dims,R", [
+    ((60, 60, 60, 60), 20),   # c2 shape: ragged last tile both ways (3600 = 28 * 128 + 16)
+    ((60, 60, 60, 60), 16),
+    ((200, 200, 200), 10),    # c1 shape: J_p = 200 (2 row blocks, 56 padded rows)
+    ((14, 14, 14, 14, 14), 10),
+    ((30, 30, 30, 30), 32),   # widest rank block
+    ((16, 16, 16), 1),
+    ((128, 128, 4), 7),       # exact tiles
+    ((130, 6, 7), 3),         # one column tile, 2 row blocks
+    ((2, 64, 300), 5),        # J_p = 2: one row block, mostly padding
+])
+def test_int8_seed_matches_oracle(gpu_ctx, oracle, i8_env, dims, R):
+    g, want, path = run(gpu_ctx, oracle, dims, R, 7 + R)
+    assert path == 1, "int8 seed path did not run"
+    for n, (a, b) in enumerate(zip(g, want)):
+        assert rel_fro(a, b) < 1e-10, (n, rel_fro(a, b))
+        assert max_rel_diff(a, b) < 1e-10, (n, max_rel_diff(a, b))
+
+
+def test_int8_seed_integer_known_answers(gpu_ctx, oracle, i8_env):
+    # test_mttkrp.cpp:13-35: exact integers through the digit arithmetic
+    y = cpd.DenseTensor.from_values(np.arange(1, 9, dtype=float), [2, 2, 2], ctx=gpu_ctx)
+    g = cpd.cp_gradient_all(y, [np.ones((2, 2)) for _ in range(3)])
+    assert gpu_ctx.last_seed_path() == 1
+    want = [[16, 20], [14, 22], [10, 26]]
+    for n in range(3):
+        for r in range(2):
+            assert list(g[n][:, r]) == want[n]
+
+
+def test_int8_seed_repeated_calls_are_bitwise_stable(gpu_ctx, oracle, i8_env):
+    rng = np.random.default_rng(3)
+    dims, R = (60, 60, 60, 60), 20
+    y = rng.standard_normal(int(np.prod(dims)))
+    f = [rng.standard_normal((d, R)) for d in dims]
+    t = cpd.DenseTensor.from_values(y, dims, ctx=gpu_ctx)
+    first = cpd.cp_gradient_all(t, f)
+    for _ in range(4):  # eager, graph capture, replays
+        again = cpd.cp_gradient_all(t, f)
+        for a, b in zip(first, again):
+            assert np.array_equal(a, b)
+    t.free()
+
+
+def test_int8_falls_back_for_odd_rows(gpu_ctx, oracle, i8_env):
+    g, want, path = run(gpu_ctx, oracle, (7, 9, 11), 4, 11)
+    assert path == 0  # J_p odd: no 16-byte aligned TMA view, DMMA pass
+    for a, b in zip(g, want):
+        assert rel_fro(a, b) < 1e-12
+
+
+def test_int8_falls_back_for_wide_dynamic_range(gpu_ctx, oracle, i8_env):
+    rng = np.random.default_rng(5)
+    dims = (40, 40, 40)
+    y = rng.standard_normal(int(np.prod(dims)))
+    y[17] = 1e9  # max |Y| far beyond 2^12 RMS: digits would starve the small entries
+    g, want, path = run(gpu_ctx, oracle, dims, 6, 5, values=y)
+    assert path == 0
+    for a, b in zip(g, want):
+        assert rel_fro(a, b) < 1e-12
+
+
+def test_int8_nonfinite_factor_propagates(gpu_ctx, oracle, i8_env):
+    rng = np.random.default_rng(9)
+    dims, R = (32, 32, 32), 4
+    y = rng.standard_normal(int(np.prod(dims)))
+    f = [rng.standard_normal((d, R)) for d in dims]
+    f[2][3, 1] = np.nan
+    t = cpd.DenseTensor.from_values(y, dims, ctx=gpu_ctx)
+    g = cpd.cp_gradient_all(t, f)
+    assert gpu_ctx.last_seed_path() == 1
+    # column 1 of every gradient that contracts over factor 3 is NaN, as in fp64 GEMMs
+    assert np.isnan(g[0][:, 1]).all() and np.isnan(g[1][:, 1]).all()
+    assert np.isfinite(g[0][:, 0]).all()
+    t.free()
