@@ -736,7 +736,7 @@ void bind_i8(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const void* ybase) {
   if (on && pl.i8.ymap_base != ybase) {
     on = cpdgpu::make_tensor_map_2d(&pl.i8.ymap, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
                                     static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
-                                    static_cast<uint64_t>(pl.Jp) * 8, 16, 16, true, false);
+                                    static_cast<uint64_t>(pl.Jp) * 8, 16, 128, true, true);
     pl.i8.ymap_base = on ? ybase : nullptr;
   }
   if (on != pl.i8.on && pl.grad_exec) {  // the recorded gradient used the other seed path
@@ -864,8 +864,9 @@ void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
   Plan::I8& g = pl.i8;
   Plan::Chunk& c = pl.chunks[0];
   const double* ys = pl.tensor->yscale8.d();
-  ctx->launches += cpdgpu::launch_kr_digits(c.KRr->d(), pl.Kp, c.sp.LDK, c.Rc, g.N, ys, g.img_r.p, g.w_r.d(), s);
-  ctx->launches += cpdgpu::launch_kr_digits(c.KRl->d(), pl.Jp, c.sp.LDK, c.Rc, g.N, ys, g.img_l.p, g.w_l.d(), s);
+  const KRSpec right = pl.spec(pl.p + 1, pl.N, c.r0);
+  ctx->launches += cpdgpu::launch_kr_digits(c.KRr->d(), pl.Kp, c.sp.LDK, c.Rc, g.N, ys, g.img_r.p, g.w_r.d(), &right, s);
+  ctx->launches += cpdgpu::launch_kr_digits(c.KRl->d(), pl.Jp, c.sp.LDK, c.Rc, g.N, ys, g.img_l.p, g.w_l.d(), nullptr, s);
   cpdgpu::SeedI8Params q{};
   q.J = pl.Jp;
   q.K = pl.Kp;
@@ -890,6 +891,8 @@ void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
     CK(cudaMemsetAsync(progress.p, 0, progress.bytes, s));
   }
   q.progress = dbg ? static_cast<unsigned*>(progress.p) : nullptr;
+  static const int knobs = std::getenv("CPDGPU_I8_KNOBS") ? std::atoi(std::getenv("CPDGPU_I8_KNOBS")) : 0;
+  q.knobs = knobs;
   q.Lpart = g.nRB == 1 ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d() + c.lpart_off;
   static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
   DevBuf tb;

@@ -11,36 +11,44 @@
 // split into six balanced base-256 digits and every digit product is exact.
 //
 // Encoding.  Y carries one power-of-two scale for the whole tensor (2^eY >= max
-// |Y|, cached per tensor version); every Khatri-Rao tile (128 rows) carries one
-// per rank column.  v = rint(x 2^(46-e)) (|v| <= 2^46) is written as
+// |Y|, cached per tensor version).  The right Khatri-Rao rows carry one scale per
+// rank column for all tiles (the product of the factor column maxima), the left
+// ones one per column and 128-row block.  v = rint(x 2^(46-e)) (|v| <= 2^46) is
 // v = sum_k d_k 256^k, d_k in [-128, 127], k = 0..5.  One DFMA produces it:
 // fma(x, 2^(46-e), 2^52 + sum_k 128 256^k) has v + sum_k 128 256^k in the low 48
 // mantissa bits, whose bytes are d_k + 128 (xor 0x80 gives the signed digit).
 // Top-first plane a = 5 - k.  The digit-pair products kept are a + b <= 5 (21 of
 // 36); the dropped ones sit 2^-48 below the leading term and random-signed, so
-// the relative error is ~1e-13 (tests/test_gpu_gradient.py holds it to 1e-10).
+// the relative error is ~1e-13 (tests/test_gpu_i8.py holds it to 1e-10).
 //
-// Tile = 128 rows i x 128 columns j.  Digit plane a is stored once as 128 rows
-// j of 128 bytes (i contiguous, 128-byte swizzle) and serves both products:
-//   right  D_R[i][r] = sum_j P_a[i][j] B_R[r][j]   A = P_a, M = i, MN-major
-//   left   D_L[j][r] = sum_i P_a[i][j] B_L[r][i]   A = P_a^T, M = j, K-major
+// Tile = 128 rows i x 128 columns j, digits in two half-tile buffers (columns
+// 0-63, 64-127).  Digit plane a of a half is 64 rows j of 128 bytes (i
+// contiguous, 128-byte swizzle) and serves both products:
+//   right  D_R[i][r] += sum_j P_a[i][j] B_R[r][j]  A = P_a, M = 128 (i), MN-major
+//   left   D_L[j][r]  = sum_i P_a[i][j] B_L[r][i]  A = P_a^T, M = 64 (j), K-major,
+//          half h in TMEM lanes 16 h .. 16 h + 15 of each 32-lane quarter
 // (layouts checked bit-exactly by tools/microbench/i8_mma.cu).  For plane a one
 // MMA per 32-deep K step covers all its partners b = 0..5-a: the Khatri-Rao
 // digit planes are stacked along N and the accumulator starts at diagonal a, so
 // column block b lands on diagonal a + b (6 accumulators of N columns per
-// product, exact int32: |sum| < 2^24 per tile).
+// product, exact int32).  The right accumulators run across a row block's tiles
+// (segments of <= kSeg tiles); the left ones are drained per tile.
 //
 // Warp roles (448 threads, one CTA per SM, persistent over a contiguous tile
 // range in row-block-major order, like seed_f64.cu):
-//   warps 0-7   split: raw fp64 slots (128 i x 16 j, 8 TMA boxes of 16 x 16 with
-//               128-byte swizzle) -> digit planes; all eight warps share each slot
+//   warps 0-7   split: raw fp64 slots (one 16 KB TMA box, 16 rows i x 128
+//               columns j, 128-byte swizzle; 8 KB boxes cap TMA near 4 TB/s,
+//               tools/microbench/tma_order.cu) -> digit planes; all eight warps
+//               share each slot
 //   warps 8-11  drain: TMEM lane = output row; Horner over the 6 diagonals in
-//               fp64 times the per-column weight 2^(eY + e_r - 52); right sums
-//               persist over a row block (-> Rpart slot), left go out per tile
-//               (-> Lpart), the same partial layouts the fp64 tail reduces.
+//               fp64 times the column weight 2^(eY + e_r - 52); right sums once
+//               per segment (-> Rpart slot at the row block's end), left per tile
+//               (-> Lpart): the partial layouts the fp64 tail reduces (TI = 128).
 //   warp 12     producer: TMA of the raw slots, bulk copies of the Khatri-Rao
-//               digit images (right per tile, left per row block)
+//               digit images (right per tile, left per row block), event loop
 //   warp 13     TMEM allocation and the MMA issue (one lane)
+// Opt-in (CPDGPU_I8=1): measured on B200 it does not yet beat the DMMA pass at
+// the BASELINE configs (DESIGN.md section 5 has the numbers and the analysis).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -58,16 +66,25 @@ constexpr int kWProd = kSplitW + kDrainW;
 constexpr int kWMma = kWProd + 1;
 constexpr int kI8Threads = (kWMma + 1) * 32;
 constexpr int kPl = 6;                       // digit planes
-constexpr int kPlane = 128 * 128;            // bytes per digit plane (one tile)
-constexpr int kRawSlot = 128 * 16 * 8;       // 16 KB: 128 i x 16 j fp64
+constexpr int kHalfPlane = 64 * 128;        // bytes per digit plane of a half tile (64 j x 128 i)
+constexpr int kHalf = 6 * kHalfPlane;        // one half-tile digit buffer (48 KB)
+constexpr int kRawSlot = 16 * 128 * 8;       // 16 KB: one TMA box, 16 rows i x 128 columns j fp64
 constexpr double kMagic = 4503599627370496.0 + 141289400074368.0;  // 2^52 + sum_{k<6} 128 256^k
+// The right accumulators run over a row block's column tiles in TMEM (the right
+// Khatri-Rao digits share one scale per column); a segment is drained at the end
+// of the row block or after kSeg tiles (int32 headroom: |D| < 6 2^21 per tile).
+constexpr int kSeg = 128;
+__device__ __forceinline__ bool seg_end(int64_t tile, int k, int n, int64_t nCT, int pos) {
+  return k == n - 1 || (tile + 1) / nCT != tile / nCT || pos == kSeg - 1;
+}
 
 template <int N>
 struct Cfg {
   static constexpr int kB = kPl * N * 128;  // one Khatri-Rao digit image
-  static constexpr int kRaw = N == 32 ? 5 : 6;   // raw ring deep enough to stream through an MMA phase
+  static constexpr int kNB = 2;                  // half-tile digit buffers (one tile)
+  static constexpr int kRaw = N == 32 ? 5 : 6;   // 16 KB TMA boxes (8 KB boxes cap TMA at ~4 TB/s)
   static constexpr int kCols = N == 32 ? 512 : 256;
-  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kPl * kPlane + 2 * kB + 256;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kNB * kHalf + 2 * kB + 256;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -168,10 +185,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
   return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
 }
-// instruction descriptor, kind::i8: s8 x s8 -> s32, M = 128, N = n, A MN- or K-major
-__device__ __forceinline__ uint32_t idesc_i8(bool a_mn, int n) {
+// instruction descriptor, kind::i8: s8 x s8 -> s32, M = m, N = n, A MN- or K-major
+__device__ __forceinline__ uint32_t idesc_i8(bool a_mn, int n, int m) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | (static_cast<uint32_t>(n >> 3) << 17) |
-         (8u << 24);
+         (static_cast<uint32_t>(m >> 4) << 24);
 }
 __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -190,6 +207,18 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
                : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+// Diagonal sums (top first, weights 256^(5-d)) -> one fp64 value.  Adjacent
+// diagonals combine in int32 where they cannot overflow (|D_0| < 2^20,
+// |D_1| < 2^22, |D_2| < 2^23, |D_3| < 2^23 per tile), so four conversions
+// replace six.
+__device__ __forceinline__ double horner6(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3, uint32_t d4,
+                                          uint32_t d5) {
+  const int c01 = static_cast<int>(d0) * 256 + static_cast<int>(d1);
+  const int c23 = static_cast<int>(d2) * 256 + static_cast<int>(d3);
+  double h = fma(static_cast<double>(c01), 65536.0, static_cast<double>(c23));
+  h = fma(h, 256.0, static_cast<double>(static_cast<int>(d4)));
+  return fma(h, 256.0, static_cast<double>(static_cast<int>(d5)));
+}
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
@@ -233,14 +262,14 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* raw = base;                               // [kRaw][16 KB]
   unsigned char* dig = raw + C::kRaw * kRawSlot;           // [6][128 j][128 B]
-  unsigned char* rbuf = dig + kPl * kPlane;                // [kB] right Khatri-Rao digits (per tile)
+  unsigned char* rbuf = dig + C::kNB * kHalf;              // [kB] right Khatri-Rao digits (per tile)
   unsigned char* lbuf = rbuf + C::kB;                      // [kB] left Khatri-Rao digits (per row block)
   uint64_t* bars = reinterpret_cast<uint64_t*>(lbuf + C::kB);
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + C::kRaw;
-  uint64_t* dig_full = raw_empty + C::kRaw;
-  uint64_t* dig_empty = dig_full + 1;
-  uint64_t* rb_full = dig_empty + 1;
+  uint64_t* dig_full = raw_empty + C::kRaw;  // [2] half-tile digit buffers
+  uint64_t* dig_empty = dig_full + 2;        // [2]
+  uint64_t* rb_full = dig_empty + 2;
   uint64_t* rb_empty = rb_full + 1;
   uint64_t* lb_full = rb_empty + 1;
   uint64_t* lb_empty = lb_full + 1;
@@ -255,8 +284,10 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], kSplitW);
     }
-    mbar_init(dig_full, kSplitW);
-    mbar_init(dig_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&dig_full[b], kSplitW);
+      mbar_init(&dig_empty[b], 1);
+    }
     mbar_init(rb_full, 1);
     mbar_init(rb_empty, 1);
     mbar_init(lb_full, 1);
@@ -287,15 +318,16 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     if (lane == 0) {
       const uint64_t pol_y = policy_evict_first(), pol_k = policy_evict_last();
       const int nslots = n * 8;
-      // Boxes wholly outside Y are not requested (the split reads them as zeros).
+      // Slot q = (tile k, row chunk c): q = 8 k + c, one box of 16 rows i x 128
+      // columns j (128-byte swizzle).  Boxes wholly outside Y are not requested
+      // (the split reads them as zeros).
       auto issue_raw = [&](int q) {
-        const int k = q >> 3, s8 = q & 7, slot = q % C::kRaw;
+        const int k = q >> 3, c = q & 7, slot = q % C::kRaw;
         const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
-        unsigned char* dst = raw + slot * kRawSlot;
-        const int j = static_cast<int>(ct * 128 + 16 * s8), i = static_cast<int>(rb * 128);
-        const int nbox = j >= p.K ? 0 : min(8, static_cast<int>((p.J - i + 15) / 16));
-        mbar_arrive_tx(&raw_full[slot], nbox * 2048);
-        for (int c = 0; c < nbox; ++c) tma_2d(dst + c * 2048, &ymap, i + 16 * c, j, &raw_full[slot], pol_y);
+        const int j = static_cast<int>(ct * 128), i = static_cast<int>(rb * 128 + 16 * c);
+        const bool live = j < p.K && i < p.J;
+        mbar_arrive_tx(&raw_full[slot], live ? kRawSlot : 0);
+        if (live) tma_2d(raw + slot * kRawSlot, &ymap, i, j, &raw_full[slot], pol_y);
       };
       const int early = nslots < C::kRaw ? nslots : C::kRaw;
       for (int q = 0; q < early; ++q) issue_raw(q);  // Y does not depend on the predecessor
@@ -324,6 +356,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         if (q < nslots && mbar_test(&raw_empty[q % C::kRaw], ((q / C::kRaw) - 1) & 1)) {
           issue_raw(q);
           ++q;
+        } else {
+          __nanosleep(64);  // nothing to issue: leave the issue slots to the split warps
         }
       }
     }
@@ -333,81 +367,109 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       const uint32_t dg = smem_u32(dig), lb = smem_u32(lbuf);
       int64_t cur_rb = -1;
       int m = 0;
+      int seg = 0, pos = 0;  // right-accumulator segment and position in it
       for (int k = 0; k < n; ++k) {
         const int64_t tile = a0 + k, rb = tile / nCT;
         const bool last_of_rb = (k == n - 1) || ((tile + 1) / nCT != rb);
-        TWAIT(0, dig_full, k & 1, 4, k);
-        TWAIT(1, rb_full, k & 1, 5, k);
-        if (k > 0) TWAIT(2, accR_empty, (k - 1) & 1, 6, k);
-        tc_fence_after();
-        const uint32_t rbb = smem_u32(rbuf);
+        const bool send = seg_end(tile, k, n, nCT, pos);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {  // half tile h: columns j in [64 h, 64 h + 64)
+          const int hb = C::kNB == 2 ? h : 0, u = C::kNB == 2 ? k : 2 * k + h;  // buffer, its use
+          TWAIT(0, &dig_full[hb], u & 1, 4, k);
+          if (h == 0) {
+            TWAIT(1, rb_full, k & 1, 5, k);
+            if (pos == 0 && seg > 0) TWAIT(2, accR_empty, (seg - 1) & 1, 6, seg);
+          }
+          tc_fence_after();
+          const uint32_t db = dg + hb * kHalf, rbb = smem_u32(rbuf) + h * 64;
+          // right: M = 128 rows i, K = this half's 64 columns (2 steps of 32 rows of the plane)
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
+          for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
-          for (int a = 0; a < kPl; ++a)
-            mma_i8(tmem + a * N, sdesc(dg + a * kPlane + ks * 4096, 16384, 1024), sdesc(rbb + ks * 32, 16, 1024),
-                   idesc_i8(true, N * (kPl - a)), (ks > 0 || a > 0) ? 1u : 0u);
-        umma_commit(accR_full);
-        umma_commit(rb_empty);
-        if (rb != cur_rb) {
-          TWAIT(3, lb_full, m & 1, 7, m);
-          cur_rb = rb;
-          ++m;
+            for (int a = 0; a < kPl; ++a)
+              if (!(p.knobs & 8)) mma_i8(tmem + a * N, sdesc(db + a * kHalfPlane + ks * 4096, 16384, 1024),
+                     sdesc(rbb + ks * 32, 16, 1024), idesc_i8(true, N * (kPl - a), 128),
+                     (ks > 0 || a > 0 || h > 0 || pos > 0) ? 1u : 0u);
+          if (h == 1) {
+            if (send) umma_commit(accR_full);
+            umma_commit(rb_empty);
+          }
+          if (h == 0) {
+            if (rb != cur_rb) {
+              TWAIT(3, lb_full, m & 1, 7, m);
+              cur_rb = rb;
+              ++m;
+            }
+            if (k > 0) TWAIT(3, accL_empty, (k - 1) & 1, 8, k);
+            tc_fence_after();
+          }
+          // left: M = 64 (this half's columns j; TMEM lanes 16 h .. +15 of each quarter), K = 128 rows i
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+            for (int a = 0; a < kPl; ++a)
+              if (!(p.knobs & 8)) mma_i8(tmem + (static_cast<uint32_t>(16 * h) << 16) + kPl * N + a * N,
+                     sdesc(db + a * kHalfPlane + ks * 32, 16, 1024), sdesc(lb + ks * 32, 16, 1024),
+                     idesc_i8(false, N * (kPl - a), 64), (ks > 0 || a > 0) ? 1u : 0u);
+          umma_commit(&dig_empty[hb]);
         }
-        if (k > 0) TWAIT(3, accL_empty, (k - 1) & 1, 8, k);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-#pragma unroll
-          for (int a = 0; a < kPl; ++a)
-            mma_i8(tmem + kPl * N + a * N, sdesc(dg + a * kPlane + ks * 32, 16, 1024), sdesc(lb + ks * 32, 16, 1024),
-                   idesc_i8(false, N * (kPl - a)), (ks > 0 || a > 0) ? 1u : 0u);
         umma_commit(accL_full);
-        umma_commit(dig_empty);
         if (last_of_rb) umma_commit(lb_empty);
+        if (send) {
+          ++seg;
+          pos = 0;
+        } else {
+          ++pos;
+        }
       }
     }
     __syncwarp();
   } else if (warp < kSplitW) {
     // ------------------------------------------------------------------ split
-    // Every split warp takes part in every raw slot (each slot's fills are then
-    // observed in order by all its waiters).  Thread = (row j = jj, 16-row chunk c,
-    // half h): 8 values i = 16 c + 8 h .. +7 -> 8 bytes of each digit plane; a
-    // half-warp (8 rows x 2 halves) stores 128 conflict-free bytes.
-    const int jj = (lane & 7) + 8 * (warp & 1), h = (lane >> 3) & 1, c = (lane >> 4) + 2 * (warp >> 1);
+    // All eight warps share every raw slot (16 rows i x 128 columns j), so each
+    // slot's fills are observed in order by all its waiters.  Thread = (column j,
+    // half hh of the 16-row chunk): 8 values -> 8 bytes of each digit plane in the
+    // half-tile buffer of column j; a half-warp stores 128 conflict-free bytes.
+    const int j = 16 * warp + (lane & 7) + 8 * (lane >> 4), hh = (lane >> 3) & 1;
+    const int hb = j >> 6;
     if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 1;
     pdl_wait();
     if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 2;
     const double sy = p.yscale[0];
-    const uint32_t dg = smem_u32(dig);
-    const int sw = ((c ^ (jj & 7)) << 4) + 8 * h;
+    const uint32_t row0 = smem_u32(dig) + hb * kHalf + (j & 63) * 128 + 8 * hh;
     for (int k = 0; k < n; ++k) {
       const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
-      const bool row_live = rb * 128 + 16 * c < p.J;
+      const bool col_live = ct * 128 < p.K;
 #pragma unroll 1
-      for (int s8 = 0; s8 < 8; ++s8) {
-        const int q = k * 8 + s8, slot = q % C::kRaw;
+      for (int c = 0; c < 8; ++c) {
+        const int q = k * 8 + c, slot = q % C::kRaw;
         TWAIT(0, &raw_full[slot], (q / C::kRaw) & 1, 9, q);
-        const unsigned char* box = raw + slot * kRawSlot + c * 2048 + jj * 128;
-        const bool live = row_live && ct * 128 + 16 * s8 < p.K;  // the box was requested
+        const unsigned char* box = raw + slot * kRawSlot + j * 128;
+        const bool rd = col_live && rb * 128 + 16 * c < p.J && !(p.knobs & 2);  // the box was requested
         double2 v[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-          v[t] = live ? *reinterpret_cast<const double2*>(box + (((4 * h + t) ^ (jj & 7)) << 4)) : make_double2(0.0, 0.0);
+          v[t] = rd ? *reinterpret_cast<const double2*>(box + (((4 * hh + t) ^ (j & 7)) << 4))
+                    : make_double2(0.0, 0.0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&raw_empty[slot]);
         uint32_t w0[6], w1[6];
         pack4(v[0].x, v[0].y, v[1].x, v[1].y, sy, w0);
         pack4(v[2].x, v[2].y, v[3].x, v[3].y, sy, w1);
-        if (s8 == 0 && k > 0) TWAIT(1, dig_empty, (k - 1) & 1, 10, k);
-        const uint32_t row = dg + (16 * s8 + jj) * 128 + sw;
+        if (c == 0 && k > 0) TWAIT(1, &dig_empty[hb], (k - 1) & 1, 10, k);
+        const uint32_t row = row0 + ((c ^ (j & 7)) << 4);
+        if (!(p.knobs & 1)) {  // experiment knob: stream only
 #pragma unroll
-        for (int kk = 0; kk < kPl; ++kk)  // byte k -> top-first plane 5 - k
-          st_shared_v2(row + (kPl - 1 - kk) * kPlane, w0[kk], w1[kk]);
+          for (int kk = 0; kk < kPl; ++kk)  // byte k -> top-first plane 5 - k
+            st_shared_v2(row + (kPl - 1 - kk) * kHalfPlane, w0[kk], w1[kk]);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(dig_full);
+      if (lane == 0) {  // warps 0-3 hold half 0, warps 4-7 half 1
+        mbar_arrive(&dig_full[0]);
+        mbar_arrive(&dig_full[1]);
+      }
     }
   } else {
     // ------------------------------------------------------------------ drain
@@ -420,31 +482,36 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 #pragma unroll
     for (int r = 0; r < N; ++r) acc[r] = 0.0;
     const int64_t rb0 = a0 / nCT;
+    int seg = 0, pos = 0;
     for (int k = 0; k < n; ++k) {
       const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
       const bool last_of_rb = (k == n - 1) || ((tile + 1) / nCT != rb);
-      // right: running sums over the row block's column tiles
-      TWAIT(0, accR_full, k & 1, 11, k);
+      const bool send = seg_end(tile, k, n, nCT, pos);
+      pos = send ? 0 : pos + 1;
+      // right: the segment's integer sums, once at its end (one scale per column)
+      if (send) {
+      TWAIT(0, accR_full, seg & 1, 11, seg);
+      ++seg;
       __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin
       tc_fence_after();
       const double* wr = p.w_r + ct * N;
 #pragma unroll
       for (int rc = 0; rc < N / 8; ++rc) {
+        if (rc * 8 >= p.R || (p.knobs & 4)) break;  // warp-uniform: columns past the rank are zero
         uint32_t d[kPl][8];
 #pragma unroll
         for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + dd * N + rc * 8, d[dd]);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          double h = static_cast<double>(static_cast<int>(d[0][e]));
-#pragma unroll
-          for (int dd = 1; dd < kPl; ++dd) h = fma(h, 256.0, static_cast<double>(static_cast<int>(d[dd][e])));
+          const double h = horner6(d[0][e], d[1][e], d[2][e], d[3][e], d[4][e], d[5][e]);
           acc[rc * 8 + e] = fma(h, __ldg(wr + rc * 8 + e), acc[rc * 8 + e]);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(accR_empty);
+      }
       if (last_of_rb) {
         double* dst = p.Rpart + (static_cast<int64_t>(cta) * p.slots + (rb - rb0)) * p.RP * 128;
 #pragma unroll
@@ -458,19 +525,19 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin
       tc_fence_after();
       const double* wl = p.w_l + rb * N;
-      const int64_t j = ct * 128 + row;
+      // M = 64 halves: column 64 h + 16 q + l lives in lane 32 q + 16 h + l
+      const int64_t j = ct * 128 + 64 * (lane >> 4) + 16 * qd + (lane & 15);
       double* lout = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K + j;
 #pragma unroll
       for (int rc = 0; rc < N / 8; ++rc) {
+        if (rc * 8 >= p.R || (p.knobs & 4)) break;
         uint32_t d[kPl][8];
 #pragma unroll
         for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + kPl * N + dd * N + rc * 8, d[dd]);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          double h = static_cast<double>(static_cast<int>(d[0][e]));
-#pragma unroll
-          for (int dd = 1; dd < kPl; ++dd) h = fma(h, 256.0, static_cast<double>(static_cast<int>(d[dd][e])));
+          const double h = horner6(d[0][e], d[1][e], d[2][e], d[3][e], d[4][e], d[5][e]);
           const int r = rc * 8 + e;
           if (r < p.R && j < p.K) lout[static_cast<int64_t>(r) * p.K] = h * __ldg(wl + r);
         }
@@ -500,7 +567,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 // column holds a non-finite value).  CTA = tile, thread = (row q, 8 columns).
 template <int N>
 __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const double* rows, int64_t L, int ldk, int R,
-                                                           const double* yscale, unsigned char* img, double* w) {
+                                                           const double* yscale, unsigned char* img, double* w,
+                                                           int global, const KRSpec spec) {
   __shared__ int ex[N];      // max exponent (frexp) per column, INT_MIN: all zero
   __shared__ int bad[N];     // non-finite seen
   __shared__ double sc[N];
@@ -526,6 +594,31 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const double* rows, i
       atomicMax(&ex[r], m);
       if (nf) bad[r] = 1;
     }
+  }
+  __syncthreads();
+  if (global && threadIdx.x < N) {
+    // one scale per column for every tile: max |KR(:, r)| = prod_m max_i |A_m(i, r)|
+    // (every index combination occurs), so the exponent needs no pass over KR
+    const int r = threadIdx.x;
+    double mx = 1.0;
+    bool fin = true;
+    for (int m = 0; m < spec.n; ++m) {
+      double cm = 0.0;
+      for (int64_t i = 0; i < spec.dims[m]; ++i) {
+        const double a = r < R ? fabs(__ldg(spec.A[m] + i + spec.dims[m] * r)) : 0.0;
+        fin = fin && isfinite(a);
+        cm = a > cm ? a : cm;
+      }
+      mx *= cm;
+    }
+    int e = -2147483647 - 1;
+    if (mx != 0.0 && isfinite(mx)) frexp(mx, &e);
+    if (e != -2147483647 - 1) {
+      int em = ex[r];  // the column's own tiles never exceed the product bound
+      e = e > em ? e : em;
+    }
+    ex[r] = e;
+    if (!fin || !isfinite(mx)) bad[r] = 1;
   }
   __syncthreads();
   if (threadIdx.x < N) {
@@ -617,14 +710,17 @@ int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t 
 }
 
 int launch_kr_digits(const double* rows, int64_t L, int ldk, int R, int N, const double* yscale, void* img, double* w,
-                     cudaStream_t s) {
+                     const KRSpec* global, cudaStream_t s) {
   const dim3 grid(static_cast<unsigned>(ceil_div(L, 128)));
+  KRSpec none{};
+  const KRSpec& spec = global ? *global : none;
+  const int g = global ? 1 : 0;
   if (N == 32)
     launch_k(kr_digits_kernel<32>, grid, dim3(512), 0, s, pdl_enabled(), rows, L, ldk, R, yscale,
-             static_cast<unsigned char*>(img), w);
+             static_cast<unsigned char*>(img), w, g, spec);
   else
     launch_k(kr_digits_kernel<16>, grid, dim3(256), 0, s, pdl_enabled(), rows, L, ldk, R, yscale,
-             static_cast<unsigned char*>(img), w);
+             static_cast<unsigned char*>(img), w, g, spec);
   return 1;
 }
 

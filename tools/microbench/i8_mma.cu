@@ -21,6 +21,11 @@ __host__ __device__ constexpr uint32_t idesc_i8(bool a_mn, int n) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | (static_cast<uint32_t>(n >> 3) << 17) |
          (8u << 24);
 }
+// M = 64 probe: left product for rows j 0..63 only; dump all 128 lanes x N columns
+__host__ __device__ constexpr uint32_t idesc_i8_m(bool a_mn, int n, int m) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
 __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
@@ -106,7 +111,7 @@ __global__ void __launch_bounds__(128, 1) check(int32_t* outR, int32_t* outL) {
 
 // Timing: per "tile" 21 digit pairs x (right 4 K-steps + left 4 K-steps), 6 + 6
 // accumulators of N columns; commit + wait per tile.
-template <int N, bool STACK>
+template <int N, bool STACK, bool HALF = false>
 __global__ void __launch_bounds__(128, 1) timing(int iters, unsigned long long* cyc) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* base = sm + ((1024 - (smem_u32(sm) & 1023)) & 1023);
@@ -134,7 +139,24 @@ __global__ void __launch_bounds__(128, 1) timing(int iters, unsigned long long* 
     const unsigned long long t0 = clock64();
     const uint32_t p = smem_u32(P), br = smem_u32(BR), bl = smem_u32(BL);
     for (int it = 0; it < iters; ++it) {
-      if (STACK) {
+      if (HALF) {
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int a = 0; a < 6; ++a)
+              mma_i8(tmem + a * N, desc(p + a * 16384 + hh * 8192 + ks * 4096, 16384, 1024),
+                     desc(br + hh * 64 + ks * 32, 16, 1024), idesc_i8(true, N * (6 - a)), (ks > 0 || a > 0 || hh > 0) ? 1u : 0u);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+            for (int a = 0; a < 6; ++a)
+              mma_i8(tmem + (static_cast<uint32_t>(16 * hh) << 16) + 6 * N + a * N,
+                     desc(p + a * 16384 + hh * 8192 + ks * 32, 16, 1024), desc(bl + ks * 32, 16, 1024),
+                     idesc_i8_m(false, N * (6 - a), 64), (ks > 0 || a > 0) ? 1u : 0u);
+        }
+      } else if (STACK) {
         // one MMA per Y plane a and K step: B planes b = 0..5-a stacked along N,
         // D starts at diagonal a (column block b -> diagonal a + b)
 #pragma unroll
@@ -171,6 +193,100 @@ __global__ void __launch_bounds__(128, 1) timing(int iters, unsigned long long* 
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
+
+template <int N>
+__global__ void __launch_bounds__(128, 1) probe_m64(int32_t* out) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* base = sm + ((1024 - (smem_u32(sm) & 1023)) & 1023);
+  unsigned char* P = base;
+  unsigned char* BL = P + 16384;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(BL + N * 128);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int e = tid; e < 128 * 128; e += 128) {
+    const int i = e & 127, j = e >> 7;
+    P[swz(j, i)] = static_cast<unsigned char>(val(1, i + 128 * j));
+  }
+  for (int e = tid; e < N * 128; e += 128) {
+    const int k = e & 127, r = e >> 7;
+    BL[swz(r, k)] = static_cast<unsigned char>(val(3, k + 128 * r));
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_u32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *slot;
+  // zero all 128 lanes x 2N columns first
+  {
+    uint32_t z = 0;
+    for (int c = 0; c < 2 * N; ++c)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c), "r"(z));
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (tid == 0) {
+    const uint32_t p = smem_u32(P), bl = smem_u32(BL);
+    for (int ks = 0; ks < 4; ++ks)
+      mma_i8(tmem, desc(p + ks * 32, 16, 1024), desc(bl + ks * 32, 16, 1024), idesc_i8_m(false, N, 64), ks > 0);
+    // second half rows 64..127 into columns N.. (same lanes as the first)
+    for (int ks = 0; ks < 4; ++ks)
+      mma_i8(tmem + (16u << 16) + N, desc(p + 8192 + ks * 32, 16, 1024), desc(bl + ks * 32, 16, 1024), idesc_i8_m(false, N, 64), ks > 0);
+    commit(bar);
+  }
+  mbar_wait(bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  for (int c = 0; c < 2 * N; ++c) {
+    uint32_t v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(v)
+                 : "r"(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    out[tid * 2 * N + c] = static_cast<int32_t>(v);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tmem));
+}
+template <int N>
+void run_probe() {
+  int32_t* d;
+  cudaMalloc(&d, 128 * 2 * N * 4);
+  const int smem = 16384 + N * 128 + 64 + 1024;
+  cudaFuncSetAttribute(probe_m64<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  probe_m64<N><<<1, 128, smem>>>(d);
+  std::vector<int32_t> h(128 * 2 * N);
+  cudaMemcpy(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost);
+  std::printf("M=64 probe N=%d: %s\n", N, cudaGetErrorString(cudaDeviceSynchronize()));
+  // expected left value for row j, column r
+  auto want = [](int j, int r) {
+    int64_t s = 0;
+    for (int k = 0; k < 128; ++k) s += static_cast<int64_t>(val(1, k + 128 * j)) * val(3, k + 128 * r);
+    return s;
+  };
+  // for each lane and column block (0: rows 0..63 MMA, 1: rows 64..127 MMA) find the matching row
+  for (int blk = 0; blk < 2; ++blk) {
+    std::printf(" block %d lanes->rows:", blk);
+    for (int lane = 0; lane < 128; ++lane) {
+      int found = -1, col_off = -1;
+      for (int j = 0; j < 128 && found < 0; ++j)
+        for (int c0 = 0; c0 < N && found < 0; c0 += 8)
+          if (h[lane * 2 * N + blk * N + c0] == want(j, c0) && want(j, c0) != 0) { found = j; col_off = c0; }
+      if (lane % 8 == 0) std::printf(" [%d]", lane);
+      std::printf(" %d", found);
+    }
+    std::printf("\n");
+  }
+}
+
 template <int N>
 int run_check() {
   int32_t *dR, *dL;
@@ -204,19 +320,19 @@ int run_check() {
   return badR + badL;
 }
 
-template <int N, bool STACK>
+template <int N, bool STACK, bool HALF = false>
 void run_timing(int sms) {
   const int smem = 6 * 16384 + 12 * N * 128 + 64 + 1024;
-  cudaFuncSetAttribute(timing<N, STACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(timing<N, STACK, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   unsigned long long* cyc;
   cudaMalloc(&cyc, sms * 8);
   const int iters = 200;
-  timing<N, STACK><<<sms, 128, smem>>>(10, cyc);
+  timing<N, STACK, HALF><<<sms, 128, smem>>>(10, cyc);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  timing<N, STACK><<<sms, 128, smem>>>(iters, cyc);
+  timing<N, STACK, HALF><<<sms, 128, smem>>>(iters, cyc);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -225,18 +341,21 @@ void run_timing(int sms) {
   cudaMemcpy(h.data(), cyc, sms * 8, cudaMemcpyDeviceToHost);
   const double macs_tile = 2.0 * 21 * 128.0 * N * 128;
   std::printf("%s N=%d: %.1f cycles per tile (21 pairs x 2 products, 128x128 tile), %.0f MAC/clk/SM, %.3f us/tile, "
-              "%.1f TOPS chip\n", STACK ? "stacked" : "pairs  ", N, static_cast<double>(h[0]) / iters, macs_tile * iters / h[0], ms * 1e3 / iters,
+              "%.1f TOPS chip\n", HALF ? "halves " : (STACK ? "stacked" : "pairs  "), N, static_cast<double>(h[0]) / iters, macs_tile * iters / h[0], ms * 1e3 / iters,
               2.0 * macs_tile * iters * sms / (ms * 1e-3) / 1e12);
 }
 
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run_probe<32>();
   int bad = run_check<16>() + run_check<32>();
   run_timing<16, false>(sms);
   run_timing<32, false>(sms);
   run_timing<16, true>(sms);
   run_timing<32, true>(sms);
+  run_timing<16, true, true>(sms);
+  run_timing<32, true, true>(sms);
   std::printf("status %s\n", bad ? "MISMATCH" : "ok");
   return 0;
 }
