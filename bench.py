@@ -321,6 +321,15 @@ def run_ours(args, cfg):
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                     "tensor": {"executed_flops": 3 * flops, "achieved_tflops": 3 * tflops,
                                "note": "3 fp16 MMAs per product (hi*hi + lo*hi + hi*lo)"}}
+    elif ctx.last_seed_path() == 1:  # CPDGPU_I8=1: both seeds in one pass on the int8 tensor cores
+        hbm_peak = peaks.get("hbm_gbs", 6539.9)
+        roofline = {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hbm_gbs / hbm_peak, "traffic": traffic,
+                    "kernel": "seed_i8_kernel (K1, fp64 as 6 base-256 digits, tcgen05 kind::i8, both seeds in one pass)",
+                    "kernel_ms": seed_avg, "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                    "tensor": {"executed_int8_macs": 21 * flops / 2 * (16 if R <= 16 else 32) / R,
+                               "note": "21 digit-pair products per fp64 product, rank padded to the MMA block"}}
     else:  # the binding roof is the slower ideal: bytes / HBM peak vs flops / FP64 DMMA peak
         hbm_peak = peaks.get("hbm_gbs", 6539.9)
         fp64 = {"achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": tflops / FP64_PEAK_TFLOPS,

@@ -24,3 +24,11 @@ if python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline >
   ncu --set full --import-source on --clock-control none -k regex:"seed_left_cols|seed_f64" -s 4 -c 2 -o $O/final_seed_c4 -f \
     python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 fi
+# opt-in int8 fused seed: bench lines for the fp64 gradient configs (not the default path)
+for c in c2 c1 c3; do
+  CPDGPU_I8=1 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline > $O/final_i8_$c.json 2>/dev/null
+done
+if CPDGPU_I8=1 python bench.py --config c2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > $O/pre_i8.json 2>&1; then
+  CPDGPU_I8=1 ncu --set full --import-source on --clock-control none -k regex:seed_i8 -s 2 -c 1 -o $O/final_i8_c2 -f \
+    python bench.py --config c2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > /dev/null 2>&1
+fi
