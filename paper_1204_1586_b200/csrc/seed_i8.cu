@@ -572,6 +572,7 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const double* rows, i
   __shared__ int ex[N];      // max exponent (frexp) per column, INT_MIN: all zero
   __shared__ int bad[N];     // non-finite seen
   __shared__ double sc[N];
+  __shared__ unsigned long long mbits[kMaxModes * N];  // factor column max |A_m(:, r)| (global scale)
   __shared__ __align__(16) unsigned char im[kPl * N * 128];
   const int q = threadIdx.x & 127, r0 = (threadIdx.x >> 7) * 8;
   const int64_t tile = blockIdx.x, row = tile * 128 + q;
@@ -579,6 +580,7 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const double* rows, i
     ex[threadIdx.x] = -2147483647 - 1;
     bad[threadIdx.x] = 0;
   }
+  for (int e = threadIdx.x; e < kMaxModes * N; e += blockDim.x) mbits[e] = 0ull;
   pdl_wait();
   __syncthreads();
   double x[8];
@@ -596,29 +598,34 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const double* rows, i
     }
   }
   __syncthreads();
-  if (global && threadIdx.x < N) {
+  if (global) {
     // one scale per column for every tile: max |KR(:, r)| = prod_m max_i |A_m(i, r)|
-    // (every index combination occurs), so the exponent needs no pass over KR
-    const int r = threadIdx.x;
-    double mx = 1.0;
-    bool fin = true;
+    // (every index combination occurs), so the exponent needs no pass over KR;
+    // all threads share the factor scans (column r, row stride parts)
+    const int r = threadIdx.x % N, part = threadIdx.x / N, parts = blockDim.x / N;
     for (int m = 0; m < spec.n; ++m) {
       double cm = 0.0;
-      for (int64_t i = 0; i < spec.dims[m]; ++i) {
-        const double a = r < R ? fabs(__ldg(spec.A[m] + i + spec.dims[m] * r)) : 0.0;
-        fin = fin && isfinite(a);
-        cm = a > cm ? a : cm;
+      const int64_t I = spec.dims[m];
+      if (r < R)
+        for (int64_t i = part; i < I; i += parts) {
+          const double a = fabs(__ldg(spec.A[m] + i + I * r));
+          cm = (a > cm || a != a) ? a : cm;  // NaN sticks
+        }
+      atomicMax(&mbits[m * N + r], static_cast<unsigned long long>(__double_as_longlong(cm)));
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+      double mx = 1.0;
+      for (int m = 0; m < spec.n; ++m) mx *= __longlong_as_double(static_cast<long long>(mbits[m * N + threadIdx.x]));
+      int e = -2147483647 - 1;
+      if (mx != 0.0 && isfinite(mx)) frexp(mx, &e);
+      if (e != -2147483647 - 1) {
+        const int em = ex[threadIdx.x];  // the column's own tiles never exceed the product bound
+        e = e > em ? e : em;
       }
-      mx *= cm;
+      ex[threadIdx.x] = e;
+      if (!isfinite(mx)) bad[threadIdx.x] = 1;
     }
-    int e = -2147483647 - 1;
-    if (mx != 0.0 && isfinite(mx)) frexp(mx, &e);
-    if (e != -2147483647 - 1) {
-      int em = ex[r];  // the column's own tiles never exceed the product bound
-      e = e > em ? e : em;
-    }
-    ex[r] = e;
-    if (!fin || !isfinite(mx)) bad[r] = 1;
   }
   __syncthreads();
   if (threadIdx.x < N) {
