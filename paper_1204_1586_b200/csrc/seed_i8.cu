@@ -66,8 +66,7 @@ constexpr int kWProd = kSplitW + kDrainW;
 constexpr int kWMma = kWProd + 1;
 constexpr int kI8Threads = (kWMma + 1) * 32;
 constexpr int kPl = 6;                       // digit planes
-constexpr int kHalfPlane = 64 * 128;        // bytes per digit plane of a half tile (64 j x 128 i)
-constexpr int kHalf = 6 * kHalfPlane;        // one half-tile digit buffer (48 KB)
+constexpr int kPlane = 128 * 128;            // bytes per digit plane of a tile (128 j x 128 i)
 constexpr int kRawSlot = 16 * 128 * 8;       // 16 KB: one TMA box, 16 rows i x 128 columns j fp64
 constexpr double kMagic = 4503599627370496.0 + 141289400074368.0;  // 2^52 + sum_{k<6} 128 256^k
 // The right accumulators run over a row block's column tiles in TMEM (the right
@@ -81,10 +80,10 @@ __device__ __forceinline__ bool seg_end(int64_t tile, int k, int n, int64_t nCT,
 template <int N>
 struct Cfg {
   static constexpr int kB = kPl * N * 128;  // one Khatri-Rao digit image
-  static constexpr int kNB = 2;                  // half-tile digit buffers (one tile)
   static constexpr int kRaw = N == 32 ? 5 : 6;   // 16 KB TMA boxes (8 KB boxes cap TMA at ~4 TB/s)
-  static constexpr int kCols = N == 32 ? 512 : 256;
-  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kNB * kHalf + 2 * kB + 256;
+  static constexpr int kLB = N == 32 ? 1 : 2;   // left accumulator buffers (TMEM: 6N right + kLB 6N left)
+  static constexpr int kCols = N == 32 ? 512 : 512;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kPl * kPlane + 2 * kB + 256;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -262,40 +261,40 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* raw = base;                               // [kRaw][16 KB]
   unsigned char* dig = raw + C::kRaw * kRawSlot;           // [6][128 j][128 B]
-  unsigned char* rbuf = dig + C::kNB * kHalf;              // [kB] right Khatri-Rao digits (per tile)
+  unsigned char* rbuf = dig + kPl * kPlane;               // [kB] right Khatri-Rao digits (per tile)
   unsigned char* lbuf = rbuf + C::kB;                      // [kB] left Khatri-Rao digits (per row block)
   uint64_t* bars = reinterpret_cast<uint64_t*>(lbuf + C::kB);
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + C::kRaw;
-  uint64_t* dig_full = raw_empty + C::kRaw;  // [2] half-tile digit buffers
-  uint64_t* dig_empty = dig_full + 2;        // [2]
-  uint64_t* rb_full = dig_empty + 2;
+  uint64_t* dig_full = raw_empty + C::kRaw;  // [4] row chunks 2 ks, 2 ks + 1 of the tile split
+  uint64_t* dig_empty = dig_full + 4;        // tile's digits consumed
+  uint64_t* rb_full = dig_empty + 1;
   uint64_t* rb_empty = rb_full + 1;
   uint64_t* lb_full = rb_empty + 1;
   uint64_t* lb_empty = lb_full + 1;
   uint64_t* accR_full = lb_empty + 1;
   uint64_t* accR_empty = accR_full + 1;
-  uint64_t* accL_full = accR_empty + 1;
-  uint64_t* accL_empty = accL_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accL_empty + 1);
+  uint64_t* accL_full = accR_empty + 1;  // [2]
+  uint64_t* accL_empty = accL_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accL_empty + 2);
 
   if (tid == 0) {
     for (int s = 0; s < C::kRaw; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], kSplitW);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&dig_full[b], kSplitW);
-      mbar_init(&dig_empty[b], 1);
-    }
+    for (int b = 0; b < 4; ++b) mbar_init(&dig_full[b], kSplitW);
+    mbar_init(dig_empty, 1);
     mbar_init(rb_full, 1);
     mbar_init(rb_empty, 1);
     mbar_init(lb_full, 1);
     mbar_init(lb_empty, 1);
     mbar_init(accR_full, 1);
     mbar_init(accR_empty, kDrainW);
-    mbar_init(accL_full, 1);
-    mbar_init(accL_empty, kDrainW);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accL_full[b], 1);
+      mbar_init(&accL_empty[b], kDrainW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == kWMma) {
@@ -372,48 +371,42 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         const int64_t tile = a0 + k, rb = tile / nCT;
         const bool last_of_rb = (k == n - 1) || ((tile + 1) / nCT != rb);
         const bool send = seg_end(tile, k, n, nCT, pos);
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {  // half tile h: columns j in [64 h, 64 h + 64)
-          const int hb = C::kNB == 2 ? h : 0, u = C::kNB == 2 ? k : 2 * k + h;  // buffer, its use
-          TWAIT(0, &dig_full[hb], u & 1, 4, k);
-          if (h == 0) {
-            TWAIT(1, rb_full, k & 1, 5, k);
-            if (pos == 0 && seg > 0) TWAIT(2, accR_empty, (seg - 1) & 1, 6, seg);
-          }
-          tc_fence_after();
-          const uint32_t db = dg + hb * kHalf, rbb = smem_u32(rbuf) + h * 64;
-          // right: M = 128 rows i, K = this half's 64 columns (2 steps of 32 rows of the plane)
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-            for (int a = 0; a < kPl; ++a)
-              if (!(p.knobs & 8)) mma_i8(tmem + a * N, sdesc(db + a * kHalfPlane + ks * 4096, 16384, 1024),
-                     sdesc(rbb + ks * 32, 16, 1024), idesc_i8(true, N * (kPl - a), 128),
-                     (ks > 0 || a > 0 || h > 0 || pos > 0) ? 1u : 0u);
-          if (h == 1) {
-            if (send) umma_commit(accR_full);
-            umma_commit(rb_empty);
-          }
-          if (h == 0) {
-            if (rb != cur_rb) {
-              TWAIT(3, lb_full, m & 1, 7, m);
-              cur_rb = rb;
-              ++m;
-            }
-            if (k > 0) TWAIT(3, accL_empty, (k - 1) & 1, 8, k);
-            tc_fence_after();
-          }
-          // left: M = 64 (this half's columns j; TMEM lanes 16 h .. +15 of each quarter), K = 128 rows i
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-#pragma unroll
-            for (int a = 0; a < kPl; ++a)
-              if (!(p.knobs & 8)) mma_i8(tmem + (static_cast<uint32_t>(16 * h) << 16) + kPl * N + a * N,
-                     sdesc(db + a * kHalfPlane + ks * 32, 16, 1024), sdesc(lb + ks * 32, 16, 1024),
-                     idesc_i8(false, N * (kPl - a), 64), (ks > 0 || a > 0) ? 1u : 0u);
-          umma_commit(&dig_empty[hb]);
+        // left: M = 128 columns j, K = rows i, one 32-row step as soon as the split
+        // has delivered its two 16-row chunks (overlaps this tile's split)
+        if (rb != cur_rb) {
+          TWAIT(3, lb_full, m & 1, 7, m);
+          cur_rb = rb;
+          ++m;
         }
-        umma_commit(accL_full);
+        const int lbk = k % C::kLB, lu = k / C::kLB;  // left buffer, its use
+        if (lu > 0) TWAIT(3, &accL_empty[lbk], (lu - 1) & 1, 8, k);
+#pragma unroll 1
+        for (int ks = 0; ks < 4; ++ks) {
+          TWAIT(0, &dig_full[ks], k & 1, 4, k);
+          tc_fence_after();
+#pragma unroll
+          for (int a = 0; a < kPl; ++a)
+            if (!(p.knobs & 8))
+              mma_i8(tmem + (1 + lbk) * kPl * N + a * N, sdesc(dg + a * kPlane + ks * 32, 16, 1024),
+                     sdesc(lb + ks * 32, 16, 1024),
+                     idesc_i8(false, N * (kPl - a), 128), (ks > 0 || a > 0) ? 1u : 0u);
+        }
+        // right: M = 128 rows i, K = the tile's 128 columns (rows of the plane), after the split
+        TWAIT(1, rb_full, k & 1, 5, k);
+        if (pos == 0 && seg > 0) TWAIT(2, accR_empty, (seg - 1) & 1, 6, seg);
+        tc_fence_after();
+        const uint32_t rbb = smem_u32(rbuf);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+          for (int a = 0; a < kPl; ++a)
+            if (!(p.knobs & 8))
+              mma_i8(tmem + a * N, sdesc(dg + a * kPlane + ks * 4096, 16384, 1024), sdesc(rbb + ks * 32, 16, 1024),
+                     idesc_i8(true, N * (kPl - a), 128), (ks > 0 || a > 0 || pos > 0) ? 1u : 0u);
+        if (send) umma_commit(accR_full);
+        umma_commit(rb_empty);
+        umma_commit(dig_empty);
+        umma_commit(&accL_full[lbk]);
         if (last_of_rb) umma_commit(lb_empty);
         if (send) {
           ++seg;
@@ -431,44 +424,52 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     // half hh of the 16-row chunk): 8 values -> 8 bytes of each digit plane in the
     // half-tile buffer of column j; a half-warp stores 128 conflict-free bytes.
     const int j = 16 * warp + (lane & 7) + 8 * (lane >> 4), hh = (lane >> 3) & 1;
-    const int hb = j >> 6;
     if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 1;
     pdl_wait();
     if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 2;
     const double sy = p.yscale[0];
-    const uint32_t row0 = smem_u32(dig) + hb * kHalf + (j & 63) * 128 + 8 * hh;
+    const uint32_t row0 = smem_u32(dig) + j * 128 + 8 * hh;
     for (int k = 0; k < n; ++k) {
       const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
       const bool col_live = ct * 128 < p.K;
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        const int q = k * 8 + c, slot = q % C::kRaw;
-        TWAIT(0, &raw_full[slot], (q / C::kRaw) & 1, 9, q);
-        const unsigned char* box = raw + slot * kRawSlot + j * 128;
-        const bool rd = col_live && rb * 128 + 16 * c < p.J && !(p.knobs & 2);  // the box was requested
-        double2 v[4];
+      for (int ks = 0; ks < 4; ++ks) {  // row chunks c = 2 ks, 2 ks + 1 together (two slots in flight)
+        double2 v[2][4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-          v[t] = rd ? *reinterpret_cast<const double2*>(box + (((4 * hh + t) ^ (j & 7)) << 4))
-                    : make_double2(0.0, 0.0);
+        for (int e = 0; e < 2; ++e) {
+          const int c = 2 * ks + e, q = k * 8 + c, slot = q % C::kRaw;
+          TWAIT(0, &raw_full[slot], (q / C::kRaw) & 1, 9, q);
+          const unsigned char* box = raw + slot * kRawSlot + j * 128;
+          const bool rd = col_live && rb * 128 + 16 * c < p.J && !(p.knobs & 2);  // the box was requested
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            v[e][t] = rd ? *reinterpret_cast<const double2*>(box + (((4 * hh + t) ^ (j & 7)) << 4))
+                         : make_double2(0.0, 0.0);
+        }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&raw_empty[slot]);
-        uint32_t w0[6], w1[6];
-        pack4(v[0].x, v[0].y, v[1].x, v[1].y, sy, w0);
-        pack4(v[2].x, v[2].y, v[3].x, v[3].y, sy, w1);
-        if (c == 0 && k > 0) TWAIT(1, &dig_empty[hb], (k - 1) & 1, 10, k);
-        const uint32_t row = row0 + ((c ^ (j & 7)) << 4);
+        if (lane == 0) {
+          mbar_arrive(&raw_empty[(k * 8 + 2 * ks) % C::kRaw]);
+          mbar_arrive(&raw_empty[(k * 8 + 2 * ks + 1) % C::kRaw]);
+        }
+        uint32_t w[2][2][6];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          pack4(v[e][0].x, v[e][0].y, v[e][1].x, v[e][1].y, sy, w[e][0]);
+          pack4(v[e][2].x, v[e][2].y, v[e][3].x, v[e][3].y, sy, w[e][1]);
+        }
+        if (ks == 0 && k > 0) TWAIT(1, dig_empty, (k - 1) & 1, 10, k);
         if (!(p.knobs & 1)) {  // experiment knob: stream only
 #pragma unroll
-          for (int kk = 0; kk < kPl; ++kk)  // byte k -> top-first plane 5 - k
-            st_shared_v2(row + (kPl - 1 - kk) * kHalfPlane, w0[kk], w1[kk]);
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t row = row0 + (((2 * ks + e) ^ (j & 7)) << 4);
+#pragma unroll
+            for (int kk = 0; kk < kPl; ++kk)  // byte k -> top-first plane 5 - k
+              st_shared_v2(row + (kPl - 1 - kk) * kPlane, w[e][0][kk], w[e][1][kk]);
+          }
         }
-      }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {  // warps 0-3 hold half 0, warps 4-7 half 1
-        mbar_arrive(&dig_full[0]);
-        mbar_arrive(&dig_full[1]);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the left MMAs of step ks may go
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dig_full[ks]);
       }
     }
   } else {
@@ -521,19 +522,19 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         }
       }
       // left: this tile's columns, complete over its 128 rows
-      TWAIT(1, accL_full, k & 1, 12, k);
+      const int lbk = k % C::kLB, lu = k / C::kLB;
+      TWAIT(1, &accL_full[lbk], lu & 1, 12, k);
       __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin
       tc_fence_after();
       const double* wl = p.w_l + rb * N;
-      // M = 64 halves: column 64 h + 16 q + l lives in lane 32 q + 16 h + l
-      const int64_t j = ct * 128 + 64 * (lane >> 4) + 16 * qd + (lane & 15);
+      const int64_t j = ct * 128 + row;  // M = 128: TMEM lane = column
       double* lout = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K + j;
 #pragma unroll
       for (int rc = 0; rc < N / 8; ++rc) {
         if (rc * 8 >= p.R || (p.knobs & 4)) break;
         uint32_t d[kPl][8];
 #pragma unroll
-        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + kPl * N + dd * N + rc * 8, d[dd]);
+        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + (1 + lbk) * kPl * N + dd * N + rc * 8, d[dd]);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(accL_empty);
+      if (lane == 0) mbar_arrive(&accL_empty[lbk]);
     }
   }
   if (p.trace && lane == 0) {
