@@ -543,8 +543,16 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
   // int8 fused seed: one rank chunk of <= 32 columns, both seeds, Y rows 16-byte
   // aligned for the 2-D TMA view
   pl.i8.ok = false;
-  const char* i8env = std::getenv("CPDGPU_I8");  // "1": fused fp64 seed on the int8 tensor cores
-  if (i8env && i8env[0] == '1' && pl.chunks.size() == 1 && pl.p + 1 <= pl.N && Jp % 2 == 0 &&
+  // Default: the int8 pass where it measured faster than the DMMA pass on B200 (large
+  // tensors whose 128 x 128 tiles waste <= 10 % of either side: c2, c3; not c1's
+  // 200-row view); CPDGPU_I8=1 / 0 forces it on / off.
+  const char* i8env = std::getenv("CPDGPU_I8");
+  const auto waste = [](int64_t L) {
+    return static_cast<double>(cpdgpu::ceil_div(L, 128) * 128 - L) / static_cast<double>(L);
+  };
+  const bool i8_want = i8env ? i8env[0] == '1'
+                             : (pl.J[pl.N] >= (int64_t{8} << 20) && waste(Jp) <= 0.10 && waste(Kp) <= 0.10);
+  if (i8_want && pl.chunks.size() == 1 && pl.p + 1 <= pl.N && Jp % 2 == 0 &&
       Jp < (1LL << 31) && Kp < (1LL << 31)) {
     Plan::I8& g = pl.i8;
     const Plan::Chunk& c = pl.chunks[0];
@@ -858,15 +866,14 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
 }
 
 // Both fp64 seeds in one pass on the int8 tensor cores: Khatri-Rao digit images
-// of both sides (from the prologue's rows), then the fused pass.
+// of both sides (one launch, from the sorted factors), then the fused pass.
 void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
   cudaStream_t s = ctx->stream;
   Plan::I8& g = pl.i8;
   Plan::Chunk& c = pl.chunks[0];
   const double* ys = pl.tensor->yscale8.d();
-  const KRSpec right = pl.spec(pl.p + 1, pl.N, c.r0);
-  ctx->launches += cpdgpu::launch_kr_digits(c.KRr->d(), pl.Kp, c.sp.LDK, c.Rc, g.N, ys, g.img_r.p, g.w_r.d(), &right, s);
-  ctx->launches += cpdgpu::launch_kr_digits(c.KRl->d(), pl.Jp, c.sp.LDK, c.Rc, g.N, ys, g.img_l.p, g.w_l.d(), nullptr, s);
+  ctx->launches += cpdgpu::launch_kr_digits(pl.spec(pl.p + 1, pl.N, c.r0), pl.Kp, pl.spec(1, pl.p, c.r0), pl.Jp, c.Rc,
+                                            g.N, ys, g.img_r.p, g.w_r.d(), g.img_l.p, g.w_l.d(), s);
   cpdgpu::SeedI8Params q{};
   q.J = pl.Jp;
   q.K = pl.Kp;
@@ -1499,7 +1506,8 @@ void sweep_body(cpdgpu_ctx* ctx, Plan& pl, const ModeCallback& after) {
 // each call patches the prologue node (input factors, output pointers).
 void run_gradient(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_base) {
   const bool left = pl.p + 1 <= pl.N;
-  cpdgpu::Prologue pr = grad_prologue(pl, fin, gout_base, left ? 3 : 1);
+  // the int8 seed builds its Khatri-Rao digits from the sorted factors itself
+  cpdgpu::Prologue pr = grad_prologue(pl, fin, gout_base, pl.i8.on ? 0 : (left ? 3 : 1));
   pr.tl = ctx->tl_ptr();
   timeline_reset(ctx);
   struct PrintAtExit {

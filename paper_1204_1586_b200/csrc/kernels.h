@@ -83,10 +83,10 @@ size_t seed_i8_smem_bytes(int N);
 // ymap: Y (dim0 J, dim1 K) fp64, box 16 x 128, 128-byte swizzle
 int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s);
 // Khatri-Rao rows [L][ldk] -> digit images [ceil(L / 128)][6][N][128] + weights [.][N]
-// global != nullptr: one scale per column for all tiles, from the factor column
-// maxima of the Khatri-Rao range (the right side: its sums run across tiles)
-int launch_kr_digits(const double* rows, int64_t L, int ldk, int R, int N, const double* yscale, void* img, double* w,
-                     const KRSpec* global, cudaStream_t s);
+// Khatri-Rao digit images [tiles][6][N][128] + column weights [tiles][N] of both
+// sides, from the factors (right: K_p rows, left: J_p rows; one launch)
+int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N,
+                     const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, cudaStream_t s);
 // fp64 tensor scale record [2^(46-eY), eY, max|Y|, sum|Y|]; scratch >= 16 bytes
 int launch_y_scale_f64(const double* y, int64_t n, void* scratch, double* out, int num_sms, cudaStream_t s);
 

@@ -11,9 +11,9 @@
 // split into six balanced base-256 digits and every digit product is exact.
 //
 // Encoding.  Y carries one power-of-two scale for the whole tensor (2^eY >= max
-// |Y|, cached per tensor version).  The right Khatri-Rao rows carry one scale per
-// rank column for all tiles (the product of the factor column maxima), the left
-// ones one per column and 128-row block.  v = rint(x 2^(46-e)) (|v| <= 2^46) is
+// |Y|, cached per tensor version).  The Khatri-Rao rows of each side carry one
+// scale per rank column for all tiles (the product of the factor column maxima),
+// and their digits are generated straight from the factors (kr_digits_kernel).  v = rint(x 2^(46-e)) (|v| <= 2^46) is
 // v = sum_k d_k 256^k, d_k in [-128, 127], k = 0..5.  One DFMA produces it:
 // fma(x, 2^(46-e), 2^52 + sum_k 128 256^k) has v + sum_k 128 256^k in the low 48
 // mantissa bits, whose bytes are d_k + 128 (xor 0x80 gives the signed digit).
@@ -562,47 +562,31 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   }
 }
 
-// Khatri-Rao rows [L][ldk] (r < R valid) -> per 128-row tile: digit image
-// [6 planes][N rank rows][128 bytes of the tile's rows, 128-byte swizzle] and the
-// per-column weights 2^(eY + e_r - 52) (0 for an all-zero column, NaN when the
-// column holds a non-finite value).  CTA = tile, thread = (row q, 8 columns).
+// Khatri-Rao digit images of both sides in one launch, straight from the sorted
+// factors: CTA = 128-row tile (right tiles first, then left), thread = (row q, 8
+// rank columns).  Every tile of a side shares one scale per column, from the
+// product of the factor column maxima (max |KR(:, r)| = prod_m max_i |A_m(i, r)|:
+// every index combination occurs), so no pass over the Khatri-Rao rows is needed.
+// Output per tile: [6 planes][N rank rows][128 bytes of the tile's rows, 128-byte
+// swizzle] and the column weights 2^(eY + e_r - 52) (0: all-zero column, NaN:
+// non-finite factor entry).
 template <int N>
-__global__ void __launch_bounds__(N * 16) kr_digits_kernel(const double* rows, int64_t L, int ldk, int R,
-                                                           const double* yscale, unsigned char* img, double* w,
-                                                           int global, const KRSpec spec) {
-  __shared__ int ex[N];      // max exponent (frexp) per column, INT_MIN: all zero
-  __shared__ int bad[N];     // non-finite seen
+__global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, int64_t Lr, const KRSpec left,
+                                                           int64_t Ll, int R, int64_t nCT, const double* yscale,
+                                                           unsigned char* img_r, double* w_r, unsigned char* img_l,
+                                                           double* w_l) {
   __shared__ double sc[N];
-  __shared__ unsigned long long mbits[kMaxModes * N];  // factor column max |A_m(:, r)| (global scale)
+  __shared__ unsigned long long mbits[kMaxModes * N];
   __shared__ __align__(16) unsigned char im[kPl * N * 128];
-  const int q = threadIdx.x & 127, r0 = (threadIdx.x >> 7) * 8;
-  const int64_t tile = blockIdx.x, row = tile * 128 + q;
-  if (threadIdx.x < N) {
-    ex[threadIdx.x] = -2147483647 - 1;
-    bad[threadIdx.x] = 0;
-  }
+  const bool is_right = blockIdx.x < nCT;
+  const KRSpec& spec = is_right ? right : left;
+  const int64_t L = is_right ? Lr : Ll, tile = is_right ? blockIdx.x : blockIdx.x - nCT;
+  unsigned char* img = is_right ? img_r : img_l;
+  double* w = is_right ? w_r : w_l;
   for (int e = threadIdx.x; e < kMaxModes * N; e += blockDim.x) mbits[e] = 0ull;
-  pdl_wait();
+  pdl_wait();  // the sorted factors come from the prologue
   __syncthreads();
-  double x[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int r = r0 + e;
-    x[e] = (row < L && r < R) ? rows[row * ldk + r] : 0.0;
-    int ee = -2147483647 - 1;
-    if (x[e] != 0.0) frexp(x[e], &ee);
-    const int m = __reduce_max_sync(0xffffffffu, ee);
-    const unsigned nf = __ballot_sync(0xffffffffu, !isfinite(x[e]));
-    if ((threadIdx.x & 31) == 0) {
-      atomicMax(&ex[r], m);
-      if (nf) bad[r] = 1;
-    }
-  }
-  __syncthreads();
-  if (global) {
-    // one scale per column for every tile: max |KR(:, r)| = prod_m max_i |A_m(i, r)|
-    // (every index combination occurs), so the exponent needs no pass over KR;
-    // all threads share the factor scans (column r, row stride parts)
+  {  // factor column maxima, all threads: column r, rows i = part (mod parts)
     const int r = threadIdx.x % N, part = threadIdx.x / N, parts = blockDim.x / N;
     for (int m = 0; m < spec.n; ++m) {
       double cm = 0.0;
@@ -614,39 +598,33 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const double* rows, i
         }
       atomicMax(&mbits[m * N + r], static_cast<unsigned long long>(__double_as_longlong(cm)));
     }
-    __syncthreads();
-    if (threadIdx.x < N) {
-      double mx = 1.0;
-      for (int m = 0; m < spec.n; ++m) mx *= __longlong_as_double(static_cast<long long>(mbits[m * N + threadIdx.x]));
-      int e = -2147483647 - 1;
-      if (mx != 0.0 && isfinite(mx)) frexp(mx, &e);
-      if (e != -2147483647 - 1) {
-        const int em = ex[threadIdx.x];  // the column's own tiles never exceed the product bound
-        e = e > em ? e : em;
-      }
-      ex[threadIdx.x] = e;
-      if (!isfinite(mx)) bad[threadIdx.x] = 1;
-    }
   }
   __syncthreads();
   if (threadIdx.x < N) {
-    const int r = threadIdx.x, e = ex[r];
-    if (bad[r]) {
-      sc[r] = 0.0;
-      w[tile * N + r] = __longlong_as_double(0x7ff8000000000000ll);
-    } else if (e == -2147483647 - 1) {
+    const int r = threadIdx.x;
+    double mx = 1.0;
+    for (int m = 0; m < spec.n; ++m) mx *= __longlong_as_double(static_cast<long long>(mbits[m * N + r]));
+    if (r >= R || mx == 0.0) {
       sc[r] = 0.0;
       w[tile * N + r] = 0.0;
+    } else if (!isfinite(mx)) {
+      sc[r] = 0.0;
+      w[tile * N + r] = __longlong_as_double(0x7ff8000000000000ll);
     } else {
+      int e;
+      frexp(mx, &e);
       sc[r] = ldexp(1.0, 46 - e);
       w[tile * N + r] = ldexp(1.0, e + static_cast<int>(yscale[1]) - 52);
     }
   }
   __syncthreads();
+  const int q = threadIdx.x & 127, r0 = (threadIdx.x >> 7) * 8;
+  const int64_t row = tile * 128 + q;
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int r = r0 + e;
-    const double u = fma(isfinite(x[e]) ? x[e] : 0.0, sc[r], kMagic);
+    const double x = (row < L && r < R) ? kr_entry(spec, row, r) : 0.0;
+    const double u = fma(isfinite(x) ? x : 0.0, sc[r], kMagic);
     const uint32_t lo = __double2loint(u), hi = __double2hiint(u);
     const int off = r * 128 + ((((q >> 4) ^ (r & 7))) << 4) + (q & 15);
 #pragma unroll
@@ -717,18 +695,16 @@ int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t 
   return 1;
 }
 
-int launch_kr_digits(const double* rows, int64_t L, int ldk, int R, int N, const double* yscale, void* img, double* w,
-                     const KRSpec* global, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>(ceil_div(L, 128)));
-  KRSpec none{};
-  const KRSpec& spec = global ? *global : none;
-  const int g = global ? 1 : 0;
+int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N,
+                     const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, cudaStream_t s) {
+  const int64_t nCT = ceil_div(Kp, 128), nRB = ceil_div(Jp, 128);
+  const dim3 grid(static_cast<unsigned>(nCT + nRB));
   if (N == 32)
-    launch_k(kr_digits_kernel<32>, grid, dim3(512), 0, s, pdl_enabled(), rows, L, ldk, R, yscale,
-             static_cast<unsigned char*>(img), w, g, spec);
+    launch_k(kr_digits_kernel<32>, grid, dim3(512), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale,
+             static_cast<unsigned char*>(img_r), w_r, static_cast<unsigned char*>(img_l), w_l);
   else
-    launch_k(kr_digits_kernel<16>, grid, dim3(256), 0, s, pdl_enabled(), rows, L, ldk, R, yscale,
-             static_cast<unsigned char*>(img), w, g, spec);
+    launch_k(kr_digits_kernel<16>, grid, dim3(256), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale,
+             static_cast<unsigned char*>(img_r), w_r, static_cast<unsigned char*>(img_l), w_l);
   return 1;
 }
 
