@@ -13,7 +13,7 @@ python bench.py --impl reference --steps 5 --warmup 1 > $O/final_ref_c2.json 2>/
 if python bench.py --config c2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > $O/pre.json 2>&1; then
   ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/final_launches_c2.csv \
     python bench.py --config c2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > /dev/null 2>&1
-  ncu --set full --import-source on --clock-control none -k regex:seed_f64 -s 6 -c 1 -o $O/final_seed_c2 -f \
+  ncu --set full --import-source on --clock-control none -k regex:"seed_i8|seed_f64" -s 6 -c 1 -o $O/final_seed_c2 -f \
     python bench.py --config c2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > /dev/null 2>&1
 fi
 if python bench.py --config c5 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > $O/pre5.json 2>&1; then
@@ -24,11 +24,15 @@ if python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline >
   ncu --set full --import-source on --clock-control none -k regex:"seed_left_cols|seed_f64" -s 4 -c 2 -o $O/final_seed_c4 -f \
     python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 fi
-# opt-in int8 fused seed: bench lines for the fp64 gradient configs (not the default path)
-for c in c2 c1 c3; do
-  CPDGPU_I8=1 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline > $O/final_i8_$c.json 2>/dev/null
+# the fp64 DMMA pass on the configs where the int8 pass is the default (comparison lines)
+for c in c2 c3; do
+  CPDGPU_I8=0 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline > $O/final_dmma_$c.json 2>/dev/null
 done
-if CPDGPU_I8=1 python bench.py --config c2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > $O/pre_i8.json 2>&1; then
-  CPDGPU_I8=1 ncu --set full --import-source on --clock-control none -k regex:seed_i8 -s 2 -c 1 -o $O/final_i8_c2 -f \
+if CPDGPU_I8=0 python bench.py --config c2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > $O/pre_dmma.json 2>&1; then
+  CPDGPU_I8=0 ncu --set full --import-source on --clock-control none -k regex:seed_f64 -s 2 -c 1 -o $O/final_dmma_c2 -f \
     python bench.py --config c2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > /dev/null 2>&1
+fi
+if python bench.py --config c3 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > $O/pre3.json 2>&1; then
+  ncu --set full --import-source on --clock-control none -k regex:"seed_i8|seed_f64" -s 2 -c 1 -o $O/final_seed_c3 -f \
+    python bench.py --config c3 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 > /dev/null 2>&1
 fi
