@@ -620,10 +620,25 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
   __syncthreads();
   const int q = threadIdx.x & 127, r0 = (threadIdx.x >> 7) * 8;
   const int64_t row = tile * 128 + q;
+  // the row's mixed-radix digits (first mode fastest, kron.cpp:54-68), once for all columns
+  int64_t off_m[kMaxModes];
+  {
+    int64_t rem = row;
+#pragma unroll 1
+    for (int m = 0; m < spec.n; ++m) {
+      off_m[m] = rem % spec.dims[m];
+      rem /= spec.dims[m];
+    }
+  }
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int r = r0 + e;
-    const double x = (row < L && r < R) ? kr_entry(spec, row, r) : 0.0;
+    double x = 0.0;
+    if (row < L && r < R) {
+      x = 1.0;
+#pragma unroll 1
+      for (int m = 0; m < spec.n; ++m) x *= __ldg(spec.A[m] + off_m[m] + spec.dims[m] * r);
+    }
     const double u = fma(isfinite(x) ? x : 0.0, sc[r], kMagic);
     const uint32_t lo = __double2loint(u), hi = __double2hiint(u);
     const int off = r * 128 + ((((q >> 4) ^ (r & 7))) << 4) + (q & 15);
