@@ -592,9 +592,15 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
       double cm = 0.0;
       const int64_t I = spec.dims[m];
       if (r < R)
-        for (int64_t i = part; i < I; i += parts) {
-          const double a = fabs(__ldg(spec.A[m] + i + I * r));
-          cm = (a > cm || a != a) ? a : cm;  // NaN sticks
+        for (int64_t i0 = part; i0 < I; i0 += 8 * static_cast<int64_t>(parts)) {
+          double a[8];  // eight independent loads in flight
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int64_t i = i0 + u * static_cast<int64_t>(parts);
+            a[u] = i < I ? fabs(__ldg(spec.A[m] + i + I * r)) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cm = (a[u] > cm || a[u] != a[u]) ? a[u] : cm;  // NaN sticks
         }
       atomicMax(&mbits[m * N + r], static_cast<unsigned long long>(__double_as_longlong(cm)));
     }
@@ -630,15 +636,21 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
       rem /= spec.dims[m];
     }
   }
+  double xs[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) xs[e] = (row < L && r0 + e < R) ? 1.0 : 0.0;
+#pragma unroll 1
+  for (int m = 0; m < spec.n; ++m) {  // eight independent loads per mode
+    const double* a = spec.A[m] + off_m[m];
+    const int64_t I = spec.dims[m];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (xs[e] != 0.0) xs[e] *= __ldg(a + I * (r0 + e));
+  }
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int r = r0 + e;
-    double x = 0.0;
-    if (row < L && r < R) {
-      x = 1.0;
-#pragma unroll 1
-      for (int m = 0; m < spec.n; ++m) x *= __ldg(spec.A[m] + off_m[m] + spec.dims[m] * r);
-    }
+    const double x = xs[e];
     const double u = fma(isfinite(x) ? x : 0.0, sc[r], kMagic);
     const uint32_t lo = __double2loint(u), hi = __double2hiint(u);
     const int off = r * 128 + ((((q >> 4) ^ (r & 7))) << 4) + (q & 15);
