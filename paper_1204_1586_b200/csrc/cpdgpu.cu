@@ -1283,7 +1283,13 @@ int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& 
   fuse_l = pl.p + 1 < pl.N && pl.sd[pl.p] <= cpdgpu::kL0MaxRows;
   const int nsides = (fuse_r ? 1 : 0) + (fuse_l ? 1 : 0);
   if (nsides == 0) return 0;
-  const int target = std::max(1, (2 * ctx->num_sms + R * nsides - 1) / (R * nsides));
+  // chunks per (side, r): at least two CTAs per SM, and about 1024 seed rows per CTA
+  // (long reductions like c3's 38416 rows per column gain from more loads in flight)
+  int64_t rows_max = 0;
+  if (fuse_r) rows_max = std::max<int64_t>(rows_max, pl.Jp);
+  if (fuse_l) rows_max = std::max<int64_t>(rows_max, pl.Kp);
+  const int target = static_cast<int>(std::max<int64_t>((2 * ctx->num_sms + R * nsides - 1) / (R * nsides),
+                                                        cpdgpu::ceil_div(rows_max, 1024)));
   auto chunks = [&](cpdgpu::L0Side& sd) {
     int64_t nq = std::min<int64_t>(target, sd.B);
     int64_t bq = cpdgpu::ceil_div(sd.B, nq);
