@@ -52,3 +52,17 @@ def test_slabs_reproduce_unsharded(gpu_ctx, oracle, gdims, R, world, f32):
     for k in range(len(gdims)):
         err = np.linalg.norm(got[k] - want[k]) / np.linalg.norm(want[k])
         assert err <= tol, (k, err)
+
+
+@pytest.mark.parametrize("gdims,R,world", [([32, 34, 36, 40], 12, 2), ([20, 30, 64], 20, 4)])
+def test_int8_slabs_reproduce_unsharded(gpu_ctx, oracle, monkeypatch, gdims, R, world):
+    # the same per-slab calls on the int8 seed path (global pivot, raw frame)
+    monkeypatch.setenv("CPDGPU_I8", "1")
+    factors = [oracle.fill_normal(70 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(gdims)]
+    got = _slab_gradients(gpu_ctx, gdims, R, world, cpd.DIST_NORMAL, cpd.F64, factors)
+    assert gpu_ctx.last_seed_path() == 1
+    yfull = cpd.DenseTensor.generate(gdims, cpd.DIST_NORMAL, seed=3, ctx=gpu_ctx)
+    want, _, _ = oracle.cp_gradient_all(yfull.values(), gdims, factors)
+    for k in range(len(gdims)):
+        err = np.linalg.norm(got[k] - want[k]) / np.linalg.norm(want[k])
+        assert err <= 1e-10, (k, err)
