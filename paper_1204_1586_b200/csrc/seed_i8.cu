@@ -424,8 +424,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     // half hh of the 16-row chunk): 8 values -> 8 bytes of each digit plane in the
     // half-tile buffer of column j; a half-warp stores 128 conflict-free bytes.
     const int j = 16 * warp + (lane & 7) + 8 * (lane >> 4), hh = (lane >> 3) & 1;
-    if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 1;
-    pdl_wait();
+    // no griddepcontrol.wait: the split reads only Y and the tensor's scale record,
+    // which is written before the gradient's launches (bind_i8), and shared memory
     if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 2;
     const double sy = p.yscale[0];
     const uint32_t row0 = smem_u32(dig) + j * 128 + 8 * hh;
@@ -584,7 +584,8 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
   unsigned char* img = is_right ? img_r : img_l;
   double* w = is_right ? w_r : w_l;
   for (int e = threadIdx.x; e < kMaxModes * N; e += blockDim.x) mbits[e] = 0ull;
-  pdl_wait();  // the sorted factors come from the prologue
+  pdl_trigger();  // the seed may launch now: its Y stream does not depend on this kernel
+  pdl_wait();     // the sorted factors come from the prologue
   __syncthreads();
   {  // factor column maxima, all threads: column r, rows i = part (mod parts)
     const int r = threadIdx.x % N, part = threadIdx.x / N, parts = blockDim.x / N;
