@@ -6,6 +6,7 @@
 //   B: box 128 i x 8 j, no swizzle (whole 1 KB column runs per request)
 //   C: 3-D view (16, J/16, K), box 16 x 8 x 8 (same bytes as B, swizzled rows)
 #include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -28,26 +29,35 @@ __device__ __forceinline__ void arrive_tx(unsigned long long* b, unsigned tx) {
 }
 
 template <int MODE>
-__global__ void stream(const __grid_constant__ CUtensorMap map, int J, int K, int stages, long total, int sbytes) {
+__global__ void stream(const __grid_constant__ CUtensorMap map, int J, int K, int stages, long total, int sbytes, int cw, const unsigned char* img, int bulk) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* base = sm + ((1024 - (smem_u32(sm) & 1023)) & 1023);
   unsigned long long* full = (unsigned long long*)(base + stages * sbytes);
   unsigned long long* empty = full + stages;
+  unsigned long long* bfull = empty + stages;
+  unsigned char* bbuf = base + stages * sbytes + 1024;  // bulk image landing area (12 KB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 4); }
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], cw); }
+    mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
   const long a0 = blockIdx.x * total / gridDim.x, a1 = (blockIdx.x + 1) * total / gridDim.x;
   const int n = (int)(a1 - a0);
   const int nCT = (K + 127) / 128;
-  if (warp == 4) {
+  if (warp == cw) {
     if (lane == 0) {
       for (int q = 0; q < n; ++q) {
         const int s = q % stages;
         if (q >= stages) wait(&empty[s], ((q / stages) - 1) & 1);
         const long u = a0 + q;
+        if (bulk && (q & 7) == 0) {  // per-tile 12 KB image from L2 (as seed_i8's Khatri-Rao digits)
+          if (q >= 8) wait(bfull, ((q >> 3) - 1) & 1);
+          arrive_tx(bfull, 12288);
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 12288, [%2];"
+                       ::"r"(smem_u32(bbuf)), "l"(img + ((u >> 3) % 301) * 12288), "r"(smem_u32(bfull)) : "memory");
+        }
         arrive_tx(&full[s], sbytes);
         unsigned dst = smem_u32(base + s * sbytes), bar = smem_u32(&full[s]);
         if (MODE == 0) {  // slot = (tile, half, chunk): c fastest
@@ -83,7 +93,7 @@ __global__ void stream(const __grid_constant__ CUtensorMap map, int J, int K, in
         }
       }
     }
-  } else {
+  } else if (warp < cw) {
     for (int q = 0; q < n; ++q) {
       const int s = q % stages;
       wait(&full[s], (q / stages) & 1);
@@ -97,13 +107,13 @@ int main() {
   PFN_cuTensorMapEncodeTiled enc; cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int J = 3584; const long K = 36000;  // J multiple of 128: no partial tiles
+  const int J = getenv("TJ") ? atoi(getenv("TJ")) : 3584; const long K = getenv("TK") ? atol(getenv("TK")) : 36000;
   double* y; cudaMalloc(&y, (size_t)J * K * 8); cudaMemset(y, 0, (size_t)J * K * 8);
-  const long tiles = (long)(J / 128) * ((K + 127) / 128);
+  const long tiles = (long)((J + 127) / 128) * ((K + 127) / 128);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  struct Cfg { int mode, rows, cols, sw, stages; };
-  Cfg cfgs[] = {{0, 16, 64, 1, 16}, {3, 16, 128, 1, 5}, {3, 16, 128, 1, 8}, {3, 16, 128, 1, 12}, {4, 128, 32, 0, 3},
-                {4, 128, 32, 0, 5}, {1, 128, 8, 0, 16}};
+  struct Cfg { int mode, rows, cols, sw, stages, cw, bulk; };
+  Cfg cfgs[] = {{3, 16, 128, 1, 6, 8, 1}};
+  unsigned char* img; cudaMalloc(&img, 301 * 12288); cudaMemset(img, 0, 301 * 12288);
   for (auto c : cfgs) {
     CUtensorMap map;
     cuuint64_t gd[2] = {(cuuint64_t)J, (cuuint64_t)K}; cuuint64_t gs[1] = {(cuuint64_t)J * 8};
@@ -114,16 +124,16 @@ int main() {
     if (r != CUDA_SUCCESS) { printf("encode failed\n"); continue; }
     const int sbytes = c.rows * c.cols * 8;
     const long nslots = tiles * (131072 / sbytes);
-    const size_t smem = 1024 + (size_t)c.stages * sbytes + 512;
+    const size_t smem = 1024 + (size_t)c.stages * sbytes + 1024 + 12288 + 512;
     auto fn = c.mode == 0 ? stream<0> : (c.mode == 1 ? stream<1> : (c.mode == 3 ? stream<3> : stream<4>));
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
-      fn<<<sms, 160, smem>>>(map, J, (int)K, c.stages, nslots, sbytes);
+      fn<<<sms, 32 * (c.cw + 1), smem>>>(map, J, (int)K, c.stages, nslots, sbytes, c.cw, img, c.bulk);
       cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      if (rep == 1) printf("box %3d x %3d sw %d stages %2d (%3d KB in flight): %7.1f GB/s\n", c.rows, c.cols, c.sw,
-                           c.stages, c.stages * sbytes / 1024, (double)J * K * 8 / ms / 1e6);
+      if (rep == 1) printf("box %3d x %3d sw %d stages %2d (%3d KB in flight) consumers %d bulk %d: %7.1f GB/s\n", c.rows,
+                           c.cols, c.sw, c.stages, c.stages * sbytes / 1024, c.cw, c.bulk, (double)J * K * 8 / ms / 1e6);
     }
   }
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
