@@ -321,7 +321,7 @@ def run_ours(args, cfg):
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                     "tensor": {"executed_flops": 3 * flops, "achieved_tflops": 3 * tflops,
                                "note": "3 fp16 MMAs per product (hi*hi + lo*hi + hi*lo)"}}
-    elif ctx.last_seed_path() == 1:  # CPDGPU_I8=1: both seeds in one pass on the int8 tensor cores
+    elif ctx.last_seed_path() == 1:  # both seeds in one pass on the int8 tensor cores (default for c2, c3)
         hbm_peak = peaks.get("hbm_gbs", 6539.9)
         roofline = {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": hbm_gbs / hbm_peak, "traffic": traffic,

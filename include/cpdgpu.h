@@ -70,7 +70,8 @@ uint64_t cpdgpu_launch_count(const cpdgpu_ctx* ctx);
 int cpdgpu_set_timing(cpdgpu_ctx* ctx, int enabled);
 int cpdgpu_last_seed_ms(cpdgpu_ctx* ctx, double* ms);
 /* Seed path of the most recent hook-free fp64 gradient: 0 = fp64 DMMA pass,
- * 1 = fused pass on the int8 tensor cores (opt-in: CPDGPU_I8=1), 2 = fp32. */
+ * 1 = fused pass on the int8 tensor cores (default for large fp64 tensors; CPDGPU_I8=1/0
+ * forces it on/off), 2 = fp32. */
 int cpdgpu_last_seed_path(const cpdgpu_ctx* ctx);
 
 /* ---- tensors (DenseTensor, dense_tensor.hpp:15-47) -------------------------

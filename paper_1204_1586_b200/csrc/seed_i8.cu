@@ -47,8 +47,9 @@
 //   warp 12     producer: TMA of the raw slots, bulk copies of the Khatri-Rao
 //               digit images (right per tile, left per row block), event loop
 //   warp 13     TMEM allocation and the MMA issue (one lane)
-// Opt-in (CPDGPU_I8=1): measured on B200 it does not yet beat the DMMA pass at
-// the BASELINE configs (DESIGN.md section 5 has the numbers and the analysis).
+// The default for large fp64 gradients with 128 x 128 tiles that waste <= 10 %
+// (c2, c3: 18-22 % faster seeds than the DMMA pass); CPDGPU_I8=1 / 0 forces it on /
+// off (cpdgpu.cu, build_f64_geometry).  DESIGN.md section 5 has the numbers.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 

@@ -1,5 +1,5 @@
 """GPU parity of the fused fp64 seed on the int8 tensor cores (seed_i8.cu,
-opt-in with CPDGPU_I8=1) against the CPU oracle.
+forced with CPDGPU_I8=1; the default only for large tensors) against the CPU oracle.
 
 The int8 path splits every fp64 value into six base-256 digits and keeps the 21
 digit-pair products a + b <= 5; its error is ~1e-13 relative (Frobenius), held
