@@ -3,9 +3,9 @@ forced with CPDGPU_I8=1; the default only for large tensors) against the CPU ora
 
 The int8 path splits every fp64 value into six base-256 digits and keeps the 21
 digit-pair products a + b <= 5; its error is ~1e-13 relative (Frobenius), held
-here to the BASELINE.json fp64 gate of 1e-10 per mode, and to the reference's
-own 1e-12 max-abs-scaled tolerance (test_util.hpp:86-89) on the small fixture
-shapes.  Shapes cover full and ragged 128 x 128 tiles, single-row-block views,
+here to the BASELINE.json fp64 gate of 1e-10 per mode, both as relative
+Frobenius and max-abs-scaled (the reference's own fixture tolerance is 1e-12,
+test_util.hpp:86-89, which the default path keeps: small tensors run DMMA).  Shapes cover full and ragged 128 x 128 tiles, single-row-block views,
 R = 1..32 (both MMA rank blocks), and the fallbacks (odd J_p, non-finite Y).
 """
 import numpy as np
@@ -97,7 +97,7 @@ def test_int8_falls_back_for_wide_dynamic_range(gpu_ctx, oracle, i8_env):
     rng = np.random.default_rng(5)
     dims = (40, 40, 40)
     y = rng.standard_normal(int(np.prod(dims)))
-    y[17] = 1e9  # max |Y| far beyond 2^12 RMS: digits would starve the small entries
+    y[17] = 1e9  # max |Y| far beyond 2^12 x mean |Y|: digits would starve the small entries
     g, want, path = run(gpu_ctx, oracle, dims, 6, 5, values=y)
     assert path == 0
     for a, b in zip(g, want):
