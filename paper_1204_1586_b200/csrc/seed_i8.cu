@@ -44,8 +44,9 @@
 //               fp64 times the column weight 2^(eY + e_r - 52); right sums once
 //               per segment (-> Rpart slot at the row block's end), left per tile
 //               (-> Lpart): the partial layouts the fp64 tail reduces (TI = 128).
-//   warp 12     producer: TMA of the raw slots, bulk copies of the Khatri-Rao
-//               digit images (right per tile, left per row block), event loop
+//   warp 12     producer: lane 0 TMA of the raw slots (no dependency wait), lane
+//               1 bulk copies of the Khatri-Rao digit images (right per tile, left
+//               per row block) after griddepcontrol.wait
 //   warp 13     TMEM allocation and the MMA issue (one lane)
 // The default for large fp64 gradients with 128 x 128 tiles that waste <= 10 %
 // (c2, c3: 18-22 % faster seeds than the DMMA pass); CPDGPU_I8=1 / 0 forces it on /
@@ -145,16 +146,6 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int
     WAIT(bar, par, code, info);                          \
     if (p.trace) tw[idx] += clock64() - t0_;             \
   } while (0)
-// non-blocking phase test
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(done)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return done != 0;
-}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
@@ -315,49 +306,40 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 
   if (warp == kWProd) {
     // ------------------------------------------------------------------ producer
+    // lane 0 streams Y (independent of the preceding kernels, no dependency wait);
+    // lane 1 waits for the Khatri-Rao digit images (griddepcontrol.wait) and loads
+    // them: right per tile, left per row block, each once the MMAs released the last.
     if (lane == 0) {
-      const uint64_t pol_y = policy_evict_first(), pol_k = policy_evict_last();
+      const uint64_t pol_y = policy_evict_first();
       const int nslots = n * 8;
       // Slot q = (tile k, row chunk c): q = 8 k + c, one box of 16 rows i x 128
       // columns j (128-byte swizzle).  Boxes wholly outside Y are not requested
       // (the split reads them as zeros).
-      auto issue_raw = [&](int q) {
+      for (int q = 0; q < nslots; ++q) {
         const int k = q >> 3, c = q & 7, slot = q % C::kRaw;
+        if (q >= C::kRaw) WAIT(&raw_empty[slot], ((q / C::kRaw) - 1) & 1, 3, q);
         const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
         const int j = static_cast<int>(ct * 128), i = static_cast<int>(rb * 128 + 16 * c);
         const bool live = j < p.K && i < p.J;
         mbar_arrive_tx(&raw_full[slot], live ? kRawSlot : 0);
         if (live) tma_2d(raw + slot * kRawSlot, &ymap, i, j, &raw_full[slot], pol_y);
-      };
-      const int early = nslots < C::kRaw ? nslots : C::kRaw;
-      for (int q = 0; q < early; ++q) issue_raw(q);  // Y does not depend on the predecessor
+      }
+    } else if (lane == 1) {
+      const uint64_t pol_k = policy_evict_last();
       pdl_wait();
-      // Event loop: raw slots go out as soon as their ring slot drains; the
-      // Khatri-Rao images (right per tile, left per row block) as soon as the
-      // MMAs released the previous one, without holding up the raw stream.
-      int q = early, kb = 0, m = 0;
+      int m = 0;
       int64_t cur_rb = -1;
-      while (q < nslots || kb < n) {
-        if (kb < n && (kb == 0 || mbar_test(rb_empty, (kb - 1) & 1))) {
-          const int64_t tile = a0 + kb, rb = tile / nCT, ct = tile - rb * nCT;
-          const bool new_rb = rb != cur_rb;
-          if (!new_rb || m == 0 || mbar_test(lb_empty, (m - 1) & 1)) {
-            mbar_arrive_tx(rb_full, C::kB);
-            bulk_load(rbuf, p.img_r + ct * C::kB, C::kB, rb_full, pol_k);
-            if (new_rb) {
-              mbar_arrive_tx(lb_full, C::kB);
-              bulk_load(lbuf, p.img_l + rb * C::kB, C::kB, lb_full, pol_k);
-              cur_rb = rb;
-              ++m;
-            }
-            ++kb;
-          }
-        }
-        if (q < nslots && mbar_test(&raw_empty[q % C::kRaw], ((q / C::kRaw) - 1) & 1)) {
-          issue_raw(q);
-          ++q;
-        } else {
-          __nanosleep(64);  // nothing to issue: leave the issue slots to the split warps
+      for (int k = 0; k < n; ++k) {
+        const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
+        if (k > 0) WAIT(rb_empty, (k - 1) & 1, 1, k);
+        mbar_arrive_tx(rb_full, C::kB);
+        bulk_load(rbuf, p.img_r + ct * C::kB, C::kB, rb_full, pol_k);
+        if (rb != cur_rb) {
+          if (m > 0) WAIT(lb_empty, (m - 1) & 1, 2, m);
+          mbar_arrive_tx(lb_full, C::kB);
+          bulk_load(lbuf, p.img_l + rb * C::kB, C::kB, lb_full, pol_k);
+          cur_rb = rb;
+          ++m;
         }
       }
     }
