@@ -273,6 +273,7 @@ struct Plan {
     bool ok = false;   // geometry built (one rank chunk, both seeds, even J_p)
     bool on = false;   // bound tensor passed the range guard and has a TMA view
     int N = 0;         // MMA rank block (16 or 32)
+    int NL = 0;        // left rank block (24 when R <= 24 < N)
     int64_t nRB = 0, nCT = 0, T = 0;
     int P = 0, slots = 0;
     DevBuf img_r, img_l, w_r, w_l;
@@ -557,6 +558,7 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
     Plan::I8& g = pl.i8;
     const Plan::Chunk& c = pl.chunks[0];
     g.N = c.Rc <= 16 ? 16 : 32;
+    g.NL = cpdgpu::i8_left_block(g.N, c.Rc);
     g.nRB = cpdgpu::ceil_div(Jp, 128);
     g.nCT = cpdgpu::ceil_div(Kp, 128);
     g.T = g.nRB * g.nCT;
@@ -571,7 +573,7 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
       pl.Lpart.ensure(std::max(pl.Lpart.bytes, static_cast<size_t>(g.nRB) * c.Rc * Kp * sizeof(double)));
     const size_t img = static_cast<size_t>(6) * g.N * 128;
     g.img_r.ensure(static_cast<size_t>(g.nCT) * img);
-    g.img_l.ensure(static_cast<size_t>(g.nRB) * img);
+    g.img_l.ensure(static_cast<size_t>(g.nRB) * cpdgpu::i8_left_image_bytes(g.NL));
     g.w_r.ensure(static_cast<size_t>(g.nCT) * g.N * sizeof(double));
     g.w_l.ensure(static_cast<size_t>(g.nRB) * g.N * sizeof(double));
     g.ok = true;
@@ -873,13 +875,14 @@ void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
   Plan::Chunk& c = pl.chunks[0];
   const double* ys = pl.tensor->yscale8.d();
   ctx->launches += cpdgpu::launch_kr_digits(pl.spec(pl.p + 1, pl.N, c.r0), pl.Kp, pl.spec(1, pl.p, c.r0), pl.Jp, c.Rc,
-                                            g.N, ys, g.img_r.p, g.w_r.d(), g.img_l.p, g.w_l.d(), s);
+                                            g.N, g.NL, ys, g.img_r.p, g.w_r.d(), g.img_l.p, g.w_l.d(), s);
   cpdgpu::SeedI8Params q{};
   q.J = pl.Jp;
   q.K = pl.Kp;
   q.R = c.Rc;
   q.RP = c.NT * 8;
   q.N = g.N;
+  q.NL = g.NL;
   q.nRB = g.nRB;
   q.nCT = g.nCT;
   q.T = g.T;

@@ -65,7 +65,7 @@ size_t seed_left_cols_smem_bytes(int NT, int TJ, int stages);
 // left partials: Lpart[(rb * R + r) * K + j] (the fp64 path's formats, TI = 128).
 struct SeedI8Params {
   int64_t J, K;          // J_p, K_p
-  int R, RP, N;          // rank columns, Rpart row stride (8 NT), MMA rank block (16 or 32)
+  int R, RP, N, NL;      // rank columns, Rpart row stride (8 NT), right / left MMA rank blocks
   int64_t nRB, nCT, T;   // 128-row blocks, 128-column tiles, nRB * nCT
   int P, slots;
   const unsigned char* img_r;  // [nCT][6][N][128] Khatri-Rao digits of the view's columns
@@ -79,13 +79,16 @@ struct SeedI8Params {
   unsigned long long* trace;  // CPDGPU_SEED_TRACE: [P][14][6] per-warp wait cycles, total, tiles
   int knobs;                  // CPDGPU_I8_KNOBS experiments (bit 0: no digit stores)
 };
-size_t seed_i8_smem_bytes(int N);
+// left rank block for a right block N and rank R (24 when it lets the left accumulators
+// double-buffer in TMEM), and the left digit image bytes per row block
+int i8_left_block(int N, int R);
+size_t i8_left_image_bytes(int NL);
 // ymap: Y (dim0 J, dim1 K) fp64, box 16 x 128, 128-byte swizzle
 int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s);
 // Khatri-Rao rows [L][ldk] -> digit images [ceil(L / 128)][6][N][128] + weights [.][N]
 // Khatri-Rao digit images [tiles][6][N][128] + column weights [tiles][N] of both
 // sides, from the factors (right: K_p rows, left: J_p rows; one launch)
-int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N,
+int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N, int NL,
                      const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, cudaStream_t s);
 // fp64 tensor scale record [2^(46-eY), eY, max|Y|, sum|Y|]; scratch >= 16 bytes
 int launch_y_scale_f64(const double* y, int64_t n, void* scratch, double* out, int num_sms, cudaStream_t s);

@@ -79,13 +79,23 @@ __device__ __forceinline__ bool seg_end(int64_t tile, int k, int n, int64_t nCT,
   return k == n - 1 || (tile + 1) / nCT != tile / nCT || pos == kSeg - 1;
 }
 
-template <int N>
+// Left digit image of an NL-row rank block: 6 planes of NL rows (+ 8 zero rows when
+// NL = 24, read by the rounded-up stacked MMAs).
+__host__ __device__ constexpr int left_image_bytes(int NL) { return kPl * NL * 128 + (NL == 24 ? 8 * 128 : 0); }
+// stacked N of Y plane a on a product with rank block n (M = 128 needs N % 16 == 0)
+__host__ __device__ constexpr int stacked_n(int n, int a) { return ((n * (kPl - a)) + 15) / 16 * 16; }
+
+template <int N, int NL>
 struct Cfg {
-  static constexpr int kB = kPl * N * 128;  // one Khatri-Rao digit image
-  static constexpr int kRaw = N == 32 ? 5 : 6;   // 16 KB TMA boxes (8 KB boxes cap TMA at ~4 TB/s)
-  static constexpr int kLB = N == 32 ? 1 : 2;   // left accumulator buffers (TMEM: 6N right + kLB 6N left)
-  static constexpr int kCols = N == 32 ? 512 : 512;
-  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kPl * kPlane + 2 * kB + 256;
+  static constexpr int kB = kPl * N * 128;         // right Khatri-Rao digit image
+  static constexpr int kBL = left_image_bytes(NL);  // left image
+  static constexpr int kRaw = N == 32 ? 5 : 6;     // 16 KB TMA boxes (8 KB boxes cap TMA near 4 TB/s)
+  // TMEM: right accumulators 6 N columns, then kLB left buffers of kLS columns
+  // (NL = 24: 6 x 24 + 8 slack columns for the rounded-up stacked N)
+  static constexpr int kLS = NL == 24 ? kPl * NL + 8 : kPl * NL;
+  static constexpr int kLB = (kPl * N + 2 * kLS <= 512) ? 2 : 1;
+  static constexpr int kCols = 512;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kPl * kPlane + kB + kBL + 256;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -239,10 +249,10 @@ __device__ __forceinline__ void pack4(double x0, double x1, double x2, double x3
   w[5] = prmt(g01, g23, 0x7632) ^ 0x80808080u;
 }
 
-template <int N>
+template <int N, int NL>
 __global__ void __launch_bounds__(kI8Threads, 1)
     seed_i8_kernel(const SeedI8Params p, const __grid_constant__ CUtensorMap ymap) {
-  using C = Cfg<N>;
+  using C = Cfg<N, NL>;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x;
   const int64_t a0 = static_cast<int64_t>(cta) * p.T / p.P;
@@ -254,8 +264,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   unsigned char* raw = base;                               // [kRaw][16 KB]
   unsigned char* dig = raw + C::kRaw * kRawSlot;           // [6][128 j][128 B]
   unsigned char* rbuf = dig + kPl * kPlane;               // [kB] right Khatri-Rao digits (per tile)
-  unsigned char* lbuf = rbuf + C::kB;                      // [kB] left Khatri-Rao digits (per row block)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lbuf + C::kB);
+  unsigned char* lbuf = rbuf + C::kB;                      // [kBL] left Khatri-Rao digits (per row block)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lbuf + C::kBL);
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + C::kRaw;
   uint64_t* dig_full = raw_empty + C::kRaw;  // [4] row chunks 2 ks, 2 ks + 1 of the tile split
@@ -336,8 +346,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         bulk_load(rbuf, p.img_r + ct * C::kB, C::kB, rb_full, pol_k);
         if (rb != cur_rb) {
           if (m > 0) WAIT(lb_empty, (m - 1) & 1, 2, m);
-          mbar_arrive_tx(lb_full, C::kB);
-          bulk_load(lbuf, p.img_l + rb * C::kB, C::kB, lb_full, pol_k);
+          mbar_arrive_tx(lb_full, C::kBL);
+          bulk_load(lbuf, p.img_l + rb * C::kBL, C::kBL, lb_full, pol_k);
           cur_rb = rb;
           ++m;
         }
@@ -370,9 +380,9 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 #pragma unroll
           for (int a = 0; a < kPl; ++a)
             if (!(p.knobs & 8))
-              mma_i8(tmem + (1 + lbk) * kPl * N + a * N, sdesc(dg + a * kPlane + ks * 32, 16, 1024),
-                     sdesc(lb + ks * 32, 16, 1024),
-                     idesc_i8(false, N * (kPl - a), 128), (ks > 0 || a > 0) ? 1u : 0u);
+              mma_i8(tmem + kPl * N + lbk * C::kLS + a * NL, sdesc(dg + a * kPlane + ks * 32, 16, 1024),
+                     sdesc(lb + ks * 32, 16, 1024), idesc_i8(false, stacked_n(NL, a), 128),
+                     (ks > 0 || a > 0) ? 1u : 0u);
         }
         // right: M = 128 rows i, K = the tile's 128 columns (rows of the plane), after the split
         TWAIT(1, rb_full, k & 1, 5, k);
@@ -513,11 +523,11 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       const int64_t j = ct * 128 + row;  // M = 128: TMEM lane = column
       double* lout = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K + j;
 #pragma unroll
-      for (int rc = 0; rc < N / 8; ++rc) {
+      for (int rc = 0; rc < NL / 8; ++rc) {
         if (rc * 8 >= p.R || (p.knobs & 4)) break;
         uint32_t d[kPl][8];
 #pragma unroll
-        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + (1 + lbk) * kPl * N + dd * N + rc * 8, d[dd]);
+        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + kPl * N + lbk * C::kLS + dd * NL + rc * 8, d[dd]);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -553,20 +563,23 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 // Output per tile: [6 planes][N rank rows][128 bytes of the tile's rows, 128-byte
 // swizzle] and the column weights 2^(eY + e_r - 52) (0: all-zero column, NaN:
 // non-finite factor entry).
-template <int N>
+template <int N, int NL>
 __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, int64_t Lr, const KRSpec left,
                                                            int64_t Ll, int R, int64_t nCT, const double* yscale,
                                                            unsigned char* img_r, double* w_r, unsigned char* img_l,
                                                            double* w_l) {
   __shared__ double sc[N];
   __shared__ unsigned long long mbits[kMaxModes * N];
-  __shared__ __align__(16) unsigned char im[kPl * N * 128];
+  __shared__ __align__(16) unsigned char im[kPl * N * 128 + 1024];
   const bool is_right = blockIdx.x < nCT;
+  const int NP = is_right ? N : NL;  // rank rows per digit plane of this side's image
+  const int IB = is_right ? kPl * N * 128 : left_image_bytes(NL);
   const KRSpec& spec = is_right ? right : left;
   const int64_t L = is_right ? Lr : Ll, tile = is_right ? blockIdx.x : blockIdx.x - nCT;
   unsigned char* img = is_right ? img_r : img_l;
   double* w = is_right ? w_r : w_l;
   for (int e = threadIdx.x; e < kMaxModes * N; e += blockDim.x) mbits[e] = 0ull;
+  for (int e = kPl * NP * 128 + threadIdx.x; e < IB; e += blockDim.x) im[e] = 0;  // zero rows past the planes
   pdl_trigger();  // the seed may launch now: its Y stream does not depend on this kernel
   pdl_wait();     // the sorted factors come from the prologue
   __syncthreads();
@@ -638,16 +651,18 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
     const double u = fma(isfinite(x) ? x : 0.0, sc[r], kMagic);
     const uint32_t lo = __double2loint(u), hi = __double2hiint(u);
     const int off = r * 128 + ((((q >> 4) ^ (r & 7))) << 4) + (q & 15);
+    if (r < NP) {
 #pragma unroll
-    for (int k = 0; k < kPl; ++k) {
-      const uint32_t b = (k < 4 ? (lo >> (8 * k)) : (hi >> (8 * (k - 4)))) & 0xFFu;
-      im[(kPl - 1 - k) * N * 128 + off] = static_cast<unsigned char>(b ^ 0x80u);
+      for (int k = 0; k < kPl; ++k) {
+        const uint32_t b = (k < 4 ? (lo >> (8 * k)) : (hi >> (8 * (k - 4)))) & 0xFFu;
+        im[(kPl - 1 - k) * NP * 128 + off] = static_cast<unsigned char>(b ^ 0x80u);
+      }
     }
   }
   __syncthreads();
-  uint4* dst = reinterpret_cast<uint4*>(img + tile * (kPl * N * 128));
+  uint4* dst = reinterpret_cast<uint4*>(img + tile * IB);
   const uint4* src = reinterpret_cast<const uint4*>(im);
-  for (int e = threadIdx.x; e < kPl * N * 8; e += N * 16) dst[e] = src[e];
+  for (int e = threadIdx.x; e < IB / 16; e += N * 16) dst[e] = src[e];
 }
 
 // max |Y| -> scale record: [0] 2^(46 - eY), [1] eY, [2] max |Y| (NaN when Y has
@@ -685,37 +700,45 @@ __global__ void y_scale_final_kernel(const unsigned long long* amax, const doubl
 
 }  // namespace
 
-size_t seed_i8_smem_bytes(int N) { return N == 32 ? Cfg<32>::kSmem : Cfg<16>::kSmem; }
+template <int N, int NL>
+void launch_one_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s) {
+  using C = Cfg<N, NL>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(seed_i8_kernel<N, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    configured = true;
+  }
+  launch_k(seed_i8_kernel<N, NL>, dim3(p.P), dim3(kI8Threads), C::kSmem, s, pdl_enabled(), p, *ymap);
+}
+
+int i8_left_block(int N, int R) { return (N == 32 && R <= 24) ? 24 : N; }
+size_t i8_left_image_bytes(int NL) { return static_cast<size_t>(left_image_bytes(NL)); }
 
 int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s) {
-  if (p.N == 32) {
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(seed_i8_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<32>::kSmem);
-      configured = true;
-    }
-    launch_k(seed_i8_kernel<32>, dim3(p.P), dim3(kI8Threads), Cfg<32>::kSmem, s, pdl_enabled(), p, *ymap);
-  } else {
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(seed_i8_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<16>::kSmem);
-      configured = true;
-    }
-    launch_k(seed_i8_kernel<16>, dim3(p.P), dim3(kI8Threads), Cfg<16>::kSmem, s, pdl_enabled(), p, *ymap);
-  }
+  if (p.N == 16)
+    launch_one_i8<16, 16>(p, ymap, s);
+  else if (p.NL == 24)
+    launch_one_i8<32, 24>(p, ymap, s);
+  else
+    launch_one_i8<32, 32>(p, ymap, s);
   return 1;
 }
 
-int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N,
+int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N, int NL,
                      const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, cudaStream_t s) {
   const int64_t nCT = ceil_div(Kp, 128), nRB = ceil_div(Jp, 128);
   const dim3 grid(static_cast<unsigned>(nCT + nRB));
-  if (N == 32)
-    launch_k(kr_digits_kernel<32>, grid, dim3(512), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale,
-             static_cast<unsigned char*>(img_r), w_r, static_cast<unsigned char*>(img_l), w_l);
+  auto* ir = static_cast<unsigned char*>(img_r);
+  auto* il = static_cast<unsigned char*>(img_l);
+  if (N == 16)
+    launch_k(kr_digits_kernel<16, 16>, grid, dim3(256), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
+             w_r, il, w_l);
+  else if (NL == 24)
+    launch_k(kr_digits_kernel<32, 24>, grid, dim3(512), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
+             w_r, il, w_l);
   else
-    launch_k(kr_digits_kernel<16>, grid, dim3(256), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale,
-             static_cast<unsigned char*>(img_r), w_r, static_cast<unsigned char*>(img_l), w_l);
+    launch_k(kr_digits_kernel<32, 32>, grid, dim3(512), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
+             w_r, il, w_l);
   return 1;
 }
 
