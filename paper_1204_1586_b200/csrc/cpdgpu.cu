@@ -571,8 +571,7 @@ void build_f64_geometry(cpdgpu_ctx* ctx, Plan& pl) {
     pl.Rpart.ensure(std::max(pl.Rpart.bytes, static_cast<size_t>(g.P) * g.slots * c.NT * 8 * 128 * sizeof(double)));
     if (!g.lpart_direct)
       pl.Lpart.ensure(std::max(pl.Lpart.bytes, static_cast<size_t>(g.nRB) * c.Rc * Kp * sizeof(double)));
-    const size_t img = static_cast<size_t>(6) * g.N * 128;
-    g.img_r.ensure(static_cast<size_t>(g.nCT) * img);
+    g.img_r.ensure(static_cast<size_t>(g.nCT) * cpdgpu::i8_right_image_bytes(g.N, g.NL));
     g.img_l.ensure(static_cast<size_t>(g.nRB) * cpdgpu::i8_left_image_bytes(g.NL));
     g.w_r.ensure(static_cast<size_t>(g.nCT) * g.N * sizeof(double));
     g.w_l.ensure(static_cast<size_t>(g.nRB) * g.N * sizeof(double));

@@ -83,6 +83,7 @@ struct SeedI8Params {
 // double-buffer in TMEM), and the left digit image bytes per row block
 int i8_left_block(int N, int R);
 size_t i8_left_image_bytes(int NL);
+size_t i8_right_image_bytes(int N, int NL);
 // ymap: Y (dim0 J, dim1 K) fp64, box 16 x 128, 128-byte swizzle
 int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s);
 // Khatri-Rao rows [L][ldk] -> digit images [ceil(L / 128)][6][N][128] + weights [.][N]

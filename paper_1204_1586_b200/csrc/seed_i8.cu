@@ -87,13 +87,15 @@ __host__ __device__ constexpr int stacked_n(int n, int a) { return ((n * (kPl - 
 
 template <int N, int NL>
 struct Cfg {
-  static constexpr int kB = kPl * N * 128;         // right Khatri-Rao digit image
-  static constexpr int kBL = left_image_bytes(NL);  // left image
+  static constexpr int kNR = (N == 32 && NL == 24) ? 24 : N;  // right rank block (24 with the left)
+  static constexpr int kB = left_image_bytes(kNR);   // right Khatri-Rao digit image
+  static constexpr int kBL = left_image_bytes(NL);   // left image
+  static constexpr int kRS = kNR == 24 ? kPl * kNR + 8 : kPl * kNR;  // right accumulator columns
   static constexpr int kRaw = N == 32 ? 5 : 6;     // 16 KB TMA boxes (8 KB boxes cap TMA near 4 TB/s)
   // TMEM: right accumulators 6 N columns, then kLB left buffers of kLS columns
   // (NL = 24: 6 x 24 + 8 slack columns for the rounded-up stacked N)
   static constexpr int kLS = NL == 24 ? kPl * NL + 8 : kPl * NL;
-  static constexpr int kLB = (kPl * N + 2 * kLS <= 512) ? 2 : 1;
+  static constexpr int kLB = (kRS + 2 * kLS <= 512) ? 2 : 1;
   static constexpr int kCols = 512;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kPl * kPlane + kB + kBL + 256;
 };
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 #pragma unroll
           for (int a = 0; a < kPl; ++a)
             if (!(p.knobs & 8))
-              mma_i8(tmem + kPl * N + lbk * C::kLS + a * NL, sdesc(dg + a * kPlane + ks * 32, 16, 1024),
+              mma_i8(tmem + C::kRS + lbk * C::kLS + a * NL, sdesc(dg + a * kPlane + ks * 32, 16, 1024),
                      sdesc(lb + ks * 32, 16, 1024), idesc_i8(false, stacked_n(NL, a), 128),
                      (ks > 0 || a > 0) ? 1u : 0u);
         }
@@ -394,8 +396,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 #pragma unroll
           for (int a = 0; a < kPl; ++a)
             if (!(p.knobs & 8))
-              mma_i8(tmem + a * N, sdesc(dg + a * kPlane + ks * 4096, 16384, 1024), sdesc(rbb + ks * 32, 16, 1024),
-                     idesc_i8(true, N * (kPl - a), 128), (ks > 0 || a > 0 || pos > 0) ? 1u : 0u);
+              mma_i8(tmem + a * C::kNR, sdesc(dg + a * kPlane + ks * 4096, 16384, 1024), sdesc(rbb + ks * 32, 16, 1024),
+                     idesc_i8(true, stacked_n(C::kNR, a), 128), (ks > 0 || a > 0 || pos > 0) ? 1u : 0u);
         if (send) umma_commit(accR_full);
         umma_commit(rb_empty);
         umma_commit(dig_empty);
@@ -490,11 +492,11 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       tc_fence_after();
       const double* wr = p.w_r + ct * N;
 #pragma unroll
-      for (int rc = 0; rc < N / 8; ++rc) {
+      for (int rc = 0; rc < C::kNR / 8; ++rc) {
         if (rc * 8 >= p.R || (p.knobs & 4)) break;  // warp-uniform: columns past the rank are zero
         uint32_t d[kPl][8];
 #pragma unroll
-        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + dd * N + rc * 8, d[dd]);
+        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + dd * C::kNR + rc * 8, d[dd]);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         if (rc * 8 >= p.R || (p.knobs & 4)) break;
         uint32_t d[kPl][8];
 #pragma unroll
-        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + kPl * N + lbk * C::kLS + dd * NL + rc * 8, d[dd]);
+        for (int dd = 0; dd < kPl; ++dd) tmem_ld8(tmem + lanes + C::kRS + lbk * C::kLS + dd * NL + rc * 8, d[dd]);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -572,8 +574,9 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
   __shared__ unsigned long long mbits[kMaxModes * N];
   __shared__ __align__(16) unsigned char im[kPl * N * 128 + 1024];
   const bool is_right = blockIdx.x < nCT;
-  const int NP = is_right ? N : NL;  // rank rows per digit plane of this side's image
-  const int IB = is_right ? kPl * N * 128 : left_image_bytes(NL);
+  constexpr int NR = (N == 32 && NL == 24) ? 24 : N;
+  const int NP = is_right ? NR : NL;  // rank rows per digit plane of this side's image
+  const int IB = left_image_bytes(NP);
   const KRSpec& spec = is_right ? right : left;
   const int64_t L = is_right ? Lr : Ll, tile = is_right ? blockIdx.x : blockIdx.x - nCT;
   unsigned char* img = is_right ? img_r : img_l;
@@ -713,6 +716,7 @@ void launch_one_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t 
 
 int i8_left_block(int N, int R) { return (N == 32 && R <= 24) ? 24 : N; }
 size_t i8_left_image_bytes(int NL) { return static_cast<size_t>(left_image_bytes(NL)); }
+size_t i8_right_image_bytes(int N, int NL) { return static_cast<size_t>(left_image_bytes((N == 32 && NL == 24) ? 24 : N)); }
 
 int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s) {
   if (p.N == 16)
