@@ -18,9 +18,11 @@ the max over ranks of the summed step time is reported.
   value      whole-job tensor bytes per second (GB/s) through the device API
   e2e        same metric through the host C-ABI (cpdgpu_cp_gradient_all): H2D
              copy of Y from pinned host memory + factors in, gradients out
-  roofline   dominant kernel = K1 seed contraction (fp64 DMMA); its CUDA-event
-             time against the FP64 tensor peak measured on B200 (compute bound
-             at R=20) with the HBM fraction beside it
+  roofline   dominant kernel = K1 seed contraction, timed with CUDA events on the
+             launching stream.  Large fp64 tensors (c2, c3) run it on the int8
+             tensor cores (seed_i8_kernel): bound = HBM.  Otherwise fp64 DMMA
+             (seed_f64_kernel, CPDGPU_I8=0 forces it): the slower of the HBM and
+             FP64-tensor ideals, the other fraction beside it
   cpu_baseline  the CPU oracle (a port of the reference) on this host's cores
 
 `--impl reference` times the reference algorithm's CPU implementation (the
