@@ -79,22 +79,28 @@ __device__ __forceinline__ bool seg_end(int64_t tile, int k, int n, int64_t nCT,
   return k == n - 1 || (tile + 1) / nCT != tile / nCT || pos == kSeg - 1;
 }
 
-// Left digit image of an NL-row rank block: 6 planes of NL rows (+ 8 zero rows when
-// NL = 24, read by the rounded-up stacked MMAs).
-__host__ __device__ constexpr int left_image_bytes(int NL) { return kPl * NL * 128 + (NL == 24 ? 8 * 128 : 0); }
 // stacked N of Y plane a on a product with rank block n (M = 128 needs N % 16 == 0)
 __host__ __device__ constexpr int stacked_n(int n, int a) { return ((n * (kPl - a)) + 15) / 16 * 16; }
+// Digit image of an NP-row rank block: 6 planes of NP rows, zero rows up to the
+// rounded-up stacked N the MMAs read (NP = 12: 80 rows)
+__host__ __device__ constexpr int left_image_bytes(int NP) { return stacked_n(NP, 0) * 128; }
+// accumulator columns of one product: diagonal d at d NP, plus the slack the
+// rounded-up stacked N writes past diagonal 5 (never read)
+__host__ __device__ constexpr int acc_cols(int NP) {
+  int m = 0;
+  for (int a = 0; a < kPl; ++a) m = (a * NP + stacked_n(NP, a)) > m ? (a * NP + stacked_n(NP, a)) : m;
+  return m;
+}
 
 template <int N, int NL>
 struct Cfg {
-  static constexpr int kNR = (N == 32 && NL == 24) ? 24 : N;  // right rank block (24 with the left)
+  static constexpr int kNR = NL < N ? NL : N;        // right rank block (the left one when smaller)
   static constexpr int kB = left_image_bytes(kNR);   // right Khatri-Rao digit image
   static constexpr int kBL = left_image_bytes(NL);   // left image
-  static constexpr int kRS = kNR == 24 ? kPl * kNR + 8 : kPl * kNR;  // right accumulator columns
-  static constexpr int kRaw = N == 32 ? 5 : 6;     // 16 KB TMA boxes (8 KB boxes cap TMA near 4 TB/s)
-  // TMEM: right accumulators 6 N columns, then kLB left buffers of kLS columns
-  // (NL = 24: 6 x 24 + 8 slack columns for the rounded-up stacked N)
-  static constexpr int kLS = NL == 24 ? kPl * NL + 8 : kPl * NL;
+  static constexpr int kRaw = N == 32 ? 5 : 6;       // 16 KB TMA boxes (8 KB boxes cap TMA near 4 TB/s)
+  // TMEM: right accumulators, then kLB left buffers
+  static constexpr int kRS = acc_cols(kNR);
+  static constexpr int kLS = acc_cols(NL);
   static constexpr int kLB = (kRS + 2 * kLS <= 512) ? 2 : 1;
   static constexpr int kCols = 512;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kRaw) * kRawSlot + kPl * kPlane + kB + kBL + 256;
@@ -492,7 +498,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       tc_fence_after();
       const double* wr = p.w_r + ct * N;
 #pragma unroll
-      for (int rc = 0; rc < C::kNR / 8; ++rc) {
+      for (int rc = 0; rc < (C::kNR + 7) / 8; ++rc) {
         if (rc * 8 >= p.R || (p.knobs & 4)) break;  // warp-uniform: columns past the rank are zero
         uint32_t d[kPl][8];
 #pragma unroll
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       const int64_t j = ct * 128 + row;  // M = 128: TMEM lane = column
       double* lout = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K + j;
 #pragma unroll
-      for (int rc = 0; rc < NL / 8; ++rc) {
+      for (int rc = 0; rc < (NL + 7) / 8; ++rc) {
         if (rc * 8 >= p.R || (p.knobs & 4)) break;
         uint32_t d[kPl][8];
 #pragma unroll
@@ -574,7 +580,7 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
   __shared__ unsigned long long mbits[kMaxModes * N];
   __shared__ __align__(16) unsigned char im[kPl * N * 128 + 1024];
   const bool is_right = blockIdx.x < nCT;
-  constexpr int NR = (N == 32 && NL == 24) ? 24 : N;
+  constexpr int NR = NL < N ? NL : N;
   const int NP = is_right ? NR : NL;  // rank rows per digit plane of this side's image
   const int IB = left_image_bytes(NP);
   const KRSpec& spec = is_right ? right : left;
@@ -653,12 +659,12 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
     const double x = xs[e];
     const double u = fma(isfinite(x) ? x : 0.0, sc[r], kMagic);
     const uint32_t lo = __double2loint(u), hi = __double2hiint(u);
-    const int off = r * 128 + ((((q >> 4) ^ (r & 7))) << 4) + (q & 15);
     if (r < NP) {
 #pragma unroll
       for (int k = 0; k < kPl; ++k) {
         const uint32_t b = (k < 4 ? (lo >> (8 * k)) : (hi >> (8 * (k - 4)))) & 0xFFu;
-        im[(kPl - 1 - k) * NP * 128 + off] = static_cast<unsigned char>(b ^ 0x80u);
+        const int g = (kPl - 1 - k) * NP + r;  // row in the image: the swizzle phase is g mod 8
+        im[g * 128 + ((((q >> 4) ^ (g & 7))) << 4) + (q & 15)] = static_cast<unsigned char>(b ^ 0x80u);
       }
     }
   }
@@ -714,12 +720,14 @@ void launch_one_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t 
   launch_k(seed_i8_kernel<N, NL>, dim3(p.P), dim3(kI8Threads), C::kSmem, s, pdl_enabled(), p, *ymap);
 }
 
-int i8_left_block(int N, int R) { return (N == 32 && R <= 24) ? 24 : N; }
+int i8_left_block(int N, int R) { return (N == 32 && R <= 24) ? 24 : ((N == 16 && R <= 12) ? 12 : N); }
 size_t i8_left_image_bytes(int NL) { return static_cast<size_t>(left_image_bytes(NL)); }
-size_t i8_right_image_bytes(int N, int NL) { return static_cast<size_t>(left_image_bytes((N == 32 && NL == 24) ? 24 : N)); }
+size_t i8_right_image_bytes(int N, int NL) { return static_cast<size_t>(left_image_bytes(NL < N ? NL : N)); }
 
 int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s) {
-  if (p.N == 16)
+  if (p.N == 16 && p.NL == 12)
+    launch_one_i8<16, 12>(p, ymap, s);
+  else if (p.N == 16)
     launch_one_i8<16, 16>(p, ymap, s);
   else if (p.NL == 24)
     launch_one_i8<32, 24>(p, ymap, s);
@@ -734,7 +742,10 @@ int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_
   const dim3 grid(static_cast<unsigned>(nCT + nRB));
   auto* ir = static_cast<unsigned char*>(img_r);
   auto* il = static_cast<unsigned char*>(img_l);
-  if (N == 16)
+  if (N == 16 && NL == 12)
+    launch_k(kr_digits_kernel<16, 12>, grid, dim3(256), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
+             w_r, il, w_l);
+  else if (N == 16)
     launch_k(kr_digits_kernel<16, 16>, grid, dim3(256), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
              w_r, il, w_l);
   else if (NL == 24)
