@@ -308,19 +308,23 @@ __global__ void __launch_bounds__(kL0Threads) l0_kernel(const L0Step st, double*
       if (has1) zs[e1] = sum[1];
     } else {
       double sum[2] = {0.0, 0.0};
+      // row-block partials: plane stride ldz, fields hoisted out of the
+      // (dynamically indexed) parameter struct
+      const int pcount = sd.pcount;
+      const int64_t ldz = sd.ldz;
       const double* z0 = sd.Z + r * sd.pK + base + e0;
       const double* z1 = sd.Z + r * sd.pK + base + (has1 ? e1 : e0);
-      for (int rb0 = 0; rb0 < sd.pcount; rb0 += 8) {
+      for (int rb0 = 0; rb0 < pcount; rb0 += 8) {
         double v0[8], v1[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const bool ok = rb0 + u < sd.pcount;
-          v0[u] = ok ? z0[static_cast<int64_t>(rb0 + u) * sd.ldz] : 0.0;
-          v1[u] = ok ? z1[static_cast<int64_t>(rb0 + u) * sd.ldz] : 0.0;
+          const bool ok = rb0 + u < pcount;
+          v0[u] = ok ? z0[(rb0 + u) * ldz] : 0.0;
+          v1[u] = ok ? z1[(rb0 + u) * ldz] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (rb0 + u < sd.pcount) {
+          if (rb0 + u < pcount) {
             sum[0] += v0[u];
             sum[1] += v1[u];
           }
