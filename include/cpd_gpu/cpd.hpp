@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <exception>
 #include <functional>
 #include <memory>
 #include <numeric>
@@ -49,6 +50,9 @@ struct DomainError : std::domain_error {
 struct NumericError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct ParseError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 // Device / driver failure (no reference counterpart).
 struct DeviceError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -62,6 +66,7 @@ namespace gpu {
     case CPDGPU_ARGUMENT_ERROR: throw ArgumentError(msg);
     case CPDGPU_NUMERIC_ERROR: throw NumericError(msg);
     case CPDGPU_DOMAIN_ERROR: throw DomainError(msg);
+    case CPDGPU_PARSE_ERROR: throw ParseError(msg);
     default: throw DeviceError(msg.empty() ? "cpdgpu: device failure" : msg);
   }
 }
@@ -344,9 +349,13 @@ struct HookCtx {
   std::vector<Matrix>* out;
   std::vector<std::vector<double>>* bufs;
   index_t R;
-  std::string error;
-  int code = 0;
+  std::exception_ptr error;  // whatever the hook (or the size check) threw
 };
+// Runs the caller's hook between modes.  Nothing may unwind through the C-ABI
+// frames, so any exception is captured here (status -1 stops the sweep) and
+// rethrown unchanged by cp_gradient_all once the C call has returned, exactly
+// as the reference's direct hook(orig, G) call would propagate it
+// (mttkrp.cpp:134-145).
 inline int hook_tramp(void* user, int mode, const double* g, int64_t rows, int64_t rank, uint64_t mults) {
   auto* h = static_cast<HookCtx*>(user);
   try {
@@ -359,20 +368,10 @@ inline int hook_tramp(void* user, int mode, const double* g, int64_t rows, int64
       throw ShapeError("cp_gradient_all: hook left factor of mode " + std::to_string(mode) + " with the wrong size");
     std::copy(F.data(), F.data() + rows * rank, (*h->bufs)[static_cast<size_t>(mode - 1)].data());
     return 0;
-  } catch (const ShapeError& e) {
-    h->error = e.what();
-    h->code = CPDGPU_SHAPE_ERROR;
-  } catch (const IndexError& e) {
-    h->error = e.what();
-    h->code = CPDGPU_INDEX_ERROR;
-  } catch (const NumericError& e) {
-    h->error = e.what();
-    h->code = CPDGPU_NUMERIC_ERROR;
-  } catch (const std::exception& e) {
-    h->error = e.what();
-    h->code = CPDGPU_ARGUMENT_ERROR;
+  } catch (...) {
+    h->error = std::current_exception();
   }
-  return h->code;
+  return CPDGPU_HOOK_ABORTED;
 }
 }  // namespace detail
 
@@ -403,10 +402,10 @@ inline std::vector<Matrix> cp_gradient_all(const DenseTensor& y, FactorList& fac
       bufs[static_cast<size_t>(m)].assign(F.data(), F.data() + F.rows() * F.cols());
       fp[static_cast<size_t>(m)] = bufs[static_cast<size_t>(m)].data();
     }
-    detail::HookCtx hc{&hook, counter, &factors, &out, &bufs, R, {}, 0};
+    detail::HookCtx hc{&hook, counter, &factors, &out, &bufs, R, nullptr};
     const int st = cpdgpu_cp_gradient_all_hook(ctx.h, y.device(), R, fp.data(), gp.data(), detail::hook_tramp, &hc,
                                                &peak);
-    if (hc.code) gpu::throw_status(hc.code, hc.error);
+    if (hc.error) std::rethrow_exception(hc.error);
     ctx.check(st);
   }
   if (stats) stats->peak_workspace_doubles = peak;

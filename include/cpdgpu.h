@@ -35,7 +35,9 @@ typedef enum {
   CPDGPU_DOMAIN_ERROR = 5,   /* cpd::DomainError   (errors.hpp:24-26) */
   CPDGPU_CUDA_ERROR = 6,     /* device / driver failure                */
   CPDGPU_NO_MEMORY = 7,      /* device allocation failed               */
-  CPDGPU_PARSE_ERROR = 8     /* cpd::ParseError    (errors.hpp:33-36) */
+  CPDGPU_PARSE_ERROR = 8,    /* cpd::ParseError    (errors.hpp:33-36) */
+  CPDGPU_HOOK_ABORTED = 9    /* the caller's mode hook failed; the caller holds
+                                its exception and rethrows it unchanged   */
 } cpdgpu_status;
 
 typedef enum { CPDGPU_F64 = 0, CPDGPU_F32 = 1 } cpdgpu_dtype;
@@ -49,7 +51,8 @@ typedef struct cpdgpu_tensor cpdgpu_tensor;
  * mode's multiplication count has been reported through `mults`.  It may
  * overwrite the caller's factor for `mode` (the buffer passed in `factors`),
  * which the sweep re-reads before moving on (mttkrp.cpp:137-144).  A non-zero
- * return aborts the sweep with that status. */
+ * return aborts the sweep with that status (CPDGPU_HOOK_ABORTED when the hook
+ * threw: the adapter rethrows the hook's own exception). */
 typedef int (*cpdgpu_mode_hook)(void* user, int mode, const double* gradient, int64_t rows,
                                 int64_t rank, uint64_t mults);
 

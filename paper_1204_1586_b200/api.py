@@ -344,7 +344,7 @@ def cp_gradient_all(y: DenseTensor, factors: list, counter: Optional[CostCounter
                 return 0
             except BaseException as e:  # noqa: BLE001 - re-raised below
                 err.append(e)
-                return 3
+                return 9  # CPDGPU_HOOK_ABORTED: the hook's own exception is re-raised below
 
         cb = _lib.HOOK(_cb)
         st = ctx._L.cpdgpu_cp_gradient_all_hook(ctx.h, y.h, R, fptr, gptr, cb, None, C.byref(peak))

@@ -62,6 +62,19 @@ inline cudaError_t launch_k(void (*kernel)(Exp...), dim3 grid, dim3 block, size_
 }
 bool pdl_enabled();  // CPDGPU_PDL=0 disables (default on)
 
+// Dynamic shared memory above 48 KB: cudaFuncSetAttribute applies to the current
+// device only, so it is set once per (kernel, device); `mask` is the caller's
+// per-kernel record of the devices done.
+template <typename K>
+inline void set_smem_attr(K kernel, int bytes, unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (mask & bit)) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  mask |= bit;
+}
+
 // A contiguous range of modes lo..hi of the sorted frame whose factor columns
 // form a Khatri-Rao row on the fly: row index q has mixed-radix digits
 // d_k (first mode fastest) and  KR[q, r] = prod_k A_k[d_k + I_k r]

@@ -221,6 +221,7 @@ struct cpdgpu_tensor {
   DevBuf yscale8;                    // fp64: int8 seed scale record [2^(46-eY), eY, max|Y|] + scratch
   uint64_t scale8_version = ~0ull;
   double amax8 = -1.0, amean8 = 0.0;
+  bool scale8_ok = false;
   size_t elem() const { return dtype == CPDGPU_F64 ? 8 : 4; }
   ~cpdgpu_tensor() {
     if (sorted && sorted != data) cudaFree(sorted);
@@ -311,10 +312,19 @@ struct Plan {
   uint64_t als_graph_launches = 0;
   bool als_warm = false;
   double als_rtol = -1.0;
-  ~Plan() {
+  const void* graph_ybase = nullptr;       // Y address the recorded graphs read
+  ~Plan() { drop_graphs(); }
+  // The recorded graphs hold Y's address and its TMA views by value: they are
+  // re-recorded whenever either changes (e.g. a re-permuted sorted copy).
+  void drop_graphs() {
     if (grad_exec) cudaGraphExecDestroy(grad_exec);
     if (grad_graph) cudaGraphDestroy(grad_graph);
     if (als_exec) cudaGraphExecDestroy(als_exec);
+    grad_exec = nullptr;
+    grad_graph = nullptr;
+    als_exec = nullptr;
+    grad_warm = false;
+    als_warm = false;
   }
 
   KRSpec spec(int lo, int hi, int r0) const {  // 1-based sorted modes lo..hi
@@ -730,7 +740,7 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
 // hold no Inf / NaN; everything else runs the fp64 DMMA pass.
 void bind_i8(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const void* ybase) {
   if (t->scale8_version != t->version) {
-    t->yscale8.ensure(64);
+    t->yscale8.ensure(32 + 16 * static_cast<size_t>(cpdgpu::y_scale_f64_blocks(t->numel, ctx->num_sms)));
     double* rec = t->yscale8.d();
     ctx->launches += cpdgpu::launch_y_scale_f64(static_cast<const double*>(ybase), t->numel, rec + 4, rec,
                                                 ctx->num_sms, ctx->stream);
@@ -739,31 +749,36 @@ void bind_i8(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const void* ybase) {
     CK(cudaStreamSynchronize(ctx->stream));
     t->amax8 = h[2];
     t->amean8 = t->numel > 0 ? h[3] / static_cast<double>(t->numel) : 0.0;
+    // the digit scale 2^(46 - eY) must be a finite normal double
+    t->scale8_ok = std::isfinite(h[0]) && h[0] >= 0x1p-1000;
     t->scale8_version = t->version;
   }
-  bool on = std::isfinite(t->amax8) && (t->amax8 == 0.0 || t->amax8 <= 4096.0 * t->amean8);
+  bool on = t->scale8_ok && std::isfinite(t->amax8) && std::isfinite(t->amean8) &&
+            (t->amax8 == 0.0 || t->amax8 <= 4096.0 * t->amean8);
   if (on && pl.i8.ymap_base != ybase) {
     on = cpdgpu::make_tensor_map_2d(&pl.i8.ymap, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
                                     static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
                                     static_cast<uint64_t>(pl.Jp) * 8, 16, 128, true, true);
     pl.i8.ymap_base = on ? ybase : nullptr;
   }
-  if (on != pl.i8.on && pl.grad_exec) {  // the recorded gradient used the other seed path
-    cudaGraphExecDestroy(pl.grad_exec);
-    cudaGraphDestroy(pl.grad_graph);
-    pl.grad_exec = nullptr;
-    pl.grad_graph = nullptr;
-    pl.grad_warm = false;
-  }
+  if (on != pl.i8.on) pl.drop_graphs();  // the recorded gradient used the other seed path
   pl.i8.on = on;
 }
 
 void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
   if (pl.f32) {
     bind_f32_inputs(ctx, pl, t);
+    if (pl.graph_ybase != pl.ymap_base) {
+      pl.drop_graphs();
+      pl.graph_ybase = pl.ymap_base;
+    }
     return;
   }
   const void* ybase = pl.raw_frame ? t->data : t->sorted;
+  if (pl.graph_ybase != ybase) {
+    pl.drop_graphs();
+    pl.graph_ybase = ybase;
+  }
   if (pl.use_lc && pl.ymapL_base != ybase) {
     if (!cpdgpu::make_tensor_map_2d(&pl.ymapL, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
                                     static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
@@ -1364,7 +1379,7 @@ int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& 
   if (pl.l0_scratch.bytes < scratch * sizeof(double)) pl.l0_scratch.ensure(scratch * sizeof(double));
   if (pl.l0_tickets.bytes < 2 * static_cast<size_t>(R) * sizeof(unsigned)) {
     pl.l0_tickets.ensure(2 * static_cast<size_t>(R) * sizeof(unsigned));
-    CK(cudaMemset(pl.l0_tickets.p, 0, pl.l0_tickets.bytes));
+    CK(cudaMemsetAsync(pl.l0_tickets.p, 0, pl.l0_tickets.bytes, ctx->stream));
   }
   size_t off = 0;
   for (int i = 0; i < l0.nsides; ++i) {

@@ -91,7 +91,9 @@ int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t 
 // sides, from the factors (right: K_p rows, left: J_p rows; one launch)
 int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N, int NL,
                      const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, cudaStream_t s);
-// fp64 tensor scale record [2^(46-eY), eY, max|Y|, sum|Y|]; scratch >= 16 bytes
+// fp64 tensor scale record [2^(46-eY), eY, max|Y|, sum|Y|] (bitwise reproducible);
+// scratch >= 16 * y_scale_f64_blocks(n, num_sms) bytes
+int y_scale_f64_blocks(int64_t n, int num_sms);
 int launch_y_scale_f64(const double* y, int64_t n, void* scratch, double* out, int num_sms, cudaStream_t s);
 
 // ---- K1 for fp32 tensors: tcgen05 split-fp16 seed contraction (seed_f32.cu) ---

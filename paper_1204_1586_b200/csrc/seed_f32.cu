@@ -593,18 +593,12 @@ int64_t seed_f32_tile_bytes() { return kKTile; }
 int launch_seed_f32(const Seed32Params& p, const CUtensorMap* ymap, int left, cudaStream_t s) {
   const size_t smem = seed_f32_smem_bytes();
   if (left) {
-    static bool cfg = false;
-    if (!cfg) {
-      cudaFuncSetAttribute(seed_f32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      cfg = true;
-    }
+    static unsigned long long cfg = 0;
+    set_smem_attr(seed_f32_kernel<1>, static_cast<int>(smem), cfg);
     launch_k(seed_f32_kernel<1>, dim3(p.P), dim3(kThreads), smem, s, pdl_enabled(), p, *ymap);
   } else {
-    static bool cfg = false;
-    if (!cfg) {
-      cudaFuncSetAttribute(seed_f32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      cfg = true;
-    }
+    static unsigned long long cfg = 0;
+    set_smem_attr(seed_f32_kernel<0>, static_cast<int>(smem), cfg);
     launch_k(seed_f32_kernel<0>, dim3(p.P), dim3(kThreads), smem, s, pdl_enabled(), p, *ymap);
   }
   return 1;

@@ -665,11 +665,8 @@ template <int NT, int MODE>
 void launch_one(const SeedParams& p, const CUtensorMap& tmap, const CUtensorMap& kmap, cudaStream_t s,
                 size_t smem) {
   auto fn = seed_f64_kernel<NT, MODE>;
-  static bool configured = false;  // one attribute call per instantiation
-  if (!configured) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    configured = true;
-  }
+  static unsigned long long configured = 0;  // devices done, per instantiation
+  set_smem_attr(fn, 232448, configured);
   launch_k(fn, dim3(p.P), dim3(kThreads), smem, s, pdl_enabled(), p, tmap, kmap);
 }
 
@@ -702,11 +699,8 @@ template <int NT>
 void launch_lc(const SeedParams& p, const CUtensorMap& ym, const CUtensorMap& km, cudaStream_t s, size_t smem) {
   constexpr int MC = 4;  // TJ = 8 warps x 4 fragments x 8 = 256 columns
   auto fn = seed_left_cols_kernel<NT, MC>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    configured = true;
-  }
+  static unsigned long long configured = 0;
+  set_smem_attr(fn, 232448, configured);
   launch_k(fn, dim3(p.P), dim3(kThreads), smem, s, pdl_enabled(), p, ym, km);
 }
 

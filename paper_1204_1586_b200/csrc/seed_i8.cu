@@ -228,6 +228,18 @@ __device__ __forceinline__ double horner6(uint32_t d0, uint32_t d1, uint32_t d2,
   h = fma(h, 256.0, static_cast<double>(static_cast<int>(d4)));
   return fma(h, 256.0, static_cast<double>(static_cast<int>(d5)));
 }
+// The same recombination for sums over many tiles (the right accumulators run
+// over up to kSeg tiles, |D_0| < 2^27): every diagonal is converted on its own,
+// since the int32 pairing D_0 * 256 + D_1 would overflow.
+__device__ __forceinline__ double horner6_wide(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3, uint32_t d4,
+                                               uint32_t d5) {
+  double h = static_cast<double>(static_cast<int>(d0));
+  h = fma(h, 256.0, static_cast<double>(static_cast<int>(d1)));
+  h = fma(h, 256.0, static_cast<double>(static_cast<int>(d2)));
+  h = fma(h, 256.0, static_cast<double>(static_cast<int>(d3)));
+  h = fma(h, 256.0, static_cast<double>(static_cast<int>(d4)));
+  return fma(h, 256.0, static_cast<double>(static_cast<int>(d5)));
+}
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
@@ -506,7 +518,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const double h = horner6(d[0][e], d[1][e], d[2][e], d[3][e], d[4][e], d[5][e]);
+          const double h = horner6_wide(d[0][e], d[1][e], d[2][e], d[3][e], d[4][e], d[5][e]);
           acc[rc * 8 + e] = fma(h, __ldg(wr + rc * 8 + e), acc[rc * 8 + e]);
         }
       }
@@ -675,8 +687,12 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
 }
 
 // max |Y| -> scale record: [0] 2^(46 - eY), [1] eY, [2] max |Y| (NaN when Y has
-// one), [3] sum |Y| (range guard only; atomics, not bitwise reproducible)
-__global__ void y_amax_kernel(const double* y, int64_t n, unsigned long long* amax, double* asum) {
+// one), [3] sum |Y| (range guard).  Per-block results land in fixed slots and
+// one thread folds them in block order, so the record (and with it the seed
+// path chosen from it) is bitwise reproducible.
+__global__ void y_amax_kernel(const double* y, int64_t n, unsigned long long* bmax, double* bsum) {
+  __shared__ unsigned long long wm[32];
+  __shared__ double ws[32];
   unsigned long long m = 0;
   double a = 0.0;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
@@ -692,19 +708,38 @@ __global__ void y_amax_kernel(const double* y, int64_t n, unsigned long long* am
     m = t > m ? t : m;
     a += __shfl_xor_sync(0xffffffffu, a, o);
   }
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
-    atomicMax(amax, m);
-    atomicAdd(asum, a);
+    wm[warp] = m;
+    ws[warp] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w) {
+      m = wm[w] > m ? wm[w] : m;
+      a += ws[w];
+    }
+    bmax[blockIdx.x] = m;
+    bsum[blockIdx.x] = a;
   }
 }
-__global__ void y_scale_final_kernel(const unsigned long long* amax, const double* asum, double* out) {
-  const double m = __longlong_as_double(static_cast<long long>(*amax));
+// Exponent from frexp for every finite max > 0; a max whose scale 2^(46 - eY)
+// leaves the double range (or a non-finite max / sum) is recorded as is, and the
+// host range guard then keeps the tensor on the fp64 DMMA pass.
+__global__ void y_scale_final_kernel(const unsigned long long* bmax, const double* bsum, int nb, double* out) {
+  unsigned long long mb = 0;
+  double a = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    mb = bmax[b] > mb ? bmax[b] : mb;
+    a += bsum[b];
+  }
+  const double m = __longlong_as_double(static_cast<long long>(mb));
   int e = 0;
-  if (m > 0.0 && m < 1e300) frexp(m, &e);
+  if (m > 0.0 && isfinite(m)) frexp(m, &e);
   out[0] = ldexp(1.0, 46 - e);
   out[1] = static_cast<double>(e);
   out[2] = m;
-  out[3] = *asum;
+  out[3] = a;
 }
 
 }  // namespace
@@ -712,11 +747,8 @@ __global__ void y_scale_final_kernel(const unsigned long long* amax, const doubl
 template <int N, int NL>
 void launch_one_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s) {
   using C = Cfg<N, NL>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(seed_i8_kernel<N, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    configured = true;
-  }
+  static unsigned long long configured = 0;
+  set_smem_attr(seed_i8_kernel<N, NL>, C::kSmem, configured);
   launch_k(seed_i8_kernel<N, NL>, dim3(p.P), dim3(kI8Threads), C::kSmem, s, pdl_enabled(), p, *ymap);
 }
 
@@ -757,15 +789,18 @@ int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_
   return 1;
 }
 
-int launch_y_scale_f64(const double* y, int64_t n, void* scratch, double* out, int num_sms, cudaStream_t s) {
-  unsigned long long* amax = static_cast<unsigned long long*>(scratch);
-  double* asum = reinterpret_cast<double*>(amax + 1);
-  cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned long long), s);
+int y_scale_f64_blocks(int64_t n, int num_sms) {
   int64_t blocks = ceil_div(n, 256);
   if (blocks > 8LL * num_sms) blocks = 8LL * num_sms;
-  if (blocks < 1) blocks = 1;
-  y_amax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(y, n, amax, asum);
-  y_scale_final_kernel<<<1, 1, 0, s>>>(amax, asum, out);
+  return blocks < 1 ? 1 : static_cast<int>(blocks);
+}
+
+int launch_y_scale_f64(const double* y, int64_t n, void* scratch, double* out, int num_sms, cudaStream_t s) {
+  const int blocks = y_scale_f64_blocks(n, num_sms);
+  unsigned long long* bmax = static_cast<unsigned long long*>(scratch);
+  double* bsum = reinterpret_cast<double*>(bmax + blocks);
+  y_amax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(y, n, bmax, bsum);
+  y_scale_final_kernel<<<1, 1, 0, s>>>(bmax, bsum, blocks, out);
   return 2;
 }
 

@@ -468,12 +468,8 @@ int launch_l0_step(const L0Step& st, double* const* gtab, cudaStream_t s) {
   int64_t extra = 0;  // KR values and opB group partials
   for (int i = 0; i < st.nsides; ++i) extra = std::max<int64_t>(extra, st.side[i].M + st.side[i].bq + kL0Threads);
   const size_t smem = static_cast<size_t>(rows + extra) * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(l0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>((3 * kL0MaxRows + kL0Threads) * sizeof(double)));
-    configured = true;
-  }
+  static unsigned long long configured = 0;
+  set_smem_attr(l0_kernel, static_cast<int>((3 * kL0MaxRows + kL0Threads) * sizeof(double)), configured);
   launch_k(l0_kernel, dim3(blocks), dim3(kL0Threads), smem, s, pdl_enabled(), st, gtab);
   return 1;
 }

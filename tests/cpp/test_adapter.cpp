@@ -209,6 +209,27 @@ void test_hook_gauss_seidel() {  // test_mttkrp.cpp:159-186
   CHECK(throws<cpd::ShapeError>([&] {
     cpd::cp_gradient_all(y, bad, nullptr, [&](int n, const cpd::Matrix&) { bad[static_cast<size_t>(n - 1)] = cpd::Matrix(1, 1); }, nullptr);
   }));
+  // whatever the hook throws reaches the caller unchanged, as the reference's direct
+  // hook(orig, G) call propagates it (mttkrp.cpp:134-145): reference types, user types,
+  // non-std exceptions; the context stays usable afterwards
+  struct UserError {
+    int code;
+  };
+  cpd::FactorList h = f0;
+  CHECK(throws<cpd::DomainError>([&] {
+    cpd::cp_gradient_all(y, h, nullptr, [](int, const cpd::Matrix&) { throw cpd::DomainError("hook domain"); }, nullptr);
+  }));
+  CHECK(throws<cpd::ParseError>([&] {
+    cpd::cp_gradient_all(y, h, nullptr, [](int, const cpd::Matrix&) { throw cpd::ParseError("hook parse"); }, nullptr);
+  }));
+  int caught = 0;
+  try {
+    cpd::cp_gradient_all(y, h, nullptr, [](int n, const cpd::Matrix&) { throw UserError{n}; }, nullptr);
+  } catch (const UserError& e) {
+    caught = e.code;
+  }
+  CHECK(caught == cpd::fast_update_order(y.shape()).front());
+  CHECK_LT(max_rel_diff(cpd::cp_gradient_all(y, f0)[0], brute(y, f0, 1)), 1e-12);
 }
 
 void test_counts_and_workspace() {  // test_counts.cpp:16-31, test_mttkrp.cpp:188-198

@@ -322,3 +322,24 @@ def test_forced_pivot_slabs_sum_to_whole(gpu_ctx, oracle):
         assert rel_fro(tot, want[k]) <= 1e-12
     rows = np.concatenate([pp[offs[3]:].reshape(-1, R, order="F") for pp in parts], axis=0)
     assert rel_fro(rows, want[3]) <= 1e-12
+
+
+def test_unsorted_tensor_update_rerecords_graph(gpu_ctx, oracle):
+    # an unsorted tensor is read through a cached sorted copy; refreshing its values
+    # re-permutes into a new buffer, and the recorded gradient graph (which holds the
+    # copy's address and TMA view) must follow it
+    dims, R = [9, 5, 7, 6], 3
+    rng = np.random.default_rng(77)
+    y1 = rng.standard_normal(int(np.prod(dims)))
+    y2 = rng.standard_normal(int(np.prod(dims)))
+    f = [rng.standard_normal((d, R)) for d in dims]
+    t = cpd.DenseTensor.from_values(y1, dims, ctx=gpu_ctx)
+    for _ in range(3):  # eager call, then graph replays
+        cpd.cp_gradient_all(t, f)
+    t.update(y2.ctypes.data)
+    for _ in range(2):
+        g = cpd.cp_gradient_all(t, f)
+        want = oracle.cp_gradient_all(y2, dims, f)[0]
+        for n in range(len(dims)):
+            assert max_rel_diff(g[n], want[n]) < 1e-12, n
+    t.free()

@@ -117,3 +117,19 @@ def test_int8_nonfinite_factor_propagates(gpu_ctx, oracle, i8_env):
     assert np.isnan(g[0][:, 1]).all() and np.isnan(g[1][:, 1]).all()
     assert np.isfinite(g[0][:, 0]).all()
     t.free()
+
+
+def test_int8_right_segments_do_not_overflow(gpu_ctx, i8_env):
+    # 14^7 (c3's shape): ~45 tiles per CTA inside one row block, so the right
+    # accumulators sum many tiles before the drain.  Constant positive Y and
+    # all-ones factors make every digit product the same sign (the worst case for
+    # the int32 diagonal sums); the answer is exact: G(n) = 0.99 * J_N / I_n.
+    dims, R = (14,) * 7, 10
+    y = np.full(14 ** 7, 0.99)
+    t = cpd.DenseTensor.from_values(y, dims, ctx=gpu_ctx)
+    g = cpd.cp_gradient_all(t, [np.ones((14, R)) for _ in dims])
+    assert gpu_ctx.last_seed_path() == 1
+    want = 0.99 * 14 ** 6
+    for n in range(7):
+        assert np.abs(g[n] / want - 1.0).max() < 1e-12, (n, g[n].min(), g[n].max())
+    t.free()
