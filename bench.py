@@ -2,28 +2,34 @@
 """Benchmark of the all-mode CP gradient on B200 (BASELINE.json metric).
 
 A "step" is one all-mode CP gradient (cp_gradient_all) of the workload tensor.
-Default workload (N=1): BASELINE.json configs[1], the 60^4 fp64 tensor with
-R=20 factors, synthetic N(0,1) inputs from the counter-based generator.
-For N>1 (torchrun, one rank per GPU) every rank holds one 60^4 slab of a
-60x60x60x(60N) tensor sharded along its last mode (weak scaling): the local
-gradient runs with the global pivot, then one NCCL all_reduce of the partial
-G(1..3) carrying the G(4) rows at each slab's offset (paper_1204_1586_b200/sharded.py).
+Default workload (N=1): BASELINE.json configs[4] (c5), the largest config that
+fits one GPU: the 300^4 fp32 tensor (32.4 GB, U(-1,1)) with R=64 N(0,1)
+factors, synthetic inputs from the counter-based generator.  For N>1 (torchrun,
+one rank per GPU) the same 300^4 tensor is sharded along its last mode (strong
+scaling, 300 -> 38/38/38/38/37/37/37/37 at N=8): every rank's slab runs with the
+global pivot, then one NCCL all_reduce of the partial G(1..3) carrying the G(4)
+rows at each slab's offset (paper_1204_1586_b200/sharded.py).  The fp64 configs
+c1..c4 run with --config (c2, c3: weak scaling, one slab per GPU).
 
 Timing: W untimed warm-up steps; then exactly K steps bracketed by a barrier +
-cuda synchronize on both sides.  Every step is preceded by an L2 flush (a
-256 MiB device memset, outside the events) because the 104 MB tensor fits in
-the 126 MB L2; each step is timed with CUDA events on the launching stream and
-the max over ranks of the summed step time is reported.
+cuda synchronize on both sides.  Tensors smaller than 4x the 256 MiB flush
+buffer are preceded by an L2 flush (a 256 MiB device memset, outside the
+events); c5's 32.4 GB tensor is far larger than L2.  Each step is timed with
+CUDA events on the launching stream and the max over ranks of the summed step
+time is reported.
 
   value      whole-job tensor bytes per second (GB/s) through the device API
   e2e        same metric through the host C-ABI (cpdgpu_cp_gradient_all): H2D
              copy of Y from pinned host memory + factors in, gradients out
   roofline   dominant kernel = K1 seed contraction, timed with CUDA events on the
-             launching stream.  Large fp64 tensors (c2, c3) run it on the int8
-             tensor cores (seed_i8_kernel): bound = HBM.  Otherwise fp64 DMMA
+             launching stream.  fp32 (c5): seed_f32 on tcgen05 kind::f16, bound =
+             HBM.  Large fp64 tensors (c2, c3) run it on the int8 tensor cores
+             (seed_i8_kernel): bound = HBM.  Otherwise fp64 DMMA
              (seed_f64_kernel, CPDGPU_I8=0 forces it): the slower of the HBM and
              FP64-tensor ideals, the other fraction beside it
-  cpu_baseline  the CPU oracle (a port of the reference) on this host's cores
+  cpu_baseline  the CPU oracle (a port of the reference) on this host's cores;
+             for c5 the streaming restatement (generated fp32 values, fp64
+             arithmetic) on a bounded last-mode slab sample at the global pivot
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle port, all host threads) on the same workload and metric.
@@ -155,23 +161,22 @@ def run_reference(args, cfg):
     n = int(np.prod(sd))
     cores = host_cores()
     esize = 4 if dtype == "f32" else 8
-    if dtype == "f32":  # fp64 oracle on the upcast fp32 values (the reference is fp64-only)
-        y = O.fill_upm1_f32(1, n, nthreads=cores).astype(np.float64)
-    else:
-        y = O.fill_normal(1, n, nthreads=cores)
+    # fp32: the streaming restatement over the generated values (fp64 arithmetic on the
+    # upcast fp32 entries; the reference is fp64-only), a slab at the global pivot
+    y = None if dtype == "f32" else O.fill_normal(1, n, nthreads=cores)
     f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(sd)]
     steps = args.steps
     for _ in range(min(args.warmup, 3)):
-        O.cp_gradient_all(y, sd, f, nthreads=cores)
+        oracle_gradient(O, cfg, sd, cores, y, f)
     t0 = time.perf_counter()
     done = 0
     while done < steps and (done < 3 or time.perf_counter() - t0 < args.cpu_seconds * 6):
-        O.cp_gradient_all(y, sd, f, nthreads=cores)
+        oracle_gradient(O, cfg, sd, cores, y, f)
         done += 1
     dt = time.perf_counter() - t0
     ms = dt / done * 1e3
     gbs = n * esize / (ms * 1e-3) / 1e9
-    what = "full" if sd == list(dims) else f"{'x'.join(map(str, sd))}-slab sample of the"
+    what = "full" if sd == list(dims) else f"{'x'.join(map(str, sd))}-slab sample (global pivot) of the"
     line = {
         "impl": "reference", "metric": f"all-mode CP gradient throughput ({desc})", "value": gbs,
         "unit": "GB/s", "n_gpus": 1, "steps": done, "warmup": min(args.warmup, 3), "ms_per_step": ms,
@@ -420,11 +425,23 @@ def host_memory_ok(nbytes):
 
 
 def sample_dims(dims, dtype):
-    """Bounded CPU sample: the first k last-mode slices of the workload tensor
-    (fp32 configs are sampled; the fp64 configs run in full)."""
+    """Bounded CPU sample: the first k last-mode slices of the workload tensor, a
+    slab at the global pivot (fp32 configs are sampled; the fp64 configs run in full)."""
     if dtype != "f32":
         return list(dims)
-    return list(dims[:-1]) + [4]
+    return list(dims[:-1]) + [10]
+
+
+def oracle_gradient(O, cfg, sd, cores, y=None, f=None):
+    """One CPU-oracle gradient of the sample: fp32 configs through the streaming
+    restatement (generated values, fp64 arithmetic, the workload's global pivot,
+    as a GPU rank runs its slab); fp64 configs on the in-memory tensor."""
+    dims, R, dtype, _ = cfg
+    if dtype == "f32":
+        J = np.cumprod([1] + list(dims))
+        p = max(n for n in range(1, len(dims) + 1) if J[n] <= J[-1] // J[n])
+        return O.cp_gradient_all_upm1_f32(sd, 1, f, pivot=int(p), nthreads=cores)
+    return O.cp_gradient_all(y, sd, f, nthreads=cores)
 
 
 def cpu_baseline(args, cfg, ydev=None):
@@ -434,25 +451,23 @@ def cpu_baseline(args, cfg, ydev=None):
     sd = sample_dims(dims, dtype)
     n = int(np.prod(sd))
     cores = host_cores()
-    if dtype == "f32":  # fp64 oracle on the upcast fp32 values
-        y = O.fill_upm1_f32(1, n, nthreads=cores).astype(np.float64)
-    else:
-        y = O.fill_normal(1, n, nthreads=cores)
+    y = None if dtype == "f32" else O.fill_normal(1, n, nthreads=cores)
     f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(sd)]
-    dims = sd
-    O.cp_gradient_all(y, dims, f, nthreads=cores)
+    oracle_gradient(O, cfg, sd, cores, y, f)
     reps, t0 = 0, time.perf_counter()
     while True:
-        O.cp_gradient_all(y, dims, f, nthreads=cores)
+        oracle_gradient(O, cfg, sd, cores, y, f)
         reps += 1
         if time.perf_counter() - t0 > args.cpu_seconds:
             break
     dt = (time.perf_counter() - t0) / reps
     esize = 4 if dtype == "f32" else 8
-    what = "full" if sd == list(cfg[0]) else f"{'x'.join(map(str, sd))}-slab sample of the"
+    what = "full" if sd == list(cfg[0]) else f"{'x'.join(map(str, sd))}-slab sample (global pivot) of the"
+    how = ("streaming restatement over the generated fp32 values, fp64 arithmetic" if dtype == "f32"
+           else "fp64 arithmetic")
     return {"value": n * esize / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
             "sample": f"{reps} {what} {args.config} gradients (~{args.cpu_seconds:.0f} s), "
-                      "oracle/cpd_oracle.c OpenMP (fp64 arithmetic)",
+                      f"oracle/cpd_oracle.c OpenMP ({how})",
             "ms_per_step": dt * 1e3}
 
 
@@ -679,7 +694,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=list(CONFIGS), default="c5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alg1", action="store_true", help="skip the Algorithm 1 (direct MTTKRP) comparison")

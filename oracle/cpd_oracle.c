@@ -221,21 +221,137 @@ static void seed_left(const double* y, ora_index Jp, ora_index Kp, ora_index R, 
   }
 }
 
+/* ---- streaming seeds over a generated fp32 tensor (config 5) ---------------
+ * Y entries are never held: Y[q] = U(-1,1) fp32 from (seed, offset + q), the
+ * ora_fill_upm1_f32 formula, upcast to fp64; the two seed products of
+ * mttkrp.cpp:160 and :207 are accumulated in fp64 over cache-sized tiles.
+ * Host memory is O(R (J_p + K_p)), so the 32.4 GB fp32 tensor of config 5 is
+ * checked at full size. */
+typedef struct {
+  const double* y; /* in-memory values (column-major), or NULL: generated */
+  uint64_t seed;
+  ora_index offset;
+} ysrc;
+
+static inline double gen_upm1(uint64_t seed, uint64_t idx) {
+  const uint64_t h = ora_hash64(seed, idx);
+  return (double)((float)((int32_t)(h >> 40) - 8388608) * 0x1.0p-23f);
+}
+
+enum { GB_I = 256, GB_C = 64 };
+
+/* right[i + Jp r] = sum_c Y[i + Jp c] KR[c + Kp r]: thread = block of GB_I rows,
+ * accumulators [GB_I][R] (rank fastest), Khatri-Rao rows transposed [Kp][R]. */
+static void seed_right_gen(const ysrc* src, ora_index Jp, ora_index Kp, ora_index R, const double* KR,
+                           double* right, int nth) {
+  double* KT = (double*)malloc((size_t)Kp * (size_t)R * sizeof(double));
+  for (ora_index c = 0; c < Kp; ++c)
+    for (ora_index r = 0; r < R; ++r) KT[c * R + r] = KR[c + Kp * r];
+  const ora_index nb = (Jp + GB_I - 1) / GB_I;
+#pragma omp parallel num_threads(nth)
+  {
+    double* acc = (double*)malloc((size_t)GB_I * (size_t)R * sizeof(double));
+    double yb[GB_I];
+#pragma omp for schedule(dynamic, 1)
+    for (ora_index b = 0; b < nb; ++b) {
+      const ora_index i0 = b * GB_I, ni = (Jp - i0) < GB_I ? (Jp - i0) : GB_I;
+      memset(acc, 0, (size_t)GB_I * (size_t)R * sizeof(double));
+      for (ora_index c = 0; c < Kp; ++c) {
+        const uint64_t base = (uint64_t)(src->offset + i0 + Jp * c);
+        for (ora_index i = 0; i < ni; ++i) yb[i] = gen_upm1(src->seed, base + (uint64_t)i);
+        const double* k = KT + (size_t)c * (size_t)R;
+        for (ora_index i = 0; i < ni; ++i) {
+          double* a = acc + (size_t)i * (size_t)R;
+          const double v = yb[i];
+          for (ora_index r = 0; r < R; ++r) a[r] += v * k[r];
+        }
+      }
+      for (ora_index i = 0; i < ni; ++i)
+        for (ora_index r = 0; r < R; ++r) right[i0 + i + Jp * r] = acc[(size_t)i * (size_t)R + r];
+    }
+    free(acc);
+  }
+  free(KT);
+}
+
+/* left[c + Kp r] = sum_i Y[i + Jp c] KR[i + Jp r]: thread = block of GB_C
+ * columns, rows in chunks of GB_I (Khatri-Rao rows transposed [Jp][R]). */
+static void seed_left_gen(const ysrc* src, ora_index Jp, ora_index Kp, ora_index R, const double* KR,
+                          double* left, int nth) {
+  double* KT = (double*)malloc((size_t)Jp * (size_t)R * sizeof(double));
+  for (ora_index i = 0; i < Jp; ++i)
+    for (ora_index r = 0; r < R; ++r) KT[i * R + r] = KR[i + Jp * r];
+  const ora_index nb = (Kp + GB_C - 1) / GB_C;
+#pragma omp parallel num_threads(nth)
+  {
+    double* acc = (double*)malloc((size_t)GB_C * (size_t)R * sizeof(double));
+    double* yb = (double*)malloc((size_t)GB_C * GB_I * sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+    for (ora_index b = 0; b < nb; ++b) {
+      const ora_index c0 = b * GB_C, nc = (Kp - c0) < GB_C ? (Kp - c0) : GB_C;
+      memset(acc, 0, (size_t)GB_C * (size_t)R * sizeof(double));
+      for (ora_index i0 = 0; i0 < Jp; i0 += GB_I) {
+        const ora_index ni = (Jp - i0) < GB_I ? (Jp - i0) : GB_I;
+        for (ora_index c = 0; c < nc; ++c) {
+          const uint64_t base = (uint64_t)(src->offset + i0 + Jp * (c0 + c));
+          for (ora_index i = 0; i < ni; ++i) yb[c * GB_I + i] = gen_upm1(src->seed, base + (uint64_t)i);
+        }
+        for (ora_index i = 0; i < ni; ++i) {
+          const double* k = KT + (size_t)(i0 + i) * (size_t)R;
+          for (ora_index c = 0; c < nc; ++c) {
+            double* a = acc + (size_t)c * (size_t)R;
+            const double v = yb[c * GB_I + i];
+            for (ora_index r = 0; r < R; ++r) a[r] += v * k[r];
+          }
+        }
+      }
+      for (ora_index c = 0; c < nc; ++c)
+        for (ora_index r = 0; r < R; ++r) left[c0 + c + Kp * r] = acc[(size_t)c * (size_t)R + r];
+    }
+    free(yb);
+    free(acc);
+  }
+  free(KT);
+}
+
+static int cp_gradient_core(int N, const ora_index* dims, const ysrc* src, ora_index R,
+                            double* const* factors, double* const* g_out, ora_hook_fn hook,
+                            void* user, uint64_t* counter, int64_t* peak_ws, int pivot, int nthreads);
+
 int ora_cp_gradient_all(int N, const ora_index* dims, const double* y, ora_index R,
                         double* const* factors, double* const* g_out, ora_hook_fn hook,
                         void* user, uint64_t* counter, int64_t* peak_ws, int pivot,
                         int nthreads) {
+  const ysrc src = {y, 0, 0};
+  return cp_gradient_core(N, dims, &src, R, factors, g_out, hook, user, counter, peak_ws, pivot, nthreads);
+}
+
+int ora_cp_gradient_all_upm1_f32(int N, const ora_index* dims, uint64_t seed, ora_index offset, ora_index R,
+                                 double* const* factors, double* const* g_out, int pivot, int nthreads) {
+  if (N < 2 || N > MAXN) return ORA_ARG;
+  const ysrc src = {NULL, seed, offset};
+  return cp_gradient_core(N, dims, &src, R, factors, g_out, NULL, NULL, NULL, NULL, pivot, nthreads);
+}
+
+static int cp_gradient_core(int N, const ora_index* dims, const ysrc* src, ora_index R,
+                            double* const* factors, double* const* g_out, ora_hook_fn hook,
+                            void* user, uint64_t* counter, int64_t* peak_ws, int pivot, int nthreads) {
+  const double* y = src->y;
   if (N < 2) return ORA_ARG; /* mttkrp.cpp:119 */
   if (N > MAXN || R < 1) return ORA_ARG;
   const int nth = set_threads(nthreads);
   int perm[MAXN];
-  const int identity = ora_sort_perm(N, dims, perm, NULL); /* mttkrp.cpp:123 */
+  int identity = ora_sort_perm(N, dims, perm, NULL); /* mttkrp.cpp:123 */
+  if (!y) { /* generated Y is read in the caller's frame (a slab of an ascending tensor) */
+    for (int j = 0; j < N; ++j) perm[j] = j + 1;
+    identity = 1;
+  }
   ora_index sd[MAXN], J[MAXN + 1];
   for (int j = 0; j < N; ++j) sd[j] = dims[perm[j] - 1];
   prefix_products(N, sd, J);
   const double* ys = y;
   double* yperm = NULL;
-  if (!identity) {
+  if (!identity && y) {
     yperm = (double*)malloc((size_t)J[N] * sizeof(double));
     ora_permute(N, dims, y, perm, yperm);
     ys = yperm;
@@ -280,7 +396,10 @@ int ora_cp_gradient_all(int N, const ora_index* dims, const double* y, ora_index
       kron_range_column(sd, sf, p + 1, N, r, KR + (size_t)r * (size_t)Kp, counter);
     track(&ws, Jp * R);
     if (counter) *counter += (uint64_t)Jp * (uint64_t)Kp * (uint64_t)R;
-    seed_right(ys, Jp, Kp, R, KR, right, nth);
+    if (ys)
+      seed_right(ys, Jp, Kp, R, KR, right, nth);
+    else
+      seed_right_gen(src, Jp, Kp, R, KR, right, nth);
     free(KR);
     track(&ws, -Kp * R);
   }
@@ -330,7 +449,10 @@ int ora_cp_gradient_all(int N, const ora_index* dims, const double* y, ora_index
         kron_range_column(sd, sf, 1, p, r, KR + (size_t)r * (size_t)Jp, counter);
       track(&ws, Kp * R);
       if (counter) *counter += (uint64_t)Kp * (uint64_t)Jp * (uint64_t)R;
-      seed_left(ys, Jp, Kp, R, KR, left, nth);
+      if (ys)
+        seed_left(ys, Jp, Kp, R, KR, left, nth);
+      else
+        seed_left_gen(src, Jp, Kp, R, KR, left, nth);
       free(KR);
       track(&ws, -Jp * R);
     }

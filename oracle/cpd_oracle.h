@@ -45,6 +45,14 @@ int ora_cp_gradient_all(int N, const ora_index* dims, const double* y, ora_index
                         int64_t* peak_ws, int pivot, int nthreads);
 
 /* entrywise definition (test_util.hpp:44-60) */
+/* The same all-mode gradient of a GENERATED fp32 tensor, in the caller frame
+ * (no mode sort: ascending dims, or a last-mode slab with a forced pivot):
+ * Y[q] = U(-1,1) from (seed, offset + q) as ora_fill_upm1_f32, upcast to fp64,
+ * streamed through the two seeds so host memory stays O(R (J_p + K_p)) —
+ * config 5 (300^4, 32.4 GB in fp32) at full size.  offset = first global index
+ * of a last-mode slab. */
+int ora_cp_gradient_all_upm1_f32(int N, const ora_index* dims, uint64_t seed, ora_index offset, ora_index R,
+                                 double* const* factors, double* const* g_out, int pivot, int nthreads);
 int ora_brute_mttkrp(int N, const ora_index* dims, const double* y, ora_index R,
                      const double* const* factors, int n, double* out);
 

@@ -129,6 +129,21 @@ def cp_gradient_all(y, dims, factors, hook=None, counter=None, pivot=0, nthreads
     return grads, int(cnt.value), int(peak.value)
 
 
+def cp_gradient_all_upm1_f32(dims, seed, factors, offset=0, pivot=0, nthreads=0):
+    """All-mode gradient of the generated fp32 U(-1,1) tensor (fill_upm1_f32 values,
+    upcast to fp64) without materialising it: the streaming restatement used for
+    config 5 at full size (ascending dims)."""
+    L = load()
+    bufs = _fbufs(factors)
+    R = bufs[0].shape[1]
+    grads = [np.zeros((int(d), R), order="F") for d in dims]
+    st = L.ora_cp_gradient_all_upm1_f32(len(dims), _dims(dims), C.c_uint64(int(seed)), c_i64(int(offset)),
+                                        c_i64(R), _ptrs(bufs), _ptrs(grads), int(pivot), int(nthreads))
+    if st:
+        raise ValueError(f"oracle status {st}")
+    return grads
+
+
 def brute_mttkrp(y, dims, factors, n):
     yv = vec(y)
     bufs = _fbufs(factors)

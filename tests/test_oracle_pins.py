@@ -446,3 +446,22 @@ def test_run_every_algorithm_pins(oracle):
     for a, b in zip(ff, fd):
         assert max_rel_diff(a, b) < 1e-12
     assert np.allclose(tf["cost"], td["cost"], rtol=1e-10)
+
+
+def test_streaming_f32_oracle_equals_in_memory(oracle):
+    """The config-5 streaming restatement (generated fp32 U(-1,1) values, never
+    materialised) equals the in-memory restatement on the same upcast values,
+    including slab offsets and a forced pivot in the caller's frame."""
+    import numpy as np
+    for dims, R, off, piv in [([3, 7, 9, 11], 5, 12345, 0), ([3, 300], 4, 0, 0),
+                              ([2, 2, 2, 2, 2, 3], 3, 7, 0), ([6, 6, 6, 4], 9, 6 ** 3 * 5, 2)]:
+        n = int(np.prod(dims))
+        y = oracle.fill_upm1_f32(11, n, offset=off).astype(np.float64)
+        f = [np.random.default_rng(k).standard_normal((d, R)) for k, d in enumerate(dims)]
+        want = oracle.cp_gradient_all(y, dims, f, pivot=piv)[0] if piv == 0 or list(dims) == sorted(dims) \
+            else None
+        got = oracle.cp_gradient_all_upm1_f32(dims, 11, f, offset=off, pivot=piv)
+        if want is None:  # unsorted slab: compare against the brute-force oracle
+            want = [oracle.brute_mttkrp(y, dims, f, m) for m in range(1, len(dims) + 1)]
+        for a, b in zip(got, want):
+            assert np.abs(a - b).max() <= 1e-12 * max(np.abs(b).max(), 1.0)
