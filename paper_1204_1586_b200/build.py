@@ -17,7 +17,7 @@ LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libcpdgpu.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["cpdgpu.cu", "seed_f64.cu", "seed_i8.cu", "seed_f32.cu", "tail.cu", "util.cu", "als.cu"]
+SOURCES = ["cpdgpu.cu", "seed_f64.cu", "seed_i8.cu", "seed_f32.cu", "seed_f32f.cu", "tail.cu", "util.cu", "als.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",

@@ -116,6 +116,31 @@ size_t seed_f32_smem_bytes();
 int seed_f32_rank_cols();         // 64
 int64_t seed_f32_tile_bytes();    // bytes of one Khatri-Rao tile (64 rows)
 int launch_seed_f32(const Seed32Params& p, const CUtensorMap* ymap, int left, cudaStream_t s);
+// ---- K1 for fp32 tensors, both seeds in one HBM pass (seed_f32f.cu) ------------
+// unit = (band of seed_f32f_band_tiles() 128-row tiles, one 64-column tile); CTA c
+// owns units [c U / P, (c + 1) U / P) band-major.  Outputs: the right seed as
+// fp64 partial blocks [slot][64 r][128 i] (slot = (c slots + band - first band) 3
+// + row tile in band; CSR per row tile for the tail), the left seed as fp32
+// partials [band][column tile][64 r][64 j] in scaled units (kOpReduceLeft32 sums
+// the bands).
+struct Seed32FParams {
+  const unsigned char* kr_tiles;  // [nC][16 KB] right Khatri-Rao tiles (kr_split layout)
+  const void* krl_img;            // [nRT][128][128] fp16 KRl^T image (launch_krl_image)
+  const float* scale_y;           // [1] power-of-two Y scale
+  const double* inv_scale_y;      // [1]
+  const double* inv_scale_kr;     // [64] right Khatri-Rao column unscales
+  double* rpart;
+  float* lpart;
+  int64_t nRT, nC, units;
+  int P, slots, window;
+  int knobs;  // CPDGPU_F32F_KNOBS timing experiments (wrong results): 1 no split stores,
+              // 2 one right MMA per k-step, 4 one left MMA per k-step, 8 no left partial stores
+};
+int seed_f32f_band_tiles();  // 3
+// ymap: the right pass's map (box 128 i x 64 j, no swizzle)
+int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream_t s);
+// fp64 rows [L][ld] (ld <= 64) -> KRl^T TMEM image [ceil(L / 128)][128][128] fp16
+int launch_krl_image(const double* rows, int64_t L, int ld, const double* scale, void* img, cudaStream_t s);
 // column scales of the right (scale[0..63]) and left (scale[64..127]) Khatri-Rao rows
 int launch_kr_scale(const KRSpec& right, const KRSpec& left, int R, double* scale, double* inv, cudaStream_t s);
 // fp64 rows [L][ld] (ld <= 64) -> tiles (see Seed32Params::kr_tiles)
@@ -129,7 +154,14 @@ int launch_pad_rows_f32(const float* src, float* dst, int64_t J, int64_t J8, int
 bool make_tensor_map_y32(CUtensorMap* out, const void* base, int64_t J8, int64_t K, int left);
 
 // ---- prologue + recursion tail (tail.cu) ------------------------------------
-enum TailOpType { kOpNone = 0, kOpContractA = 1, kOpContractB = 2, kOpReduceRight = 3, kOpReduceLeft = 4 };
+enum TailOpType {
+  kOpNone = 0,
+  kOpContractA = 1,
+  kOpContractB = 2,
+  kOpReduceRight = 3,
+  kOpReduceLeft = 4,
+  kOpReduceLeft32 = 5  // Ls[r][j] = us_y us_r[r] sum_b Z32[((b ldz + j / 64) 64 + r) 64 + j % 64] (fused fp32 seed)
+};
 
 // One rank-batched contraction / reduction (all R columns):
 //  ContractA: out[r*ldo + b] = sum_{a<M} Z[r*ldz + a + M*b] * KR(kr)[a, r]   (Eq 3.12 / 3.22)
@@ -152,6 +184,9 @@ struct TailOp {
   const int* rb_ptr;
   const int* slot_list;
   int cta;  // set by launch_tail_step: long contractions run one output per CTA
+  const float* Z32;                    // kOpReduceLeft32: fp32 partials, scaled units
+  const double* us_y;                  // ... and their unscale, us_y[0] * us_r[r]
+  const double* us_r;
 };
 constexpr int kMaxTailOps = 8;
 struct TailStep {

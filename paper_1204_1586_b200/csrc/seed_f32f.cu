@@ -1,0 +1,579 @@
+// seed_f32f.cu — both split-point seeds of an fp32 tensor in ONE pass over Y on
+// the 5th-generation tensor cores (tcgen05.mma kind::f16, accumulators in TMEM).
+//
+//   right  Rs[i, r] = sum_j Y[i + J j] KR(p+1..N)[j, r]   (mttkrp.cpp:149-163)
+//   left   Ls[j, r] = sum_i Y[i + J j] KR(1..p)[i, r]     (mttkrp.cpp:195-210)
+//
+// Both reference products read the same J_p x K_p view of Y (mttkrp.cpp:160,
+// 207); here every 128 i x 64 j tile of it is read from HBM once, split once
+// into fp16 hi / lo planes in shared memory, and feeds both products:
+//
+//   right  D_R[i][r]  += Y[i][j]   KRr[j][r]   A = Y plane (smem, MN-major: i
+//                                              contiguous), B = KRr tile (smem,
+//                                              K-major), M = 128 i, N = 64 r
+//   left   D_L[m][j]  += KRl^T[m][i] Y[i][j]   A = KRl^T (TMEM: lane m = 2 r
+//                                              holds the hi part of rank r,
+//                                              lane 2 r + 1 the lo part), B =
+//                                              the same Y plane read K-major,
+//                                              M = 128, N = 64 j
+//
+// fp32 accuracy from fp16 tensor cores: x = x_hi + x_lo (22 significant bits);
+// right: Y_hi KR_hi + Y_hi KR_lo + Y_lo KR_hi into one accumulator; left: both
+// Y planes against the interleaved [KR_hi; KR_lo] rows, the lane pairs added
+// at the drain with one shuffle (the extra lo * lo term only adds accuracy).
+// Y and every Khatri-Rao column are scaled by powers of two into [-1, 1] first
+// (exact).
+//
+// Work: unit = (band of kA = 3 row tiles, one 64-column tile); a CTA walks a
+// contiguous range of units band-major, so its three right accumulators (one
+// per row tile) persist across a band's columns while the left accumulator
+// covers 384 rows of one column tile per unit:
+//   right: the fp32 TMEM accumulators are drained every `window` units (tensor-
+//          core fp32 accumulation truncates: 256-column windows keep ~1e-6) into
+//          fp32 registers of the drain warps, and written once per band segment
+//          as an fp64 partial block (a few slots per row tile: tail reduction).
+//   left:  one fp32 partial [64 r][64 j] per unit, summed over the bands in
+//          fp64 by the tail (kOpReduceLeft32).
+//
+// Pipeline (one CTA per SM, persistent, 512 threads):
+//   warp 12      producer: TMA of the fp32 Y tiles into a 4-slot landing ring,
+//                bulk copy of the KRr tiles
+//   warps 0-3    split: thread = row pair x column half; reads its 64 fp32
+//                values, frees the landing slot, converts, and writes fp16 hi /
+//                lo words into a 2-slot plane ring (128-byte-swizzled operand
+//                layout).  The landing ring holds 128 KB of loads in flight and
+//                is released right after the split reads it, not after the MMAs.
+//   warp 13      MMAs: the whole warp waits, one elected lane issues (uniform
+//                operands: no per-instruction waterfall), commits free slots
+//   warps 4-11   drains: TMEM lane quarter w % 4 x rank / column half: the
+//                right windows, the left partial per unit, the band's KRl^T image
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.h"
+
+namespace cpdgpu {
+namespace {
+
+constexpr int kTI = 128;                      // tile rows (i) = right MMA M
+constexpr int kTJ = 64;                       // tile columns (j) = left MMA N
+constexpr int kA = 3;                         // row tiles per band
+constexpr int kRP = 64;                       // rank columns (right MMA N)
+constexpr int kNL = 4;                        // fp32 landing slots (loads in flight)
+constexpr int kNP = 2;                        // fp16 plane slots (split -> MMA)
+constexpr int kYBytes = kTI * kTJ * 4;        // 32 KB fp32 tile
+constexpr int kPlane = kTI * kTJ * 2;         // 16 KB fp16 plane: [i half][64 j][128 B]
+constexpr int kKRBytes = 2 * kTJ * kRP * 2;   // 16 KB KRr tile: [hi | lo][64 r][64 j] (kr_split)
+constexpr int kSplitWarps = 4, kDrainWarps = 8;  // drains: lane quarter x column half
+constexpr int kWDrain0 = kSplitWarps, kWProd = kSplitWarps + kDrainWarps, kWMma = kWProd + 1;
+constexpr int kThreads = (kWMma + 3) * 32;  // + 2 idle warps: 16 warps keep 128 registers per thread
+constexpr uint32_t kColR = 0;                 // D_R[t]: columns [64 t, 64 t + 64)
+constexpr uint32_t kColK = kA * kRP;          // KRl^T[t]: [192 + 64 t, +64)
+constexpr uint32_t kColL = 2 * kA * kRP;      // D_L[lb]: [384 + 64 lb, +64)
+constexpr int kTmemCols = 512;
+constexpr int kOffPlanes = kNL * kYBytes;
+constexpr int kOffKR = kOffPlanes + kNP * 2 * kPlane;
+constexpr int kOffBars = kOffKR + 2 * kKRBytes;
+constexpr int kSmem = 1024 + kOffBars + 512 + kRP * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p != 0;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// tcgen05 shared-memory matrix descriptor (sm_100 version 1): start, leading / stride
+// byte offsets, layout type 2 = 128-byte swizzle (atoms of 8 rows x 128 B).  The
+// start field is addr >> 4 in the low 14 bits: a byte offset d (< 256 KB total)
+// is added to a descriptor as d >> 4.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+// Instruction descriptor kind::f16: fp16 A / B, fp32 D, M = 128, N = 64, A major.
+__host__ __device__ constexpr uint32_t idesc_f16(bool a_mn_major) {
+  return (1u << 4) | ((a_mn_major ? 1u : 0u) << 15) | (static_cast<uint32_t>(64 >> 3) << 17) |
+         (static_cast<uint32_t>(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+// 32 lanes x 16 consecutive 32-bit columns (no wait: the caller waits once)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 (&q)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(taddr),
+      "r"(q[0].x), "r"(q[0].y), "r"(q[0].z), "r"(q[0].w), "r"(q[1].x), "r"(q[1].y), "r"(q[1].z), "r"(q[1].w),
+      "r"(q[2].x), "r"(q[2].y), "r"(q[2].z), "r"(q[2].w), "r"(q[3].x), "r"(q[3].y), "r"(q[3].z), "r"(q[3].w),
+      "r"(q[4].x), "r"(q[4].y), "r"(q[4].z), "r"(q[4].w), "r"(q[5].x), "r"(q[5].y), "r"(q[5].z), "r"(q[5].w),
+      "r"(q[6].x), "r"(q[6].y), "r"(q[6].z), "r"(q[6].w), "r"(q[7].x), "r"(q[7].y), "r"(q[7].z), "r"(q[7].w)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Unit walk of one CTA: units [a, b) of u = band * nC + column tile (32-bit: a
+// tensor that fits in HBM has far fewer than 2^31 units of 32 KB).
+struct FWalk {
+  int a, b, nC, nRT;
+  int window;
+  __device__ int band(int u) const { return u / nC; }
+  __device__ int tiles(int u) const {
+    const int r = nRT - band(u) * kA;
+    return r < kA ? r : kA;
+  }
+  __device__ bool band_start(int u) const { return u == a || u % nC == 0; }
+  __device__ bool seg_end(int u) const { return u + 1 == b || (u + 1) % nC == 0; }
+  // position of u in its segment (the CTA's run of units inside one band)
+  __device__ int seg_pos(int u) const {
+    const int s0 = u - u % nC;
+    return u - (s0 > a ? s0 : a);
+  }
+  __device__ bool win_end(int u) const { return seg_end(u) || seg_pos(u) % window == window - 1; }
+  __device__ bool win_start(int u) const { return band_start(u) || seg_pos(u) % window == 0; }
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    seed_f32f_kernel(const Seed32FParams p, const __grid_constant__ CUtensorMap ymap) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cta = blockIdx.x;
+  FWalk w;
+  w.a = static_cast<int>(static_cast<int64_t>(cta) * p.units / p.P);
+  w.b = static_cast<int>(static_cast<int64_t>(cta + 1) * p.units / p.P);
+  w.nC = static_cast<int>(p.nC);
+  w.nRT = static_cast<int>(p.nRT);
+  w.window = p.window;
+  const int seg0 = w.a / w.nC;  // first band of this CTA (segment index = band - seg0)
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const uint32_t land_u = smem_u32(base);                // [kNL][32 KB] fp32 tiles
+  const uint32_t planes_u = smem_u32(base + kOffPlanes);  // [kNP][hi 16 KB | lo 16 KB]
+  const uint32_t krt_u = smem_u32(base + kOffKR);         // [2][16 KB] KRr tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kOffBars);
+  uint64_t* full = bars;                 // [kNL] Y tile landed            (1 + tx)
+  uint64_t* lfree = full + kNL;          // [kNL] landing slot read        (4 split warps)
+  uint64_t* pfull = lfree + kNL;         // [kNP] planes written           (4 split warps)
+  uint64_t* pfree = pfull + kNP;         // [kNP] planes consumed          (MMA commit)
+  uint64_t* kfull = pfree + kNP;         // [2] KRr tile landed            (1 + tx)
+  uint64_t* kempty = kfull + 2;          // [2] KRr tile consumed          (MMA commit)
+  uint64_t* lfull = kempty + 2;          // [2] left unit accumulated      (MMA commit)
+  uint64_t* lempty = lfull + 2;          // [2] left accumulator drained   (8 drain warps)
+  uint64_t* rfull = lempty + 2;          // [kA] right window accumulated  (MMA commit)
+  uint64_t* rempty = rfull + kA;         // [kA] right window drained      (the row tile's 4 drain warps)
+  uint64_t* kl_full = rempty + kA;       // band's KRl^T in TMEM           (8 drain warps)
+  uint64_t* kl_free = kl_full + 1;       // band's MMAs done               (MMA commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kl_free + 1);
+  double* unscale = reinterpret_cast<double*>(base + kOffBars + 512);  // [64] 1 / (scale_y scale_r)
+
+  if (tid == 0) {
+    for (int s = 0; s < kNL; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&lfree[s], kSplitWarps);
+    }
+    for (int s = 0; s < kNP; ++s) {
+      mbar_init(&pfull[s], kSplitWarps);
+      mbar_init(&pfree[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+      mbar_init(&lfull[s], 1);
+      mbar_init(&lempty[s], kDrainWarps);
+    }
+    for (int t = 0; t < kA; ++t) {
+      mbar_init(&rfull[t], 1);
+      mbar_init(&rempty[t], kDrainWarps);
+    }
+    mbar_init(kl_full, kDrainWarps);
+    mbar_init(kl_free, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp != kWProd) pdl_wait();  // scales, Khatri-Rao images: the preceding kernels
+  if (tid < kRP) unscale[tid] = p.inv_scale_y[0] * p.inv_scale_kr[tid];
+  if (warp == kWMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (warp == kWProd && lane == 0)
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&ymap)));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == kWProd) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_y = policy_evict_first(), pol_k = policy_evict_last();
+      int k = 0;  // running tile index
+      bool waited = false;
+      for (int u = w.a; u < w.b; ++u) {
+        const int b = w.band(u), c = u % w.nC;
+        const int nt = w.tiles(u);
+        const int ul = u - w.a;
+        for (int t = 0; t < nt; ++t, ++k) {
+          const int s = k % kNL;
+          if (k >= kNL) mbar_wait(&lfree[s], static_cast<uint32_t>((k / kNL - 1) & 1));
+          mbar_arrive_tx(&full[s], kYBytes);
+          tma_load_2d(land_u + s * kYBytes, &ymap, static_cast<int>((b * kA + t) * kTI), static_cast<int>(c * kTJ),
+                      &full[s], pol_y);
+          if (t == 0) {  // the unit's KRr tile (Khatri-Rao images come from the preceding kernels)
+            if (!waited) {
+              pdl_wait();
+              waited = true;
+            }
+            const int ks = static_cast<int>(ul & 1);
+            if (ul >= 2) mbar_wait(&kempty[ks], static_cast<uint32_t>(((ul >> 1) - 1) & 1));
+            mbar_arrive_tx(&kfull[ks], kKRBytes);
+            bulk_load(krt_u + ks * kKRBytes, p.kr_tiles + static_cast<int64_t>(c) * kKRBytes, kKRBytes, &kfull[ks],
+                      pol_k);
+          }
+        }
+      }
+    }
+  } else if (warp == kWMma) {
+    // ------------------------------------------------------------------ MMA issuer
+    // The whole warp runs the loop and waits; one elected lane issues.  Every
+    // operand below is warp-uniform, so the MMAs go out back to back.
+    constexpr uint32_t id_r = idesc_f16(true), id_l = idesc_f16(false);
+    const uint64_t dA0 = sdesc(planes_u, 8192, 1024);  // right A: Y plane, MN-major
+    const uint64_t dB0 = sdesc(krt_u, 16, 1024);       // right B: KRr tile, K-major
+    const uint64_t dL0 = sdesc(planes_u, 16, 1024);    // left B: Y plane, K-major
+    const bool all_terms_r = !(p.knobs & 2), all_terms_l = !(p.knobs & 4);
+    int k = 0, bc = 0;
+    int wc[kA] = {0, 0, 0};  // right windows started per row tile
+    for (int u = w.a; u < w.b; ++u) {
+      const int nt = w.tiles(u);
+      const int ul = u - w.a;
+      const int ks = static_cast<int>(ul & 1), lb = static_cast<int>(ul & 1);
+      if (w.band_start(u)) mbar_wait(kl_full, static_cast<uint32_t>(bc & 1));
+      if (ul >= 2) mbar_wait(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1));
+      mbar_wait(&kfull[ks], static_cast<uint32_t>((ul >> 1) & 1));
+      tc_fence_after();
+      const bool wstart = w.win_start(u), wend = w.win_end(u);
+      const uint64_t kb = dB0 + static_cast<uint64_t>((ks * kKRBytes) >> 4);
+      const uint32_t dL = tmem + kColL + kRP * lb;
+#pragma unroll
+      for (int t = 0; t < kA; ++t) {
+        if (t >= nt) break;
+        const int ps = k % kNP;
+        if (wstart && wc[t] > 0) mbar_wait(&rempty[t], static_cast<uint32_t>((wc[t] - 1) & 1));
+        mbar_wait(&pfull[ps], static_cast<uint32_t>((k / kNP) & 1));
+        tc_fence_after();
+        const uint64_t pa = static_cast<uint64_t>((ps * 2 * kPlane) >> 4);
+        const uint64_t aH = dA0 + pa, aL = aH + (kPlane >> 4), lH = dL0 + pa, lL = lH + (kPlane >> 4);
+        const uint32_t dR = tmem + kColR + kRP * t, aK = tmem + kColK + kRP * t;
+        if (elect_one()) {
+          // right: K = 64 columns j in 4 steps of 16 (2 KB of plane rows each)
+#pragma unroll
+          for (int q = 0; q < kTJ / 16; ++q) {
+            mma_ss(dR, aH + q * 128, kb + q * 2, id_r, (wstart && q == 0) ? 0u : 1u);
+            if (all_terms_r) {
+              mma_ss(dR, aH + q * 128, kb + 512 + q * 2, id_r, 1u);
+              mma_ss(dR, aL + q * 128, kb + q * 2, id_r, 1u);
+            }
+          }
+          // left: K = 128 rows i in 8 steps of 16 (i half q / 4, 32 B steps inside the 128 B rows)
+#pragma unroll
+          for (int q = 0; q < kTI / 16; ++q) {
+            const uint32_t off = ((q >> 2) * 8192 + (q & 3) * 32) >> 4;
+            mma_ts(dL, aK + 8 * q, lH + off, id_l, (t == 0 && q == 0) ? 0u : 1u);
+            if (all_terms_l) mma_ts(dL, aK + 8 * q, lL + off, id_l, 1u);
+          }
+          umma_commit(&pfree[ps]);
+          if (wend) umma_commit(&rfull[t]);
+        }
+        __syncwarp();
+        if (wend) ++wc[t];
+        ++k;
+      }
+      if (elect_one()) {
+        umma_commit(&kempty[ks]);
+        umma_commit(&lfull[lb]);
+        if (w.seg_end(u)) umma_commit(kl_free);
+      }
+      __syncwarp();
+      if (w.seg_end(u)) ++bc;
+    }
+  } else if (warp > kWMma) {
+    // idle (warps 14, 15: 16 warps keep the 128-register budget)
+  } else if (warp < kWDrain0) {
+    // ------------------------------------------------------------------ split
+    // thread = row pair (2 pr, 2 pr + 1) x column half jh: 32 float2 loads (one
+    // 8-byte row pair per column, conflict-free), then per column one packed hi
+    // and one packed lo word at the pair's position of the swizzled planes
+    // (the 32 lanes of a warp cover one 128-byte plane row: no bank conflicts).
+    const float sy = p.scale_y[0];
+    const bool scale = sy != 1.0f, store = !(p.knobs & 1);
+    const int st = warp * 32 + lane;
+    const int pr = st & 63, jh = st >> 6;
+    const int i0 = 2 * pr, c0 = (i0 & 63) >> 3;
+    uint32_t base8[8];  // plane offset of column j (j % 8 == k) minus j * 128
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      base8[k] = (i0 >> 6) * 8192 + jh * 32 * 128 + (((c0 ^ k)) << 4) + (i0 & 7) * 2;
+    const unsigned char* land = base;
+    int k = 0;
+    for (int u = w.a; u < w.b; ++u) {
+      const int nt = w.tiles(u);
+      for (int t = 0; t < nt; ++t, ++k) {
+        const int ls = k % kNL, ps = k % kNP;
+        mbar_wait(&full[ls], static_cast<uint32_t>((k / kNL) & 1));
+        const float2* src = reinterpret_cast<const float2*>(land + ls * kYBytes) + jh * 32 * (kTI / 2) + pr;
+        uint32_t hw[32], lw[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          float2 x = src[e * (kTI / 2)];
+          if (scale) {
+            x.x *= sy;
+            x.y *= sy;
+          }
+          hw[e] = pack_half2(x.x, x.y);
+          const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&hw[e]));
+          lw[e] = pack_half2(x.x - back.x, x.y - back.y);
+        }
+        __syncwarp();  // every lane's reads of the landing slot are done (their values are in use)
+        if (lane == 0) mbar_arrive(&lfree[ls]);
+        if (k >= kNP) mbar_wait(&pfree[ps], static_cast<uint32_t>((k / kNP - 1) & 1));
+        if (store) {
+          const uint32_t hi = planes_u + ps * 2 * kPlane, lo = hi + kPlane;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const uint32_t off = base8[e & 7] + e * 128;
+            asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(hi + off), "r"(hw[e]) : "memory");
+            asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(lo + off), "r"(lw[e]) : "memory");
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> MMA reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[ps]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ drains
+    // warp (q, h): TMEM lane quarter q (== warp % 4), column half h: ranks
+    // [32 h, 32 h + 32) of the three right accumulators (fp32 second-level sums),
+    // the KRl^T image words [32 h, 32 h + 32), left-partial columns [32 h, +32)
+    const int d = warp - kWDrain0, q = d & 3, h = d >> 2;
+    const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+    const int odd = lane & 1;
+    const bool lstore = !(p.knobs & 8);
+    float acc[kA][32];
+#pragma unroll
+    for (int t = 0; t < kA; ++t)
+#pragma unroll
+      for (int e = 0; e < 32; ++e) acc[t][e] = 0.0f;
+    int bc = 0, wc = 0;
+    for (int u = w.a; u < w.b; ++u) {
+      const int nt = w.tiles(u);
+      const int b = w.band(u), ul = u - w.a, c = u % w.nC;
+      const int lb = ul & 1;
+      if (w.band_start(u)) {  // the band's KRl^T image into TMEM, once its previous band is done
+        if (bc > 0) mbar_wait(kl_free, static_cast<uint32_t>((bc - 1) & 1));
+        __syncwarp();
+        tc_fence_after();
+        for (int t = 0; t < nt; ++t) {
+          const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __half*>(p.krl_img) +
+                                                            (static_cast<int64_t>(b * kA + t) * 128 + q * 32 + lane) *
+                                                                kTI) +
+                             h * 8;  // words [32 h, 32 h + 32) of the slot's 64
+          uint4 x[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = __ldg(src + e);
+          tmem_st32(tmem + lanes + kColK + kRP * t + 32 * h, x);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kl_full);
+      }
+      // right: drain the window into the fp32 second level (before the left drain:
+      // the next window's first MMA into these accumulators waits for it)
+      if (w.win_end(u)) {
+#pragma unroll
+        for (int t = 0; t < kA; ++t) {
+          if (t >= nt) break;
+          mbar_wait(&rfull[t], static_cast<uint32_t>(wc & 1));
+          __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin
+          tc_fence_after();
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8) {
+            uint32_t y[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                         : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3]), "=r"(y[4]), "=r"(y[5]), "=r"(y[6]),
+                           "=r"(y[7])
+                         : "r"(tmem + lanes + kColR + kRP * t + 32 * h + 8 * c8));
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[t][8 * c8 + e] += __uint_as_float(y[e]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rempty[t]);
+        }
+        ++wc;
+      }
+      // left: lanes (2 r', 2 r' + 1) hold the hi / lo products of rank 16 q + r';
+      // per 8-column chunk the pair sums with one shuffle and each lane stores 4
+      mbar_wait(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1));
+      __syncwarp();
+      tc_fence_after();
+      const int r = 16 * q + (lane >> 1);
+      float* lrow = p.lpart + ((static_cast<int64_t>(b) * w.nC + c) * kRP + r) * kTJ + 32 * h + 4 * odd;
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint32_t v[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(tmem + lanes + kColL + kRP * lb + 32 * h + 8 * c8));
+        tmem_wait_ld();
+        if (c8 == 3) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&lempty[lb]);
+        }
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float keep = __uint_as_float(odd ? v[4 + e] : v[e]);  // the columns this lane stores
+          const float give = __uint_as_float(odd ? v[e] : v[4 + e]);  // the partner's columns
+          o[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+        }
+        if (lstore) *reinterpret_cast<float4*>(lrow + 8 * c8) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+      if (w.seg_end(u)) {
+        const int64_t slot0 = (static_cast<int64_t>(cta) * p.slots + (b - seg0)) * kA;  // CSR slots
+#pragma unroll
+        for (int t = 0; t < kA; ++t) {
+          if (t >= nt) break;
+          double* out = p.rpart + ((slot0 + t) * kRP + 32 * h) * kTI + q * 32 + lane;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            out[e * kTI] = static_cast<double>(acc[t][e]) * unscale[32 * h + e];
+            acc[t][e] = 0.0f;
+          }
+        }
+        ++bc;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWMma) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// KRl^T image for the left MMA's TMEM A operand: [row tile][128 slots][128 i] fp16,
+// slot m = 2 r: hi part of rank r, m = 2 r + 1: its lo part, from the fp64
+// Khatri-Rao rows [L][ld] scaled by the left column scales; rows past L are zero.
+__global__ void krl_image_kernel(const double* __restrict__ rows, int64_t L, int ld, const double* __restrict__ scale,
+                                 __half* __restrict__ img, int64_t ntiles) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // (tile, slot, i)
+  if (e >= ntiles * 128 * kTI) return;
+  const int i = static_cast<int>(e % kTI);
+  const int m = static_cast<int>((e / kTI) % 128);
+  const int64_t t = e / (static_cast<int64_t>(kTI) * 128);
+  const int r = m >> 1;
+  const int64_t row = t * kTI + i;
+  const double x = (row < L && r < ld) ? rows[row * ld + r] * scale[r] : 0.0;
+  const __half hi = __double2half(x);
+  img[e] = (m & 1) ? __double2half(x - static_cast<double>(__half2float(hi))) : hi;
+}
+
+}  // namespace
+
+int seed_f32f_band_tiles() { return kA; }
+
+int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream_t s) {
+  static unsigned long long cfg = 0;
+  set_smem_attr(seed_f32f_kernel, kSmem, cfg);
+  launch_k(seed_f32f_kernel, dim3(p.P), dim3(kThreads), kSmem, s, pdl_enabled(), p, *ymap);
+  return 1;
+}
+
+int launch_krl_image(const double* rows, int64_t L, int ld, const double* scale, void* img, cudaStream_t s) {
+  const int64_t ntiles = ceil_div(L, kTI);
+  const int64_t work = ntiles * 128 * kTI;
+  krl_image_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, s>>>(rows, L, ld, scale,
+                                                                             static_cast<__half*>(img), ntiles);
+  return 1;
+}
+
+}  // namespace cpdgpu

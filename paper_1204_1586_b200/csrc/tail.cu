@@ -72,6 +72,7 @@ __host__ __device__ inline int64_t op_units(const TailOp& o) {
     case kOpReduceRight:                                       // B == 1: warp per output (lanes over slots)
       return o.B == 1 ? o.M * o.R : ((o.M + 31) / 32) * o.R;   // else 32 rows per warp
     case kOpReduceLeft: return ((o.M + 31) / 32) * o.R;        // 32 columns per warp
+    case kOpReduceLeft32: return ((o.M + 31) / 32) * o.R;      // 32 columns per warp
     default: return 0;
   }
 }
@@ -111,6 +112,24 @@ __device__ void run_unit(const TailOp& o, int64_t u, int lane, double* const* gt
       for (int q = o.rb_ptr[rb]; q < o.rb_ptr[rb + 1]; ++q)
         s += o.Z[(static_cast<int64_t>(o.slot_list[q]) * o.RP + r) * o.TI + il];
       out[r * o.ldo + i] = s;
+    }
+  } else if (o.type == kOpReduceLeft32) {  // lanes over columns: 128-byte runs of the [r][64 j] partials
+    const int64_t chunks = (o.M + 31) / 32;
+    const int r = static_cast<int>(u / chunks);
+    const int64_t j = (u - r * chunks) * 32 + lane;
+    if (j < o.M) {
+      const float* z = o.Z32 + ((j >> 6) * 64 + r) * 64 + (j & 63);
+      const int64_t stride = o.ldz * 64 * 64;  // one band: ldz column tiles of [64 r][64 j]
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // fixed order: bands b = 0, 1, ... in four lanes of sums
+      int64_t b = 0;
+      for (; b + 3 < o.B; b += 4) {
+        s0 += static_cast<double>(z[b * stride]);
+        s1 += static_cast<double>(z[(b + 1) * stride]);
+        s2 += static_cast<double>(z[(b + 2) * stride]);
+        s3 += static_cast<double>(z[(b + 3) * stride]);
+      }
+      for (; b < o.B; ++b) s0 += static_cast<double>(z[b * stride]);
+      out[r * o.ldo + j] = ((s0 + s1) + (s2 + s3)) * (o.us_y[0] * o.us_r[r]);
     }
   } else if (o.type == kOpReduceLeft) {  // Ls[r][j] = sum_rb Lpart[rb][r][j]
     const int64_t chunks = (o.M + 31) / 32;
