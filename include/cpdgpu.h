@@ -147,6 +147,44 @@ int cpdgpu_cp_gradient_all_hook(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R,
 int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R,
                                   const double* factors_dev, double* gradients_dev, int pivot);
 
+/* ---- multi-GPU: last-mode slab sharding ----------------------
+ * Replaces running cp_gradient_all (mttkrp.hpp:59-69) on one huge tensor: each
+ * rank (one process per GPU) holds the contiguous last-mode slab [lo, hi) of a
+ * global tensor whose dims are ascending, computes its slab's gradient with the
+ * GLOBAL pivot p* (the right seed and G(1..N-1) are linear sums over slabs, the
+ * rows of G(N) belong to the slab), and ONE all-reduce(sum) of
+ * [partial G(1..N-1) | G(N) rows at the slab's offset, zeros elsewhere]
+ * finishes it inside the library.  The collective is NCCL (dlopen'ed
+ * libnccl.so.2, in-place ncclAllReduce on the context stream over NVLink) or a
+ * caller-supplied host all-reduce (e.g. MPI or gloo). */
+#define CPDGPU_COMM_ID_BYTES 128
+/* Host all-reduce: sum `count` doubles of `buf` across the ranks, in place. */
+typedef int (*cpdgpu_allreduce_fn)(void* user, double* buf, int64_t count);
+/* Rank 0 creates the id (ncclGetUniqueId) and the caller broadcasts it. */
+int cpdgpu_comm_unique_id(unsigned char* id /* CPDGPU_COMM_ID_BYTES */);
+/* Joins the NCCL communicator on the context's device (ncclCommInitRank). */
+int cpdgpu_comm_init(cpdgpu_ctx* ctx, const unsigned char* id, int nranks, int rank);
+/* The exchange runs through `fn` on host memory instead of NCCL. */
+int cpdgpu_comm_init_host(cpdgpu_ctx* ctx, int nranks, int rank, cpdgpu_allreduce_fn fn, void* user);
+int cpdgpu_comm_destroy(cpdgpu_ctx* ctx);
+/* Balanced contiguous split of the last mode (sizes differ by at most one:
+ * 300 over 8 ranks -> 38,38,38,38,37,37,37,37). */
+int cpdgpu_slab_bounds(int64_t extent, int nranks, int rank, int64_t* lo, int64_t* hi);
+/* Sharded all-mode gradient.  slab: this rank's tensor, dims = global_dims
+ * except the last (hi - lo, with [lo, hi) = cpdgpu_slab_bounds of the
+ * communicator's rank).  factors / gradients: the GLOBAL I_n x R matrices
+ * (host, caller's mode order); every rank receives the full gradients.
+ * mults (optional, N entries): the per-mode charges of the unsharded call
+ * (fast_count_realized on global_dims). */
+int cpdgpu_cp_gradient_all_sharded(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims,
+                                   int64_t R, const double* const* factors, double* const* gradients,
+                                   uint64_t* mults);
+/* Device form, ordered on the context stream: factors_dev = the slab's packed
+ * factors (modes 1..N-1 whole, rows [lo, hi) of mode N); out_dev = the packed
+ * GLOBAL result, (sum_{n<N} I_n + I_N) x R doubles: G(1..N-1) then G(N). */
+int cpdgpu_cp_gradient_all_sharded_device(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims,
+                                          int64_t R, const double* factors_dev, double* out_dev);
+
 /* ---- direct MTTKRP (Algorithm 1 cost model; mttkrp.hpp:19-20, mttkrp.cpp:29-54)
  * One pass over Y for one mode: out = Y_(n) (KR_{k != n} A(k)), I_n x R column-major,
  * caller's mode order; mults (optional) receives the reference's charge. */

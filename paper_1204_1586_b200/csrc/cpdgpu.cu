@@ -22,6 +22,9 @@
 #include <tuple>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is opened at run time (cpdgpu_comm_init)
+
 #include "../../include/cpdgpu.h"
 #include "kernels.h"
 
@@ -297,6 +300,15 @@ struct Plan {
     DevBuf tab;  // CSR of partial slots per output block
   };
   F32Pass fr, fl;
+  // hook-free fp32 gradients with R <= 64: both seeds in one pass (seed_f32f.cu)
+  struct F32Fused {
+    bool on = false;
+    int64_t nRT = 0, nB = 0, nC = 0, U = 0;
+    int P = 0, slots = 0, window = 4;
+    DevBuf tab;  // CSR of right-partial slots per 128-row tile
+    int tab_len = 0, tab_max = 0;
+    DevBuf krl_img, lpart32;
+  } ff;
   int64_t J8 = 0;               // J_p rounded up to 8 (3-D TMA view)
   DevBuf ypad;                  // padded copy when J_p % 8 != 0
   CUtensorMap ymap_r{}, ymap_l{};
@@ -341,8 +353,57 @@ struct Plan {
   int64_t K(int m) const { return J[N] / J[m]; }
 };
 
+// Communicator of the sharded gradient: NCCL (in-place all-reduce on the context
+// stream) or the caller's host all-reduce.  libnccl.so.2 is dlopen'ed on first
+// use, so the library has no link-time NCCL dependency (and shares the process's
+// already-loaded NCCL, e.g. torch's, when there is one).
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("libnccl.so.2 not found: ") + dlerror();
+      return a;
+    }
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.init_rank && a.all_reduce && a.destroy && a.error_string;
+    if (!a.ok) a.why = "libnccl.so.2 lacks the expected entry points";
+    return a;
+  }();
+  return api;
+}
+struct Comm {
+  int nranks = 1, rank = 0;
+  ncclComm_t nccl = nullptr;
+  cpdgpu_allreduce_fn host_fn = nullptr;
+  void* user = nullptr;
+  DevBuf fbuf;   // packed slab factors (host entry)
+  DevBuf xbuf;   // exchange / packed global result (host entry)
+  DevBuf lbuf;   // packed slab gradients
+  HostBuf hbuf;  // host exchange staging
+  ~Comm() {
+    if (nccl) nccl_api().destroy(nccl);
+  }
+};
+
 struct cpdgpu_ctx {
   int device = 0;
+  std::unique_ptr<Comm> comm;
   int num_sms = 148;
   cudaStream_t own = nullptr, stream = nullptr;
   std::string err;
@@ -636,6 +697,42 @@ void build_f32_geometry(cpdgpu_ctx* ctx, Plan& pl) {
     lpart += static_cast<size_t>(pl.fl.P) * pl.fl.slots * RPc * 128;
     pl.chunks.push_back(std::move(c));
   }
+  // fused single pass (hook-free gradients): bands of kA row tiles x 64-column tiles
+  Plan::F32Fused& ff = pl.ff;
+  static const char* fused_env = std::getenv("CPDGPU_F32_FUSED");
+  ff.on = pl.chunks.size() == 1 && pl.p < pl.N && !(fused_env && std::atoi(fused_env) == 0);
+  if (ff.on) {
+    const int kA = cpdgpu::seed_f32f_band_tiles();
+    ff.nRT = cpdgpu::ceil_div(Jp, 128);
+    ff.nB = cpdgpu::ceil_div(ff.nRT, kA);
+    ff.nC = cpdgpu::ceil_div(Kp, 64);
+    ff.U = ff.nB * ff.nC;
+    ff.P = static_cast<int>(std::min<int64_t>(ctx->num_sms, ff.U));
+    ff.slots = static_cast<int>(cpdgpu::ceil_div(cpdgpu::ceil_div(ff.U, ff.P), ff.nC) + 1);
+    static const char* win_env = std::getenv("CPDGPU_F32_WINDOW");
+    ff.window = win_env && std::atoi(win_env) > 0 ? std::atoi(win_env) : 4;
+    std::vector<std::vector<int>> per(static_cast<size_t>(ff.nRT));
+    for (int64_t c = 0; c < ff.P; ++c) {
+      const int64_t a = c * ff.U / ff.P, b = (c + 1) * ff.U / ff.P;
+      if (a >= b) continue;
+      for (int64_t band = a / ff.nC; band <= (b - 1) / ff.nC; ++band)
+        for (int t = 0; t < kA && band * kA + t < ff.nRT; ++t)
+          per[static_cast<size_t>(band * kA + t)].push_back(
+              static_cast<int>((c * ff.slots + (band - a / ff.nC)) * kA + t));
+    }
+    std::vector<int> tab(static_cast<size_t>(ff.nRT) + 1, 0);
+    for (int64_t rt = 0; rt < ff.nRT; ++rt) {
+      tab[rt + 1] = tab[rt] + static_cast<int>(per[static_cast<size_t>(rt)].size());
+      ff.tab_max = std::max(ff.tab_max, static_cast<int>(per[static_cast<size_t>(rt)].size()));
+    }
+    for (auto& v : per) tab.insert(tab.end(), v.begin(), v.end());
+    ff.tab.ensure(tab.size() * sizeof(int));
+    CK(cudaMemcpy(ff.tab.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+    ff.tab_len = static_cast<int>(ff.nRT) + 1;
+    ff.krl_img.ensure(static_cast<size_t>(ff.nRT) * 128 * 128 * 2);
+    ff.lpart32.ensure(static_cast<size_t>(ff.nB * ff.nC) * 64 * 64 * sizeof(float));
+    rpart = std::max(rpart, static_cast<size_t>(ff.P) * ff.slots * kA * RPc * 128);
+  }
   pl.Rpart.ensure(rpart * sizeof(double));
   pl.Lpart.ensure(lpart * sizeof(double));
 }
@@ -828,6 +925,34 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
   cudaStream_t s = ctx->stream;
   const int RPc = cpdgpu::seed_f32_rank_cols();
   const char* yb = static_cast<const char*>(t->yscale.p);
+  if (mode == 3 && pl.ff.on) {  // both seeds in one pass over Y
+    Plan::Chunk& c = pl.chunks[0];
+    double* sc = c.scales->d();
+    ctx->launches += cpdgpu::launch_kr_scale(pl.spec(pl.p + 1, pl.N, c.r0), pl.spec(1, pl.p, c.r0), c.Rc, sc,
+                                             sc + 2 * RPc, s);
+    ctx->launches += cpdgpu::launch_kr_split(c.KRr->d(), pl.Kp, RPc, sc, c.KRr16->p, s);
+    ctx->launches += cpdgpu::launch_krl_image(c.KRl->d(), pl.Jp, RPc, sc + RPc, pl.ff.krl_img.p, s);
+    cpdgpu::Seed32FParams q{};
+    q.kr_tiles = static_cast<const unsigned char*>(c.KRr16->p);
+    q.krl_img = pl.ff.krl_img.p;
+    q.scale_y = reinterpret_cast<const float*>(yb);
+    q.inv_scale_y = reinterpret_cast<const double*>(yb + 8);
+    q.inv_scale_kr = sc + 2 * RPc;
+    q.rpart = pl.Rpart.d();
+    q.lpart = static_cast<float*>(pl.ff.lpart32.p);
+    q.nRT = pl.ff.nRT;
+    q.nC = pl.ff.nC;
+    q.units = pl.ff.U;
+    q.P = pl.ff.P;
+    q.slots = pl.ff.slots;
+    q.window = pl.ff.window;
+    static const char* knob_env = std::getenv("CPDGPU_F32F_KNOBS");
+    q.knobs = knob_env ? std::atoi(knob_env) : 0;
+    if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+    ctx->launches += cpdgpu::launch_seed_f32f(q, &pl.ymap_r, s);
+    if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
+    return;
+  }
   for (auto& c : pl.chunks) {
     double* sc = c.scales->d();
     ctx->launches += cpdgpu::launch_kr_scale(pl.spec(pl.p + 1, pl.N, c.r0), pl.spec(1, pl.p, c.r0), c.Rc, sc,
@@ -1124,6 +1249,33 @@ cpdgpu::TailOp op_base(int type, int R) {
 
 // Seed-partial reductions for the given seed mode.
 void add_reduce_ops(const Plan& pl, cpdgpu::TailStep& st, int mode) {
+  if (pl.f32 && mode == 3 && pl.ff.on) {  // fused pass: right slots per row tile, left fp32 per band
+    const Plan::Chunk& c = pl.chunks[0];
+    const Plan::F32Fused& ff = pl.ff;
+    cpdgpu::TailOp o = op_base(cpdgpu::kOpReduceRight, c.Rc);
+    o.Z = pl.Rpart.d();
+    o.B = ff.tab_max >= 16 ? 1 : 0;
+    o.M = pl.Jp;
+    o.RP = cpdgpu::seed_f32_rank_cols();
+    o.TI = 128;
+    o.rb_ptr = static_cast<const int*>(ff.tab.p);
+    o.slot_list = static_cast<const int*>(ff.tab.p) + ff.tab_len;
+    o.out = pl.Rs.d();
+    o.ldo = pl.Jp;
+    st.op[st.n++] = o;
+    cpdgpu::TailOp l = op_base(cpdgpu::kOpReduceLeft32, c.Rc);
+    l.Z32 = static_cast<const float*>(ff.lpart32.p);
+    l.ldz = ff.nC;
+    l.M = pl.Kp;
+    l.B = ff.nB;
+    const int RPc = cpdgpu::seed_f32_rank_cols();
+    l.us_y = reinterpret_cast<const double*>(static_cast<const char*>(pl.tensor->yscale.p) + 8);
+    l.us_r = c.scales->d() + 3 * RPc;
+    l.out = pl.Ls.d();
+    l.ldo = pl.Kp;
+    st.op[st.n++] = l;
+    return;
+  }
   if (pl.f32) {  // both sides: per-CTA fp64 partial blocks [slot][64][128]
     for (const auto& c : pl.chunks)
       for (int side = 0; side < 2; ++side) {
@@ -2744,6 +2896,193 @@ int cpdgpu_als_run(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, double* const* 
     for (auto& e : ev) cudaEventDestroy(e);
     *iters_run = done;
     download_factors(ctx, pl, y, factors);
+  });
+}
+
+// ---- multi-GPU: last-mode slab sharding ---------------------------
+
+int cpdgpu_comm_unique_id(unsigned char* id) {
+  return guarded(nullptr, [&] {
+    if (!id) fail(CPDGPU_ARGUMENT_ERROR, "comm_unique_id: null id");
+    NcclApi& a = nccl_api();
+    if (!a.ok) fail(CPDGPU_CUDA_ERROR, "comm_unique_id: %s", a.why.c_str());
+    ncclUniqueId u;
+    const ncclResult_t r = a.get_unique_id(&u);
+    if (r != ncclSuccess) fail(CPDGPU_CUDA_ERROR, "ncclGetUniqueId: %s", a.error_string(r));
+    std::memcpy(id, u.internal, CPDGPU_COMM_ID_BYTES);
+  });
+}
+
+int cpdgpu_comm_init(cpdgpu_ctx* ctx, const unsigned char* id, int nranks, int rank) {
+  return guarded(ctx, [&] {
+    if (!ctx || !id) fail(CPDGPU_ARGUMENT_ERROR, "comm_init: null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+      fail(CPDGPU_ARGUMENT_ERROR, "comm_init: rank %d outside 0..%d", rank, nranks - 1);
+    NcclApi& a = nccl_api();
+    if (!a.ok) fail(CPDGPU_CUDA_ERROR, "comm_init: %s", a.why.c_str());
+    use_device(ctx);
+    auto c = std::make_unique<Comm>();
+    c->nranks = nranks;
+    c->rank = rank;
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, CPDGPU_COMM_ID_BYTES);
+    const ncclResult_t r = a.init_rank(&c->nccl, nranks, u, rank);
+    if (r != ncclSuccess) fail(CPDGPU_CUDA_ERROR, "ncclCommInitRank: %s", a.error_string(r));
+    ctx->comm = std::move(c);
+  });
+}
+
+int cpdgpu_comm_init_host(cpdgpu_ctx* ctx, int nranks, int rank, cpdgpu_allreduce_fn fn, void* user) {
+  return guarded(ctx, [&] {
+    if (!ctx || !fn) fail(CPDGPU_ARGUMENT_ERROR, "comm_init_host: null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+      fail(CPDGPU_ARGUMENT_ERROR, "comm_init_host: rank %d outside 0..%d", rank, nranks - 1);
+    auto c = std::make_unique<Comm>();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->host_fn = fn;
+    c->user = user;
+    ctx->comm = std::move(c);
+  });
+}
+
+int cpdgpu_comm_destroy(cpdgpu_ctx* ctx) {
+  return guarded(ctx, [&] {
+    if (!ctx) fail(CPDGPU_ARGUMENT_ERROR, "comm_destroy: null context");
+    if (ctx->comm) use_device(ctx);
+    ctx->comm.reset();
+  });
+}
+
+int cpdgpu_slab_bounds(int64_t extent, int nranks, int rank, int64_t* lo, int64_t* hi) {
+  return guarded(nullptr, [&] {
+    if (!lo || !hi || nranks < 1 || rank < 0 || rank >= nranks || extent < 0)
+      fail(CPDGPU_ARGUMENT_ERROR, "slab_bounds: bad argument");
+    const int64_t base = extent / nranks, extra = extent % nranks;
+    *lo = rank * base + std::min<int64_t>(rank, extra);
+    *hi = *lo + base + (rank < extra ? 1 : 0);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+struct ShardGeom {
+  std::vector<int64_t> gdims;
+  int N = 0, pivot = 0;
+  int64_t lo = 0, hi = 0, partial = 0, total = 0;  // packed G(1..N-1) length, + I_N R
+};
+
+ShardGeom shard_geometry(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims, int64_t R,
+                         const char* who) {
+  if (!ctx || !slab || !global_dims) fail(CPDGPU_ARGUMENT_ERROR, "%s: null argument", who);
+  if (!ctx->comm) fail(CPDGPU_ARGUMENT_ERROR, "%s: no communicator (cpdgpu_comm_init)", who);
+  ShardGeom g;
+  g.N = N;
+  g.gdims.assign(global_dims, global_dims + N);
+  validate_common(ctx, slab, R, who);
+  if (N < 2 || static_cast<int>(slab->dims.size()) != N)
+    fail(CPDGPU_SHAPE_ERROR, "%s: slab order %zu, global order %d", who, slab->dims.size(), N);
+  for (int k = 0; k + 1 < N; ++k) {
+    if (g.gdims[k] < 1 || (k > 0 && g.gdims[k] < g.gdims[k - 1]))
+      fail(CPDGPU_ARGUMENT_ERROR, "%s: global dims must be positive and ascending (sort modes first)", who);
+    if (slab->dims[k] != g.gdims[k])
+      fail(CPDGPU_SHAPE_ERROR, "%s: slab mode %d has extent %lld, global %lld", who, k + 1,
+           static_cast<long long>(slab->dims[k]), static_cast<long long>(g.gdims[k]));
+  }
+  if (g.gdims[N - 1] < g.gdims[N - 2])
+    fail(CPDGPU_ARGUMENT_ERROR, "%s: global dims must be ascending (sort modes first)", who);
+  const Comm& c = *ctx->comm;
+  if (cpdgpu_slab_bounds(g.gdims[N - 1], c.nranks, c.rank, &g.lo, &g.hi) != CPDGPU_OK || g.hi - g.lo < 1)
+    fail(CPDGPU_ARGUMENT_ERROR, "%s: last mode %lld has fewer slices than the %d ranks", who,
+         static_cast<long long>(g.gdims[N - 1]), c.nranks);
+  if (slab->dims[N - 1] != g.hi - g.lo)
+    fail(CPDGPU_SHAPE_ERROR, "%s: rank %d holds slices [%lld, %lld) but its slab has %lld", who, c.rank,
+         static_cast<long long>(g.lo), static_cast<long long>(g.hi), static_cast<long long>(slab->dims[N - 1]));
+  g.pivot = select_pivot(g.gdims);
+  if (g.pivot >= N) fail(CPDGPU_ARGUMENT_ERROR, "%s: the pivot is the last mode; nothing to shard", who);
+  for (int k = 0; k + 1 < N; ++k) g.partial += g.gdims[k] * R;
+  g.total = g.partial + g.gdims[N - 1] * R;
+  return g;
+}
+
+// local gradient of the slab at the global pivot, then ONE in-place all-reduce of
+// [partial G(1..N-1) | G(N) rows placed at the slab's offset] into out_dev
+void sharded_device(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, const ShardGeom& g, int64_t R, const double* fdev,
+                    double* out_dev) {
+  Comm& c = *ctx->comm;
+  const int64_t rows = g.hi - g.lo, IN = g.gdims[g.N - 1];
+  c.lbuf.ensure(static_cast<size_t>(g.partial + rows * R) * sizeof(double));
+  Plan& pl = *get_plan(ctx, slab, R, g.pivot);
+  bind_seed_inputs(ctx, pl, slab);
+  run_gradient(ctx, pl, fdev, c.lbuf.d());
+  CK(cudaMemcpyAsync(out_dev, c.lbuf.d(), static_cast<size_t>(g.partial) * sizeof(double), cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  CK(cudaMemsetAsync(out_dev + g.partial, 0, static_cast<size_t>(IN * R) * sizeof(double), ctx->stream));
+  CK(cudaMemcpy2DAsync(out_dev + g.partial + g.lo, static_cast<size_t>(IN) * sizeof(double), c.lbuf.d() + g.partial,
+                       static_cast<size_t>(rows) * sizeof(double), static_cast<size_t>(rows) * sizeof(double),
+                       static_cast<size_t>(R), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (c.nranks == 1) return;
+  if (c.nccl) {
+    NcclApi& a = nccl_api();
+    const ncclResult_t r = a.all_reduce(out_dev, out_dev, static_cast<size_t>(g.total), ncclFloat64, ncclSum, c.nccl,
+                                        ctx->stream);
+    if (r != ncclSuccess) fail(CPDGPU_CUDA_ERROR, "ncclAllReduce: %s", a.error_string(r));
+    return;
+  }
+  const size_t bytes = static_cast<size_t>(g.total) * sizeof(double);
+  c.hbuf.ensure(bytes);
+  CK(cudaMemcpyAsync(c.hbuf.p, out_dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int st = c.host_fn(c.user, c.hbuf.d(), g.total);
+  if (st != 0) fail(st > 0 ? st : CPDGPU_CUDA_ERROR, "cp_gradient_all_sharded: host all-reduce failed (%d)", st);
+  CK(cudaMemcpyAsync(out_dev, c.hbuf.p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+int cpdgpu_cp_gradient_all_sharded_device(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims,
+                                          int64_t R, const double* factors_dev, double* out_dev) {
+  return guarded(ctx, [&] {
+    const ShardGeom g = shard_geometry(ctx, slab, N, global_dims, R, "cp_gradient_all_sharded");
+    if (!factors_dev || !out_dev) fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all_sharded: null device buffer");
+    sharded_device(ctx, slab, g, R, factors_dev, out_dev);
+    CK(cudaGetLastError());
+  });
+}
+
+int cpdgpu_cp_gradient_all_sharded(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims,
+                                   int64_t R, const double* const* factors, double* const* gradients,
+                                   uint64_t* mults) {
+  return guarded(ctx, [&] {
+    const ShardGeom g = shard_geometry(ctx, slab, N, global_dims, R, "cp_gradient_all_sharded");
+    if (!factors || !gradients) fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all_sharded: null factor or gradient list");
+    Comm& c = *ctx->comm;
+    const int64_t rows = g.hi - g.lo;
+    // the slab's packed factors: modes 1..N-1 whole, rows [lo, hi) of mode N
+    std::vector<double> hf(static_cast<size_t>(g.partial + rows * R));
+    for (int64_t m = 0, at = 0; m + 1 < N; ++m) {
+      std::memcpy(hf.data() + at, factors[m], static_cast<size_t>(g.gdims[m] * R) * sizeof(double));
+      at += g.gdims[m] * R;
+    }
+    for (int64_t r = 0; r < R; ++r)
+      std::memcpy(hf.data() + g.partial + r * rows, factors[N - 1] + r * g.gdims[N - 1] + g.lo,
+                  static_cast<size_t>(rows) * sizeof(double));
+    c.fbuf.ensure(hf.size() * sizeof(double));
+    c.xbuf.ensure(static_cast<size_t>(g.total) * sizeof(double));
+    CK(cudaMemcpyAsync(c.fbuf.p, hf.data(), hf.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    sharded_device(ctx, slab, g, R, c.fbuf.d(), c.xbuf.d());
+    for (int64_t m = 0, at = 0; m < N; ++m) {
+      CK(cudaMemcpyAsync(gradients[m], c.xbuf.d() + at, static_cast<size_t>(g.gdims[m] * R) * sizeof(double),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      at += g.gdims[m] * R;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (mults)
+      for (int m = 0; m < N; ++m) mults[m] = count_realized(g.gdims, R, m + 1);
   });
 }
 
