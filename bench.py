@@ -319,11 +319,16 @@ def run_ours(args, cfg):
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    if f32:  # two tcgen05 passes over Y (right and left seeds): HBM-bound
+    if f32:  # tcgen05 kind::f16 split-fp16 seeds: HBM-bound
         hbm_peak = peaks.get("hbm_gbs", 6539.9)
+        path = ctx.last_seed_path()
+        kname = {4: "seed_f32i_kernel (K1, tcgen05 kind::f16 on the tensor's fp16 hi/lo operand image, "
+                    "both seeds in one pass)",
+                 3: "seed_f32f_kernel (K1, tcgen05 kind::f16, fp32 split to hi/lo in the kernel, both seeds "
+                    "in one pass)"}.get(path, "seed_f32_kernel<0>+<1> (K1, tcgen05 kind::f16 split-fp16, two passes)")
         roofline = {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": hbm_gbs / hbm_peak, "traffic": traffic,
-                    "kernel": "seed_f32_kernel<0>+<1> (K1, tcgen05 kind::f16 split-fp16, two passes)",
+                    "kernel": kname,
                     "kernel_ms": seed_avg, "algorithmic_flops": flops, "algorithmic_bytes": bytes_alg,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                     "tensor": {"executed_flops": 3 * flops, "achieved_tflops": 3 * tflops,

@@ -74,7 +74,9 @@ int cpdgpu_set_timing(cpdgpu_ctx* ctx, int enabled);
 int cpdgpu_last_seed_ms(cpdgpu_ctx* ctx, double* ms);
 /* Seed path of the most recent hook-free fp64 gradient: 0 = fp64 DMMA pass,
  * 1 = fused pass on the int8 tensor cores (default for large fp64 tensors; CPDGPU_I8=1/0
- * forces it on/off), 2 = fp32. */
+ * forces it on/off), 2 = fp32 two passes, 3 = fp32 one fused pass splitting Y in
+ * the kernel, 4 = fp32 one fused pass over the tensor's cached fp16 operand image
+ * (the default; CPDGPU_F32_IMAGE=0 / CPDGPU_F32_FUSED=0 select 3 / 2). */
 int cpdgpu_last_seed_path(const cpdgpu_ctx* ctx);
 
 /* ---- tensors (DenseTensor, dense_tensor.hpp:15-47) -------------------------

@@ -308,6 +308,15 @@ struct Plan {
     DevBuf tab;  // CSR of right-partial slots per 128-row tile
     int tab_len = 0, tab_max = 0;
     DevBuf krl_img, lpart32;
+    // the tensor's fp16 hi / lo operand image (built once per tensor version; the
+    // kernel then has no split stage); off when it does not fit in memory
+    bool img_on = false;
+    void* img = nullptr;
+    uint64_t img_version = ~0ull;
+    CUtensorMap imap{};
+    ~F32Fused() {
+      if (img) cudaFree(img);
+    }
   } ff;
   int64_t J8 = 0;               // J_p rounded up to 8 (3-D TMA view)
   DevBuf ypad;                  // padded copy when J_p % 8 != 0
@@ -822,6 +831,27 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
     }
     base = pl.ypad.p;
   }
+  if (pl.ff.on) {  // operand image for the fused seed (CPDGPU_F32_IMAGE=0: split in the kernel)
+    static const char* img_env = std::getenv("CPDGPU_F32_IMAGE");
+    Plan::F32Fused& ff = pl.ff;
+    if (!ff.img && !(img_env && std::atoi(img_env) == 0)) {
+      const size_t bytes = static_cast<size_t>(2 * cpdgpu::f16_image_ld(pl.Jp) * pl.Kp) * 2;
+      if (cudaMalloc(&ff.img, bytes) != cudaSuccess) {
+        cudaGetLastError();  // out of memory: keep the split-in-kernel path
+        ff.img = nullptr;
+      } else if (!cpdgpu::make_tensor_map_f16_image(&ff.imap, ff.img, pl.Jp, pl.Kp)) {
+        cudaFree(ff.img);
+        ff.img = nullptr;
+      }
+    }
+    ff.img_on = ff.img != nullptr;
+    if (ff.img_on && ff.img_version != t->version) {
+      ctx->launches += cpdgpu::launch_build_f16_image(src, pl.Jp, pl.Jp, pl.Kp, static_cast<const float*>(t->yscale.p),
+                                                      ff.img, ctx->num_sms, ctx->stream);
+      CK(cudaGetLastError());
+      ff.img_version = t->version;
+    }
+  }
   if (pl.ymap_base != base) {
     if (!cpdgpu::make_tensor_map_y32(&pl.ymap_r, base, pl.J8, pl.Kp, 0) ||
         !cpdgpu::make_tensor_map_y32(&pl.ymap_l, base, pl.J8, pl.Kp, 1))
@@ -948,8 +978,29 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
     q.window = pl.ff.window;
     static const char* knob_env = std::getenv("CPDGPU_F32F_KNOBS");
     q.knobs = knob_env ? std::atoi(knob_env) : 0;
+    static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
+    DevBuf tb;
+    if (trace && pl.ff.img_on) {
+      tb.ensure(static_cast<size_t>(q.P) * 16 * 8 * 8);
+      CK(cudaMemsetAsync(tb.p, 0, tb.bytes, s));
+      q.trace = static_cast<unsigned long long*>(tb.p);
+    }
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
-    ctx->launches += cpdgpu::launch_seed_f32f(q, &pl.ymap_r, s);
+    ctx->launches += pl.ff.img_on ? cpdgpu::launch_seed_f32i(q, &pl.ff.imap, s)
+                                  : cpdgpu::launch_seed_f32f(q, &pl.ymap_r, s);
+    if (q.trace) {
+      std::vector<unsigned long long> h(static_cast<size_t>(q.P) * 128);
+      CK(cudaMemcpyAsync(h.data(), tb.p, tb.bytes, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      double a[16][8] = {};
+      for (int c = 0; c < q.P; ++c)
+        for (int w = 0; w < 16; ++w)
+          for (int k = 0; k < 8; ++k) a[w][k] += static_cast<double>(h[(static_cast<size_t>(c) * 16 + w) * 8 + k]) / q.P;
+      std::fprintf(stderr, "[f32i trace] avg cycles per CTA (%.0f tiles): mma total %.0f wait full %.0f lempty %.0f "
+                   "kfull %.0f rempty %.0f kl_full %.0f issue %.0f | producer total %.0f wait empty %.0f | drain0 "
+                   "total %.0f rfull %.0f lfull %.0f\n", a[13][7], a[13][6], a[13][0], a[13][1], a[13][2], a[13][3],
+                   a[13][4], a[13][5], a[12][6], a[12][0], a[0][6], a[0][0], a[0][1]);
+    }
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
     return;
   }
@@ -1263,18 +1314,7 @@ void add_reduce_ops(const Plan& pl, cpdgpu::TailStep& st, int mode) {
     o.out = pl.Rs.d();
     o.ldo = pl.Jp;
     st.op[st.n++] = o;
-    cpdgpu::TailOp l = op_base(cpdgpu::kOpReduceLeft32, c.Rc);
-    l.Z32 = static_cast<const float*>(ff.lpart32.p);
-    l.ldz = ff.nC;
-    l.M = pl.Kp;
-    l.B = ff.nB;
-    const int RPc = cpdgpu::seed_f32_rank_cols();
-    l.us_y = reinterpret_cast<const double*>(static_cast<const char*>(pl.tensor->yscale.p) + 8);
-    l.us_r = c.scales->d() + 3 * RPc;
-    l.out = pl.Ls.d();
-    l.ldo = pl.Kp;
-    st.op[st.n++] = l;
-    return;
+    return;  // the left partials: launch_reduce_left32 right after the seed
   }
   if (pl.f32) {  // both sides: per-CTA fp64 partial blocks [slot][64][128]
     for (const auto& c : pl.chunks)
@@ -1546,7 +1586,7 @@ int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& 
 void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
   const bool left = pl.p + 1 <= pl.N;
   I8Geometry geometry(pl);
-  ctx->last_seed_path = pl.f32 ? 2 : (pl.i8.on ? 1 : 0);
+  ctx->last_seed_path = pl.f32 ? ((left && pl.ff.on) ? (pl.ff.img_on ? 4 : 3) : 2) : (pl.i8.on ? 1 : 0);
   if (pl.i8.on)
     run_seeds_i8(ctx, pl);
   else
@@ -1559,6 +1599,15 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
   if (g1_direct) redirect_to_gradient(pl, st, /*right=*/true);
   const bool gN_direct = left && pl.p + 1 == pl.N && !pl.lpart_direct;  // the left seed is L^(N)
   if (gN_direct) redirect_to_gradient(pl, st, /*right=*/false);
+  if (pl.f32 && left && pl.ff.on) {  // fused fp32 seed: its fp32 left partials, summed over the bands
+    const Plan::Chunk& c = pl.chunks[0];
+    const int RPc = cpdgpu::seed_f32_rank_cols();
+    ctx->launches += cpdgpu::launch_reduce_left32(
+        static_cast<const float*>(pl.ff.lpart32.p), pl.ff.nB, pl.ff.nC, pl.Kp, c.Rc,
+        reinterpret_cast<const double*>(static_cast<const char*>(pl.tensor->yscale.p) + 8), c.scales->d() + 3 * RPc,
+        gN_direct ? nullptr : pl.Ls.d(), static_cast<double* const*>(pl.gtab.p), gN_direct ? pl.perm[pl.N - 1] - 1 : -1,
+        pl.Kp, ctx->stream);
+  }
   cpdgpu::L0Step l0{};
   bool fuse_r = false, fuse_l = false;
   const int nl0 = build_l0(ctx, pl, l0, fuse_r, fuse_l);

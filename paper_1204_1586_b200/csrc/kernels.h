@@ -133,12 +133,23 @@ struct Seed32FParams {
   float* lpart;
   int64_t nRT, nC, units;
   int P, slots, window;
+  unsigned long long* trace;  // CPDGPU_SEED_TRACE: [P][16 warps][8] cycle counters (image kernel)
   int knobs;  // CPDGPU_F32F_KNOBS timing experiments (wrong results): 1 no split stores,
-              // 2 one right MMA per k-step, 4 one left MMA per k-step, 8 no left partial stores
+              // 2 one right MMA per k-step, 4 one left MMA per k-step, 8 no left partial stores,
+              // 16 (image kernel) no plane refills after the first ring, 32 (image kernel) no MMAs
 };
 int seed_f32f_band_tiles();  // 3
 // ymap: the right pass's map (box 128 i x 64 j, no swizzle)
 int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream_t s);
+// The same kernel reading a cached operand image of the tensor instead of the fp32
+// values (no split stage).  imap: make_tensor_map_f16_image of that image.
+int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s);
+// operand image of an fp32 view (J x K, leading dimension ldy): [2][K][LD] fp16
+// planes hi = fp16(s y), lo = fp16(s y - hi), LD = f16_image_ld(J) (rows past J zero)
+int64_t f16_image_ld(int64_t J);
+int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
+                           int num_sms, cudaStream_t s);
+bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K);
 // fp64 rows [L][ld] (ld <= 64) -> KRl^T TMEM image [ceil(L / 128)][128][128] fp16
 int launch_krl_image(const double* rows, int64_t L, int ld, const double* scale, void* img, cudaStream_t s);
 // column scales of the right (scale[0..63]) and left (scale[64..127]) Khatri-Rao rows
@@ -159,8 +170,7 @@ enum TailOpType {
   kOpContractA = 1,
   kOpContractB = 2,
   kOpReduceRight = 3,
-  kOpReduceLeft = 4,
-  kOpReduceLeft32 = 5  // Ls[r][j] = us_y us_r[r] sum_b Z32[((b ldz + j / 64) 64 + r) 64 + j % 64] (fused fp32 seed)
+  kOpReduceLeft = 4
 };
 
 // One rank-batched contraction / reduction (all R columns):
@@ -184,9 +194,6 @@ struct TailOp {
   const int* rb_ptr;
   const int* slot_list;
   int cta;  // set by launch_tail_step: long contractions run one output per CTA
-  const float* Z32;                    // kOpReduceLeft32: fp32 partials, scaled units
-  const double* us_y;                  // ... and their unscale, us_y[0] * us_r[r]
-  const double* us_r;
 };
 constexpr int kMaxTailOps = 8;
 struct TailStep {
@@ -236,6 +243,11 @@ constexpr int64_t kL0MaxRows = 6144;  // Z rows per CTA staged in shared memory 
 int launch_l0_step(const L0Step& st, double* const* gtab, cudaStream_t s);
 
 int64_t tail_step_units(const TailStep& st);
+// fused fp32 seed: Ls[r][j] = us_y[0] us_r[r] sum_b Z[((b nC + j / 64) 64 + r) 64 + j % 64]
+// into out, or into gtab[out_slot] when out_slot >= 0 (the left seed is a gradient)
+int launch_reduce_left32(const float* Z, int64_t nB, int64_t nC, int64_t M, int R, const double* us_y,
+                         const double* us_r, double* out, double* const* gtab, int out_slot, int64_t ldo,
+                         cudaStream_t s);
 int launch_tail_step(const TailStep& st, double* const* gtab, int num_sms, cudaStream_t s);
 
 // Khatri-Rao rows for K1: out[q*LDK + r] = KR(spec)[q, r] for q < L (zero past R).

@@ -207,6 +207,46 @@ struct FWalk {
   __device__ bool win_start(int u) const { return band_start(u) || seg_pos(u) % window == 0; }
 };
 
+// The same walk as an incremental iterator (no runtime-divisor division or
+// modulo per unit: the MMA warp's bookkeeping sits between MMA issue bursts).
+struct UnitIter {
+  int u, end, b, c, nt, wpos, nC, nRT, window;
+  bool first;
+  __device__ void init(const FWalk& w) {
+    u = w.a;
+    end = w.b;
+    nC = w.nC;
+    nRT = w.nRT;
+    window = w.window;
+    b = u / nC;
+    c = u - b * nC;
+    nt = tiles_of(b);
+    wpos = 0;
+    first = true;
+  }
+  __device__ int tiles_of(int band) const {
+    const int r = nRT - band * kA;
+    return r < kA ? r : kA;
+  }
+  __device__ bool more() const { return u < end; }
+  __device__ bool band_start() const { return first || c == 0; }
+  __device__ bool seg_end() const { return u + 1 == end || c + 1 == nC; }
+  __device__ bool win_start() const { return first || c == 0 || wpos == 0; }
+  __device__ bool win_end() const { return seg_end() || wpos == window - 1; }
+  __device__ void next() {
+    first = false;
+    ++u;
+    if (++c == nC) {
+      c = 0;
+      ++b;
+      nt = tiles_of(b);
+      wpos = 0;
+    } else {
+      wpos = wpos + 1 == window ? 0 : wpos + 1;
+    }
+  }
+};
+
 __global__ void __launch_bounds__(kThreads, 1)
     seed_f32f_kernel(const Seed32FParams p, const __grid_constant__ CUtensorMap ymap) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -540,6 +580,368 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ==================================================================================
+// timed wait (CPDGPU_SEED_TRACE): cycles spent waiting added to *acc
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  *acc += static_cast<unsigned long long>(clock64() - t0);
+}
+
+// Operand-image variant: the tensor's fp16 hi / lo planes are built once per tensor
+// version (build_f16_image_kernel, same 4 bytes per entry as the fp32 tensor) and
+// TMA-loaded straight into the 128-byte-swizzled operand layout, so the kernel
+// has no split stage: per 32 KB tile the shared-memory port carries the TMA write
+// and the MMA operand reads only (136 KB instead of 200 KB).
+//
+//   warps 0-11   drains (q, t): TMEM lane quarter q == warp % 4, row tile t of the
+//                band: the right window drains (64 fp32 second-level sums per
+//                lane), the KRl^T image of row tile t, left chunks t, t+3, t+6
+//   warp 12      producer: 4 TMA boxes (64 i x 64 j, one plane) per tile into a
+//                5-slot ring
+//   warp 13      MMAs (whole warp waits, one elected lane issues)
+//   warp 14      Khatri-Rao producer: the unit's KRr tile into a 4-deep ring (its
+//                own warp: the Y stream never waits on a Khatri-Rao slot)
+//   warp 15      idle (16 warps keep 128 registers per thread)
+constexpr int kINS = 5;                        // image slots (160 KB of loads in flight)
+constexpr int kINK = 4;                        // KRr slots (units of look-ahead)
+constexpr int kIDrain = 12, kIWProd = kIDrain, kIWMma = kIDrain + 1, kIWKr = kIDrain + 2;
+constexpr int kIThreads = 16 * 32;
+constexpr int kIOffKR = kINS * 2 * kPlane;
+constexpr int kIOffBars = kIOffKR + kINK * kKRBytes;
+constexpr int kISmem = 1024 + kIOffBars + 512 + kRP * 8;
+
+__global__ void __launch_bounds__(kIThreads, 1)
+    seed_f32i_kernel(const Seed32FParams p, const __grid_constant__ CUtensorMap imap) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cta = blockIdx.x;
+  FWalk w;
+  w.a = static_cast<int>(static_cast<int64_t>(cta) * p.units / p.P);
+  w.b = static_cast<int>(static_cast<int64_t>(cta + 1) * p.units / p.P);
+  w.nC = static_cast<int>(p.nC);
+  w.nRT = static_cast<int>(p.nRT);
+  w.window = p.window;
+  const int seg0 = w.a / w.nC;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const uint32_t ring_u = smem_u32(base);            // [kINS][hi 16 KB | lo 16 KB]
+  const uint32_t krt_u = smem_u32(base + kIOffKR);   // [kINK][16 KB] KRr tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kIOffBars);
+  uint64_t* full = bars;                 // [kINS] planes landed            (1 + tx)
+  uint64_t* empty = full + kINS;         // [kINS] planes consumed          (MMA commit)
+  uint64_t* kfull = empty + kINS;        // [kINK] KRr tile landed          (1 + tx)
+  uint64_t* kempty = kfull + kINK;       // [kINK] KRr tile consumed        (MMA commit)
+  uint64_t* lfull = kempty + kINK;       // [2] left unit accumulated       (MMA commit)
+  uint64_t* lempty = lfull + 2;          // [2] left accumulator drained    (12 drain warps)
+  uint64_t* rfull = lempty + 2;          // [kA] right window accumulated   (MMA commit)
+  uint64_t* rempty = rfull + kA;         // [kA] right window drained       (the row tile's 4 warps)
+  uint64_t* kl_full = rempty + kA;       // band's KRl^T in TMEM            (12 drain warps)
+  uint64_t* kl_free = kl_full + 1;       // band's MMAs done                (MMA commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kl_free + 1);
+  double* unscale = reinterpret_cast<double*>(base + kIOffBars + 512);  // [64] 1 / (scale_y scale_r)
+
+  if (tid == 0) {
+    for (int s = 0; s < kINS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kINK; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&lfull[s], 1);
+      mbar_init(&lempty[s], kIDrain);
+    }
+    for (int t = 0; t < kA; ++t) {
+      mbar_init(&rfull[t], 1);
+      mbar_init(&rempty[t], 4);
+    }
+    mbar_init(kl_full, kIDrain);
+    mbar_init(kl_free, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp != kIWProd) pdl_wait();  // scales, Khatri-Rao images: the preceding kernels (Y: not)
+  if (tid < kRP) unscale[tid] = p.inv_scale_y[0] * p.inv_scale_kr[tid];
+  if (warp == kIWMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (warp == kIWProd && lane == 0)
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&imap)));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kIWProd) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_y = policy_evict_first();
+      int k = 0;
+      unsigned long long tw = 0;
+      const long long tstart = clock64();
+      int s = 0;
+      uint32_t ph = 0;  // ring slot s, its empty-phase parity for this lap
+      UnitIter it;
+      for (it.init(w); it.more(); it.next()) {
+        const int b = it.b, c = it.c, nt = it.nt;
+        for (int t = 0; t < nt; ++t, ++k) {
+          if (k >= kINS) mbar_wait_t(&empty[s], ph ^ 1u, &tw);
+          if ((p.knobs & 16) && k >= kINS) {  // timing experiment: no refill (stale planes)
+            mbar_arrive(&full[s]);
+          } else {
+          mbar_arrive_tx(&full[s], 2 * kPlane);
+          const int i0 = (b * kA + t) * kTI, j0 = c * kTJ;
+#pragma unroll
+          for (int pl = 0; pl < 2; ++pl)
+#pragma unroll
+            for (int ih = 0; ih < 2; ++ih)
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                  " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(ring_u + s * 2 * kPlane + pl * kPlane + ih * 8192),
+                  "l"(reinterpret_cast<uint64_t>(&imap)), "r"(i0 + 64 * ih), "r"(j0), "r"(pl), "r"(smem_u32(&full[s])),
+                  "l"(pol_y)
+                  : "memory");
+          }
+          if (++s == kINS) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+      if (p.trace) {
+        p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + 0] = tw;
+        p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + 6] = static_cast<unsigned long long>(clock64() - tstart);
+      }
+    }
+  } else if (warp == kIWKr) {
+    // ------------------------------------------------------------------ KRr producer
+    if (lane == 0) {
+      const uint64_t pol_k = policy_evict_last();
+      int ul = 0;
+      UnitIter it;
+      for (it.init(w); it.more(); it.next(), ++ul) {
+        const int ks = ul & (kINK - 1);
+        if (ul >= kINK) mbar_wait(&kempty[ks], static_cast<uint32_t>(((ul / kINK) - 1) & 1));
+        mbar_arrive_tx(&kfull[ks], kKRBytes);
+        bulk_load(krt_u + ks * kKRBytes, p.kr_tiles + static_cast<int64_t>(it.c) * kKRBytes, kKRBytes, &kfull[ks],
+                  pol_k);
+      }
+    }
+  } else if (warp == kIWMma) {
+    // ------------------------------------------------------------------ MMA issuer
+    constexpr uint32_t id_r = idesc_f16(true), id_l = idesc_f16(false);
+    const uint64_t dA0 = sdesc(ring_u, 8192, 1024);  // right A: Y plane, MN-major
+    const uint64_t dB0 = sdesc(krt_u, 16, 1024);     // right B: KRr tile, K-major
+    const uint64_t dL0 = sdesc(ring_u, 16, 1024);    // left B: Y plane, K-major
+    const bool all_terms_r = !(p.knobs & 2), all_terms_l = !(p.knobs & 4);
+    int k = 0, bc = 0;
+    int wc[kA] = {0, 0, 0};
+    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long tstart = clock64();
+    int s = 0;
+    uint32_t ph = 0;  // ring slot and its full-phase parity
+    int ul = 0;
+    UnitIter it;
+    for (it.init(w); it.more(); it.next(), ++ul) {
+      const int nt = it.nt;
+      const int ks = ul & (kINK - 1), lb = ul & 1;
+      const bool seg_end = it.seg_end();
+      if (it.band_start()) mbar_wait_t(kl_full, static_cast<uint32_t>(bc & 1), &tr[4]);
+      if (ul >= 2) mbar_wait_t(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1), &tr[1]);
+      mbar_wait_t(&kfull[ks], static_cast<uint32_t>((ul / kINK) & 1), &tr[2]);
+      tc_fence_after();
+      const bool wstart = it.win_start(), wend = it.win_end();
+      const uint64_t kb = dB0 + static_cast<uint64_t>((ks * kKRBytes) >> 4);
+      const uint32_t dL = tmem + kColL + kRP * lb;
+#pragma unroll
+      for (int t = 0; t < kA; ++t) {
+        if (t >= nt) break;
+        if (wstart && wc[t] > 0) mbar_wait_t(&rempty[t], static_cast<uint32_t>((wc[t] - 1) & 1), &tr[3]);
+        mbar_wait_t(&full[s], ph, &tr[0]);
+        tc_fence_after();
+        const long long ti = clock64();
+        const uint64_t pa = static_cast<uint64_t>((s * 2 * kPlane) >> 4);
+        const uint64_t aH = dA0 + pa, aL = aH + (kPlane >> 4), lH = dL0 + pa, lL = lH + (kPlane >> 4);
+        const uint32_t dR = tmem + kColR + kRP * t, aK = tmem + kColK + kRP * t;
+        if (elect_one()) {
+          if (!(p.knobs & 32)) {  // timing experiment 32: no MMAs
+#pragma unroll
+          for (int q = 0; q < kTJ / 16; ++q) {
+            if (p.knobs & 256) break;  // timing experiment: no right MMAs
+            mma_ss(dR, aH + q * 128, kb + q * 2, id_r, (wstart && q == 0) ? 0u : 1u);
+            if (all_terms_r) {
+              mma_ss(dR, aH + q * 128, kb + 512 + q * 2, id_r, 1u);
+              mma_ss(dR, aL + q * 128, kb + q * 2, id_r, 1u);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kTI / 16; ++q) {
+            if (p.knobs & 128) break;  // timing experiment: no left MMAs
+            const uint32_t off = ((q >> 2) * 8192 + (q & 3) * 32) >> 4;
+            mma_ts(dL, aK + 8 * q, lH + off, id_l, (t == 0 && q == 0) ? 0u : 1u);
+            if (all_terms_l) mma_ts(dL, aK + 8 * q, lL + off, id_l, 1u);
+          }
+          }
+          umma_commit(&empty[s]);
+          if (wend) umma_commit(&rfull[t]);
+        }
+        __syncwarp();
+        tr[5] += static_cast<unsigned long long>(clock64() - ti);
+        if (wend) ++wc[t];
+        ++k;
+        if (++s == kINS) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+      if (elect_one()) {
+        umma_commit(&kempty[ks]);
+        umma_commit(&lfull[lb]);
+        if (seg_end) umma_commit(kl_free);
+      }
+      __syncwarp();
+      if (seg_end) ++bc;
+    }
+    if (p.trace && lane == 0) {
+      tr[6] = static_cast<unsigned long long>(clock64() - tstart);
+      tr[7] = static_cast<unsigned long long>(k);
+      for (int e = 0; e < 8; ++e) p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + e] = tr[e];
+    }
+  } else if (warp < kIDrain) {
+    // ------------------------------------------------------------------ drains
+    const int q = warp & 3, t = warp >> 2;
+    const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+    const int odd = lane & 1;
+    const bool lstore = !(p.knobs & 8);
+    float acc[kRP];
+#pragma unroll
+    for (int e = 0; e < kRP; ++e) acc[e] = 0.0f;
+    int bc = 0, wc = 0;
+    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long tstart = clock64();
+    int ul = 0;
+    UnitIter it;
+    for (it.init(w); it.more(); it.next(), ++ul) {
+      const int nt = it.nt;
+      const bool mine = t < nt;
+      const int b = it.b, c = it.c;
+      const int lb = ul & 1;
+      if (it.band_start()) {  // row tile t's KRl^T image into TMEM, once the previous band is done
+        if (bc > 0) mbar_wait(kl_free, static_cast<uint32_t>((bc - 1) & 1));
+        __syncwarp();
+        tc_fence_after();
+        if (mine) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __half*>(p.krl_img) +
+                                                              (static_cast<int64_t>(b * kA + t) * 128 + q * 32 + lane) *
+                                                                  kTI) +
+                               hh * 8;
+            uint4 x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = __ldg(src + e);
+            tmem_st32(tmem + lanes + kColK + kRP * t + 32 * hh, x);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kl_full);
+      }
+      if (mine && it.win_end()) {  // right window -> fp32 second level
+        mbar_wait_t(&rfull[t], static_cast<uint32_t>(wc & 1), &tr[0]);
+        __syncwarp();
+        tc_fence_after();
+#pragma unroll
+        for (int c16 = 0; c16 < kRP / 16; ++c16) {
+          if (p.knobs & 64) break;  // timing experiment: no TMEM reads in the drains
+          uint32_t y[16];
+          tmem_ld16(tmem + lanes + kColR + kRP * t + 16 * c16, y);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[16 * c16 + e] += __uint_as_float(y[e]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[t]);
+        ++wc;
+      }
+      // left: lane pairs (hi, lo) of rank 16 q + lane / 2, chunks t, t + 3, t + 6
+      mbar_wait_t(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1), &tr[1]);
+      __syncwarp();
+      tc_fence_after();
+      const int r = 16 * q + (lane >> 1);
+      float* lrow = p.lpart + ((static_cast<int64_t>(b) * w.nC + c) * kRP + r) * kTJ + 4 * odd;
+#pragma unroll
+      for (int c8 = t; c8 < kTJ / 8; c8 += kA) {
+        if (p.knobs & 64) break;
+        uint32_t v[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(tmem + lanes + kColL + kRP * lb + 8 * c8));
+        tmem_wait_ld();
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float keep = __uint_as_float(odd ? v[4 + e] : v[e]);
+          const float give = __uint_as_float(odd ? v[e] : v[4 + e]);
+          o[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+        }
+        if (lstore) *reinterpret_cast<float4*>(lrow + 8 * c8) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lempty[lb]);
+      if (it.seg_end()) {
+        if (mine) {
+          const int64_t slot = (static_cast<int64_t>(cta) * p.slots + (b - seg0)) * kA + t;  // CSR slot
+          double* out = p.rpart + slot * kRP * kTI + q * 32 + lane;
+#pragma unroll
+          for (int e = 0; e < kRP; ++e) {
+            out[e * kTI] = static_cast<double>(acc[e]) * unscale[e];
+            acc[e] = 0.0f;
+          }
+        }
+        ++bc;
+      }
+    }
+    if (p.trace && lane == 0) {
+      tr[6] = static_cast<unsigned long long>(clock64() - tstart);
+      for (int e = 0; e < 8; ++e) p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + e] = tr[e];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kIWMma) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// Operand image of an fp32 tensor view (J rows, K columns, column-major, leading
+// dimension ldy): planes [2][K][LD] fp16, hi = fp16(s y), lo = fp16(s y - hi), rows
+// J..LD-1 zero; s = the tensor's power-of-two scale.  Two rows per thread.
+__global__ void build_f16_image_kernel(const float* __restrict__ y, int64_t J, int64_t ldy, int64_t K, int64_t LD,
+                                       const float* __restrict__ scale, __half2* __restrict__ img) {
+  const float sy = scale[0];
+  const int64_t half = LD / 2, n = half * K, plane = n;  // in half2 units
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / half, i = 2 * (e - j * half);
+    const float* col = y + j * ldy;
+    const float a = i < J ? __ldcs(col + i) * sy : 0.0f;
+    const float b = i + 1 < J ? __ldcs(col + i + 1) * sy : 0.0f;
+    const __half2 hi = __floats2half2_rn(a, b);
+    const float2 back = __half22float2(hi);
+    __stcs(img + e, hi);
+    __stcs(img + plane + e, __floats2half2_rn(a - back.x, b - back.y));
+  }
+}
+
 // KRl^T image for the left MMA's TMEM A operand: [row tile][128 slots][128 i] fp16,
 // slot m = 2 r: hi part of rank r, m = 2 r + 1: its lo part, from the fp64
 // Khatri-Rao rows [L][ld] scaled by the left column scales; rows past L are zero.
@@ -566,6 +968,43 @@ int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream
   set_smem_attr(seed_f32f_kernel, kSmem, cfg);
   launch_k(seed_f32f_kernel, dim3(p.P), dim3(kThreads), kSmem, s, pdl_enabled(), p, *ymap);
   return 1;
+}
+
+int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s) {
+  static unsigned long long cfg = 0;
+  set_smem_attr(seed_f32i_kernel, kISmem, cfg);
+  launch_k(seed_f32i_kernel, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
+  return 1;
+}
+
+int64_t f16_image_ld(int64_t J) { return ceil_div(J, 64) * 64; }
+
+int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
+                           int num_sms, cudaStream_t s) {
+  build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, f16_image_ld(J), scale, static_cast<__half2*>(img));
+  return 1;
+}
+
+bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  const int64_t LD = f16_image_ld(J);
+  if ((reinterpret_cast<uintptr_t>(img) & 127) || K >= (1ll << 31) || LD >= (1ll << 31)) return false;
+  // [2 planes][K][LD] fp16; box 64 i (128 B, swizzled) x 64 j x 1 plane
+  const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(LD), static_cast<cuuint64_t>(K), 2};
+  const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(LD) * 2, static_cast<cuuint64_t>(LD * K) * 2};
+  const cuuint32_t box[3] = {64, 64, 1};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(img), gdim, gstride, box, estride,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int launch_krl_image(const double* rows, int64_t L, int ld, const double* scale, void* img, cudaStream_t s) {

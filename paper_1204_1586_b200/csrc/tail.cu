@@ -72,7 +72,6 @@ __host__ __device__ inline int64_t op_units(const TailOp& o) {
     case kOpReduceRight:                                       // B == 1: warp per output (lanes over slots)
       return o.B == 1 ? o.M * o.R : ((o.M + 31) / 32) * o.R;   // else 32 rows per warp
     case kOpReduceLeft: return ((o.M + 31) / 32) * o.R;        // 32 columns per warp
-    case kOpReduceLeft32: return ((o.M + 31) / 32) * o.R;      // 32 columns per warp
     default: return 0;
   }
 }
@@ -112,24 +111,6 @@ __device__ void run_unit(const TailOp& o, int64_t u, int lane, double* const* gt
       for (int q = o.rb_ptr[rb]; q < o.rb_ptr[rb + 1]; ++q)
         s += o.Z[(static_cast<int64_t>(o.slot_list[q]) * o.RP + r) * o.TI + il];
       out[r * o.ldo + i] = s;
-    }
-  } else if (o.type == kOpReduceLeft32) {  // lanes over columns: 128-byte runs of the [r][64 j] partials
-    const int64_t chunks = (o.M + 31) / 32;
-    const int r = static_cast<int>(u / chunks);
-    const int64_t j = (u - r * chunks) * 32 + lane;
-    if (j < o.M) {
-      const float* z = o.Z32 + ((j >> 6) * 64 + r) * 64 + (j & 63);
-      const int64_t stride = o.ldz * 64 * 64;  // one band: ldz column tiles of [64 r][64 j]
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // fixed order: bands b = 0, 1, ... in four lanes of sums
-      int64_t b = 0;
-      for (; b + 3 < o.B; b += 4) {
-        s0 += static_cast<double>(z[b * stride]);
-        s1 += static_cast<double>(z[(b + 1) * stride]);
-        s2 += static_cast<double>(z[(b + 2) * stride]);
-        s3 += static_cast<double>(z[(b + 3) * stride]);
-      }
-      for (; b < o.B; ++b) s0 += static_cast<double>(z[b * stride]);
-      out[r * o.ldo + j] = ((s0 + s1) + (s2 + s3)) * (o.us_y[0] * o.us_r[r]);
     }
   } else if (o.type == kOpReduceLeft) {  // Ls[r][j] = sum_rb Lpart[rb][r][j]
     const int64_t chunks = (o.M + 31) / 32;
@@ -444,6 +425,55 @@ bool pdl_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+
+// fp32 left partials of the fused fp32 seed, [band][column tile][64 r][64 j] in
+// scaled units: Ls[r][j] = us_y us_r[r] sum_b Z[b][j / 64][r][j % 64].  Thread =
+// four columns of one rank; eight bands' 16-byte loads in flight per thread, the
+// bands summed in a fixed order (b % 2 into two fp64 sums, then added).
+__global__ void __launch_bounds__(256) reduce_left32_kernel(const float* __restrict__ Z, int64_t nB, int64_t nC,
+                                                            int64_t M, int R, const double* __restrict__ us_y,
+                                                            const double* __restrict__ us_r, double* out,
+                                                            double* const* gtab, int out_slot, int64_t ldo) {
+  pdl_wait();
+  if (out_slot >= 0) out = gtab[out_slot];  // the left seed is G(N): written in place
+  const int64_t quads = (M + 3) / 4;
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= quads * R) return;
+  const int r = static_cast<int>(e / quads);
+  const int64_t j0 = (e - r * quads) * 4;  // the four columns share a 64-column tile (padded past M)
+  const float4* z = reinterpret_cast<const float4*>(Z + ((j0 >> 6) * 64 + r) * 64 + (j0 & 63));
+  const int64_t stride = nC * 64 * 64 / 4;  // one band
+  double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t k = 0;
+  for (; k + 7 < nB; k += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldcs(z + (k + q) * stride);
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      a[0] += v[q].x; a[1] += v[q].y; a[2] += v[q].z; a[3] += v[q].w;
+      b[0] += v[q + 1].x; b[1] += v[q + 1].y; b[2] += v[q + 1].z; b[3] += v[q + 1].w;
+    }
+  }
+  for (; k < nB; ++k) {
+    const float4 v = __ldcs(z + k * stride);
+    double* d = (k & 1) ? b : a;
+    d[0] += v.x; d[1] += v.y; d[2] += v.z; d[3] += v.w;
+  }
+  const double us = us_y[0] * us_r[r];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (j0 + c < M) out[r * ldo + j0 + c] = (a[c] + b[c]) * us;
+}
+
+int launch_reduce_left32(const float* Z, int64_t nB, int64_t nC, int64_t M, int R, const double* us_y,
+                         const double* us_r, double* out, double* const* gtab, int out_slot, int64_t ldo,
+                         cudaStream_t s) {
+  const int64_t threads = ((M + 3) / 4) * R;
+  launch_k(reduce_left32_kernel, dim3(static_cast<unsigned>((threads + 255) / 256)), dim3(256), 0, s, pdl_enabled(),
+           Z, nB, nC, M, R, us_y, us_r, out, gtab, out_slot, ldo);
+  return 1;
 }
 
 int launch_tail_step(const TailStep& st0, double* const* gtab, int num_sms, cudaStream_t s) {

@@ -138,3 +138,52 @@ def test_f32_streaming_oracle_slab(gpu_ctx, oracle):
     y.free()
     want = oracle.cp_gradient_all_upm1_f32(slab, 5, f, offset=off, pivot=2)
     assert max(rel_errs(got, want)) <= TOL
+
+
+def test_f32_default_path_is_operand_image(gpu_ctx, oracle):
+    """Hook-free fp32 gradients with R <= 64 run the one-pass seed over the tensor's
+    cached fp16 operand image (seed path 4), rebuilt when the values change."""
+    dims, R = [24, 20, 16, 12], 9
+    y, yv, f = _case(gpu_ctx, oracle, dims, R, seed=21)
+    got = cpd.cp_gradient_all(y, f)
+    assert gpu_ctx.last_seed_path() == 4
+    want, _, _ = oracle.cp_gradient_all(yv, dims, f)
+    assert max(rel_errs(got, want)) <= TOL
+    vals2 = np.random.default_rng(8).uniform(-1, 1, yv.size).astype(np.float32)
+    y.update(vals2.ctypes.data)  # new version: the operand image is rebuilt
+    got2 = cpd.cp_gradient_all(y, f)
+    assert gpu_ctx.last_seed_path() == 4
+    want2, _, _ = oracle.cp_gradient_all(vals2.astype(np.float64), dims, f)
+    assert max(rel_errs(got2, want2)) <= TOL
+
+
+_PATH_CHECK = r"""
+import sys, json, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + '/oracle')
+import oracle as O, paper_1204_1586_b200 as cpd
+ctx = cpd.Context(0)
+out = []
+for dims, R in [([40, 40, 40, 40], 64), ([7, 9, 11, 13], 8), ([130, 257], 3), ([300, 300, 20], 16)]:
+    y = cpd.DenseTensor.generate(dims, cpd.DIST_UNIFORM_PM1, seed=11, ctx=ctx, dtype=cpd.F32)
+    yv = y.values().astype(np.float64)
+    f = [O.fill_normal(110 + k, d * R).reshape(d, R, order='F') for k, d in enumerate(dims)]
+    g = cpd.cp_gradient_all(y, f)
+    w, _, _ = O.cp_gradient_all(yv, dims, f)
+    err = max(float(np.linalg.norm(a - b) / np.linalg.norm(b)) for a, b in zip(g, w))
+    out.append([ctx.last_seed_path(), err])
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env,path", [({"CPDGPU_F32_IMAGE": "0"}, 3), ({"CPDGPU_F32_FUSED": "0"}, 2)])
+def test_f32_alternate_seed_paths(env, path):
+    """The fused pass with the split inside the kernel (3, used when the operand
+    image does not fit in memory) and the two-pass seed (2) against the oracle."""
+    import json, os, subprocess, sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    res = subprocess.run([sys.executable, "-c", _PATH_CHECK.format(root=root)], env={**os.environ, **env},
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    for got_path, err in json.loads(res.stdout.strip().splitlines()[-1]):
+        assert got_path == path and err <= TOL, (got_path, err)

@@ -14,6 +14,6 @@ for k in ${KNOBS:-0 1 2 6 8 15}; do
   CPDGPU_F32F_KNOBS=$k timeout 300 $B >> gpurun_out/${TAG}_bench.txt 2>&1
 done
 if [ "${NCU:-1}" = 1 ]; then
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:seed_f32f -c 1 -o gpurun_out/${TAG}_c5 -f \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:${KREGEX:-seed_f32} -c 1 -o gpurun_out/${TAG}_c5 -f \
   python bench.py --config c5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-alg1 > gpurun_out/${TAG}_ncu.log 2>&1
 fi
