@@ -10,7 +10,8 @@ from .api import (DIST_NORMAL, DIST_UNIFORM_PM1, F32, F64, Context, CostCounter,
                   cp_gradient_all, cp_gradient_all_device, default_context, fast_count_realized,
                   fast_update_order, pinv_psd, run, select_pivot, sort_modes, mttkrp_direct,
                   mttkrp_direct_device, als_sweep_direct, mu_sweep, gd_step, uniform01, random_init,
-                  generate_problem, cost, relative_error, cp_gradient_set)
+                  generate_problem, cost, relative_error, cp_gradient_set, Communicator,
+                  comm_unique_id, slab_bounds, cp_gradient_all_sharded, cp_gradient_all_sharded_device)
 
 __all__ = [
     "ArgumentError", "CpdError", "DeviceError", "DomainError", "IndexError", "NumericError", "ParseError",
@@ -19,5 +20,6 @@ __all__ = [
     "als_update_mode", "cp_gradient_all", "cp_gradient_all_device", "default_context",
     "fast_count_realized", "fast_update_order", "pinv_psd", "run", "select_pivot", "sort_modes",
     "mttkrp_direct", "mttkrp_direct_device", "als_sweep_direct", "mu_sweep", "gd_step", "uniform01",
-    "random_init", "generate_problem", "cost", "relative_error", "cp_gradient_set",
+    "random_init", "generate_problem", "cost", "relative_error", "cp_gradient_set", "Communicator",
+    "comm_unique_id", "slab_bounds", "cp_gradient_all_sharded", "cp_gradient_all_sharded_device",
 ]

@@ -20,6 +20,9 @@ c_dbl_p = C.POINTER(C.c_double)
 c_dbl_pp = C.POINTER(c_dbl_p)
 
 HOOK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, c_dbl_p, c_i64, c_i64, c_u64)
+# cpdgpu_allreduce_fn: sum `count` doubles of buf across the ranks, in place
+ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, c_dbl_p, c_i64)
+COMM_ID_BYTES = 128
 
 # name -> (restype, argtypes); mirrors include/cpdgpu.h one to one
 SIGNATURES = {
@@ -55,6 +58,15 @@ SIGNATURES = {
     "cpdgpu_cost": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, c_dbl_p]),
     "cpdgpu_tensor_load_tdnb": (C.c_int, [C.c_void_p, C.c_char_p, c_i64, c_i64, C.POINTER(C.c_void_p)]),
     "cpdgpu_tensor_save_tdnb": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p]),
+    "cpdgpu_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "cpdgpu_comm_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "cpdgpu_comm_init_host": (C.c_int, [C.c_void_p, C.c_int, C.c_int, ALLREDUCE, C.c_void_p]),
+    "cpdgpu_comm_destroy": (C.c_int, [C.c_void_p]),
+    "cpdgpu_slab_bounds": (C.c_int, [c_i64, C.c_int, C.c_int, C.POINTER(c_i64), C.POINTER(c_i64)]),
+    "cpdgpu_cp_gradient_all_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(c_i64), c_i64, c_dbl_pp,
+                                                 c_dbl_pp, C.POINTER(c_u64)]),
+    "cpdgpu_cp_gradient_all_sharded_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(c_i64), c_i64,
+                                                        C.c_void_p, C.c_void_p]),
     "cpdgpu_mttkrp_direct": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_int, c_dbl_p, C.POINTER(c_u64)]),
     "cpdgpu_mttkrp_direct_device": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, C.c_void_p, C.c_int, C.c_void_p]),
     "cpdgpu_als_sweep_direct": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.POINTER(C.c_int), C.c_int,

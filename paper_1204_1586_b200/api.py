@@ -365,6 +365,92 @@ def cp_gradient_all_device(y: DenseTensor, R: int, factors_dev_ptr: int, grads_d
                                                     C.c_void_p(grads_dev_ptr), int(pivot)), ctx.h)
 
 
+# ---- multi-GPU: last-mode slabs, the exchange inside libcpdgpu.so (SURVEY.md §8e) ----
+
+def slab_bounds(extent: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) of rank's contiguous last-mode slab (cpdgpu_slab_bounds)."""
+    L = _lib.load()
+    lo, hi = C.c_int64(), C.c_int64()
+    _lib.check(L.cpdgpu_slab_bounds(int(extent), int(world), int(rank), C.byref(lo), C.byref(hi)))
+    return int(lo.value), int(hi.value)
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 makes it, the caller broadcasts it)."""
+    L = _lib.load()
+    buf = (C.c_ubyte * _lib.COMM_ID_BYTES)()
+    _lib.check(L.cpdgpu_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Communicator:
+    """The context's communicator for cp_gradient_all_sharded: NCCL (one rank per
+    GPU, in-place ncclAllReduce on the context stream) or a caller-supplied host
+    all-reduce ``fn(np.ndarray) -> None`` that sums a float64 buffer in place
+    across the ranks (gloo, MPI, ...)."""
+
+    def __init__(self, ctx: Context, world: int, rank: int, unique_id: Optional[bytes] = None,
+                 host_allreduce: Optional[Callable[[np.ndarray], None]] = None) -> None:
+        self.ctx, self.world, self.rank = ctx, int(world), int(rank)
+        self._cb = None
+        L = ctx._L
+        if host_allreduce is not None:
+            err: list = []
+
+            def _ar(user, buf, count):
+                try:
+                    host_allreduce(np.ctypeslib.as_array(buf, shape=(int(count),)))
+                    return 0
+                except BaseException as e:  # noqa: BLE001 - surfaced through the status
+                    err.append(e)
+                    return 7  # CPDGPU_CUDA_ERROR class: the exchange failed
+            self._errors = err
+            self._cb = _lib.ALLREDUCE(_ar)
+            _lib.check(L.cpdgpu_comm_init_host(ctx.h, self.world, self.rank, self._cb, None), ctx.h)
+        else:
+            if unique_id is None or len(unique_id) != _lib.COMM_ID_BYTES:
+                raise errors.ArgumentError("Communicator: need the 128-byte NCCL unique id or a host all-reduce")
+            buf = (C.c_ubyte * _lib.COMM_ID_BYTES).from_buffer_copy(unique_id)
+            _lib.check(L.cpdgpu_comm_init(ctx.h, buf, self.world, self.rank), ctx.h)
+
+    def bounds(self, extent: int) -> tuple[int, int]:
+        return slab_bounds(extent, self.world, self.rank)
+
+    def close(self) -> None:
+        if self.ctx is not None and self.ctx.h:
+            _lib.check(self.ctx._L.cpdgpu_comm_destroy(self.ctx.h), self.ctx.h)
+        self.ctx = None
+
+
+def cp_gradient_all_sharded(slab: DenseTensor, global_dims: Sequence[int], factors: list,
+                            counter: Optional[CostCounter] = None) -> list[np.ndarray]:
+    """Sharded all-mode gradient (mttkrp.hpp:59-69 over a last-mode slab): every
+    rank passes its slab and the GLOBAL factors and receives every global G(n).
+    The context needs a Communicator; the exchange runs inside the library."""
+    gd = [int(d) for d in global_dims]
+    bufs = _factor_bufs(factors, gd)
+    R = bufs[0].shape[1]
+    grads = [np.empty((d, R), dtype=np.float64, order="F") for d in gd]
+    mults = (C.c_uint64 * len(gd))()
+    ctx = slab.ctx
+    _lib.check(ctx._L.cpdgpu_cp_gradient_all_sharded(ctx.h, slab.h, len(gd), _dims_arg(gd), R, _ptr_array(bufs),
+                                                     _ptr_array(grads), mults), ctx.h)
+    if counter is not None:
+        counter.charge(sum(int(m) for m in mults))
+    return grads
+
+
+def cp_gradient_all_sharded_device(slab: DenseTensor, global_dims: Sequence[int], R: int, factors_dev_ptr: int,
+                                   out_dev_ptr: int) -> None:
+    """Device form, ordered on the context stream: the slab's packed factors in,
+    the packed GLOBAL gradients [G(1..N-1) | G(N)] out (every rank)."""
+    gd = [int(d) for d in global_dims]
+    ctx = slab.ctx
+    _lib.check(ctx._L.cpdgpu_cp_gradient_all_sharded_device(ctx.h, slab.h, len(gd), _dims_arg(gd), int(R),
+                                                            C.c_void_p(factors_dev_ptr), C.c_void_p(out_dev_ptr)),
+               ctx.h)
+
+
 # ---- direct MTTKRP (mttkrp.hpp:19-20): Algorithm 1's one-pass-per-mode cost ---------
 
 def mttkrp_direct(y: DenseTensor, factors: list, n: int, counter: Optional[CostCounter] = None) -> np.ndarray:

@@ -127,3 +127,23 @@ def sharded_gradient(plan: SlabPlan, local_compute: Callable, dist, group=None):
     (1-D torch tensor); then the exchange."""
     local_out = local_compute()
     return exchange(plan, local_out, dist, group)
+
+
+def library_comm(ctx, dist, group=None):
+    """The library-side communicator (cpdgpu_comm_*) of this rank, built from an
+    initialised torch.distributed group: NCCL backends get an NCCL communicator
+    inside libcpdgpu.so (rank 0's unique id broadcast over the group), anything
+    else (gloo) a host all-reduce through the group."""
+    import torch
+    from . import api
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if dist.get_backend(group) == "nccl":
+        obj = [api.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return api.Communicator(ctx, world, rank, unique_id=obj[0])
+
+    def host_allreduce(buf):
+        t = torch.from_numpy(buf)  # shares the library's pinned host buffer
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    return api.Communicator(ctx, world, rank, host_allreduce=host_allreduce)

@@ -106,3 +106,15 @@ def test_status_mapping():
     for code, cls in [(1, cpd.ShapeError), (2, cpd.IndexError), (3, cpd.ArgumentError), (4, cpd.NumericError),
                       (5, cpd.DomainError), (6, cpd.DeviceError), (8, cpd.ParseError)]:
         assert isinstance(errors.from_status(code, "m"), cls)
+
+
+def test_slab_bounds_through_the_abi(lib):
+    """cpdgpu_slab_bounds (host logic, no device) splits the last mode like sharded.slab_bounds."""
+    from paper_1204_1586_b200 import sharded
+    for extent, world in [(300, 8), (300, 3), (10, 3), (7, 7), (60, 2)]:
+        want = sharded.slab_bounds(extent, world)
+        assert [cpd.slab_bounds(extent, world, r) for r in range(world)] == want
+    with pytest.raises(cpd.ArgumentError):
+        cpd.slab_bounds(10, 0, 0)
+    with pytest.raises(cpd.ArgumentError):
+        cpd.slab_bounds(10, 2, 2)
