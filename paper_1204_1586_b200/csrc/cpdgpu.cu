@@ -275,7 +275,9 @@ struct Plan {
   // tile geometry; gradient_body swaps it in for the seed partials' consumers.
   struct I8 {
     bool ok = false;   // geometry built (one rank chunk, both seeds, even J_p)
-    bool on = false;   // bound tensor passed the range guard and has a TMA view
+    bool on = false;   // tensor_ok && factors_ok: the gradient runs the int8 pass
+    bool tensor_ok = false;   // bound tensor passed the range guard and has a TMA view
+    bool factors_ok = true;   // the call's factors passed the Khatri-Rao range guard
     int N = 0;         // MMA rank block (16 or 32)
     int NL = 0;        // left rank block (24 when R <= 24 < N)
     int64_t nRB = 0, nCT = 0, T = 0;
@@ -310,10 +312,9 @@ struct Plan {
     DevBuf krl_img, lpart32;
     // the tensor's fp16 hi / lo operand image (built once per tensor version; the
     // kernel then has no split stage); off when it does not fit in memory
-    bool img_on = false;
+    bool img_on = false, img_failed = false;
     void* img = nullptr;
     uint64_t img_version = ~0ull;
-    CUtensorMap imap{};
     ~F32Fused() {
       if (img) cudaFree(img);
     }
@@ -435,8 +436,17 @@ struct cpdgpu_ctx {
     return static_cast<unsigned long long*>(tl.p);
   }
   int tl_slot() { return tl_next < 64 ? tl_next++ : 63; }
+  // pipeline watchdog (seed kernels): a barrier wait that never completes sets this
+  // word (mapped pinned host memory, so the host reads it without a copy) and the
+  // kernel unwinds instead of trapping; the next API return reports it
+  volatile int* fault_host = nullptr;
+  int* fault_dev = nullptr;
+  volatile int* guard_host = nullptr;  // int8 factor-range guard result (mapped)
+  int* guard_dev = nullptr;
   ~cpdgpu_ctx() {
     for (auto e : seed_events) cudaEventDestroy(e);
+    if (fault_host) cudaFreeHost(const_cast<int*>(fault_host));
+    if (guard_host) cudaFreeHost(const_cast<int*>(guard_host));
   }
 };
 
@@ -451,6 +461,13 @@ template <typename F>
 int guarded(cpdgpu_ctx* ctx, F&& f) {
   try {
     f();
+    if (ctx && ctx->fault_host && *ctx->fault_host) {  // a seed kernel's watchdog fired
+      const int code = *ctx->fault_host;
+      *ctx->fault_host = 0;
+      return set_error(ctx, CPDGPU_CUDA_ERROR,
+                       "seed pipeline stalled (watchdog code " + std::to_string(code) +
+                           "): the kernel unwound, results of the calls since the last check are invalid");
+    }
     if (ctx) ctx->err.clear();
     return CPDGPU_OK;
   } catch (const Failure& e) {
@@ -807,9 +824,13 @@ Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
   return raw;
 }
 
-// fp32: power-of-two Y scale (cached per tensor version), rows padded to a
-// multiple of 8 when needed, and the two 3-D TMA views.  Runs eagerly.
-void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
+// fp32: power-of-two Y scale (cached per tensor version), then either the fp16
+// operand image (hook-free gradients on the fused pass: the only view that pass
+// reads) or the split passes' view: rows padded to J8 when needed and the two 3-D
+// TMA maps.  Each is built lazily, once per tensor version, eagerly (outside any
+// graph capture): a fused-gradient caller never makes the padded copy (at 300^4
+// that is 32 GB of HBM and a 29 ms copy the fused pass would not read).
+void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gradient) {
   const float* src = static_cast<const float*>(pl.raw_frame ? t->data : t->sorted);
   if (t->scale_version != t->version) {
     t->yscale.ensure(32);
@@ -819,6 +840,26 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
                                             reinterpret_cast<double*>(b + 8), ctx->num_sms, ctx->stream);
     CK(cudaGetLastError());
     t->scale_version = t->version;
+  }
+  if (pl.ff.on && fused_gradient) {  // operand image for the fused seed (CPDGPU_F32_IMAGE=0: split in the kernel)
+    static const char* img_env = std::getenv("CPDGPU_F32_IMAGE");
+    Plan::F32Fused& ff = pl.ff;
+    if (!ff.img && !ff.img_failed && !(img_env && std::atoi(img_env) == 0)) {
+      const size_t bytes = static_cast<size_t>(cpdgpu::f16_image_bytes(pl.Jp, pl.Kp));
+      if (cudaMalloc(&ff.img, bytes) != cudaSuccess) {
+        cudaGetLastError();  // out of memory: keep the split-in-kernel path
+        ff.img = nullptr;
+        ff.img_failed = true;
+      }
+    }
+    ff.img_on = ff.img != nullptr;
+    if (ff.img_on && ff.img_version != t->version) {
+      ctx->launches += cpdgpu::launch_build_f16_image(src, pl.Jp, pl.Jp, pl.Kp, static_cast<const float*>(t->yscale.p),
+                                                      ff.img, ctx->num_sms, ctx->stream);
+      CK(cudaGetLastError());
+      ff.img_version = t->version;
+    }
+    if (ff.img_on) return;
   }
   const void* base = src;
   if (pl.J8 != pl.Jp) {
@@ -831,33 +872,18 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
     }
     base = pl.ypad.p;
   }
-  if (pl.ff.on) {  // operand image for the fused seed (CPDGPU_F32_IMAGE=0: split in the kernel)
-    static const char* img_env = std::getenv("CPDGPU_F32_IMAGE");
-    Plan::F32Fused& ff = pl.ff;
-    if (!ff.img && !(img_env && std::atoi(img_env) == 0)) {
-      const size_t bytes = static_cast<size_t>(2 * cpdgpu::f16_image_ld(pl.Jp) * pl.Kp) * 2;
-      if (cudaMalloc(&ff.img, bytes) != cudaSuccess) {
-        cudaGetLastError();  // out of memory: keep the split-in-kernel path
-        ff.img = nullptr;
-      } else if (!cpdgpu::make_tensor_map_f16_image(&ff.imap, ff.img, pl.Jp, pl.Kp)) {
-        cudaFree(ff.img);
-        ff.img = nullptr;
-      }
-    }
-    ff.img_on = ff.img != nullptr;
-    if (ff.img_on && ff.img_version != t->version) {
-      ctx->launches += cpdgpu::launch_build_f16_image(src, pl.Jp, pl.Jp, pl.Kp, static_cast<const float*>(t->yscale.p),
-                                                      ff.img, ctx->num_sms, ctx->stream);
-      CK(cudaGetLastError());
-      ff.img_version = t->version;
-    }
-  }
   if (pl.ymap_base != base) {
     if (!cpdgpu::make_tensor_map_y32(&pl.ymap_r, base, pl.J8, pl.Kp, 0) ||
         !cpdgpu::make_tensor_map_y32(&pl.ymap_l, base, pl.J8, pl.Kp, 1))
       fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: fp32 tensor view not addressable by TMA");
     pl.ymap_base = base;
   }
+}
+
+void set_i8_on(Plan& pl) {
+  const bool on = pl.i8.tensor_ok && pl.i8.factors_ok;
+  if (on != pl.i8.on) pl.drop_graphs();  // the recorded gradient used the other seed path
+  pl.i8.on = on;
 }
 
 // int8 fused seed: the tensor's scale record (cached per tensor version), the
@@ -888,16 +914,81 @@ void bind_i8(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const void* ybase) {
                                     static_cast<uint64_t>(pl.Jp) * 8, 16, 128, true, true);
     pl.i8.ymap_base = on ? ybase : nullptr;
   }
-  if (on != pl.i8.on) pl.drop_graphs();  // the recorded gradient used the other seed path
-  pl.i8.on = on;
+  pl.i8.tensor_ok = on;
+  set_i8_on(pl);
 }
 
-void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
+// int8 range guard for the call's factors.  The pass holds every product to ~2^-47
+// max|Y| S_r absolute (48-bit digits of Y scaled by max|Y| and of each Khatri-Rao
+// column by S_r = prod_m max_i |A_m[i, r]|, kr_digits_kernel; 21 of 36 digit
+// pairs), while a gradient entry is ~ rms(Y) rms(KR_r) per term, so the relative
+// error is ~2^-47 (max|Y| / mean|Y|) (S_r / rms KR_r) with rms KR_r =
+// prod_m rms_i A_m[i, r] (mean |Y| <= rms |Y|: conservative).  The pass runs only
+// while that product stays <= 2^11 (<= ~1.5e-11, under the 1e-10 gate): N(0,1)
+// data sits near 2^7 (c2 ~110, c3 ~60).  Otherwise, and for non-finite factors,
+// the call runs the fp64 DMMA pass (kron.cpp:54-68 products, mttkrp.cpp:160,207).
+constexpr double kI8ErrorBudget = 2048.0;
+double i8_factor_limit(const cpdgpu_tensor* t) {
+  return t->amax8 > 0.0 ? kI8ErrorBudget * t->amean8 / t->amax8 : kI8ErrorBudget;
+}
+bool i8_factors_ok_host(const Plan& pl, const double* const* mode_factors, bool caller_order, double limit) {
+  for (int side = 0; side < 2; ++side) {
+    const int lo = side == 0 ? pl.p + 1 : 1, hi = side == 0 ? pl.N : pl.p;
+    for (int64_t r = 0; r < pl.R; ++r) {
+      double ratio = 1.0;
+      for (int j = lo; j <= hi; ++j) {
+        const int m = caller_order ? pl.perm[j - 1] - 1 : j - 1;
+        const int64_t I = pl.sd[j - 1];
+        const double* col = mode_factors[m] + I * r;
+        double mx = 0.0, ss = 0.0;
+        for (int64_t i = 0; i < I; ++i) {
+          const double a = std::abs(col[i]);
+          if (!std::isfinite(a)) return false;
+          mx = std::max(mx, a);
+          ss += a * a;
+        }
+        if (mx == 0.0) {  // a zero column: its Khatri-Rao column is exactly 0
+          ratio = 0.0;
+          break;
+        }
+        ratio *= mx / std::sqrt(ss / static_cast<double>(I));
+      }
+      if (!(ratio <= limit)) return false;
+    }
+  }
+  return true;
+}
+
+KRSpec spec_over(const Plan& pl, const double* base, bool orig, int lo, int hi, int r0);
+
+// The same guard on device-resident factors (the packed caller-order buffer of the
+// device entry points): one tiny kernel into mapped host memory and a stream sync,
+// paid only by calls that would otherwise take the int8 pass.
+bool i8_factors_ok_device(cpdgpu_ctx* ctx, const Plan& pl, const double* fdev, double limit) {
+  *ctx->guard_host = 0;
+  ctx->launches += cpdgpu::launch_i8_factor_guard(spec_over(pl, fdev, true, pl.p + 1, pl.N, 0),
+                                                  spec_over(pl, fdev, true, 1, pl.p, 0), static_cast<int>(pl.R),
+                                                  limit, ctx->guard_dev, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return *ctx->guard_host == 0;
+}
+
+void i8_apply_factor_guard(Plan& pl, bool ok) {
+  pl.i8.factors_ok = ok;
+  set_i8_on(pl);
+}
+
+// fused_gradient: the caller runs a hook-free all-mode gradient (the fp32 fused
+// pass reads the operand image, not the split passes' view)
+void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gradient = false) {
   if (pl.f32) {
-    bind_f32_inputs(ctx, pl, t);
-    if (pl.graph_ybase != pl.ymap_base) {
+    bind_f32_inputs(ctx, pl, t, fused_gradient);
+    // a recorded gradient follows the view it read (the image buffer is stable)
+    const void* gb = fused_gradient && pl.ff.img_on ? pl.ff.img : pl.ymap_base;
+    if (pl.graph_ybase != gb) {
       pl.drop_graphs();
-      pl.graph_ybase = pl.ymap_base;
+      pl.graph_ybase = gb;
     }
     return;
   }
@@ -937,6 +1028,13 @@ void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t) {
   if (pl.i8.ok) bind_i8(ctx, pl, t, ybase);
 }
 
+// Tests only: CPDGPU_FORCE_STALL=1 makes the next seed launches stall on purpose so
+// the watchdog path (fault word, no trap) can be exercised; read per launch.
+int force_stall() {
+  const char* e = std::getenv("CPDGPU_FORCE_STALL");
+  return e && std::atoi(e) != 0 ? 1 : 0;
+}
+
 // ---- K1 launches ---------------------------------------------------------------
 cudaEvent_t seed_event(cpdgpu_ctx* ctx) {
   if (ctx->seed_used == ctx->seed_events.size()) {
@@ -958,10 +1056,9 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
   if (mode == 3 && pl.ff.on) {  // both seeds in one pass over Y
     Plan::Chunk& c = pl.chunks[0];
     double* sc = c.scales->d();
-    ctx->launches += cpdgpu::launch_kr_scale(pl.spec(pl.p + 1, pl.N, c.r0), pl.spec(1, pl.p, c.r0), c.Rc, sc,
-                                             sc + 2 * RPc, s);
-    ctx->launches += cpdgpu::launch_kr_split(c.KRr->d(), pl.Kp, RPc, sc, c.KRr16->p, s);
-    ctx->launches += cpdgpu::launch_krl_image(c.KRl->d(), pl.Jp, RPc, sc + RPc, pl.ff.krl_img.p, s);
+    // scales, right B tiles and the KRl^T image straight from the sorted factors
+    ctx->launches += cpdgpu::launch_kr_fused_operands(pl.spec(pl.p + 1, pl.N, c.r0), pl.Kp, pl.spec(1, pl.p, c.r0),
+                                                      pl.Jp, c.Rc, sc, sc + 2 * RPc, c.KRr16->p, pl.ff.krl_img.p, s);
     cpdgpu::Seed32FParams q{};
     q.kr_tiles = static_cast<const unsigned char*>(c.KRr16->p);
     q.krl_img = pl.ff.krl_img.p;
@@ -978,6 +1075,8 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
     q.window = pl.ff.window;
     static const char* knob_env = std::getenv("CPDGPU_F32F_KNOBS");
     q.knobs = knob_env ? std::atoi(knob_env) : 0;
+    q.fault = ctx->fault_dev;
+    q.stall = force_stall();
     static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
     DevBuf tb;
     if (trace && pl.ff.img_on) {
@@ -986,7 +1085,8 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
       q.trace = static_cast<unsigned long long*>(tb.p);
     }
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
-    ctx->launches += pl.ff.img_on ? cpdgpu::launch_seed_f32i(q, &pl.ff.imap, s)
+    q.img = static_cast<const unsigned char*>(pl.ff.img);
+    ctx->launches += pl.ff.img_on ? cpdgpu::launch_seed_f32i(q, s)
                                   : cpdgpu::launch_seed_f32f(q, &pl.ymap_r, s);
     if (q.trace) {
       std::vector<unsigned long long> h(static_cast<size_t>(q.P) * 128);
@@ -1093,6 +1193,8 @@ void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
   q.progress = dbg ? static_cast<unsigned*>(progress.p) : nullptr;
   static const int knobs = std::getenv("CPDGPU_I8_KNOBS") ? std::atoi(std::getenv("CPDGPU_I8_KNOBS")) : 0;
   q.knobs = knobs;
+  q.fault = ctx->fault_dev;
+  q.stall = force_stall();
   q.Lpart = g.nRB == 1 ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d() + c.lpart_off;
   static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
   DevBuf tb;
@@ -1730,8 +1832,10 @@ void sweep_body(cpdgpu_ctx* ctx, Plan& pl, const ModeCallback& after) {
 // each call patches the prologue node (input factors, output pointers).
 void run_gradient(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_base) {
   const bool left = pl.p + 1 <= pl.N;
-  // the int8 seed builds its Khatri-Rao digits from the sorted factors itself
-  cpdgpu::Prologue pr = grad_prologue(pl, fin, gout_base, pl.i8.on ? 0 : (left ? 3 : 1));
+  // the int8 seed builds its Khatri-Rao digits from the sorted factors itself, and
+  // the fused fp32 pass its fp16 operands (launch_kr_fused_operands): no fp64 rows
+  const bool own_kr = pl.i8.on || (pl.f32 && left && pl.ff.on);
+  cpdgpu::Prologue pr = grad_prologue(pl, fin, gout_base, own_kr ? 0 : (left ? 3 : 1));
   pr.tl = ctx->tl_ptr();
   timeline_reset(ctx);
   struct PrintAtExit {
@@ -2156,6 +2260,16 @@ int cpdgpu_create(cpdgpu_ctx** out, int device) {
            device, major, minor);
     CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
     ctx->stream = ctx->own;
+    int* fh = nullptr;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&fh), sizeof(int), cudaHostAllocMapped));
+    *fh = 0;
+    ctx->fault_host = fh;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->fault_dev), fh, 0));
+    int* gh = nullptr;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&gh), sizeof(int), cudaHostAllocMapped));
+    *gh = 0;
+    ctx->guard_host = gh;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->guard_dev), gh, 0));
   });
   if (st != CPDGPU_OK) return st;
   *out = ctx.release();
@@ -2575,7 +2689,8 @@ int cpdgpu_cp_gradient_all(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, const d
     if (!factors || !gradients) fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: null factor or gradient list");
     ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, 0);
-    bind_seed_inputs(ctx, pl, y);
+    bind_seed_inputs(ctx, pl, y, true);
+    if (pl.i8.tensor_ok) i8_apply_factor_guard(pl, i8_factors_ok_host(pl, factors, true, i8_factor_limit(y)));
     upload_host_factors(ctx, pl, y, factors);
     run_gradient(ctx, pl, pl.Forig.d(), pl.Gorig.d());
     CK(cudaMemcpyAsync(pl.hG.d(), pl.Gorig.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
@@ -2633,7 +2748,8 @@ int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, 
       fail(CPDGPU_ARGUMENT_ERROR, "cp_gradient_all: pivot %d outside 0..%zu", pivot, y->dims.size());
     if (pivot == 0) ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, pivot);
-    bind_seed_inputs(ctx, pl, y);
+    bind_seed_inputs(ctx, pl, y, true);
+    if (pl.i8.tensor_ok) i8_apply_factor_guard(pl, i8_factors_ok_device(ctx, pl, factors_dev, i8_factor_limit(y)));
     run_gradient(ctx, pl, factors_dev, gradients_dev);
     CK(cudaGetLastError());
   });
@@ -3064,7 +3180,8 @@ void sharded_device(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, const ShardGeom& g, in
   const int64_t rows = g.hi - g.lo, IN = g.gdims[g.N - 1];
   c.lbuf.ensure(static_cast<size_t>(g.partial + rows * R) * sizeof(double));
   Plan& pl = *get_plan(ctx, slab, R, g.pivot);
-  bind_seed_inputs(ctx, pl, slab);
+  bind_seed_inputs(ctx, pl, slab, true);
+  if (pl.i8.tensor_ok) i8_apply_factor_guard(pl, i8_factors_ok_device(ctx, pl, fdev, i8_factor_limit(slab)));
   run_gradient(ctx, pl, fdev, c.lbuf.d());
   CK(cudaMemcpyAsync(out_dev, c.lbuf.d(), static_cast<size_t>(g.partial) * sizeof(double), cudaMemcpyDeviceToDevice,
                      ctx->stream));

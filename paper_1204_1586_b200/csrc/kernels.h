@@ -78,6 +78,8 @@ struct SeedI8Params {
   unsigned* progress;  // CPDGPU_I8_DEBUG: [P][16] per-warp positions for the watchdog report
   unsigned long long* trace;  // CPDGPU_SEED_TRACE: [P][14][6] per-warp wait cycles, total, tiles
   int knobs;                  // CPDGPU_I8_KNOBS experiments (bit 0: no digit stores)
+  int* fault;                 // context fault word: the watchdog's report (no trap)
+  int stall;                  // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
 };
 // left rank block for a right block N and rank R (24 when it lets the left accumulators
 // double-buffer in TMEM), and the left digit image bytes per row block
@@ -86,6 +88,9 @@ size_t i8_left_image_bytes(int NL);
 size_t i8_right_image_bytes(int N, int NL);
 // ymap: Y (dim0 J, dim1 K) fp64, box 16 x 128, 128-byte swizzle
 int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s);
+// int8 factor-range guard (both sides' Khatri-Rao columns): *flag |= 1 when a column's
+// max / rms product exceeds `limit` or a factor entry is not finite
+int launch_i8_factor_guard(const KRSpec& right, const KRSpec& left, int R, double limit, int* flag, cudaStream_t s);
 // Khatri-Rao rows [L][ldk] -> digit images [ceil(L / 128)][6][N][128] + weights [.][N]
 // Khatri-Rao digit images [tiles][6][N][128] + column weights [tiles][N] of both
 // sides, from the factors (right: K_p rows, left: J_p rows; one launch)
@@ -137,21 +142,25 @@ struct Seed32FParams {
   int knobs;  // CPDGPU_F32F_KNOBS timing experiments (wrong results): 1 no split stores,
               // 2 one right MMA per k-step, 4 one left MMA per k-step, 8 no left partial stores,
               // 16 (image kernel) no plane refills after the first ring, 32 (image kernel) no MMAs
+  int* fault;  // context fault word: the watchdog's report (no trap)
+  int stall;   // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
+  const unsigned char* img;  // image kernel: the tensor's operand image (launch_build_f16_image)
 };
 int seed_f32f_band_tiles();  // 3
 // ymap: the right pass's map (box 128 i x 64 j, no swizzle)
 int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream_t s);
 // The same kernel reading a cached operand image of the tensor instead of the fp32
-// values (no split stage).  imap: make_tensor_map_f16_image of that image.
-int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s);
-// operand image of an fp32 view (J x K, leading dimension ldy): [2][K][LD] fp16
-// planes hi = fp16(s y), lo = fp16(s y - hi), LD = f16_image_ld(J) (rows past J zero)
-int64_t f16_image_ld(int64_t J);
+// values (no split stage): Seed32FParams::img, launch_build_f16_image's layout.
+int launch_seed_f32i(const Seed32FParams& p, cudaStream_t s);
+// operand image of an fp32 view (J x K, leading dimension ldy): 32 KB pre-swizzled
+// fp16 hi / lo tiles in the fused pass's unit order (f16_image_bytes in total)
+int64_t f16_image_bytes(int64_t J, int64_t K);
 int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
                            int num_sms, cudaStream_t s);
-bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K);
-// fp64 rows [L][ld] (ld <= 64) -> KRl^T TMEM image [ceil(L / 128)][128][128] fp16
-int launch_krl_image(const double* rows, int64_t L, int ld, const double* scale, void* img, cudaStream_t s);
+// fused pass: column scales, right B tiles and the KRl^T image straight from the
+// sorted factors (two launches, no fp64 Khatri-Rao rows)
+int launch_kr_fused_operands(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, double* scale,
+                             double* inv, void* rtiles, void* limg, cudaStream_t s);
 // column scales of the right (scale[0..63]) and left (scale[64..127]) Khatri-Rao rows
 int launch_kr_scale(const KRSpec& right, const KRSpec& left, int R, double* scale, double* inv, cudaStream_t s);
 // fp64 rows [L][ld] (ld <= 64) -> tiles (see Seed32Params::kr_tiles)

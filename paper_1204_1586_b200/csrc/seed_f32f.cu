@@ -89,15 +89,47 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
                : "memory");
 }
+// Watchdog (per CTA, static shared state of this file's kernels): a wait that
+// spins wd_limit times records the fault in the context's fault word and raises
+// the CTA's abort flag, after which every wait returns at once, so a broken
+// pipeline unwinds and exits instead of hanging the GPU or trapping.
+__shared__ int wd_abort;
+__shared__ int* wd_fault;
+__shared__ uint32_t wd_limit;
+__device__ __forceinline__ void wd_init(int* fault, int stall) {
+  wd_abort = 0;
+  wd_fault = fault;
+  wd_limit = stall ? (1u << 16) : (1u << 31);
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
+  uint32_t done = 0, spins = 0;
   while (!done) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    if (done) break;
+    if (*reinterpret_cast<volatile int*>(&wd_abort)) return;
+    if (++spins >= wd_limit) {
+      if (wd_fault) atomicExch(wd_fault, 2000);
+      *reinterpret_cast<volatile int*>(&wd_abort) = 1;
+      __threadfence_block();
+      return;
+    }
   }
+}
+__device__ __forceinline__ bool wd_aborted() { return *reinterpret_cast<volatile int*>(&wd_abort) != 0; }
+// Unwinding after an abort: issued async work (bulk copies, MMAs) lands before the
+// CTA exits; it completes in bounded time, so this wait ignores the abort flag.
+__device__ __forceinline__ void mbar_drain_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  while (!done && ++spins < (1u << 22))
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t p;
@@ -281,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* unscale = reinterpret_cast<double*>(base + kOffBars + 512);  // [64] 1 / (scale_y scale_r)
 
   if (tid == 0) {
+    wd_init(p.fault, 0);
     for (int s = 0; s < kNL; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&lfree[s], kSplitWarps);
@@ -604,6 +637,10 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsi
 //                own warp: the Y stream never waits on a Khatri-Rao slot)
 //   warp 15      idle (16 warps keep 128 registers per thread)
 constexpr int kINS = 5;                        // image slots (160 KB of loads in flight)
+#ifndef CPDGPU_IMG_PIECES
+#define CPDGPU_IMG_PIECES 4
+#endif
+constexpr int kImgPieces = CPDGPU_IMG_PIECES;  // bulk copies per 32 KB tile
 constexpr int kINK = 4;                        // KRr slots (units of look-ahead)
 constexpr int kIDrain = 12, kIWProd = kIDrain, kIWMma = kIDrain + 1, kIWKr = kIDrain + 2;
 constexpr int kIThreads = 16 * 32;
@@ -612,7 +649,7 @@ constexpr int kIOffBars = kIOffKR + kINK * kKRBytes;
 constexpr int kISmem = 1024 + kIOffBars + 512 + kRP * 8;
 
 __global__ void __launch_bounds__(kIThreads, 1)
-    seed_f32i_kernel(const Seed32FParams p, const __grid_constant__ CUtensorMap imap) {
+    seed_f32i_kernel(const Seed32FParams p) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x;
   FWalk w;
@@ -638,10 +675,12 @@ __global__ void __launch_bounds__(kIThreads, 1)
   uint64_t* rempty = rfull + kA;         // [kA] right window drained       (the row tile's 4 warps)
   uint64_t* kl_full = rempty + kA;       // band's KRl^T in TMEM            (12 drain warps)
   uint64_t* kl_free = kl_full + 1;       // band's MMAs done                (MMA commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kl_free + 1);
+  uint64_t* fin = kl_free + 1;           // every MMA of the CTA done       (MMA commit, before dealloc)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
   double* unscale = reinterpret_cast<double*>(base + kIOffBars + 512);  // [64] 1 / (scale_y scale_r)
 
   if (tid == 0) {
+    wd_init(p.fault, p.stall);
     for (int s = 0; s < kINS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -660,6 +699,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     }
     mbar_init(kl_full, kIDrain);
     mbar_init(kl_free, 1);
+    mbar_init(fin, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp != kIWProd) pdl_wait();  // scales, Khatri-Rao images: the preceding kernels (Y: not)
@@ -669,8 +709,6 @@ __global__ void __launch_bounds__(kIThreads, 1)
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
-  if (warp == kIWProd && lane == 0)
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&imap)));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -686,25 +724,23 @@ __global__ void __launch_bounds__(kIThreads, 1)
       int s = 0;
       uint32_t ph = 0;  // ring slot s, its empty-phase parity for this lap
       UnitIter it;
-      for (it.init(w); it.more(); it.next()) {
+      for (it.init(w); it.more() && !wd_aborted(); it.next()) {
         const int b = it.b, c = it.c, nt = it.nt;
         for (int t = 0; t < nt; ++t, ++k) {
           if (k >= kINS) mbar_wait_t(&empty[s], ph ^ 1u, &tw);
+          if (wd_aborted()) break;  // watchdog: no new loads
           if ((p.knobs & 16) && k >= kINS) {  // timing experiment: no refill (stale planes)
             mbar_arrive(&full[s]);
           } else {
           mbar_arrive_tx(&full[s], 2 * kPlane);
-          const int i0 = (b * kA + t) * kTI, j0 = c * kTJ;
+          // tests (p.stall): the first tile is announced but never requested (watchdog path)
+          if (!(p.stall && k == 0)) {
+            const unsigned char* src = p.img + ((static_cast<int64_t>(b) * w.nC + c) * kA + t) * (2 * kPlane);
 #pragma unroll
-          for (int pl = 0; pl < 2; ++pl)
-#pragma unroll
-            for (int ih = 0; ih < 2; ++ih)
-              asm volatile(
-                  "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-                  " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(ring_u + s * 2 * kPlane + pl * kPlane + ih * 8192),
-                  "l"(reinterpret_cast<uint64_t>(&imap)), "r"(i0 + 64 * ih), "r"(j0), "r"(pl), "r"(smem_u32(&full[s])),
-                  "l"(pol_y)
-                  : "memory");
+            for (int q = 0; q < kImgPieces; ++q)  // several requests in flight per tile
+              bulk_load(ring_u + s * 2 * kPlane + q * (2 * kPlane / kImgPieces), src + q * (2 * kPlane / kImgPieces),
+                        2 * kPlane / kImgPieces, &full[s], pol_y);
+          }
           }
           if (++s == kINS) {
             s = 0;
@@ -712,6 +748,9 @@ __global__ void __launch_bounds__(kIThreads, 1)
           }
         }
       }
+      if (wd_aborted())  // the last load of each ring slot lands before the CTA exits
+        for (int q = k > kINS ? k - kINS : 0; q < k; ++q)
+          if (!(p.stall && q == 0)) mbar_drain_wait(&full[q % kINS], static_cast<uint32_t>((q / kINS) & 1));
       if (p.trace) {
         p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + 0] = tw;
         p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + 6] = static_cast<unsigned long long>(clock64() - tstart);
@@ -726,10 +765,14 @@ __global__ void __launch_bounds__(kIThreads, 1)
       for (it.init(w); it.more(); it.next(), ++ul) {
         const int ks = ul & (kINK - 1);
         if (ul >= kINK) mbar_wait(&kempty[ks], static_cast<uint32_t>(((ul / kINK) - 1) & 1));
+        if (wd_aborted()) break;  // watchdog: no new loads
         mbar_arrive_tx(&kfull[ks], kKRBytes);
         bulk_load(krt_u + ks * kKRBytes, p.kr_tiles + static_cast<int64_t>(it.c) * kKRBytes, kKRBytes, &kfull[ks],
                   pol_k);
       }
+      if (wd_aborted())
+        for (int q = ul > kINK ? ul - kINK : 0; q < ul; ++q)
+          mbar_drain_wait(&kfull[q & (kINK - 1)], static_cast<uint32_t>((q / kINK) & 1));
     }
   } else if (warp == kIWMma) {
     // ------------------------------------------------------------------ MMA issuer
@@ -746,7 +789,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     uint32_t ph = 0;  // ring slot and its full-phase parity
     int ul = 0;
     UnitIter it;
-    for (it.init(w); it.more(); it.next(), ++ul) {
+    for (it.init(w); it.more() && !wd_aborted(); it.next(), ++ul) {
       const int nt = it.nt;
       const int ks = ul & (kINK - 1), lb = ul & 1;
       const bool seg_end = it.seg_end();
@@ -805,6 +848,20 @@ __global__ void __launch_bounds__(kIThreads, 1)
       }
       __syncwarp();
       if (seg_end) ++bc;
+    }
+    // every issued MMA has completed before TMEM is released (after a watchdog abort
+    // the drains no longer wait for them); MMA completion is bounded, so this spin
+    // ignores the abort flag
+    if (elect_one()) umma_commit(fin);
+    __syncwarp();
+    {
+      uint32_t done = 0;
+      while (!done)
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(fin)), "r"(0u)
+            : "memory");
     }
     if (p.trace && lane == 0) {
       tr[6] = static_cast<unsigned long long>(clock64() - tstart);
@@ -923,40 +980,121 @@ __global__ void __launch_bounds__(kIThreads, 1)
 }
 
 // Operand image of an fp32 tensor view (J rows, K columns, column-major, leading
-// dimension ldy): planes [2][K][LD] fp16, hi = fp16(s y), lo = fp16(s y - hi), rows
-// J..LD-1 zero; s = the tensor's power-of-two scale.  Two rows per thread.
-__global__ void build_f16_image_kernel(const float* __restrict__ y, int64_t J, int64_t ldy, int64_t K, int64_t LD,
-                                       const float* __restrict__ scale, __half2* __restrict__ img) {
+// dimension ldy), laid out in the fused pass's consumption order: tile (row tile
+// rt = kA b + t, column tile c) is the 32 KB block ((b nC + c) kA + t), holding
+// [plane hi | lo][i half][64 j][128 B of 64 i] fp16 with the 128-byte swizzle
+// already applied (16-byte chunk i8 of row j at chunk i8 ^ (j % 8)), i.e. the
+// exact bytes the MMA descriptors read from a ring slot.  A unit is 96 KB of
+// contiguous HBM and a CTA's whole range one contiguous stream, moved by plain
+// bulk copies.  hi = fp16(s y), lo = fp16(s y - hi) (s = the tensor's power-of-two
+// scale); rows past J and columns past K are zero.  One 16-byte chunk per thread.
+__global__ void build_f16_image_kernel(const float* __restrict__ y, int64_t J, int64_t ldy, int64_t K, int64_t nC,
+                                       int64_t chunks, const float* __restrict__ scale,
+                                       unsigned char* __restrict__ img) {
   const float sy = scale[0];
-  const int64_t half = LD / 2, n = half * K, plane = n;  // in half2 units
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < chunks;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = e / half, i = 2 * (e - j * half);
-    const float* col = y + j * ldy;
-    const float a = i < J ? __ldcs(col + i) * sy : 0.0f;
-    const float b = i + 1 < J ? __ldcs(col + i + 1) * sy : 0.0f;
-    const __half2 hi = __floats2half2_rn(a, b);
-    const float2 back = __half22float2(hi);
-    __stcs(img + e, hi);
-    __stcs(img + plane + e, __floats2half2_rn(a - back.x, b - back.y));
+    const int q = static_cast<int>(e & 7);            // chunk position in the 128-byte row
+    const int jj = static_cast<int>((e >> 3) & 63);   // column in the tile
+    const int ih = static_cast<int>((e >> 9) & 1);    // i half
+    const int64_t tile = e >> 10;
+    const int64_t t = tile % kA, bc = tile / kA, c = bc % nC, b = bc / nC;
+    const int i8 = q ^ (jj & 7);
+    const int64_t i0 = (b * kA + t) * kTI + ih * 64 + i8 * 8, j = c * kTJ + jj;
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (j < K && i0 + k < J) ? __ldcs(y + j * ldy + i0 + k) * sy : 0.0f;
+    uint4 hi, lo;
+    uint32_t* h = reinterpret_cast<uint32_t*>(&hi);
+    uint32_t* l = reinterpret_cast<uint32_t*>(&lo);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      h[k] = pack_half2(v[2 * k], v[2 * k + 1]);
+      const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&h[k]));
+      l[k] = pack_half2(v[2 * k] - back.x, v[2 * k + 1] - back.y);
+    }
+    unsigned char* dst = img + tile * (2 * kPlane) + ih * 8192 + jj * 128 + q * 16;
+    __stcs(reinterpret_cast<uint4*>(dst), hi);
+    __stcs(reinterpret_cast<uint4*>(dst + kPlane), lo);
   }
 }
 
-// KRl^T image for the left MMA's TMEM A operand: [row tile][128 slots][128 i] fp16,
-// slot m = 2 r: hi part of rank r, m = 2 r + 1: its lo part, from the fp64
-// Khatri-Rao rows [L][ld] scaled by the left column scales; rows past L are zero.
-__global__ void krl_image_kernel(const double* __restrict__ rows, int64_t L, int ld, const double* __restrict__ scale,
-                                 __half* __restrict__ img, int64_t ntiles) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // (tile, slot, i)
-  if (e >= ntiles * 128 * kTI) return;
-  const int i = static_cast<int>(e % kTI);
-  const int m = static_cast<int>((e / kTI) % 128);
-  const int64_t t = e / (static_cast<int64_t>(kTI) * 128);
-  const int r = m >> 1;
-  const int64_t row = t * kTI + i;
-  const double x = (row < L && r < ld) ? rows[row * ld + r] * scale[r] : 0.0;
-  const __half hi = __double2half(x);
-  img[e] = (m & 1) ? __double2half(x - static_cast<double>(__half2float(hi))) : hi;
+// ---- Khatri-Rao operands of the fused pass, straight from the sorted factors ----
+// (the north star's "never materialised when it can be recomputed": no fp64
+// Khatri-Rao rows in HBM; each operand entry prod_m A_m[d_m, r] (kron.cpp:54-68)
+// is formed once, scaled and split to fp16 hi / lo where it is stored)
+
+// Column scales: one block per (side, rank column); max_x |KR[x, r]| =
+// prod_m max_i |A_m[i, r]| (every index combination occurs), as a power of two.
+__global__ void __launch_bounds__(128) kr_scale_cols_kernel(const KRSpec right, const KRSpec left, int R,
+                                                            double* scale, double* inv) {
+  const int side = blockIdx.x / kRP, r = blockIdx.x % kRP;
+  const KRSpec& sp = side == 0 ? right : left;
+  __shared__ double red[4];
+  double bound = r < R ? 1.0 : 0.0;
+  for (int m = 0; m < sp.n && r < R; ++m) {
+    const int64_t I = sp.dims[m];
+    double mx = 0.0;
+    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) mx = fmax(mx, fabs(__ldg(sp.A[m] + i + I * r)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+    __syncthreads();
+    bound *= mx;
+  }
+  if (threadIdx.x == 0) {
+    int e = 0;
+    if (bound > 0.0 && isfinite(bound)) frexp(bound, &e);
+    scale[side * kRP + r] = ldexp(1.0, -e);
+    inv[side * kRP + r] = ldexp(1.0, e);
+  }
+}
+
+// Both operands in one launch.  Items [0, nR): right B tiles, K-major 128-byte
+// swizzled (tile t = rows j in [64 t, 64 t + 64): [hi | lo][64 r][64 j], 16-byte
+// chunk j8 of row r at chunk j8 ^ (r % 8)), 8 consecutive j per item.  Items
+// [nR, nR + nL): the left KRl^T image [row tile][128 slots][128 i] (slot 2 r: hi
+// of rank r, 2 r + 1: its lo), 8 consecutive i per item.  Rows past the view are 0.
+__global__ void __launch_bounds__(256) kr_images_kernel(const KRSpec right, int64_t Kp, const KRSpec left, int64_t Jp,
+                                                        int R, const double* __restrict__ scale, __half* rtiles,
+                                                        int64_t nR, __half* limg, int64_t nL) {
+  int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  __half hi[8], lo[8];
+  if (e < nR) {  // (t, r, j8): 8 consecutive items fill one 128-byte row of the tile
+    const int j8 = static_cast<int>(e & 7);
+    const int r = static_cast<int>((e >> 3) % kRP);
+    const int64_t t = (e >> 3) / kRP;
+    const double sc = scale[r];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int64_t j = t * kTJ + j8 * 8 + jj;
+      const double x = (j < Kp && r < R) ? kr_entry(right, j, r) * sc : 0.0;
+      hi[jj] = __double2half(x);
+      lo[jj] = __double2half(x - static_cast<double>(__half2float(hi[jj])));
+    }
+    __half* dst = rtiles + t * (kKRBytes / 2) + static_cast<int64_t>(r) * kTJ + ((j8 ^ (r & 7)) << 3);
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hi);
+    *reinterpret_cast<uint4*>(dst + kTJ * kRP) = *reinterpret_cast<const uint4*>(lo);
+    return;
+  }
+  e -= nR;
+  if (e >= nL) return;
+  const int i8 = static_cast<int>(e & 15);  // (t, r, i8)
+  const int r = static_cast<int>((e >> 4) % kRP);
+  const int64_t t = (e >> 4) / kRP;
+  const double sc = scale[kRP + r];
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii) {
+    const int64_t i = t * kTI + i8 * 8 + ii;
+    const double x = (i < Jp && r < R) ? kr_entry(left, i, r) * sc : 0.0;
+    hi[ii] = __double2half(x);
+    lo[ii] = __double2half(x - static_cast<double>(__half2float(hi[ii])));
+  }
+  __half* dst = limg + (t * 128 + 2 * r) * kTI + i8 * 8;
+  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hi);
+  *reinterpret_cast<uint4*>(dst + kTI) = *reinterpret_cast<const uint4*>(lo);
 }
 
 }  // namespace
@@ -970,49 +1108,33 @@ int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream
   return 1;
 }
 
-int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s) {
+int launch_seed_f32i(const Seed32FParams& p, cudaStream_t s) {
   static unsigned long long cfg = 0;
   set_smem_attr(seed_f32i_kernel, kISmem, cfg);
-  launch_k(seed_f32i_kernel, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
+  launch_k(seed_f32i_kernel, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p);
   return 1;
 }
 
-int64_t f16_image_ld(int64_t J) { return ceil_div(J, 64) * 64; }
+int64_t f16_image_bytes(int64_t J, int64_t K) {
+  return ceil_div(ceil_div(J, kTI), kA) * ceil_div(K, kTJ) * kA * (2 * kPlane);
+}
 
 int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
                            int num_sms, cudaStream_t s) {
-  build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, f16_image_ld(J), scale, static_cast<__half2*>(img));
+  const int64_t chunks = f16_image_bytes(J, K) / (2 * 16);
+  build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, ceil_div(K, kTJ), chunks, scale,
+                                                      static_cast<unsigned char*>(img));
   return 1;
 }
 
-bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K) {
-  static PFN_cuTensorMapEncodeTiled encode = nullptr;
-  if (!encode) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return false;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
-  }
-  const int64_t LD = f16_image_ld(J);
-  if ((reinterpret_cast<uintptr_t>(img) & 127) || K >= (1ll << 31) || LD >= (1ll << 31)) return false;
-  // [2 planes][K][LD] fp16; box 64 i (128 B, swizzled) x 64 j x 1 plane
-  const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(LD), static_cast<cuuint64_t>(K), 2};
-  const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(LD) * 2, static_cast<cuuint64_t>(LD * K) * 2};
-  const cuuint32_t box[3] = {64, 64, 1};
-  const cuuint32_t estride[3] = {1, 1, 1};
-  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(img), gdim, gstride, box, estride,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+int launch_kr_fused_operands(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, double* scale,
+                             double* inv, void* rtiles, void* limg, cudaStream_t s) {
+  kr_scale_cols_kernel<<<2 * kRP, 128, 0, s>>>(right, left, R, scale, inv);
+  const int64_t nR = ceil_div(Kp, kTJ) * 8 * kRP, nL = ceil_div(Jp, kTI) * kRP * 16;
+  kr_images_kernel<<<static_cast<unsigned>((nR + nL + 255) / 256), 256, 0, s>>>(
+      right, Kp, left, Jp, R, scale, static_cast<__half*>(rtiles), nR, static_cast<__half*>(limg), nL);
+  return 2;
 }
 
-int launch_krl_image(const double* rows, int64_t L, int ld, const double* scale, void* img, cudaStream_t s) {
-  const int64_t ntiles = ceil_div(L, kTI);
-  const int64_t work = ntiles * 128 * kTI;
-  krl_image_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, s>>>(rows, L, ld, scale,
-                                                                             static_cast<__half*>(img), ntiles);
-  return 1;
-}
 
 }  // namespace cpdgpu

@@ -128,36 +128,57 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
-// Barrier wait with a watchdog: a wait that spins ~2^31 times (seconds) traps,
-// so a broken pipeline surfaces as a launch error instead of a hung GPU.  With
-// SeedI8Params::debug each warp posts its position (progress[cta][warp]) and the
-// first stuck thread prints its CTA's table before trapping.
+// Barrier wait with a watchdog: a wait that spins ~2^31 times (seconds) gives up,
+// records the fault in the context's fault word (mapped host memory, reported by
+// the next API return as CPDGPU_CUDA_ERROR) and raises the CTA's abort flag, after
+// which every wait of the CTA returns at once: the kernel unwinds and exits
+// normally instead of trapping (a trap would poison the whole CUDA context of the
+// caller's process).  With SeedI8Params::progress each warp posts its position
+// (progress[cta][warp]) and the first stuck thread prints its CTA's table.
+__shared__ int wd_abort;  // per CTA
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int code, int info,
-                                             unsigned* progress) {
+                                             unsigned* progress, int* fault, uint32_t limit) {
   uint32_t done = 0;
   uint32_t spins = 0;
   if (progress && (threadIdx.x & 31) == 0)
     *reinterpret_cast<volatile unsigned*>(progress + blockIdx.x * 16 + (threadIdx.x >> 5)) =
         static_cast<unsigned>(code * 100000 + info);
-  const uint32_t limit = progress ? (1u << 24) : (1u << 31);
   while (!done) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-    if (!done && ++spins >= limit) {
+    if (done) break;
+    if (*reinterpret_cast<volatile int*>(&wd_abort)) return;
+    if (++spins >= limit) {
       if (progress) {
         const volatile unsigned* t = progress + blockIdx.x * 16;
         printf("seed_i8 stuck: cta %d warp %d code %d info %d | warps: %u %u %u %u %u %u %u %u | %u %u %u %u | %u %u\n",
                blockIdx.x, threadIdx.x >> 5, code, info, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[8], t[9],
                t[10], t[11], t[12], t[13]);
       }
-      __trap();
+      if (fault) atomicExch(fault, 1000 + code);
+      *reinterpret_cast<volatile int*>(&wd_abort) = 1;
+      __threadfence_block();
+      return;
     }
   }
 }
-#define WAIT(bar, par, code, info) mbar_wait_wd(bar, par, code, info, p.progress)
+__device__ __forceinline__ bool wd_aborted() { return *reinterpret_cast<volatile int*>(&wd_abort) != 0; }
+// Unwinding after an abort: wait for async work that WAS issued (TMA / bulk copies,
+// MMAs) to land before the CTA exits.  That work completes in bounded time, so this
+// wait ignores the abort flag (and gives up after ~2^22 spins regardless).
+__device__ __forceinline__ void mbar_drain_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  while (!done && ++spins < (1u << 22))
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+#define WAIT(bar, par, code, info) mbar_wait_wd(bar, par, code, info, p.progress, p.fault, wd_limit)
 #define TWAIT(idx, bar, par, code, info)                 \
   do {                                                   \
     const long long t0_ = p.trace ? clock64() : 0;       \
@@ -298,9 +319,13 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   uint64_t* accR_empty = accR_full + 1;
   uint64_t* accL_full = accR_empty + 1;  // [2]
   uint64_t* accL_empty = accL_full + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accL_empty + 2);
+  uint64_t* fin = accL_empty + 2;        // every MMA of the CTA done (before TMEM is released)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
 
+  // spins before the watchdog fires: forced-stall tests and the debug table use short limits
+  const uint32_t wd_limit = p.stall ? (1u << 16) : (p.progress ? (1u << 24) : (1u << 31));
   if (tid == 0) {
+    wd_abort = 0;
     for (int s = 0; s < C::kRaw; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], kSplitW);
@@ -317,6 +342,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       mbar_init(&accL_full[b], 1);
       mbar_init(&accL_empty[b], kDrainW);
     }
+    mbar_init(fin, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == kWMma) {
@@ -345,32 +371,51 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       // Slot q = (tile k, row chunk c): q = 8 k + c, one box of 16 rows i x 128
       // columns j (128-byte swizzle).  Boxes wholly outside Y are not requested
       // (the split reads them as zeros).
+      const auto issued = [&](int q) {  // box q was requested from HBM
+        const int64_t tile = a0 + (q >> 3), rb = tile / nCT, ct = tile - rb * nCT;
+        return ct * 128 < p.K && rb * 128 + 16 * (q & 7) < p.J && !(p.stall && q == 0);
+      };
+      int qn = 0;  // boxes announced
       for (int q = 0; q < nslots; ++q) {
         const int k = q >> 3, c = q & 7, slot = q % C::kRaw;
         if (q >= C::kRaw) WAIT(&raw_empty[slot], ((q / C::kRaw) - 1) & 1, 3, q);
+        if (wd_aborted()) break;  // watchdog: no new loads
         const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
         const int j = static_cast<int>(ct * 128), i = static_cast<int>(rb * 128 + 16 * c);
         const bool live = j < p.K && i < p.J;
         mbar_arrive_tx(&raw_full[slot], live ? kRawSlot : 0);
-        if (live) tma_2d(raw + slot * kRawSlot, &ymap, i, j, &raw_full[slot], pol_y);
+        // p.stall (tests): the first box is announced but never requested, so its
+        // consumers wait until the watchdog fires
+        if (issued(q)) tma_2d(raw + slot * kRawSlot, &ymap, i, j, &raw_full[slot], pol_y);
+        qn = q + 1;
       }
+      if (wd_aborted())  // the last loads of each slot land before the CTA exits
+        for (int q = qn > C::kRaw ? qn - C::kRaw : 0; q < qn; ++q)
+          if (issued(q)) mbar_drain_wait(&raw_full[q % C::kRaw], (q / C::kRaw) & 1);
     } else if (lane == 1) {
       const uint64_t pol_k = policy_evict_last();
       pdl_wait();
-      int m = 0;
+      int m = 0, kn = 0;  // left / right image loads issued
       int64_t cur_rb = -1;
       for (int k = 0; k < n; ++k) {
         const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
         if (k > 0) WAIT(rb_empty, (k - 1) & 1, 1, k);
+        if (wd_aborted()) break;
         mbar_arrive_tx(rb_full, C::kB);
         bulk_load(rbuf, p.img_r + ct * C::kB, C::kB, rb_full, pol_k);
+        kn = k + 1;
         if (rb != cur_rb) {
           if (m > 0) WAIT(lb_empty, (m - 1) & 1, 2, m);
+          if (wd_aborted()) break;
           mbar_arrive_tx(lb_full, C::kBL);
           bulk_load(lbuf, p.img_l + rb * C::kBL, C::kBL, lb_full, pol_k);
           cur_rb = rb;
           ++m;
         }
+      }
+      if (wd_aborted()) {
+        if (kn > 0) mbar_drain_wait(rb_full, (kn - 1) & 1);
+        if (m > 0) mbar_drain_wait(lb_full, (m - 1) & 1);
       }
     }
   } else if (warp == kWMma) {
@@ -381,6 +426,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       int m = 0;
       int seg = 0, pos = 0;  // right-accumulator segment and position in it
       for (int k = 0; k < n; ++k) {
+        if (wd_aborted()) break;  // watchdog: no new MMAs
         const int64_t tile = a0 + k, rb = tile / nCT;
         const bool last_of_rb = (k == n - 1) || ((tile + 1) / nCT != rb);
         const bool send = seg_end(tile, k, n, nCT, pos);
@@ -428,6 +474,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           ++pos;
         }
       }
+      umma_commit(fin);  // TMEM is released only after every issued MMA completed
+      mbar_drain_wait(fin, 0);
     }
     __syncwarp();
   } else if (warp < kSplitW) {
@@ -802,6 +850,54 @@ int launch_y_scale_f64(const double* y, int64_t n, void* scratch, double* out, i
   y_amax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(y, n, bmax, bsum);
   y_scale_final_kernel<<<1, 1, 0, s>>>(bmax, bsum, blocks, out);
   return 2;
+}
+
+// int8 factor-range guard on device factors: one block per (side, rank column);
+// sets *flag when prod_m max_i |A_m[i, r]| / rms_i A_m[i, r] exceeds `limit` or a
+// factor entry is not finite (the host then runs the DMMA pass).
+__global__ void __launch_bounds__(128) i8_factor_guard_kernel(const KRSpec right, const KRSpec left, int R,
+                                                              double limit, int* flag) {
+  const int side = blockIdx.x / R, r = blockIdx.x % R;
+  const KRSpec& sp = side == 0 ? right : left;
+  __shared__ double rm[4], rs[4];
+  double ratio = 1.0;
+  bool bad = false;
+  for (int m = 0; m < sp.n; ++m) {
+    const int64_t I = sp.dims[m];
+    double mx = 0.0, ss = 0.0;
+    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
+      const double a = fabs(sp.A[m][i + I * r]);
+      mx = a > mx || a != a ? a : mx;  // NaN wins
+      ss += a * a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = t > mx || t != t ? t : mx;
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      rm[threadIdx.x >> 5] = mx;
+      rs[threadIdx.x >> 5] = ss;
+    }
+    __syncthreads();
+    mx = 0.0;
+    ss = 0.0;
+    for (int w = 0; w < 4; ++w) {
+      mx = rm[w] > mx || rm[w] != rm[w] ? rm[w] : mx;
+      ss += rs[w];
+    }
+    __syncthreads();
+    if (!isfinite(mx) || !isfinite(ss)) bad = true;
+    else if (mx == 0.0) ratio = 0.0;
+    else ratio *= mx / sqrt(ss / static_cast<double>(I));
+  }
+  if (threadIdx.x == 0 && (bad || !(ratio <= limit))) atomicOr(flag, 1);
+}
+
+int launch_i8_factor_guard(const KRSpec& right, const KRSpec& left, int R, double limit, int* flag, cudaStream_t s) {
+  i8_factor_guard_kernel<<<2 * R, 128, 0, s>>>(right, left, R, limit, flag);
+  return 1;
 }
 
 }  // namespace cpdgpu
