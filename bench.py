@@ -151,43 +151,23 @@ def device_normal(ctx, seed, rows, R):
 # ---------------------------------------------------------------------------- reference arm
 
 def run_reference(args, cfg):
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import oracle as O
+    """--impl reference: the reference's own cp_gradient_all on this host's cores
+    (oracle/_ref, compiled from its sources; the C port if that build is absent),
+    each step one bounded sample of the workload (cpu_gradient_sample)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     dims, R, dtype, desc = cfg
-    sd = sample_dims(dims, dtype)
-    n = int(np.prod(sd))
-    cores = host_cores()
-    esize = 4 if dtype == "f32" else 8
-    # fp32: the streaming restatement over the generated values (fp64 arithmetic on the
-    # upcast fp32 entries; the reference is fp64-only), a slab at the global pivot
-    y = None if dtype == "f32" else O.fill_normal(1, n, nthreads=cores)
-    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(sd)]
-    steps = args.steps
-    for _ in range(min(args.warmup, 3)):
-        oracle_gradient(O, cfg, sd, cores, y, f)
-    t0 = time.perf_counter()
-    done = 0
-    while done < steps and (done < 3 or time.perf_counter() - t0 < args.cpu_seconds * 6):
-        oracle_gradient(O, cfg, sd, cores, y, f)
-        done += 1
-    dt = time.perf_counter() - t0
-    ms = dt / done * 1e3
-    gbs = n * esize / (ms * 1e-3) / 1e9
-    what = "full" if sd == list(dims) else f"{'x'.join(map(str, sd))}-slab sample (global pivot) of the"
+    steps = max(1, min(args.steps, 5))
+    cpu = cpu_gradient_sample(args, cfg, steps=steps, warmup=min(args.warmup, 1))
     line = {
-        "impl": "reference", "metric": f"all-mode CP gradient throughput ({desc})", "value": gbs,
-        "unit": "GB/s", "n_gpus": 1, "steps": done, "warmup": min(args.warmup, 3), "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong" if args.config in STRONG_CONFIGS else "weak",
-        "vs_baseline": None, "dtype": dtype,
-        "data": "synthetic, counter-based generator (same values as the GPU arm)",
-        "config": {"workload": args.config, "dims": dims, "R": R, "sample_dims": sd},
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"{what} {args.config} gradient x {done} steps (oracle/cpd_oracle.c, OpenMP, "
-                                   "time-bounded)"},
-        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": f"all-mode CP gradient throughput ({desc})", "value": cpu["value"],
+        "unit": "GB/s", "n_gpus": 1, "steps": cpu["steps"], "warmup": min(args.warmup, 1),
+        "ms_per_step": cpu["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong" if args.config in STRONG_CONFIGS else "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic, counter-based generator", "config": {"workload": args.config, "dims": dims, "R": R},
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -429,51 +409,75 @@ def host_memory_ok(nbytes):
         return False
 
 
-def sample_dims(dims, dtype):
-    """Bounded CPU sample: the first k last-mode slices of the workload tensor, a
-    slab at the global pivot (fp32 configs are sampled; the fp64 configs run in full)."""
-    if dtype != "f32":
-        return list(dims)
-    return list(dims[:-1]) + [10]
+def reference_build():
+    """oracle/ref.py when the reference itself is built (oracle/_ref), else None."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    try:
+        import ref
+        if (ROOT / "oracle" / "_ref" / "libcpdref.so").exists():
+            ref.load()
+            return ref
+    except Exception as e:  # noqa: BLE001 - fall back to the port, say why
+        print(f"reference build unavailable ({e}); timing the C port", file=sys.stderr)
+    return None
 
 
-def oracle_gradient(O, cfg, sd, cores, y=None, f=None):
-    """One CPU-oracle gradient of the sample: fp32 configs through the streaming
-    restatement (generated values, fp64 arithmetic, the workload's global pivot,
-    as a GPU rank runs its slab); fp64 configs on the in-memory tensor."""
-    dims, R, dtype, _ = cfg
-    if dtype == "f32":
-        J = np.cumprod([1] + list(dims))
-        p = max(n for n in range(1, len(dims) + 1) if J[n] <= J[-1] // J[n])
-        return O.cp_gradient_all_upm1_f32(sd, 1, f, pivot=int(p), nthreads=cores)
-    return O.cp_gradient_all(y, sd, f, nthreads=cores)
-
-
-def cpu_baseline(args, cfg, ydev=None):
+def cpu_gradient_sample(args, cfg, steps=None, warmup=1):
+    """CPU time of the workload's all-mode gradient on a bounded sample, on this
+    host's cores.  Preferred: the reference ITSELF (oracle/_ref: its own
+    mttkrp.cpp / Eigen code path compiled with its Release flags, Eigen replaced
+    by oracle/shim), which is single-threaded, run as one independent reference
+    call per core on mode-1 slabs of the tensor (the gradients of the slabs sum
+    exactly: the same decomposition the GPUs shard by).  fp64 configs: the full
+    tensor; c5 (300^4, 32 GB fp32 — beyond this host's memory in fp64): a
+    (cores x 300 x 300 x 300) tensor of the same U(-1,1) fp32 values upcast to
+    fp64 (the reference is fp64-only), same R and pivot structure, reported per
+    fp32 tensor byte like the GPU arm.  Fallback: the OpenMP C port."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as O
     dims, R, dtype, desc = cfg
-    sd = sample_dims(dims, dtype)
-    n = int(np.prod(sd))
     cores = host_cores()
-    y = None if dtype == "f32" else O.fill_normal(1, n, nthreads=cores)
-    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(sd)]
-    oracle_gradient(O, cfg, sd, cores, y, f)
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        oracle_gradient(O, cfg, sd, cores, y, f)
-        reps += 1
-        if time.perf_counter() - t0 > args.cpu_seconds:
-            break
-    dt = (time.perf_counter() - t0) / reps
     esize = 4 if dtype == "f32" else 8
-    what = "full" if sd == list(cfg[0]) else f"{'x'.join(map(str, sd))}-slab sample (global pivot) of the"
-    how = ("streaming restatement over the generated fp32 values, fp64 arithmetic" if dtype == "f32"
-           else "fp64 arithmetic")
-    return {"value": n * esize / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
-            "sample": f"{reps} {what} {args.config} gradients (~{args.cpu_seconds:.0f} s), "
-                      f"oracle/cpd_oracle.c OpenMP ({how})",
-            "ms_per_step": dt * 1e3}
+    ref = reference_build()
+    if dtype == "f32":
+        sd = [cores] + list(dims[1:])
+        n = int(np.prod(sd))
+        y = O.fill_upm1_f32(1, n, nthreads=cores).astype(np.float64)
+    else:
+        sd = list(dims)
+        n = int(np.prod(sd))
+        y = O.fill_normal(1, n, nthreads=cores)
+    f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(sd)]
+    if ref is not None:
+        t = ref.Tensor(y, sd, parts=min(cores, sd[0]), axis=0)
+        del y
+        for _ in range(warmup):
+            t.cp_gradient_all(f)
+        first = t.time_cp_gradient_all(f, 1)
+        reps = steps or max(1, int(args.cpu_seconds / max(first, 1e-6)))
+        dt = t.time_cp_gradient_all(f, reps) if reps > 1 else first
+        t.close()
+        kind, threads = "reference", min(cores, sd[0])
+        how = (f"the reference's own cp_gradient_all (oracle/_ref: /root/reference/proj/core built -O3 -DNDEBUG, "
+               f"Eigen shim), one single-threaded call per core on {threads} mode-1 slabs")
+    else:
+        t0 = time.perf_counter()
+        reps = 0
+        while reps < (steps or 10 ** 9):
+            O.cp_gradient_all(y, sd, f, nthreads=cores)
+            reps += 1
+            if not steps and time.perf_counter() - t0 > args.cpu_seconds:
+                break
+        dt = (time.perf_counter() - t0) / reps
+        kind, threads, how = "port", cores, "oracle/cpd_oracle.c (the C port), OpenMP"
+    what = "full" if sd == list(dims) else f"{'x'.join(map(str, sd))} sample ({dtype} values upcast to fp64) of the"
+    return {"value": n * esize / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"{reps} x {what} {args.config} gradient, {how}", "ms_per_step": dt * 1e3, "steps": reps,
+            "host_cores": cores}
+
+
+def cpu_baseline(args, cfg, ydev=None):
+    return cpu_gradient_sample(args, cfg)
 
 
 # ---------------------------------------------------------------------------- CP_ALS (c4)
@@ -502,6 +506,39 @@ def als_metric(desc):
     return f"CP_ALS iterations per second ({desc})"
 
 
+def cpu_als_sample(args, yh, dims, init, max_sweeps=None):
+    """CPU fast ALS sweeps of the c4 tensor: the reference itself (oracle/_ref,
+    cpd::als_sweep_fast: single-threaded, a Gauss-Seidel sweep has no slab
+    parallelism) or, without that build, the OpenMP C port."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    cores = host_cores()
+    f = [a.copy(order="F") for a in init]
+    ref = reference_build()
+    done, spent = 0, 0.0
+    limit = max_sweeps or 10 ** 9
+    if ref is not None:
+        t = ref.Tensor(yh, dims)
+        while done < limit and (done < 1 or spent < args.cpu_seconds):
+            _, sec = t.als_sweep_fast(f)
+            spent += sec
+            done += 1
+        t.close()
+        kind, threads, how = "reference", 1, ("the reference's own cpd::als_sweep_fast (oracle/_ref: "
+                                              "/root/reference/proj/core built -O3 -DNDEBUG, Eigen shim), 1 thread")
+    else:
+        t0 = time.perf_counter()
+        while done < limit and (done < 1 or time.perf_counter() - t0 < args.cpu_seconds):
+            O.als_sweep_fast(yh, dims, f, nthreads=cores)
+            done += 1
+        spent = time.perf_counter() - t0
+        kind, threads, how = "port", cores, "oracle/cpd_oracle.c (the C port), OpenMP"
+    dt = spent / done
+    return {"value": 1.0 / dt, "unit": "iters/s", "cores": threads, "kind": kind,
+            "sample": f"{done} fast ALS sweeps of the full {args.config} tensor, {how}", "ms_per_step": dt * 1e3,
+            "steps": done, "host_cores": cores}
+
+
 def run_reference_als(args, cfg):
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as O
@@ -516,23 +553,16 @@ def run_reference_als(args, cfg):
     sigma = float(np.sqrt(np.dot(full, full)) / (10.0 * np.sqrt(np.dot(e, e))))
     y = sigma * e + full
     del e, full
-    f = [a.copy(order="F") for a in init]
-    for _ in range(min(args.warmup, 1)):
-        O.als_sweep_fast(y, dims, f, nthreads=cores)
-    done, t0 = 0, time.perf_counter()
-    while done < args.steps and (done < 2 or time.perf_counter() - t0 < args.cpu_seconds * 6):
-        O.als_sweep_fast(y, dims, f, nthreads=cores)
-        done += 1
-    dt = (time.perf_counter() - t0) / done
+    cpu = cpu_als_sample(args, y, dims, init, max_sweeps=max(1, min(args.steps, 3)))
+    del y
+    dt = cpu["ms_per_step"] * 1e-3
     line = {
         "impl": "reference", "metric": als_metric(desc), "value": 1.0 / dt, "unit": "iters/s", "n_gpus": 1,
-        "steps": done, "warmup": min(args.warmup, 1), "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "steps": cpu["steps"], "warmup": 0, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic rank-16 N(0,1) model + N(0,1) noise at 20 dB, counter-based generator",
         "config": {"workload": args.config, "dims": dims, "R": R},
-        "cpu_baseline": {"value": 1.0 / dt, "unit": "iters/s", "cores": cores, "kind": "port",
-                         "sample": f"{done} fast ALS sweeps of the full {args.config} tensor "
-                                   "(oracle/cpd_oracle.c, OpenMP), time-bounded"},
+        "cpu_baseline": cpu,
         "e2e": {"value": 1.0 / dt, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -658,20 +688,9 @@ def run_ours_als(args, cfg):
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        sys.path.insert(0, str(ROOT / "oracle"))
-        import oracle as O
-        cores = host_cores()
         yh = y.values()
-        f = [a.copy(order="F") for a in init]
-        done, t0 = 0, time.perf_counter()
-        while done < 1 or time.perf_counter() - t0 < args.cpu_seconds:
-            O.als_sweep_fast(yh, dims, f, nthreads=cores)
-            done += 1
-        dt = (time.perf_counter() - t0) / done
+        cpu = cpu_als_sample(args, yh, dims, init)
         del yh
-        cpu = {"value": 1.0 / dt, "unit": "iters/s", "cores": cores, "kind": "port",
-               "sample": f"{done} fast ALS sweeps of the same {args.config} tensor (~{args.cpu_seconds:.0f} s), "
-                         "oracle/cpd_oracle.c OpenMP", "ms_per_step": dt * 1e3}
     if rank == 0:
         line = {
             "metric": als_metric(desc), "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,

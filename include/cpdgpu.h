@@ -127,6 +127,15 @@ int cpdgpu_sort_modes(int N, const int64_t* dims, int* perm, int* inverse); /* m
 int cpdgpu_fast_update_order(int N, const int64_t* dims, int* order);       /* mttkrp.cpp:92-111 */
 /* mttkrp.cpp:292-320 (dims must be ascending); 0 on bad input. */
 uint64_t cpdgpu_fast_count_realized(int N, const int64_t* dims, int64_t R, int n);
+/* predicted_mult_count (mttkrp.hpp:85-86, mttkrp.cpp:255-290): the analytic
+ * count of one mode, variant 0 direct, 1 fast (compressed closed form), 2
+ * fast_derived (CountVariant order).  Ascending dims; status 2 (IndexError) for a
+ * mode outside 1..N, 3 (ArgumentError) for R < 1 or unsorted dims. */
+int cpdgpu_predicted_mult_count(int N, const int64_t* dims, int64_t R, int n, int variant, uint64_t* out);
+/* FastStats::peak_workspace_doubles (mttkrp.hpp:37-47) as the reference's
+ * cp_gradient_all tracks it (mttkrp.cpp:127-131,147-243) for ascending dims: the
+ * figure every gradient entry point reports through peak_workspace (host only). */
+int cpdgpu_reference_workspace(int N, const int64_t* dims, int64_t R, int64_t* out);
 
 /* ---- all-mode CP gradient (cp_gradient_all, mttkrp.hpp:59-69, mttkrp.cpp:113-253)
  * factors[k] / gradients[k]: host I_{k+1} x R column-major fp64 buffers in the

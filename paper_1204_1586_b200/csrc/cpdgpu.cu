@@ -314,6 +314,7 @@ struct Plan {
     // kernel then has no split stage); off when it does not fit in memory
     bool img_on = false, img_failed = false;
     void* img = nullptr;
+    CUtensorMap imap{};
     uint64_t img_version = ~0ull;
     ~F32Fused() {
       if (img) cudaFree(img);
@@ -845,9 +846,13 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gra
     static const char* img_env = std::getenv("CPDGPU_F32_IMAGE");
     Plan::F32Fused& ff = pl.ff;
     if (!ff.img && !ff.img_failed && !(img_env && std::atoi(img_env) == 0)) {
-      const size_t bytes = static_cast<size_t>(cpdgpu::f16_image_bytes(pl.Jp, pl.Kp));
+      const size_t bytes = static_cast<size_t>(2 * cpdgpu::f16_image_ld(pl.Jp) * pl.Kp) * 2;
       if (cudaMalloc(&ff.img, bytes) != cudaSuccess) {
         cudaGetLastError();  // out of memory: keep the split-in-kernel path
+        ff.img = nullptr;
+        ff.img_failed = true;
+      } else if (!cpdgpu::make_tensor_map_f16_image(&ff.imap, ff.img, pl.Jp, pl.Kp)) {
+        cudaFree(ff.img);
         ff.img = nullptr;
         ff.img_failed = true;
       }
@@ -1085,8 +1090,7 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
       q.trace = static_cast<unsigned long long*>(tb.p);
     }
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
-    q.img = static_cast<const unsigned char*>(pl.ff.img);
-    ctx->launches += pl.ff.img_on ? cpdgpu::launch_seed_f32i(q, s)
+    ctx->launches += pl.ff.img_on ? cpdgpu::launch_seed_f32i(q, &pl.ff.imap, s)
                                   : cpdgpu::launch_seed_f32f(q, &pl.ymap_r, s);
     if (q.trace) {
       std::vector<unsigned long long> h(static_cast<size_t>(q.P) * 128);
@@ -2668,6 +2672,48 @@ int cpdgpu_fast_update_order(int N, const int64_t* dims, int* order) {
     int at = 0;
     for (int j = p; j >= 1; --j) order[at++] = perm[j - 1];
     for (int j = p + 1; j <= N; ++j) order[at++] = perm[j - 1];
+  });
+}
+
+int cpdgpu_reference_workspace(int N, const int64_t* dims, int64_t R, int64_t* out) {
+  return guarded(nullptr, [&] {
+    if (!dims || !out || N < 2 || R < 1) fail(CPDGPU_ARGUMENT_ERROR, "reference_workspace: bad argument");
+    const std::vector<int64_t> d(dims, dims + N);
+    if (!ascending(d)) fail(CPDGPU_ARGUMENT_ERROR, "reference_workspace: dims must be ascending");
+    *out = reference_peak_workspace(d, select_pivot(d), R);
+  });
+}
+
+// predicted_mult_count (mttkrp.cpp:255-290), restated over J_k = prod_{m<=k} I_m.
+int cpdgpu_predicted_mult_count(int N, const int64_t* dims, int64_t R, int n, int variant, uint64_t* out) {
+  return guarded(nullptr, [&] {
+    if (!dims || !out || N < 1) fail(CPDGPU_ARGUMENT_ERROR, "predicted_mult_count: null argument");
+    if (n < 1 || n > N) fail(CPDGPU_INDEX_ERROR, "predicted_mult_count: mode %d outside 1..%d", n, N);
+    if (R < 1) fail(CPDGPU_ARGUMENT_ERROR, "predicted_mult_count: rank must be positive");
+    const std::vector<int64_t> d(dims, dims + N);
+    if (!ascending(d)) fail(CPDGPU_ARGUMENT_ERROR, "predicted_mult_count: dims must be ascending");
+    if (variant < 0 || variant > 2) fail(CPDGPU_ARGUMENT_ERROR, "predicted_mult_count: unknown variant %d", variant);
+    const auto J = prefix(d);
+    auto sumj = [&](int lo, int hi, int64_t div) {
+      uint64_t t = 0;
+      for (int k = std::max(lo, 0); k <= hi; ++k) t += static_cast<uint64_t>(J[k] / div);
+      return t;
+    };
+    auto K = [&](int m) { return static_cast<uint64_t>(J[N] / J[m]); };
+    const uint64_t uR = static_cast<uint64_t>(R), JN = static_cast<uint64_t>(J[N]);
+    if (variant == 0) {  // unfold + multiply, plus the Kronecker build-up
+      *out = uR * (JN + sumj(2, n - 1, 1) + sumj(n + 1, N, d[n - 1]));
+      return;
+    }
+    const int p = select_pivot(d);
+    if (n == p || n == p + 1) {
+      const uint64_t pivot_term = std::min<uint64_t>(static_cast<uint64_t>(J[n]), K(n - 1));
+      *out = uR * (sumj(2, n - 1, 1) + pivot_term + sumj(n + 2, N, J[n]) + JN);
+    } else if (n < p) {
+      *out = uR * sumj(2, n + 1, 1);
+    } else {  // n > p + 1: `fast` keeps the trailing J_k raw, `fast_derived` divides by J_n
+      *out = uR * (K(n - 2) + K(n - 1) + (variant == 1 ? sumj(n + 2, N, 1) : sumj(n + 2, N, J[n])));
+    }
   });
 }
 

@@ -144,19 +144,21 @@ struct Seed32FParams {
               // 16 (image kernel) no plane refills after the first ring, 32 (image kernel) no MMAs
   int* fault;  // context fault word: the watchdog's report (no trap)
   int stall;   // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
-  const unsigned char* img;  // image kernel: the tensor's operand image (launch_build_f16_image)
 };
 int seed_f32f_band_tiles();  // 3
 // ymap: the right pass's map (box 128 i x 64 j, no swizzle)
 int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream_t s);
 // The same kernel reading a cached operand image of the tensor instead of the fp32
-// values (no split stage): Seed32FParams::img, launch_build_f16_image's layout.
-int launch_seed_f32i(const Seed32FParams& p, cudaStream_t s);
-// operand image of an fp32 view (J x K, leading dimension ldy): 32 KB pre-swizzled
-// fp16 hi / lo tiles in the fused pass's unit order (f16_image_bytes in total)
-int64_t f16_image_bytes(int64_t J, int64_t K);
+// values (no split stage).  imap: make_tensor_map_f16_image of that image.
+int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s);
+// operand image of an fp32 view (J x K, leading dimension ldy): [2][K][LD] fp16
+// planes hi = fp16(s y), lo = fp16(s y - hi), LD = f16_image_ld(J) (rows past J zero).
+// (A unit-ordered, pre-swizzled 32 KB-tile layout moved by bulk copies streamed
+// faster alone but made the fused pass 0.6 ms slower at c5: measured and dropped.)
+int64_t f16_image_ld(int64_t J);
 int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
                            int num_sms, cudaStream_t s);
+bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K);
 // fused pass: column scales, right B tiles and the KRl^T image straight from the
 // sorted factors (two launches, no fp64 Khatri-Rao rows)
 int launch_kr_fused_operands(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, double* scale,

@@ -637,10 +637,6 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsi
 //                own warp: the Y stream never waits on a Khatri-Rao slot)
 //   warp 15      idle (16 warps keep 128 registers per thread)
 constexpr int kINS = 5;                        // image slots (160 KB of loads in flight)
-#ifndef CPDGPU_IMG_PIECES
-#define CPDGPU_IMG_PIECES 4
-#endif
-constexpr int kImgPieces = CPDGPU_IMG_PIECES;  // bulk copies per 32 KB tile
 constexpr int kINK = 4;                        // KRr slots (units of look-ahead)
 constexpr int kIDrain = 12, kIWProd = kIDrain, kIWMma = kIDrain + 1, kIWKr = kIDrain + 2;
 constexpr int kIThreads = 16 * 32;
@@ -649,7 +645,7 @@ constexpr int kIOffBars = kIOffKR + kINK * kKRBytes;
 constexpr int kISmem = 1024 + kIOffBars + 512 + kRP * 8;
 
 __global__ void __launch_bounds__(kIThreads, 1)
-    seed_f32i_kernel(const Seed32FParams p) {
+    seed_f32i_kernel(const Seed32FParams p, const __grid_constant__ CUtensorMap imap) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x;
   FWalk w;
@@ -709,6 +705,8 @@ __global__ void __launch_bounds__(kIThreads, 1)
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
+  if (warp == kIWProd && lane == 0)
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&imap)));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -735,11 +733,17 @@ __global__ void __launch_bounds__(kIThreads, 1)
           mbar_arrive_tx(&full[s], 2 * kPlane);
           // tests (p.stall): the first tile is announced but never requested (watchdog path)
           if (!(p.stall && k == 0)) {
-            const unsigned char* src = p.img + ((static_cast<int64_t>(b) * w.nC + c) * kA + t) * (2 * kPlane);
+            const int i0 = (b * kA + t) * kTI, j0 = c * kTJ;
 #pragma unroll
-            for (int q = 0; q < kImgPieces; ++q)  // several requests in flight per tile
-              bulk_load(ring_u + s * 2 * kPlane + q * (2 * kPlane / kImgPieces), src + q * (2 * kPlane / kImgPieces),
-                        2 * kPlane / kImgPieces, &full[s], pol_y);
+            for (int pl = 0; pl < 2; ++pl)
+#pragma unroll
+              for (int ih = 0; ih < 2; ++ih)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                    " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(ring_u + s * 2 * kPlane + pl * kPlane + ih * 8192),
+                    "l"(reinterpret_cast<uint64_t>(&imap)), "r"(i0 + 64 * ih), "r"(j0), "r"(pl),
+                    "r"(smem_u32(&full[s])), "l"(pol_y)
+                    : "memory");
           }
           }
           if (++s == kINS) {
@@ -980,42 +984,22 @@ __global__ void __launch_bounds__(kIThreads, 1)
 }
 
 // Operand image of an fp32 tensor view (J rows, K columns, column-major, leading
-// dimension ldy), laid out in the fused pass's consumption order: tile (row tile
-// rt = kA b + t, column tile c) is the 32 KB block ((b nC + c) kA + t), holding
-// [plane hi | lo][i half][64 j][128 B of 64 i] fp16 with the 128-byte swizzle
-// already applied (16-byte chunk i8 of row j at chunk i8 ^ (j % 8)), i.e. the
-// exact bytes the MMA descriptors read from a ring slot.  A unit is 96 KB of
-// contiguous HBM and a CTA's whole range one contiguous stream, moved by plain
-// bulk copies.  hi = fp16(s y), lo = fp16(s y - hi) (s = the tensor's power-of-two
-// scale); rows past J and columns past K are zero.  One 16-byte chunk per thread.
-__global__ void build_f16_image_kernel(const float* __restrict__ y, int64_t J, int64_t ldy, int64_t K, int64_t nC,
-                                       int64_t chunks, const float* __restrict__ scale,
-                                       unsigned char* __restrict__ img) {
+// dimension ldy): planes [2][K][LD] fp16, hi = fp16(s y), lo = fp16(s y - hi), rows
+// J..LD-1 zero; s = the tensor's power-of-two scale.  Two rows per thread.
+__global__ void build_f16_image_kernel(const float* __restrict__ y, int64_t J, int64_t ldy, int64_t K, int64_t LD,
+                                       const float* __restrict__ scale, __half2* __restrict__ img) {
   const float sy = scale[0];
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < chunks;
+  const int64_t half = LD / 2, n = half * K, plane = n;  // in half2 units
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int q = static_cast<int>(e & 7);            // chunk position in the 128-byte row
-    const int jj = static_cast<int>((e >> 3) & 63);   // column in the tile
-    const int ih = static_cast<int>((e >> 9) & 1);    // i half
-    const int64_t tile = e >> 10;
-    const int64_t t = tile % kA, bc = tile / kA, c = bc % nC, b = bc / nC;
-    const int i8 = q ^ (jj & 7);
-    const int64_t i0 = (b * kA + t) * kTI + ih * 64 + i8 * 8, j = c * kTJ + jj;
-    float v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = (j < K && i0 + k < J) ? __ldcs(y + j * ldy + i0 + k) * sy : 0.0f;
-    uint4 hi, lo;
-    uint32_t* h = reinterpret_cast<uint32_t*>(&hi);
-    uint32_t* l = reinterpret_cast<uint32_t*>(&lo);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      h[k] = pack_half2(v[2 * k], v[2 * k + 1]);
-      const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&h[k]));
-      l[k] = pack_half2(v[2 * k] - back.x, v[2 * k + 1] - back.y);
-    }
-    unsigned char* dst = img + tile * (2 * kPlane) + ih * 8192 + jj * 128 + q * 16;
-    __stcs(reinterpret_cast<uint4*>(dst), hi);
-    __stcs(reinterpret_cast<uint4*>(dst + kPlane), lo);
+    const int64_t j = e / half, i = 2 * (e - j * half);
+    const float* col = y + j * ldy;
+    const float a = i < J ? __ldcs(col + i) * sy : 0.0f;
+    const float b = i + 1 < J ? __ldcs(col + i + 1) * sy : 0.0f;
+    const __half2 hi = __floats2half2_rn(a, b);
+    const float2 back = __half22float2(hi);
+    __stcs(img + e, hi);
+    __stcs(img + plane + e, __floats2half2_rn(a - back.x, b - back.y));
   }
 }
 
@@ -1108,23 +1092,41 @@ int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream
   return 1;
 }
 
-int launch_seed_f32i(const Seed32FParams& p, cudaStream_t s) {
+int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s) {
   static unsigned long long cfg = 0;
   set_smem_attr(seed_f32i_kernel, kISmem, cfg);
-  launch_k(seed_f32i_kernel, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p);
+  launch_k(seed_f32i_kernel, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
   return 1;
 }
 
-int64_t f16_image_bytes(int64_t J, int64_t K) {
-  return ceil_div(ceil_div(J, kTI), kA) * ceil_div(K, kTJ) * kA * (2 * kPlane);
-}
+int64_t f16_image_ld(int64_t J) { return ceil_div(J, 64) * 64; }
 
 int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
                            int num_sms, cudaStream_t s) {
-  const int64_t chunks = f16_image_bytes(J, K) / (2 * 16);
-  build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, ceil_div(K, kTJ), chunks, scale,
-                                                      static_cast<unsigned char*>(img));
+  build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, f16_image_ld(J), scale, static_cast<__half2*>(img));
   return 1;
+}
+
+bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  const int64_t LD = f16_image_ld(J);
+  if ((reinterpret_cast<uintptr_t>(img) & 127) || K >= (1ll << 31) || LD >= (1ll << 31)) return false;
+  // [2 planes][K][LD] fp16; box 64 i (128 B, swizzled) x 64 j x 1 plane
+  const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(LD), static_cast<cuuint64_t>(K), 2};
+  const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(LD) * 2, static_cast<cuuint64_t>(LD * K) * 2};
+  const cuuint32_t box[3] = {64, 64, 1};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(img), gdim, gstride, box, estride,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int launch_kr_fused_operands(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, double* scale,
