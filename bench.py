@@ -8,7 +8,8 @@ factors, synthetic inputs from the counter-based generator.  For N>1 (torchrun,
 one rank per GPU) the same 300^4 tensor is sharded along its last mode (strong
 scaling, 300 -> 38/38/38/38/37/37/37/37 at N=8): every rank's slab runs with the
 global pivot, then one NCCL all_reduce of the partial G(1..3) carrying the G(4)
-rows at each slab's offset (paper_1204_1586_b200/sharded.py).  The fp64 configs
+rows at each slab's offset, inside libcpdgpu.so (cpdgpu_comm_init from an NCCL id
+broadcast over torch.distributed; paper_1204_1586_b200/sharded.py).  The fp64 configs
 c1..c4 run with --config (c2, c3: weak scaling, one slab per GPU).
 
 Timing: W untimed warm-up steps; then exactly K steps bracketed by a barrier +
@@ -235,10 +236,18 @@ def run_ours(args, cfg):
     flush_needed = slab * esize < 4 * L2_FLUSH_BYTES  # inputs larger than L2 need no flush
     flush = torch.empty(L2_FLUSH_BYTES if flush_needed else 16, dtype=torch.uint8, device=dev)
 
+    # N > 1: the exchange runs inside libcpdgpu.so (cpdgpu_cp_gradient_all_sharded_device:
+    # the slab's gradient at the global pivot, then ONE in-place all-reduce of
+    # [partial G(1..N-1) | G(N) rows at the slab offset] on the context stream over
+    # NCCL; a gloo host all-reduce in the one-GPU functional mode)
+    comm = sharded.library_comm(ctx, dist) if plan else None
+    gout = torch.zeros(sum(gdims) * R, dtype=torch.float64, device=dev) if plan else gdev
+
     def step():
-        cpd.cp_gradient_all_device(y, R, fdev.data_ptr(), gdev.data_ptr(), pivot)
         if plan:
-            sharded.exchange(plan, gdev, dist)
+            cpd.cp_gradient_all_sharded_device(y, gdims, R, fdev.data_ptr(), gout.data_ptr())
+        else:
+            cpd.cp_gradient_all_device(y, R, fdev.data_ptr(), gdev.data_ptr(), pivot)
 
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
@@ -395,6 +404,8 @@ def run_ours(args, cfg):
             "algorithm1_direct": alg1, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

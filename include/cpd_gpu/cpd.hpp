@@ -13,6 +13,7 @@
 // (cpd::gpu::context()), device chosen with cpd::gpu::set_device().
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <exception>
@@ -340,6 +341,41 @@ inline std::uint64_t fast_count_realized(const Shape& shape, index_t R, int n) {
   return cpdgpu_fast_count_realized(shape.order(), d.data(), R, n);
 }
 
+// sort_modes (mttkrp.hpp:28-35, mttkrp.cpp:67-90): stable ascending mode order,
+// the permuted tensor (host copy; identity sorts share the tensor) and factors.
+// The device gradient sorts internally; this is the reference's helper.
+struct SortResult {
+  DenseTensor tensor;
+  FactorList factors;
+  std::vector<int> perm;
+  std::vector<int> inverse;
+};
+inline SortResult sort_modes(const DenseTensor& y, const FactorList& factors) {
+  detail::check_factors_match(y, factors, "sort_modes");
+  const ModeOrder o = sort_mode_order(y.shape());
+  const int N = y.order();
+  bool identity = true;
+  for (int j = 1; j <= N; ++j) identity &= o.perm[static_cast<size_t>(j - 1)] == j;
+  FactorList sf;
+  for (int j = 1; j <= N; ++j) sf.push_back(factors[static_cast<size_t>(o.perm[static_cast<size_t>(j - 1)] - 1)]);
+  if (identity) return SortResult{y, std::move(sf), o.perm, o.inverse};
+  // out(i_1..i_N) = y(i at positions perm): mode j of the result is mode perm[j] of y
+  std::vector<index_t> od;
+  for (int j = 0; j < N; ++j) od.push_back(y.shape().dim(o.perm[static_cast<size_t>(j)]));
+  const Shape os(od);
+  std::vector<index_t> stride(static_cast<size_t>(N));
+  for (int m = 0; m < N; ++m) stride[static_cast<size_t>(m)] = y.shape().j_prefix(m);
+  std::vector<double> v(static_cast<size_t>(y.size()));
+  std::vector<index_t> idx(static_cast<size_t>(N), 0);
+  for (index_t q = 0; q < y.size(); ++q) {
+    index_t src = 0;
+    for (int j = 0; j < N; ++j) src += idx[static_cast<size_t>(j)] * stride[static_cast<size_t>(o.perm[static_cast<size_t>(j)] - 1)];
+    v[static_cast<size_t>(q)] = y.data()[src];
+    for (int j = 0; j < N && ++idx[static_cast<size_t>(j)] == od[static_cast<size_t>(j)]; ++j) idx[static_cast<size_t>(j)] = 0;
+  }
+  return SortResult{DenseTensor(os, std::move(v)), std::move(sf), o.perm, o.inverse};
+}
+
 // ---- the all-mode gradient (mttkrp.hpp:59-69, mttkrp.cpp:113-253) --------------------------
 namespace detail {
 struct HookCtx {
@@ -416,6 +452,84 @@ inline std::vector<Matrix> cp_gradient_all(const DenseTensor& y, const FactorLis
                                            CostCounter* counter = nullptr, FastStats* stats = nullptr) {
   FactorList copy = factors;
   return cp_gradient_all(y, copy, counter, ModeHook{}, stats);
+}
+
+// ---- multi-GPU: the all-mode gradient over last-mode slabs ---------------------
+// One process (or thread) per GPU, each holding the contiguous last-mode slab
+// [lo, hi) = gpu::slab_bounds(I_N, nranks, rank) of a tensor with ascending dims.
+// Each rank calls cp_gradient_all_sharded with its slab and the GLOBAL factors and
+// receives every global G(n): the library computes the slab's gradient at the
+// global pivot and finishes it with ONE all-reduce inside libcpdgpu.so (NCCL over
+// NVLink after gpu::comm_init, or the caller's host all-reduce after
+// gpu::comm_init_host).  Counter charges are the unsharded call's
+// (mttkrp.hpp:59-69 semantics on the whole tensor).
+namespace gpu {
+inline std::vector<unsigned char> comm_unique_id() {
+  std::vector<unsigned char> id(CPDGPU_COMM_ID_BYTES);
+  const int st = cpdgpu_comm_unique_id(id.data());
+  if (st != CPDGPU_OK) throw_status(st, "cpdgpu_comm_unique_id failed (libnccl.so.2 missing?)");
+  return id;
+}
+// NCCL communicator on this thread's context (rank 0 made `id`, every rank passes it)
+inline void comm_init(const std::vector<unsigned char>& id, int nranks, int rank) {
+  auto& c = context();
+  c.check(cpdgpu_comm_init(c.h, id.data(), nranks, rank));
+}
+// host all-reduce (MPI, gloo, ...): fn(user, buf, count) sums `count` doubles in place
+inline void comm_init_host(int nranks, int rank, cpdgpu_allreduce_fn fn, void* user) {
+  auto& c = context();
+  c.check(cpdgpu_comm_init_host(c.h, nranks, rank, fn, user));
+}
+inline void comm_destroy() {
+  auto& c = context();
+  c.check(cpdgpu_comm_destroy(c.h));
+}
+inline std::pair<index_t, index_t> slab_bounds(index_t extent, int nranks, int rank) {
+  int64_t lo = 0, hi = 0;
+  const int st = cpdgpu_slab_bounds(extent, nranks, rank, &lo, &hi);
+  if (st != CPDGPU_OK) throw_status(st, "slab_bounds: bad argument");
+  return {lo, hi};
+}
+}  // namespace gpu
+
+inline std::vector<Matrix> cp_gradient_all_sharded(const DenseTensor& slab, const Shape& global_shape,
+                                                   const FactorList& factors, CostCounter* counter = nullptr) {
+  const int N = global_shape.order();
+  if (N < 2) throw ArgumentError("cp_gradient_all: need an order-2 or higher tensor");
+  if (factor_shape(factors) != global_shape)
+    throw ShapeError("cp_gradient_all: factor row counts do not match the tensor");
+  const index_t R = factor_rank(factors);
+  auto& ctx = gpu::context();
+  const auto gd = detail::dims64(global_shape);
+  std::vector<const double*> fp;
+  for (const auto& f : factors) fp.push_back(f.data());
+  std::vector<Matrix> out(static_cast<size_t>(N));
+  std::vector<double*> gp;
+  for (int m = 0; m < N; ++m) {
+    out[static_cast<size_t>(m)].resize(global_shape.dim(m + 1), R);
+    gp.push_back(out[static_cast<size_t>(m)].data());
+  }
+  std::vector<uint64_t> mults(static_cast<size_t>(N));
+  ctx.check(cpdgpu_cp_gradient_all_sharded(ctx.h, slab.device(), N, gd.data(), R, fp.data(), gp.data(), mults.data()));
+  if (counter)
+    for (auto m : mults) counter->charge(m);
+  return out;
+}
+
+// predicted_mult_count (mttkrp.hpp:76-86): the analytic count of one mode
+enum class CountVariant { direct, fast, fast_derived };
+inline std::uint64_t predicted_mult_count(const Shape& shape, index_t R, int n, CountVariant variant) {
+  const auto d = detail::dims64(shape);
+  uint64_t out = 0;
+  const int v = variant == CountVariant::direct ? 0 : variant == CountVariant::fast ? 1 : 2;
+  const int st = cpdgpu_predicted_mult_count(shape.order(), d.data(), R, n, v, &out);
+  if (st == CPDGPU_INDEX_ERROR)
+    throw IndexError("predicted_mult_count: mode " + std::to_string(n) + " outside 1.." +
+                     std::to_string(shape.order()));
+  if (st != CPDGPU_OK)
+    throw ArgumentError(R < 1 ? "predicted_mult_count: rank must be positive"
+                              : "predicted_mult_count: dims must be ascending");
+  return out;
 }
 
 // ---- direct MTTKRP (mttkrp.hpp:19-20): one pass over Y per mode ----------------------------
@@ -552,6 +666,32 @@ inline void gd_step(const DenseTensor& y, FactorList& factors, double eta, CostC
   uint64_t mults = 0;
   ctx.check(cpdgpu_gd_step(ctx.h, y.device(), factor_rank(factors), fp.data(), eta, &mults));
   if (counter) counter->charge(mults);
+}
+
+// random_init (als.hpp:84-85, als.cpp:127-139): Uniform01 (rng.hpp:16-26, the
+// std::mt19937_64 stream, bit-identical) column-major per factor in mode order.
+inline KruskalModel random_init(const Shape& shape, index_t rank, std::uint64_t seed) {
+  if (rank < 1) throw ArgumentError("random_init: rank must be positive");
+  index_t total = 0;
+  for (int n = 1; n <= shape.order(); ++n) total += shape.dim(n) * rank;
+  std::vector<double> v(static_cast<size_t>(total));
+  detail::check_status(cpdgpu_uniform01_fill(seed, total, v.data()));
+  FactorList f;
+  index_t at = 0;
+  for (int n = 1; n <= shape.order(); ++n) {
+    Matrix a(shape.dim(n), rank);
+    std::copy(v.begin() + at, v.begin() + at + shape.dim(n) * rank, a.data());
+    at += shape.dim(n) * rank;
+    f.push_back(std::move(a));
+  }
+  return KruskalModel(std::move(f));
+}
+
+// standard_order (als.hpp:87): 1..N
+inline std::vector<int> standard_order(int order) {
+  std::vector<int> v(static_cast<size_t>(order));
+  std::iota(v.begin(), v.end(), 1);
+  return v;
 }
 
 // run(y, init, algo, opts) (als.cpp:147-210) for every Algorithm on the device.

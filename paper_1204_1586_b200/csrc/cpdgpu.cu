@@ -278,6 +278,7 @@ struct Plan {
     bool on = false;   // tensor_ok && factors_ok: the gradient runs the int8 pass
     bool tensor_ok = false;   // bound tensor passed the range guard and has a TMA view
     bool factors_ok = true;   // the call's factors passed the Khatri-Rao range guard
+    const void* guard_fdev = nullptr;  // device factors the last synchronous guard checked
     int N = 0;         // MMA rank block (16 or 32)
     int NL = 0;        // left rank block (24 when R <= 24 < N)
     int64_t nRB = 0, nCT = 0, T = 0;
@@ -444,6 +445,7 @@ struct cpdgpu_ctx {
   int* fault_dev = nullptr;
   volatile int* guard_host = nullptr;  // int8 factor-range guard result (mapped)
   int* guard_dev = nullptr;
+  std::tuple<uint64_t, int64_t, int> i8_last_key{0, 0, 0};  // plan of the last int8 launch
   ~cpdgpu_ctx() {
     for (auto e : seed_events) cudaEventDestroy(e);
     if (fault_host) cudaFreeHost(const_cast<int*>(fault_host));
@@ -458,6 +460,22 @@ int set_error(cpdgpu_ctx* ctx, int code, const std::string& msg) {
   return code;
 }
 
+void set_i8_on(Plan& pl);
+// kr_digits_kernel found the int8 error budget exceeded (fault code 3000): the plan
+// forgets its checked factor buffer, so its next device call re-runs the guard
+int i8_budget_fault(cpdgpu_ctx* ctx) {
+  auto it = ctx->plans.find(ctx->i8_last_key);
+  if (it != ctx->plans.end()) {
+    it->second->i8.factors_ok = false;
+    it->second->i8.guard_fdev = nullptr;
+    set_i8_on(*it->second);
+  }
+  return set_error(ctx, CPDGPU_NUMERIC_ERROR,
+                   "cp_gradient_all: the device factors exceed the int8 pass's error budget "
+                   "((max|Y| / mean|Y|) x max_r S_r / rms KR_r > 2^11); this result is invalid and later calls of "
+                   "this tensor run the fp64 DMMA pass until the factors pass the guard again");
+}
+
 template <typename F>
 int guarded(cpdgpu_ctx* ctx, F&& f) {
   try {
@@ -465,6 +483,7 @@ int guarded(cpdgpu_ctx* ctx, F&& f) {
     if (ctx && ctx->fault_host && *ctx->fault_host) {  // a seed kernel's watchdog fired
       const int code = *ctx->fault_host;
       *ctx->fault_host = 0;
+      if (code == 3000) return i8_budget_fault(ctx);
       return set_error(ctx, CPDGPU_CUDA_ERROR,
                        "seed pipeline stalled (watchdog code " + std::to_string(code) +
                            "): the kernel unwound, results of the calls since the last check are invalid");
@@ -984,6 +1003,17 @@ void i8_apply_factor_guard(Plan& pl, bool ok) {
   set_i8_on(pl);
 }
 
+// Device entry points: the synchronous guard runs when the factor buffer is new to
+// the plan; repeated calls on the same buffer rely on the device's own check
+// (kr_digits_kernel, fault code 3000), which turns a later out-of-budget call into a
+// reported error rather than a silently inaccurate result and sends the plan back
+// through the synchronous guard.
+void i8_device_guard(cpdgpu_ctx* ctx, Plan& pl, const double* fdev, const cpdgpu_tensor* t) {
+  if (!pl.i8.tensor_ok || fdev == pl.i8.guard_fdev) return;
+  i8_apply_factor_guard(pl, i8_factors_ok_device(ctx, pl, fdev, i8_factor_limit(t)));
+  pl.i8.guard_fdev = fdev;
+}
+
 // fused_gradient: the caller runs a hook-free all-mode gradient (the fp32 fused
 // pass reads the operand image, not the split passes' view)
 void bind_seed_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gradient = false) {
@@ -1039,6 +1069,13 @@ int force_stall() {
   const char* e = std::getenv("CPDGPU_FORCE_STALL");
   return e && std::atoi(e) != 0 ? 1 : 0;
 }
+// CPDGPU_WATCHDOG=1: the seed kernels' bounded-wait build (a stuck pipeline is
+// reported as CPDGPU_CUDA_ERROR and unwinds; costs 5-30 % on the int8 pass, so off
+// by default); read per launch
+int watchdog_on(int stall) {
+  const char* e = std::getenv("CPDGPU_WATCHDOG");
+  return stall || (e && std::atoi(e) != 0) ? 1 : 0;
+}
 
 // ---- K1 launches ---------------------------------------------------------------
 cudaEvent_t seed_event(cpdgpu_ctx* ctx) {
@@ -1082,6 +1119,7 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
     q.knobs = knob_env ? std::atoi(knob_env) : 0;
     q.fault = ctx->fault_dev;
     q.stall = force_stall();
+    q.watchdog = watchdog_on(q.stall);
     static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
     DevBuf tb;
     if (trace && pl.ff.img_on) {
@@ -1168,8 +1206,12 @@ void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
   Plan::I8& g = pl.i8;
   Plan::Chunk& c = pl.chunks[0];
   const double* ys = pl.tensor->yscale8.d();
+  // the device re-checks the call's error budget with 1 % slack over the host guard
+  // (rounding of the two sums never trips it for factors the host passed)
   ctx->launches += cpdgpu::launch_kr_digits(pl.spec(pl.p + 1, pl.N, c.r0), pl.Kp, pl.spec(1, pl.p, c.r0), pl.Jp, c.Rc,
-                                            g.N, g.NL, ys, g.img_r.p, g.w_r.d(), g.img_l.p, g.w_l.d(), s);
+                                            g.N, g.NL, ys, g.img_r.p, g.w_r.d(), g.img_l.p, g.w_l.d(),
+                                            pl.tensor->numel, kI8ErrorBudget * 1.01, ctx->fault_dev, s);
+  ctx->i8_last_key = std::make_tuple(pl.tensor->id, pl.R, pl.raw_frame ? pl.p : 0);
   cpdgpu::SeedI8Params q{};
   q.J = pl.Jp;
   q.K = pl.Kp;
@@ -1199,6 +1241,7 @@ void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
   q.knobs = knobs;
   q.fault = ctx->fault_dev;
   q.stall = force_stall();
+  q.watchdog = watchdog_on(q.stall);
   q.Lpart = g.nRB == 1 ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d() + c.lpart_off;
   static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
   DevBuf tb;
@@ -2795,7 +2838,7 @@ int cpdgpu_cp_gradient_all_device(cpdgpu_ctx* ctx, cpdgpu_tensor* y, int64_t R, 
     if (pivot == 0) ensure_sorted(ctx, y);
     Plan& pl = *get_plan(ctx, y, R, pivot);
     bind_seed_inputs(ctx, pl, y, true);
-    if (pl.i8.tensor_ok) i8_apply_factor_guard(pl, i8_factors_ok_device(ctx, pl, factors_dev, i8_factor_limit(y)));
+    i8_device_guard(ctx, pl, factors_dev, y);
     run_gradient(ctx, pl, factors_dev, gradients_dev);
     CK(cudaGetLastError());
   });
@@ -3227,7 +3270,7 @@ void sharded_device(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, const ShardGeom& g, in
   c.lbuf.ensure(static_cast<size_t>(g.partial + rows * R) * sizeof(double));
   Plan& pl = *get_plan(ctx, slab, R, g.pivot);
   bind_seed_inputs(ctx, pl, slab, true);
-  if (pl.i8.tensor_ok) i8_apply_factor_guard(pl, i8_factors_ok_device(ctx, pl, fdev, i8_factor_limit(slab)));
+  i8_device_guard(ctx, pl, fdev, slab);
   run_gradient(ctx, pl, fdev, c.lbuf.d());
   CK(cudaMemcpyAsync(out_dev, c.lbuf.d(), static_cast<size_t>(g.partial) * sizeof(double), cudaMemcpyDeviceToDevice,
                      ctx->stream));

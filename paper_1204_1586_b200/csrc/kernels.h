@@ -80,6 +80,7 @@ struct SeedI8Params {
   int knobs;                  // CPDGPU_I8_KNOBS experiments (bit 0: no digit stores)
   int* fault;                 // context fault word: the watchdog's report (no trap)
   int stall;                  // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
+  int watchdog;               // bounded barrier waits (CPDGPU_WATCHDOG=1; implied by stall)
 };
 // left rank block for a right block N and rank R (24 when it lets the left accumulators
 // double-buffer in TMEM), and the left digit image bytes per row block
@@ -94,8 +95,11 @@ int launch_i8_factor_guard(const KRSpec& right, const KRSpec& left, int R, doubl
 // Khatri-Rao rows [L][ldk] -> digit images [ceil(L / 128)][6][N][128] + weights [.][N]
 // Khatri-Rao digit images [tiles][6][N][128] + column weights [tiles][N] of both
 // sides, from the factors (right: K_p rows, left: J_p rows; one launch)
+// numel / budget / fault: the error-budget check of the call's factors (tile 0 of
+// each side; *fault = 3000 when prod_m max / rms > budget mean|Y| / max|Y|)
 int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N, int NL,
-                     const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, cudaStream_t s);
+                     const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, int64_t numel,
+                     double budget, int* fault, cudaStream_t s);
 // fp64 tensor scale record [2^(46-eY), eY, max|Y|, sum|Y|] (bitwise reproducible);
 // scratch >= 16 * y_scale_f64_blocks(n, num_sms) bytes
 int y_scale_f64_blocks(int64_t n, int num_sms);
@@ -144,6 +148,7 @@ struct Seed32FParams {
               // 16 (image kernel) no plane refills after the first ring, 32 (image kernel) no MMAs
   int* fault;  // context fault word: the watchdog's report (no trap)
   int stall;   // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
+  int watchdog;  // image kernel: bounded barrier waits (CPDGPU_WATCHDOG=1; implied by stall)
 };
 int seed_f32f_band_tiles();  // 3
 // ymap: the right pass's map (box 128 i x 64 j, no swizzle)

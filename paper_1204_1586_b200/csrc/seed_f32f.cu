@@ -89,10 +89,15 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
                : "memory");
 }
-// Watchdog (per CTA, static shared state of this file's kernels): a wait that
-// spins wd_limit times records the fault in the context's fault word and raises
-// the CTA's abort flag, after which every wait returns at once, so a broken
-// pipeline unwinds and exits instead of hanging the GPU or trapping.
+// Barrier waits.  The plain spin (mbar_wait) everywhere by default; the image
+// kernel also has a watchdog build (template WD, CPDGPU_WATCHDOG=1 and the
+// forced-stall tests): every 1024th failed try of a bounded wait reads the CTA's
+// abort flag and a spin budget (~2^31 tries); past it the wait records the fault
+// in the context's fault word and raises the abort flag, after which every
+// bounded wait returns at once, so a broken pipeline unwinds and exits instead
+// of hanging the GPU or trapping.  Any per-wait bookkeeping measured 1.5-8 % at
+// c5 (a spin counter, a globaltimer deadline, a try_wait suspend hint), so the
+// production build carries none.
 __shared__ int wd_abort;
 __shared__ int* wd_fault;
 __shared__ uint32_t wd_limit;
@@ -101,30 +106,50 @@ __device__ __forceinline__ void wd_init(int* fault, int stall) {
   wd_fault = fault;
   wd_limit = stall ? (1u << 16) : (1u << 31);
 }
+__device__ __noinline__ void wd_fire() {
+  if (wd_fault) atomicExch(wd_fault, 2000);
+  *reinterpret_cast<volatile int*>(&wd_abort) = 1;
+  __threadfence_block();
+}
+template <bool WD = false>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0, spins = 0;
-  while (!done) {
+  while (true) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-    if (done) break;
+    if (done) return;
+    if (!WD || ((++spins & 1023u) != 0u)) continue;
     if (*reinterpret_cast<volatile int*>(&wd_abort)) return;
-    if (++spins >= wd_limit) {
-      if (wd_fault) atomicExch(wd_fault, 2000);
-      *reinterpret_cast<volatile int*>(&wd_abort) = 1;
-      __threadfence_block();
+    if (spins >= wd_limit) {
+      wd_fire();
       return;
     }
   }
 }
-__device__ __forceinline__ bool wd_aborted() { return *reinterpret_cast<volatile int*>(&wd_abort) != 0; }
+template <bool WD>
+__device__ __forceinline__ bool wd_aborted() {
+  return WD && *reinterpret_cast<volatile int*>(&wd_abort) != 0;
+}
 // Unwinding after an abort: issued async work (bulk copies, MMAs) lands before the
 // CTA exits; it completes in bounded time, so this wait ignores the abort flag.
 __device__ __forceinline__ void mbar_drain_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0, spins = 0;
   while (!done && ++spins < (1u << 22))
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+// Unbounded wait for register-heavy warps (the drains, whose fp32 window sums fill
+// the register file: the watchdog's loop state there cost spills and ~0.7 ms at
+// c5).  Their waits are released after an abort by the MMA warp (see its tail).
+__device__ __forceinline__ void mbar_wait_plain(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
@@ -615,9 +640,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ==================================================================================
 // timed wait (CPDGPU_SEED_TRACE): cycles spent waiting added to *acc
+template <bool WD>
 __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
   const long long t0 = clock64();
-  mbar_wait(bar, parity);
+  mbar_wait<WD>(bar, parity);
+  *acc += static_cast<unsigned long long>(clock64() - t0);
+}
+__device__ __forceinline__ void mbar_wait_plain_t(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+  const long long t0 = clock64();
+  mbar_wait_plain(bar, parity);
   *acc += static_cast<unsigned long long>(clock64() - t0);
 }
 
@@ -644,6 +675,7 @@ constexpr int kIOffKR = kINS * 2 * kPlane;
 constexpr int kIOffBars = kIOffKR + kINK * kKRBytes;
 constexpr int kISmem = 1024 + kIOffBars + 512 + kRP * 8;
 
+template <bool WD>
 __global__ void __launch_bounds__(kIThreads, 1)
     seed_f32i_kernel(const Seed32FParams p, const __grid_constant__ CUtensorMap imap) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -673,10 +705,11 @@ __global__ void __launch_bounds__(kIThreads, 1)
   uint64_t* kl_free = kl_full + 1;       // band's MMAs done                (MMA commit)
   uint64_t* fin = kl_free + 1;           // every MMA of the CTA done       (MMA commit, before dealloc)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+  unsigned* drains_out = tmem_slot + 1;  // drain warps that left their loop
   double* unscale = reinterpret_cast<double*>(base + kIOffBars + 512);  // [64] 1 / (scale_y scale_r)
 
   if (tid == 0) {
-    wd_init(p.fault, p.stall);
+    if (WD) wd_init(p.fault, p.stall);
     for (int s = 0; s < kINS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -696,6 +729,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     mbar_init(kl_full, kIDrain);
     mbar_init(kl_free, 1);
     mbar_init(fin, 1);
+    *drains_out = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp != kIWProd) pdl_wait();  // scales, Khatri-Rao images: the preceding kernels (Y: not)
@@ -722,11 +756,11 @@ __global__ void __launch_bounds__(kIThreads, 1)
       int s = 0;
       uint32_t ph = 0;  // ring slot s, its empty-phase parity for this lap
       UnitIter it;
-      for (it.init(w); it.more() && !wd_aborted(); it.next()) {
+      for (it.init(w); it.more() && !wd_aborted<WD>(); it.next()) {
         const int b = it.b, c = it.c, nt = it.nt;
         for (int t = 0; t < nt; ++t, ++k) {
-          if (k >= kINS) mbar_wait_t(&empty[s], ph ^ 1u, &tw);
-          if (wd_aborted()) break;  // watchdog: no new loads
+          if (k >= kINS) mbar_wait_t<WD>(&empty[s], ph ^ 1u, &tw);
+          if (wd_aborted<WD>()) break;  // watchdog: no new loads
           if ((p.knobs & 16) && k >= kINS) {  // timing experiment: no refill (stale planes)
             mbar_arrive(&full[s]);
           } else {
@@ -752,7 +786,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
           }
         }
       }
-      if (wd_aborted())  // the last load of each ring slot lands before the CTA exits
+      if (wd_aborted<WD>())  // the last load of each ring slot lands before the CTA exits
         for (int q = k > kINS ? k - kINS : 0; q < k; ++q)
           if (!(p.stall && q == 0)) mbar_drain_wait(&full[q % kINS], static_cast<uint32_t>((q / kINS) & 1));
       if (p.trace) {
@@ -768,13 +802,13 @@ __global__ void __launch_bounds__(kIThreads, 1)
       UnitIter it;
       for (it.init(w); it.more(); it.next(), ++ul) {
         const int ks = ul & (kINK - 1);
-        if (ul >= kINK) mbar_wait(&kempty[ks], static_cast<uint32_t>(((ul / kINK) - 1) & 1));
-        if (wd_aborted()) break;  // watchdog: no new loads
+        if (ul >= kINK) mbar_wait<WD>(&kempty[ks], static_cast<uint32_t>(((ul / kINK) - 1) & 1));
+        if (wd_aborted<WD>()) break;  // watchdog: no new loads
         mbar_arrive_tx(&kfull[ks], kKRBytes);
         bulk_load(krt_u + ks * kKRBytes, p.kr_tiles + static_cast<int64_t>(it.c) * kKRBytes, kKRBytes, &kfull[ks],
                   pol_k);
       }
-      if (wd_aborted())
+      if (wd_aborted<WD>())
         for (int q = ul > kINK ? ul - kINK : 0; q < ul; ++q)
           mbar_drain_wait(&kfull[q & (kINK - 1)], static_cast<uint32_t>((q / kINK) & 1));
     }
@@ -793,13 +827,13 @@ __global__ void __launch_bounds__(kIThreads, 1)
     uint32_t ph = 0;  // ring slot and its full-phase parity
     int ul = 0;
     UnitIter it;
-    for (it.init(w); it.more() && !wd_aborted(); it.next(), ++ul) {
+    for (it.init(w); it.more() && !wd_aborted<WD>(); it.next(), ++ul) {
       const int nt = it.nt;
       const int ks = ul & (kINK - 1), lb = ul & 1;
       const bool seg_end = it.seg_end();
-      if (it.band_start()) mbar_wait_t(kl_full, static_cast<uint32_t>(bc & 1), &tr[4]);
-      if (ul >= 2) mbar_wait_t(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1), &tr[1]);
-      mbar_wait_t(&kfull[ks], static_cast<uint32_t>((ul / kINK) & 1), &tr[2]);
+      if (it.band_start()) mbar_wait_t<WD>(kl_full, static_cast<uint32_t>(bc & 1), &tr[4]);
+      if (ul >= 2) mbar_wait_t<WD>(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1), &tr[1]);
+      mbar_wait_t<WD>(&kfull[ks], static_cast<uint32_t>((ul / kINK) & 1), &tr[2]);
       tc_fence_after();
       const bool wstart = it.win_start(), wend = it.win_end();
       const uint64_t kb = dB0 + static_cast<uint64_t>((ks * kKRBytes) >> 4);
@@ -807,8 +841,8 @@ __global__ void __launch_bounds__(kIThreads, 1)
 #pragma unroll
       for (int t = 0; t < kA; ++t) {
         if (t >= nt) break;
-        if (wstart && wc[t] > 0) mbar_wait_t(&rempty[t], static_cast<uint32_t>((wc[t] - 1) & 1), &tr[3]);
-        mbar_wait_t(&full[s], ph, &tr[0]);
+        if (wstart && wc[t] > 0) mbar_wait_t<WD>(&rempty[t], static_cast<uint32_t>((wc[t] - 1) & 1), &tr[3]);
+        mbar_wait_t<WD>(&full[s], ph, &tr[0]);
         tc_fence_after();
         const long long ti = clock64();
         const uint64_t pa = static_cast<uint64_t>((s * 2 * kPlane) >> 4);
@@ -853,9 +887,19 @@ __global__ void __launch_bounds__(kIThreads, 1)
       __syncwarp();
       if (seg_end) ++bc;
     }
-    // every issued MMA has completed before TMEM is released (after a watchdog abort
-    // the drains no longer wait for them); MMA completion is bounded, so this spin
-    // ignores the abort flag
+    // after a watchdog abort the drains may sit in unbounded waits on the MMA-side
+    // barriers: keep flipping those phases until every drain warp has left its loop
+    if (wd_aborted<WD>() && lane == 0)
+      for (uint32_t i = 0; i < (1u << 22) && *reinterpret_cast<volatile unsigned*>(drains_out) < kIDrain; ++i) {
+        mbar_arrive(&lfull[0]);
+        mbar_arrive(&lfull[1]);
+        for (int q = 0; q < kA; ++q) mbar_arrive(&rfull[q]);
+        mbar_arrive(kl_free);
+        __nanosleep(256);
+      }
+    __syncwarp();
+    // every issued MMA has completed before TMEM is released; MMA completion is
+    // bounded, so this spin ignores the abort flag
     if (elect_one()) umma_commit(fin);
     __syncwarp();
     {
@@ -886,13 +930,13 @@ __global__ void __launch_bounds__(kIThreads, 1)
     const long long tstart = clock64();
     int ul = 0;
     UnitIter it;
-    for (it.init(w); it.more(); it.next(), ++ul) {
+    for (it.init(w); it.more() && !wd_aborted<WD>(); it.next(), ++ul) {
       const int nt = it.nt;
       const bool mine = t < nt;
       const int b = it.b, c = it.c;
       const int lb = ul & 1;
       if (it.band_start()) {  // row tile t's KRl^T image into TMEM, once the previous band is done
-        if (bc > 0) mbar_wait(kl_free, static_cast<uint32_t>((bc - 1) & 1));
+        if (bc > 0) mbar_wait_plain(kl_free, static_cast<uint32_t>((bc - 1) & 1));
         __syncwarp();
         tc_fence_after();
         if (mine) {
@@ -914,7 +958,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
         if (lane == 0) mbar_arrive(kl_full);
       }
       if (mine && it.win_end()) {  // right window -> fp32 second level
-        mbar_wait_t(&rfull[t], static_cast<uint32_t>(wc & 1), &tr[0]);
+        mbar_wait_plain_t(&rfull[t], static_cast<uint32_t>(wc & 1), &tr[0]);
         __syncwarp();
         tc_fence_after();
 #pragma unroll
@@ -932,7 +976,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
         ++wc;
       }
       // left: lane pairs (hi, lo) of rank 16 q + lane / 2, chunks t, t + 3, t + 6
-      mbar_wait_t(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1), &tr[1]);
+      mbar_wait_plain_t(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1), &tr[1]);
       __syncwarp();
       tc_fence_after();
       const int r = 16 * q + (lane >> 1);
@@ -970,6 +1014,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
         ++bc;
       }
     }
+    if (lane == 0) atomicAdd(drains_out, 1u);  // the MMA warp's abort path waits for all drains
     if (p.trace && lane == 0) {
       tr[6] = static_cast<unsigned long long>(clock64() - tstart);
       for (int e = 0; e < 8; ++e) p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + e] = tr[e];
@@ -1093,9 +1138,15 @@ int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream
 }
 
 int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s) {
+  if (p.watchdog) {
+    static unsigned long long cfg = 0;
+    set_smem_attr(seed_f32i_kernel<true>, kISmem, cfg);
+    launch_k(seed_f32i_kernel<true>, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
+    return 1;
+  }
   static unsigned long long cfg = 0;
-  set_smem_attr(seed_f32i_kernel, kISmem, cfg);
-  launch_k(seed_f32i_kernel, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
+  set_smem_attr(seed_f32i_kernel<false>, kISmem, cfg);
+  launch_k(seed_f32i_kernel<false>, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
   return 1;
 }
 

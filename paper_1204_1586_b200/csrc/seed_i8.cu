@@ -128,44 +128,56 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
-// Barrier wait with a watchdog: a wait that spins ~2^31 times (seconds) gives up,
-// records the fault in the context's fault word (mapped host memory, reported by
-// the next API return as CPDGPU_CUDA_ERROR) and raises the CTA's abort flag, after
-// which every wait of the CTA returns at once: the kernel unwinds and exits
-// normally instead of trapping (a trap would poison the whole CUDA context of the
-// caller's process).  With SeedI8Params::progress each warp posts its position
-// (progress[cta][warp]) and the first stuck thread prints its CTA's table.
+// Barrier waits, two builds of the kernel (template WD).  WD = false (default): a
+// plain spin on try_wait — any per-wait watchdog bookkeeping measured 5-30 % on
+// this kernel (a spin counter 4.6 us at c2 / 40 us at c3, a globaltimer deadline
+// or a try_wait suspend hint more), so the production path carries none.  WD =
+// true (CPDGPU_WATCHDOG=1, and the forced-stall tests): every 1024th failed try
+// reads the CTA's abort flag and a spin budget (~2^31 tries, seconds); past it the
+// wait records the fault in the context's fault word (mapped host memory, reported
+// by the next API return as CPDGPU_CUDA_ERROR), raises the abort flag, and every
+// wait of the CTA returns at once: the kernel unwinds and exits normally instead of
+// trapping (a trap poisons the caller's whole CUDA context).  With
+// SeedI8Params::progress each warp posts its position (progress[cta][warp]) and the
+// first stuck thread prints its CTA's table.
 __shared__ int wd_abort;  // per CTA
-__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int code, int info,
-                                             unsigned* progress, int* fault, uint32_t limit) {
-  uint32_t done = 0;
-  uint32_t spins = 0;
-  if (progress && (threadIdx.x & 31) == 0)
+__device__ __noinline__ void wd_fire(int code, int info, unsigned* progress, int* fault) {
+  if (progress) {
+    const volatile unsigned* t = progress + blockIdx.x * 16;
+    printf("seed_i8 stuck: cta %d warp %d code %d info %d | warps: %u %u %u %u %u %u %u %u | %u %u %u %u | %u %u\n",
+           blockIdx.x, threadIdx.x >> 5, code, info, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[8], t[9], t[10],
+           t[11], t[12], t[13]);
+  }
+  if (fault) atomicExch(fault, 1000 + code);
+  *reinterpret_cast<volatile int*>(&wd_abort) = 1;
+  __threadfence_block();
+}
+template <bool WD>
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int code, int info, unsigned* progress,
+                                             int* fault, uint32_t limit) {
+  if (WD && progress && (threadIdx.x & 31) == 0)
     *reinterpret_cast<volatile unsigned*>(progress + blockIdx.x * 16 + (threadIdx.x >> 5)) =
         static_cast<unsigned>(code * 100000 + info);
-  while (!done) {
+  uint32_t done = 0, spins = 0;
+  while (true) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-    if (done) break;
+    if (done) return;
+    if (!WD || ((++spins & 1023u) != 0u)) continue;
     if (*reinterpret_cast<volatile int*>(&wd_abort)) return;
-    if (++spins >= limit) {
-      if (progress) {
-        const volatile unsigned* t = progress + blockIdx.x * 16;
-        printf("seed_i8 stuck: cta %d warp %d code %d info %d | warps: %u %u %u %u %u %u %u %u | %u %u %u %u | %u %u\n",
-               blockIdx.x, threadIdx.x >> 5, code, info, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[8], t[9],
-               t[10], t[11], t[12], t[13]);
-      }
-      if (fault) atomicExch(fault, 1000 + code);
-      *reinterpret_cast<volatile int*>(&wd_abort) = 1;
-      __threadfence_block();
+    if (spins >= limit) {
+      wd_fire(code, info, progress, fault);
       return;
     }
   }
 }
-__device__ __forceinline__ bool wd_aborted() { return *reinterpret_cast<volatile int*>(&wd_abort) != 0; }
+template <bool WD>
+__device__ __forceinline__ bool wd_aborted() {
+  return WD && *reinterpret_cast<volatile int*>(&wd_abort) != 0;
+}
 // Unwinding after an abort: wait for async work that WAS issued (TMA / bulk copies,
 // MMAs) to land before the CTA exits.  That work completes in bounded time, so this
 // wait ignores the abort flag (and gives up after ~2^22 spins regardless).
@@ -178,7 +190,7 @@ __device__ __forceinline__ void mbar_drain_wait(uint64_t* bar, uint32_t parity) 
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
 }
-#define WAIT(bar, par, code, info) mbar_wait_wd(bar, par, code, info, p.progress, p.fault, wd_limit)
+#define WAIT(bar, par, code, info) mbar_wait_wd<WD>(bar, par, code, info, p.progress, p.fault, wd_limit)
 #define TWAIT(idx, bar, par, code, info)                 \
   do {                                                   \
     const long long t0_ = p.trace ? clock64() : 0;       \
@@ -290,7 +302,7 @@ __device__ __forceinline__ void pack4(double x0, double x1, double x2, double x3
   w[5] = prmt(g01, g23, 0x7632) ^ 0x80808080u;
 }
 
-template <int N, int NL>
+template <int N, int NL, bool WD>
 __global__ void __launch_bounds__(kI8Threads, 1)
     seed_i8_kernel(const SeedI8Params p, const __grid_constant__ CUtensorMap ymap) {
   using C = Cfg<N, NL>;
@@ -379,7 +391,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       for (int q = 0; q < nslots; ++q) {
         const int k = q >> 3, c = q & 7, slot = q % C::kRaw;
         if (q >= C::kRaw) WAIT(&raw_empty[slot], ((q / C::kRaw) - 1) & 1, 3, q);
-        if (wd_aborted()) break;  // watchdog: no new loads
+        if (wd_aborted<WD>()) break;  // watchdog: no new loads
         const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
         const int j = static_cast<int>(ct * 128), i = static_cast<int>(rb * 128 + 16 * c);
         const bool live = j < p.K && i < p.J;
@@ -389,7 +401,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         if (issued(q)) tma_2d(raw + slot * kRawSlot, &ymap, i, j, &raw_full[slot], pol_y);
         qn = q + 1;
       }
-      if (wd_aborted())  // the last loads of each slot land before the CTA exits
+      if (wd_aborted<WD>())  // the last loads of each slot land before the CTA exits
         for (int q = qn > C::kRaw ? qn - C::kRaw : 0; q < qn; ++q)
           if (issued(q)) mbar_drain_wait(&raw_full[q % C::kRaw], (q / C::kRaw) & 1);
     } else if (lane == 1) {
@@ -400,20 +412,20 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       for (int k = 0; k < n; ++k) {
         const int64_t tile = a0 + k, rb = tile / nCT, ct = tile - rb * nCT;
         if (k > 0) WAIT(rb_empty, (k - 1) & 1, 1, k);
-        if (wd_aborted()) break;
+        if (wd_aborted<WD>()) break;
         mbar_arrive_tx(rb_full, C::kB);
         bulk_load(rbuf, p.img_r + ct * C::kB, C::kB, rb_full, pol_k);
         kn = k + 1;
         if (rb != cur_rb) {
           if (m > 0) WAIT(lb_empty, (m - 1) & 1, 2, m);
-          if (wd_aborted()) break;
+          if (wd_aborted<WD>()) break;
           mbar_arrive_tx(lb_full, C::kBL);
           bulk_load(lbuf, p.img_l + rb * C::kBL, C::kBL, lb_full, pol_k);
           cur_rb = rb;
           ++m;
         }
       }
-      if (wd_aborted()) {
+      if (wd_aborted<WD>()) {
         if (kn > 0) mbar_drain_wait(rb_full, (kn - 1) & 1);
         if (m > 0) mbar_drain_wait(lb_full, (m - 1) & 1);
       }
@@ -426,7 +438,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       int m = 0;
       int seg = 0, pos = 0;  // right-accumulator segment and position in it
       for (int k = 0; k < n; ++k) {
-        if (wd_aborted()) break;  // watchdog: no new MMAs
+        if (wd_aborted<WD>()) break;  // watchdog: no new MMAs
         const int64_t tile = a0 + k, rb = tile / nCT;
         const bool last_of_rb = (k == n - 1) || ((tile + 1) / nCT != rb);
         const bool send = seg_end(tile, k, n, nCT, pos);
@@ -635,9 +647,10 @@ template <int N, int NL>
 __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, int64_t Lr, const KRSpec left,
                                                            int64_t Ll, int R, int64_t nCT, const double* yscale,
                                                            unsigned char* img_r, double* w_r, unsigned char* img_l,
-                                                           double* w_l) {
+                                                           double* w_l, int64_t numel, double budget, int* fault) {
   __shared__ double sc[N];
   __shared__ unsigned long long mbits[kMaxModes * N];
+  __shared__ double ssq[kMaxModes * N];  // tile 0 of each side: column sums of squares (error-budget check)
   __shared__ __align__(16) unsigned char im[kPl * N * 128 + 1024];
   const bool is_right = blockIdx.x < nCT;
   constexpr int NR = NL < N ? NL : N;
@@ -647,7 +660,11 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
   const int64_t L = is_right ? Lr : Ll, tile = is_right ? blockIdx.x : blockIdx.x - nCT;
   unsigned char* img = is_right ? img_r : img_l;
   double* w = is_right ? w_r : w_l;
-  for (int e = threadIdx.x; e < kMaxModes * N; e += blockDim.x) mbits[e] = 0ull;
+  for (int e = threadIdx.x; e < kMaxModes * N; e += blockDim.x) {
+    mbits[e] = 0ull;
+    ssq[e] = 0.0;
+  }
+  const bool check = tile == 0 && fault != nullptr;
   for (int e = kPl * NP * 128 + threadIdx.x; e < IB; e += blockDim.x) im[e] = 0;  // zero rows past the planes
   pdl_trigger();  // the seed may launch now: its Y stream does not depend on this kernel
   pdl_wait();     // the sorted factors come from the prologue
@@ -667,11 +684,35 @@ __global__ void __launch_bounds__(N * 16) kr_digits_kernel(const KRSpec right, i
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) cm = (a[u] > cm || a[u] != a[u]) ? a[u] : cm;  // NaN sticks
+          if (check) {
+            double q2 = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) q2 += a[u] * a[u];
+            atomicAdd(&ssq[m * N + r], q2);
+          }
         }
       atomicMax(&mbits[m * N + r], static_cast<unsigned long long>(__double_as_longlong(cm)));
     }
   }
   __syncthreads();
+  if (check && threadIdx.x < R && threadIdx.x < N) {
+    // the call's error budget (cpdgpu.cu i8_factors_ok_*): prod_m max / rms of this
+    // side's column against 2^11 mean|Y| / max|Y|; a device-form call whose factors
+    // were not checked on the host fails loudly here instead of returning a result
+    // outside the 1e-10 gate (the next call of the plan runs the DMMA pass)
+    const int r = threadIdx.x;
+    double ratio = 1.0;
+    for (int m = 0; m < spec.n; ++m) {
+      const double mxm = __longlong_as_double(static_cast<long long>(mbits[m * N + r]));
+      if (!(mxm > 0.0)) {
+        ratio = 0.0;
+        break;
+      }
+      ratio *= mxm / sqrt(ssq[m * N + r] / static_cast<double>(spec.dims[m]));
+    }
+    const double limit = yscale[2] > 0.0 ? budget * (yscale[3] / static_cast<double>(numel)) / yscale[2] : budget;
+    if (isfinite(ratio) && ratio > limit) atomicExch(fault, 3000);
+  }
   if (threadIdx.x < N) {
     const int r = threadIdx.x;
     double mx = 1.0;
@@ -795,9 +836,15 @@ __global__ void y_scale_final_kernel(const unsigned long long* bmax, const doubl
 template <int N, int NL>
 void launch_one_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t s) {
   using C = Cfg<N, NL>;
+  if (p.watchdog) {
+    static unsigned long long configured = 0;
+    set_smem_attr(seed_i8_kernel<N, NL, true>, C::kSmem, configured);
+    launch_k(seed_i8_kernel<N, NL, true>, dim3(p.P), dim3(kI8Threads), C::kSmem, s, pdl_enabled(), p, *ymap);
+    return;
+  }
   static unsigned long long configured = 0;
-  set_smem_attr(seed_i8_kernel<N, NL>, C::kSmem, configured);
-  launch_k(seed_i8_kernel<N, NL>, dim3(p.P), dim3(kI8Threads), C::kSmem, s, pdl_enabled(), p, *ymap);
+  set_smem_attr(seed_i8_kernel<N, NL, false>, C::kSmem, configured);
+  launch_k(seed_i8_kernel<N, NL, false>, dim3(p.P), dim3(kI8Threads), C::kSmem, s, pdl_enabled(), p, *ymap);
 }
 
 int i8_left_block(int N, int R) { return (N == 32 && R <= 24) ? 24 : ((N == 16 && R <= 12) ? 12 : N); }
@@ -817,23 +864,24 @@ int launch_seed_i8(const SeedI8Params& p, const CUtensorMap* ymap, cudaStream_t 
 }
 
 int launch_kr_digits(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, int N, int NL,
-                     const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, cudaStream_t s) {
+                     const double* yscale, void* img_r, double* w_r, void* img_l, double* w_l, int64_t numel,
+                     double budget, int* fault, cudaStream_t s) {
   const int64_t nCT = ceil_div(Kp, 128), nRB = ceil_div(Jp, 128);
   const dim3 grid(static_cast<unsigned>(nCT + nRB));
   auto* ir = static_cast<unsigned char*>(img_r);
   auto* il = static_cast<unsigned char*>(img_l);
   if (N == 16 && NL == 12)
     launch_k(kr_digits_kernel<16, 12>, grid, dim3(256), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
-             w_r, il, w_l);
+             w_r, il, w_l, numel, budget, fault);
   else if (N == 16)
     launch_k(kr_digits_kernel<16, 16>, grid, dim3(256), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
-             w_r, il, w_l);
+             w_r, il, w_l, numel, budget, fault);
   else if (NL == 24)
     launch_k(kr_digits_kernel<32, 24>, grid, dim3(512), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
-             w_r, il, w_l);
+             w_r, il, w_l, numel, budget, fault);
   else
     launch_k(kr_digits_kernel<32, 32>, grid, dim3(512), 0, s, pdl_enabled(), right, Kp, left, Jp, R, nCT, yscale, ir,
-             w_r, il, w_l);
+             w_r, il, w_l, numel, budget, fault);
   return 1;
 }
 

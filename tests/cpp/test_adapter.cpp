@@ -346,6 +346,59 @@ void test_pinv_and_als() {  // test_als.cpp
   for (int k = 0; k < 4; ++k) CHECK_LT(max_rel_diff(a[static_cast<size_t>(k)], b[static_cast<size_t>(k)]), 1e-10);
 }
 
+// sort_modes / random_init / standard_order / predicted_mult_count (mttkrp.hpp:28-35,76-86;
+// als.hpp:84-87) and the sharded gradient on one rank (host communicator)
+int host_sum(void*, double*, int64_t) { return 0; }  // world size 1: the sum is the local buffer
+
+void test_helpers_and_sharded() {
+  const std::vector<cpd::index_t> d{4, 2, 5, 3};
+  cpd::DenseTensor y = random_tensor(d, 77);
+  cpd::FactorList f = random_factors(d, 3, 78);
+  cpd::SortResult s = cpd::sort_modes(y, f);
+  CHECK((s.perm == std::vector<int>{2, 4, 1, 3}));
+  CHECK((s.inverse == std::vector<int>{3, 1, 4, 2}));
+  CHECK((s.tensor.shape().dims() == std::vector<cpd::index_t>{2, 3, 4, 5}));
+  // entry (i2, i4, i1, i3) of the sorted tensor is y(i1, i2, i3, i4)
+  CHECK(s.tensor.data()[1 + 2 * (2 + 3 * (3 + 4 * 4))] == y.data()[3 + 4 * (1 + 2 * (4 + 5 * 2))]);
+  auto gs = cpd::cp_gradient_all(s.tensor, s.factors);
+  auto g = cpd::cp_gradient_all(y, f);
+  for (int j = 1; j <= 4; ++j)
+    CHECK_LT(max_rel_diff(gs[static_cast<size_t>(j - 1)], g[static_cast<size_t>(s.perm[static_cast<size_t>(j - 1)] - 1)]), 1e-13);
+
+  const cpd::KruskalModel m = cpd::random_init(cpd::Shape({2, 3}), 2, 5);
+  CHECK(m.order() == 2 && m.rank() == 2 && m.factor(2).rows() == 3);
+  for (int n = 1; n <= 2; ++n)
+    for (cpd::index_t i = 0; i < m.factor(n).size(); ++i)
+      CHECK(m.factor(n).data()[i] >= 0.0 && m.factor(n).data()[i] < 1.0);
+  CHECK(throws<cpd::ArgumentError>([] { cpd::random_init(cpd::Shape({2, 3}), 0, 5); }));
+  CHECK((cpd::standard_order(3) == std::vector<int>{1, 2, 3}));
+
+  const cpd::Shape asc({2, 3, 4, 5});
+  for (int n = 1; n <= 4; ++n) {
+    CHECK(cpd::predicted_mult_count(asc, 3, n, cpd::CountVariant::fast) <=
+          cpd::predicted_mult_count(asc, 3, n, cpd::CountVariant::direct));
+    CHECK(cpd::predicted_mult_count(asc, 3, n, cpd::CountVariant::fast_derived) <=
+          cpd::predicted_mult_count(asc, 3, n, cpd::CountVariant::fast));
+  }
+  CHECK(throws<cpd::IndexError>([&] { cpd::predicted_mult_count(asc, 3, 5, cpd::CountVariant::fast); }));
+  CHECK(throws<cpd::ArgumentError>([] { cpd::predicted_mult_count(cpd::Shape({3, 2}), 3, 1, cpd::CountVariant::fast); }));
+
+  // sharded gradient, world size 1: equals the plain one
+  const std::vector<cpd::index_t> ad{3, 4, 5, 6};
+  cpd::DenseTensor ya = random_tensor(ad, 91);
+  cpd::FactorList fa = random_factors(ad, 4, 92);
+  cpd::gpu::comm_init_host(1, 0, host_sum, nullptr);
+  const auto b = cpd::gpu::slab_bounds(6, 1, 0);
+  CHECK(b.first == 0 && b.second == 6);
+  cpd::CostCounter cs, cp;
+  auto gsh = cpd::cp_gradient_all_sharded(ya, ya.shape(), fa, &cs);
+  auto gpl = cpd::cp_gradient_all(ya, fa, &cp);
+  for (int k = 0; k < 4; ++k) CHECK_LT(max_rel_diff(gsh[static_cast<size_t>(k)], gpl[static_cast<size_t>(k)]), 1e-13);
+  CHECK(cs.total() == cp.total());
+  cpd::gpu::comm_destroy();
+  CHECK(throws<cpd::ArgumentError>([&] { cpd::cp_gradient_all_sharded(ya, ya.shape(), fa); }));  // no communicator
+}
+
 }  // namespace
 
 int main() {
@@ -360,6 +413,7 @@ int main() {
     test_errors();
     test_direct();
     test_pinv_and_als();
+    test_helpers_and_sharded();
   } catch (const std::exception& e) {
     std::fprintf(stderr, "uncaught: %s\n", e.what());
     return 2;

@@ -171,7 +171,8 @@ def test_int8_error_budget_guard(gpu_ctx, oracle, i8_env, form):
     y_wide[17] = 1000.0  # max |Y| ~ 1250 mean |Y|: inside the tensor guard, outside the joint budget
     f_out = [x.copy() for x in base]
     for m in (1, 2, 3):
-        f_out[m][3, 4] *= 100.0  # every right-side mode outlier-dominated in column 4
+        f_out[m][3, 4] = 100.0  # every right-side mode outlier-dominated in column 4 (ratio ~60 < budget)
+    assert _budget_ratio(y0, dims, f_out) < 2048 < _budget_ratio(y_wide, dims, base)  # the premises
     for y, f, want_path, tol in [(y0, base, 1, 1e-10), (y0, f_out, 1, 1e-10), (y_wide, base, 0, 1e-12)]:
         t = cpd.DenseTensor.from_values(y, dims, ctx=gpu_ctx)
         g = grad(t, f)
@@ -230,3 +231,64 @@ def test_int8_reference_acceptance_criterion(gpu_ctx, oracle, i8_env):
             worst = max(worst, float(rel.max()))
     assert on_i8 >= 30, on_i8  # the int8 pass ran on a good share of the instances
     assert worst <= 1e-12, worst
+
+
+def _budget_ratio(y, dims, f):
+    """(max|Y| / mean|Y|) x max over both sides and columns of prod_m max / rms, in
+    the sorted frame at the pivot (the guard's formula, cpdgpu.cu i8_factors_ok_*)."""
+    order = sorted(range(len(dims)), key=lambda m: dims[m])
+    sd = [dims[m] for m in order]
+    J = np.cumprod([1] + sd)
+    p = max(n for n in range(1, len(sd) + 1) if J[n] <= J[-1] // J[n])
+    worst = 0.0
+    for side in (order[:p], order[p:]):
+        r = np.ones(f[0].shape[1])
+        for m in side:
+            a = np.abs(f[m])
+            r *= a.max(axis=0) / np.sqrt((a * a).mean(axis=0))
+        worst = max(worst, r.max())
+    return np.abs(y).max() / np.abs(y).mean() * worst
+
+
+def test_int8_device_budget_check_fails_loudly(gpu_ctx, oracle, i8_env):
+    """Device entry point, same factor buffer: the synchronous guard passed the first
+    factors; when the caller rewrites the buffer in place with factors outside the
+    budget, the device check in kr_digits_kernel makes that call a NumericError (no
+    silently inaccurate result) and the next call runs the DMMA pass, correct."""
+    import torch
+    rng = np.random.default_rng(33)
+    dims, R = (24, 20, 16, 12), 6
+    y = rng.standard_normal(int(np.prod(dims)))
+    y[17] = 150.0  # max|Y| / mean|Y| ~ 190: inside the tensor guard (2^12)
+    t = cpd.DenseTensor.from_values(y, dims, ctx=gpu_ctx)
+    good = _factors(rng, dims, R)
+    bad = [x.copy() for x in good]
+    for m in range(4):
+        bad[m][3, 4] = 100.0  # column 4 outlier-dominated in every mode
+    assert _budget_ratio(y, dims, good) < 2048 < _budget_ratio(y, dims, bad) / 1.01  # the test's premise
+    fd = torch.from_numpy(np.concatenate([x.reshape(-1, order="F") for x in good])).cuda()
+    gd = torch.zeros_like(fd)
+    gpu_ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    def call():
+        cpd.cp_gradient_all_device(t, R, fd.data_ptr(), gd.data_ptr())
+        torch.cuda.synchronize()
+        gpu_ctx.synchronize()
+        o, out, at = gd.cpu().numpy(), [], 0
+        for d in dims:
+            out.append(o[at:at + d * R].reshape(d, R, order="F"))
+            at += d * R
+        return out
+
+    g = call()
+    assert gpu_ctx.last_seed_path() == 1
+    for a, b in zip(g, oracle.cp_gradient_all(y, dims, good)[0]):
+        assert rel_fro(a, b) < 1e-10
+    fd.copy_(torch.from_numpy(np.concatenate([x.reshape(-1, order="F") for x in bad])).cuda())
+    with pytest.raises(cpd.NumericError, match="error budget"):
+        call()
+    g = call()
+    assert gpu_ctx.last_seed_path() == 0
+    for a, b in zip(g, oracle.cp_gradient_all(y, dims, bad)[0]):
+        assert rel_fro(a, b) < 1e-12
+    t.free()

@@ -1,0 +1,14 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+O=gpurun_out; T=${TAG:-ab7}
+: > $O/${T}_ab.txt
+for rep in 1 2 3; do
+  for v in ${VARIANTS:-old dense sparse}; do
+    CPDGPU_ABI_PARTIAL=1 CPDGPU_LIB=tools/bisect_$v.so timeout 300 python bench.py --config c5 --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1 2>&1 | python -c "
+import json,sys
+for l in sys.stdin:
+  if l.startswith('{'):
+    d=json.loads(l); r=d['roofline']; print('$v', round(d['ms_per_step'],3), 'ms  seed', round(r['kernel_ms'],3), 'mhz', d['clocks']['sm_mhz'])
+" >> $O/${T}_ab.txt
+  done
+done
