@@ -933,9 +933,12 @@ void bind_i8(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const void* ybase) {
   bool on = t->scale8_ok && std::isfinite(t->amax8) && std::isfinite(t->amean8) &&
             (t->amax8 == 0.0 || t->amax8 <= 4096.0 * t->amean8);
   if (on && pl.i8.ymap_base != ybase) {
+    // L2 promotion of the 16-row boxes: 256 B (default) or CPDGPU_I8_PROMO = 0 / 64 / 128
+    static const char* promo_env = std::getenv("CPDGPU_I8_PROMO");
+    const int promo = promo_env ? std::atoi(promo_env) : 256;
     on = cpdgpu::make_tensor_map_2d(&pl.i8.ymap, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
                                     static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
-                                    static_cast<uint64_t>(pl.Jp) * 8, 16, 128, true, true);
+                                    static_cast<uint64_t>(pl.Jp) * 8, 16, 128, true, promo);
     pl.i8.ymap_base = on ? ybase : nullptr;
   }
   pl.i8.tensor_ok = on;

@@ -50,7 +50,7 @@ int launch_seed_f64(const SeedParams& p, const CUtensorMap* tmap, const CUtensor
 // Host helper: 2-D tiled tensor map (driver entry point, no -lcuda link).
 bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, int elem_bytes,
                         uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1,
-                        bool swizzle128 = false, bool promote = true);
+                        bool swizzle128 = false, int promote = true);
 // Left seed alone with column-block accumulation (ALS / hook second pass): TI =
 // columns per block (256), nRB = column blocks, nCT = 32-row stages per block,
 // Rpart = partial slots [P * slots][8 NT][TI].  ymap: Y (dim0 J, dim1 K), box

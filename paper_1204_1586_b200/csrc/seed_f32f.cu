@@ -1099,7 +1099,7 @@ __global__ void __launch_bounds__(256) kr_images_kernel(const KRSpec right, int6
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
       const int64_t j = t * kTJ + j8 * 8 + jj;
-      const double x = (j < Kp && r < R) ? kr_entry(right, j, r) * sc : 0.0;
+      const double x = (j < Kp && r < R) ? (j < (1LL << 31) ? kr_entry32(right, static_cast<uint32_t>(j), r) : kr_entry(right, j, r)) * sc : 0.0;
       hi[jj] = __double2half(x);
       lo[jj] = __double2half(x - static_cast<double>(__half2float(hi[jj])));
     }
@@ -1117,7 +1117,7 @@ __global__ void __launch_bounds__(256) kr_images_kernel(const KRSpec right, int6
 #pragma unroll
   for (int ii = 0; ii < 8; ++ii) {
     const int64_t i = t * kTI + i8 * 8 + ii;
-    const double x = (i < Jp && r < R) ? kr_entry(left, i, r) * sc : 0.0;
+    const double x = (i < Jp && r < R) ? (i < (1LL << 31) ? kr_entry32(left, static_cast<uint32_t>(i), r) : kr_entry(left, i, r)) * sc : 0.0;
     hi[ii] = __double2half(x);
     lo[ii] = __double2half(x - static_cast<double>(__half2float(hi[ii])));
   }

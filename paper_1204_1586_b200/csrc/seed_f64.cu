@@ -736,7 +736,7 @@ int launch_seed_f64(const SeedParams& p, const CUtensorMap* tmap, const CUtensor
 
 bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, int elem_bytes,
                         uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1,
-                        bool swizzle128, bool promote) {
+                        bool swizzle128, int promote) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -755,7 +755,11 @@ bool make_tensor_map_2d(CUtensorMap* out, const void* base, CUtensorMapDataType 
   const cuuint32_t estride[2] = {1, 1};
   return encode(out, dtype, 2, const_cast<void*>(base), gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                promote ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                promote >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                : promote >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                : promote >= 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                : promote == 1   ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B  // bool true from older callers
+                                 : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
