@@ -286,6 +286,11 @@ struct Plan {
     DevBuf img_r, img_l, w_r, w_l;
     CUtensorMap ymap{};
     const void* ymap_base = nullptr;
+    // 128-byte-aligned column copy of Y when J_p * 8 is not a multiple of 128 (per
+    // tensor version): the 16-row TMA boxes then stream at full rate
+    DevBuf ypad;
+    int64_t ld = 0;
+    uint64_t ypad_version = ~0ull;
     // swapped with the fp64 geometry while an int8 gradient is recorded
     int TI_s = 128;
     int64_t nRB_s = 0;
@@ -932,14 +937,31 @@ void bind_i8(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const void* ybase) {
   }
   bool on = t->scale8_ok && std::isfinite(t->amax8) && std::isfinite(t->amean8) &&
             (t->amax8 == 0.0 || t->amax8 <= 4096.0 * t->amean8);
-  if (on && pl.i8.ymap_base != ybase) {
+  // columns whose starts are not 128-byte aligned (c3: 2744 rows) stream from a
+  // padded copy made once per tensor version (CPDGPU_I8_PAD=0 reads Y in place)
+  static const char* pad_env = std::getenv("CPDGPU_I8_PAD");
+  const void* view = ybase;
+  pl.i8.ld = pl.Jp;
+  if (on && (pl.Jp * 8) % 128 != 0 && !(pad_env && std::atoi(pad_env) == 0)) {
+    const int64_t ld = cpdgpu::ceil_div(pl.Jp, 16) * 16;
+    if (!pl.i8.ypad.p || pl.i8.ypad_version != t->version) {
+      pl.i8.ypad.ensure(static_cast<size_t>(ld * pl.Kp) * sizeof(double));
+      ctx->launches += cpdgpu::launch_pad_rows_f64(static_cast<const double*>(ybase), pl.i8.ypad.d(), pl.Jp, ld, pl.Kp,
+                                                   ctx->num_sms, ctx->stream);
+      CK(cudaGetLastError());
+      pl.i8.ypad_version = t->version;
+    }
+    view = pl.i8.ypad.p;
+    pl.i8.ld = ld;
+  }
+  if (on && pl.i8.ymap_base != view) {
     // L2 promotion of the 16-row boxes: 256 B (default) or CPDGPU_I8_PROMO = 0 / 64 / 128
     static const char* promo_env = std::getenv("CPDGPU_I8_PROMO");
     const int promo = promo_env ? std::atoi(promo_env) : 256;
-    on = cpdgpu::make_tensor_map_2d(&pl.i8.ymap, ybase, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+    on = cpdgpu::make_tensor_map_2d(&pl.i8.ymap, view, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
                                     static_cast<uint64_t>(pl.Jp), static_cast<uint64_t>(pl.Kp),
-                                    static_cast<uint64_t>(pl.Jp) * 8, 16, 128, true, promo);
-    pl.i8.ymap_base = on ? ybase : nullptr;
+                                    static_cast<uint64_t>(pl.i8.ld) * 8, 16, 128, true, promo);
+    pl.i8.ymap_base = on ? view : nullptr;
   }
   pl.i8.tensor_ok = on;
   set_i8_on(pl);

@@ -174,6 +174,9 @@ int launch_kr_scale(const KRSpec& right, const KRSpec& left, int R, double* scal
 int launch_kr_split(const double* rows, int64_t L, int ld, const double* scale, void* tiles, cudaStream_t s);
 int launch_y_scale(const float* y, int64_t n, unsigned int* amax_scratch, float* scale, double* inv, int num_sms,
                    cudaStream_t s);
+// fp64 view J x K (leading dimension J) -> leading dimension LD (even, >= J), rows past J zero
+int launch_pad_rows_f64(const double* src, double* dst, int64_t J, int64_t LD, int64_t K, int num_sms,
+                        cudaStream_t s);
 int launch_pad_rows_f32(const float* src, float* dst, int64_t J, int64_t J8, int64_t K, int num_sms,
                         cudaStream_t s);
 // 2-D map of a J8 x K column-major fp32 matrix; box for the right (128 i x 64 j)

@@ -948,4 +948,27 @@ int launch_i8_factor_guard(const KRSpec& right, const KRSpec& left, int R, doubl
   return 1;
 }
 
+// Column-padded copy of an fp64 view (J rows -> leading dimension LD, rows J..LD-1
+// zero): 128-byte column starts for the int8 pass's 16-row boxes (c3's 2744-row
+// columns start 64 bytes off a line every other column).  Two doubles per thread.
+__global__ void pad_rows_f64_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t J, int64_t LD,
+                                    int64_t K) {
+  const int64_t half = LD / 2;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < half * K;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / half, i = 2 * (e - j * half);
+    const double* col = src + j * J;
+    double2 v;
+    v.x = i < J ? __ldcs(col + i) : 0.0;
+    v.y = i + 1 < J ? __ldcs(col + i + 1) : 0.0;
+    __stcs(reinterpret_cast<double2*>(dst + j * LD + i), v);
+  }
+}
+
+int launch_pad_rows_f64(const double* src, double* dst, int64_t J, int64_t LD, int64_t K, int num_sms,
+                        cudaStream_t s) {
+  pad_rows_f64_kernel<<<num_sms * 8, 256, 0, s>>>(src, dst, J, LD, K);
+  return 1;
+}
+
 }  // namespace cpdgpu
