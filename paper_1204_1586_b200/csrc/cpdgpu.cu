@@ -1659,7 +1659,13 @@ void timeline_print(cpdgpu_ctx* ctx, const char* what) {
 int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& fuse_l) {
   static const bool disabled = std::getenv("CPDGPU_NO_L0") != nullptr;
   fuse_r = fuse_l = false;
-  if (disabled || pl.f32 || pl.chunks.size() != 1 || pl.slot_tab_max >= 16) return 0;
+  // fp32: the fused pass only (right slots [slot][64 r][128 i] like the int8 pass's;
+  // its left side reads Ls, which reduce_left32 has summed from the band partials)
+  const bool f32f = pl.f32 && pl.ff.on && pl.p + 1 <= pl.N;
+  static const char* l0f_env = std::getenv("CPDGPU_F32_L0");
+  if (disabled || (pl.f32 && (!f32f || (l0f_env && std::atoi(l0f_env) == 0))) || pl.chunks.size() != 1 ||
+      (f32f ? pl.ff.tab_max : pl.slot_tab_max) >= 16)
+    return 0;
   const Plan::Chunk& c = pl.chunks[0];
   const int R = static_cast<int>(pl.R);
   fuse_r = pl.p >= 2 && pl.J[pl.p - 1] <= cpdgpu::kL0MaxRows;
@@ -1671,8 +1677,10 @@ int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& 
   int64_t rows_max = 0;
   if (fuse_r) rows_max = std::max<int64_t>(rows_max, pl.Jp);
   if (fuse_l) rows_max = std::max<int64_t>(rows_max, pl.Kp);
+  static const char* rows_env = std::getenv("CPDGPU_L0_ROWS");  // A/B knob: seed rows per CTA
+  const int64_t per_cta = rows_env && std::atoi(rows_env) > 0 ? std::atoi(rows_env) : 1024;
   const int target = static_cast<int>(std::max<int64_t>((2 * ctx->num_sms + R * nsides - 1) / (R * nsides),
-                                                        cpdgpu::ceil_div(rows_max, 1024)));
+                                                        cpdgpu::ceil_div(rows_max, per_cta)));
   auto chunks = [&](cpdgpu::L0Side& sd) {
     int64_t nq = std::min<int64_t>(target, sd.B);
     int64_t bq = cpdgpu::ceil_div(sd.B, nq);
@@ -1688,10 +1696,18 @@ int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& 
     const int j = pl.p;
     sd.zsrc = 1;
     sd.Z = pl.Rpart.d() + c.rpart_off;
-    sd.RP = c.NT * 8;
-    sd.TI = c.sp.TI;
-    sd.rb_ptr = static_cast<const int*>(pl.slot_tab.p);
-    sd.slot_list = static_cast<const int*>(pl.slot_tab.p) + pl.slot_tab_ptr_len;
+    if (f32f) {
+      sd.Z = pl.Rpart.d();
+      sd.RP = cpdgpu::seed_f32_rank_cols();
+      sd.TI = 128;
+      sd.rb_ptr = static_cast<const int*>(pl.ff.tab.p);
+      sd.slot_list = static_cast<const int*>(pl.ff.tab.p) + pl.ff.tab_len;
+    } else {
+      sd.RP = c.NT * 8;
+      sd.TI = c.sp.TI;
+      sd.rb_ptr = static_cast<const int*>(pl.slot_tab.p);
+      sd.slot_list = static_cast<const int*>(pl.slot_tab.p) + pl.slot_tab_ptr_len;
+    }
     sd.M = pl.J[j - 1];
     sd.B = pl.sd[j - 1];
     sd.krA = spec_over(pl, pl.Fs.d(), false, 1, j - 1, 0);
@@ -1713,7 +1729,7 @@ int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& 
   if (fuse_l) {  // left: opA recursion L^(p+2) (G(N) when p + 2 == N), opB extraction G(p+1)
     cpdgpu::L0Side& sd = l0.side[l0.nsides++];
     const int j = pl.p + 1;
-    if (pl.lpart_direct) {
+    if (pl.lpart_direct || f32f) {
       sd.zsrc = 0;
       sd.Z = pl.Ls.d();
       sd.ldz = pl.Kp;

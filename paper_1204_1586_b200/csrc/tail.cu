@@ -392,7 +392,15 @@ __global__ void __launch_bounds__(kL0Threads) l0_kernel(const L0Step st, double*
     const double* p0 = sd.scratch + static_cast<int64_t>(r) * sd.nq * M;
     for (int64_t a = tid; a < M; a += kL0Threads) {
       double s = 0.0;
-      for (int q = 0; q < sd.nq; ++q) s += __ldcg(p0 + static_cast<int64_t>(q) * M + a);
+      int q = 0;
+      for (; q + 8 <= sd.nq; q += 8) {  // eight loads in flight, added in chunk order
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(p0 + static_cast<int64_t>(q + u) * M + a);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; q < sd.nq; ++q) s += __ldcg(p0 + static_cast<int64_t>(q) * M + a);
       outB[r * sd.ldoB + a] = s;
     }
     if (tid == 0) sd.tickets[r] = 0u;  // ready for the next replay

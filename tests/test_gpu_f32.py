@@ -188,3 +188,29 @@ def test_f32_alternate_seed_paths(env, path):
     assert res.returncode == 0, res.stderr[-2000:]
     for got_path, err in json.loads(res.stdout.strip().splitlines()[-1]):
         assert got_path == path and err <= TOL, (got_path, err)
+
+
+def _rand_shapes(seed, count):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        N = int(rng.integers(3, 6))
+        dims = sorted(int(x) for x in rng.integers(3, 60, size=N))
+        if np.prod(dims) > 4_000_000 or np.prod(dims) < 2000:
+            continue
+        out.append((dims, int(rng.choice([7, 16, 33, 64]))))
+    return out
+
+
+@pytest.mark.parametrize("dims,R", _rand_shapes(2026, 10))
+def test_f32_fused_random_shapes(gpu_ctx, oracle, dims, R):
+    """Random ascending fp32 shapes through the default path (the fused pass over
+    the operand image: ragged bands, ragged column tiles, the first level fused
+    with the partial reductions) against the fp64 oracle on the same values."""
+    y = cpd.DenseTensor.generate(dims, cpd.DIST_UNIFORM_PM1, seed=sum(dims), ctx=gpu_ctx, dtype=cpd.F32)
+    f = [oracle.fill_normal(700 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
+    g = cpd.cp_gradient_all(y, f)
+    want = oracle.cp_gradient_all(y.values().astype(np.float64), dims, f)[0]
+    errs = rel_errs(g, want)
+    assert max(errs) <= TOL, (dims, R, errs)
+    y.free()
