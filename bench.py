@@ -270,12 +270,13 @@ def run_ours(args, cfg):
         gpu_launches = ctx.launch_count() - launches0  # kernels of the K timed steps
         if world > 1:
             dist.barrier()
-        # clocks need a busy window long enough to sample: keep the same step
-        # running for ~1 s after the timed region when the region was short
+        # clocks need a busy window long enough to sample: keep the slab's
+        # gradient running for ~1 s after the timed region when the region was
+        # short (no collective here: the ranks may loop a different number of times)
         t_end = time.time() + 1.0
         while time.time() < t_end and len(clk.lines) < 10:
             for _ in range(50):
-                step()
+                cpd.cp_gradient_all_device(y, R, fdev.data_ptr(), gdev.data_ptr(), pivot)
             torch.cuda.synchronize(dev)
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, stops)]
     tot_ms = float(np.sum(step_ms))
@@ -522,6 +523,23 @@ def c4_device_tensor(ctx, dims, truth, seed=4):
     return y
 
 
+def c4_slab_tensor(ctx, dims, truth, lo, hi, allsum, seed=4):
+    """Rows [lo, hi) of the last mode of c4_device_tensor's Y (the same counter-based
+    noise and model; the noise scale from the global norms via `allsum`)."""
+    import paper_1204_1586_b200 as cpd
+    ldims = list(dims[:-1]) + [hi - lo]
+    off = lo * int(np.prod(dims[:-1]))
+    ltruth = list(truth[:-1]) + [np.asfortranarray(truth[-1][lo:hi])]
+    y = cpd.DenseTensor.generate(ldims, cpd.DIST_NORMAL, seed=seed, ctx=ctx, offset=off)
+    e2 = allsum(y.norm2())
+    t = cpd.DenseTensor.generate(ldims, cpd.DIST_NORMAL, seed=seed, ctx=ctx, offset=off)
+    t.axpby_kruskal(0.0, 1.0, ltruth)
+    full2 = allsum(t.norm2())
+    t.free()
+    y.axpby_kruskal(float(np.sqrt(full2) / (10.0 * np.sqrt(e2))), 1.0, ltruth)
+    return y
+
+
 def als_metric(desc):
     return f"CP_ALS iterations per second ({desc})"
 
@@ -591,13 +609,15 @@ def run_reference_als(args, cfg):
 
 def run_ours_als(args, cfg):
     """c4: K fast ALS sweeps on the device (cpdgpu_als_run), per-sweep CUDA events
-    on the launching stream.  Y (6.2 GB) is far larger than L2.  N>1 runs
-    independent replicas (the Gauss-Seidel sweep is not sharded)."""
+    on the launching stream.  Y (6.2 GB) is far larger than L2.  N>1 shards the
+    last mode (cpdgpu_als_run_sharded: the global Gauss-Seidel order, an all-reduce
+    of each G(n), n < N, before its update; strong scaling)."""
     import torch
     import torch.distributed as dist
 
     import paper_1204_1586_b200 as cpd
     from paper_1204_1586_b200 import build as B
+    from paper_1204_1586_b200 import sharded
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -620,16 +640,36 @@ def run_ours_als(args, cfg):
     B.build()
     dims, R, dtype, desc = cfg
     N = len(dims)
-    slab = int(np.prod(dims))
     esize = 8
     ctx = cpd.Context(local)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     truth, init = c4_truth(dims[0], R, N, 4, lambda s, n: device_normal(ctx, s, n, 1).reshape(-1))
-    y = c4_device_tensor(ctx, dims, truth)
+    if world > 1:
+        lo, hi = cpd.slab_bounds(dims[-1], world, rank)
 
-    cpd.run(y, init, cpd.SolveOptions(max_iters=max(args.warmup, 3)))  # warm-up (graph capture)
+        def allsum(v):
+            t = torch.tensor([v], device=dev, dtype=torch.float64)
+            dist.all_reduce(t)
+            return float(t.item())
+
+        y = c4_slab_tensor(ctx, dims, truth, lo, hi, allsum)
+        loc_init = list(init[:-1]) + [init[-1][lo:hi]]
+        comm = sharded.library_comm(ctx, dist)
+
+        def run_sweeps(k):
+            return cpd.als_run_sharded(y, dims, [f.copy(order="F") for f in init], max_iters=k)
+    else:
+        y = c4_device_tensor(ctx, dims, truth)
+        loc_init = init
+        comm = None
+
+        def run_sweeps(k):
+            return cpd.run(y, init, cpd.SolveOptions(max_iters=k)).trace
+    slab = int(np.prod(y.dims))
+
+    run_sweeps(max(args.warmup, 3))  # warm-up (graph capture)
     torch.cuda.synchronize(dev)
     launches0 = ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -638,30 +678,34 @@ def run_ours_als(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
         ev0.record(stream)
-        res = cpd.run(y, init, cpd.SolveOptions(max_iters=args.steps))
+        trace = run_sweeps(args.steps)
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         gpu_launches = ctx.launch_count() - launches0
         if world > 1:
             dist.barrier()
-        t_end = time.time() + 2.0  # keep the same sweep busy until the sampler has seen it
-        while time.time() < t_end and len(clk.lines) < 10:
-            cpd.run(y, init, cpd.SolveOptions(max_iters=20))
-    sweep_s = float(np.sum(res.trace.seconds))
+            for _ in range(2):  # a fixed count: every rank runs the same collectives
+                run_sweeps(20)
+        else:
+            t_end = time.time() + 2.0  # keep the same sweep busy until the sampler has seen it
+            while time.time() < t_end and len(clk.lines) < 10:
+                run_sweeps(20)
+    sweep_s = float(np.sum(trace.seconds))
     if world > 1:
         t = torch.tensor([sweep_s], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sweep_s = float(t.item())
+        comm.close()
     ms = sweep_s / args.steps * 1e3
-    value = world * args.steps / sweep_s
+    value = args.steps / sweep_s
 
     # dominant kernels: the two seed passes of a sweep (K1 right pass, then the
     # column-block left pass after the right phase's updates), CUDA events around
     # each launch on the launching stream (ctx timing mode runs the sweep eagerly)
     ctx.set_timing(True)
     seed_ms = []
-    f_h = [np.array(f, dtype=np.float64, order="F", copy=True) for f in init]
-    for _ in range(6):
+    f_h = [np.array(f, dtype=np.float64, order="F", copy=True) for f in loc_init]
+    for _ in range(6):  # N > 1: the slab's own (local) sweep, whose seeds are the sharded sweep's
         cpd.als_sweep_fast(y, f_h)
         seed_ms.append(ctx.last_seed_ms())
     ctx.set_timing(False)
@@ -707,21 +751,21 @@ def run_ours_als(args, cfg):
                "final_rel_error": r2.trace.rel_error[-1]}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline:
         yh = y.values()
         cpu = cpu_als_sample(args, yh, dims, init)
         del yh
     if rank == 0:
         line = {
             "metric": als_metric(desc), "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic rank-16 N(0,1) model + N(0,1) noise at 20 dB, counter-based generator",
             "config": {"workload": args.config, "dims": dims, "R": R,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": f"last-mode slabs x{world} (sharded ALS)" if world > 1 else "single",
                        "l2": "inputs larger than L2 (6.2 GB tensor)",
                        "run_ms_incl_fit": ev0.elapsed_time(ev1),
-                       "final_rel_error": res.trace.rel_error[-1]},
+                       "final_rel_error": trace.rel_error[-1]},
             "gpu_launches": gpu_launches, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }

@@ -516,6 +516,26 @@ inline std::vector<Matrix> cp_gradient_all_sharded(const DenseTensor& slab, cons
   return out;
 }
 
+// Sharded als_sweep_fast (als.cpp:69-78): every rank passes its slab and the
+// GLOBAL factors, which leave identical on every rank; returns the global cost.
+inline double als_sweep_fast_sharded(const DenseTensor& slab, const Shape& global_shape, FactorList& factors,
+                                     double pinv_rtol = 1e-12, CostCounter* counter = nullptr) {
+  const int N = global_shape.order();
+  if (N < 2) throw ArgumentError("cp_gradient_all: need an order-2 or higher tensor");
+  if (factor_shape(factors) != global_shape)
+    throw ShapeError("cp_gradient_all: factor row counts do not match the tensor");
+  auto& ctx = gpu::context();
+  const auto gd = detail::dims64(global_shape);
+  std::vector<double*> fp;
+  for (auto& f : factors) fp.push_back(f.data());
+  double cost = 0.0;
+  uint64_t mults = 0;
+  ctx.check(cpdgpu_als_sweep_sharded(ctx.h, slab.device(), N, gd.data(), factor_rank(factors), fp.data(), pinv_rtol,
+                                     &cost, &mults));
+  if (counter) counter->charge(mults);
+  return cost;
+}
+
 // predicted_mult_count (mttkrp.hpp:76-86): the analytic count of one mode
 enum class CountVariant { direct, fast, fast_derived };
 inline std::uint64_t predicted_mult_count(const Shape& shape, index_t R, int n, CountVariant variant) {

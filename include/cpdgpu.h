@@ -195,6 +195,19 @@ int cpdgpu_cp_gradient_all_sharded(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, 
  * GLOBAL result, (sum_{n<N} I_n + I_N) x R doubles: G(1..N-1) then G(N). */
 int cpdgpu_cp_gradient_all_sharded_device(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims,
                                           int64_t R, const double* factors_dev, double* out_dev);
+/* Sharded als_sweep_fast (als.cpp:69-78) in the global sweep order: all-reduce
+ * of each G(n), n < N, before A_n's update (I_n x R), of A_N's Gram after its
+ * row-local update (R x R), and of [A_N | G(N)] rows for the cost and the
+ * caller's whole A_N (2 I_N x R).  factors: the GLOBAL matrices, updated in
+ * place identically on every rank.  A NumericError on any rank fails the call on
+ * every rank.  cost_out / mults optional (mults: the unsharded sweep's charge). */
+int cpdgpu_als_sweep_sharded(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims, int64_t R,
+                             double* const* factors, double pinv_rtol, double* cost_out, uint64_t* mults);
+/* run(y, init, Algorithm::als_fast, opts) (als.cpp:147-210) over slabs; traces
+ * as cpdgpu_als_run (the cost and fit are global; every rank stops together). */
+int cpdgpu_als_run_sharded(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims, int64_t R,
+                           double* const* factors, int max_iters, double tol, double pinv_rtol, double* cost_trace,
+                           double* rel_trace, double* sec_trace, uint64_t* mults_trace, int* iters_run);
 
 /* ---- direct MTTKRP (Algorithm 1 cost model; mttkrp.hpp:19-20, mttkrp.cpp:29-54)
  * One pass over Y for one mode: out = Y_(n) (KR_{k != n} A(k)), I_n x R column-major,

@@ -11,7 +11,8 @@ from .api import (DIST_NORMAL, DIST_UNIFORM_PM1, F32, F64, Context, CostCounter,
                   fast_update_order, pinv_psd, run, select_pivot, sort_modes, mttkrp_direct,
                   mttkrp_direct_device, als_sweep_direct, mu_sweep, gd_step, uniform01, random_init,
                   generate_problem, cost, relative_error, cp_gradient_set, Communicator,
-                  comm_unique_id, slab_bounds, cp_gradient_all_sharded, cp_gradient_all_sharded_device)
+                  comm_unique_id, slab_bounds, cp_gradient_all_sharded, cp_gradient_all_sharded_device,
+                  als_sweep_sharded, als_run_sharded)
 
 __all__ = [
     "ArgumentError", "CpdError", "DeviceError", "DomainError", "IndexError", "NumericError", "ParseError",
@@ -22,4 +23,5 @@ __all__ = [
     "mttkrp_direct", "mttkrp_direct_device", "als_sweep_direct", "mu_sweep", "gd_step", "uniform01",
     "random_init", "generate_problem", "cost", "relative_error", "cp_gradient_set", "Communicator",
     "comm_unique_id", "slab_bounds", "cp_gradient_all_sharded", "cp_gradient_all_sharded_device",
+    "als_sweep_sharded", "als_run_sharded",
 ]

@@ -69,6 +69,11 @@ SIGNATURES = {
                                                  c_dbl_pp, C.POINTER(c_u64)]),
     "cpdgpu_cp_gradient_all_sharded_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(c_i64), c_i64,
                                                         C.c_void_p, C.c_void_p]),
+    "cpdgpu_als_sweep_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(c_i64), c_i64, c_dbl_pp,
+                                           C.c_double, c_dbl_p, C.POINTER(c_u64)]),
+    "cpdgpu_als_run_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(c_i64), c_i64, c_dbl_pp, C.c_int,
+                                         C.c_double, C.c_double, c_dbl_p, c_dbl_p, c_dbl_p, C.POINTER(c_u64),
+                                         C.POINTER(C.c_int)]),
     "cpdgpu_mttkrp_direct": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.c_int, c_dbl_p, C.POINTER(c_u64)]),
     "cpdgpu_mttkrp_direct_device": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, C.c_void_p, C.c_int, C.c_void_p]),
     "cpdgpu_als_sweep_direct": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, C.POINTER(C.c_int), C.c_int,

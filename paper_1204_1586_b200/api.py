@@ -451,6 +451,48 @@ def cp_gradient_all_sharded_device(slab: DenseTensor, global_dims: Sequence[int]
                ctx.h)
 
 
+def als_sweep_sharded(slab: DenseTensor, global_dims: Sequence[int], factors: list, pinv_rtol: float = 1e-12,
+                      counter: Optional[CostCounter] = None) -> float:
+    """Sharded fast ALS sweep (als.cpp:69-78 over a last-mode slab): every rank
+    passes its slab and the GLOBAL factors, which are replaced (list elements)
+    by the same updated factors on every rank.  Returns the global cost after
+    the sweep (kruskal.cpp:58-77)."""
+    gd = [int(d) for d in global_dims]
+    bufs = [b.copy(order="F") for b in _factor_bufs(factors, gd)]
+    R = bufs[0].shape[1]
+    cost, mults = C.c_double(), C.c_uint64()
+    ctx = slab.ctx
+    _lib.check(ctx._L.cpdgpu_als_sweep_sharded(ctx.h, slab.h, len(gd), _dims_arg(gd), R, _ptr_array(bufs), pinv_rtol,
+                                               C.byref(cost), C.byref(mults)), ctx.h)
+    for k, b in enumerate(bufs):
+        factors[k] = b
+    if counter is not None:
+        counter.charge(int(mults.value))
+    return float(cost.value)
+
+
+def als_run_sharded(slab: DenseTensor, global_dims: Sequence[int], factors: list, max_iters: int = 20,
+                    tol: float = 0.0, pinv_rtol: float = 1e-12) -> "RunTrace":
+    """run(..., Algorithm::als_fast) (als.cpp:147-210) over last-mode slabs;
+    factors replaced in place (list elements), identical on every rank."""
+    gd = [int(d) for d in global_dims]
+    bufs = [b.copy(order="F") for b in _factor_bufs(factors, gd)]
+    R = bufs[0].shape[1]
+    cost, rel, sec = (np.zeros(max_iters) for _ in range(3))
+    mults = (C.c_uint64 * max_iters)()
+    it = C.c_int()
+    ctx = slab.ctx
+    dp = lambda a: a.ctypes.data_as(_lib.c_dbl_p)  # noqa: E731
+    _lib.check(ctx._L.cpdgpu_als_run_sharded(ctx.h, slab.h, len(gd), _dims_arg(gd), R, _ptr_array(bufs),
+                                             int(max_iters), float(tol), float(pinv_rtol), dp(cost), dp(rel),
+                                             dp(sec), mults, C.byref(it)), ctx.h)
+    for k, b in enumerate(bufs):
+        factors[k] = b
+    n = it.value
+    return RunTrace(cost=list(cost[:n]), rel_error=list(rel[:n]), seconds=list(sec[:n]),
+                    mults=[int(m) for m in mults[:n]], iters_run=n)
+
+
 # ---- direct MTTKRP (mttkrp.hpp:19-20): Algorithm 1's one-pass-per-mode cost ---------
 
 def mttkrp_direct(y: DenseTensor, factors: list, n: int, counter: Optional[CostCounter] = None) -> np.ndarray:

@@ -3302,6 +3302,27 @@ ShardGeom shard_geometry(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int6
   return g;
 }
 
+// In-place sum of `count` device doubles across the communicator, ordered on the
+// context stream (NCCL), or staged through host memory for the caller's collective.
+void comm_allreduce(cpdgpu_ctx* ctx, double* dev, int64_t count, const char* who) {
+  Comm& c = *ctx->comm;
+  if (c.nranks == 1) return;
+  if (c.nccl) {
+    NcclApi& a = nccl_api();
+    const ncclResult_t r =
+        a.all_reduce(dev, dev, static_cast<size_t>(count), ncclFloat64, ncclSum, c.nccl, ctx->stream);
+    if (r != ncclSuccess) fail(CPDGPU_CUDA_ERROR, "%s: ncclAllReduce: %s", who, a.error_string(r));
+    return;
+  }
+  const size_t bytes = static_cast<size_t>(count) * sizeof(double);
+  c.hbuf.ensure(bytes);
+  CK(cudaMemcpyAsync(c.hbuf.p, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int st = c.host_fn(c.user, c.hbuf.d(), count);
+  if (st != 0) fail(st > 0 ? st : CPDGPU_CUDA_ERROR, "%s: host all-reduce failed (%d)", who, st);
+  CK(cudaMemcpyAsync(dev, c.hbuf.p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+}
+
 // local gradient of the slab at the global pivot, then ONE in-place all-reduce of
 // [partial G(1..N-1) | G(N) rows placed at the slab's offset] into out_dev
 void sharded_device(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, const ShardGeom& g, int64_t R, const double* fdev,
@@ -3319,21 +3340,98 @@ void sharded_device(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, const ShardGeom& g, in
   CK(cudaMemcpy2DAsync(out_dev + g.partial + g.lo, static_cast<size_t>(IN) * sizeof(double), c.lbuf.d() + g.partial,
                        static_cast<size_t>(rows) * sizeof(double), static_cast<size_t>(rows) * sizeof(double),
                        static_cast<size_t>(R), cudaMemcpyDeviceToDevice, ctx->stream));
-  if (c.nranks == 1) return;
-  if (c.nccl) {
-    NcclApi& a = nccl_api();
-    const ncclResult_t r = a.all_reduce(out_dev, out_dev, static_cast<size_t>(g.total), ncclFloat64, ncclSum, c.nccl,
-                                        ctx->stream);
-    if (r != ncclSuccess) fail(CPDGPU_CUDA_ERROR, "ncclAllReduce: %s", a.error_string(r));
-    return;
-  }
-  const size_t bytes = static_cast<size_t>(g.total) * sizeof(double);
-  c.hbuf.ensure(bytes);
-  CK(cudaMemcpyAsync(c.hbuf.p, out_dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  comm_allreduce(ctx, out_dev, g.total, "cp_gradient_all_sharded");
+}
+
+// ---- sharded fast ALS (als.cpp:69-78 over last-mode slabs) ------------------------
+// The sweep keeps its Gauss-Seidel order (the global frame: modes p*..1, then
+// p*+1..N).  G(j), j < N, is a linear sum over slabs: one all-reduce of I_j x R
+// before A_j's update, identical on every rank, which the recursion then
+// consumes.  A_N's rows belong to the slab: the update is local and only its Gram
+// (R x R) is summed.  The cost (kruskal.cpp:58-77) needs <Y, Yhat> over A_N's
+// rows: one all-reduce of [A_N rows | G(N) rows] placed at the slab offset, which
+// also hands every rank the whole updated A_N.
+
+void sharded_als_prepare(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* slab, const ShardGeom& g,
+                         const double* const* factors) {
+  const int64_t R = pl.R, rows = g.hi - g.lo;
+  for (int m = 0; m + 1 < pl.N; ++m)
+    std::memcpy(pl.hF.d() + pl.off_orig[m], factors[m], static_cast<size_t>(g.gdims[m] * R) * sizeof(double));
+  for (int64_t r = 0; r < R; ++r)
+    std::memcpy(pl.hF.d() + pl.off_orig[pl.N - 1] + r * rows, factors[pl.N - 1] + r * g.gdims[pl.N - 1] + g.lo,
+                static_cast<size_t>(rows) * sizeof(double));
+  CK(cudaMemcpyAsync(pl.Forig.d(), pl.hF.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  compute_norm2(ctx, slab);  // the slab's ||Y||^2, summed below
+  CK(cudaMemcpyAsync(pl.norm.d(), &slab->norm2, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(pl.status.p, 0, sizeof(int), ctx->stream));
+  gather_factors(ctx, pl, pl.Forig.d());
+  set_gtab(ctx, pl, pl.Gorig.d());
+  init_grams(ctx, pl);
+  comm_allreduce(ctx, pl.norm.d(), 1, "als_sweep_sharded");
+  comm_allreduce(ctx, pl.grams.d() + static_cast<int64_t>(pl.N - 1) * R * R, R * R, "als_sweep_sharded");
+}
+
+void sharded_als_sweep(cpdgpu_ctx* ctx, Plan& pl, const ShardGeom& g, double rtol, double* cost_slot) {
+  Comm& c = *ctx->comm;
+  const int R = static_cast<int>(pl.R);
+  const int64_t rows = g.hi - g.lo, IN = g.gdims[pl.N - 1];
+  sweep_body(ctx, pl, [&](int j) {
+    double* G = pl.Gorig.d() + pl.off_orig[j - 1];  // global frame: sorted j is caller j
+    double* gram = pl.grams.d() + static_cast<int64_t>(j - 1) * R * R;
+    if (j < pl.N) comm_allreduce(ctx, G, pl.sd[j - 1] * R, "als_sweep_sharded");
+    ctx->launches += cpdgpu::launch_als_update(G, pl.sd[j - 1], R, pl.grams.d(), pl.N, j - 1, rtol, pl.factor(j),
+                                               gram, static_cast<int*>(pl.status.p), ctx->stream);
+    if (j == pl.N) comm_allreduce(ctx, gram, static_cast<int64_t>(R) * R, "als_sweep_sharded");
+  });
+  // [A_N | G(N)] at the slab offset, zeros elsewhere, summed: whole A_N and G(N)
+  c.xbuf.ensure(static_cast<size_t>(2 * IN * R) * sizeof(double));
+  double* x = c.xbuf.d();
+  CK(cudaMemsetAsync(x, 0, static_cast<size_t>(2 * IN * R) * sizeof(double), ctx->stream));
+  const size_t pitch = static_cast<size_t>(IN) * sizeof(double), w = static_cast<size_t>(rows) * sizeof(double);
+  CK(cudaMemcpy2DAsync(x + g.lo, pitch, pl.factor(pl.N), w, w, static_cast<size_t>(R), cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  CK(cudaMemcpy2DAsync(x + IN * R + g.lo, pitch, pl.Gorig.d() + pl.off_orig[pl.N - 1], w, w, static_cast<size_t>(R),
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+  comm_allreduce(ctx, x, 2 * IN * R, "als_sweep_sharded");
+  if (cost_slot)
+    ctx->launches += cpdgpu::launch_als_cost(x, x + IN * R, IN, R, pl.grams.d(), pl.N, pl.norm.d(), cost_slot,
+                                             ctx->stream);
+}
+
+// Every rank reports the same outcome: a NumericError (status 4, or the int8
+// budget fault) on any rank fails the call on all of them.
+void sharded_agree(cpdgpu_ctx* ctx, Plan& pl) {
+  int st = 0;
+  CK(cudaMemcpyAsync(&st, pl.status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  const int st = c.host_fn(c.user, c.hbuf.d(), g.total);
-  if (st != 0) fail(st > 0 ? st : CPDGPU_CUDA_ERROR, "cp_gradient_all_sharded: host all-reduce failed (%d)", st);
-  CK(cudaMemcpyAsync(out_dev, c.hbuf.p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const int fault = *ctx->fault_host;
+  Comm& c = *ctx->comm;
+  c.lbuf.ensure(2 * sizeof(double));
+  const double flags[2] = {st == 4 ? 1.0 : 0.0, fault != 0 ? 1.0 : 0.0};
+  CK(cudaMemcpyAsync(c.lbuf.p, flags, sizeof(flags), cudaMemcpyHostToDevice, ctx->stream));
+  comm_allreduce(ctx, c.lbuf.d(), 2, "als_sweep_sharded");
+  double any[2] = {0.0, 0.0};
+  CK(cudaMemcpyAsync(any, c.lbuf.p, sizeof(any), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (fault) return;  // guarded() reports this rank's own fault
+  if (st == 4) fail(CPDGPU_NUMERIC_ERROR, "als_update_mode: non-finite gradient input");
+  if (any[0] > 0.0) fail(CPDGPU_NUMERIC_ERROR, "als_sweep_sharded: non-finite gradient input on another rank");
+  if (any[1] > 0.0)
+    fail(CPDGPU_NUMERIC_ERROR, "als_sweep_sharded: another rank's seed pass failed its check; this sweep is invalid");
+}
+
+void sharded_als_download(cpdgpu_ctx* ctx, Plan& pl, const ShardGeom& g, double* const* factors) {
+  Comm& c = *ctx->comm;
+  const int64_t R = pl.R, IN = g.gdims[pl.N - 1];
+  scatter_factors(ctx, pl, pl.Forig.d());
+  CK(cudaMemcpyAsync(pl.hF.d(), pl.Forig.d(), static_cast<size_t>(pl.total_factor) * sizeof(double),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(factors[pl.N - 1], c.xbuf.d(), static_cast<size_t>(IN * R) * sizeof(double),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int m = 0; m + 1 < pl.N; ++m)
+    std::memcpy(factors[m], pl.hF.d() + pl.off_orig[m], static_cast<size_t>(g.gdims[m] * R) * sizeof(double));
 }
 
 }  // namespace
@@ -3379,6 +3477,102 @@ int cpdgpu_cp_gradient_all_sharded(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, 
     CK(cudaStreamSynchronize(ctx->stream));
     if (mults)
       for (int m = 0; m < N; ++m) mults[m] = count_realized(g.gdims, R, m + 1);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// max_iters sharded sweeps (run(), als.cpp:147-210, Algorithm::als_fast) with the
+// per-sweep costs in pl.costs; returns the number of sweeps done
+int sharded_als_loop(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, const ShardGeom& g, int64_t R,
+                     double* const* factors, int max_iters, double tol, double rtol, double* sec_trace) {
+  if (R > 64) fail(CPDGPU_ARGUMENT_ERROR, "als_sweep_sharded: rank above the device ALS limit 64");
+  if (rtol < 0.0 || tol < 0.0) fail(CPDGPU_ARGUMENT_ERROR, "als_sweep_sharded: tolerances must be nonnegative");
+  if (!factors) fail(CPDGPU_ARGUMENT_ERROR, "als_sweep_sharded: null factor list");
+  Plan& pl = *get_plan(ctx, slab, R, g.pivot);
+  bind_seed_inputs(ctx, pl, slab);
+  sharded_als_prepare(ctx, pl, slab, g, factors);
+  if (pl.i8.tensor_ok) {
+    std::vector<const double*> mf(pl.N);
+    for (int m = 0; m < pl.N; ++m) mf[m] = pl.hF.d() + pl.off_orig[m];
+    i8_apply_factor_guard(pl, i8_factors_ok_host(pl, mf.data(), true, i8_factor_limit(slab)));
+  }
+  pl.costs.ensure(static_cast<size_t>(max_iters) * sizeof(double));
+  std::vector<cudaEvent_t> ev(sec_trace ? 2 * static_cast<size_t>(max_iters) : 0);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  struct Free {
+    std::vector<cudaEvent_t>& v;
+    ~Free() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } free_events{ev};
+  double prev = std::nan("");
+  int done = 0;
+  for (int it = 1; it <= max_iters; ++it) {
+    if (sec_trace) CK(cudaEventRecord(ev[2 * (it - 1)], ctx->stream));
+    sharded_als_sweep(ctx, pl, g, rtol, pl.costs.d() + (it - 1));
+    if (sec_trace) CK(cudaEventRecord(ev[2 * (it - 1) + 1], ctx->stream));
+    ++done;
+    if (tol > 0.0) {  // the cost is global, so every rank stops at the same sweep
+      double d = 0.0;
+      CK(cudaMemcpyAsync(&d, pl.costs.d() + (it - 1), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (it > 1 && std::abs(d - prev) / std::max(prev, 1e-15) < tol) break;
+      prev = d;
+    }
+  }
+  sharded_agree(ctx, pl);
+  for (int i = 0; sec_trace && i < done; ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+    sec_trace[i] = ms * 1e-3;
+  }
+  sharded_als_download(ctx, pl, g, factors);
+  return done;
+}
+
+uint64_t als_sweep_count(const std::vector<int64_t>& dims, int64_t R) {
+  uint64_t tot = 0;
+  for (int j = 1; j <= static_cast<int>(dims.size()); ++j) tot += count_realized(dims, R, j);
+  return tot;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cpdgpu_als_sweep_sharded(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims, int64_t R,
+                             double* const* factors, double pinv_rtol, double* cost_out, uint64_t* mults) {
+  return guarded(ctx, [&] {
+    const ShardGeom g = shard_geometry(ctx, slab, N, global_dims, R, "als_sweep_sharded");
+    sharded_als_loop(ctx, slab, g, R, factors, 1, 0.0, pinv_rtol, nullptr);
+    Plan& pl = *get_plan(ctx, slab, R, g.pivot);
+    if (cost_out) CK(cudaMemcpy(cost_out, pl.costs.d(), sizeof(double), cudaMemcpyDeviceToHost));
+    if (mults) *mults = als_sweep_count(g.gdims, R);
+  });
+}
+
+int cpdgpu_als_run_sharded(cpdgpu_ctx* ctx, cpdgpu_tensor* slab, int N, const int64_t* global_dims, int64_t R,
+                           double* const* factors, int max_iters, double tol, double pinv_rtol, double* cost_trace,
+                           double* rel_trace, double* sec_trace, uint64_t* mults_trace, int* iters_run) {
+  return guarded(ctx, [&] {
+    const ShardGeom g = shard_geometry(ctx, slab, N, global_dims, R, "run_sharded");
+    if (max_iters < 1) fail(CPDGPU_ARGUMENT_ERROR, "run_sharded: max_iters must be at least 1");
+    if (!cost_trace || !rel_trace || !iters_run) fail(CPDGPU_ARGUMENT_ERROR, "run_sharded: null argument");
+    const int done = sharded_als_loop(ctx, slab, g, R, factors, max_iters, tol, pinv_rtol, sec_trace);
+    Plan& pl = *get_plan(ctx, slab, R, g.pivot);
+    double ynorm2 = 0.0;
+    CK(cudaMemcpy(&ynorm2, pl.norm.d(), sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cost_trace, pl.costs.d(), static_cast<size_t>(done) * sizeof(double), cudaMemcpyDeviceToHost));
+    const double ynorm = std::sqrt(ynorm2);
+    const uint64_t per_sweep = als_sweep_count(g.gdims, R);
+    for (int i = 0; i < done; ++i) {
+      rel_trace[i] = ynorm > 0.0 ? std::sqrt(cost_trace[i]) / ynorm : std::sqrt(cost_trace[i]);
+      if (mults_trace) mults_trace[i] = per_sweep * static_cast<uint64_t>(i + 1);
+    }
+    *iters_run = done;
   });
 }
 

@@ -395,6 +395,14 @@ void test_helpers_and_sharded() {
   auto gpl = cpd::cp_gradient_all(ya, fa, &cp);
   for (int k = 0; k < 4; ++k) CHECK_LT(max_rel_diff(gsh[static_cast<size_t>(k)], gpl[static_cast<size_t>(k)]), 1e-13);
   CHECK(cs.total() == cp.total());
+  // sharded ALS sweep, world size 1: equals the plain sweep
+  cpd::FactorList fs = fa, fp = fa;
+  cpd::CostCounter ss, sp;
+  const double cost = cpd::als_sweep_fast_sharded(ya, ya.shape(), fs, 1e-12, &ss);
+  cpd::als_sweep_fast(ya, fp, 1e-12, &sp);
+  for (int k = 0; k < 4; ++k) CHECK_LT(max_rel_diff(fs[static_cast<size_t>(k)], fp[static_cast<size_t>(k)]), 1e-11);
+  CHECK(ss.total() == sp.total());
+  CHECK(cost >= 0.0);
   cpd::gpu::comm_destroy();
   CHECK(throws<cpd::ArgumentError>([&] { cpd::cp_gradient_all_sharded(ya, ya.shape(), fa); }));  // no communicator
 }

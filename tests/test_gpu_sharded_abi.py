@@ -118,3 +118,74 @@ def test_sharded_single_rank_is_the_plain_gradient(gpu_ctx, oracle):
             cpd.cp_gradient_all_sharded(y, [5, 6, 7, 9], [np.ones((d, R)) for d in [5, 6, 7, 9]])
     finally:
         comm.close()
+
+
+def _als_worker(rank, world, port, dims, R, iters, f32, out_q):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    sys.path.insert(0, str(root / "oracle"))
+    import torch.distributed as dist
+    import oracle as O
+    import paper_1204_1586_b200 as cpd
+    from paper_1204_1586_b200 import sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = cpd.Context(0)
+        comm = sharded.library_comm(ctx, dist)
+        lo, hi = comm.bounds(dims[-1])
+        front = int(np.prod(dims[:-1]))
+        dist_kind = cpd.DIST_UNIFORM_PM1 if f32 else cpd.DIST_NORMAL
+        dt = cpd.F32 if f32 else cpd.F64
+        y = cpd.DenseTensor.generate(list(dims[:-1]) + [hi - lo], dist_kind, seed=13, ctx=ctx, offset=lo * front,
+                                     dtype=dt)
+        init = cpd.random_init(dims, R, 5)
+        fr = [f.copy(order="F") for f in init]
+        trace = cpd.als_run_sharded(y, dims, fr, max_iters=iters)
+        fs = [f.copy(order="F") for f in init]
+        counter = cpd.CostCounter()
+        c1 = cpd.als_sweep_sharded(y, dims, fs, counter=counter)
+        comm.close()
+        full = cpd.DenseTensor.generate(list(dims), dist_kind, seed=13, ctx=ctx, dtype=dt)
+        yv = full.values().astype(np.float64)
+        of, ot = O.run_als_fast(yv, dims, init, max_iters=iters)
+        o1 = O.als_sweep_fast(yv, dims, [f.copy(order="F") for f in init])
+        ferr = max(float(np.max(np.abs(a - b)) / np.max(np.abs(b))) for a, b in zip(fr, of))
+        cerr = max(abs(a - b) / b for a, b in zip(trace.cost, ot["cost"]))
+        serr = max(float(np.max(np.abs(a - b)) / np.max(np.abs(b))) for a, b in zip(fs, o1))
+        c1err = abs(c1 - O.cost(yv, dims, o1)) / c1
+        want_mults = sum(cpd.fast_count_realized(dims, R, n) for n in range(1, len(dims) + 1))
+        digest = float(sum(np.sum(f * (k + 1)) for k, f in enumerate(fr)))
+        out_q.put((rank, trace.iters_run, ferr, cerr, serr, c1err, counter.total() == want_mults, digest))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims,R,f32", [([6, 7, 8, 9], 5, False), ([12, 14, 16, 20], 12, False),
+                                        ([5, 6, 7], 3, False), ([16, 16, 16, 17], 8, True)])
+def test_sharded_als_matches_oracle(dims, R, f32):
+    """Sharded fast ALS (cpdgpu_als_run_sharded / cpdgpu_als_sweep_sharded) over two
+    last-mode slabs against the oracle's unsharded run on the whole tensor
+    (als.cpp:69-78, 147-210): same Gauss-Seidel order, so the factors and the
+    cost trace agree to summation order; both ranks hold identical factors."""
+    world, iters = 2, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_als_worker, args=(r, world, port, dims, R, iters, f32, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    tol = 1e-4 if f32 else 1e-9  # ALS amplifies the gradient's rounding by the Gram conditioning
+    for rank, done, ferr, cerr, serr, c1err, counted, _ in res:
+        assert done == iters
+        assert ferr <= tol and serr <= tol, (rank, ferr, serr)
+        assert cerr <= tol and c1err <= tol, (rank, cerr, c1err)
+        assert counted
+    assert res[0][-1] == res[1][-1]  # every rank leaves with the same factors
