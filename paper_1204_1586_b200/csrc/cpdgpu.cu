@@ -1116,6 +1116,16 @@ cudaEvent_t seed_event(cpdgpu_ctx* ctx) {
 // The Khatri-Rao rows must already be in the chunks' KRr / KRl buffers.
 // fp32 seeds: Khatri-Rao column scales and split tiles from the sorted factors
 // (Fs), then one tcgen05 pass per requested side.
+// CPDGPU_F32_LRED=1: the fused fp32 seed's drains add their left partials into one
+// band slot with red.global.add (L2) instead of storing one slot per band
+bool f32_left_red() {
+  static const bool on = [] {
+    const char* e = std::getenv("CPDGPU_F32_LRED");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) {
   cudaStream_t s = ctx->stream;
   const int RPc = cpdgpu::seed_f32_rank_cols();
@@ -1142,6 +1152,10 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
     q.window = pl.ff.window;
     static const char* knob_env = std::getenv("CPDGPU_F32F_KNOBS");
     q.knobs = knob_env ? std::atoi(knob_env) : 0;
+    if (pl.ff.img_on && f32_left_red()) {  // one band slot, summed in L2 by the drains
+      q.knobs |= 512;
+      CK(cudaMemsetAsync(pl.ff.lpart32.p, 0, static_cast<size_t>(pl.ff.nC) * 64 * 64 * sizeof(float), s));
+    }
     q.fault = ctx->fault_dev;
     q.stall = force_stall();
     q.watchdog = watchdog_on(q.stall);
@@ -1793,7 +1807,7 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
     const Plan::Chunk& c = pl.chunks[0];
     const int RPc = cpdgpu::seed_f32_rank_cols();
     ctx->launches += cpdgpu::launch_reduce_left32(
-        static_cast<const float*>(pl.ff.lpart32.p), pl.ff.nB, pl.ff.nC, pl.Kp, c.Rc,
+        static_cast<const float*>(pl.ff.lpart32.p), pl.ff.img_on && f32_left_red() ? 1 : pl.ff.nB, pl.ff.nC, pl.Kp, c.Rc,
         reinterpret_cast<const double*>(static_cast<const char*>(pl.tensor->yscale.p) + 8), c.scales->d() + 3 * RPc,
         gN_direct ? nullptr : pl.Ls.d(), static_cast<double* const*>(pl.gtab.p), gN_direct ? pl.perm[pl.N - 1] - 1 : -1,
         pl.Kp, ctx->stream);

@@ -922,6 +922,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
     const int odd = lane & 1;
     const bool lstore = !(p.knobs & 8);
+    const bool lred = (p.knobs & 512) != 0;  // left partials summed in L2 (red.add) into band slot 0
     float acc[kRP];
 #pragma unroll
     for (int e = 0; e < kRP; ++e) acc[e] = 0.0f;
@@ -980,7 +981,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
       __syncwarp();
       tc_fence_after();
       const int r = 16 * q + (lane >> 1);
-      float* lrow = p.lpart + ((static_cast<int64_t>(b) * w.nC + c) * kRP + r) * kTJ + 4 * odd;
+      float* lrow = p.lpart + ((static_cast<int64_t>(lred ? 0 : b) * w.nC + c) * kRP + r) * kTJ + 4 * odd;
 #pragma unroll
       for (int c8 = t; c8 < kTJ / 8; c8 += kA) {
         if (p.knobs & 64) break;
@@ -996,7 +997,12 @@ __global__ void __launch_bounds__(kIThreads, 1)
           const float give = __uint_as_float(odd ? v[e] : v[4 + e]);
           o[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
         }
-        if (lstore) *reinterpret_cast<float4*>(lrow + 8 * c8) = make_float4(o[0], o[1], o[2], o[3]);
+        if (lred)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(lrow + 8 * c8), "f"(o[0]), "f"(o[1]),
+                       "f"(o[2]), "f"(o[3])
+                       : "memory");
+        else if (lstore)
+          *reinterpret_cast<float4*>(lrow + 8 * c8) = make_float4(o[0], o[1], o[2], o[3]);
       }
       tc_fence_before();
       __syncwarp();
