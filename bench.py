@@ -469,7 +469,26 @@ def cpu_gradient_sample(args, cfg, steps=None, warmup=1):
         n = int(np.prod(sd))
         y = O.fill_normal(1, n, nthreads=cores)
     f = [O.fill_normal(100 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(sd)]
+    single = None
     if ref is not None:
+        # single-core figure: the reference as built, one thread,
+        # one call on the whole fp64 tensor (c5: one 300^3 slab of the sample)
+        if dtype == "f32":
+            sd1 = [1] + list(sd[1:])
+            y1 = np.ascontiguousarray(y.reshape(sd, order="F")[:1].reshape(-1, order="F"))
+            f1 = [np.asfortranarray(f[0][:1])] + f[1:]
+        else:
+            sd1, y1, f1 = sd, y, f
+        t1 = ref.Tensor(y1, sd1, parts=1)
+        if y1.size * 8 <= (256 << 20):
+            t1.cp_gradient_all(f1)
+        s1 = t1.time_cp_gradient_all(f1, 1)
+        t1.close()
+        del y1
+        single = {"value": int(np.prod(sd1)) * esize / s1 / 1e9, "unit": "GB/s", "cores": 1,
+                  "ms_per_step": s1 * 1e3,
+                  "sample": f"one call of the reference's cp_gradient_all on the {'x'.join(map(str, sd1))} fp64 "
+                            "tensor, one thread"}
         t = ref.Tensor(y, sd, parts=min(cores, sd[0]), axis=0)
         del y
         for _ in range(warmup):
@@ -494,7 +513,7 @@ def cpu_gradient_sample(args, cfg, steps=None, warmup=1):
     what = "full" if sd == list(dims) else f"{'x'.join(map(str, sd))} sample ({dtype} values upcast to fp64) of the"
     return {"value": n * esize / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
             "sample": f"{reps} x {what} {args.config} gradient, {how}", "ms_per_step": dt * 1e3, "steps": reps,
-            "host_cores": cores}
+            "host_cores": cores, "single_core": single}
 
 
 def cpu_baseline(args, cfg, ydev=None):

@@ -32,6 +32,7 @@ SIGNATURES = {
     "cpdgpu_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cpdgpu_synchronize": (C.c_int, [C.c_void_p]),
     "cpdgpu_set_graphs": (C.c_int, [C.c_void_p, C.c_int]),
+    "cpdgpu_set_deterministic": (C.c_int, [C.c_void_p, C.c_int]),
     "cpdgpu_launch_count": (c_u64, [C.c_void_p]),
     "cpdgpu_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "cpdgpu_last_seed_ms": (C.c_int, [C.c_void_p, c_dbl_p]),

@@ -85,6 +85,15 @@ class Context:
     def set_timing(self, enabled: bool) -> None:
         _lib.check(self._L.cpdgpu_set_timing(self.h, int(bool(enabled))), self.h)
 
+    def set_graphs(self, enabled: bool) -> None:
+        _lib.check(self._L.cpdgpu_set_graphs(self.h, int(bool(enabled))), self.h)
+
+    def set_deterministic(self, enabled: bool) -> None:
+        """Bitwise-reproducible results run to run (cpdgpu_set_deterministic): only
+        the fused fp32 gradient changes (its left partials summed in a fixed order
+        instead of by red.add in L2)."""
+        _lib.check(self._L.cpdgpu_set_deterministic(self.h, int(bool(enabled))), self.h)
+
     def last_seed_path(self) -> int:
         """0: fp64 DMMA seed pass, 1: fused int8 tensor-core pass, 2: fp32 pass."""
         return int(self._L.cpdgpu_last_seed_path(self.h))

@@ -319,6 +319,7 @@ struct Plan {
     // the tensor's fp16 hi / lo operand image (built once per tensor version; the
     // kernel then has no split stage); off when it does not fit in memory
     bool img_on = false, img_failed = false;
+    bool lred = false;  // left partials added in L2 (red.add) into one band slot
     void* img = nullptr;
     CUtensorMap imap{};
     uint64_t img_version = ~0ull;
@@ -425,6 +426,11 @@ struct cpdgpu_ctx {
   cudaStream_t own = nullptr, stream = nullptr;
   std::string err;
   bool graphs = true;
+  // bitwise-reproducible results (cpdgpu_set_deterministic / CPDGPU_DETERMINISTIC=1)
+  bool deterministic = [] {
+    const char* e = std::getenv("CPDGPU_DETERMINISTIC");
+    return e && e[0] == '1';
+  }();
   uint64_t launches = 0;
   int last_seed_path = 0;  // cpdgpu_last_seed_path
   uint64_t next_id = 1;
@@ -888,7 +894,14 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gra
       CK(cudaGetLastError());
       ff.img_version = t->version;
     }
-    if (ff.img_on) return;
+    if (ff.img_on) {
+      // left partials: summed in L2 by red.add (fast; the fp32 addition order varies
+      // run to run) unless the context asks for bitwise-reproducible results
+      const bool lred = !ctx->deterministic;
+      if (lred != ff.lred) pl.drop_graphs();
+      ff.lred = lred;
+      return;
+    }
   }
   const void* base = src;
   if (pl.J8 != pl.Jp) {
@@ -1116,16 +1129,6 @@ cudaEvent_t seed_event(cpdgpu_ctx* ctx) {
 // The Khatri-Rao rows must already be in the chunks' KRr / KRl buffers.
 // fp32 seeds: Khatri-Rao column scales and split tiles from the sorted factors
 // (Fs), then one tcgen05 pass per requested side.
-// CPDGPU_F32_LRED=1: the fused fp32 seed's drains add their left partials into one
-// band slot with red.global.add (L2) instead of storing one slot per band
-bool f32_left_red() {
-  static const bool on = [] {
-    const char* e = std::getenv("CPDGPU_F32_LRED");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) {
   cudaStream_t s = ctx->stream;
   const int RPc = cpdgpu::seed_f32_rank_cols();
@@ -1152,7 +1155,7 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
     q.window = pl.ff.window;
     static const char* knob_env = std::getenv("CPDGPU_F32F_KNOBS");
     q.knobs = knob_env ? std::atoi(knob_env) : 0;
-    if (pl.ff.img_on && f32_left_red()) {  // one band slot, summed in L2 by the drains
+    if (pl.ff.img_on && pl.ff.lred) {  // one band slot, summed in L2 by the drains
       q.knobs |= 512;
       CK(cudaMemsetAsync(pl.ff.lpart32.p, 0, static_cast<size_t>(pl.ff.nC) * 64 * 64 * sizeof(float), s));
     }
@@ -1807,7 +1810,7 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
     const Plan::Chunk& c = pl.chunks[0];
     const int RPc = cpdgpu::seed_f32_rank_cols();
     ctx->launches += cpdgpu::launch_reduce_left32(
-        static_cast<const float*>(pl.ff.lpart32.p), pl.ff.img_on && f32_left_red() ? 1 : pl.ff.nB, pl.ff.nC, pl.Kp, c.Rc,
+        static_cast<const float*>(pl.ff.lpart32.p), pl.ff.img_on && pl.ff.lred ? 1 : pl.ff.nB, pl.ff.nC, pl.Kp, c.Rc,
         reinterpret_cast<const double*>(static_cast<const char*>(pl.tensor->yscale.p) + 8), c.scales->d() + 3 * RPc,
         gN_direct ? nullptr : pl.Ls.d(), static_cast<double* const*>(pl.gtab.p), gN_direct ? pl.perm[pl.N - 1] - 1 : -1,
         pl.Kp, ctx->stream);
@@ -2406,6 +2409,12 @@ int cpdgpu_synchronize(cpdgpu_ctx* ctx) {
 int cpdgpu_set_graphs(cpdgpu_ctx* ctx, int enabled) {
   if (!ctx) return CPDGPU_ARGUMENT_ERROR;
   ctx->graphs = enabled != 0;
+  return CPDGPU_OK;
+}
+
+int cpdgpu_set_deterministic(cpdgpu_ctx* ctx, int enabled) {
+  if (!ctx) return CPDGPU_ARGUMENT_ERROR;
+  ctx->deterministic = enabled != 0;
   return CPDGPU_OK;
 }
 
