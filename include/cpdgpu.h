@@ -66,11 +66,13 @@ int cpdgpu_synchronize(cpdgpu_ctx* ctx);
 /* 1 = capture the per-gradient launch sequence into a CUDA graph (default 1). */
 int cpdgpu_set_graphs(cpdgpu_ctx* ctx, int enabled);
 /* 1 = bitwise-reproducible results run to run (default 0; CPDGPU_DETERMINISTIC=1
- * sets the default).  Only the fused fp32 gradient differs: by default its
- * drains add the per-band left partials in L2 (red.add, fp32 order varies,
- * results within its ~1e-6 error); deterministic mode stores one slot per band
- * and sums them in a fixed order (c5: +0.9 ms per gradient).  The fp64 paths
- * are always deterministic. */
+ * sets the default).  Two seed passes differ: by default the drains of the
+ * fused fp32 seed and of the int8 fp64 seed add their per-band / per-row-block
+ * left partials in L2 (red.add; the addition order varies, so repeats differ in
+ * the last bits: ~1e-7 relative for fp32, ~1e-16 for fp64); deterministic mode
+ * stores one partial slot per band / row block and sums them in a fixed order
+ * (c5: +0.9 ms per gradient).  The DMMA and split fp32 passes are always
+ * deterministic. */
 int cpdgpu_set_deterministic(cpdgpu_ctx* ctx, int enabled);
 /* Kernels launched by this context so far (evidence counter for bench.py). */
 uint64_t cpdgpu_launch_count(const cpdgpu_ctx* ctx);

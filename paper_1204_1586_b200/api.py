@@ -89,9 +89,9 @@ class Context:
         _lib.check(self._L.cpdgpu_set_graphs(self.h, int(bool(enabled))), self.h)
 
     def set_deterministic(self, enabled: bool) -> None:
-        """Bitwise-reproducible results run to run (cpdgpu_set_deterministic): only
-        the fused fp32 gradient changes (its left partials summed in a fixed order
-        instead of by red.add in L2)."""
+        """Bitwise-reproducible results run to run (cpdgpu_set_deterministic): the
+        fused fp32 and int8 fp64 seeds then sum their left partials in a fixed
+        order instead of by red.add in L2."""
         _lib.check(self._L.cpdgpu_set_deterministic(self.h, int(bool(enabled))), self.h)
 
     def last_seed_path(self) -> int:

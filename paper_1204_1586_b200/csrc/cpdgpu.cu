@@ -297,6 +297,9 @@ struct Plan {
     DevBuf tab;
     int tab_len = 0, tab_max = 0;
     bool lpart_direct = false;
+    // left partials added in L2 (red.add.f64) into one row-block slot (not in
+    // deterministic mode): the tail then reads one partial instead of nRB
+    bool lred = false;
   } i8;
   HostBuf hF, hG;
   // fp32 tensors: tcgen05 seed passes (seed_f32.cu), one per side
@@ -977,6 +980,9 @@ void bind_i8(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, const void* ybase) {
     pl.i8.ymap_base = on ? view : nullptr;
   }
   pl.i8.tensor_ok = on;
+  const bool lred = !ctx->deterministic && pl.i8.nRB > 1;
+  if (lred != pl.i8.lred) pl.drop_graphs();
+  pl.i8.lred = lred;
   set_i8_on(pl);
 }
 
@@ -1285,6 +1291,7 @@ void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
   q.stall = force_stall();
   q.watchdog = watchdog_on(q.stall);
   q.Lpart = g.nRB == 1 ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d() + c.lpart_off;
+  q.lred = g.lred ? 1 : 0;  // slot 0 zeroed by this gradient's prologue
   static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
   DevBuf tb;
   if (trace) {
@@ -1556,7 +1563,7 @@ void add_reduce_ops(const Plan& pl, cpdgpu::TailStep& st, int mode) {
       cpdgpu::TailOp o = op_base(cpdgpu::kOpReduceLeft, c.Rc);
       o.Z = pl.Lpart.d() + c.lpart_off;
       o.M = pl.Kp;
-      o.B = c.sp.nRB;
+      o.B = pl.i8.on && pl.i8.lred ? 1 : c.sp.nRB;
       o.out = pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp;
       o.ldo = pl.Kp;
       st.op[st.n++] = o;
@@ -1753,7 +1760,7 @@ int build_l0(cpdgpu_ctx* ctx, Plan& pl, cpdgpu::L0Step& l0, bool& fuse_r, bool& 
     } else {
       sd.zsrc = 2;
       sd.Z = pl.Lpart.d() + c.lpart_off;
-      sd.pcount = static_cast<int>(c.sp.nRB);
+      sd.pcount = pl.i8.on && pl.i8.lred ? 1 : static_cast<int>(c.sp.nRB);
       sd.pK = pl.Kp;
       sd.ldz = static_cast<int64_t>(R) * pl.Kp;
     }
@@ -1942,6 +1949,10 @@ void run_gradient(cpdgpu_ctx* ctx, Plan& pl, const double* fin, double* gout_bas
   const bool own_kr = pl.i8.on || (pl.f32 && left && pl.ff.on);
   cpdgpu::Prologue pr = grad_prologue(pl, fin, gout_base, own_kr ? 0 : (left ? 3 : 1));
   pr.tl = ctx->tl_ptr();
+  if (pl.i8.on && pl.i8.lred) {  // the int8 seed adds its left partials into this slot
+    pr.zero = pl.Lpart.d() + pl.chunks[0].lpart_off;
+    pr.zero_n = pl.chunks[0].Rc * pl.Kp;
+  }
   timeline_reset(ctx);
   struct PrintAtExit {
     cpdgpu_ctx* c;

@@ -78,6 +78,7 @@ struct SeedI8Params {
   unsigned* progress;  // CPDGPU_I8_DEBUG: [P][16] per-warp positions for the watchdog report
   unsigned long long* trace;  // CPDGPU_SEED_TRACE: [P][14][6] per-warp wait cycles, total, tiles
   int knobs;                  // CPDGPU_I8_KNOBS experiments (bit 0: no digit stores)
+  int lred;                   // left partials red.add'ed into row-block slot 0 (zeroed by the host)
   int* fault;                 // context fault word: the watchdog's report (no trap)
   int stall;                  // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
   int watchdog;               // bounded barrier waits (CPDGPU_WATCHDOG=1; implied by stall)
@@ -288,6 +289,8 @@ struct Prologue {
   int nkr;
   KRJob kr[kMaxKRJobs];
   unsigned long long* tl = nullptr;  // launch timeline (CPDGPU_TIMELINE), slot 0
+  double* zero = nullptr;            // zeroed here: the int8 seed's red.add left-partial slot
+  int64_t zero_n = 0;
 };
 int launch_prologue(const Prologue& pr, double** gtab, int num_sms, cudaStream_t s);
 const void* prologue_kernel_fn();

@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       tc_fence_after();
       const double* wl = p.w_l + rb * N;
       const int64_t j = ct * 128 + row;  // M = 128: TMEM lane = column
-      double* lout = p.Lpart + rb * static_cast<int64_t>(p.R) * p.K + j;
+      double* lout = p.Lpart + (p.lred ? 0 : rb) * static_cast<int64_t>(p.R) * p.K + j;
 #pragma unroll
       for (int rc = 0; rc < (NL + 7) / 8; ++rc) {
         if (rc * 8 >= p.R || (p.knobs & 4)) break;
@@ -613,7 +613,12 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         for (int e = 0; e < 8; ++e) {
           const double h = horner6(d[0][e], d[1][e], d[2][e], d[3][e], d[4][e], d[5][e]);
           const int r = rc * 8 + e;
-          if (r < p.R && j < p.K) lout[static_cast<int64_t>(r) * p.K] = h * __ldg(wl + r);
+          if (r < p.R && j < p.K) {
+            if (p.lred)
+              atomicAdd(lout + static_cast<int64_t>(r) * p.K, h * __ldg(wl + r));  // red.global.add.f64 (L2)
+            else
+              lout[static_cast<int64_t>(r) * p.K] = h * __ldg(wl + r);
+          }
         }
       }
       tc_fence_before();

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(256) prologue_kernel(const Prologue pr, double
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
   if (t < kMaxModes && t < pr.N) gtab[t] = pr.gout[t];
+  for (int64_t e = t; e < pr.zero_n; e += nt) pr.zero[e] = 0.0;
   if (pr.Fs)
     for (int j = 0; j < pr.N; ++j)
       for (int64_t e = t; e < pr.len[j]; e += nt) pr.Fs[pr.dst_off[j] + e] = pr.fin[pr.src_off[j] + e];
@@ -511,6 +512,7 @@ void prologue_geometry(const Prologue& pr, int num_sms, dim3* grid, dim3* block)
   int64_t work = 0;
   for (int j = 0; j < pr.N; ++j) work = work > pr.len[j] ? work : pr.len[j];
   for (int c = 0; c < pr.nkr; ++c) work = work > pr.kr[c].L * pr.kr[c].LDK ? work : pr.kr[c].L * pr.kr[c].LDK;
+  work = work > pr.zero_n / 4 ? work : pr.zero_n / 4;
   *grid = dim3(static_cast<unsigned>(grid_for(work, 256, num_sms * 8)));
   *block = dim3(256);
 }

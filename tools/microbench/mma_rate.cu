@@ -80,7 +80,10 @@ int main() {
       {"SS M128 N128 A mn", 0, 128, 128, true, false}, {"SS M128 N256 A mn", 0, 128, 256, true, false},
       {"TS M128 N64      ", 1, 128, 64, false, false}, {"TS M128 N128     ", 1, 128, 128, false, false},
       {"TS M128 N256     ", 1, 128, 256, false, false}, {"TS M128 N64 B mn ", 1, 128, 64, false, true},
-      {"TS M128 N128 B mn", 1, 128, 128, false, true},
+      {"TS M128 N128 B mn", 1, 128, 128, false, true}, {"SS M64 N64   A k ", 0, 64, 64, false, false},
+      {"TS M64 N64       ", 1, 64, 64, false, false},  {"TS M64 N128      ", 1, 64, 128, false, false},
+      {"SS M128 N128 A k ", 0, 128, 128, false, false}, {"SS M128 N32  A k ", 0, 128, 32, false, false},
+      {"TS M128 N32      ", 1, 128, 32, false, false},
   };
   for (int grid : {1, 148}) {
     for (auto& c : cs) {
