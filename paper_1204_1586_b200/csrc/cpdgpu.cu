@@ -858,6 +858,16 @@ Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
   return raw;
 }
 
+// Operand image layout of the fused fp32 seed: 64-row chunks of the columns side
+// by side (CPDGPU_F32_IMG_CHUNK=1) or whole columns (0)
+int f32_image_chunked() {
+  static const int v = [] {
+    const char* e = std::getenv("CPDGPU_F32_IMG_CHUNK");
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : 0;
+  }();
+  return v;
+}
+
 // fp32: power-of-two Y scale (cached per tensor version), then either the fp16
 // operand image (hook-free gradients on the fused pass: the only view that pass
 // reads) or the split passes' view: rows padded to J8 when needed and the two 3-D
@@ -884,7 +894,7 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gra
         cudaGetLastError();  // out of memory: keep the split-in-kernel path
         ff.img = nullptr;
         ff.img_failed = true;
-      } else if (!cpdgpu::make_tensor_map_f16_image(&ff.imap, ff.img, pl.Jp, pl.Kp)) {
+      } else if (!cpdgpu::make_tensor_map_f16_image(&ff.imap, ff.img, pl.Jp, pl.Kp, f32_image_chunked())) {
         cudaFree(ff.img);
         ff.img = nullptr;
         ff.img_failed = true;
@@ -893,7 +903,7 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gra
     ff.img_on = ff.img != nullptr;
     if (ff.img_on && ff.img_version != t->version) {
       ctx->launches += cpdgpu::launch_build_f16_image(src, pl.Jp, pl.Jp, pl.Kp, static_cast<const float*>(t->yscale.p),
-                                                      ff.img, ctx->num_sms, ctx->stream);
+                                                      ff.img, ctx->num_sms, f32_image_chunked(), ctx->stream);
       CK(cudaGetLastError());
       ff.img_version = t->version;
     }

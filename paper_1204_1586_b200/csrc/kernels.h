@@ -163,8 +163,8 @@ int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream
 // faster alone but made the fused pass 0.6 ms slower at c5: measured and dropped.)
 int64_t f16_image_ld(int64_t J);
 int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
-                           int num_sms, cudaStream_t s);
-bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K);
+                           int num_sms, int chunked, cudaStream_t s);
+bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K, int chunked);
 // fused pass: column scales, right B tiles and the KRl^T image straight from the
 // sorted factors (two launches, no fp64 Khatri-Rao rows)
 int launch_kr_fused_operands(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, double* scale,

@@ -641,12 +641,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ==================================================================================
 // timed wait (CPDGPU_SEED_TRACE): cycles spent waiting added to *acc
 template <bool WD>
+// acc == nullptr (no CPDGPU_SEED_TRACE): no clock reads on the pipeline's roles
 __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+  if (!acc) {
+    mbar_wait<WD>(bar, parity);
+    return;
+  }
   const long long t0 = clock64();
   mbar_wait<WD>(bar, parity);
   *acc += static_cast<unsigned long long>(clock64() - t0);
 }
 __device__ __forceinline__ void mbar_wait_plain_t(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+  if (!acc) {
+    mbar_wait_plain(bar, parity);
+    return;
+  }
   const long long t0 = clock64();
   mbar_wait_plain(bar, parity);
   *acc += static_cast<unsigned long long>(clock64() - t0);
@@ -680,6 +689,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     seed_f32i_kernel(const Seed32FParams p, const __grid_constant__ CUtensorMap imap) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x;
+  const bool trc = p.trace != nullptr;  // per-role wait timers (CPDGPU_SEED_TRACE)
   FWalk w;
   w.a = static_cast<int>(static_cast<int64_t>(cta) * p.units / p.P);
   w.b = static_cast<int>(static_cast<int64_t>(cta + 1) * p.units / p.P);
@@ -759,7 +769,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
       for (it.init(w); it.more() && !wd_aborted<WD>(); it.next()) {
         const int b = it.b, c = it.c, nt = it.nt;
         for (int t = 0; t < nt; ++t, ++k) {
-          if (k >= kINS) mbar_wait_t<WD>(&empty[s], ph ^ 1u, &tw);
+          if (k >= kINS) mbar_wait_t<WD>(&empty[s], ph ^ 1u, trc ? &tw : nullptr);
           if (wd_aborted<WD>()) break;  // watchdog: no new loads
           if ((p.knobs & 16) && k >= kINS) {  // timing experiment: no refill (stale planes)
             mbar_arrive(&full[s]);
@@ -773,9 +783,9 @@ __global__ void __launch_bounds__(kIThreads, 1)
 #pragma unroll
               for (int ih = 0; ih < 2; ++ih)
                 asm volatile(
-                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-                    " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(ring_u + s * 2 * kPlane + pl * kPlane + ih * 8192),
-                    "l"(reinterpret_cast<uint64_t>(&imap)), "r"(i0 + 64 * ih), "r"(j0), "r"(pl),
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                    " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;\n" ::"r"(ring_u + s * 2 * kPlane + pl * kPlane + ih * 8192),
+                    "l"(reinterpret_cast<uint64_t>(&imap)), "r"(0), "r"((i0 >> 6) + ih), "r"(j0), "r"(pl),
                     "r"(smem_u32(&full[s])), "l"(pol_y)
                     : "memory");
           }
@@ -831,9 +841,9 @@ __global__ void __launch_bounds__(kIThreads, 1)
       const int nt = it.nt;
       const int ks = ul & (kINK - 1), lb = ul & 1;
       const bool seg_end = it.seg_end();
-      if (it.band_start()) mbar_wait_t<WD>(kl_full, static_cast<uint32_t>(bc & 1), &tr[4]);
-      if (ul >= 2) mbar_wait_t<WD>(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1), &tr[1]);
-      mbar_wait_t<WD>(&kfull[ks], static_cast<uint32_t>((ul / kINK) & 1), &tr[2]);
+      if (it.band_start()) mbar_wait_t<WD>(kl_full, static_cast<uint32_t>(bc & 1), trc ? &tr[4] : nullptr);
+      if (ul >= 2) mbar_wait_t<WD>(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1), trc ? &tr[1] : nullptr);
+      mbar_wait_t<WD>(&kfull[ks], static_cast<uint32_t>((ul / kINK) & 1), trc ? &tr[2] : nullptr);
       tc_fence_after();
       const bool wstart = it.win_start(), wend = it.win_end();
       const uint64_t kb = dB0 + static_cast<uint64_t>((ks * kKRBytes) >> 4);
@@ -841,10 +851,11 @@ __global__ void __launch_bounds__(kIThreads, 1)
 #pragma unroll
       for (int t = 0; t < kA; ++t) {
         if (t >= nt) break;
-        if (wstart && wc[t] > 0) mbar_wait_t<WD>(&rempty[t], static_cast<uint32_t>((wc[t] - 1) & 1), &tr[3]);
-        mbar_wait_t<WD>(&full[s], ph, &tr[0]);
+        if (wstart && wc[t] > 0)
+          mbar_wait_t<WD>(&rempty[t], static_cast<uint32_t>((wc[t] - 1) & 1), trc ? &tr[3] : nullptr);
+        mbar_wait_t<WD>(&full[s], ph, trc ? &tr[0] : nullptr);
         tc_fence_after();
-        const long long ti = clock64();
+        const long long ti = trc ? clock64() : 0;
         const uint64_t pa = static_cast<uint64_t>((s * 2 * kPlane) >> 4);
         const uint64_t aH = dA0 + pa, aL = aH + (kPlane >> 4), lH = dL0 + pa, lL = lH + (kPlane >> 4);
         const uint32_t dR = tmem + kColR + kRP * t, aK = tmem + kColK + kRP * t;
@@ -871,7 +882,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
           if (wend) umma_commit(&rfull[t]);
         }
         __syncwarp();
-        tr[5] += static_cast<unsigned long long>(clock64() - ti);
+        if (trc) tr[5] += static_cast<unsigned long long>(clock64() - ti);
         if (wend) ++wc[t];
         ++k;
         if (++s == kINS) {
@@ -959,7 +970,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
         if (lane == 0) mbar_arrive(kl_full);
       }
       if (mine && it.win_end()) {  // right window -> fp32 second level
-        mbar_wait_plain_t(&rfull[t], static_cast<uint32_t>(wc & 1), &tr[0]);
+        mbar_wait_plain_t(&rfull[t], static_cast<uint32_t>(wc & 1), trc ? &tr[0] : nullptr);
         __syncwarp();
         tc_fence_after();
 #pragma unroll
@@ -977,7 +988,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
         ++wc;
       }
       // left: lane pairs (hi, lo) of rank 16 q + lane / 2, chunks t, t + 3, t + 6
-      mbar_wait_plain_t(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1), &tr[1]);
+      mbar_wait_plain_t(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1), trc ? &tr[1] : nullptr);
       __syncwarp();
       tc_fence_after();
       const int r = 16 * q + (lane >> 1);
@@ -1037,8 +1048,11 @@ __global__ void __launch_bounds__(kIThreads, 1)
 // Operand image of an fp32 tensor view (J rows, K columns, column-major, leading
 // dimension ldy): planes [2][K][LD] fp16, hi = fp16(s y), lo = fp16(s y - hi), rows
 // J..LD-1 zero; s = the tensor's power-of-two scale.  Two rows per thread.
+// chunked = 0: [2][K][LD] (column j: LD consecutive i); chunked = 1: [2][LD / 64][K][64]
+// (64-row chunks of every column side by side, so one 64 i x 64 j TMA box is 8 KB
+// of consecutive bytes instead of 64 rows 2 LD bytes apart)
 __global__ void build_f16_image_kernel(const float* __restrict__ y, int64_t J, int64_t ldy, int64_t K, int64_t LD,
-                                       const float* __restrict__ scale, __half2* __restrict__ img) {
+                                       const float* __restrict__ scale, __half2* __restrict__ img, int chunked) {
   const float sy = scale[0];
   const int64_t half = LD / 2, n = half * K, plane = n;  // in half2 units
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
@@ -1049,8 +1063,9 @@ __global__ void build_f16_image_kernel(const float* __restrict__ y, int64_t J, i
     const float b = i + 1 < J ? __ldcs(col + i + 1) * sy : 0.0f;
     const __half2 hi = __floats2half2_rn(a, b);
     const float2 back = __half22float2(hi);
-    __stcs(img + e, hi);
-    __stcs(img + plane + e, __floats2half2_rn(a - back.x, b - back.y));
+    const int64_t o = chunked ? ((i >> 6) * K * 64 + j * 64 + (i & 63)) / 2 : e;
+    __stcs(img + o, hi);
+    __stcs(img + plane + o, __floats2half2_rn(a - back.x, b - back.y));
   }
 }
 
@@ -1159,12 +1174,13 @@ int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream
 int64_t f16_image_ld(int64_t J) { return ceil_div(J, 64) * 64; }
 
 int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
-                           int num_sms, cudaStream_t s) {
-  build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, f16_image_ld(J), scale, static_cast<__half2*>(img));
+                           int num_sms, int chunked, cudaStream_t s) {
+  build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, f16_image_ld(J), scale, static_cast<__half2*>(img),
+                                                     chunked);
   return 1;
 }
 
-bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K) {
+bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K, int chunked) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -1176,12 +1192,17 @@ bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int
   }
   const int64_t LD = f16_image_ld(J);
   if ((reinterpret_cast<uintptr_t>(img) & 127) || K >= (1ll << 31) || LD >= (1ll << 31)) return false;
-  // [2 planes][K][LD] fp16; box 64 i (128 B, swizzled) x 64 j x 1 plane
-  const cuuint64_t gdim[3] = {static_cast<cuuint64_t>(LD), static_cast<cuuint64_t>(K), 2};
-  const cuuint64_t gstride[2] = {static_cast<cuuint64_t>(LD) * 2, static_cast<cuuint64_t>(LD * K) * 2};
-  const cuuint32_t box[3] = {64, 64, 1};
-  const cuuint32_t estride[3] = {1, 1, 1};
-  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(img), gdim, gstride, box, estride,
+  // 4-D view (64 i in a chunk, i chunk, j, plane) of either layout; box 64 i (128 B,
+  // swizzled) x 1 chunk x 64 j x 1 plane, coordinates (0, i0 / 64, j0, plane)
+  const int64_t nIC = LD / 64;
+  const cuuint64_t gdim[4] = {64, static_cast<cuuint64_t>(nIC), static_cast<cuuint64_t>(K), 2};
+  const cuuint64_t gstride[3] = {
+      static_cast<cuuint64_t>(chunked ? K * 128 : 128),  // i chunk
+      static_cast<cuuint64_t>(chunked ? 128 : LD * 2),   // j
+      static_cast<cuuint64_t>(LD * K) * 2};              // plane
+  const cuuint32_t box[4] = {64, 1, 64, 1};
+  const cuuint32_t estride[4] = {1, 1, 1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(img), gdim, gstride, box, estride,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
