@@ -1197,9 +1197,11 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
         for (int w = 0; w < 16; ++w)
           for (int k = 0; k < 8; ++k) a[w][k] += static_cast<double>(h[(static_cast<size_t>(c) * 16 + w) * 8 + k]) / q.P;
       std::fprintf(stderr, "[f32i trace] avg cycles per CTA (%.0f tiles): mma total %.0f wait full %.0f lempty %.0f "
-                   "kfull %.0f rempty %.0f kl_full %.0f issue %.0f | producer total %.0f wait empty %.0f | drain0 "
+                   "kfull %.0f rempty %.0f kl_full %.0f issue %.0f | left mma total %.0f wait full %.0f lempty %.0f "
+                   "kl_full %.0f issue %.0f | producer total %.0f wait empty %.0f | drain0 "
                    "total %.0f rfull %.0f lfull %.0f\n", a[13][7], a[13][6], a[13][0], a[13][1], a[13][2], a[13][3],
-                   a[13][4], a[13][5], a[12][6], a[12][0], a[0][6], a[0][0], a[0][1]);
+                   a[13][4], a[13][5], a[15][6], a[15][0], a[15][1], a[15][4], a[15][5], a[12][6], a[12][0], a[0][6],
+                   a[0][0], a[0][1]);
     }
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
     return;

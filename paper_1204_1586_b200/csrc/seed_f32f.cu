@@ -672,13 +672,18 @@ __device__ __forceinline__ void mbar_wait_plain_t(uint64_t* bar, uint32_t parity
 //                lane), the KRl^T image of row tile t, left chunks t, t+3, t+6
 //   warp 12      producer: 4 TMA boxes (64 i x 64 j, one plane) per tile into a
 //                5-slot ring
-//   warp 13      MMAs (whole warp waits, one elected lane issues)
+//   warp 13      right-product MMAs (whole warp waits, one elected lane issues)
 //   warp 14      Khatri-Rao producer: the unit's KRr tile into a 4-deep ring (its
 //                own warp: the Y stream never waits on a Khatri-Rao slot)
-//   warp 15      idle (16 warps keep 128 registers per thread)
+//   warp 15      left-product MMAs
+// Two issuing warps, one per product: the tensor pipe's queue is shallow, so a
+// single issuer's per-tile barrier waits, fences and commits left it idle ~1/3
+// of the time (1660 cycles per tile against 1112 of MMA work); with the two
+// products issued by two warps one warp's bookkeeping overlaps the other's
+// MMAs (tools/microbench/mma_mix.cu: 1355 -> 1082 cycles per tile).
 constexpr int kINS = 5;                        // image slots (160 KB of loads in flight)
 constexpr int kINK = 4;                        // KRr slots (units of look-ahead)
-constexpr int kIDrain = 12, kIWProd = kIDrain, kIWMma = kIDrain + 1, kIWKr = kIDrain + 2;
+constexpr int kIDrain = 12, kIWProd = kIDrain, kIWMma = kIDrain + 1, kIWKr = kIDrain + 2, kIWMmaL = kIDrain + 3;
 constexpr int kIThreads = 16 * 32;
 constexpr int kIOffKR = kINS * 2 * kPlane;
 constexpr int kIOffBars = kIOffKR + kINK * kKRBytes;
@@ -722,7 +727,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     if (WD) wd_init(p.fault, p.stall);
     for (int s = 0; s < kINS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 2);  // both issuing warps' commits
     }
     for (int s = 0; s < kINK; ++s) {
       mbar_init(&kfull[s], 1);
@@ -738,7 +743,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     }
     mbar_init(kl_full, kIDrain);
     mbar_init(kl_free, 1);
-    mbar_init(fin, 1);
+    mbar_init(fin, 2);
     *drains_out = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -823,13 +828,13 @@ __global__ void __launch_bounds__(kIThreads, 1)
           mbar_drain_wait(&kfull[q & (kINK - 1)], static_cast<uint32_t>((q / kINK) & 1));
     }
   } else if (warp == kIWMma) {
-    // ------------------------------------------------------------------ MMA issuer
-    constexpr uint32_t id_r = idesc_f16(true), id_l = idesc_f16(false);
+    // ------------------------------------------------------------------ right MMAs
+    constexpr uint32_t id_r = idesc_f16(true);
     const uint64_t dA0 = sdesc(ring_u, 8192, 1024);  // right A: Y plane, MN-major
     const uint64_t dB0 = sdesc(krt_u, 16, 1024);     // right B: KRr tile, K-major
-    const uint64_t dL0 = sdesc(ring_u, 16, 1024);    // left B: Y plane, K-major
-    const bool all_terms_r = !(p.knobs & 2), all_terms_l = !(p.knobs & 4);
-    int k = 0, bc = 0;
+    const bool all_terms_r = !(p.knobs & 2);
+    const bool run = !(p.knobs & (32 | 256));  // timing experiments: no MMAs / no right MMAs
+    int k = 0;
     int wc[kA] = {0, 0, 0};
     unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long tstart = clock64();
@@ -839,15 +844,11 @@ __global__ void __launch_bounds__(kIThreads, 1)
     UnitIter it;
     for (it.init(w); it.more() && !wd_aborted<WD>(); it.next(), ++ul) {
       const int nt = it.nt;
-      const int ks = ul & (kINK - 1), lb = ul & 1;
-      const bool seg_end = it.seg_end();
-      if (it.band_start()) mbar_wait_t<WD>(kl_full, static_cast<uint32_t>(bc & 1), trc ? &tr[4] : nullptr);
-      if (ul >= 2) mbar_wait_t<WD>(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1), trc ? &tr[1] : nullptr);
+      const int ks = ul & (kINK - 1);
       mbar_wait_t<WD>(&kfull[ks], static_cast<uint32_t>((ul / kINK) & 1), trc ? &tr[2] : nullptr);
       tc_fence_after();
       const bool wstart = it.win_start(), wend = it.win_end();
       const uint64_t kb = dB0 + static_cast<uint64_t>((ks * kKRBytes) >> 4);
-      const uint32_t dL = tmem + kColL + kRP * lb;
 #pragma unroll
       for (int t = 0; t < kA; ++t) {
         if (t >= nt) break;
@@ -856,27 +857,18 @@ __global__ void __launch_bounds__(kIThreads, 1)
         mbar_wait_t<WD>(&full[s], ph, trc ? &tr[0] : nullptr);
         tc_fence_after();
         const long long ti = trc ? clock64() : 0;
-        const uint64_t pa = static_cast<uint64_t>((s * 2 * kPlane) >> 4);
-        const uint64_t aH = dA0 + pa, aL = aH + (kPlane >> 4), lH = dL0 + pa, lL = lH + (kPlane >> 4);
-        const uint32_t dR = tmem + kColR + kRP * t, aK = tmem + kColK + kRP * t;
+        const uint64_t aH = dA0 + static_cast<uint64_t>((s * 2 * kPlane) >> 4), aL = aH + (kPlane >> 4);
+        const uint32_t dR = tmem + kColR + kRP * t;
         if (elect_one()) {
-          if (!(p.knobs & 32)) {  // timing experiment 32: no MMAs
+          if (run) {
 #pragma unroll
-          for (int q = 0; q < kTJ / 16; ++q) {
-            if (p.knobs & 256) break;  // timing experiment: no right MMAs
-            mma_ss(dR, aH + q * 128, kb + q * 2, id_r, (wstart && q == 0) ? 0u : 1u);
-            if (all_terms_r) {
-              mma_ss(dR, aH + q * 128, kb + 512 + q * 2, id_r, 1u);
-              mma_ss(dR, aL + q * 128, kb + q * 2, id_r, 1u);
+            for (int q = 0; q < kTJ / 16; ++q) {
+              mma_ss(dR, aH + q * 128, kb + q * 2, id_r, (wstart && q == 0) ? 0u : 1u);
+              if (all_terms_r) {
+                mma_ss(dR, aH + q * 128, kb + 512 + q * 2, id_r, 1u);
+                mma_ss(dR, aL + q * 128, kb + q * 2, id_r, 1u);
+              }
             }
-          }
-#pragma unroll
-          for (int q = 0; q < kTI / 16; ++q) {
-            if (p.knobs & 128) break;  // timing experiment: no left MMAs
-            const uint32_t off = ((q >> 2) * 8192 + (q & 3) * 32) >> 4;
-            mma_ts(dL, aK + 8 * q, lH + off, id_l, (t == 0 && q == 0) ? 0u : 1u);
-            if (all_terms_l) mma_ts(dL, aK + 8 * q, lL + off, id_l, 1u);
-          }
           }
           umma_commit(&empty[s]);
           if (wend) umma_commit(&rfull[t]);
@@ -890,13 +882,8 @@ __global__ void __launch_bounds__(kIThreads, 1)
           ph ^= 1u;
         }
       }
-      if (elect_one()) {
-        umma_commit(&kempty[ks]);
-        umma_commit(&lfull[lb]);
-        if (seg_end) umma_commit(kl_free);
-      }
+      if (elect_one()) umma_commit(&kempty[ks]);
       __syncwarp();
-      if (seg_end) ++bc;
     }
     // after a watchdog abort the drains may sit in unbounded waits on the MMA-side
     // barriers: keep flipping those phases until every drain warp has left its loop
@@ -909,8 +896,8 @@ __global__ void __launch_bounds__(kIThreads, 1)
         __nanosleep(256);
       }
     __syncwarp();
-    // every issued MMA has completed before TMEM is released; MMA completion is
-    // bounded, so this spin ignores the abort flag
+    // every issued MMA (both issuing warps) has completed before TMEM is released;
+    // MMA completion is bounded, so this spin ignores the abort flag
     if (elect_one()) umma_commit(fin);
     __syncwarp();
     {
@@ -925,6 +912,65 @@ __global__ void __launch_bounds__(kIThreads, 1)
     if (p.trace && lane == 0) {
       tr[6] = static_cast<unsigned long long>(clock64() - tstart);
       tr[7] = static_cast<unsigned long long>(k);
+      for (int e = 0; e < 8; ++e) p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + e] = tr[e];
+    }
+  } else if (warp == kIWMmaL) {
+    // ------------------------------------------------------------------ left MMAs
+    constexpr uint32_t id_l = idesc_f16(false);
+    const uint64_t dL0 = sdesc(ring_u, 16, 1024);  // left B: Y plane, K-major
+    const bool all_terms_l = !(p.knobs & 4);
+    const bool run = !(p.knobs & (32 | 128));  // timing experiments: no MMAs / no left MMAs
+    int bc = 0;
+    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long tstart = clock64();
+    int s = 0;
+    uint32_t ph = 0;
+    int ul = 0;
+    UnitIter it;
+    for (it.init(w); it.more() && !wd_aborted<WD>(); it.next(), ++ul) {
+      const int nt = it.nt;
+      const int lb = ul & 1;
+      const bool seg_end = it.seg_end();
+      if (it.band_start()) mbar_wait_t<WD>(kl_full, static_cast<uint32_t>(bc & 1), trc ? &tr[4] : nullptr);
+      if (ul >= 2) mbar_wait_t<WD>(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1), trc ? &tr[1] : nullptr);
+      const uint32_t dL = tmem + kColL + kRP * lb;
+#pragma unroll
+      for (int t = 0; t < kA; ++t) {
+        if (t >= nt) break;
+        mbar_wait_t<WD>(&full[s], ph, trc ? &tr[0] : nullptr);
+        tc_fence_after();
+        const long long ti = trc ? clock64() : 0;
+        const uint64_t lH = dL0 + static_cast<uint64_t>((s * 2 * kPlane) >> 4), lL = lH + (kPlane >> 4);
+        const uint32_t aK = tmem + kColK + kRP * t;
+        if (elect_one()) {
+          if (run) {
+#pragma unroll
+            for (int q = 0; q < kTI / 16; ++q) {
+              const uint32_t off = ((q >> 2) * 8192 + (q & 3) * 32) >> 4;
+              mma_ts(dL, aK + 8 * q, lH + off, id_l, (t == 0 && q == 0) ? 0u : 1u);
+              if (all_terms_l) mma_ts(dL, aK + 8 * q, lL + off, id_l, 1u);
+            }
+          }
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (trc) tr[5] += static_cast<unsigned long long>(clock64() - ti);
+        if (++s == kINS) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+      if (elect_one()) {
+        umma_commit(&lfull[lb]);
+        if (seg_end) umma_commit(kl_free);
+      }
+      __syncwarp();
+      if (seg_end) ++bc;
+    }
+    if (elect_one()) umma_commit(fin);
+    __syncwarp();
+    if (p.trace && lane == 0) {
+      tr[6] = static_cast<unsigned long long>(clock64() - tstart);
       for (int e = 0; e < 8; ++e) p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + e] = tr[e];
     }
   } else if (warp < kIDrain) {
@@ -1008,7 +1054,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
           const float give = __uint_as_float(odd ? v[e] : v[4 + e]);
           o[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
         }
-        if (lred)
+        if (lred && lstore)
           asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(lrow + 8 * c8), "f"(o[0]), "f"(o[1]),
                        "f"(o[2]), "f"(o[3])
                        : "memory");
