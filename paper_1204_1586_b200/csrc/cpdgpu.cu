@@ -316,6 +316,7 @@ struct Plan {
     bool on = false;
     int64_t nRT = 0, nB = 0, nC = 0, U = 0;
     int P = 0, slots = 0, window = 4;
+    int band = 3;  // row tiles per band (2: the image kernel's stacked right product)
     DevBuf tab;  // CSR of right-partial slots per 128-row tile
     int tab_len = 0, tab_max = 0;
     DevBuf krl_img, lpart32;
@@ -762,7 +763,13 @@ void build_f32_geometry(cpdgpu_ctx* ctx, Plan& pl) {
   static const char* fused_env = std::getenv("CPDGPU_F32_FUSED");
   ff.on = pl.chunks.size() == 1 && pl.p < pl.N && !(fused_env && std::atoi(fused_env) == 0);
   if (ff.on) {
-    const int kA = cpdgpu::seed_f32f_band_tiles();
+    // bands of 2 row tiles (the operand-image kernel's stacked right product) unless
+    // the image is off (the in-kernel-split variant has bands of 3) or CPDGPU_F32_BAND=3
+    static const char* band_env = std::getenv("CPDGPU_F32_BAND");
+    static const char* img_env = std::getenv("CPDGPU_F32_IMAGE");
+    const bool img_off = img_env && std::atoi(img_env) == 0;
+    ff.band = img_off ? cpdgpu::seed_f32f_band_tiles() : (band_env && std::atoi(band_env) == 3 ? 3 : 2);
+    const int kA = ff.band;
     ff.nRT = cpdgpu::ceil_div(Jp, 128);
     ff.nB = cpdgpu::ceil_div(ff.nRT, kA);
     ff.nC = cpdgpu::ceil_div(Kp, 64);
@@ -863,7 +870,7 @@ Plan* get_plan(cpdgpu_ctx* ctx, cpdgpu_tensor* t, int64_t R, int pivot) {
 int f32_image_chunked() {
   static const int v = [] {
     const char* e = std::getenv("CPDGPU_F32_IMG_CHUNK");
-    return e ? (std::atoi(e) != 0 ? 1 : 0) : 0;
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : 1;
   }();
   return v;
 }
@@ -891,7 +898,7 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gra
     if (!ff.img && !ff.img_failed && !(img_env && std::atoi(img_env) == 0)) {
       const size_t bytes = static_cast<size_t>(2 * cpdgpu::f16_image_ld(pl.Jp) * pl.Kp) * 2;
       if (cudaMalloc(&ff.img, bytes) != cudaSuccess) {
-        cudaGetLastError();  // out of memory: keep the split-in-kernel path
+        cudaGetLastError();  // out of memory: the split-in-kernel path (bands of 3) or two passes
         ff.img = nullptr;
         ff.img_failed = true;
       } else if (!cpdgpu::make_tensor_map_f16_image(&ff.imap, ff.img, pl.Jp, pl.Kp, f32_image_chunked())) {
@@ -1169,6 +1176,7 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
     q.P = pl.ff.P;
     q.slots = pl.ff.slots;
     q.window = pl.ff.window;
+    q.band_tiles = pl.ff.band;
     static const char* knob_env = std::getenv("CPDGPU_F32F_KNOBS");
     q.knobs = knob_env ? std::atoi(knob_env) : 0;
     if (pl.ff.img_on && pl.ff.lred) {  // one band slot, summed in L2 by the drains
@@ -1199,9 +1207,9 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
       std::fprintf(stderr, "[f32i trace] avg cycles per CTA (%.0f tiles): mma total %.0f wait full %.0f lempty %.0f "
                    "kfull %.0f rempty %.0f kl_full %.0f issue %.0f | left mma total %.0f wait full %.0f lempty %.0f "
                    "kl_full %.0f issue %.0f | producer total %.0f wait empty %.0f | drain0 "
-                   "total %.0f rfull %.0f lfull %.0f\n", a[13][7], a[13][6], a[13][0], a[13][1], a[13][2], a[13][3],
-                   a[13][4], a[13][5], a[15][6], a[15][0], a[15][1], a[15][4], a[15][5], a[12][6], a[12][0], a[0][6],
-                   a[0][0], a[0][1]);
+                   "total %.0f rfull %.0f lfull %.0f | drain8 rfull %.0f lfull %.0f\n", a[13][7], a[13][6], a[13][0], a[13][1],
+                   a[13][2], a[13][3], a[13][4], a[13][5], a[15][6], a[15][0], a[15][1], a[15][4], a[15][5], a[12][6],
+                   a[12][0], a[0][6], a[0][0], a[0][1], a[8][0], a[8][1]);
     }
     if (ctx->timing) CK(cudaEventRecord(seed_event(ctx), s));
     return;
@@ -1832,7 +1840,7 @@ void gradient_body(cpdgpu_ctx* ctx, Plan& pl) {
         static_cast<const float*>(pl.ff.lpart32.p), pl.ff.img_on && pl.ff.lred ? 1 : pl.ff.nB, pl.ff.nC, pl.Kp, c.Rc,
         reinterpret_cast<const double*>(static_cast<const char*>(pl.tensor->yscale.p) + 8), c.scales->d() + 3 * RPc,
         gN_direct ? nullptr : pl.Ls.d(), static_cast<double* const*>(pl.gtab.p), gN_direct ? pl.perm[pl.N - 1] - 1 : -1,
-        pl.Kp, ctx->stream);
+        pl.Kp, pl.ff.img_on ? 1 : 0, ctx->stream);
   }
   cpdgpu::L0Step l0{};
   bool fuse_r = false, fuse_l = false;

@@ -150,8 +150,9 @@ struct Seed32FParams {
   int* fault;  // context fault word: the watchdog's report (no trap)
   int stall;   // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
   int watchdog;  // image kernel: bounded barrier waits (CPDGPU_WATCHDOG=1; implied by stall)
+  int band_tiles;  // row tiles per band: 3, or 2 (image kernel only: stacked right product)
 };
-int seed_f32f_band_tiles();  // 3
+int seed_f32f_band_tiles();  // 3 (the in-kernel-split variant)
 // ymap: the right pass's map (box 128 i x 64 j, no swizzle)
 int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream_t s);
 // The same kernel reading a cached operand image of the tensor instead of the fp32
@@ -264,10 +265,11 @@ int launch_l0_step(const L0Step& st, double* const* gtab, cudaStream_t s);
 
 int64_t tail_step_units(const TailStep& st);
 // fused fp32 seed: Ls[r][j] = us_y[0] us_r[r] sum_b Z[((b nC + j / 64) 64 + r) 64 + j % 64]
-// into out, or into gtab[out_slot] when out_slot >= 0 (the left seed is a gradient)
+// into out, or into gtab[out_slot] when out_slot >= 0 (the left seed is a gradient);
+// chunked = 1: the operand-image kernel's layout Z[(((b nC + j / 64) 8 + j % 64 / 8) 64 + r) 8 + j % 8]
 int launch_reduce_left32(const float* Z, int64_t nB, int64_t nC, int64_t M, int R, const double* us_y,
                          const double* us_r, double* out, double* const* gtab, int out_slot, int64_t ldo,
-                         cudaStream_t s);
+                         int chunked, cudaStream_t s);
 int launch_tail_step(const TailStep& st, double* const* gtab, int num_sms, cudaStream_t s);
 
 // Khatri-Rao rows for K1: out[q*LDK + r] = KR(spec)[q, r] for q < L (zero past R).

@@ -227,6 +227,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+// 32 lanes x 64 consecutive 32-bit columns (no wait)
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 (&q)[8]) {
   asm volatile(
@@ -248,10 +254,11 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 struct FWalk {
   int a, b, nC, nRT;
   int window;
+  int A = kA;  // row tiles per band
   __device__ int band(int u) const { return u / nC; }
   __device__ int tiles(int u) const {
-    const int r = nRT - band(u) * kA;
-    return r < kA ? r : kA;
+    const int r = nRT - band(u) * A;
+    return r < A ? r : A;
   }
   __device__ bool band_start(int u) const { return u == a || u % nC == 0; }
   __device__ bool seg_end(int u) const { return u + 1 == b || (u + 1) % nC == 0; }
@@ -267,9 +274,10 @@ struct FWalk {
 // The same walk as an incremental iterator (no runtime-divisor division or
 // modulo per unit: the MMA warp's bookkeeping sits between MMA issue bursts).
 struct UnitIter {
-  int u, end, b, c, nt, wpos, nC, nRT, window;
+  int u, end, b, c, nt, wpos, nC, nRT, window, A;
   bool first;
   __device__ void init(const FWalk& w) {
+    A = w.A;
     u = w.a;
     end = w.b;
     nC = w.nC;
@@ -282,8 +290,8 @@ struct UnitIter {
     first = true;
   }
   __device__ int tiles_of(int band) const {
-    const int r = nRT - band * kA;
-    return r < kA ? r : kA;
+    const int r = nRT - band * A;
+    return r < A ? r : A;
   }
   __device__ bool more() const { return u < end; }
   __device__ bool band_start() const { return first || c == 0; }
@@ -682,16 +690,31 @@ __device__ __forceinline__ void mbar_wait_plain_t(uint64_t* bar, uint32_t parity
 // products issued by two warps one warp's bookkeeping overlaps the other's
 // MMAs (tools/microbench/mma_mix.cu: 1355 -> 1082 cycles per tile).
 constexpr int kINS = 5;                        // image slots (160 KB of loads in flight)
-constexpr int kINK = 4;                        // KRr slots (units of look-ahead)
+constexpr int kINK = 2;                        // KRr slots (units of look-ahead)
+constexpr int kStage = kRP * kTJ * 4;          // 16 KB left-partial staging buffer [8 chunks][64 r][8 j] fp32
 constexpr int kIDrain = 12, kIWProd = kIDrain, kIWMma = kIDrain + 1, kIWKr = kIDrain + 2, kIWMmaL = kIDrain + 3;
 constexpr int kIThreads = 16 * 32;
 constexpr int kIOffKR = kINS * 2 * kPlane;
-constexpr int kIOffBars = kIOffKR + kINK * kKRBytes;
+constexpr int kIOffStage = kIOffKR + kINK * kKRBytes;
+constexpr int kIOffBars = kIOffStage + 2 * kStage;
 constexpr int kISmem = 1024 + kIOffBars + 512 + kRP * 8;
 
-template <bool WD>
+template <bool WD, int A>
 __global__ void __launch_bounds__(kIThreads, 1)
     seed_f32i_kernel(const Seed32FParams p, const __grid_constant__ CUtensorMap imap) {
+  // A = 3: one 64-column right accumulator per row tile, three N = 64 MMAs per K step.
+  // A = 2 (stacked): 128 columns per row tile, [Y_hi KR_hi | Y_hi KR_lo + Y_lo KR_hi]:
+  // one N = 128 MMA against the [KR_hi | KR_lo] tile and one N = 64 MMA per K step, so
+  // the Y plane is read from shared memory twice instead of three times.
+  constexpr bool STK = A == 2;
+  constexpr uint32_t cRw = STK ? 2 * kRP : kRP;  // right accumulator columns per row tile
+  constexpr uint32_t cK = A * cRw;               // KRl^T[t]: [cK + 64 t, +64)
+  constexpr uint32_t cL = cK + A * kRP;          // D_L[lb]: [cL + 64 lb, +64)
+  static_assert(cL + 2 * kRP <= kTmemCols, "TMEM columns");
+  // drain warps of the left accumulator: all 12 (A = 3), or the lane-quarter group
+  // without a row tile (A = 2: warps 8-11 drain only the left accumulator, warps 0-7
+  // only the right windows, so a late left product never delays a right drain)
+  constexpr int kLW = STK ? 4 : kIDrain;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x;
   const bool trc = p.trace != nullptr;  // per-role wait timers (CPDGPU_SEED_TRACE)
@@ -701,12 +724,14 @@ __global__ void __launch_bounds__(kIThreads, 1)
   w.nC = static_cast<int>(p.nC);
   w.nRT = static_cast<int>(p.nRT);
   w.window = p.window;
+  w.A = A;
   const int seg0 = w.a / w.nC;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const uint32_t ring_u = smem_u32(base);            // [kINS][hi 16 KB | lo 16 KB]
   const uint32_t krt_u = smem_u32(base + kIOffKR);   // [kINK][16 KB] KRr tiles
+  const uint32_t stage_u = smem_u32(base + kIOffStage);  // [2][16 KB] left partial of a unit
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + kIOffBars);
   uint64_t* full = bars;                 // [kINS] planes landed            (1 + tx)
   uint64_t* empty = full + kINS;         // [kINS] planes consumed          (MMA commit)
@@ -719,7 +744,9 @@ __global__ void __launch_bounds__(kIThreads, 1)
   uint64_t* kl_full = rempty + kA;       // band's KRl^T in TMEM            (12 drain warps)
   uint64_t* kl_free = kl_full + 1;       // band's MMAs done                (MMA commit)
   uint64_t* fin = kl_free + 1;           // every MMA of the CTA done       (MMA commit, before dealloc)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+  uint64_t* sfull = fin + 1;             // [2] staging buffer written      (12 drain warps)
+  uint64_t* sfree = sfull + 2;           // [2] staging buffer read by its bulk operation (the issuing lane)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
   unsigned* drains_out = tmem_slot + 1;  // drain warps that left their loop
   double* unscale = reinterpret_cast<double*>(base + kIOffBars + 512);  // [64] 1 / (scale_y scale_r)
 
@@ -735,13 +762,15 @@ __global__ void __launch_bounds__(kIThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&lfull[s], 1);
-      mbar_init(&lempty[s], kIDrain);
+      mbar_init(&lempty[s], kLW);
+      mbar_init(&sfull[s], kLW);
+      mbar_init(&sfree[s], 1);
     }
     for (int t = 0; t < kA; ++t) {
       mbar_init(&rfull[t], 1);
       mbar_init(&rempty[t], 4);
     }
-    mbar_init(kl_full, kIDrain);
+    mbar_init(kl_full, kIDrain - (STK ? kLW : 0));
     mbar_init(kl_free, 1);
     mbar_init(fin, 2);
     *drains_out = 0;
@@ -782,7 +811,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
           mbar_arrive_tx(&full[s], 2 * kPlane);
           // tests (p.stall): the first tile is announced but never requested (watchdog path)
           if (!(p.stall && k == 0)) {
-            const int i0 = (b * kA + t) * kTI, j0 = c * kTJ;
+            const int i0 = (b * A + t) * kTI, j0 = c * kTJ;
 #pragma unroll
             for (int pl = 0; pl < 2; ++pl)
 #pragma unroll
@@ -830,6 +859,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
   } else if (warp == kIWMma) {
     // ------------------------------------------------------------------ right MMAs
     constexpr uint32_t id_r = idesc_f16(true);
+    constexpr uint32_t id_r2 = id_r + (static_cast<uint32_t>(64 >> 3) << 17);  // N = 128
     const uint64_t dA0 = sdesc(ring_u, 8192, 1024);  // right A: Y plane, MN-major
     const uint64_t dB0 = sdesc(krt_u, 16, 1024);     // right B: KRr tile, K-major
     const bool all_terms_r = !(p.knobs & 2);
@@ -850,7 +880,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
       const bool wstart = it.win_start(), wend = it.win_end();
       const uint64_t kb = dB0 + static_cast<uint64_t>((ks * kKRBytes) >> 4);
 #pragma unroll
-      for (int t = 0; t < kA; ++t) {
+      for (int t = 0; t < A; ++t) {
         if (t >= nt) break;
         if (wstart && wc[t] > 0)
           mbar_wait_t<WD>(&rempty[t], static_cast<uint32_t>((wc[t] - 1) & 1), trc ? &tr[3] : nullptr);
@@ -858,11 +888,16 @@ __global__ void __launch_bounds__(kIThreads, 1)
         tc_fence_after();
         const long long ti = trc ? clock64() : 0;
         const uint64_t aH = dA0 + static_cast<uint64_t>((s * 2 * kPlane) >> 4), aL = aH + (kPlane >> 4);
-        const uint32_t dR = tmem + kColR + kRP * t;
+        const uint32_t dR = tmem + cRw * t;
         if (elect_one()) {
           if (run) {
 #pragma unroll
             for (int q = 0; q < kTJ / 16; ++q) {
+              if (STK) {
+                mma_ss(dR, aH + q * 128, kb + q * 2, id_r2, (wstart && q == 0) ? 0u : 1u);
+                if (all_terms_r) mma_ss(dR + kRP, aL + q * 128, kb + q * 2, id_r, 1u);
+                continue;
+              }
               mma_ss(dR, aH + q * 128, kb + q * 2, id_r, (wstart && q == 0) ? 0u : 1u);
               if (all_terms_r) {
                 mma_ss(dR, aH + q * 128, kb + 512 + q * 2, id_r, 1u);
@@ -891,7 +926,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
       for (uint32_t i = 0; i < (1u << 22) && *reinterpret_cast<volatile unsigned*>(drains_out) < kIDrain; ++i) {
         mbar_arrive(&lfull[0]);
         mbar_arrive(&lfull[1]);
-        for (int q = 0; q < kA; ++q) mbar_arrive(&rfull[q]);
+        for (int q = 0; q < A; ++q) mbar_arrive(&rfull[q]);
         mbar_arrive(kl_free);
         __nanosleep(256);
       }
@@ -933,15 +968,15 @@ __global__ void __launch_bounds__(kIThreads, 1)
       const bool seg_end = it.seg_end();
       if (it.band_start()) mbar_wait_t<WD>(kl_full, static_cast<uint32_t>(bc & 1), trc ? &tr[4] : nullptr);
       if (ul >= 2) mbar_wait_t<WD>(&lempty[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1), trc ? &tr[1] : nullptr);
-      const uint32_t dL = tmem + kColL + kRP * lb;
+      const uint32_t dL = tmem + cL + kRP * lb;
 #pragma unroll
-      for (int t = 0; t < kA; ++t) {
+      for (int t = 0; t < A; ++t) {
         if (t >= nt) break;
         mbar_wait_t<WD>(&full[s], ph, trc ? &tr[0] : nullptr);
         tc_fence_after();
         const long long ti = trc ? clock64() : 0;
         const uint64_t lH = dL0 + static_cast<uint64_t>((s * 2 * kPlane) >> 4), lL = lH + (kPlane >> 4);
-        const uint32_t aK = tmem + kColK + kRP * t;
+        const uint32_t aK = tmem + cK + kRP * t;
         if (elect_one()) {
           if (run) {
 #pragma unroll
@@ -969,6 +1004,80 @@ __global__ void __launch_bounds__(kIThreads, 1)
     }
     if (elect_one()) umma_commit(fin);
     __syncwarp();
+    if (p.trace && lane == 0) {
+      tr[6] = static_cast<unsigned long long>(clock64() - tstart);
+      for (int e = 0; e < 8; ++e) p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + e] = tr[e];
+    }
+  } else if (STK && warp >= kIDrain - kLW && warp < kIDrain) {
+    // ------------------------------------------------------------------ left drains (A = 2)
+    // One warp per TMEM lane quarter: the unit's whole 64-column accumulator in ONE
+    // tcgen05.ld (the load's round trip under a busy tensor pipe is what a drain costs;
+    // two chunks at a time kept these four warps busy 98 % of the pass).
+    const int q = warp & 3;
+    const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+    const int odd = lane & 1;
+    const bool lstore = !(p.knobs & 8);
+    const bool lred = (p.knobs & 512) != 0;
+    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long tstart = clock64();
+    const int r = 16 * q + (lane >> 1);
+    int ul = 0;
+    UnitIter it;
+    for (it.init(w); it.more() && !wd_aborted<WD>(); it.next(), ++ul) {
+      const int b = it.b, c = it.c;
+      const int lb = ul & 1;
+      mbar_wait_plain_t(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1), trc ? &tr[1] : nullptr);
+      __syncwarp();
+      tc_fence_after();
+      uint32_t v[64];
+      if (!(p.knobs & 64)) {
+        tmem_ld64(tmem + lanes + cL + kRP * lb, v);
+        tmem_wait_ld();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lempty[lb]);  // the accumulator is in registers
+      if (ul >= 2) mbar_wait<WD>(&sfree[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1));
+      const uint32_t st_u = stage_u + lb * kStage + (r * 8 + 4 * odd) * 4;
+      if (!(p.knobs & 64)) {
+#pragma unroll
+        for (int c8 = 0; c8 < kTJ / 8; ++c8) {
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float keep = __uint_as_float(odd ? v[8 * c8 + 4 + e] : v[8 * c8 + e]);
+            const float give = __uint_as_float(odd ? v[8 * c8 + e] : v[8 * c8 + 4 + e]);
+            o[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+          }
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(st_u + c8 * (kRP * 32)), "f"(o[0]), "f"(o[1]),
+                       "f"(o[2]), "f"(o[3])
+                       : "memory");
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull[lb]);
+      if (warp == kIDrain - kLW && lane == 0) {  // the issuing lane: one bulk operation per unit
+        mbar_wait<WD>(&sfull[lb], static_cast<uint32_t>((ul >> 1) & 1));
+        if (lstore && !(p.knobs & 64) && !wd_aborted<WD>()) {
+          float* dst = p.lpart + (static_cast<int64_t>(lred ? 0 : b) * w.nC + c) * (kRP * kTJ);
+          if (lred)
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(dst),
+                         "r"(stage_u + lb * kStage), "r"(kStage)
+                         : "memory");
+          else
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+                         "r"(stage_u + lb * kStage), "r"(kStage)
+                         : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        if (ul >= 1) mbar_arrive(&sfree[lb ^ 1]);
+      }
+      __syncwarp();
+    }
+    if (warp == kIDrain - kLW && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    if (lane == 0) atomicAdd(drains_out, 1u);
     if (p.trace && lane == 0) {
       tr[6] = static_cast<unsigned long long>(clock64() - tstart);
       for (int e = 0; e < 8; ++e) p.trace[(static_cast<int64_t>(cta) * 16 + warp) * 8 + e] = tr[e];
@@ -1001,13 +1110,13 @@ __global__ void __launch_bounds__(kIThreads, 1)
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __half*>(p.krl_img) +
-                                                              (static_cast<int64_t>(b * kA + t) * 128 + q * 32 + lane) *
+                                                              (static_cast<int64_t>(b * A + t) * 128 + q * 32 + lane) *
                                                                   kTI) +
                                hh * 8;
             uint4 x[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) x[e] = __ldg(src + e);
-            tmem_st32(tmem + lanes + kColK + kRP * t + 32 * hh, x);
+            tmem_st32(tmem + lanes + cK + kRP * t + 32 * hh, x);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         }
@@ -1023,7 +1132,15 @@ __global__ void __launch_bounds__(kIThreads, 1)
         for (int c16 = 0; c16 < kRP / 16; ++c16) {
           if (p.knobs & 64) break;  // timing experiment: no TMEM reads in the drains
           uint32_t y[16];
-          tmem_ld16(tmem + lanes + kColR + kRP * t + 16 * c16, y);
+          tmem_ld16(tmem + lanes + cRw * t + 16 * c16, y);
+          if (STK) {  // main and correction halves
+            uint32_t z[16];
+            tmem_ld16(tmem + lanes + cRw * t + kRP + 16 * c16, z);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[16 * c16 + e] += __uint_as_float(y[e]) + __uint_as_float(z[e]);
+            continue;
+          }
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 16; ++e) acc[16 * c16 + e] += __uint_as_float(y[e]);
@@ -1033,40 +1150,102 @@ __global__ void __launch_bounds__(kIThreads, 1)
         if (lane == 0) mbar_arrive(&rempty[t]);
         ++wc;
       }
-      // left: lane pairs (hi, lo) of rank 16 q + lane / 2, chunks t, t + 3, t + 6
+      // left: lane pairs (hi, lo) of rank 16 q + lane / 2; 8-column chunks of the unit's
+      // accumulator per warp (A = 3: t, t + 3, t + 6; A = 2: all eight, on the four
+      // left-only warps), two chunks in flight.  The partial goes
+      // through a 16 KB staging buffer [chunk][64 r][8 j] (512 consecutive bytes per
+      // warp store) and ONE bulk operation per unit: an L2 reduce-add into the band
+      // slot (cp.reduce.async.bulk), or a bulk store of the band's own partial in
+      // deterministic mode.  Per-lane red.global.add cost the drains ~0.3 ms at
+      // A = 3 and 1.7 ms at A = 2 (their LSU issue rate, profiles/r02_f32i_knobs.txt).
+      if (!STK) {
       mbar_wait_plain_t(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1), trc ? &tr[1] : nullptr);
       __syncwarp();
       tc_fence_after();
       const int r = 16 * q + (lane >> 1);
-      float* lrow = p.lpart + ((static_cast<int64_t>(lred ? 0 : b) * w.nC + c) * kRP + r) * kTJ + 4 * odd;
-#pragma unroll
-      for (int c8 = t; c8 < kTJ / 8; c8 += kA) {
-        if (p.knobs & 64) break;
-        uint32_t v[8];
+      const uint32_t st_u = stage_u + lb * kStage + (r * 8 + 4 * odd) * 4;
+      const int lc0 = t, lcs = 3;
+      const int ln = t == 2 ? 2 : 3;
+      bool freed = ul < 2;
+      for (int i0 = 0; i0 < ln; i0 += 2) {
+        if (p.knobs & 64) {
+          if (i0 + 2 >= ln) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&lempty[lb]);
+          }
+          continue;
+        }
+        const bool two = i0 + 1 < ln;
+        const int ca = lc0 + i0 * lcs, cb = ca + lcs;
+        uint32_t va[8], vb[8];
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                     : "r"(tmem + lanes + kColL + kRP * lb + 8 * c8));
+                     : "=r"(va[0]), "=r"(va[1]), "=r"(va[2]), "=r"(va[3]), "=r"(va[4]), "=r"(va[5]), "=r"(va[6]),
+                       "=r"(va[7])
+                     : "r"(tmem + lanes + cL + kRP * lb + 8 * ca));
+        if (two)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                       : "=r"(vb[0]), "=r"(vb[1]), "=r"(vb[2]), "=r"(vb[3]), "=r"(vb[4]), "=r"(vb[5]), "=r"(vb[6]),
+                         "=r"(vb[7])
+                       : "r"(tmem + lanes + cL + kRP * lb + 8 * cb));
         tmem_wait_ld();
-        float o[4];
+        if (i0 + 2 >= ln) {  // the accumulator is in registers: the next unit's MMAs may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&lempty[lb]);
+        }
+        float oa[4], ob[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float keep = __uint_as_float(odd ? v[4 + e] : v[e]);
-          const float give = __uint_as_float(odd ? v[e] : v[4 + e]);
-          o[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+          const float keep = __uint_as_float(odd ? va[4 + e] : va[e]);
+          const float give = __uint_as_float(odd ? va[e] : va[4 + e]);
+          oa[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
         }
-        if (lred && lstore)
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(lrow + 8 * c8), "f"(o[0]), "f"(o[1]),
-                       "f"(o[2]), "f"(o[3])
+        if (two) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float keep = __uint_as_float(odd ? vb[4 + e] : vb[e]);
+            const float give = __uint_as_float(odd ? vb[e] : vb[4 + e]);
+            ob[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+          }
+        }
+        if (!freed) {  // the bulk operation that read this buffer two units ago is done with it
+          mbar_wait<WD>(&sfree[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1));
+          freed = true;
+        }
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(st_u + ca * (kRP * 32)), "f"(oa[0]), "f"(oa[1]),
+                     "f"(oa[2]), "f"(oa[3])
+                     : "memory");
+        if (two)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(st_u + cb * (kRP * 32)), "f"(ob[0]),
+                       "f"(ob[1]), "f"(ob[2]), "f"(ob[3])
                        : "memory");
-        else if (lstore)
-          *reinterpret_cast<float4*>(lrow + 8 * c8) = make_float4(o[0], o[1], o[2], o[3]);
       }
-      tc_fence_before();
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&lempty[lb]);
+      if (lane == 0) mbar_arrive(&sfull[lb]);
+      if (warp == kIDrain - kLW && lane == 0) {  // the issuing lane: one bulk operation per unit
+        mbar_wait<WD>(&sfull[lb], static_cast<uint32_t>((ul >> 1) & 1));
+        if (lstore && !(p.knobs & 64) && !wd_aborted<WD>()) {
+          float* dst = p.lpart + (static_cast<int64_t>(lred ? 0 : b) * w.nC + c) * (kRP * kTJ);
+          if (lred)
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(dst),
+                         "r"(stage_u + lb * kStage), "r"(kStage)
+                         : "memory");
+          else
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+                         "r"(stage_u + lb * kStage), "r"(kStage)
+                         : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        if (ul >= 1) mbar_arrive(&sfree[lb ^ 1]);
+      }
+      __syncwarp();
+      }
       if (it.seg_end()) {
         if (mine) {
-          const int64_t slot = (static_cast<int64_t>(cta) * p.slots + (b - seg0)) * kA + t;  // CSR slot
+          const int64_t slot = (static_cast<int64_t>(cta) * p.slots + (b - seg0)) * A + t;  // CSR slot
           double* out = p.rpart + slot * kRP * kTI + q * 32 + lane;
 #pragma unroll
           for (int e = 0; e < kRP; ++e) {
@@ -1077,6 +1256,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
         ++bc;
       }
     }
+    if (warp == kIDrain - kLW && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // the bulk operations have landed
     if (lane == 0) atomicAdd(drains_out, 1u);  // the MMA warp's abort path waits for all drains
     if (p.trace && lane == 0) {
       tr[6] = static_cast<unsigned long long>(clock64() - tstart);
@@ -1204,16 +1384,21 @@ int launch_seed_f32f(const Seed32FParams& p, const CUtensorMap* ymap, cudaStream
   return 1;
 }
 
-int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s) {
-  if (p.watchdog) {
-    static unsigned long long cfg = 0;
-    set_smem_attr(seed_f32i_kernel<true>, kISmem, cfg);
-    launch_k(seed_f32i_kernel<true>, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
-    return 1;
-  }
+template <bool WD, int A>
+static void launch_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s) {
   static unsigned long long cfg = 0;
-  set_smem_attr(seed_f32i_kernel<false>, kISmem, cfg);
-  launch_k(seed_f32i_kernel<false>, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
+  set_smem_attr(seed_f32i_kernel<WD, A>, kISmem, cfg);
+  launch_k(seed_f32i_kernel<WD, A>, dim3(p.P), dim3(kIThreads), kISmem, s, pdl_enabled(), p, *imap);
+}
+
+int launch_seed_f32i(const Seed32FParams& p, const CUtensorMap* imap, cudaStream_t s) {
+  if (p.band_tiles == 2) {
+    if (p.watchdog) launch_f32i<true, 2>(p, imap, s);
+    else launch_f32i<false, 2>(p, imap, s);
+  } else {
+    if (p.watchdog) launch_f32i<true, 3>(p, imap, s);
+    else launch_f32i<false, 3>(p, imap, s);
+  }
   return 1;
 }
 

@@ -437,13 +437,15 @@ bool pdl_enabled() {
 }
 
 // fp32 left partials of the fused fp32 seed, [band][column tile][64 r][64 j] in
-// scaled units: Ls[r][j] = us_y us_r[r] sum_b Z[b][j / 64][r][j % 64].  Thread =
+// scaled units: Ls[r][j] = us_y us_r[r] sum_b Z[b][j / 64][r][j % 64] (chunked = 1,
+// the operand-image kernel's staging layout: [band][column tile][8 chunks][64 r][8 j]).  Thread =
 // four columns of one rank; eight bands' 16-byte loads in flight per thread, the
 // bands summed in a fixed order (b % 2 into two fp64 sums, then added).
 __global__ void __launch_bounds__(256) reduce_left32_kernel(const float* __restrict__ Z, int64_t nB, int64_t nC,
                                                             int64_t M, int R, const double* __restrict__ us_y,
                                                             const double* __restrict__ us_r, double* out,
-                                                            double* const* gtab, int out_slot, int64_t ldo) {
+                                                            double* const* gtab, int out_slot, int64_t ldo,
+                                                            int chunked) {
   pdl_wait();
   if (out_slot >= 0) out = gtab[out_slot];  // the left seed is G(N): written in place
   const int64_t quads = (M + 3) / 4;
@@ -451,7 +453,9 @@ __global__ void __launch_bounds__(256) reduce_left32_kernel(const float* __restr
   if (e >= quads * R) return;
   const int r = static_cast<int>(e / quads);
   const int64_t j0 = (e - r * quads) * 4;  // the four columns share a 64-column tile (padded past M)
-  const float4* z = reinterpret_cast<const float4*>(Z + ((j0 >> 6) * 64 + r) * 64 + (j0 & 63));
+  const int64_t jj = j0 & 63;
+  const float4* z = reinterpret_cast<const float4*>(
+      chunked ? Z + (((j0 >> 6) * 8 + (jj >> 3)) * 64 + r) * 8 + (jj & 7) : Z + ((j0 >> 6) * 64 + r) * 64 + jj);
   const int64_t stride = nC * 64 * 64 / 4;  // one band
   double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
   int64_t k = 0;
@@ -478,10 +482,10 @@ __global__ void __launch_bounds__(256) reduce_left32_kernel(const float* __restr
 
 int launch_reduce_left32(const float* Z, int64_t nB, int64_t nC, int64_t M, int R, const double* us_y,
                          const double* us_r, double* out, double* const* gtab, int out_slot, int64_t ldo,
-                         cudaStream_t s) {
+                         int chunked, cudaStream_t s) {
   const int64_t threads = ((M + 3) / 4) * R;
   launch_k(reduce_left32_kernel, dim3(static_cast<unsigned>((threads + 255) / 256)), dim3(256), 0, s, pdl_enabled(),
-           Z, nB, nC, M, R, us_y, us_r, out, gtab, out_slot, ldo);
+           Z, nB, nC, M, R, us_y, us_r, out, gtab, out_slot, ldo, chunked);
   return 1;
 }
 

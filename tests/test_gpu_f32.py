@@ -189,10 +189,15 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env,path", [({"CPDGPU_F32_IMAGE": "0"}, 3), ({"CPDGPU_F32_FUSED": "0"}, 2)])
+@pytest.mark.parametrize("env,path", [({"CPDGPU_F32_IMAGE": "0"}, 3), ({"CPDGPU_F32_FUSED": "0"}, 2),
+                                      ({"CPDGPU_F32_BAND": "3"}, 4), ({"CPDGPU_F32_IMG_CHUNK": "0"}, 4),
+                                      ({"CPDGPU_F32_BAND": "3", "CPDGPU_F32_IMG_CHUNK": "0"}, 4)])
 def test_f32_alternate_seed_paths(env, path):
     """The fused pass with the split inside the kernel (3, used when the operand
-    image does not fit in memory) and the two-pass seed (2) against the oracle."""
+    image does not fit in memory), the two-pass seed (2), and the operand-image pass (4)
+    with bands of three row tiles and / or the whole-column image layout (the defaults
+    are bands of two with the stacked right product over the 64-row-chunked image)
+    against the oracle."""
     import json, os, subprocess, sys
     from pathlib import Path
     root = str(Path(__file__).resolve().parents[1])
