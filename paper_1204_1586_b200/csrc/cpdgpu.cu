@@ -763,12 +763,13 @@ void build_f32_geometry(cpdgpu_ctx* ctx, Plan& pl) {
   static const char* fused_env = std::getenv("CPDGPU_F32_FUSED");
   ff.on = pl.chunks.size() == 1 && pl.p < pl.N && !(fused_env && std::atoi(fused_env) == 0);
   if (ff.on) {
-    // bands of 2 row tiles (the operand-image kernel's stacked right product) unless
-    // the image is off (the in-kernel-split variant has bands of 3) or CPDGPU_F32_BAND=3
+    // bands of 3 row tiles; CPDGPU_F32_BAND=2: bands of 2 with the operand-image kernel's
+    // stacked right product (fewer tensor-pipe cycles, 1.5x the left partial traffic:
+    // the same time within noise at c5, profiles/r02_f32i_band2.txt)
     static const char* band_env = std::getenv("CPDGPU_F32_BAND");
     static const char* img_env = std::getenv("CPDGPU_F32_IMAGE");
     const bool img_off = img_env && std::atoi(img_env) == 0;
-    ff.band = img_off ? cpdgpu::seed_f32f_band_tiles() : (band_env && std::atoi(band_env) == 3 ? 3 : 2);
+    ff.band = !img_off && band_env && std::atoi(band_env) == 2 ? 2 : cpdgpu::seed_f32f_band_tiles();
     const int kA = ff.band;
     ff.nRT = cpdgpu::ceil_div(Jp, 128);
     ff.nB = cpdgpu::ceil_div(ff.nRT, kA);
@@ -1161,7 +1162,8 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
     double* sc = c.scales->d();
     // scales, right B tiles and the KRl^T image straight from the sorted factors
     ctx->launches += cpdgpu::launch_kr_fused_operands(pl.spec(pl.p + 1, pl.N, c.r0), pl.Kp, pl.spec(1, pl.p, c.r0),
-                                                      pl.Jp, c.Rc, sc, sc + 2 * RPc, c.KRr16->p, pl.ff.krl_img.p, s);
+                                                      pl.Jp, c.Rc, sc, sc + 2 * RPc, c.KRr16->p, pl.ff.krl_img.p, pl.ff.img_on ? 1 : 0,
+                                                      s);
     cpdgpu::Seed32FParams q{};
     q.kr_tiles = static_cast<const unsigned char*>(c.KRr16->p);
     q.krl_img = pl.ff.krl_img.p;
@@ -1177,6 +1179,8 @@ void run_seeds_f32(cpdgpu_ctx* ctx, Plan& pl, int mode, const cpdgpu_tensor* t) 
     q.slots = pl.ff.slots;
     q.window = pl.ff.window;
     q.band_tiles = pl.ff.band;
+    static const char* m64_env = std::getenv("CPDGPU_F32_LEFT_M64");
+    q.left_m64 = m64_env ? (std::atoi(m64_env) != 0 ? 1 : 0) : 1;
     static const char* knob_env = std::getenv("CPDGPU_F32F_KNOBS");
     q.knobs = knob_env ? std::atoi(knob_env) : 0;
     if (pl.ff.img_on && pl.ff.lred) {  // one band slot, summed in L2 by the drains

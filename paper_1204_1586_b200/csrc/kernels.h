@@ -151,6 +151,7 @@ struct Seed32FParams {
   int stall;   // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
   int watchdog;  // image kernel: bounded barrier waits (CPDGPU_WATCHDOG=1; implied by stall)
   int band_tiles;  // row tiles per band: 3, or 2 (image kernel only: stacked right product)
+  int left_m64;    // image kernel: the left Y_lo MMA with M = 64 (hi parts only, no lo * lo product)
 };
 int seed_f32f_band_tiles();  // 3 (the in-kernel-split variant)
 // ymap: the right pass's map (box 128 i x 64 j, no swizzle)
@@ -168,8 +169,10 @@ int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, co
 bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int64_t K, int chunked);
 // fused pass: column scales, right B tiles and the KRl^T image straight from the
 // sorted factors (two launches, no fp64 Khatri-Rao rows)
+// (lane_halves: the KRl^T slot of (rank r, part) is 32 (r / 16) + 16 part + r % 16, the
+// operand-image kernel's TMEM lane layout, instead of 2 r + part)
 int launch_kr_fused_operands(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, double* scale,
-                             double* inv, void* rtiles, void* limg, cudaStream_t s);
+                             double* inv, void* rtiles, void* limg, int lane_halves, cudaStream_t s);
 // column scales of the right (scale[0..63]) and left (scale[64..127]) Khatri-Rao rows
 int launch_kr_scale(const KRSpec& right, const KRSpec& left, int R, double* scale, double* inv, cudaStream_t s);
 // fp64 rows [L][ld] (ld <= 64) -> tiles (see Seed32Params::kr_tiles)
@@ -266,7 +269,7 @@ int launch_l0_step(const L0Step& st, double* const* gtab, cudaStream_t s);
 int64_t tail_step_units(const TailStep& st);
 // fused fp32 seed: Ls[r][j] = us_y[0] us_r[r] sum_b Z[((b nC + j / 64) 64 + r) 64 + j % 64]
 // into out, or into gtab[out_slot] when out_slot >= 0 (the left seed is a gradient);
-// chunked = 1: the operand-image kernel's layout Z[(((b nC + j / 64) 8 + j % 64 / 8) 64 + r) 8 + j % 8]
+// chunked = 1: the operand-image kernel's layout Z[(((b nC + j / 64) 16 + j % 64 / 4) 64 + r) 4 + j % 4]
 int launch_reduce_left32(const float* Z, int64_t nB, int64_t nC, int64_t M, int R, const double* us_y,
                          const double* us_r, double* out, double* const* gtab, int out_slot, int64_t ldo,
                          int chunked, cudaStream_t s);

@@ -195,9 +195,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
 }
 // Instruction descriptor kind::f16: fp16 A / B, fp32 D, M = 128, N = 64, A major.
-__host__ __device__ constexpr uint32_t idesc_f16(bool a_mn_major) {
+__host__ __device__ constexpr uint32_t idesc_f16(bool a_mn_major, int M = 128) {
   return (1u << 4) | ((a_mn_major ? 1u : 0u) << 15) | (static_cast<uint32_t>(64 >> 3) << 17) |
-         (static_cast<uint32_t>(128 >> 4) << 24);
+         (static_cast<uint32_t>(M >> 4) << 24);
 }
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -691,7 +691,7 @@ __device__ __forceinline__ void mbar_wait_plain_t(uint64_t* bar, uint32_t parity
 // MMAs (tools/microbench/mma_mix.cu: 1355 -> 1082 cycles per tile).
 constexpr int kINS = 5;                        // image slots (160 KB of loads in flight)
 constexpr int kINK = 2;                        // KRr slots (units of look-ahead)
-constexpr int kStage = kRP * kTJ * 4;          // 16 KB left-partial staging buffer [8 chunks][64 r][8 j] fp32
+constexpr int kStage = kRP * kTJ * 4;          // 16 KB left-partial staging buffer [16 column quads][64 r][4 j] fp32
 constexpr int kIDrain = 12, kIWProd = kIDrain, kIWMma = kIDrain + 1, kIWKr = kIDrain + 2, kIWMmaL = kIDrain + 3;
 constexpr int kIThreads = 16 * 32;
 constexpr int kIOffKR = kINS * 2 * kPlane;
@@ -952,6 +952,9 @@ __global__ void __launch_bounds__(kIThreads, 1)
   } else if (warp == kIWMmaL) {
     // ------------------------------------------------------------------ left MMAs
     constexpr uint32_t id_l = idesc_f16(false);
+    // the Y_lo plane against the hi parts only (M = 64: TMEM lanes 0-15 of every lane
+    // quarter, where the image kernel's KRl^T layout keeps them): no lo * lo product
+    const uint32_t id_l2 = p.left_m64 ? idesc_f16(false, 64) : id_l;
     const uint64_t dL0 = sdesc(ring_u, 16, 1024);  // left B: Y plane, K-major
     const bool all_terms_l = !(p.knobs & 4);
     const bool run = !(p.knobs & (32 | 128));  // timing experiments: no MMAs / no left MMAs
@@ -983,7 +986,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
             for (int q = 0; q < kTI / 16; ++q) {
               const uint32_t off = ((q >> 2) * 8192 + (q & 3) * 32) >> 4;
               mma_ts(dL, aK + 8 * q, lH + off, id_l, (t == 0 && q == 0) ? 0u : 1u);
-              if (all_terms_l) mma_ts(dL, aK + 8 * q, lL + off, id_l, 1u);
+              if (all_terms_l) mma_ts(dL, aK + 8 * q, lL + off, id_l2, 1u);
             }
           }
           umma_commit(&empty[s]);
@@ -1015,12 +1018,12 @@ __global__ void __launch_bounds__(kIThreads, 1)
     // two chunks at a time kept these four warps busy 98 % of the pass).
     const int q = warp & 3;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
-    const int odd = lane & 1;
+    const int odd = lane >> 4;  // hi / lo part of rank 16 q + lane % 16 (lanes l, l + 16)
     const bool lstore = !(p.knobs & 8);
     const bool lred = (p.knobs & 512) != 0;
     unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long tstart = clock64();
-    const int r = 16 * q + (lane >> 1);
+    const int r = 16 * q + (lane & 15);
     int ul = 0;
     UnitIter it;
     for (it.init(w); it.more() && !wd_aborted<WD>(); it.next(), ++ul) {
@@ -1038,7 +1041,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&lempty[lb]);  // the accumulator is in registers
       if (ul >= 2) mbar_wait<WD>(&sfree[lb], static_cast<uint32_t>(((ul >> 1) - 1) & 1));
-      const uint32_t st_u = stage_u + lb * kStage + (r * 8 + 4 * odd) * 4;
+      const uint32_t st_u = stage_u + lb * kStage + odd * (kRP * 16) + r * 16;
       if (!(p.knobs & 64)) {
 #pragma unroll
         for (int c8 = 0; c8 < kTJ / 8; ++c8) {
@@ -1047,7 +1050,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
           for (int e = 0; e < 4; ++e) {
             const float keep = __uint_as_float(odd ? v[8 * c8 + 4 + e] : v[8 * c8 + e]);
             const float give = __uint_as_float(odd ? v[8 * c8 + e] : v[8 * c8 + 4 + e]);
-            o[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+            o[e] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
           }
           asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(st_u + c8 * (kRP * 32)), "f"(o[0]), "f"(o[1]),
                        "f"(o[2]), "f"(o[3])
@@ -1086,7 +1089,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     // ------------------------------------------------------------------ drains
     const int q = warp & 3, t = warp >> 2;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
-    const int odd = lane & 1;
+    const int odd = lane >> 4;  // hi / lo part of rank 16 q + lane % 16 (lanes l, l + 16)
     const bool lstore = !(p.knobs & 8);
     const bool lred = (p.knobs & 512) != 0;  // left partials summed in L2 (red.add) into band slot 0
     float acc[kRP];
@@ -1150,11 +1153,11 @@ __global__ void __launch_bounds__(kIThreads, 1)
         if (lane == 0) mbar_arrive(&rempty[t]);
         ++wc;
       }
-      // left: lane pairs (hi, lo) of rank 16 q + lane / 2; 8-column chunks of the unit's
+      // left: lanes l, l + 16 (hi, lo) of rank 16 q + l; 8-column chunks of the unit's
       // accumulator per warp (A = 3: t, t + 3, t + 6; A = 2: all eight, on the four
       // left-only warps), two chunks in flight.  The partial goes
-      // through a 16 KB staging buffer [chunk][64 r][8 j] (512 consecutive bytes per
-      // warp store) and ONE bulk operation per unit: an L2 reduce-add into the band
+      // through a 16 KB staging buffer [chunk][column half][64 r][4 j] (256 consecutive
+      // bytes per half-warp store) and ONE bulk operation per unit: an L2 reduce-add into the band
       // slot (cp.reduce.async.bulk), or a bulk store of the band's own partial in
       // deterministic mode.  Per-lane red.global.add cost the drains ~0.3 ms at
       // A = 3 and 1.7 ms at A = 2 (their LSU issue rate, profiles/r02_f32i_knobs.txt).
@@ -1162,8 +1165,8 @@ __global__ void __launch_bounds__(kIThreads, 1)
       mbar_wait_plain_t(&lfull[lb], static_cast<uint32_t>((ul >> 1) & 1), trc ? &tr[1] : nullptr);
       __syncwarp();
       tc_fence_after();
-      const int r = 16 * q + (lane >> 1);
-      const uint32_t st_u = stage_u + lb * kStage + (r * 8 + 4 * odd) * 4;
+      const int r = 16 * q + (lane & 15);
+      const uint32_t st_u = stage_u + lb * kStage + odd * (kRP * 16) + r * 16;
       const int lc0 = t, lcs = 3;
       const int ln = t == 2 ? 2 : 3;
       bool freed = ul < 2;
@@ -1199,14 +1202,14 @@ __global__ void __launch_bounds__(kIThreads, 1)
         for (int e = 0; e < 4; ++e) {
           const float keep = __uint_as_float(odd ? va[4 + e] : va[e]);
           const float give = __uint_as_float(odd ? va[e] : va[4 + e]);
-          oa[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+          oa[e] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
         }
         if (two) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float keep = __uint_as_float(odd ? vb[4 + e] : vb[e]);
             const float give = __uint_as_float(odd ? vb[e] : vb[4 + e]);
-            ob[e] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+            ob[e] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
           }
         }
         if (!freed) {  // the bulk operation that read this buffer two units ago is done with it
@@ -1335,7 +1338,7 @@ __global__ void __launch_bounds__(128) kr_scale_cols_kernel(const KRSpec right, 
 // of rank r, 2 r + 1: its lo), 8 consecutive i per item.  Rows past the view are 0.
 __global__ void __launch_bounds__(256) kr_images_kernel(const KRSpec right, int64_t Kp, const KRSpec left, int64_t Jp,
                                                         int R, const double* __restrict__ scale, __half* rtiles,
-                                                        int64_t nR, __half* limg, int64_t nL) {
+                                                        int64_t nR, __half* limg, int64_t nL, int lane_halves) {
   int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   __half hi[8], lo[8];
   if (e < nR) {  // (t, r, j8): 8 consecutive items fill one 128-byte row of the tile
@@ -1368,9 +1371,13 @@ __global__ void __launch_bounds__(256) kr_images_kernel(const KRSpec right, int6
     hi[ii] = __double2half(x);
     lo[ii] = __double2half(x - static_cast<double>(__half2float(hi[ii])));
   }
-  __half* dst = limg + (t * 128 + 2 * r) * kTI + i8 * 8;
+  // slot of (rank r, part): 2 r + part, or (lane_halves, the operand-image kernel) hi in
+  // TMEM lanes 0-15 of lane quarter r / 16 and lo in lanes 16-31: an M = 64 MMA reads
+  // exactly the hi parts
+  const int slot = lane_halves ? 32 * (r >> 4) + (r & 15) : 2 * r, lo_off = lane_halves ? 16 : 1;
+  __half* dst = limg + (t * 128 + slot) * kTI + i8 * 8;
   *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hi);
-  *reinterpret_cast<uint4*>(dst + kTI) = *reinterpret_cast<const uint4*>(lo);
+  *reinterpret_cast<uint4*>(dst + lo_off * kTI) = *reinterpret_cast<const uint4*>(lo);
 }
 
 }  // namespace
@@ -1439,11 +1446,11 @@ bool make_tensor_map_f16_image(CUtensorMap* out, const void* img, int64_t J, int
 }
 
 int launch_kr_fused_operands(const KRSpec& right, int64_t Kp, const KRSpec& left, int64_t Jp, int R, double* scale,
-                             double* inv, void* rtiles, void* limg, cudaStream_t s) {
+                             double* inv, void* rtiles, void* limg, int lane_halves, cudaStream_t s) {
   kr_scale_cols_kernel<<<2 * kRP, 128, 0, s>>>(right, left, R, scale, inv);
   const int64_t nR = ceil_div(Kp, kTJ) * 8 * kRP, nL = ceil_div(Jp, kTI) * kRP * 16;
   kr_images_kernel<<<static_cast<unsigned>((nR + nL + 255) / 256), 256, 0, s>>>(
-      right, Kp, left, Jp, R, scale, static_cast<__half*>(rtiles), nR, static_cast<__half*>(limg), nL);
+      right, Kp, left, Jp, R, scale, static_cast<__half*>(rtiles), nR, static_cast<__half*>(limg), nL, lane_halves);
   return 2;
 }
 

@@ -438,7 +438,7 @@ bool pdl_enabled() {
 
 // fp32 left partials of the fused fp32 seed, [band][column tile][64 r][64 j] in
 // scaled units: Ls[r][j] = us_y us_r[r] sum_b Z[b][j / 64][r][j % 64] (chunked = 1,
-// the operand-image kernel's staging layout: [band][column tile][8 chunks][64 r][8 j]).  Thread =
+// the operand-image kernel's staging layout: [band][column tile][16 column quads][64 r][4 j]).  Thread =
 // four columns of one rank; eight bands' 16-byte loads in flight per thread, the
 // bands summed in a fixed order (b % 2 into two fp64 sums, then added).
 __global__ void __launch_bounds__(256) reduce_left32_kernel(const float* __restrict__ Z, int64_t nB, int64_t nC,
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(256) reduce_left32_kernel(const float* __restr
   const int64_t j0 = (e - r * quads) * 4;  // the four columns share a 64-column tile (padded past M)
   const int64_t jj = j0 & 63;
   const float4* z = reinterpret_cast<const float4*>(
-      chunked ? Z + (((j0 >> 6) * 8 + (jj >> 3)) * 64 + r) * 8 + (jj & 7) : Z + ((j0 >> 6) * 64 + r) * 64 + jj);
+      chunked ? Z + (((j0 >> 6) * 16 + (jj >> 2)) * 64 + r) * 4 : Z + ((j0 >> 6) * 64 + r) * 64 + jj);
   const int64_t stride = nC * 64 * 64 / 4;  // one band
   double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
   int64_t k = 0;

@@ -190,14 +190,16 @@ print(json.dumps(out))
 
 
 @pytest.mark.parametrize("env,path", [({"CPDGPU_F32_IMAGE": "0"}, 3), ({"CPDGPU_F32_FUSED": "0"}, 2),
-                                      ({"CPDGPU_F32_BAND": "3"}, 4), ({"CPDGPU_F32_IMG_CHUNK": "0"}, 4),
-                                      ({"CPDGPU_F32_BAND": "3", "CPDGPU_F32_IMG_CHUNK": "0"}, 4)])
+                                      ({"CPDGPU_F32_BAND": "2"}, 4), ({"CPDGPU_F32_IMG_CHUNK": "0"}, 4),
+                                      ({"CPDGPU_F32_BAND": "2", "CPDGPU_F32_IMG_CHUNK": "0"}, 4),
+                                      ({"CPDGPU_F32_LEFT_M64": "0"}, 4)])
 def test_f32_alternate_seed_paths(env, path):
     """The fused pass with the split inside the kernel (3, used when the operand
     image does not fit in memory), the two-pass seed (2), and the operand-image pass (4)
-    with bands of three row tiles and / or the whole-column image layout (the defaults
-    are bands of two with the stacked right product over the 64-row-chunked image)
-    against the oracle."""
+    with bands of two row tiles (stacked right product, left-only drain warps) and / or
+    the whole-column image layout, and with the lo * lo left product kept (M = 128), against
+    the oracle (the defaults: bands of three over the 64-row-chunked image, M = 64 for the
+    Y_lo left product)."""
     import json, os, subprocess, sys
     from pathlib import Path
     root = str(Path(__file__).resolve().parents[1])

@@ -38,4 +38,9 @@ if [ "${NCU:-1}" = 1 ] && timeout 300 $B > /dev/null 2>&1; then
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:"seed_i8" -s 2 -c 1 -o $O/${T}_seed_c2 -f \
     $B > $O/${T}_ncu_seed_c2.log 2>&1
 fi
+B="python bench.py --config c5 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-alg1"
+if [ "${NCU5:-1}" = 1 ] && timeout 300 $B > /dev/null 2>&1; then
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"seed_f32i" -s 2 -c 1 -o $O/${T}_seed_c5 -f \
+    $B > $O/${T}_ncu_seed_c5.log 2>&1
+fi
 echo done > $O/${T}_done.txt
