@@ -1316,6 +1316,13 @@ void run_seeds_i8(cpdgpu_ctx* ctx, Plan& pl) {
   q.watchdog = watchdog_on(q.stall);
   q.Lpart = g.nRB == 1 ? pl.Ls.d() + static_cast<int64_t>(c.r0) * pl.Kp : pl.Lpart.d() + c.lpart_off;
   q.lred = g.lred ? 1 : 0;  // slot 0 zeroed by this gradient's prologue
+  // CPDGPU_I8_RHALF=1 (read when the gradient's launches are recorded): the right product as two
+  // M = 64 row halves, the first issued while the tile is still being split.  Exact like the
+  // default, but measured 1-4 % slower at c2 / c3: it removes the split's wait for the planes and
+  // doubles the right product's MMAs, and the pass is then bound by the tensor pipe's operand reads
+  // (profiles/r02_i8_rhalf.txt), so it stays opt-in.
+  const char* rhalf_env = std::getenv("CPDGPU_I8_RHALF");
+  q.rhalf = rhalf_env && std::atoi(rhalf_env) != 0 ? 1 : 0;
   static const bool trace = std::getenv("CPDGPU_SEED_TRACE") != nullptr;
   DevBuf tb;
   if (trace) {

@@ -79,6 +79,7 @@ struct SeedI8Params {
   unsigned long long* trace;  // CPDGPU_SEED_TRACE: [P][14][6] per-warp wait cycles, total, tiles
   int knobs;                  // CPDGPU_I8_KNOBS experiments (bit 0: no digit stores)
   int lred;                   // left partials red.add'ed into row-block slot 0 (zeroed by the host)
+  int rhalf;                  // right product as two M = 64 row halves issued while the split runs (CPDGPU_I8_RHALF)
   int* fault;                 // context fault word: the watchdog's report (no trap)
   int stall;                  // tests: force a pipeline stall (CPDGPU_FORCE_STALL)
   int watchdog;               // bounded barrier waits (CPDGPU_WATCHDOG=1; implied by stall)

@@ -237,6 +237,11 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
@@ -322,8 +327,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + C::kRaw;
   uint64_t* dig_full = raw_empty + C::kRaw;  // [4] row chunks 2 ks, 2 ks + 1 of the tile split
-  uint64_t* dig_empty = dig_full + 4;        // tile's digits consumed
-  uint64_t* rb_full = dig_empty + 1;
+  uint64_t* dig_empty = dig_full + 4;        // [2] tile's digits consumed (rhalf: rows 0-63 / 64-127)
+  uint64_t* rb_full = dig_empty + 2;
   uint64_t* rb_empty = rb_full + 1;
   uint64_t* lb_full = rb_empty + 1;
   uint64_t* lb_empty = lb_full + 1;
@@ -343,7 +348,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       mbar_init(&raw_empty[s], kSplitW);
     }
     for (int b = 0; b < 4; ++b) mbar_init(&dig_full[b], kSplitW);
-    mbar_init(dig_empty, 1);
+    mbar_init(&dig_empty[0], 1);
+    mbar_init(&dig_empty[1], 1);
     mbar_init(rb_full, 1);
     mbar_init(rb_empty, 1);
     mbar_init(lb_full, 1);
@@ -432,53 +438,108 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     }
   } else if (warp == kWMma) {
     // ------------------------------------------------------------------ MMA issue
-    if (lane == 0) {
-      const uint32_t dg = smem_u32(dig), lb = smem_u32(lbuf);
+    // The whole warp runs the loop (lane 0 waits, then the warp reconverges) and one
+    // elected lane issues: descriptors and accumulator addresses are warp-uniform, so
+    // each tcgen05.mma is one instruction on uniform registers.  Issued from inside an
+    // `if (lane == 0)` the compiler wrapped every MMA in an elect / R2UR.BROADCAST
+    // waterfall loop (~16 instructions), and the issuing thread, not the tensor pipe,
+    // set the pace (115 cycles per MMA at c3, the MMA warp busy 72 % of the pass).
+    {
+      const uint32_t dg = smem_u32(dig), lb = smem_u32(lbuf), rbb = smem_u32(rbuf);
+      // base descriptors; a byte offset d inside the buffers is added as d >> 4
+      const uint64_t dAl = sdesc(dg, 16, 1024), dBl = sdesc(lb, 16, 1024);
+      const uint64_t dAr = sdesc(dg, 16384, 1024), dBr = sdesc(rbb, 16, 1024);
+      const bool run = !(p.knobs & 8);
       int64_t cur_rb = -1;
       int m = 0;
       int seg = 0, pos = 0;  // right-accumulator segment and position in it
       for (int k = 0; k < n; ++k) {
-        if (wd_aborted<WD>()) break;  // watchdog: no new MMAs
+        if (WD && __shfl_sync(0xffffffffu, wd_aborted<WD>() ? 1 : 0, 0)) break;  // watchdog: no new MMAs (warp-uniform)
         const int64_t tile = a0 + k, rb = tile / nCT;
         const bool last_of_rb = (k == n - 1) || ((tile + 1) / nCT != rb);
         const bool send = seg_end(tile, k, n, nCT, pos);
         // left: M = 128 columns j, K = rows i, one 32-row step as soon as the split
         // has delivered its two 16-row chunks (overlaps this tile's split)
+        const int lbk = k % C::kLB, lu = k / C::kLB;  // left buffer, its use
+        if (lane == 0) {
+          if (rb != cur_rb) TWAIT(3, lb_full, m & 1, 7, m);
+          if (lu > 0) TWAIT(3, &accL_empty[lbk], (lu - 1) & 1, 8, k);
+        }
         if (rb != cur_rb) {
-          TWAIT(3, lb_full, m & 1, 7, m);
           cur_rb = rb;
           ++m;
         }
-        const int lbk = k % C::kLB, lu = k / C::kLB;  // left buffer, its use
-        if (lu > 0) TWAIT(3, &accL_empty[lbk], (lu - 1) & 1, 8, k);
+        const uint32_t dL = tmem + C::kRS + lbk * C::kLS;
 #pragma unroll 1
         for (int ks = 0; ks < 4; ++ks) {
-          TWAIT(0, &dig_full[ks], k & 1, 4, k);
+          if (lane == 0) TWAIT(0, &dig_full[ks], k & 1, 4, k);
+          __syncwarp();
           tc_fence_after();
+          if (elect_one() && run) {
+            const uint64_t a_ks = dAl + static_cast<uint64_t>((ks * 32) >> 4), b_ks = dBl + static_cast<uint64_t>((ks * 32) >> 4);
 #pragma unroll
-          for (int a = 0; a < kPl; ++a)
-            if (!(p.knobs & 8))
-              mma_i8(tmem + C::kRS + lbk * C::kLS + a * NL, sdesc(dg + a * kPlane + ks * 32, 16, 1024),
-                     sdesc(lb + ks * 32, 16, 1024), idesc_i8(false, stacked_n(NL, a), 128),
-                     (ks > 0 || a > 0) ? 1u : 0u);
+            for (int a = 0; a < kPl; ++a)
+              mma_i8(dL + a * NL, a_ks + static_cast<uint64_t>((a * kPlane) >> 4), b_ks,
+                     idesc_i8(false, stacked_n(NL, a), 128), (ks > 0 || a > 0) ? 1u : 0u);
+          }
+          __syncwarp();
+          if (p.rhalf && ks == 1) {  // rows 0-63 are split: their right product, M = 64
+            if (lane == 0) {
+              TWAIT(1, rb_full, k & 1, 5, k);
+              if (pos == 0 && seg > 0) TWAIT(2, accR_empty, (seg - 1) & 1, 6, seg);
+            }
+            __syncwarp();
+            tc_fence_after();
+            if (elect_one()) {
+              if (run) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                  for (int a = 0; a < kPl; ++a)
+                    mma_i8(tmem + a * C::kNR, dAr + static_cast<uint64_t>((a * kPlane + kk * 4096) >> 4),
+                           dBr + static_cast<uint64_t>((kk * 32) >> 4), idesc_i8(true, stacked_n(C::kNR, a), 64),
+                           (kk > 0 || a > 0 || pos > 0) ? 1u : 0u);
+              }
+              umma_commit(&dig_empty[0]);  // every MMA over rows 0-63 (left ks 0, 1 and this half) is issued
+            }
+            __syncwarp();
+          }
         }
-        // right: M = 128 rows i, K = the tile's 128 columns (rows of the plane), after the split
-        TWAIT(1, rb_full, k & 1, 5, k);
-        if (pos == 0 && seg > 0) TWAIT(2, accR_empty, (seg - 1) & 1, 6, seg);
-        tc_fence_after();
-        const uint32_t rbb = smem_u32(rbuf);
+        // right: M = rows i, K = the tile's 128 columns (rows of the plane).  rhalf: as two
+        // M = 64 row halves, rows 0-63 issued inside the loop above after ks = 1 and rows
+        // 64-127 here, so only the second half runs after the split and the next tile's
+        // split of rows 0-63 never waits for it.  Otherwise one M = 128 product here.
+        if (!p.rhalf) {
+          if (lane == 0) {
+            TWAIT(1, rb_full, k & 1, 5, k);
+            if (pos == 0 && seg > 0) TWAIT(2, accR_empty, (seg - 1) & 1, 6, seg);
+          }
+          __syncwarp();
+          tc_fence_after();
+        }
+        if (elect_one()) {
+          if (run) {
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
+            for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
-          for (int a = 0; a < kPl; ++a)
-            if (!(p.knobs & 8))
-              mma_i8(tmem + a * C::kNR, sdesc(dg + a * kPlane + ks * 4096, 16384, 1024), sdesc(rbb + ks * 32, 16, 1024),
-                     idesc_i8(true, stacked_n(C::kNR, a), 128), (ks > 0 || a > 0 || pos > 0) ? 1u : 0u);
-        if (send) umma_commit(accR_full);
-        umma_commit(rb_empty);
-        umma_commit(dig_empty);
-        umma_commit(&accL_full[lbk]);
-        if (last_of_rb) umma_commit(lb_empty);
+              for (int a = 0; a < kPl; ++a) {
+                if (p.rhalf)  // rows 64-127: the second 64 bytes of the plane rows, TMEM lanes 16-31 of each quarter
+                  mma_i8(tmem + (16u << 16) + a * C::kNR, dAr + static_cast<uint64_t>((a * kPlane + ks * 4096 + 64) >> 4),
+                         dBr + static_cast<uint64_t>((ks * 32) >> 4), idesc_i8(true, stacked_n(C::kNR, a), 64),
+                         (ks > 0 || a > 0 || pos > 0) ? 1u : 0u);
+                else
+                  mma_i8(tmem + a * C::kNR, dAr + static_cast<uint64_t>((a * kPlane + ks * 4096) >> 4),
+                         dBr + static_cast<uint64_t>((ks * 32) >> 4), idesc_i8(true, stacked_n(C::kNR, a), 128),
+                         (ks > 0 || a > 0 || pos > 0) ? 1u : 0u);
+              }
+          }
+          if (send) umma_commit(accR_full);
+          umma_commit(rb_empty);
+          umma_commit(&dig_empty[p.rhalf ? 1 : 0]);
+          umma_commit(&accL_full[lbk]);
+          if (last_of_rb) umma_commit(lb_empty);
+        }
+        __syncwarp();
         if (send) {
           ++seg;
           pos = 0;
@@ -486,7 +547,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           ++pos;
         }
       }
-      umma_commit(fin);  // TMEM is released only after every issued MMA completed
+      if (elect_one()) umma_commit(fin);  // TMEM is released only after every issued MMA completed
+      __syncwarp();
       mbar_drain_wait(fin, 0);
     }
     __syncwarp();
@@ -530,7 +592,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           pack4(v[e][0].x, v[e][0].y, v[e][1].x, v[e][1].y, sy, w[e][0]);
           pack4(v[e][2].x, v[e][2].y, v[e][3].x, v[e][3].y, sy, w[e][1]);
         }
-        if (ks == 0 && k > 0) TWAIT(1, dig_empty, (k - 1) & 1, 10, k);
+        // the planes' rows 0-63 (ks 0, 1) / 64-127 (ks 2, 3) are free once the last tile's MMAs over them are done
+        if (k > 0 && (ks == 0 || (p.rhalf && ks == 2))) TWAIT(1, &dig_empty[ks >> 1], (k - 1) & 1, 10, k);
         if (!(p.knobs & 1)) {  // experiment knob: stream only
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
@@ -548,6 +611,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   } else {
     // ------------------------------------------------------------------ drain
     const int qd = warp & 3, row = 32 * qd + lane;
+    // rhalf: the M = 64 right halves keep row i = 64 h + 16 q + l in TMEM lane 32 q + 16 h + l
+    const int rrow = p.rhalf ? 64 * (lane >> 4) + 16 * qd + (lane & 15) : row;
     const uint32_t lanes = static_cast<uint32_t>(32 * qd) << 16;
     if (p.progress && lane == 0) reinterpret_cast<volatile unsigned*>(p.progress)[cta * 16 + warp] = 1;
     pdl_wait();
@@ -590,7 +655,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         double* dst = p.Rpart + (static_cast<int64_t>(cta) * p.slots + (rb - rb0)) * p.RP * 128;
 #pragma unroll
         for (int r = 0; r < N; ++r) {
-          if (r < p.RP) dst[r * 128 + row] = acc[r];
+          if (r < p.RP) dst[r * 128 + rrow] = acc[r];
           acc[r] = 0.0;
         }
       }

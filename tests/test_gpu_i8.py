@@ -16,9 +16,12 @@ import paper_1204_1586_b200 as cpd
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture
-def i8_env(monkeypatch):
+@pytest.fixture(params=["0", "1"], ids=["m128", "rhalf"])
+def i8_env(monkeypatch, request):
     monkeypatch.setenv("CPDGPU_I8", "1")  # read when the tensor's plan is built
+    # the right product as one M = 128 MMA set per tile (default) or as two M = 64 row
+    # halves overlapped with the split (read when the gradient's launches are recorded)
+    monkeypatch.setenv("CPDGPU_I8_RHALF", request.param)
 
 
 def rel_fro(got, want):
