@@ -189,3 +189,45 @@ def test_sharded_als_matches_oracle(dims, R, f32):
         assert cerr <= tol and c1err <= tol, (rank, cerr, c1err)
         assert counted
     assert res[0][-1] == res[1][-1]  # every rank leaves with the same factors
+
+
+def test_sharded_nccl_world_size_one(gpu_ctx, oracle):
+    """The library's NCCL communicator itself (libnccl dlopen'ed, ncclGetUniqueId,
+    ncclCommInitRank, the in-place ncclAllReduce on the context stream, destroy) on
+    the one GPU of the box as a world of one rank: the sharded gradient, device
+    form and ALS sweep through it equal the oracle's unsharded results.  (With more
+    GPUs the same calls run one rank per GPU; the slab split itself is covered by
+    the two-process test above over the host all-reduce.)"""
+    import torch
+    import paper_1204_1586_b200 as cpd
+    dims, R = [9, 10, 11, 12], 7
+    comm = cpd.Communicator(gpu_ctx, 1, 0, unique_id=cpd.comm_unique_id())
+    try:
+        assert comm.bounds(dims[-1]) == (0, dims[-1])
+        y = cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=21, ctx=gpu_ctx)
+        f = [oracle.fill_normal(70 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
+        want, _, _ = oracle.cp_gradient_all(y.values(), dims, f)
+        got = cpd.cp_gradient_all_sharded(y, dims, f)
+        for g, w in zip(got, want):
+            assert np.linalg.norm(g - w) / np.linalg.norm(w) <= 1e-12
+        packed = np.concatenate([x.reshape(-1, order="F") for x in f])
+        fd = torch.from_numpy(packed).cuda()
+        out = torch.zeros(sum(dims) * R, dtype=torch.float64, device="cuda")
+        gpu_ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        cpd.cp_gradient_all_sharded_device(y, dims, R, fd.data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        gpu_ctx.set_stream(0)
+        o, at = out.cpu().numpy(), 0
+        for d, w in zip(dims, want):
+            g = o[at:at + d * R].reshape(d, R, order="F")
+            at += d * R
+            assert np.linalg.norm(g - w) / np.linalg.norm(w) <= 1e-12
+        f2 = [x.copy() for x in f]
+        cost = cpd.als_sweep_sharded(y, dims, f2)
+        f3 = [x.copy() for x in f]
+        oracle.als_sweep_fast(y.values(), dims, f3)
+        for a, b in zip(f2, f3):
+            assert np.abs(a - b).max() <= 1e-9 * np.abs(b).max()
+        assert np.isfinite(cost)
+    finally:
+        comm.close()
