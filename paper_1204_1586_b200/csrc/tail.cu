@@ -275,35 +275,41 @@ __global__ void __launch_bounds__(kL0Threads) l0_kernel(const L0Step st, double*
       zs[e0] = sd.Z[r * sd.ldz + base + e0];
       if (has1) zs[e1] = sd.Z[r * sd.ldz + base + e1];
     } else if (sd.zsrc == 1) {
+      // slot partials [slot][RP][TI] listed per row tile (CSR); fields hoisted out of the
+      // dynamically indexed parameter struct, four partial loads per row in flight (a
+      // row tile has 1-3 slots at c5 and ~6 at c2: the former batches of eight spent
+      // ~280 instructions per element on predicated-off loads and their addresses)
+      const double* __restrict__ Zp = sd.Z;
+      const int* __restrict__ sl = sd.slot_list;
+      const int* __restrict__ rbp = sd.rb_ptr;
+      const uint32_t TI = static_cast<uint32_t>(sd.TI);
+      const int64_t sstride = static_cast<int64_t>(sd.RP) * sd.TI;
       double sum[2] = {0.0, 0.0};
       int q0[2], q1[2];
-      int64_t il[2];
+      const double* pk[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int64_t idx = base + (k ? (has1 ? e1 : e0) : e0);
-        const uint32_t rb = static_cast<uint32_t>(idx) / static_cast<uint32_t>(sd.TI);
-        il[k] = idx - static_cast<int64_t>(rb) * sd.TI;
-        q0[k] = sd.rb_ptr[rb];
-        q1[k] = sd.rb_ptr[rb + 1];
+        const uint32_t rb = static_cast<uint32_t>(idx) / TI;
+        pk[k] = Zp + static_cast<int64_t>(r) * TI + (idx - static_cast<int64_t>(rb) * TI);
+        q0[k] = rbp[rb];
+        q1[k] = rbp[rb + 1];
       }
-      for (int qq = 0;; qq += 8) {
-        bool more = false;
-        double v[2][8];
+      const int nmax = max(q1[0] - q0[0], q1[1] - q0[1]);
+      for (int qq = 0; qq < nmax; qq += 4) {
+        double v[2][4];
 #pragma unroll
         for (int k = 0; k < 2; ++k)
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 4; ++u) {
             const int q = q0[k] + qq + u;
-            v[k][u] = q < q1[k] ? sd.Z[(static_cast<int64_t>(sd.slot_list[q]) * sd.RP + r) * sd.TI + il[k]] : 0.0;
+            v[k][u] = q < q1[k] ? pk[k][static_cast<int64_t>(sl[q]) * sstride] : 0.0;
           }
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < 2; ++k)
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < 4; ++u)
             if (q0[k] + qq + u < q1[k]) sum[k] += v[k][u];
-          more = more || q0[k] + qq + 8 < q1[k];
-        }
-        if (!more) break;
       }
       zs[e0] = sum[0];
       if (has1) zs[e1] = sum[1];
