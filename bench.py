@@ -78,6 +78,32 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "_source": "fallback (B200_PROFILING.md)"}
 
 
+def pageable_upload_rates(cpd, ctx, f32: bool, nbytes: int = 2 << 30) -> dict:
+    """H2D rate of cpdgpu_tensor_update from PAGEABLE host memory (what a caller holding the
+    reference's std::vector-backed DenseTensor passes): the library's staged copy (pinned
+    buffers filled by host threads) against a plain cudaMemcpy (CPDGPU_STAGED_UPLOAD=0),
+    on a 2 GiB sample.  The headline e2e above uses pinned memory, as the contract asks."""
+    n = nbytes // (4 if f32 else 8)
+    src = np.ones(n, dtype=np.float32 if f32 else np.float64)  # pageable
+    t = cpd.DenseTensor.generate([n // 1024, 1024], cpd.DIST_UNIFORM_PM1 if f32 else cpd.DIST_NORMAL, seed=1,
+                                 ctx=ctx, dtype=cpd.F32 if f32 else cpd.F64)
+    out = {"sample_bytes": int(src.nbytes)}
+    try:
+        for key, env in (("staged_gbs", "1"), ("plain_gbs", "0")):
+            os.environ["CPDGPU_STAGED_UPLOAD"] = env
+            best = 0.0
+            for _ in range(3):
+                t0 = time.perf_counter()
+                t.update(src.ctypes.data)
+                ctx.synchronize()
+                best = max(best, src.nbytes / (time.perf_counter() - t0) / 1e9)
+            out[key] = best
+    finally:
+        os.environ.pop("CPDGPU_STAGED_UPLOAD", None)
+        t.free()
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled while the GPU is busy."""
 
@@ -398,6 +424,8 @@ def run_ours(args, cfg):
                "timing": "wall clock around synchronous host-API calls: update = H2D of Y from pinned memory "
                          "(cpdgpu_tensor_update), gradient call = factors in, per-tensor-version scale record, "
                          "gradient, gradients out"}
+
+        e2e["pageable_upload"] = pageable_upload_rates(cpd, ctx, f32)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -7,6 +7,7 @@
 //   update (on device) / gradients out.
 // Everything below the C-ABI is sm_100a device code; there is no CPU fallback.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -19,6 +20,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -423,8 +425,10 @@ struct Comm {
   }
 };
 
+struct HostStager;
 struct cpdgpu_ctx {
   int device = 0;
+  std::shared_ptr<HostStager> stager;  // pinned staging buffers for uploads from pageable memory
   std::unique_ptr<Comm> comm;
   int num_sms = 148;
   cudaStream_t own = nullptr, stream = nullptr;
@@ -2484,12 +2488,109 @@ int cpdgpu_last_seed_ms(cpdgpu_ctx* ctx, double* ms) {
   });
 }
 
+}  // extern "C"
+
+// ---- host -> device copies of Y ---------------------------------------------------
+// A caller of the reference holds Y in pageable memory (DenseTensor's std::vector,
+// dense_tensor.hpp:15-47).  cudaMemcpy from pageable memory is staged by the driver
+// on one thread; here large pageable sources go through the library's own pinned
+// staging buffers, filled by a few host threads (one stream and two 8 MB slots
+// each), so the copy runs near the PCIe rate instead of one core's memcpy rate.
+// Pinned / registered sources and small copies take the plain cudaMemcpyAsync.
+// CPDGPU_STAGED_UPLOAD=0 turns the staging off; CPDGPU_UPLOAD_THREADS sets the threads.
+struct HostStager {
+  static constexpr size_t kChunk = size_t(8) << 20;
+  int device = 0, W = 0;
+  std::vector<void*> pin;            // [W][2]
+  std::vector<cudaStream_t> st;      // [W]
+  std::vector<cudaEvent_t> ev;       // [W][2]
+  explicit HostStager(int dev) : device(dev) {
+    const char* e = std::getenv("CPDGPU_UPLOAD_THREADS");
+    int w = e ? std::atoi(e) : static_cast<int>(std::thread::hardware_concurrency() / 2);
+    W = std::max(1, std::min(w, 8));
+    pin.assign(static_cast<size_t>(2 * W), nullptr);
+    st.assign(static_cast<size_t>(W), nullptr);
+    ev.assign(static_cast<size_t>(2 * W), nullptr);
+    for (int i = 0; i < 2 * W; ++i) {
+      if (cudaHostAlloc(&pin[i], kChunk, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        pin[i] = nullptr;
+        W = 0;  // no pinned memory to be had: the plain copy
+        return;
+      }
+      CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    for (int i = 0; i < W; ++i) CK(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+  }
+  ~HostStager() {
+    cudaSetDevice(device);
+    for (auto s : st) if (s) cudaStreamDestroy(s);
+    for (auto e : ev) if (e) cudaEventDestroy(e);
+    for (auto p : pin) if (p) cudaFreeHost(p);
+  }
+  // dst (device) <- src (pageable host); returns when the bytes are on the device
+  void copy(void* dst, const void* src, size_t bytes) {
+    const size_t nchunk = (bytes + kChunk - 1) / kChunk;
+    std::atomic<int> err{0};
+    auto work = [&](int w) {
+      if (cudaSetDevice(device) != cudaSuccess) { err = 1; return; }
+      int use = 0;
+      for (size_t c = static_cast<size_t>(w); c < nchunk && !err; c += static_cast<size_t>(W), ++use) {
+        const int slot = 2 * w + (use & 1);
+        const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
+        if (use >= 2 && cudaEventSynchronize(ev[slot]) != cudaSuccess) { err = 1; return; }
+        std::memcpy(pin[slot], static_cast<const char*>(src) + off, n);
+        if (cudaMemcpyAsync(static_cast<char*>(dst) + off, pin[slot], n, cudaMemcpyHostToDevice, st[w]) != cudaSuccess ||
+            cudaEventRecord(ev[slot], st[w]) != cudaSuccess) { err = 1; return; }
+      }
+      if (cudaStreamSynchronize(st[w]) != cudaSuccess) err = 1;
+    };
+    std::vector<std::thread> th;
+    for (int w = 1; w < W; ++w) th.emplace_back(work, w);
+    work(0);
+    for (auto& t : th) t.join();
+    if (err) {
+      const cudaError_t e = cudaGetLastError();
+      fail(CPDGPU_CUDA_ERROR, "staged upload failed: %s", cudaGetErrorString(e));
+    }
+  }
+};
+
+namespace {
+bool host_is_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Y's bytes to the device, ordered after the work already on the context stream;
+// `sync`: return only when they have landed (pageable sources always do)
+void upload_bytes(cpdgpu_ctx* ctx, void* dst, const void* host, size_t bytes, bool sync) {
+  const char* staged_env = std::getenv("CPDGPU_STAGED_UPLOAD");  // per call: tests and bench compare both
+  const bool staged_on = !(staged_env && staged_env[0] == '0');
+  if (staged_on && bytes >= (size_t(32) << 20) && host_is_pageable(host)) {
+    if (!ctx->stager) ctx->stager = std::make_shared<HostStager>(ctx->device);
+    if (ctx->stager->W > 0) {
+      CK(cudaStreamSynchronize(ctx->stream));  // earlier readers of dst are done
+      ctx->stager->copy(dst, host, bytes);
+      return;
+    }
+  }
+  CK(cudaMemcpyAsync(dst, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (sync) CK(cudaStreamSynchronize(ctx->stream));
+}
+}  // namespace
+
+extern "C" {
+
 int cpdgpu_tensor_update(cpdgpu_ctx* ctx, cpdgpu_tensor* t, const void* host) {
   return guarded(ctx, [&] {
     if (!ctx || !t || !host) fail(CPDGPU_ARGUMENT_ERROR, "tensor_update: null argument");
     use_device(ctx);
-    CK(cudaMemcpyAsync(t->data, host, static_cast<size_t>(t->numel) * t->elem(), cudaMemcpyHostToDevice,
-                       ctx->stream));
+    upload_bytes(ctx, t->data, host, static_cast<size_t>(t->numel) * t->elem(), /*sync=*/false);
     t->norm2 = -1.0;
     ++t->version;
     if (!t->identity && t->sorted_ready) {  // refresh the sorted copy lazily
@@ -2509,7 +2610,7 @@ int cpdgpu_tensor_upload(cpdgpu_ctx* ctx, const void* host, cpdgpu_dtype dtype, 
     const size_t bytes = static_cast<size_t>(t->numel) * t->elem();
     CK(cudaMalloc(&t->data, bytes));
     t->owned = true;
-    if (host) CK(cudaMemcpyAsync(t->data, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (host) upload_bytes(ctx, t->data, host, bytes, /*sync=*/true);
     else CK(cudaMemsetAsync(t->data, 0, bytes, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     *out = t.release();

@@ -81,3 +81,25 @@ def test_parser_errors_carry_byte_offsets(gpu_ctx, tmp_path, mutate, word):
 def test_missing_file(gpu_ctx, tmp_path):
     with pytest.raises(cpd.ParseError):
         cpd.DenseTensor.load_tdnb(tmp_path / "does_not_exist.tdnb", ctx=gpu_ctx)
+
+
+@pytest.mark.parametrize("staged", ["1", "0"])
+def test_pageable_upload_roundtrip(gpu_ctx, monkeypatch, staged):
+    """Uploads from pageable host memory (numpy arrays; the reference's DenseTensor is a
+    std::vector) of more than 32 MB go through the library's pinned staging buffers,
+    filled by several host threads: upload and update return the exact bytes, ragged last
+    chunk included; CPDGPU_STAGED_UPLOAD=0 takes the plain copy."""
+    monkeypatch.setenv("CPDGPU_STAGED_UPLOAD", staged)
+    rng = np.random.default_rng(5)
+    dims = [301, 299, 101]  # 72.7 MB of fp64: 8 MB chunks with a ragged tail
+    y = rng.standard_normal(int(np.prod(dims)))
+    t = cpd.DenseTensor.from_values(y, dims, ctx=gpu_ctx)
+    assert np.array_equal(t.values().reshape(-1), y)
+    y2 = rng.standard_normal(y.size)
+    t.update(y2.ctypes.data)
+    assert np.array_equal(t.values().reshape(-1), y2)
+    y32 = rng.standard_normal(y.size).astype(np.float32)
+    t32 = cpd.DenseTensor.from_values(y32, dims, ctx=gpu_ctx, dtype=cpd.F32)
+    assert np.array_equal(t32.values().reshape(-1), y32)
+    t.free()
+    t32.free()
