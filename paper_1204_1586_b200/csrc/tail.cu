@@ -268,51 +268,59 @@ __global__ void __launch_bounds__(kL0Threads) l0_kernel(const L0Step st, double*
   //    two rows per thread and step, each summed from batches of eight
   //    partial loads issued together (order of the reduction ops kept)
   const int64_t base = b0 * M;
+  if (sd.zsrc == 1) {
+    // slot partials [slot][RP][TI] listed per row tile (CSR).  Four rows per thread and
+    // step, so a chunk of up to 1024 rows is one step: the row-tile pointer, slot list
+    // and partial loads are three dependent round trips per STEP, and a second step
+    // doubled them (each CTA's life is this latency chain).  Fields hoisted out of the
+    // dynamically indexed parameter struct; two partial loads per row in flight (a row
+    // tile has 1-3 slots at c5, ~6 at c2); the sum runs in slot-list order.
+    const double* __restrict__ Zp = sd.Z;
+    const int* __restrict__ sl = sd.slot_list;
+    const int* __restrict__ rbp = sd.rb_ptr;
+    const uint32_t TI = static_cast<uint32_t>(sd.TI);
+    const int64_t sstride = static_cast<int64_t>(sd.RP) * sd.TI;
+    for (int64_t e0 = tid; e0 < rows; e0 += 4 * kL0Threads) {
+      double sum[4] = {0.0, 0.0, 0.0, 0.0};
+      int q0[4], q1[4];
+      const double* pk[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t e = e0 + k * kL0Threads;
+        const bool has = e < rows;
+        const int64_t idx = base + (has ? e : e0);
+        const uint32_t rb = static_cast<uint32_t>(idx) / TI;
+        pk[k] = Zp + static_cast<int64_t>(r) * TI + (idx - static_cast<int64_t>(rb) * TI);
+        q0[k] = rbp[rb];
+        q1[k] = has ? rbp[rb + 1] : q0[k];
+      }
+      const int nmax = max(max(q1[0] - q0[0], q1[1] - q0[1]), max(q1[2] - q0[2], q1[3] - q0[3]));
+      for (int qq = 0; qq < nmax; qq += 2) {
+        double v[4][2];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int q = q0[k] + qq + u;
+            v[k][u] = q < q1[k] ? pk[k][static_cast<int64_t>(sl[q]) * sstride] : 0.0;
+          }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (q0[k] + qq + u < q1[k]) sum[k] += v[k][u];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (e0 + k * kL0Threads < rows) zs[e0 + k * kL0Threads] = sum[k];
+    }
+  } else
   for (int64_t e0 = tid; e0 < rows; e0 += 2 * kL0Threads) {
     const int64_t e1 = e0 + kL0Threads;
     const bool has1 = e1 < rows;
     if (sd.zsrc == 0) {
       zs[e0] = sd.Z[r * sd.ldz + base + e0];
       if (has1) zs[e1] = sd.Z[r * sd.ldz + base + e1];
-    } else if (sd.zsrc == 1) {
-      // slot partials [slot][RP][TI] listed per row tile (CSR); fields hoisted out of the
-      // dynamically indexed parameter struct, four partial loads per row in flight (a
-      // row tile has 1-3 slots at c5 and ~6 at c2: the former batches of eight spent
-      // ~280 instructions per element on predicated-off loads and their addresses)
-      const double* __restrict__ Zp = sd.Z;
-      const int* __restrict__ sl = sd.slot_list;
-      const int* __restrict__ rbp = sd.rb_ptr;
-      const uint32_t TI = static_cast<uint32_t>(sd.TI);
-      const int64_t sstride = static_cast<int64_t>(sd.RP) * sd.TI;
-      double sum[2] = {0.0, 0.0};
-      int q0[2], q1[2];
-      const double* pk[2];
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int64_t idx = base + (k ? (has1 ? e1 : e0) : e0);
-        const uint32_t rb = static_cast<uint32_t>(idx) / TI;
-        pk[k] = Zp + static_cast<int64_t>(r) * TI + (idx - static_cast<int64_t>(rb) * TI);
-        q0[k] = rbp[rb];
-        q1[k] = rbp[rb + 1];
-      }
-      const int nmax = max(q1[0] - q0[0], q1[1] - q0[1]);
-      for (int qq = 0; qq < nmax; qq += 4) {
-        double v[2][4];
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int q = q0[k] + qq + u;
-            v[k][u] = q < q1[k] ? pk[k][static_cast<int64_t>(sl[q]) * sstride] : 0.0;
-          }
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (q0[k] + qq + u < q1[k]) sum[k] += v[k][u];
-      }
-      zs[e0] = sum[0];
-      if (has1) zs[e1] = sum[1];
     } else {
       double sum[2] = {0.0, 0.0};
       // row-block partials: plane stride ldz, fields hoisted out of the
