@@ -176,6 +176,18 @@ inline void set_device(int device) {
   device_index() = device;
   context_slot().reset();
 }
+// The device workspace the library holds besides the tensors' values, in bytes (in use,
+// high-water mark): this implementation's own FastStats::peak_workspace figure
+// (mttkrp.hpp:37-47); FastStats itself keeps the reference algorithm's number.
+struct DeviceWorkspace {
+  std::int64_t current_bytes = 0, peak_bytes = 0;
+};
+inline DeviceWorkspace device_workspace() {
+  DeviceWorkspace w;
+  auto& c = context();
+  c.check(cpdgpu_device_workspace(c.h, &w.current_bytes, &w.peak_bytes));
+  return w;
+}
 }  // namespace gpu
 
 // ---- Shape (shape.hpp:15-42) ---------------------------------------------------------

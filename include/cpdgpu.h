@@ -145,6 +145,14 @@ int cpdgpu_predicted_mult_count(int N, const int64_t* dims, int64_t R, int n, in
  * cp_gradient_all tracks it (mttkrp.cpp:127-131,147-243) for ascending dims: the
  * figure every gradient entry point reports through peak_workspace (host only). */
 int cpdgpu_reference_workspace(int N, const int64_t* dims, int64_t R, int64_t* out);
+/* The DEVICE workspace this implementation holds, in bytes: seed partials, Khatri-Rao
+ * operands, operand images, padded / sorted copies and tables of every live plan and
+ * tensor of the process (not the tensors' own values) -- now and at its high-water mark.
+ * This is what FastStats::peak_workspace_doubles (mttkrp.hpp:37-47, tracked at
+ * mttkrp.cpp:127-131,243) measures for the reference; the gradient entry points keep
+ * reporting the reference algorithm's figure (above) so the bound its tests check
+ * (test_mttkrp.cpp:188-198) holds, and this call reports the real one. */
+int cpdgpu_device_workspace(cpdgpu_ctx* ctx, int64_t* current_bytes, int64_t* peak_bytes);
 
 /* ---- all-mode CP gradient (cp_gradient_all, mttkrp.hpp:59-69, mttkrp.cpp:113-253)
  * factors[k] / gradients[k]: host I_{k+1} x R column-major fp64 buffers in the

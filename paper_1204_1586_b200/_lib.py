@@ -52,6 +52,7 @@ SIGNATURES = {
     "cpdgpu_fast_count_realized": (c_u64, [C.c_int, C.POINTER(c_i64), c_i64, C.c_int]),
     "cpdgpu_predicted_mult_count": (C.c_int, [C.c_int, C.POINTER(c_i64), c_i64, C.c_int, C.c_int, C.POINTER(c_u64)]),
     "cpdgpu_reference_workspace": (C.c_int, [C.c_int, C.POINTER(c_i64), c_i64, C.POINTER(c_i64)]),
+    "cpdgpu_device_workspace": (C.c_int, [C.c_void_p, C.POINTER(c_i64), C.POINTER(c_i64)]),
     "cpdgpu_cp_gradient_all": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, c_dbl_pp, C.POINTER(c_u64), C.POINTER(c_i64)]),
     "cpdgpu_cp_gradient_all_hook": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, c_dbl_pp, c_dbl_pp, HOOK, C.c_void_p, C.POINTER(c_i64)]),
     "cpdgpu_cp_gradient_all_device": (C.c_int, [C.c_void_p, C.c_void_p, c_i64, C.c_void_p, C.c_void_p, C.c_int]),

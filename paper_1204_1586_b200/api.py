@@ -82,6 +82,14 @@ class Context:
     def launch_count(self) -> int:
         return int(self._L.cpdgpu_launch_count(self.h))
 
+    def device_workspace(self) -> tuple[int, int]:
+        """(bytes now, high-water bytes) of device workspace the library holds besides the
+        tensors' own values: this implementation's FastStats::peak_workspace figure
+        (mttkrp.hpp:37-47); the gradient calls report the reference algorithm's."""
+        cur, peak = C.c_int64(), C.c_int64()
+        _lib.check(self._L.cpdgpu_device_workspace(self.h, C.byref(cur), C.byref(peak)), self.h)
+        return int(cur.value), int(peak.value)
+
     def set_timing(self, enabled: bool) -> None:
         _lib.check(self._L.cpdgpu_set_timing(self.h, int(bool(enabled))), self.h)
 

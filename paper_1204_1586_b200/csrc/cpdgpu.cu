@@ -57,6 +57,18 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 #define CK(x) cuda_check((x), #x)
 
+// Device workspace the library itself holds (seed partials, Khatri-Rao operands, operand
+// images, padded / sorted copies, tables: everything but the tensors' own values), bytes in
+// use and the high-water mark, per process: what FastStats::peak_workspace_doubles
+// (mttkrp.cpp:127-131,243) would be for THIS implementation (cpdgpu_device_workspace).
+std::atomic<long long> g_ws_cur{0}, g_ws_peak{0};
+void ws_add(long long b) {
+  const long long now = g_ws_cur.fetch_add(b) + b;
+  long long pk = g_ws_peak.load();
+  while (now > pk && !g_ws_peak.compare_exchange_weak(pk, now)) {
+  }
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -64,15 +76,22 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      ws_add(-static_cast<long long>(bytes));
+    }
   }
   void ensure(size_t b) {
     if (b <= bytes) return;
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      ws_add(-static_cast<long long>(bytes));
+    }
     p = nullptr;
     bytes = 0;
     CK(cudaMalloc(&p, b));
     bytes = b;
+    ws_add(static_cast<long long>(b));
   }
   double* d() const { return static_cast<double*>(p); }
 };
@@ -229,7 +248,10 @@ struct cpdgpu_tensor {
   bool scale8_ok = false;
   size_t elem() const { return dtype == CPDGPU_F64 ? 8 : 4; }
   ~cpdgpu_tensor() {
-    if (sorted && sorted != data) cudaFree(sorted);
+    if (sorted && sorted != data) {
+      cudaFree(sorted);
+      ws_add(-static_cast<long long>(numel * static_cast<int64_t>(elem())));
+    }
     if (owned && data) cudaFree(data);
   }
 };
@@ -327,10 +349,14 @@ struct Plan {
     bool img_on = false, img_failed = false;
     bool lred = false;  // left partials added in L2 (red.add) into one band slot
     void* img = nullptr;
+    size_t img_bytes = 0;
     CUtensorMap imap{};
     uint64_t img_version = ~0ull;
     ~F32Fused() {
-      if (img) cudaFree(img);
+      if (img) {
+        cudaFree(img);
+        ws_add(-static_cast<long long>(img_bytes));
+      }
     }
   } ff;
   int64_t J8 = 0;               // J_p rounded up to 8 (3-D TMA view)
@@ -524,6 +550,7 @@ void ensure_sorted(cpdgpu_ctx* ctx, cpdgpu_tensor* t) {
     t->sorted = t->data;
   } else {  // hoisted sort_modes copy (als.cpp:159-165)
     CK(cudaMalloc(&t->sorted, static_cast<size_t>(t->numel) * t->elem()));
+    ws_add(static_cast<long long>(t->numel * static_cast<int64_t>(t->elem())));
     ctx->launches += cpdgpu::launch_permute(t->data, t->sorted, static_cast<int>(t->elem()),
                                             static_cast<int>(t->dims.size()), t->dims.data(),
                                             t->perm.data(), ctx->stream);
@@ -910,6 +937,9 @@ void bind_f32_inputs(cpdgpu_ctx* ctx, Plan& pl, cpdgpu_tensor* t, bool fused_gra
         cudaFree(ff.img);
         ff.img = nullptr;
         ff.img_failed = true;
+      } else {
+        ff.img_bytes = bytes;
+        ws_add(static_cast<long long>(bytes));
       }
     }
     ff.img_on = ff.img != nullptr;
@@ -2439,6 +2469,13 @@ int cpdgpu_destroy(cpdgpu_ctx* ctx) {
 
 const char* cpdgpu_last_error(const cpdgpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+int cpdgpu_device_workspace(cpdgpu_ctx* ctx, int64_t* current_bytes, int64_t* peak_bytes) {
+  if (!ctx) return CPDGPU_ARGUMENT_ERROR;
+  if (current_bytes) *current_bytes = static_cast<int64_t>(g_ws_cur.load());
+  if (peak_bytes) *peak_bytes = static_cast<int64_t>(g_ws_peak.load());
+  return CPDGPU_OK;
+}
+
 int cpdgpu_set_stream(cpdgpu_ctx* ctx, void* stream) {
   if (!ctx) return CPDGPU_ARGUMENT_ERROR;
   ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
@@ -2595,6 +2632,7 @@ int cpdgpu_tensor_update(cpdgpu_ctx* ctx, cpdgpu_tensor* t, const void* host) {
     ++t->version;
     if (!t->identity && t->sorted_ready) {  // refresh the sorted copy lazily
       cudaFree(t->sorted);
+      ws_add(-static_cast<long long>(t->numel * static_cast<int64_t>(t->elem())));
       t->sorted = nullptr;
       t->sorted_ready = false;
     }
@@ -2677,6 +2715,7 @@ int cpdgpu_tensor_axpby_kruskal(cpdgpu_ctx* ctx, cpdgpu_tensor* t, double alpha,
     t->sorted_ready = t->identity ? t->sorted_ready : false;
     if (!t->identity && t->sorted) {
       cudaFree(t->sorted);
+      ws_add(-static_cast<long long>(t->numel * static_cast<int64_t>(t->elem())));
       t->sorted = nullptr;
     }
   });

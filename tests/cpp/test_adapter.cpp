@@ -244,6 +244,9 @@ void test_counts_and_workspace() {  // test_counts.cpp:16-31, test_mttkrp.cpp:18
   CHECK(c.total() == want);
   const cpd::index_t J = 4 * 5, big = std::max<cpd::index_t>(J, 6 * 7);
   CHECK(st.peak_workspace_doubles > 0 && st.peak_workspace_doubles <= 2 * 3 * big + big);
+  // the device's own workspace (bytes in use / high-water mark) is reported beside it
+  const auto ws = cpd::gpu::device_workspace();
+  CHECK(ws.peak_bytes >= ws.current_bytes && ws.peak_bytes >= 8 * st.peak_workspace_doubles);
   // per-mode charges land before the hook
   cpd::CostCounter c2;
   std::vector<std::uint64_t> seen;

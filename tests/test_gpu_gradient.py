@@ -343,3 +343,26 @@ def test_unsorted_tensor_update_rerecords_graph(gpu_ctx, oracle):
         for n in range(len(dims)):
             assert max_rel_diff(g[n], want[n]) < 1e-12, n
     t.free()
+
+
+def test_device_workspace_is_reported(gpu_ctx, oracle):
+    """FastStats (mttkrp.hpp:37-47): the gradient calls report the reference algorithm's
+    peak_workspace_doubles (so test_mttkrp.cpp:188-198's bound holds); the device's own
+    workspace -- seed partials, Khatri-Rao operands, tables -- is reported by
+    cpdgpu_device_workspace: it grows with a new plan, never drops below what is live,
+    and exceeds the reference's figure for the same call (the partial buffers)."""
+    dims, R = [24, 26, 28, 30], 6
+    cur0, peak0 = gpu_ctx.device_workspace()
+    assert 0 <= cur0 <= peak0
+    y = cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=9, ctx=gpu_ctx)
+    f = [oracle.fill_normal(80 + k, d * R).reshape(d, R, order="F") for k, d in enumerate(dims)]
+    stats = cpd.FastStats()
+    cpd.cp_gradient_all(y, f, stats=stats)
+    cur1, peak1 = gpu_ctx.device_workspace()
+    assert cur1 > cur0 and peak1 >= cur1
+    # the device's buffers (partials per CTA / row block, operands, tables) exceed the
+    # reference algorithm's high-water figure for the same call
+    assert cur1 - cur0 >= 8 * stats.peak_workspace_doubles
+    y.free()
+    cur2, peak2 = gpu_ctx.device_workspace()
+    assert peak2 >= peak1 and cur2 <= peak2
