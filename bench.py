@@ -23,17 +23,20 @@ time is reported.
   e2e        same metric through the host C-ABI (cpdgpu_cp_gradient_all): H2D
              copy of Y from pinned host memory + factors in, gradients out
   roofline   dominant kernel = K1 seed contraction, timed with CUDA events on the
-             launching stream.  fp32 (c5): seed_f32 on tcgen05 kind::f16, bound =
-             HBM.  Large fp64 tensors (c2, c3) run it on the int8 tensor cores
+             launching stream.  fp32 (c5): seed_f32i_kernel on tcgen05 kind::f16 over
+             the fp16 hi/lo operand image, both seeds in one pass, bound = HBM.  Large fp64 tensors (c2, c3) run it on the int8 tensor cores
              (seed_i8_kernel): bound = HBM.  Otherwise fp64 DMMA
              (seed_f64_kernel, CPDGPU_I8=0 forces it): the slower of the HBM and
              FP64-tensor ideals, the other fraction beside it
-  cpu_baseline  the CPU oracle (a port of the reference) on this host's cores;
-             for c5 the streaming restatement (generated fp32 values, fp64
-             arithmetic) on a bounded last-mode slab sample at the global pivot
+             (e2e.pageable_upload: the upload rate from PAGEABLE host memory
+             through the library's staged copy against a plain cudaMemcpy)
+  cpu_baseline  the reference itself (oracle/_ref: its own sources built -O3
+             -DNDEBUG over the Eigen shim), one single-threaded call per host
+             core on mode-1 slabs of a bounded sample (kind "reference"); the C
+             port of the reference (kind "port") only when that build is absent
 
-`--impl reference` times the reference algorithm's CPU implementation (the
-oracle port, all host threads) on the same workload and metric.
+`--impl reference` times the same reference build on all host cores on the same
+workload and metric (the port as fallback).
 """
 from __future__ import annotations
 
