@@ -677,13 +677,19 @@ __device__ __forceinline__ void mbar_wait_plain_t(uint64_t* bar, uint32_t parity
 //
 //   warps 0-11   drains (q, t): TMEM lane quarter q == warp % 4, row tile t of the
 //                band: the right window drains (64 fp32 second-level sums per
-//                lane), the KRl^T image of row tile t, left chunks t, t+3, t+6
-//   warp 12      producer: 4 TMA boxes (64 i x 64 j, one plane) per tile into a
-//                5-slot ring
-//   warp 13      right-product MMAs (whole warp waits, one elected lane issues)
-//   warp 14      Khatri-Rao producer: the unit's KRr tile into a 4-deep ring (its
+//                lane), the KRl^T image of row tile t, left chunks t, t+3, t+6 of
+//                the unit's accumulator, staged in shared memory and added in L2 by
+//                one bulk reduce per unit (A = 2: warps 8-11 drain only the left
+//                accumulator, one tcgen05.ld per unit, warps 0-7 only right windows)
+//   warp 12      producer: 4 TMA boxes (64 i x 64 j, one plane: 8 KB of consecutive
+//                bytes in the 64-row-chunked image) per tile into a 5-slot ring
+//   warp 13      right-product MMAs (whole warp waits, one elected lane issues):
+//                three N = 64 MMAs per K step, or (A = 2) one N = 128 against the
+//                [KR_hi | KR_lo] tile and one N = 64
+//   warp 14      Khatri-Rao producer: the unit's KRr tile into a 2-deep ring (its
 //                own warp: the Y stream never waits on a Khatri-Rao slot)
-//   warp 15      left-product MMAs
+//   warp 15      left-product MMAs: Y_hi against all 128 KRl^T lanes (M = 128),
+//                Y_lo against the hi lanes only (M = 64: lanes 0-15 of each quarter)
 // Two issuing warps, one per product: the tensor pipe's queue is shallow, so a
 // single issuer's per-tile barrier waits, fences and commits left it idle ~1/3
 // of the time (1660 cycles per tile against 1112 of MMA work); with the two
