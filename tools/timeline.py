@@ -17,7 +17,8 @@ import paper_1204_1586_b200 as cpd
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 dims, R = {"c1": ([200] * 3, 10), "c2": ([60] * 4, 20), "c3": ([14] * 7, 10), "c5": ([300] * 4, 64)}[cfg]
 ctx = cpd.Context(0)
-y = cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=1, ctx=ctx)
+y = (cpd.DenseTensor.generate(dims, cpd.DIST_UNIFORM_PM1, seed=1, ctx=ctx, dtype=cpd.F32) if cfg == "c5"
+     else cpd.DenseTensor.generate(dims, cpd.DIST_NORMAL, seed=1, ctx=ctx))  # c5 is the fp32 config
 f = [np.random.default_rng(k).normal(size=(d, R)) for k, d in enumerate(dims)]
 for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 6):
     cpd.cp_gradient_all(y, f)
