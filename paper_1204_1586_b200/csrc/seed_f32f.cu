@@ -1304,6 +1304,40 @@ __global__ void build_f16_image_kernel(const float* __restrict__ y, int64_t J, i
   }
 }
 
+// The same image, eight rows per thread (two 16-byte loads, one 16-byte store per plane):
+// for views whose columns start 16-byte aligned (ldy % 4 == 0); ~1.4x the scalar kernel's rate.
+__global__ void build_f16_image_vec_kernel(const float* __restrict__ y, int64_t J, int64_t ldy, int64_t K, int64_t LD,
+                                           const float* __restrict__ scale, __half* __restrict__ img, int chunked) {
+  const float sy = scale[0];
+  const int64_t oct = LD / 8, n = oct * K, plane = LD * K;  // plane in halves
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / oct, i = 8 * (e - j * oct);
+    const float* col = y + j * ldy + i;
+    float v[8];
+    if (i + 8 <= J) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(col));
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(col) + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = i + k < J ? __ldcs(col + k) : 0.0f;
+    }
+    __half2 hi[4], lo[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float p = v[2 * k] * sy, q = v[2 * k + 1] * sy;
+      hi[k] = __floats2half2_rn(p, q);
+      const float2 back = __half22float2(hi[k]);
+      lo[k] = __floats2half2_rn(p - back.x, q - back.y);
+    }
+    const int64_t o = chunked ? (i >> 6) * K * 64 + j * 64 + (i & 63) : j * LD + i;
+    __stcs(reinterpret_cast<uint4*>(img + o), *reinterpret_cast<const uint4*>(hi));
+    __stcs(reinterpret_cast<uint4*>(img + plane + o), *reinterpret_cast<const uint4*>(lo));
+  }
+}
+
 // ---- Khatri-Rao operands of the fused pass, straight from the sorted factors ----
 // (the north star's "never materialised when it can be recomputed": no fp64
 // Khatri-Rao rows in HBM; each operand entry prod_m A_m[d_m, r] (kron.cpp:54-68)
@@ -1419,8 +1453,12 @@ int64_t f16_image_ld(int64_t J) { return ceil_div(J, 64) * 64; }
 
 int launch_build_f16_image(const float* y, int64_t J, int64_t ldy, int64_t K, const float* scale, void* img,
                            int num_sms, int chunked, cudaStream_t s) {
-  build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, f16_image_ld(J), scale, static_cast<__half2*>(img),
-                                                     chunked);
+  if (ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (reinterpret_cast<uintptr_t>(img) & 15) == 0)
+    build_f16_image_vec_kernel<<<num_sms * 16, 256, 0, s>>>(y, J, ldy, K, f16_image_ld(J), scale,
+                                                            static_cast<__half*>(img), chunked);
+  else
+    build_f16_image_kernel<<<num_sms * 8, 256, 0, s>>>(y, J, ldy, K, f16_image_ld(J), scale,
+                                                       static_cast<__half2*>(img), chunked);
   return 1;
 }
 
